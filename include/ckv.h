@@ -1,0 +1,207 @@
+/*
+ * ckv.h — C-ABI of the B200-native Cocktail chunk-level KV-cache hot path.
+ *
+ * The reference's operator boundary is the Python facade `chunkkv.kernels`
+ * (/root/reference/pkg/src/chunkkv/kernels/__init__.py:9-57) plus the callers
+ * it serves (quantizer.py, retrieval.py, kv_store.py, attention.py).  Every
+ * entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless the name ends in `_host`.
+ *   - No entry point allocates or synchronises; the caller owns every buffer
+ *     (outputs and workspace) and passes the CUDA stream as `void* stream`.
+ *   - Return 0 (CKV_OK) on success, a negative CKV_ERR_* on a bad argument.
+ *     Data-dependent errors (non-finite input, zero-norm query, crossing
+ *     thresholds) are reported through an int32 device flag word the caller
+ *     reads after the stream completes (bits CKV_FLAG_*), mirroring the
+ *     reference's ValueError sites.
+ *   - Re-entrant per stream; one process per GPU.
+ */
+#ifndef CKV_H_
+#define CKV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define CKV_OK 0
+#define CKV_ERR_BITS (-1)        /* bitwidth not in {2,4}      (_core.pyx:21-24)      */
+#define CKV_ERR_GROUP (-2)       /* group_size < 1            (_core.pyx:29-31)      */
+#define CKV_ERR_SHAPE (-3)       /* dimension mismatch        (_core.pyx:156-159)    */
+#define CKV_ERR_CAPACITY (-4)    /* count beyond packed words (_core.pyx:104-105)    */
+#define CKV_ERR_UNSUPPORTED (-5) /* shape outside the specialised D=128/G=32 path    */
+#define CKV_ERR_ARG (-6)         /* null pointer / negative size / bad alpha,beta    */
+#define CKV_ERR_CUDA (-7)        /* kernel launch failed                             */
+
+/* ---- device error-flag bits ---------------------------------------------- */
+#define CKV_FLAG_NONFINITE 1     /* quantizer.py:71-72                      */
+#define CKV_FLAG_ZERO_QUERY 2    /* retrieval.py:212-213                    */
+#define CKV_FLAG_CROSSING 4      /* retrieval.py:231-234                    */
+#define CKV_FLAG_EMPTY_SCORES 8  /* retrieval.py:225-226                    */
+
+/* tier codes (tiers.py:6-15) */
+#define CKV_TIER_INT2 0
+#define CKV_TIER_INT4 1
+#define CKV_TIER_FP16 2
+
+int32_t ckv_abi_version(void);
+const char* ckv_status_string(int32_t status);
+
+/* ======================================================================
+ * Generic per-block kernels: the five callables of kernels/__init__.py:43-47.
+ * float64 in / float64 out with the reference's expression trees, so codes,
+ * words and metadata are bit-identical to _numpy.py / _core.pyx.
+ * ==================================================================== */
+
+/* kernels.quantize_groups (_numpy.py:27-67, _core.pyx:27-79).
+ * x f64[rows, cols] row-major -> codes u8[rows*cols], scales/zero_points f64[rows*ceil(cols/gs)].
+ * Sets CKV_FLAG_NONFINITE in *flag when x holds inf/nan (quantizer.py:71-72). */
+int32_t ckv_quantize_groups_f64(const double* x, int64_t rows, int64_t cols, int32_t bits,
+                                int64_t group_size, uint8_t* codes, double* scales,
+                                double* zero_points, int32_t* flag, void* stream);
+
+/* Same contract for float16 input (bit patterns as uint16); metadata still f64. */
+int32_t ckv_quantize_groups_f16(const uint16_t* x, int64_t rows, int64_t cols, int32_t bits,
+                                int64_t group_size, uint8_t* codes, double* scales,
+                                double* zero_points, int32_t* flag, void* stream);
+
+/* kernels.pack_codes (_numpy.py:70-86, _core.pyx:82-97): u8[n] -> u32[ceil(n*bits/32)]. */
+int32_t ckv_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint32_t* packed,
+                       void* stream);
+
+/* kernels.unpack_codes (_numpy.py:89-99, _core.pyx:100-116). */
+int32_t ckv_unpack_codes(const uint32_t* packed, int64_t n_words, int32_t bits, int64_t count,
+                         uint8_t* codes, void* stream);
+
+/* kernels.dequantize_codes (_numpy.py:102-112, _core.pyx:119-145): zp + scale*code, no FMA. */
+int32_t ckv_dequantize_codes_f64(const uint32_t* packed, int64_t n_words, const double* scales,
+                                 const double* zero_points, int64_t rows, int64_t cols,
+                                 int32_t bits, int64_t group_size, double* out, void* stream);
+
+/* kernels.matmul_packed (_numpy.py:115-125, _core.pyx:148-192).
+ * transpose!=0: out f64[m, rows] = a f64[m, cols] . deq^T ; else out f64[m, cols] = a[m, rows] . deq.
+ * `accumulate`!=0 adds into out instead of overwriting (used to fuse the per-tier PV sum). */
+int32_t ckv_matmul_packed_f64(const double* a, int64_t m, int64_t a_cols, int64_t lda,
+                              const uint32_t* packed, int64_t n_words, const double* scales,
+                              const double* zero_points, int64_t rows, int64_t cols, int32_t bits,
+                              int64_t group_size, int32_t transpose, double* out, int64_t ldo,
+                              int32_t accumulate, void* stream);
+
+/* Dense f64 products used by attention.py:77,90,104,112 on the float regions:
+ * transpose!=0: out[m, n] (+)= a[m, k] . b[n, k]^T ; else out[m, n] (+)= a[m, k] . b[k, n]. */
+int32_t ckv_matmul_f64(const double* a, int64_t m, int64_t k, int64_t lda, const double* b,
+                       int64_t n, int64_t ldb, int32_t transpose, double* out, int64_t ldo,
+                       int32_t accumulate, void* stream);
+
+/* attention.stable_softmax (attention.py:24-31) fused with `att *= scale; att += mask`
+ * (attention.py:79-81).  x f64[m, n] in place; mask may be NULL. */
+int32_t ckv_scale_mask_softmax_f64(double* x, int64_t m, int64_t n, double scale,
+                                   const double* mask, void* stream);
+
+/* kv_store.reconstruct scatter (kv_store.py:236-253): dst[order[r]] = src[r] rows of width cols. */
+int32_t ckv_scatter_rows_f64(const double* src, int64_t rows, int64_t cols, const int64_t* order,
+                             double* dst, void* stream);
+
+/* ======================================================================
+ * Batched hot path: fp16 K/V, head_dim 128, group 32, chunk 32.
+ * ==================================================================== */
+
+/* (1) Chunk-level quantization search (retrieval.py:199-250 + kv_store.py:190-206).
+ * Per sequence b: cosine of q[b] with each chunk embedding (zero-norm chunks take the
+ * minimum valid score, retrieval.py:217-219), thresholds (retrieval.py:222-237), strict
+ * three-way tier rule (retrieval.py:240-250), stable INT2||INT4||FP16 permutation.
+ *   emb f64[B, n_chunks, dim], emb_norm f64[B, n_chunks], q f64[B, dim], q_norm f64[B]
+ *   -> scores f64[B, n_chunks], stats f64[B, 4] = (s_min, s_max, t_low, t_high),
+ *      tiers u8[B, n_chunks], perm u32[B, n_chunks], seg_counts i32[B, 3], flags i32[B].
+ * seq_chunks (nullable) i32[B]: per-sequence chunk count <= n_chunks (ragged batches).
+ * emb == NULL selects the scores-given mode: `scores` is read as input and only
+ * compute_thresholds / assign_tiers / the stable permutation run (retrieval.py:222-250). */
+int32_t ckv_search(const double* emb, const double* emb_norm, const double* q,
+                   const double* q_norm, const int32_t* seq_chunks, int32_t batch,
+                   int32_t n_chunks, int32_t dim,
+                   double alpha, double beta, double* scores, double* stats, uint8_t* tiers,
+                   uint32_t* perm, int32_t* seg_counts, int32_t* flags, void* stream);
+
+/* assign_tiers with caller-given thresholds (retrieval.py:240-250) plus the stable grouping:
+ * scores f64[B, n_chunks] (read only), thresholds f64[B, 2] = (t_low, t_high)
+ *   -> tiers u8[B, n_chunks], perm u32[B, n_chunks], seg_counts i32[B, 3], stats f64[B, 4],
+ *      flags i32[B]. */
+int32_t ckv_assign_tiers(const double* scores, const double* thresholds,
+                         const int32_t* seq_chunks, int32_t batch, int32_t n_chunks,
+                         uint8_t* tiers, uint32_t* perm, int32_t* seg_counts, double* stats,
+                         int32_t* flags, void* stream);
+
+/* Arena set for one of K or V over [layers, kv_heads]; rows are concatenated over the
+ * batch (varlen).  Row formats match the reference's packing bit for bit (one D=128 row
+ * packs into 8 (INT2) / 16 (INT4) little-endian u32 words, _numpy.py:70-86). */
+typedef struct ckv_arena {
+  uint32_t* codes2;   /* u32 [L][H][rows2][8]                                   */
+  uint32_t* meta2;    /* half2 (lo, hi) [L][H][rows2][4]                         */
+  uint32_t* codes4;   /* u32 [L][H][rows4][16]                                  */
+  uint32_t* meta4;    /* half2 (lo, hi) [L][H][rows4][4]                         */
+  uint16_t* fp;       /* fp16 [L][H][rows_fp][128] (FP16 chunks || tail || decode) */
+  int64_t rows2, rows4, rows_fp;
+} ckv_arena;
+
+/* Per-sequence segment table (device, int32 [B][8]):
+ *   off2, len2, off4, len4, off_fp, len_fp, tail_src, context_len
+ * Offsets are rows into the arenas; len_fp grows with decode appends (kv_store.py:135-148).
+ * context_len = 32 * (chunks in perm) + tail; tail_src is the source token index of the tail
+ * (normally 32 * n_chunks; differs for a sequence-split shard that owns the global tail). */
+#define CKV_SEQ_FIELDS 8
+
+/* (2) Chunk-level reorder + quantize + pack (kv_store.build_cache, kv_store.py:169-219 with
+ * quantizer.quantize / kernels.quantize_groups / pack_codes).  One pass over fp16 K and V:
+ *   k, v fp16 element strides (layer, batch, token, head); head_dim contiguous.
+ *   perm u32[B, max_chunks] (from ckv_search), seq i32[B][8].
+ * Writes codes/meta to the INT arenas and verbatim rows to the FP16 region (FP16-tier
+ * chunks, then the context tail).  Sets CKV_FLAG_NONFINITE on inf/nan input. */
+int32_t ckv_reorder_quantize_pack(const uint16_t* k, const uint16_t* v, int32_t layers,
+                                  int32_t batch, int32_t kv_heads, int64_t s_layer,
+                                  int64_t s_batch, int64_t s_token, int64_t s_head,
+                                  const uint32_t* perm, int32_t max_chunks, const int32_t* seq,
+                                  int32_t max_ctx, ckv_arena k_arena, ckv_arena v_arena,
+                                  int32_t* flag, void* stream);
+
+/* Decode-token append into the FP16 region (kv_store.append_decode_token, kv_store.py:222-224):
+ * k_new, v_new fp16 [L][B][H][128]; each row lands at off_fp + len_fp of its sequence, then
+ * len_fp += 1 (stream-ordered second kernel).  The caller checks len_fp < cap_fp on its host
+ * mirror of the segment table before calling (capacity growth is a host decision). */
+int32_t ckv_append_tokens(const uint16_t* k_new, const uint16_t* v_new, int32_t layers,
+                          int32_t batch, int32_t kv_heads, int32_t* seq, ckv_arena k_arena,
+                          ckv_arena v_arena, void* stream);
+
+/* Arena metadata (lo, hi) fp16 pairs -> the reference's float64 scale = (hi - lo) / qmax and
+ * zero_point = lo (quantize_groups, _numpy.py:65-66); exact because fp16 differences are exact
+ * in f64.  Used to export arenas as reference QuantizedBlocks (quantizer.py:20-57). */
+int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, double* scales,
+                        double* zero_points, void* stream);
+
+/* (3) Mixed-precision decode attention (attention.mixed_decode_attention, attention.py:63-90,
+ * for every (layer, sequence, kv-head) unit at once).  q fp16 [L][B][H*m][128] (strides
+ * q_s_layer, q_s_batch in elements), m = q heads per kv head (1..8).  Online softmax over the
+ * virtual sequence INT2 || INT4 || FP16 with split-KV; scale = softmax scale (1/sqrt(128)).
+ * Output fp16 [L][B][H*m][128].  Workspace: ckv_decode_workspace_bytes(). */
+int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
+                                   int32_t splits);
+int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                             ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                             int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
+                             float scale, int32_t splits, void* workspace, uint16_t* out,
+                             int64_t o_s_layer, int64_t o_s_batch, float* partial_out,
+                             void* stream);
+
+/* Split-KV merge across ranks (new; the NCCL-exchanged partials of SURVEY §8e):
+ * partials f32 [P][rows][128 + 2] = (acc[128] unnormalised at m, m (log2 domain), l);
+ * out fp16 [rows][128].  o = sum_p acc_p 2^(m_p - m*) / sum_p l_p 2^(m_p - m*). */
+int32_t ckv_lse_merge(const float* partials, int32_t n_parts, int64_t rows, uint16_t* out,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CKV_H_ */

@@ -1,0 +1,259 @@
+"""Batched fp16 hot path: the B200-resident chunked KV cache for all
+(layer, sequence, kv-head) units of a model, head_dim 128, group 32, chunk 32.
+
+Pipeline (one launch each, everything stays in HBM):
+
+  search_batched(...)           -> tiers, perm, per-tier counts     (retrieval.py:199-250)
+  BatchedKVCache.build(k, v, s) -> INT2/INT4 arenas + FP16 region    (kv_store.py:169-219)
+  cache.decode(q)               -> attention output per q head       (attention.py:63-90)
+  cache.append(k_new, v_new)    -> decode-token append               (kv_store.py:135-148)
+
+HBM layout (per K and V, see include/ckv.h ckv_arena):
+  codes2 u32 [L][H][rows2][8]     meta2 half2(lo,hi) [L][H][rows2][4]
+  codes4 u32 [L][H][rows4][16]    meta4 half2(lo,hi) [L][H][rows4][4]
+  fp     fp16 [L][H][rows_fp][128]
+Rows of one sequence are contiguous inside each arena (varlen concatenation over the
+batch); the per-sequence table seq i32 [B][8] holds the offsets and lengths.  Packed rows
+are bit-identical to the reference's pack_codes of the same rows.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib, kernels, quantizer
+from .kv_store import ChunkedKVCache
+from .quantizer import QuantizedBlock
+
+HEAD_DIM = 128
+GROUP = 32
+CHUNK = 32
+TILE = 16
+# algorithmic bytes per token per kv-head, K+V (codes + fp16 (lo,hi) metadata)
+BYTES_INT2 = 2 * (32 + 16)
+BYTES_INT4 = 2 * (64 + 16)
+BYTES_FP16 = 2 * 256
+
+
+def _round_up(x, m):
+    return -(-x // m) * m
+
+
+def _num_sms():
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def plan_layout(n2, n4, nfp, context_lens, decode_capacity=128, tail_src=None):
+    """Host-side arena layout: the per-sequence table i32 [B, 8] (include/ckv.h) and the FP16
+    region capacity per sequence (rounded to whole 16-token tiles)."""
+    n2 = np.asarray(n2, np.int64).reshape(-1)
+    n4 = np.asarray(n4, np.int64).reshape(-1)
+    nfp = np.asarray(nfp, np.int64).reshape(-1)
+    ctx = np.asarray(context_lens, np.int64).reshape(-1)
+    if not (n2.size == n4.size == nfp.size == ctx.size):
+        raise ValueError("per-sequence arrays must have equal length")
+    if (n2 < 0).any() or (n4 < 0).any() or (nfp < 0).any():
+        raise ValueError("negative chunk counts")
+    tail = ctx - CHUNK * (n2 + n4 + nfp)
+    if (tail < 0).any() or (tail >= CHUNK).any():
+        raise ValueError("context_lens inconsistent with chunk counts")
+    len2, len4 = n2 * CHUNK, n4 * CHUNK
+    len_fp = nfp * CHUNK + tail
+    cap_fp = np.array([_round_up(int(x) + int(decode_capacity), TILE) for x in len_fp], np.int64)
+    excl = lambda a: np.concatenate([[0], np.cumsum(a)[:-1]]).astype(np.int64) if a.size else a  # noqa: E731
+    tsrc = CHUNK * (n2 + n4 + nfp) if tail_src is None else np.asarray(tail_src, np.int64).reshape(-1)
+    seq = np.stack([excl(len2), len2, excl(len4), len4, excl(cap_fp), len_fp, tsrc, ctx], axis=1)
+    if seq.size and (seq[:, [0, 2, 4]].max() + np.maximum(cap_fp, np.maximum(len2, len4)).max() >= 2**31):
+        raise ValueError("arena rows exceed int32 offsets")
+    return seq.astype(np.int32).reshape(-1, 8), cap_fp
+
+
+class BatchedKVCache:
+    """Device-resident chunked KV cache for [layers, batch, kv_heads] units."""
+
+    def __init__(self, layers, batch, kv_heads, n2, n4, nfp, context_lens, decode_capacity=128,
+                 tail_src=None, device=None):
+        self.L, self.B, self.H = int(layers), int(batch), int(kv_heads)
+        dev = device or _lib.device()
+        self.device = dev
+        self.seq_host, self.cap_fp = plan_layout(n2, n4, nfp, context_lens, decode_capacity, tail_src)
+        if self.seq_host.shape[0] != self.B:
+            raise ValueError("per-sequence arrays must have length batch")
+        self.rows2 = int(self.seq_host[:, 1].sum())
+        self.rows4 = int(self.seq_host[:, 3].sum())
+        self.rows_fp = int(self.cap_fp.sum())
+        self.seq = torch.from_numpy(self.seq_host.copy()).to(dev)
+        L, H = self.L, self.H
+        z32 = lambda *s: torch.zeros(s, dtype=torch.int32, device=dev)  # noqa: E731
+        self.k = dict(codes2=z32(L, H, self.rows2, 8), meta2=z32(L, H, self.rows2, 4),
+                      codes4=z32(L, H, self.rows4, 16), meta4=z32(L, H, self.rows4, 4),
+                      fp=torch.zeros((L, H, self.rows_fp, HEAD_DIM), dtype=torch.float16, device=dev))
+        self.v = {k: torch.zeros_like(t) for k, t in self.k.items()}
+        self._ws = {}
+
+    # -- construction ------------------------------------------------------------------
+    @classmethod
+    def from_search(cls, k, v, search, context_lens=None, decode_capacity=128, check=True):
+        """Build from fp16 K/V [L, B, T, H, 128] (any strides, head_dim contiguous) and a
+        SearchResult (perm + seg_counts on the device).  One host sync for the layout."""
+        L, B, T, H, D = k.shape
+        if D != HEAD_DIM:
+            raise ValueError(f"batched path requires head_dim {HEAD_DIM}")
+        counts = search.seg_counts.cpu().numpy().astype(np.int64)
+        ctx = np.full(B, T, np.int64) if context_lens is None else np.asarray(context_lens, np.int64)
+        cache = cls(L, B, H, counts[:, 0], counts[:, 1], counts[:, 2], ctx, decode_capacity,
+                    device=k.device)
+        cache.build(k, v, search.perm, check=check)
+        return cache
+
+    def arena(self, which):
+        t = self.k if which == "k" else self.v
+        return _lib.Arena(t["codes2"].data_ptr(), t["meta2"].data_ptr(), t["codes4"].data_ptr(),
+                          t["meta4"].data_ptr(), t["fp"].data_ptr(), self.rows2, self.rows4,
+                          self.rows_fp)
+
+    def build(self, k, v, perm, check=True):
+        """ckv_reorder_quantize_pack over every unit; perm i32/u32 [B, max_chunks]."""
+        if k.dtype != torch.float16 or v.dtype != torch.float16:
+            raise ValueError("batched build expects fp16 K/V")
+        if k.shape != v.shape or k.stride() != v.stride():
+            raise ValueError("k and v must have equal shape and strides")
+        L, B, T, H, D = k.shape
+        if (L, B, H) != (self.L, self.B, self.H) or D != HEAD_DIM or k.stride(4) != 1:
+            raise ValueError("K/V shape does not match the cache")
+        perm = kernels.to_dev(perm, torch.int32)
+        flag = torch.zeros(1, dtype=torch.int32, device=k.device)
+        _lib.call("ckv_reorder_quantize_pack", _lib.ptr(k), _lib.ptr(v), L, B, H, k.stride(0),
+                  k.stride(1), k.stride(2), k.stride(3), _lib.ptr(perm), perm.shape[1],
+                  _lib.ptr(self.seq), int(self.seq_host[:, 7].max()) if B else 0,
+                  self.arena("k"), self.arena("v"), _lib.ptr(flag), _lib.stream())
+        if check and int(flag.item()) & _lib.FLAG_NONFINITE:
+            raise ValueError("matrix contains non-finite values")
+        return self
+
+    # -- decode ------------------------------------------------------------------------
+    def total_tokens(self):
+        s = self.seq_host
+        return (s[:, 1] + s[:, 3] + s[:, 5]).astype(np.int64)
+
+    def default_splits(self, m):
+        """Enough CTAs for ~2 waves of 4 CTAs/SM, capped by tiles per unit."""
+        units = self.L * self.B * self.H
+        target = 8 * _num_sms()
+        tiles = int(max(1, (self.total_tokens().max() + TILE - 1) // TILE))
+        return int(max(1, min(-(-target // max(units, 1)), tiles // 4 if tiles >= 8 else 1, 64)))
+
+    def _workspace(self, m, splits):
+        key = (m, splits)
+        if key not in self._ws:
+            nbytes = _lib.load().ckv_decode_workspace_bytes(self.L, self.B, self.H, m, splits)
+            self._ws[key] = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
+        return self._ws[key]
+
+    def decode(self, q, splits=None, out=None, scale=None):
+        """Mixed-precision decode attention for q fp16 [L, B, H*m, 128] -> fp16 same shape."""
+        L, B, Hq, D = q.shape
+        if (L, B) != (self.L, self.B) or D != HEAD_DIM or Hq % self.H:
+            raise ValueError("q shape does not match the cache")
+        if q.dtype != torch.float16 or q.stride(3) != 1 or q.stride(2) != HEAD_DIM:
+            raise ValueError("q must be fp16 with contiguous heads")
+        if (self.total_tokens() == 0).any():
+            raise ValueError("cache holds no tokens")  # attention.py:71-72
+        m = Hq // self.H
+        splits = self.default_splits(m) if splits is None else int(splits)
+        if out is None:
+            out = torch.empty((L, B, Hq, D), dtype=torch.float16, device=q.device)
+        ws = self._workspace(m, splits)
+        scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+        _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k"),
+                  self.arena("v"), _lib.ptr(self.seq), L, B, self.H, m, scale, splits,
+                  _lib.ptr(ws), _lib.ptr(out), out.stride(0), out.stride(1), None, _lib.stream())
+        return out
+
+    def decode_partial(self, q, splits=None, scale=None):
+        """Unnormalised split-KV partials f32 [L*B*H*m, 130] = (acc[128], m (log2), l)."""
+        L, B, Hq, D = q.shape
+        m = Hq // self.H
+        splits = self.default_splits(m) if splits is None else int(splits)
+        part = torch.empty((L * B * Hq, HEAD_DIM + 2), dtype=torch.float32, device=q.device)
+        ws = self._workspace(m, splits)
+        scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+        _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k"),
+                  self.arena("v"), _lib.ptr(self.seq), L, B, self.H, m, scale, splits,
+                  _lib.ptr(ws), None, 0, 0, _lib.ptr(part), _lib.stream())
+        return part
+
+    def append(self, k_new, v_new):
+        """Append one decode token per (layer, sequence, kv-head): fp16 [L, B, H, 128]."""
+        if k_new.shape != (self.L, self.B, self.H, HEAD_DIM) or k_new.shape != v_new.shape:
+            raise ValueError(f"decode vectors must have shape {(self.L, self.B, self.H, HEAD_DIM)}")
+        if (self.seq_host[:, 5] + 1 > self.cap_fp).any():
+            raise ValueError("decode capacity exhausted; rebuild with a larger decode_capacity")
+        k_new = k_new.to(torch.float16).contiguous()
+        v_new = v_new.to(torch.float16).contiguous()
+        _lib.call("ckv_append_tokens", _lib.ptr(k_new), _lib.ptr(v_new), self.L, self.B, self.H,
+                  _lib.ptr(self.seq), self.arena("k"), self.arena("v"), _lib.stream())
+        self.seq_host[:, 5] += 1
+
+    # -- accounting --------------------------------------------------------------------
+    def algorithmic_bytes(self, m):
+        """K/V bytes one decode step must read + q and o."""
+        s = self.seq_host.astype(np.int64)
+        per_unit = s[:, 1] * BYTES_INT2 + s[:, 3] * BYTES_INT4 + s[:, 5] * BYTES_FP16
+        return int(self.L * self.H * per_unit.sum() + 2 * self.L * self.B * self.H * m * HEAD_DIM * 2)
+
+    def memory_bytes(self):
+        return sum(t.numel() * t.element_size() for d in (self.k, self.v) for t in d.values())
+
+    # -- export to the reference per-head format ------------------------------------------
+    def export_unit(self, layer, seq, head, perm=None):
+        """The reference-format ChunkedKVCache of one unit (kv_store.py:24-166): packed words are
+        the arena rows verbatim, f64 scale/zero_point expanded from (lo, hi) on the device."""
+        s = self.seq_host[seq]
+        off2, len2, off4, len4, offf, lenf, _, ctx = (int(x) for x in s)
+
+        def block(t, which, bits):
+            codes = t["codes2" if bits == 2 else "codes4"][layer, head]
+            meta = t["meta2" if bits == 2 else "meta4"][layer, head]
+            off, rows = (off2, len2) if bits == 2 else (off4, len4)
+            packed = codes[off:off + rows].reshape(-1).contiguous()
+            mt = meta[off:off + rows].reshape(-1).contiguous()
+            sc = torch.empty(mt.numel(), dtype=torch.float64, device=self.device)
+            zp = torch.empty(mt.numel(), dtype=torch.float64, device=self.device)
+            _lib.call("ckv_expand_meta", _lib.ptr(mt), mt.numel(), bits, _lib.ptr(sc), _lib.ptr(zp),
+                      _lib.stream())
+            return QuantizedBlock._from_device(rows, HEAD_DIM, bits, GROUP, packed, sc, zp)
+
+        n_chunks = ctx // CHUNK
+        if perm is None:
+            perm = np.arange(n_chunks, dtype=np.uint32)
+        kf = self.k["fp"][layer, head, offf:offf + lenf].double().cpu().numpy()
+        vf = self.v["fp"][layer, head, offf:offf + lenf].double().cpu().numpy()
+        return ChunkedKVCache(CHUNK, HEAD_DIM, GROUP, ctx, np.asarray(perm, np.uint32)[:n_chunks],
+                              block(self.k, "k", 2), block(self.v, "v", 2), block(self.k, "k", 4),
+                              block(self.v, "v", 4), kf, vf)
+
+
+def build_cache_batched(k, v, search, context_lens=None, decode_capacity=128, check=True):
+    """Batched kv_store.build_cache: fp16 K/V [L, B, T, H, 128] + SearchResult -> BatchedKVCache."""
+    return BatchedKVCache.from_search(k, v, search, context_lens, decode_capacity, check)
+
+
+def mixed_decode_attention_batched(cache: BatchedKVCache, q, splits=None, out=None):
+    """Batched attention.mixed_decode_attention: q fp16 [L, B, H*m, 128] -> fp16 output."""
+    return cache.decode(q, splits=splits, out=out)
+
+
+def lse_merge(partials, out=None):
+    """Merge split-KV partials f32 [P, rows, 130] (from several shards/ranks) -> fp16 [rows, 128]."""
+    P, rows, w = partials.shape
+    if w != HEAD_DIM + 2:
+        raise ValueError("partials must be [P, rows, 130]")
+    partials = partials.contiguous()
+    if out is None:
+        out = torch.empty((rows, HEAD_DIM), dtype=torch.float16, device=partials.device)
+    _lib.call("ckv_lse_merge", _lib.ptr(partials), P, rows, _lib.ptr(out), _lib.stream())
+    return out

@@ -1,0 +1,232 @@
+// Chunk-level KV reorder + quantize + pack (Module II, prefill side), batched over
+// [layers, sequences, kv_heads].  One pass over fp16 K/V:
+//   kv_store.build_cache           kv_store.py:169-219 (tier-contiguous gather, perm order)
+//   quantizer.quantize             quantizer.py:60-83  (non-finite -> error flag)
+//   kernels.quantize_groups        _numpy.py:27-67 / _core.pyx:27-79 (min-max, round-half-up)
+//   kernels.pack_codes             _numpy.py:70-86 (row-major little-endian u32 words)
+// plus the FP16 region (FP16-tier chunks || context tail, kv_store.py:199-202) and the
+// decode-token append (kv_store.py:135-148, 222-224).
+//
+// Codes are bit-exact with the reference's float64 expression
+//   code = floor((x - lo) * qmax / (hi - lo) + 0.5)
+// For fp16 inputs that f64 result equals the exact rational floor((2(x-lo)qmax + span) / 2span)
+// (x - lo and span are exact in f64; the two remaining roundings move the value by < 2^-49
+// while a non-tie is >= 2^-42 from the boundary).  The kernel evaluates a fast fp32 candidate
+// whose error is < 2^-17 and recomputes in IEEE f64 (same tree) only when the candidate lies
+// within 2^-14 of a rounding boundary.
+#include "ckv_common.cuh"
+
+namespace ckv {
+
+constexpr int kQWarps = 4;
+constexpr float kGuard = 1.0f / 16384.0f;  // 2^-14
+
+struct SeqRow {
+  int off2, len2, off4, len4, off_fp, len_fp, tail_src, ctx;
+};
+
+__device__ __forceinline__ SeqRow load_seq(const int32_t* seq, int b) {
+  const int4 a = reinterpret_cast<const int4*>(seq)[2 * b];
+  const int4 c = reinterpret_cast<const int4*>(seq)[2 * b + 1];
+  return SeqRow{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+}
+
+__device__ __forceinline__ uint32_t exact_code(float x, float lo, float hi, float qinv,
+                                               float qmax) {
+  const float t = fmaf(x - lo, qinv, 0.5f);
+  float n = floorf(t);
+  const float fr = t - n;
+  if (fr < kGuard || fr > 1.0f - kGuard) {
+    // IEEE f64 with the reference's tree (_numpy.py:61): ((x - m) * qmax) / span + 0.5
+    const double dd = __dadd_rn(__ddiv_rn(__dmul_rn(__dsub_rn((double)x, (double)lo), (double)qmax),
+                                          __dsub_rn((double)hi, (double)lo)), 0.5);
+    n = (float)floor(dd);
+  }
+  n = fminf(fmaxf(n, 0.0f), qmax);
+  return (uint32_t)n;
+}
+
+// One warp per (layer, sequence, kv-head, destination chunk slot).  Slot p < N takes source
+// chunk perm[p]; slot p == N is the context tail (if any).
+__global__ void __launch_bounds__(kQWarps * 32)
+reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
+                             int H, int B, int64_t sL, int64_t sB, int64_t sT, int64_t sH,
+                             const uint32_t* __restrict__ perm, int max_chunks,
+                             const int32_t* __restrict__ seq, ckv_arena KA, ckv_arena VA,
+                             int32_t* flag) {
+  __shared__ __align__(16) uint32_t s_codes[kQWarps][512];  // 2 KB per warp (INT4 chunk)
+  __shared__ __align__(16) uint32_t s_meta[kQWarps][128];   // 512 B per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * kQWarps + warp;
+  const int h = blockIdx.y;
+  const int l = blockIdx.z / B, b = blockIdx.z % B;
+  const SeqRow sr = load_seq(seq, b);
+  const int N = sr.ctx / kChunk;
+  const int tail = sr.ctx - N * kChunk;
+  if (p > N || (p == N && tail == 0)) return;
+  const int n2 = sr.len2 / kChunk, n4 = sr.len4 / kChunk;
+  int tier, rows, src_tok0, dst_row0;
+  if (p < N) {
+    const int src = (int)perm[(int64_t)b * max_chunks + p];
+    src_tok0 = src * kChunk;
+    rows = kChunk;
+    if (p < n2) { tier = 0; dst_row0 = sr.off2 + p * kChunk; }
+    else if (p < n2 + n4) { tier = 1; dst_row0 = sr.off4 + (p - n2) * kChunk; }
+    else { tier = 2; dst_row0 = sr.off_fp + (p - n2 - n4) * kChunk; }
+  } else {
+    tier = 2; rows = tail; src_tok0 = sr.tail_src;
+    dst_row0 = sr.off_fp + (N - n2 - n4) * kChunk;
+  }
+  const int sub = lane >> 4, j = lane & 15;  // 2 rows per warp step, 8 fp16 per lane
+  bool bad = false;
+  const int64_t unit = (int64_t)l * H + h;
+#pragma unroll 1
+  for (int tsel = 0; tsel < 2; ++tsel) {
+    const uint16_t* src = (tsel ? v : k) + l * sL + b * sB + h * sH + (int64_t)src_tok0 * sT;
+    const ckv_arena& A = tsel ? VA : KA;
+    if (tier == 2) {
+      uint16_t* dst = A.fp + (unit * A.rows_fp + dst_row0) * kHeadDim;
+#pragma unroll 4
+      for (int rr = 0; rr < 16; ++rr) {
+        const int r = 2 * rr + sub;
+        if (r < rows) {
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(src + r * sT) + j);
+          const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            bad |= !fp16_bits_finite(w[e] & 0xFFFF) || !fp16_bits_finite(w[e] >> 16);
+          reinterpret_cast<uint4*>(dst + (int64_t)r * kHeadDim)[j] = x;
+        }
+      }
+      continue;
+    }
+    const float qmax = tier == 0 ? 3.0f : 15.0f;
+#pragma unroll 2
+    for (int rr = 0; rr < 16; ++rr) {
+      const int r = 2 * rr + sub;
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(src + r * sT) + j);
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+      float f[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        bad |= !fp16_bits_finite(w[e] & 0xFFFF) || !fp16_bits_finite(w[e] >> 16);
+        const float2 t = __half22float2(u32_as_h2(w[e]));
+        f[2 * e] = t.x;
+        f[2 * e + 1] = t.y;
+      }
+      float lo = f[0], hi = f[0];
+#pragma unroll
+      for (int e = 1; e < 8; ++e) { lo = fminf(lo, f[e]); hi = fmaxf(hi, f[e]); }
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+      const float span = hi - lo;  // only compared against 0 and used in the guarded candidate
+      uint32_t packed = 0;
+      if (span > 0.0f) {
+        const float qinv = qmax * (1.0f / span);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          packed |= exact_code(f[e], lo, hi, qinv, qmax) << (e * (tier == 0 ? 2 : 4));
+      }
+      if (tier == 0) reinterpret_cast<uint16_t*>(s_codes[warp])[r * 16 + j] = (uint16_t)packed;
+      else s_codes[warp][r * 16 + j] = packed;
+      if ((j & 3) == 0) s_meta[warp][r * 4 + (j >> 2)] = h2_as_u32(__floats2half2_rn(lo, hi));
+    }
+    __syncwarp();
+    // 128-bit coalesced stores of the packed chunk (1 KB INT2 / 2 KB INT4) and its metadata
+    uint32_t* codes = tier == 0 ? A.codes2 + (unit * A.rows2 + dst_row0) * 8
+                                : A.codes4 + (unit * A.rows4 + dst_row0) * 16;
+    uint32_t* meta = tier == 0 ? A.meta2 + (unit * A.rows2 + dst_row0) * 4
+                               : A.meta4 + (unit * A.rows4 + dst_row0) * 4;
+    const int n16 = tier == 0 ? 64 : 128;
+    for (int i = lane; i < n16; i += 32)
+      reinterpret_cast<uint4*>(codes)[i] = reinterpret_cast<const uint4*>(s_codes[warp])[i];
+    reinterpret_cast<uint4*>(meta)[lane] = reinterpret_cast<const uint4*>(s_meta[warp])[lane];
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE);
+}
+
+// Decode append: row (l, b, h) of k_new/v_new -> FP16 region row off_fp + len_fp.
+__global__ void append_rows_kernel(const uint16_t* __restrict__ kn, const uint16_t* __restrict__ vn,
+                                   int B, int H, const int32_t* __restrict__ seq, ckv_arena KA,
+                                   ckv_arena VA) {
+  const int unit = blockIdx.x;  // (l, b, h)
+  const int h = unit % H, b = (unit / H) % B, l = unit / (H * B);
+  const SeqRow sr = load_seq(seq, b);
+  const int t = threadIdx.x;  // 32 threads x 16 B for K, V
+  const int tsel = t >> 4, j = t & 15;
+  const uint16_t* src = (tsel ? vn : kn) + (int64_t)unit * kHeadDim;
+  const ckv_arena& A = tsel ? VA : KA;
+  uint16_t* dst = A.fp + (((int64_t)l * H + h) * A.rows_fp + sr.off_fp + sr.len_fp) * kHeadDim;
+  reinterpret_cast<uint4*>(dst)[j] = reinterpret_cast<const uint4*>(src)[j];
+}
+
+__global__ void bump_len_kernel(int32_t* seq, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) seq[b * CKV_SEQ_FIELDS + 5] += 1;
+}
+
+// (lo, hi) fp16 metadata -> the reference's f64 scale = (hi - lo) / qmax, zero_point = lo
+// (quantize_groups: scales = span / qmax, zero_points = mins, _numpy.py:65-66).
+__global__ void expand_meta_kernel(const uint32_t* __restrict__ meta, int64_t n, double qmax,
+                                   double* __restrict__ scales, double* __restrict__ zps) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float2 lh = __half22float2(u32_as_h2(meta[i]));
+  const double lo = lh.x, hi = lh.y;
+  scales[i] = __ddiv_rn(__dsub_rn(hi, lo), qmax);
+  zps[i] = lo;
+}
+
+}  // namespace ckv
+
+using namespace ckv;
+
+extern "C" {
+
+int32_t ckv_reorder_quantize_pack(const uint16_t* k, const uint16_t* v, int32_t layers,
+                                  int32_t batch, int32_t kv_heads, int64_t s_layer,
+                                  int64_t s_batch, int64_t s_token, int64_t s_head,
+                                  const uint32_t* perm, int32_t max_chunks, const int32_t* seq,
+                                  int32_t max_ctx, ckv_arena k_arena, ckv_arena v_arena,
+                                  int32_t* flag, void* stream) {
+  if (layers < 0 || batch < 0 || kv_heads < 0 || max_chunks < 0 || max_ctx < 0) return CKV_ERR_ARG;
+  if (!k || !v || !seq || !flag) return CKV_ERR_ARG;
+  if ((s_token % 8) || (s_head % 8) || (s_batch % 8) || (s_layer % 8)) return CKV_ERR_UNSUPPORTED;
+  if (layers == 0 || batch == 0 || kv_heads == 0) return CKV_OK;
+  const int slots = (int)(cdiv(max_ctx, kChunk)) + 1;
+  dim3 grid((unsigned)cdiv(slots, kQWarps), (unsigned)kv_heads, (unsigned)(layers * batch));
+  reorder_quantize_pack_kernel<<<grid, kQWarps * 32, 0, as_stream(stream)>>>(
+      k, v, kv_heads, batch, s_layer, s_batch, s_token, s_head, perm, max_chunks, seq, k_arena,
+      v_arena, flag);
+  CKV_LAUNCH_CHECK();
+  return CKV_OK;
+}
+
+int32_t ckv_append_tokens(const uint16_t* k_new, const uint16_t* v_new, int32_t layers,
+                          int32_t batch, int32_t kv_heads, int32_t* seq, ckv_arena k_arena,
+                          ckv_arena v_arena, void* stream) {
+  if (layers < 0 || batch < 0 || kv_heads < 0) return CKV_ERR_ARG;
+  if (layers * batch * kv_heads == 0) return CKV_OK;
+  append_rows_kernel<<<layers * batch * kv_heads, 32, 0, as_stream(stream)>>>(
+      k_new, v_new, batch, kv_heads, seq, k_arena, v_arena);
+  CKV_LAUNCH_CHECK();
+  bump_len_kernel<<<(unsigned)cdiv(batch, 128), 128, 0, as_stream(stream)>>>(seq, batch);
+  CKV_LAUNCH_CHECK();
+  return CKV_OK;
+}
+
+int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, double* scales,
+                        double* zero_points, void* stream) {
+  if (bits != 2 && bits != 4) return CKV_ERR_BITS;
+  if (n_groups < 0) return CKV_ERR_ARG;
+  if (n_groups == 0) return CKV_OK;
+  expand_meta_kernel<<<(unsigned)cdiv(n_groups, 256), 256, 0, as_stream(stream)>>>(
+      meta, n_groups, (double)((1 << bits) - 1), scales, zero_points);
+  CKV_LAUNCH_CHECK();
+  return CKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+"""Multi-GPU partitioning of the hot path.  One process per GPU.
+
+* Batch x kv-head sharding (cfg4): independent units, no exchange -> ``batch_shard``.
+* Sequence split-KV (cfg3, long contexts): every rank owns a chunk-aligned 1/P slice of
+  each tier segment (INT2, INT4 and FP16 chunks separately, so bytes are balanced); the
+  last rank also owns the context tail and the decode tokens.  Each rank computes
+  unnormalised partials (acc[128], m, l) for all (layer, q-head) rows of its slice; one
+  ``all_gather_into_tensor`` (NCCL over NVLink/NVSwitch) exchanges them, batched over all
+  layers of the step, and ``ckv_lse_merge`` combines them:
+      m* = max_p m_p,  o = sum_p acc_p 2^(m_p - m*) / sum_p l_p 2^(m_p - m*).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import kernels
+from .batched import CHUNK, HEAD_DIM, BatchedKVCache, lse_merge
+
+
+def batch_shard(batch, world, rank):
+    """Contiguous slice of sequences owned by `rank` (cfg4 weak scaling)."""
+    lo = rank * batch // world
+    hi = (rank + 1) * batch // world
+    return lo, hi
+
+
+def _split(n, world, rank):
+    return rank * n // world, (rank + 1) * n // world
+
+
+def sequence_shard_plan(seg_counts, world, rank):
+    """Per-sequence chunk ranges of this rank inside each tier segment (perm order).
+
+    seg_counts int [B, 3] (n2, n4, nfp).  Returns int64 [B, 6] = (a2, b2, a4, b4, af, bf)
+    in perm positions, plus owns_tail (bool): the last rank owns the tail/decode tokens.
+    """
+    seg_counts = np.asarray(seg_counts, np.int64).reshape(-1, 3)
+    out = np.zeros((seg_counts.shape[0], 6), np.int64)
+    for b, (n2, n4, nf) in enumerate(seg_counts):
+        a2, b2 = _split(n2, world, rank)
+        a4, b4 = _split(n4, world, rank)
+        af, bf = _split(nf, world, rank)
+        out[b] = (a2, b2, n2 + a4, n2 + b4, n2 + n4 + af, n2 + n4 + bf)
+    return out, rank == world - 1
+
+
+def build_sequence_shard(k, v, search, world, rank, decode_capacity=128, check=True):
+    """This rank's BatchedKVCache for a sequence-split (split-KV) layout.
+
+    k, v fp16 [L, B, T, H, 128] (the full context, e.g. prefilled redundantly or loaded
+    per rank); search = SearchResult of the full context (tiers are global).
+    """
+    L, B, T, H, D = k.shape
+    counts = search.seg_counts.cpu().numpy().astype(np.int64)
+    plan, owns_tail = sequence_shard_plan(counts, world, rank)
+    perm = search.perm
+    n_max = perm.shape[1]
+    rows = []
+    n2r = plan[:, 1] - plan[:, 0]
+    n4r = plan[:, 3] - plan[:, 2]
+    nfr = plan[:, 5] - plan[:, 4]
+    width = int((n2r + n4r + nfr).max()) if B else 0
+    idx = np.zeros((B, max(width, 1)), np.int64)
+    for b in range(B):
+        sel = np.concatenate([np.arange(plan[b, 0], plan[b, 1]), np.arange(plan[b, 2], plan[b, 3]),
+                              np.arange(plan[b, 4], plan[b, 5])])
+        idx[b, :sel.size] = sel
+    idx_d = torch.from_numpy(idx).to(perm.device)
+    perm_r = torch.gather(perm, 1, idx_d.clamp(max=n_max - 1)) if n_max else perm
+    n_glob = counts.sum(axis=1)
+    tail = T - CHUNK * n_glob
+    ctx_r = CHUNK * (n2r + n4r + nfr) + (tail if owns_tail else 0)
+    cache = BatchedKVCache(L, B, H, n2r, n4r, nfr, ctx_r, decode_capacity if owns_tail else 0,
+                           tail_src=CHUNK * n_glob, device=k.device)
+    cache.build(k, v, perm_r, check=check)
+    return cache
+
+
+def exchange_partials(part, group=None):
+    """all_gather of f32 partials [rows, 130] -> [P, rows, 130] (NCCL on GPU, gloo on CPU)."""
+    world = dist.get_world_size(group)
+    part = part.contiguous()
+    out = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype,
+                      device=part.device)
+    dist.all_gather_into_tensor(out, part, group=group)
+    return out.view((world,) + tuple(part.shape))
+
+
+def split_kv_decode(cache: BatchedKVCache, q, group=None, splits=None):
+    """Sequence-split decode step across ranks: local partials -> all_gather -> LSE merge.
+
+    q fp16 [L, B, H*m, 128] (replicated on every rank) -> fp16 [L, B, H*m, 128]."""
+    part = cache.decode_partial(q, splits=splits)
+    gathered = exchange_partials(part, group)
+    out = lse_merge(gathered)
+    return out.view(q.shape)
+
+
+__all__ = ["batch_shard", "sequence_shard_plan", "build_sequence_shard", "exchange_partials",
+           "split_kv_decode"]

@@ -1,0 +1,99 @@
+"""CPU: the C-ABI library loads without a GPU and exports exactly what include/ckv.h declares;
+host-side layout and shard planning."""
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from paper_2503_23294_b200 import _build, _lib
+from paper_2503_23294_b200.batched import CHUNK, plan_layout
+from paper_2503_23294_b200.distributed import batch_shard, sequence_shard_plan
+
+
+def test_library_is_built_for_sm100a():
+    _build.build()  # no-op when up to date
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = _lib.header_functions()
+    assert len(names) >= 19
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib._SIGNATURES), "ctypes signatures out of sync with ckv.h"
+
+
+def test_status_strings_and_version():
+    lib = _lib.load()
+    assert lib.ckv_abi_version() == 1
+    assert b"bitwidth" in lib.ckv_status_string(_lib.CKV_ERR_BITS)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.CKV_ERR_SHAPE)
+    with pytest.raises(RuntimeError):
+        _lib.check(_lib.CKV_ERR_CUDA)
+
+
+def test_argument_validation_without_gpu():
+    lib = _lib.load()
+    # validation happens before any launch, so these run on a CPU-only host
+    assert lib.ckv_pack_codes(None, 4, 3, None, None) == _lib.CKV_ERR_BITS
+    assert lib.ckv_unpack_codes(None, 1, 2, 17, None, None) == _lib.CKV_ERR_CAPACITY
+    assert lib.ckv_quantize_groups_f64(None, 2, 2, 4, 0, None, None, None, None, None) == _lib.CKV_ERR_GROUP
+    assert lib.ckv_matmul_packed_f64(None, 2, 5, 5, None, 6, None, None, 4, 6, 4, 3, 0, None, 6, 0,
+                                     None) == _lib.CKV_ERR_SHAPE
+    assert lib.ckv_search(None, None, None, None, None, 1, 4, 8, 1.5, 0.0, None, None, None, None,
+                          None, None, None) == _lib.CKV_ERR_ARG
+    ar = _lib.Arena()
+    assert lib.ckv_decode_attention(ctypes.c_void_p(16), 0, 0, ar, ar, ctypes.c_void_p(16), 1, 1, 1, 9,
+                                    0.1, 1, None, ctypes.c_void_p(16), 0, 0, None, None) == _lib.CKV_ERR_UNSUPPORTED
+    # zero-size work is a no-op success
+    assert lib.ckv_pack_codes(None, 0, 2, None, None) == _lib.CKV_OK
+
+
+def test_header_declares_reference_citations():
+    text = open(_lib.HEADER_PATH).read()
+    for cite in ("_core.pyx", "_numpy.py", "retrieval.py", "kv_store.py", "attention.py", "quantizer.py"):
+        assert cite in text
+
+
+def test_plan_layout_offsets_and_capacity():
+    seq, cap = plan_layout([3, 1, 0], [1, 0, 0], [0, 2, 1], [4 * CHUNK + 5, 3 * CHUNK, CHUNK], 10)
+    off2, len2, off4, len4, offf, lenf, tsrc, ctx = seq.T
+    assert len2.tolist() == [96, 32, 0] and off2.tolist() == [0, 96, 128]
+    assert len4.tolist() == [32, 0, 0] and off4.tolist() == [0, 32, 32]
+    assert lenf.tolist() == [5, 64, 32]
+    assert (cap % 16 == 0).all() and (cap >= lenf + 10).all()
+    assert offf.tolist() == [0, cap[0], cap[0] + cap[1]]
+    assert tsrc.tolist() == [128, 96, 32]
+    with pytest.raises(ValueError):
+        plan_layout([1], [0], [0], [CHUNK + CHUNK], 0)  # tail >= chunk
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sequence_shard_plan_partitions_every_tier(world):
+    counts = np.array([[100, 13, 2], [7, 0, 1], [0, 0, 0], [1, 1, 1]])
+    seen = [set() for _ in counts]
+    for r in range(world):
+        plan, owns_tail = sequence_shard_plan(counts, world, r)
+        assert owns_tail == (r == world - 1)
+        for b, (a2, b2, a4, b4, af, bf) in enumerate(plan):
+            n2, n4, nf = counts[b]
+            assert 0 <= a2 <= b2 <= n2 and n2 <= a4 <= b4 <= n2 + n4 and n2 + n4 <= af <= bf <= n2 + n4 + nf
+            for lo, hi in ((a2, b2), (a4, b4), (af, bf)):
+                rng = set(range(lo, hi))
+                assert not (rng & seen[b])
+                seen[b] |= rng
+    for b, c in enumerate(counts):
+        assert seen[b] == set(range(int(c.sum())))
+
+
+def test_batch_shard_covers_batch():
+    for world in (1, 2, 4, 8):
+        spans = [batch_shard(64, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == 64
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
