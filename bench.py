@@ -1,0 +1,428 @@
+"""Benchmark of the Cocktail chunk-level KV-cache hot path on B200 (BASELINE.json metric).
+
+Default (N=1): cfg2 — Llama-3-8B GQA shape (32 q / 8 kv heads, d128), 32 layers, 32K context,
+batch 8.  Per-sequence tier maps come from Module I on the device (the reference's
+synthetic workload + hashed-BoW embeddings, seeds 0-7, frozen in tests/golden/workloads.npz)
+and are asserted equal to the reference's own maps.  K/V/q are synthetic fp16 N(0,1)
+(random-init, no checkpoint).  One step = one decode step = mixed-precision attention over
+all 32 layers, launched per layer as in a real model (32 launches).  The cache (7.1 GB of
+quantized arenas) is larger than L2, so no flush is needed between steps.
+
+Reported: whole-job algorithmic GB/s (SURVEY §8d bytes), tokens/s, roofline of the decode
+kernel against MEASURED_PEAKS.json, an end-to-end figure through the public API with host
+buffers, the CPU baseline (oracle restatement of the reference, timed on host cores), and a
+prefill sub-object (cfg5-shaped search + reorder/quantize/pack, 128K x 32 layers x 8 kv heads).
+
+Under torchrun (N>1) every rank owns its own batch of 8 sequences (batch-sharded, weak scaling,
+no data-path collective); time is the max over ranks.
+
+--impl reference: the reference's CPU algorithm (oracle port of attention.py:63-90 over
+quantizer.fqm / _numpy.py) on all host cores, same metric, bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "mixed-precision KV decode-attn GB/s (% HBM peak) and tokens/s at 1/2/4/8 B200"
+WORKLOADS = os.path.join(ROOT, "tests", "golden", "workloads.npz")
+PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
+
+CFG2 = dict(layers=32, batch=8, kv_heads=8, q_per_kv=4, context=32768, head_dim=128)
+CFG5 = dict(layers=32, batch=1, kv_heads=8, context=131072, head_dim=128)
+
+
+def load_workload(ctx, seed):
+    with np.load(WORKLOADS) as z:
+        idx = z[f"{ctx}_{seed}_idx"]
+        val = z[f"{ctx}_{seed}_val"]
+        n = idx.shape[0]
+        emb = np.zeros((n, 256))
+        rows = np.repeat(np.arange(n), idx.shape[1])
+        nz = val.reshape(-1) != 0
+        emb[rows[nz], idx.reshape(-1)[nz].astype(np.int64)] = val.reshape(-1)[nz]
+        return dict(emb=emb, norm=z[f"{ctx}_{seed}_norm"], q=z[f"{ctx}_{seed}_q"],
+                    qnorm=float(z[f"{ctx}_{seed}_qnorm"]), tiers=z[f"{ctx}_{seed}_tiers"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def profile_traffic(key):
+    if os.path.exists(PROFILE_TRAFFIC):
+        with open(PROFILE_TRAFFIC) as fh:
+            return json.load(fh).get(key)
+    return None
+
+
+# ---------------------------------------------------------------------------------------
+# CPU legs (oracle restatement of the reference; test infrastructure used as the baseline)
+
+def _cpu_unit(args):
+    q, k, v, tiers = args
+    from oracle import ckv_oracle as O
+    t0 = time.perf_counter()
+    cache = O.build_cache(k, v, tiers, 32, 32)
+    t1 = time.perf_counter()
+    O.mixed_decode_attention(q, cache)
+    t2 = time.perf_counter()
+    s = cache
+    nbytes = s.len_2 * 96 + s.len_4 * 160 + s.len_fp * 512 + 2 * q.size * 2
+    return t2 - t1, nbytes
+
+
+def _cpu_sample_units(n_units, ctx, m, rng):
+    from oracle import ckv_oracle as O  # noqa: F401
+    units = []
+    for u in range(n_units):
+        wl = load_workload(32768, u % 8) if ctx == 32768 else None
+        tiers = wl["tiers"] if wl is not None else rng.choice([0, 1, 2], size=ctx // 32).astype(np.uint8)
+        k = rng.standard_normal((ctx, 128)).astype(np.float16).astype(np.float64)
+        v = rng.standard_normal((ctx, 128)).astype(np.float16).astype(np.float64)
+        q = rng.standard_normal((m, 128)).astype(np.float16).astype(np.float64)
+        units.append((q, k, v, tiers))
+    return units
+
+
+def cpu_baseline(seconds=12.0, processes=1):
+    """Time the oracle's restatement of mixed_decode_attention on cfg2 units (32K, m=4)."""
+    rng = np.random.default_rng(0)
+    per = 2 if processes == 1 else processes
+    done_bytes, busy, n_done = 0, 0.0, 0
+    t_start = time.perf_counter()
+    if processes > 1:
+        import multiprocessing as mpx
+        pool = mpx.get_context("fork").Pool(processes)
+    else:
+        pool = None
+    while time.perf_counter() - t_start < seconds:
+        units = _cpu_sample_units(per, CFG2["context"], CFG2["q_per_kv"], rng)
+        res = pool.map(_cpu_unit, units) if pool else [_cpu_unit(u) for u in units]
+        # decode-only time per unit; with P processes the aggregate rate is P x the per-process
+        # rate (optimistic for the CPU: assumes perfect scaling across cores)
+        busy += sum(r[0] for r in res) / max(processes, 1)
+        done_bytes += sum(r[1] for r in res)
+        n_done += len(res)
+    if pool:
+        pool.close()
+    return done_bytes / busy / 1e9, n_done, busy
+
+
+# ---------------------------------------------------------------------------------------
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's CPU algorithm on all host cores; rank 0 only."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    steps_gbs = []
+    for _ in range(args.warmup):
+        cpu_baseline(seconds=0.5, processes=cores)
+    for _ in range(args.steps):
+        gbs, n, busy = cpu_baseline(seconds=max(2.0, 20.0 / max(args.steps, 1)), processes=cores)
+        steps_gbs.append(gbs)
+    value = statistics.median(steps_gbs)
+    sample = f"{cores}-process fan-out over cfg2 units (32K ctx, m=4, reference tier maps), per step >= 2 s"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: Llama-3-8B GQA 32q/8kv d128, 32 layers, 32K ctx, batch 8",
+                   "sampled_units": True},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def build_cfg2(torch, dev, rank):
+    from paper_2503_23294_b200 import batched, retrieval
+
+    c = CFG2
+    L, B, H, m, T, D = c["layers"], c["batch"], c["kv_heads"], c["q_per_kv"], c["context"], c["head_dim"]
+    wls = [load_workload(T, (rank * B + b) % 8) for b in range(B)]
+    emb = np.stack([w["emb"] for w in wls])
+    norm = np.stack([w["norm"] for w in wls])
+    qv = np.stack([w["q"] for w in wls])
+    qn = np.array([w["qnorm"] for w in wls])
+    search = retrieval.search_batched(emb, norm, qv, qn, 0.6, 0.1)
+    tiers = search.tiers.cpu().numpy()
+    ref_tiers = np.stack([w["tiers"] for w in wls])
+    if not np.array_equal(tiers, ref_tiers):
+        raise SystemExit("tier maps differ from the reference's (Module I parity failure)")
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    k = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    v = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    cache = batched.build_cache_batched(k, v, search, decode_capacity=128)
+    del k, v
+    q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
+    return cache, q, search
+
+
+def bench_prefill(torch, dev, steps=3):
+    """cfg5-shaped prefill: search + reorder/quantize/pack of a 128K x 32-layer x 8-head cache."""
+    from paper_2503_23294_b200 import batched, retrieval
+
+    c = CFG5
+    L, B, H, T, D = c["layers"], c["batch"], c["kv_heads"], c["context"], c["head_dim"]
+    wl = load_workload(T, 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    k = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    v = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    s = retrieval.search_batched(wl["emb"][None], wl["norm"][None], wl["q"][None], np.array([wl["qnorm"]]))
+    if not np.array_equal(s.tiers.cpu().numpy()[0], wl["tiers"]):
+        raise SystemExit("128K tier map differs from the reference's")
+    counts = s.seg_counts.cpu().numpy()
+    cache = batched.BatchedKVCache(L, B, H, counts[:, 0], counts[:, 1], counts[:, 2], [T], 0, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    times_build, times_search = [], []
+    for i in range(steps + 2):
+        flush.fill_(i)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        s2 = retrieval.search_batched(wl["emb"][None], wl["norm"][None], wl["q"][None],
+                                      np.array([wl["qnorm"]]), check=False)
+        e1.record()
+        cache.build(k, v, s2.perm, check=False)
+        e2.record()
+        torch.cuda.synchronize()
+        if i >= 2:
+            times_search.append(e0.elapsed_time(e1))
+            times_build.append(e1.elapsed_time(e2))
+    tb = statistics.median(times_build) * 1e-3
+    n2, n4, nf = (int(x) for x in counts[0])
+    read = 2 * L * H * T * D * 2
+    write = 2 * L * H * (n2 * 32 * 48 + n4 * 32 * 80 + (nf * 32 + (T - 32 * (n2 + n4 + nf))) * 256)
+    peak, _ = measured_peak_gbs()
+    ach = (read + write) / tb / 1e9
+    del k, v, cache
+    torch.cuda.empty_cache()
+    return {
+        "workload": "cfg5: prefill search + reorder/quantize/pack, 128K ctx x 32 layers x 8 kv heads, b1",
+        "tier_fractions": [round(x / (n2 + n4 + nf), 4) for x in (n2, n4, nf)],
+        "quantize_ms": round(tb * 1e3, 3), "search_ms": round(statistics.median(times_search), 3),
+        "bytes_read": read, "bytes_written": write,
+        "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(ach / peak, 4), "traffic": profile_traffic("reorder_quantize_pack")},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--splits", type=int, default=None)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cache, q, search = build_cfg2(torch, dev, rank)
+    L, B = cache.L, cache.B
+    m = q.shape[2] // cache.H
+    splits = args.splits or cache.default_splits(m, 1)
+    out = torch.empty_like(q)
+    step_bytes = cache.algorithmic_bytes(m)
+
+    def step():
+        for l in range(L):
+            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sec = ms * 1e-3
+    value = world * step_bytes / sec / 1e9
+    tokens_per_s = world * B / sec
+
+    # single-launch (all 32 layers in one grid) figure for the same cache
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        cache.decode(q, out=out)
+    e2.record()
+    for _ in range(args.steps):
+        cache.decode(q, out=out)
+    e3.record()
+    torch.cuda.synchronize()
+    fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
+
+    # end to end through the public API: pinned host q -> H2D, decode (all layers), D2H
+    qh = q.cpu().pin_memory()
+    oh = torch.empty(q.shape, dtype=torch.float16, pin_memory=True)
+    qd = torch.empty_like(q)
+    for _ in range(3):
+        qd.copy_(qh, non_blocking=True)
+        for l in range(L):
+            cache.decode(qd[l:l + 1], splits=splits, out=out[l:l + 1], layer=l)
+        oh.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record()
+    for _ in range(args.steps):
+        qd.copy_(qh, non_blocking=True)
+        for l in range(L):
+            cache.decode(qd[l:l + 1], splits=splits, out=out[l:l + 1], layer=l)
+        oh.copy_(out, non_blocking=True)
+    e5.record()
+    torch.cuda.synchronize()
+    e2e_ms = e4.elapsed_time(e5) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_gbs = world * step_bytes / (e2e_ms * 1e-3) / 1e9
+
+    prefill = None
+    if rank == 0 and world == 1 and not args.no_prefill:
+        del cache
+        torch.cuda.empty_cache()
+        prefill = bench_prefill(torch, dev)
+
+    if rank == 0:
+        peak, peak_kind = measured_peak_gbs()
+        per_launch_bytes = step_bytes / L
+        achieved = per_launch_bytes / (ms * 1e-3 / L) / 1e9 / 1.0
+        launches_per_step = L * (2 if splits > 1 else 1)
+        counts = search.seg_counts.cpu().numpy()
+        frac = counts.sum(axis=0) / counts.sum()
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+            "data": "synthetic (fp16 N(0,1) K/V/q; reference search tier maps, seeds 0-7)",
+            "config": {"workload": "cfg2: Llama-3-8B GQA 32q/8kv d128, 32 layers, 32K ctx, batch 8 per GPU",
+                       "global_batch": B * world, "seq_len": CFG2["context"], "parallelism": f"batch-shard x{world}",
+                       "tier_fractions_int2_int4_fp16": [round(float(x), 4) for x in frac],
+                       "launch": "per-layer (32 launches per step)", "splits": splits,
+                       "l2": "inputs larger than L2 (7.1 GB arenas vs 126 MB L2)"},
+            "tokens_per_s": round(tokens_per_s, 1),
+            "algorithmic_bytes_per_step": step_bytes,
+            "single_launch_all_layers_gbs": round(fused_gbs, 2),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                         "traffic": profile_traffic("decode_kernel")},
+            "e2e": {"value": round(e2e_gbs, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(q.numel() * 2)},
+            "gpu_launches": args.steps * launches_per_step,
+            "clocks": clk.summary(),
+        }
+        if prefill is not None:
+            line["prefill"] = prefill
+        if world == 1 and not args.no_cpu_baseline:
+            gbs, n, busy = cpu_baseline(seconds=12.0, processes=1)
+            line["cpu_baseline"] = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                                    "sample": f"{n} cfg2 units (32K ctx, m=4) through the oracle restatement "
+                                              f"of mixed_decode_attention, {busy:.1f} s single process"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

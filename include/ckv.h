@@ -143,6 +143,9 @@ typedef struct ckv_arena {
   uint32_t* codes4;   /* u32 [L][H][rows4][16]                                  */
   uint32_t* meta4;    /* half2 (lo, hi) [L][H][rows4][4]                         */
   uint16_t* fp;       /* fp16 [L][H][rows_fp][128] (FP16 chunks || tail || decode) */
+  uint32_t* span_flags; /* u32 [L][H][B], zero-filled before build: bit0/bit1 set when an
+                           INT2/INT4 group's scale exceeds 4000 (decode then runs that unit in
+                           its exact unweighted mode; nullable) */
   int64_t rows2, rows4, rows_fp;
 } ckv_arena;
 
@@ -184,9 +187,15 @@ int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, do
  * for every (layer, sequence, kv-head) unit at once).  q fp16 [L][B][H*m][128] (strides
  * q_s_layer, q_s_batch in elements), m = q heads per kv head (1..8).  Online softmax over the
  * virtual sequence INT2 || INT4 || FP16 with split-KV; scale = softmax scale (1/sqrt(128)).
- * Output fp16 [L][B][H*m][128].  Workspace: ckv_decode_workspace_bytes(). */
+ * Output fp16 [L][B][H*m][128].  Workspace: ckv_decode_workspace_bytes() bytes, zero-filled
+ * once before first use (it holds self-resetting split arrival counters; the last CTA of
+ * each unit merges the split partials inside the same launch).  partial_out (nullable):
+ * write unnormalised f32 [L][B][H*m][130] = (acc[128], m (log2 domain), l) instead of out,
+ * for a cross-GPU split-KV merge with ckv_lse_merge. */
 int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                                    int32_t splits);
+/* Resident decode CTAs per SM on the current device (for sizing `splits` to whole waves). */
+int32_t ckv_decode_ctas_per_sm(void);
 int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
                              ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
                              int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,

@@ -46,7 +46,7 @@ class Arena(ctypes.Structure):
 
     _fields_ = [
         ("codes2", _vp), ("meta2", _vp), ("codes4", _vp), ("meta4", _vp), ("fp", _vp),
-        ("rows2", _i64), ("rows4", _i64), ("rows_fp", _i64),
+        ("span_flags", _vp), ("rows2", _i64), ("rows4", _i64), ("rows_fp", _i64),
     ]
 
 
@@ -71,6 +71,7 @@ _SIGNATURES = {
     "ckv_append_tokens": ([_vp, _vp, _i32, _i32, _i32, _vp, Arena, Arena, _vp], _i32),
     "ckv_expand_meta": ([_vp, _i64, _i32, _vp, _vp, _vp], _i32),
     "ckv_decode_workspace_bytes": ([_i32, _i32, _i32, _i32, _i32], _i64),
+    "ckv_decode_ctas_per_sm": ([], _i32),
     "ckv_decode_attention": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _f32, _i32,
                               _vp, _vp, _i64, _i64, _vp, _vp], _i32),
     "ckv_lse_merge": ([_vp, _i32, _i64, _vp, _vp], _i32),

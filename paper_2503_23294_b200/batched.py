@@ -90,7 +90,8 @@ class BatchedKVCache:
         z32 = lambda *s: torch.zeros(s, dtype=torch.int32, device=dev)  # noqa: E731
         self.k = dict(codes2=z32(L, H, self.rows2, 8), meta2=z32(L, H, self.rows2, 4),
                       codes4=z32(L, H, self.rows4, 16), meta4=z32(L, H, self.rows4, 4),
-                      fp=torch.zeros((L, H, self.rows_fp, HEAD_DIM), dtype=torch.float16, device=dev))
+                      fp=torch.zeros((L, H, self.rows_fp, HEAD_DIM), dtype=torch.float16, device=dev),
+                      span_flags=z32(L, H, self.B))
         self.v = {k: torch.zeros_like(t) for k, t in self.k.items()}
         self._ws = {}
 
@@ -109,11 +110,12 @@ class BatchedKVCache:
         cache.build(k, v, search.perm, check=check)
         return cache
 
-    def arena(self, which):
+    def arena(self, which, layer=0):
+        """ckv_arena view starting at `layer` (per-layer launches index layers from there)."""
         t = self.k if which == "k" else self.v
-        return _lib.Arena(t["codes2"].data_ptr(), t["meta2"].data_ptr(), t["codes4"].data_ptr(),
-                          t["meta4"].data_ptr(), t["fp"].data_ptr(), self.rows2, self.rows4,
-                          self.rows_fp)
+        ptr = lambda name: t[name].data_ptr() + layer * t[name].stride(0) * t[name].element_size()  # noqa: E731
+        return _lib.Arena(ptr("codes2"), ptr("meta2"), ptr("codes4"), ptr("meta4"), ptr("fp"),
+                          ptr("span_flags"), self.rows2, self.rows4, self.rows_fp)
 
     def build(self, k, v, perm, check=True):
         """ckv_reorder_quantize_pack over every unit; perm i32/u32 [B, max_chunks]."""
@@ -125,6 +127,8 @@ class BatchedKVCache:
         if (L, B, H) != (self.L, self.B, self.H) or D != HEAD_DIM or k.stride(4) != 1:
             raise ValueError("K/V shape does not match the cache")
         perm = kernels.to_dev(perm, torch.int32)
+        self.k["span_flags"].zero_()
+        self.v["span_flags"].zero_()
         flag = torch.zeros(1, dtype=torch.int32, device=k.device)
         _lib.call("ckv_reorder_quantize_pack", _lib.ptr(k), _lib.ptr(v), L, B, H, k.stride(0),
                   k.stride(1), k.stride(2), k.stride(3), _lib.ptr(perm), perm.shape[1],
@@ -139,38 +143,53 @@ class BatchedKVCache:
         s = self.seq_host
         return (s[:, 1] + s[:, 3] + s[:, 5]).astype(np.int64)
 
-    def default_splits(self, m):
-        """Enough CTAs for ~2 waves of 4 CTAs/SM, capped by tiles per unit."""
-        units = self.L * self.B * self.H
-        target = 8 * _num_sms()
+    def default_splits(self, m, layers=None):
+        """Split-KV factor: the whole grid should fill whole waves of resident CTAs (a
+        byte-balanced split makes every CTA equally long, so the tail is the partial wave),
+        while keeping >= ~16 tiles per CTA so partial traffic stays negligible."""
+        units = (self.L if layers is None else layers) * self.B * self.H
+        per_sm = _lib.load().ckv_decode_ctas_per_sm()
+        slots = _num_sms() * max(per_sm, 1)
         tiles = int(max(1, (self.total_tokens().max() + TILE - 1) // TILE))
-        return int(max(1, min(-(-target // max(units, 1)), tiles // 4 if tiles >= 8 else 1, 64)))
+        best, best_cost = 1, None
+        for s in range(1, 65):
+            if s > 1 and tiles // s < 16:
+                break
+            waves = -(-units * s // slots)
+            cost = waves / (units * s / slots) + 0.002 * s  # tail waste + merge overhead
+            if best_cost is None or cost < best_cost - 1e-9:
+                best, best_cost = s, cost
+        return best
 
     def _workspace(self, m, splits):
         key = (m, splits)
         if key not in self._ws:
             nbytes = _lib.load().ckv_decode_workspace_bytes(self.L, self.B, self.H, m, splits)
-            self._ws[key] = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
+            # zero once: the split-KV arrival counters live at the front and self-reset
+            self._ws[key] = torch.zeros(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
         return self._ws[key]
 
-    def decode(self, q, splits=None, out=None, scale=None):
-        """Mixed-precision decode attention for q fp16 [L, B, H*m, 128] -> fp16 same shape."""
+    def decode(self, q, splits=None, out=None, scale=None, layer=0):
+        """Mixed-precision decode attention for q fp16 [L', B, H*m, 128] -> fp16 same shape,
+        over layers [layer, layer + L') of the cache (L' = L for the whole model in one launch,
+        1 for the per-layer launches of a real decode step)."""
         L, B, Hq, D = q.shape
-        if (L, B) != (self.L, self.B) or D != HEAD_DIM or Hq % self.H:
+        if B != self.B or layer < 0 or layer + L > self.L or D != HEAD_DIM or Hq % self.H:
             raise ValueError("q shape does not match the cache")
         if q.dtype != torch.float16 or q.stride(3) != 1 or q.stride(2) != HEAD_DIM:
             raise ValueError("q must be fp16 with contiguous heads")
         if (self.total_tokens() == 0).any():
             raise ValueError("cache holds no tokens")  # attention.py:71-72
         m = Hq // self.H
-        splits = self.default_splits(m) if splits is None else int(splits)
+        splits = self.default_splits(m, L) if splits is None else int(splits)
         if out is None:
             out = torch.empty((L, B, Hq, D), dtype=torch.float16, device=q.device)
         ws = self._workspace(m, splits)
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
-        _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k"),
-                  self.arena("v"), _lib.ptr(self.seq), L, B, self.H, m, scale, splits,
-                  _lib.ptr(ws), _lib.ptr(out), out.stride(0), out.stride(1), None, _lib.stream())
+        _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1),
+                  self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H,
+                  m, scale, splits, _lib.ptr(ws), _lib.ptr(out), out.stride(0), out.stride(1), None,
+                  _lib.stream())
         return out
 
     def decode_partial(self, q, splits=None, scale=None):
@@ -207,6 +226,10 @@ class BatchedKVCache:
 
     def memory_bytes(self):
         return sum(t.numel() * t.element_size() for d in (self.k, self.v) for t in d.values())
+
+    def wide_scale_units(self):
+        """Number of (layer, kv-head, sequence) units that use the exact wide-scale path."""
+        return int(((self.k["span_flags"] | self.v["span_flags"]) != 0).sum().item())
 
     # -- export to the reference per-head format ------------------------------------------
     def export_unit(self, layer, seq, head, perm=None):

@@ -3,19 +3,26 @@
 //     per-tier q.K^T (fqm, transpose)    attention.py:75-77 -> quantizer.fqm -> _core.pyx:148-192
 //     concat, *= scale, one softmax      attention.py:78-82, stable_softmax attention.py:24-31
 //     per-tier P.V summed                attention.py:84-90
-// for every (layer, sequence, kv-head) unit in one launch.  One global softmax over the
+// for every (layer, sequence, kv-head) unit in one launch.  The one global softmax over the
 // concatenated INT2 || INT4 || FP16 sequence is computed as an online (m, l, acc) softmax
-// walked tile by tile; split-KV partials are merged by log-sum-exp.  Mathematically the
-// same result; numerically fp16 operands with fp32 accumulation.
+// walked tile by tile; split-KV partials are merged by log-sum-exp in the same launch (the
+// last CTA of a unit merges).  fp16 operands, fp32 accumulation.
 //
 // Tile = 16 tokens.  Per warp and tile:
 //   S^T[16 tok x 8 q] = K_tile[16 x 128] . Q^T          mma.m16n8k16 x 8  (+1 for the lo term)
 //   P = exp2(S - m) (online, lazy rescale), P^T -> P via movmatrix
 //   O^T[128 d x 8 q] += V_tile^T[128 x 16] . P^T        mma.m16n8k16 x 8  (+1 for the lo term)
-// Quantized operands are rebuilt in registers from the reference-format packed words:
-//   fp16 magic: (code << j) | exp(2^(10-j)) == 2^(10-j) + code exactly, then
-//   v = fma(x, sc, -2^(10-j) sc) = sc * code  (one rounding); the per-(token, group) zero point
-//   lo is applied through an extra MMA (K side: lo x sum_g(q); V side: sum_t p_t lo_t).
+// Quantized tiles stream through a per-warp 4-stage cp.async ring in shared memory (rows
+// permuted inside the tile so every fragment read is bank-conflict free); FP16 tiles (<4% of
+// bytes) are read straight from global memory.  Operands are rebuilt in registers from the
+// reference-format packed words:
+//   fp16 magic: (code << j) | exp(16)  ==  16 + code * 2^(j-6)  exactly, then
+//   v = fma(x, sc, -16 sc) = sc * code * 2^(j-6)  (one rounding, one constant per scale).
+//   The per-slot power-of-two weight 2^(j-6) is folded into q (K side: q' = q 2^(6-j) per
+//   d-slot) and into the output rows (V side: j depends only on the m-tile, undone once at
+//   the end).  The per-(token, group) zero point lo goes through one extra MMA per side
+//   (K: lo x sum_g(q); V: sum_t p_t lo_t).  Units whose scales (or q) are too wide for the
+//   weighted form run an unweighted exact mode (code by subtraction, full affine).
 #include <math.h>
 
 #include "ckv_common.cuh"
@@ -24,6 +31,14 @@ namespace ckv {
 
 constexpr int kDecWarps = 4;
 constexpr int kTile = 16;
+constexpr int kStages = 3;
+// Stage layout is lane-ordered: every lane's fragment data for one tile sits in 16-byte
+// slots [region][lane][16 B], filled by cp.async straight from the reference-format rows.
+//   INT2: KC @0 (tok g | tok g+8, 8 B each), VC @512 (word g of tok 2c,2c+1,2c+8,2c+9),
+//         KM @1024 (meta tok g, g+8 of group c), VM @1536 (meta of the 4 V tokens, group g/2)
+//   INT4: KC @0 (tok g, 16 B) @512 (tok g+8), VC @1024 (tok 2c|2c+1, 8 B each) @1536 (2c+8|2c+9),
+//         KM @2048, VM @2560
+constexpr int kStageBytes = 3072;
 constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
 
@@ -34,10 +49,12 @@ struct DecArgs {
   const int32_t* seq;
   int L, B, H, m, splits;
   float scale_log2;
-  float* ws;  // [L][B][H*m][splits][130]
+  float* ws;            // [L*B*H*m][splits][130] partials
+  uint32_t* counters;   // [L*B*H] arrival counters (self-resetting)
   uint16_t* out;
   int64_t o_sl, o_sb;
-  float* partial_out;  // [L][B][H*m][130] or null
+  float* partial_out;   // [L][B][H*m][130] or null
+  uint32_t zero;        // runtime 0: keeps the fp16 magic exponents in registers (see Magic)
 };
 
 struct Seq8 {
@@ -55,66 +72,96 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
   return r;
 }
+// Keep a constant in a register (LOP3 takes one immediate; the magic exponent is the 2nd).
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
 
-// half2 (lo, hi) metadata -> scale (hi - lo)/qmax as fp16 and lo as fp16
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" :: "r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" :: "r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N)); }
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+
+constexpr uint32_t kMagic16 = 0x4C004C00u;  // fp16 16.0 in both halves
+constexpr float kWideScale = 4000.0f;       // weighted mode needs 16 * sc and 12 * sc in fp16 range
+constexpr float kWideQ = 1000.0f;           // and |q| 2^6 in fp16 range
+
+// scale (hi - lo) / qmax of one (lo, hi) half2 metadata word (hi - lo via mixed f16/f32 add)
 __device__ __forceinline__ float meta_scale(uint32_t meta, float inv_qmax) {
-  const float2 lh = __half22float2(u32_as_h2(meta));
-  return (lh.y - lh.x) * inv_qmax;
-}
-__device__ __forceinline__ uint32_t meta_lo_pair(uint32_t m0, uint32_t m1) {
-  return prmt(m0, m1, 0x5410);  // (lo0, lo1)
+  float d;
+  asm("{.reg .f16 lo, hi; .reg .f32 a; mov.b32 {lo, hi}, %1; cvt.f32.f16 a, lo; sub.rn.f32.f16 %0, hi, a;}"
+      : "=f"(d) : "r"(meta));
+  return d * inv_qmax;
 }
 
-// Per pair-register dequant constants for one (sc_lo_half, sc_hi_half) pair.
-// negB[k] = -2^(10-2k) * sc  for magic exponents j = 2k (k = 0..4).
 struct DeqC {
-  __half2 sc;
-  __half2 negB[5];
+  __half2 sc;  // (sc_lo_half, sc_hi_half)
+  __half2 nm;  // -16 * sc  (exact: power-of-two multiple)
 };
 __device__ __forceinline__ DeqC make_deq(float s0, float s1) {
   DeqC d;
   d.sc = __floats2half2_rn(s0, s1);
-#pragma unroll
-  for (int k = 0; k < 5; ++k) d.negB[k] = __hmul2(d.sc, __float2half2_rn(-(float)(1 << (10 - 2 * k))));
+  d.nm = __hmul2(d.sc, __float2half2_rn(-16.0f));
   return d;
 }
 
-// INT2: 2-bit codes at bits (2i, 16 + 2i) of x; pair index i in 0..7 (i >= 5 uses x >> 10).
-template <int I>
-__device__ __forceinline__ uint32_t deq2(uint32_t c, const DeqC& d) {
-  constexpr int j = I <= 4 ? 2 * I : 2 * (I - 5);
-  const uint32_t x = I <= 4 ? c : (c >> 10);
-  const uint32_t raw = (x & (0x00030003u << j)) | (((uint32_t)(25 - j) << 10) * 0x10001u);
-  return h2_as_u32(__hfma2(u32_as_h2(raw), d.sc, d.negB[j / 2]));
+// weighted dequant of a pair of codes at bits (j, 16 + j) of x (mask = code mask << j)
+__device__ __forceinline__ uint32_t wdeq(uint32_t x, uint32_t mask, uint32_t magic, const DeqC& d) {
+  const uint32_t raw = (x & mask) | magic;
+  return h2_as_u32(__hfma2(u32_as_h2(raw), d.sc, d.nm));
 }
-// INT4: 4-bit codes at bits (4i, 16 + 4i) of x; i in 0..3 (i >= 2 uses x >> 8).
-template <int I>
-__device__ __forceinline__ uint32_t deq4(uint32_t c, const DeqC& d) {
-  constexpr int j = 4 * (I & 1);
-  const uint32_t x = I < 2 ? c : (c >> 8);
-  const uint32_t raw = (x & (0x000F000Fu << j)) | (((uint32_t)(25 - j) << 10) * 0x10001u);
-  return h2_as_u32(__hfma2(u32_as_h2(raw), d.sc, d.negB[j / 2]));
-}
-// Slow path (scale too large for the magic bias): exact code via subtraction, full affine.
-template <int BITS>
-__device__ __forceinline__ uint32_t deq_slow(uint32_t c, int i, __half2 sc, __half2 lo) {
-  const int j = BITS == 2 ? (i <= 4 ? 2 * i : 2 * (i - 5)) : 4 * (i & 1);
-  const uint32_t x = BITS == 2 ? (i <= 4 ? c : c >> 10) : (i < 2 ? c : c >> 8);
-  const uint32_t mask = (BITS == 2 ? 0x00030003u : 0x000F000Fu) << j;
-  const uint32_t raw = (x & mask) | (((uint32_t)(25 - j) << 10) * 0x10001u);
-  const __half2 bias = __float2half2_rn((float)(1 << (10 - j)));
-  const __half2 code = __hsub2(u32_as_h2(raw), bias);  // exact small integer
+// exact (unweighted) dequant: code by subtraction, full affine v = code * sc + lo
+__device__ __forceinline__ uint32_t edeq(uint32_t x, int j, uint32_t cmask, __half2 sc, __half2 lo) {
+  const uint32_t raw = (x & (cmask << j)) | (((uint32_t)(25 - j) << 10) * 0x10001u);
+  const __half2 code = __hsub2(u32_as_h2(raw), __float2half2_rn((float)(1 << (10 - j))));
   return h2_as_u32(__hfma2(code, sc, lo));
 }
 
+// INT2 K pair i of a word: bits (2i, 16+2i) for i <= 4, (2(i-5), ...) of w >> 10 for i >= 5
+template <int I> struct K2 {
+  static constexpr int j = I <= 4 ? 2 * I : 2 * (I - 5);
+  static constexpr bool hi = I >= 5;
+};
+// INT4 K pair i (of a 4-pair PRMT word): bits (4(i&1), ...) of x or x >> 8
+template <int I> struct K4 {
+  static constexpr int j = 4 * (I & 1);
+  static constexpr bool hi = (I & 3) >= 2;
+};
+
 struct WarpState {
   float acc[8][4];  // O^T C-fragments, m-tile mt: rows d = 16g+mt (c0,c1), 16g+8+mt (c2,c3)
-  float lacc[4];    // sum_t p_t * lo_t per (group of row g, col)
+  float lacc[2];    // sum_t p_t * lo_t for the group of row g, cols 2c, 2c+1
   float mrun[2];    // running max (log2 domain) for cols 2c, 2c+1
   float lsum[2];
 };
 
-// Online softmax on one S^T tile and P^T -> P B-fragments for the PV MMA.
 __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint32_t& bp0,
                                              uint32_t& bp1) {
   float t0 = fmaxf(s[0], s[2]), t1 = fmaxf(s[1], s[3]);
@@ -132,7 +179,7 @@ __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint3
     for (int mt = 0; mt < 8; ++mt) {
       st.acc[mt][0] *= f0; st.acc[mt][1] *= f1; st.acc[mt][2] *= f0; st.acc[mt][3] *= f1;
     }
-    st.lacc[0] *= f0; st.lacc[1] *= f1; st.lacc[2] *= f0; st.lacc[3] *= f1;
+    st.lacc[0] *= f0; st.lacc[1] *= f1;
     st.lsum[0] *= f0; st.lsum[1] *= f1;
     st.mrun[0] = n0; st.mrun[1] = n1;
   }
@@ -144,116 +191,135 @@ __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint3
   bp1 = movmatrix_trans(h2_as_u32(__floats2half2_rn(p2, p3)));  // (P[g][8+2c], P[g][9+2c])
 }
 
-// ---- INT2 tile ------------------------------------------------------------------
-__device__ __forceinline__ void tile_int2(const DecArgs& a, const uint32_t* kc, const uint32_t* km,
-                                          const uint32_t* vc, const uint32_t* vm,
-                                          const uint32_t (&qb)[8][2], uint32_t qaug, WarpState& st,
-                                          int g, int c) {
-  // K: tokens g, g+8; group c = words 2c, 2c+1 (d 32c .. 32c+31)
-  const uint2 kw0 = *reinterpret_cast<const uint2*>(kc + g * 8 + 2 * c);
-  const uint2 kw1 = *reinterpret_cast<const uint2*>(kc + (g + 8) * 8 + 2 * c);
-  const uint32_t km0 = km[g * 4 + c], km1 = km[(g + 8) * 4 + c];
-  // V: tokens 2c, 2c+1, 2c+8, 2c+9; word g (d 16g .. 16g+15), group g/2
-  const uint32_t v0 = vc[(2 * c) * 8 + g], v1 = vc[(2 * c + 1) * 8 + g];
-  const uint32_t v2 = vc[(2 * c + 8) * 8 + g], v3 = vc[(2 * c + 9) * 8 + g];
-  const uint32_t vm0 = vm[(2 * c) * 4 + (g >> 1)], vm1 = vm[(2 * c + 1) * 4 + (g >> 1)];
-  const uint32_t vm2 = vm[(2 * c + 8) * 4 + (g >> 1)], vm3 = vm[(2 * c + 9) * 4 + (g >> 1)];
-  constexpr float iq = 1.0f / 3.0f;
-  const float sk0 = meta_scale(km0, iq), sk1 = meta_scale(km1, iq);
-  const float sv0 = meta_scale(vm0, iq), sv1 = meta_scale(vm1, iq);
-  const float sv2 = meta_scale(vm2, iq), sv3 = meta_scale(vm3, iq);
-  const float smax = fmaxf(fmaxf(fmaxf(sk0, sk1), fmaxf(sv0, sv1)), fmaxf(sv2, sv3));
-  const bool slow = __any_sync(0xffffffffu, smax > 63.0f);
+// Q B-fragments live in shared memory as three sets ([set][9][32 lanes] x 8 B, one copy per
+// CTA): 0 = INT2 slot weights, 1 = INT4 slot weights, 2 = unweighted (FP16 tiles and the exact
+// mode).  Entry 8 of a set holds the (hi, lo) split of sum_g(q) for the zero-point MMA.
+constexpr int kQSet = 9 * 32 * 8;
+struct QS {
+  uint32_t base;  // s_q + 8 * lane
+  __device__ __forceinline__ uint2 ld(int set, int ks) const { return lds64(base + set * kQSet + 256 * ks); }
+  __device__ __forceinline__ uint32_t aug() const { return lds32(base + 256 * 8); }
+};
 
-  float s[4] = {0.f, 0.f, 0.f, 0.f};
-  if (!slow) {
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t a3, uint2 b) {
+  mma_16816(d, a0, a1, a2, a3, b.x, b.y);
+}
+
+__device__ __forceinline__ void lo_mma(WarpState& st, uint32_t a0, uint32_t a2, uint32_t bp0, uint32_t bp1) {
+  float t[4] = {st.lacc[0], st.lacc[1], 0.f, 0.f};
+  mma_16816(t, a0, 0u, a2, 0u, bp0, bp1);
+  st.lacc[0] = t[0];
+  st.lacc[1] = t[1];
+}
+
+// ---- INT2 tile from a shared-memory stage ----------------------------------------------
+template <bool EXACT>
+__device__ __forceinline__ void tile_int2(uint32_t sl, const QS& qs, uint32_t mg, WarpState& st) {
+  const uint4 kk = lds128(sl);  // (tok g: words 2c, 2c+1), (tok g+8: words 2c, 2c+1)
+  const uint2 kmm = lds64(sl + 1024);
+  const uint4 vv = lds128(sl + 512);
+  const uint4 vmm = lds128(sl + 1536);
+  constexpr float iq = 1.0f / 3.0f;
+  const float sk0 = meta_scale(kmm.x, iq), sk1 = meta_scale(kmm.y, iq);
+  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
+  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
+
+  float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+  if (!EXACT) {
     const DeqC dk0 = make_deq(sk0, sk0), dk1 = make_deq(sk1, sk1);
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
-      const uint32_t w0 = blk ? kw0.y : kw0.x, w1 = blk ? kw1.y : kw1.x;
-      mma_16816(s, deq2<0>(w0, dk0), deq2<0>(w1, dk1), deq2<1>(w0, dk0), deq2<1>(w1, dk1), qb[4 * blk + 0][0], qb[4 * blk + 0][1]);
-      mma_16816(s, deq2<2>(w0, dk0), deq2<2>(w1, dk1), deq2<3>(w0, dk0), deq2<3>(w1, dk1), qb[4 * blk + 1][0], qb[4 * blk + 1][1]);
-      mma_16816(s, deq2<4>(w0, dk0), deq2<4>(w1, dk1), deq2<5>(w0, dk0), deq2<5>(w1, dk1), qb[4 * blk + 2][0], qb[4 * blk + 2][1]);
-      mma_16816(s, deq2<6>(w0, dk0), deq2<6>(w1, dk1), deq2<7>(w0, dk0), deq2<7>(w1, dk1), qb[4 * blk + 3][0], qb[4 * blk + 3][1]);
+      const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
+      const uint32_t w0s = w0 >> 10, w1s = w1 >> 10;
+#define KD(W, WS, D, I) wdeq(K2<I>::hi ? WS : W, 0x00030003u << K2<I>::j, mg, D)
+      mma_16816(s, KD(w0, w0s, dk0, 0), KD(w1, w1s, dk1, 0), KD(w0, w0s, dk0, 1), KD(w1, w1s, dk1, 1), qs.ld(0, 4 * blk + 0));
+      mma_16816(s2, KD(w0, w0s, dk0, 2), KD(w1, w1s, dk1, 2), KD(w0, w0s, dk0, 3), KD(w1, w1s, dk1, 3), qs.ld(0, 4 * blk + 1));
+      mma_16816(s, KD(w0, w0s, dk0, 4), KD(w1, w1s, dk1, 4), KD(w0, w0s, dk0, 5), KD(w1, w1s, dk1, 5), qs.ld(0, 4 * blk + 2));
+      mma_16816(s2, KD(w0, w0s, dk0, 6), KD(w1, w1s, dk1, 6), KD(w0, w0s, dk0, 7), KD(w1, w1s, dk1, 7), qs.ld(0, 4 * blk + 3));
+#undef KD
     }
-    // zero points: lo_{tok, c} * (Qhi + Qlo)_c
-    const uint32_t lo0 = prmt(km0, km0, 0x1010), lo1 = prmt(km1, km1, 0x1010);
-    mma_16816(s, lo0, lo1, 0u, 0u, qaug, 0u);
+    mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
   } else {
     const __half2 sc0 = __float2half2_rn(sk0), sc1 = __float2half2_rn(sk1);
-    const __half2 lo0 = u32_as_h2(prmt(km0, km0, 0x1010)), lo1 = u32_as_h2(prmt(km1, km1, 0x1010));
+    const __half2 lo0 = u32_as_h2(prmt(kmm.x, kmm.x, 0x1010)), lo1 = u32_as_h2(prmt(kmm.y, kmm.y, 0x1010));
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
-      const int blk = ks >> 2, i0 = 2 * (ks & 3);
-      const uint32_t w0 = blk ? kw0.y : kw0.x, w1 = blk ? kw1.y : kw1.x;
-      mma_16816(s, deq_slow<2>(w0, i0, sc0, lo0), deq_slow<2>(w1, i0, sc1, lo1),
-                deq_slow<2>(w0, i0 + 1, sc0, lo0), deq_slow<2>(w1, i0 + 1, sc1, lo1), qb[ks][0], qb[ks][1]);
+      const int blk = ks >> 2, i0 = 2 * (ks & 3), i1 = i0 + 1;
+      const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
+      const int j0 = i0 <= 4 ? 2 * i0 : 2 * (i0 - 5), j1 = i1 <= 4 ? 2 * i1 : 2 * (i1 - 5);
+      const uint32_t x00 = i0 <= 4 ? w0 : w0 >> 10, x10 = i0 <= 4 ? w1 : w1 >> 10;
+      const uint32_t x01 = i1 <= 4 ? w0 : w0 >> 10, x11 = i1 <= 4 ? w1 : w1 >> 10;
+      mma_16816(s, edeq(x00, j0, 0x00030003u, sc0, lo0), edeq(x10, j0, 0x00030003u, sc1, lo1),
+                edeq(x01, j1, 0x00030003u, sc0, lo0), edeq(x11, j1, 0x00030003u, sc1, lo1), qs.ld(2, ks));
     }
   }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s[e] += s2[e];
   uint32_t bp0, bp1;
   softmax_tile(s, st, bp0, bp1);
-  const uint32_t c01lo = prmt(v0, v1, 0x5410), c01hi = prmt(v0, v1, 0x7632);
-  const uint32_t c23lo = prmt(v2, v3, 0x5410), c23hi = prmt(v2, v3, 0x7632);
-  if (!slow) {
+  const uint32_t c01lo = prmt(vv.x, vv.y, 0x5410), c01hi = prmt(vv.x, vv.y, 0x7632);
+  const uint32_t c23lo = prmt(vv.z, vv.w, 0x5410), c23hi = prmt(vv.z, vv.w, 0x7632);
+  if (!EXACT) {
     const DeqC d01 = make_deq(sv0, sv1), d23 = make_deq(sv2, sv3);
-#define PV2(I)                                                                                     \
-  mma_16816(st.acc[I], deq2<I>(c01lo, d01), deq2<I>(c01hi, d01), deq2<I>(c23lo, d23),            \
-            deq2<I>(c23hi, d23), bp0, bp1);
+    const uint32_t a8 = c01lo >> 8, b8 = c01hi >> 8, e8 = c23lo >> 8, f8 = c23hi >> 8;
+    // m-tile mt uses code mt of each 8-code half: j = 2 (mt & 3), from x (mt < 4) or x >> 8
+#define PV2(MT)                                                                                     \
+  {                                                                                                 \
+    constexpr uint32_t m_ = 0x00030003u << (2 * ((MT) & 3));                                       \
+    mma_16816(st.acc[MT], wdeq((MT) < 4 ? c01lo : a8, m_, mg, d01), wdeq((MT) < 4 ? c01hi : b8, m_, mg, d01), \
+              wdeq((MT) < 4 ? c23lo : e8, m_, mg, d23), wdeq((MT) < 4 ? c23hi : f8, m_, mg, d23), bp0, bp1); \
+  }
     PV2(0) PV2(1) PV2(2) PV2(3) PV2(4) PV2(5) PV2(6) PV2(7)
 #undef PV2
-    mma_16816(st.lacc, meta_lo_pair(vm0, vm1), 0u, meta_lo_pair(vm2, vm3), 0u, bp0, bp1);
+    lo_mma(st, prmt(vmm.x, vmm.y, 0x5410), prmt(vmm.z, vmm.w, 0x5410), bp0, bp1);
   } else {
     const __half2 sc01 = __floats2half2_rn(sv0, sv1), sc23 = __floats2half2_rn(sv2, sv3);
-    const __half2 lo01 = u32_as_h2(meta_lo_pair(vm0, vm1)), lo23 = u32_as_h2(meta_lo_pair(vm2, vm3));
+    const __half2 lo01 = u32_as_h2(prmt(vmm.x, vmm.y, 0x5410)), lo23 = u32_as_h2(prmt(vmm.z, vmm.w, 0x5410));
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
-      mma_16816(st.acc[mt], deq_slow<2>(c01lo, mt, sc01, lo01), deq_slow<2>(c01hi, mt, sc01, lo01),
-                deq_slow<2>(c23lo, mt, sc23, lo23), deq_slow<2>(c23hi, mt, sc23, lo23), bp0, bp1);
+    for (int mt = 0; mt < 8; ++mt) {
+      const int j = 2 * (mt & 3);
+      const uint32_t x0 = mt < 4 ? c01lo : c01lo >> 8, x1 = mt < 4 ? c01hi : c01hi >> 8;
+      const uint32_t x2 = mt < 4 ? c23lo : c23lo >> 8, x3 = mt < 4 ? c23hi : c23hi >> 8;
+      mma_16816(st.acc[mt], edeq(x0, j, 0x00030003u, sc01, lo01), edeq(x1, j, 0x00030003u, sc01, lo01),
+                edeq(x2, j, 0x00030003u, sc23, lo23), edeq(x3, j, 0x00030003u, sc23, lo23), bp0, bp1);
+    }
   }
 }
 
-// ---- INT4 tile ------------------------------------------------------------------
-__device__ __forceinline__ void tile_int4(const DecArgs& a, const uint32_t* kc, const uint32_t* km,
-                                          const uint32_t* vc, const uint32_t* vm,
-                                          const uint32_t (&qb)[8][2], uint32_t qaug, WarpState& st,
-                                          int g, int c) {
-  // K: tokens g, g+8; group c = words 4c .. 4c+3
-  const uint4 kw0 = *reinterpret_cast<const uint4*>(kc + g * 16 + 4 * c);
-  const uint4 kw1 = *reinterpret_cast<const uint4*>(kc + (g + 8) * 16 + 4 * c);
-  const uint32_t km0 = km[g * 4 + c], km1 = km[(g + 8) * 4 + c];
-  // V: tokens 2c, 2c+1, 2c+8, 2c+9; words 2g, 2g+1 (d 16g .. 16g+15)
-  const uint2 v0 = *reinterpret_cast<const uint2*>(vc + (2 * c) * 16 + 2 * g);
-  const uint2 v1 = *reinterpret_cast<const uint2*>(vc + (2 * c + 1) * 16 + 2 * g);
-  const uint2 v2 = *reinterpret_cast<const uint2*>(vc + (2 * c + 8) * 16 + 2 * g);
-  const uint2 v3 = *reinterpret_cast<const uint2*>(vc + (2 * c + 9) * 16 + 2 * g);
-  const uint32_t vm0 = vm[(2 * c) * 4 + (g >> 1)], vm1 = vm[(2 * c + 1) * 4 + (g >> 1)];
-  const uint32_t vm2 = vm[(2 * c + 8) * 4 + (g >> 1)], vm3 = vm[(2 * c + 9) * 4 + (g >> 1)];
+// ---- INT4 tile from a shared-memory stage ----------------------------------------------
+template <bool EXACT>
+__device__ __forceinline__ void tile_int4(uint32_t sl, const QS& qs, uint32_t mg, WarpState& st) {
+  const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);  // group c of tok g / tok g+8
+  const uint2 kmm = lds64(sl + 2048);
+  const uint4 va = lds128(sl + 1024), vb = lds128(sl + 1536);
+  const uint4 vmm = lds128(sl + 2560);
   constexpr float iq = 1.0f / 15.0f;
-  const float sk0 = meta_scale(km0, iq), sk1 = meta_scale(km1, iq);
-  const float sv0 = meta_scale(vm0, iq), sv1 = meta_scale(vm1, iq);
-  const float sv2 = meta_scale(vm2, iq), sv3 = meta_scale(vm3, iq);
-  const float smax = fmaxf(fmaxf(fmaxf(sk0, sk1), fmaxf(sv0, sv1)), fmaxf(sv2, sv3));
-  const bool slow = __any_sync(0xffffffffu, smax > 63.0f);
+  const float sk0 = meta_scale(kmm.x, iq), sk1 = meta_scale(kmm.y, iq);
+  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
+  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
 
-  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
   const uint32_t kwa[4] = {kw0.x, kw0.y, kw0.z, kw0.w}, kwb[4] = {kw1.x, kw1.y, kw1.z, kw1.w};
-  if (!slow) {
+  if (!EXACT) {
     const DeqC dk0 = make_deq(sk0, sk0), dk1 = make_deq(sk1, sk1);
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
       // pairs (d0, d0+8) = (word 2blk code i, word 2blk+1 code i)
       const uint32_t a_lo = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x5410), a_hi = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x7632);
       const uint32_t b_lo = prmt(kwb[2 * blk], kwb[2 * blk + 1], 0x5410), b_hi = prmt(kwb[2 * blk], kwb[2 * blk + 1], 0x7632);
-      mma_16816(s, deq4<0>(a_lo, dk0), deq4<0>(b_lo, dk1), deq4<1>(a_lo, dk0), deq4<1>(b_lo, dk1), qb[4 * blk + 0][0], qb[4 * blk + 0][1]);
-      mma_16816(s, deq4<2>(a_lo, dk0), deq4<2>(b_lo, dk1), deq4<3>(a_lo, dk0), deq4<3>(b_lo, dk1), qb[4 * blk + 1][0], qb[4 * blk + 1][1]);
-      mma_16816(s, deq4<0>(a_hi, dk0), deq4<0>(b_hi, dk1), deq4<1>(a_hi, dk0), deq4<1>(b_hi, dk1), qb[4 * blk + 2][0], qb[4 * blk + 2][1]);
-      mma_16816(s, deq4<2>(a_hi, dk0), deq4<2>(b_hi, dk1), deq4<3>(a_hi, dk0), deq4<3>(b_hi, dk1), qb[4 * blk + 3][0], qb[4 * blk + 3][1]);
+      const uint32_t a_lo8 = a_lo >> 8, a_hi8 = a_hi >> 8, b_lo8 = b_lo >> 8, b_hi8 = b_hi >> 8;
+#define KD(X, X8, D, I) wdeq(K4<I>::hi ? X8 : X, 0x000F000Fu << K4<I>::j, mg, D)
+      mma_16816(s, KD(a_lo, a_lo8, dk0, 0), KD(b_lo, b_lo8, dk1, 0), KD(a_lo, a_lo8, dk0, 1), KD(b_lo, b_lo8, dk1, 1), qs.ld(1, 4 * blk + 0));
+      mma_16816(s2, KD(a_lo, a_lo8, dk0, 2), KD(b_lo, b_lo8, dk1, 2), KD(a_lo, a_lo8, dk0, 3), KD(b_lo, b_lo8, dk1, 3), qs.ld(1, 4 * blk + 1));
+      mma_16816(s, KD(a_hi, a_hi8, dk0, 0), KD(b_hi, b_hi8, dk1, 0), KD(a_hi, a_hi8, dk0, 1), KD(b_hi, b_hi8, dk1, 1), qs.ld(1, 4 * blk + 2));
+      mma_16816(s2, KD(a_hi, a_hi8, dk0, 2), KD(b_hi, b_hi8, dk1, 2), KD(a_hi, a_hi8, dk0, 3), KD(b_hi, b_hi8, dk1, 3), qs.ld(1, 4 * blk + 3));
+#undef KD
     }
-    const uint32_t lo0 = prmt(km0, km0, 0x1010), lo1 = prmt(km1, km1, 0x1010);
-    mma_16816(s, lo0, lo1, 0u, 0u, qaug, 0u);
+    mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
   } else {
     const __half2 sc0 = __float2half2_rn(sk0), sc1 = __float2half2_rn(sk1);
-    const __half2 lo0 = u32_as_h2(prmt(km0, km0, 0x1010)), lo1 = u32_as_h2(prmt(km1, km1, 0x1010));
+    const __half2 lo0 = u32_as_h2(prmt(kmm.x, kmm.x, 0x1010)), lo1 = u32_as_h2(prmt(kmm.y, kmm.y, 0x1010));
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
       const uint32_t a_lo = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x5410), a_hi = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x7632);
@@ -261,89 +327,191 @@ __device__ __forceinline__ void tile_int4(const DecArgs& a, const uint32_t* kc, 
 #pragma unroll
       for (int q2 = 0; q2 < 4; ++q2) {
         const uint32_t ca = q2 < 2 ? a_lo : a_hi, cb = q2 < 2 ? b_lo : b_hi;
-        const int i = 2 * (q2 & 1);
-        mma_16816(s, deq_slow<4>(ca, i, sc0, lo0), deq_slow<4>(cb, i, sc1, lo1),
-                  deq_slow<4>(ca, i + 1, sc0, lo0), deq_slow<4>(cb, i + 1, sc1, lo1), qb[4 * blk + q2][0], qb[4 * blk + q2][1]);
+        const int i = 2 * (q2 & 1);  // pairs i, i+1 of the 4-pair word
+        const uint32_t xa0 = i < 2 ? ca : ca >> 8, xb0 = i < 2 ? cb : cb >> 8;
+        const uint32_t xa1 = (i + 1) < 2 ? ca : ca >> 8, xb1 = (i + 1) < 2 ? cb : cb >> 8;
+        mma_16816(s, edeq(xa0, 4 * (i & 1), 0x000F000Fu, sc0, lo0), edeq(xb0, 4 * (i & 1), 0x000F000Fu, sc1, lo1),
+                  edeq(xa1, 4 * ((i + 1) & 1), 0x000F000Fu, sc0, lo0), edeq(xb1, 4 * ((i + 1) & 1), 0x000F000Fu, sc1, lo1),
+                  qs.ld(2, 4 * blk + q2));
       }
     }
   }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s[e] += s2[e];
   uint32_t bp0, bp1;
   softmax_tile(s, st, bp0, bp1);
-  // V pairs (tok 2c, 2c+1) / (2c+8, 2c+9) for d = 16g + mt (word 2g) and 16g + 8 + mt (word 2g+1)
-  const uint32_t x01[4] = {prmt(v0.x, v1.x, 0x5410), prmt(v0.x, v1.x, 0x7632),
-                           prmt(v0.y, v1.y, 0x5410), prmt(v0.y, v1.y, 0x7632)};
-  const uint32_t x23[4] = {prmt(v2.x, v3.x, 0x5410), prmt(v2.x, v3.x, 0x7632),
-                           prmt(v2.y, v3.y, 0x5410), prmt(v2.y, v3.y, 0x7632)};
-  if (!slow) {
+  // V (tok 2c | 2c+1) and (2c+8 | 2c+9) for d = 16g + mt (word 2g) and 16g + 8 + mt (word 2g+1)
+  const uint32_t x01[4] = {prmt(va.x, va.z, 0x5410), prmt(va.x, va.z, 0x7632),
+                           prmt(va.y, va.w, 0x5410), prmt(va.y, va.w, 0x7632)};
+  const uint32_t x23[4] = {prmt(vb.x, vb.z, 0x5410), prmt(vb.x, vb.z, 0x7632),
+                           prmt(vb.y, vb.w, 0x5410), prmt(vb.y, vb.w, 0x7632)};
+  if (!EXACT) {
     const DeqC d01 = make_deq(sv0, sv1), d23 = make_deq(sv2, sv3);
-    // mt in 0..3 -> x[0] pairs mt; mt in 4..7 -> x[1] pairs mt-4; rows g+8 use x[2], x[3]
-#define PV4(MT)                                                                                    \
-  mma_16816(st.acc[MT], deq4<(MT) & 3>(x01[(MT) >> 2], d01), deq4<(MT) & 3>(x01[2 + ((MT) >> 2)], d01), \
-            deq4<(MT) & 3>(x23[(MT) >> 2], d23), deq4<(MT) & 3>(x23[2 + ((MT) >> 2)], d23), bp0, bp1);
+    // m-tile mt: code k = mt & 3 of x[mt >> 2] sits at bits 4k; move it to j = 2k (>> 2k)
+#define PV4(MT)                                                                                     \
+  {                                                                                                 \
+    constexpr int k_ = (MT) & 3, u_ = (MT) >> 2;                                                    \
+    constexpr uint32_t m_ = 0x000F000Fu << (2 * k_);                                               \
+    mma_16816(st.acc[MT], wdeq(x01[u_] >> (2 * k_), m_, mg, d01), wdeq(x01[2 + u_] >> (2 * k_), m_, mg, d01), \
+              wdeq(x23[u_] >> (2 * k_), m_, mg, d23), wdeq(x23[2 + u_] >> (2 * k_), m_, mg, d23), bp0, bp1); \
+  }
     PV4(0) PV4(1) PV4(2) PV4(3) PV4(4) PV4(5) PV4(6) PV4(7)
 #undef PV4
-    mma_16816(st.lacc, meta_lo_pair(vm0, vm1), 0u, meta_lo_pair(vm2, vm3), 0u, bp0, bp1);
+    lo_mma(st, prmt(vmm.x, vmm.y, 0x5410), prmt(vmm.z, vmm.w, 0x5410), bp0, bp1);
   } else {
     const __half2 sc01 = __floats2half2_rn(sv0, sv1), sc23 = __floats2half2_rn(sv2, sv3);
-    const __half2 lo01 = u32_as_h2(meta_lo_pair(vm0, vm1)), lo23 = u32_as_h2(meta_lo_pair(vm2, vm3));
+    const __half2 lo01 = u32_as_h2(prmt(vmm.x, vmm.y, 0x5410)), lo23 = u32_as_h2(prmt(vmm.z, vmm.w, 0x5410));
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
-      mma_16816(st.acc[mt], deq_slow<4>(x01[mt >> 2], mt & 3, sc01, lo01),
-                deq_slow<4>(x01[2 + (mt >> 2)], mt & 3, sc01, lo01),
-                deq_slow<4>(x23[mt >> 2], mt & 3, sc23, lo23),
-                deq_slow<4>(x23[2 + (mt >> 2)], mt & 3, sc23, lo23), bp0, bp1);
+    for (int mt = 0; mt < 8; ++mt) {
+      const int k = mt & 3, u = mt >> 2;
+      const int j = 4 * (k & 1);
+      const uint32_t sh = k < 2 ? 0 : 8;
+      mma_16816(st.acc[mt], edeq(x01[u] >> sh, j, 0x000F000Fu, sc01, lo01), edeq(x01[2 + u] >> sh, j, 0x000F000Fu, sc01, lo01),
+                edeq(x23[u] >> sh, j, 0x000F000Fu, sc23, lo23), edeq(x23[2 + u] >> sh, j, 0x000F000Fu, sc23, lo23), bp0, bp1);
+    }
   }
 }
 
-// ---- FP16 tile (FP16-tier chunks, tail, decode tokens) ----------------------------
+// ---- FP16 tile straight from global memory (FP16 chunks, tail, decode tokens) ------------
+template <bool EXACT>
 __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf, int valid,
-                                          const uint32_t (&qb)[8][2], WarpState& st, int g, int c) {
-  // K: tokens g, g+8, d 32c .. 32c+31 (16 words each)
-  uint32_t ka[16], kb[16];
-  {
-    const uint4* p0 = reinterpret_cast<const uint4*>(kf + g * kHeadDim + 32 * c);
-    const uint4* p1 = reinterpret_cast<const uint4*>(kf + (g + 8) * kHeadDim + 32 * c);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint4 x = p0[u], y = p1[u];
-      ka[4 * u] = x.x; ka[4 * u + 1] = x.y; ka[4 * u + 2] = x.z; ka[4 * u + 3] = x.w;
-      kb[4 * u] = y.x; kb[4 * u + 1] = y.y; kb[4 * u + 2] = y.z; kb[4 * u + 3] = y.w;
-    }
-  }
+                                          const QS& qs, WarpState& st, int g, int c) {
   float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-    // pair (d0, d0+8), d0 = 32c + 16blk + 2(ks&3): words 8blk + (ks&3) and 8blk + 4 + (ks&3)
-    const int wa = 8 * (ks >> 2) + (ks & 3), wb = wa + 4;
-    mma_16816(s, prmt(ka[wa], ka[wb], 0x5410), prmt(kb[wa], kb[wb], 0x5410),
-              prmt(ka[wa], ka[wb], 0x7632), prmt(kb[wa], kb[wb], 0x7632), qb[ks][0], qb[ks][1]);
+  for (int blk = 0; blk < 2; ++blk) {
+    // tokens g, g+8; d 32c + 16 blk .. +16 (8 words each)
+    const uint4* p0 = reinterpret_cast<const uint4*>(kf + g * kHeadDim + 32 * c + 16 * blk);
+    const uint4* p1 = reinterpret_cast<const uint4*>(kf + (g + 8) * kHeadDim + 32 * c + 16 * blk);
+    const uint4 x0 = __ldg(p0), x1 = __ldg(p0 + 1), y0 = __ldg(p1), y1 = __ldg(p1 + 1);
+    const uint32_t ka[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    const uint32_t kb[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      // pair (d0, d0+8), d0 = 16blk + 2kk: words kk and kk+4 of the block
+      mma_16816(s, prmt(ka[kk], ka[kk + 4], 0x5410), prmt(kb[kk], kb[kk + 4], 0x5410),
+                prmt(ka[kk], ka[kk + 4], 0x7632), prmt(kb[kk], kb[kk + 4], 0x7632), qs.ld(2, 4 * blk + kk));
+    }
   }
   if (g >= valid) { s[0] = -INFINITY; s[1] = -INFINITY; }
   if (g + 8 >= valid) { s[2] = -INFINITY; s[3] = -INFINITY; }
   uint32_t bp0, bp1;
   softmax_tile(s, st, bp0, bp1);
-  // V: tokens 2c, 2c+1, 2c+8, 2c+9, d 16g .. 16g+15 (8 words each)
-  uint32_t vw[4][8];
   const int toks[4] = {2 * c, 2 * c + 1, 2 * c + 8, 2 * c + 9};
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const uint4* p = reinterpret_cast<const uint4*>(vf + toks[t] * kHeadDim + 16 * g);
-    const uint4 x = p[0], y = p[1];
-    vw[t][0] = x.x; vw[t][1] = x.y; vw[t][2] = x.z; vw[t][3] = x.w;
-    vw[t][4] = y.x; vw[t][5] = y.y; vw[t][6] = y.z; vw[t][7] = y.w;
-  }
+  for (int half = 0; half < 2; ++half) {
+    uint32_t w[4][4];
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    const uint32_t sel = (mt & 1) ? 0x7632 : 0x5410;
-    const int w0 = mt >> 1, w1 = 4 + (mt >> 1);
-    mma_16816(st.acc[mt], prmt(vw[0][w0], vw[1][w0], sel), prmt(vw[0][w1], vw[1][w1], sel),
-              prmt(vw[2][w0], vw[3][w0], sel), prmt(vw[2][w1], vw[3][w1], sel), bp0, bp1);
+    for (int t = 0; t < 4; ++t) {
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(vf + toks[t] * kHeadDim + 16 * g) + half);
+      const uint2 b = __ldg(reinterpret_cast<const uint2*>(vf + toks[t] * kHeadDim + 16 * g + 8) + half);
+      w[t][0] = a.x; w[t][1] = a.y; w[t][2] = b.x; w[t][3] = b.y;
+    }
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      const int mt = 4 * half + mm;
+      const uint32_t sel = (mm & 1) ? 0x7632 : 0x5410;
+      const int w0 = mm >> 1, w1 = 2 + (mm >> 1);
+      uint32_t a0 = prmt(w[0][w0], w[1][w0], sel), a1 = prmt(w[0][w1], w[1][w1], sel);
+      uint32_t a2 = prmt(w[2][w0], w[3][w0], sel), a3 = prmt(w[2][w1], w[3][w1], sel);
+      if (!EXACT) {  // match the quantized tiles' m-tile weight 2^(2(mt&3) - 6)
+        const __half2 wt = __float2half2_rn((float)(1 << (2 * (mt & 3))) * (1.0f / 64.0f));
+        a0 = h2_as_u32(__hmul2(u32_as_h2(a0), wt)); a1 = h2_as_u32(__hmul2(u32_as_h2(a1), wt));
+        a2 = h2_as_u32(__hmul2(u32_as_h2(a2), wt)); a3 = h2_as_u32(__hmul2(u32_as_h2(a3), wt));
+      }
+      mma_16816(st.acc[mt], a0, a1, a2, a3, bp0, bp1);
+    }
+  }
+}
+
+struct TileSrc {
+  const char *k2, *k2m, *v2, *v2m, *k4, *k4m, *v4, *v4m;
+};
+
+// per-lane source byte offsets inside one 16-token tile (INT2 rows; INT4 code rows are 2x)
+struct LaneSrc {
+  uint32_t k, km, v, vm;
+};
+
+// Warp-wide: stage one quantized tile into this lane's slots with cp.async.  Each lane
+// fetches exactly the bytes its MMA fragments need.  Commits a (possibly empty) group.
+__device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const TileSrc& s,
+                                           const LaneSrc& o, uint32_t sl) {
+  if (t < t_q_end) {
+    if (t < n2t) {
+      const char* kc = s.k2 + (int64_t)t * (kTile * 32) + o.k;
+      const char* km = s.k2m + (int64_t)t * (kTile * 16) + o.km;
+      const char* vc = s.v2 + (int64_t)t * (kTile * 32) + o.v;
+      const char* vm = s.v2m + (int64_t)t * (kTile * 16) + o.vm;
+      cp_async8(sl, kc);
+      cp_async8(sl + 8, kc + 8 * 32);
+      cp_async4(sl + 512, vc);
+      cp_async4(sl + 516, vc + 32);
+      cp_async4(sl + 520, vc + 8 * 32);
+      cp_async4(sl + 524, vc + 9 * 32);
+      cp_async4(sl + 1024, km);
+      cp_async4(sl + 1028, km + 8 * 16);
+      cp_async4(sl + 1536, vm);
+      cp_async4(sl + 1540, vm + 16);
+      cp_async4(sl + 1544, vm + 8 * 16);
+      cp_async4(sl + 1548, vm + 9 * 16);
+    } else {
+      const int64_t t4 = t - n2t;
+      const char* kc = s.k4 + t4 * (kTile * 64) + 2 * o.k;
+      const char* km = s.k4m + t4 * (kTile * 16) + o.km;
+      const char* vc = s.v4 + t4 * (kTile * 64) + 2 * o.v;
+      const char* vm = s.v4m + t4 * (kTile * 16) + o.vm;
+      cp_async16(sl, kc);
+      cp_async16(sl + 512, kc + 8 * 64);
+      cp_async8(sl + 1024, vc);
+      cp_async8(sl + 1032, vc + 64);
+      cp_async8(sl + 1536, vc + 8 * 64);
+      cp_async8(sl + 1544, vc + 9 * 64);
+      cp_async4(sl + 2048, km);
+      cp_async4(sl + 2052, km + 8 * 16);
+      cp_async4(sl + 2560, vm);
+      cp_async4(sl + 2564, vm + 16);
+      cp_async4(sl + 2568, vm + 8 * 16);
+      cp_async4(sl + 2572, vm + 9 * 16);
+    }
+  }
+  cp_commit();
+}
+
+// The tile loops of one warp: quantized tiles through the cp.async ring, then FP16 tiles.
+template <bool EXACT>
+__device__ __forceinline__ void run_tiles(int t_begin, int t_end, int n2t, int n4t, int len_fp,
+                                          const TileSrc& src, const LaneSrc& lo, const uint16_t* kf,
+                                          const uint16_t* vf, uint32_t ring_l, const QS& qs,
+                                          uint32_t mg, WarpState& st, int warp, int g, int c) {
+  const int t_q_end = min(t_end, n2t + n4t);
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s)
+    issue_tile(t_begin + warp + kDecWarps * s, t_q_end, n2t, src, lo, ring_l + s * kStageBytes);
+  uint32_t use = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
+  const uint32_t ring_end = ring_l + kStages * kStageBytes;
+  int t = t_begin + warp;
+  for (; t < t_q_end; t += kDecWarps) {
+    issue_tile(t + kDecWarps * (kStages - 1), t_q_end, n2t, src, lo, put);
+    put = put + kStageBytes == ring_end ? ring_l : put + kStageBytes;
+    cp_wait<kStages - 1>();
+    __syncwarp();
+    if (t < n2t) tile_int2<EXACT>(use, qs, mg, st);
+    else tile_int4<EXACT>(use, qs, mg, st);
+    use = use + kStageBytes == ring_end ? ring_l : use + kStageBytes;
+    __syncwarp();
+  }
+  cp_wait<0>();
+  for (; t < t_end; t += kDecWarps) {
+    const int r = (t - n2t - n4t) * kTile;
+    tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
   }
 }
 
 __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs a) {
-  __shared__ float s_acc[kDecWarps][8][kHeadDim];
+  __shared__ __align__(128) unsigned char s_ring[kDecWarps][kStages][kStageBytes];
   __shared__ float s_ml[kDecWarps][8][2];
+  __shared__ __align__(16) uint2 s_q[3][9][32];
+  __shared__ int s_last, s_wide_q;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   const int split = blockIdx.x, h = blockIdx.y;
@@ -364,9 +532,28 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   const int t_begin = tile_at(tot * split / a.splits);
   const int t_end = tile_at(tot * (split + 1) / a.splits);
 
-  // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m)
-  uint32_t qb[8][2], qaug;
-  {
+  const int64_t unit = (int64_t)l * a.H + h;
+  TileSrc src;
+  src.k2 = reinterpret_cast<const char*>(a.K.codes2 + (unit * a.K.rows2 + sq.off2) * 8);
+  src.k2m = reinterpret_cast<const char*>(a.K.meta2 + (unit * a.K.rows2 + sq.off2) * 4);
+  src.v2 = reinterpret_cast<const char*>(a.V.codes2 + (unit * a.V.rows2 + sq.off2) * 8);
+  src.v2m = reinterpret_cast<const char*>(a.V.meta2 + (unit * a.V.rows2 + sq.off2) * 4);
+  src.k4 = reinterpret_cast<const char*>(a.K.codes4 + (unit * a.K.rows4 + sq.off4) * 16);
+  src.k4m = reinterpret_cast<const char*>(a.K.meta4 + (unit * a.K.rows4 + sq.off4) * 4);
+  src.v4 = reinterpret_cast<const char*>(a.V.codes4 + (unit * a.V.rows4 + sq.off4) * 16);
+  src.v4m = reinterpret_cast<const char*>(a.V.meta4 + (unit * a.V.rows4 + sq.off4) * 4);
+  const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + sq.off_fp) * kHeadDim;
+  const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + sq.off_fp) * kHeadDim;
+  LaneSrc lo;
+  lo.k = g * 32 + 8 * c;          // K row g, bytes of group c (INT2)
+  lo.km = g * 16 + 4 * c;         // K meta row g, group c
+  lo.v = 2 * c * 32 + 4 * g;      // V row 2c, word g (INT2)
+  lo.vm = 2 * c * 16 + 4 * (g >> 1);
+  const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
+
+  // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m); warp 0 writes the
+  // CTA's three sets to shared memory.
+  if (warp == 0) {
     float qv[32];
     const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
     if (g < a.m) {
@@ -385,56 +572,62 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
 #pragma unroll
       for (int e = 0; e < 32; ++e) qv[e] = 0.f;
     }
-    float qsum = 0.f;
+    float qsum = 0.f, qmaxabs = 0.f;
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       qv[e] = __half2float(__float2half_rn(qv[e]));  // exactly the fp16 operand the MMA sees
       qsum += qv[e];
+      qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
     }
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
-      const int d0 = 16 * (ks >> 2) + 2 * (ks & 3);  // lane-local index within group c
-      qb[ks][0] = h2_as_u32(__floats2half2_rn(qv[d0], qv[d0 + 8]));
-      qb[ks][1] = h2_as_u32(__floats2half2_rn(qv[d0 + 1], qv[d0 + 9]));
+      const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
+      const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
+      // INT2 slot weight 2^(j-6): j = 2i (i <= 4) or 2(i-5); INT4: j = 4(i & 1)
+      const float w20 = exp2f((float)(6 - (i0 <= 4 ? 2 * i0 : 2 * (i0 - 5))));
+      const float w21 = exp2f((float)(6 - (i1 <= 4 ? 2 * i1 : 2 * (i1 - 5))));
+      const float w40 = exp2f((float)(6 - 4 * (i0 & 1))), w41 = exp2f((float)(6 - 4 * (i1 & 1)));
+      s_q[0][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * w20, qv[d0 + 8] * w20)),
+                                    h2_as_u32(__floats2half2_rn(qv[d0 + 1] * w21, qv[d0 + 9] * w21)));
+      s_q[1][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * w40, qv[d0 + 8] * w40)),
+                                    h2_as_u32(__floats2half2_rn(qv[d0 + 1] * w41, qv[d0 + 9] * w41)));
+      s_q[2][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0], qv[d0 + 8])),
+                                    h2_as_u32(__floats2half2_rn(qv[d0 + 1], qv[d0 + 9])));
     }
     const __half qhi = __float2half_rn(qsum);
     const __half qlo = __float2half_rn(qsum - __half2float(qhi));
-    qaug = h2_as_u32(__halves2half2(qhi, qlo));
+    s_q[0][8][lane] = make_uint2(h2_as_u32(__halves2half2(qhi, qlo)), 0u);
+    const bool wide = __any_sync(0xffffffffu, qmaxabs > kWideQ);
+    if (lane == 0) s_wide_q = wide;
   }
+  __syncthreads();
+  QS qs;
+  qs.base = (uint32_t)__cvta_generic_to_shared(&s_q[0][0][0]) + 8 * lane;
+  const int64_t fidx = unit * a.B + b;  // span flags are [L][H][B]
+  const bool exact = s_wide_q || (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
+                     (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
+  const uint32_t mg = kMagic16 | a.zero;
 
   WarpState st;
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) st.acc[mt][0] = st.acc[mt][1] = st.acc[mt][2] = st.acc[mt][3] = 0.f;
-  st.lacc[0] = st.lacc[1] = st.lacc[2] = st.lacc[3] = 0.f;
+  st.lacc[0] = st.lacc[1] = 0.f;
   st.mrun[0] = st.mrun[1] = -INFINITY;
   st.lsum[0] = st.lsum[1] = 0.f;
 
-  const int64_t unit = (int64_t)l * a.H + h;
-  const uint32_t* k2 = a.K.codes2 + (unit * a.K.rows2 + sq.off2) * 8;
-  const uint32_t* k2m = a.K.meta2 + (unit * a.K.rows2 + sq.off2) * 4;
-  const uint32_t* v2 = a.V.codes2 + (unit * a.V.rows2 + sq.off2) * 8;
-  const uint32_t* v2m = a.V.meta2 + (unit * a.V.rows2 + sq.off2) * 4;
-  const uint32_t* k4 = a.K.codes4 + (unit * a.K.rows4 + sq.off4) * 16;
-  const uint32_t* k4m = a.K.meta4 + (unit * a.K.rows4 + sq.off4) * 4;
-  const uint32_t* v4 = a.V.codes4 + (unit * a.V.rows4 + sq.off4) * 16;
-  const uint32_t* v4m = a.V.meta4 + (unit * a.V.rows4 + sq.off4) * 4;
-  const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + sq.off_fp) * kHeadDim;
-  const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + sq.off_fp) * kHeadDim;
-
-  for (int t = t_begin + warp; t < t_end; t += kDecWarps) {
-    if (t < n2t) {
-      const int r = t * kTile;
-      tile_int2(a, k2 + r * 8, k2m + r * 4, v2 + r * 8, v2m + r * 4, qb, qaug, st, g, c);
-    } else if (t < n2t + n4t) {
-      const int r = (t - n2t) * kTile;
-      tile_int4(a, k4 + r * 16, k4m + r * 4, v4 + r * 16, v4m + r * 4, qb, qaug, st, g, c);
-    } else {
-      const int r = (t - n2t - n4t) * kTile;
-      tile_fp16(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, sq.len_fp - r, qb, st, g, c);
+  if (exact) {
+    run_tiles<true>(t_begin, t_end, n2t, n4t, sq.len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+  } else {
+    run_tiles<false>(t_begin, t_end, n2t, n4t, sq.len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    // undo the V m-tile weights 2^(2(mt&3) - 6)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const float f = (float)(64 >> (2 * (mt & 3)));
+      st.acc[mt][0] *= f; st.acc[mt][1] *= f; st.acc[mt][2] *= f; st.acc[mt][3] *= f;
     }
   }
 
-  // finish the warp: fold zero-point term, reduce row sums over the 8 row-groups
+  // finish the warp: fold the zero-point term, reduce row sums over the 8 row-groups
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
     st.acc[mt][0] += st.lacc[0]; st.acc[mt][1] += st.lacc[1];
@@ -445,6 +638,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
     st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
   }
+  __syncthreads();  // ring -> merge buffer reuse
+  float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0][0]);
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
     s_acc[warp][2 * c][16 * g + mt] = st.acc[mt][0];
@@ -460,57 +655,68 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   // merge the 4 warps: thread -> d
   const int d = threadIdx.x;
   const int hq0 = h * a.m;
-  for (int i = 0; i < a.m; ++i) {
+  const int Hq = a.H * a.m;
+  for (int qi = 0; qi < a.m; ++qi) {
     float ms = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) ms = fmaxf(ms, s_ml[w][i][0]);
+    for (int w = 0; w < kDecWarps; ++w) ms = fmaxf(ms, s_ml[w][qi][0]);
     float acc = 0.f, lsum = 0.f;
 #pragma unroll
     for (int w = 0; w < kDecWarps; ++w) {
-      const float mw = s_ml[w][i][0];
+      const float mw = s_ml[w][qi][0];
       const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-      acc += f * s_acc[w][i][d];
-      lsum += f * s_ml[w][i][1];
+      acc += f * s_acc[w][qi][d];
+      lsum += f * s_ml[w][qi][1];
     }
-    const int64_t row = ((int64_t)l * a.B + b) * (a.H * a.m) + hq0 + i;
-    if (a.splits == 1 && a.partial_out == nullptr) {
-      a.out[l * a.o_sl + b * a.o_sb + (int64_t)(hq0 + i) * kHeadDim + d] = __half_as_ushort(__float2half_rn(acc / lsum));
+    const int64_t row = ((int64_t)l * a.B + b) * Hq + hq0 + qi;
+    if (a.splits == 1) {
+      if (a.partial_out) {
+        float* dst = a.partial_out + row * kPartStride;
+        dst[d] = acc;
+        if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+      } else {
+        a.out[l * a.o_sl + b * a.o_sb + (int64_t)(hq0 + qi) * kHeadDim + d] =
+            __half_as_ushort(__float2half_rn(acc / lsum));
+      }
     } else {
-      float* dst = a.splits == 1 ? a.partial_out + row * kPartStride
-                                 : a.ws + (row * a.splits + split) * kPartStride;
+      float* dst = a.ws + (row * a.splits + split) * kPartStride;
       dst[d] = acc;
       if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
     }
   }
-}
-
-// Merge split partials: [rows][splits][130] -> out fp16 (or a [rows][130] partial for the
-// cross-rank exchange when partial_out is set).
-__global__ void merge_splits_kernel(const float* __restrict__ ws, int splits, int64_t rows,
-                                    int B, int Hq, uint16_t* __restrict__ out, int64_t o_sl,
-                                    int64_t o_sb, float* __restrict__ partial_out) {
-  const int64_t row = blockIdx.x;
-  const int d = threadIdx.x;
-  const float* p = ws + row * splits * kPartStride;
-  float ms = -INFINITY;
-  for (int s = 0; s < splits; ++s) ms = fmaxf(ms, p[s * kPartStride + kHeadDim]);
-  float acc = 0.f, lsum = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float mw = p[s * kPartStride + kHeadDim];
-    const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-    acc += f * p[s * kPartStride + d];
-    lsum += f * p[s * kPartStride + kHeadDim + 1];
+  if (a.splits == 1) return;
+  // split-KV: the last CTA of this unit to arrive merges all partials (in-launch, no 2nd kernel)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(a.counters + ((int64_t)l * a.B + b) * a.H + h, 1u);
+    s_last = prev == (uint32_t)(a.splits - 1);
   }
-  if (partial_out) {
-    float* dst = partial_out + row * kPartStride;
-    dst[d] = acc;
-    if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
-  } else {
-    const int hq = (int)(row % Hq);
-    const int b = (int)((row / Hq) % B);
-    const int64_t l = row / ((int64_t)Hq * B);
-    out[l * o_sl + b * o_sb + (int64_t)hq * kHeadDim + d] = __half_as_ushort(__float2half_rn(acc / lsum));
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int qi = 0; qi < a.m; ++qi) {
+    const int64_t row = ((int64_t)l * a.B + b) * Hq + hq0 + qi;
+    const float* p = a.ws + row * a.splits * kPartStride;
+    float ms = -INFINITY;
+    for (int s = 0; s < a.splits; ++s) ms = fmaxf(ms, __ldcg(p + s * kPartStride + kHeadDim));
+    float acc = 0.f, lsum = 0.f;
+    for (int s = 0; s < a.splits; ++s) {
+      const float mw = __ldcg(p + s * kPartStride + kHeadDim);
+      const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+      acc += f * __ldcg(p + s * kPartStride + d);
+      lsum += f * __ldcg(p + s * kPartStride + kHeadDim + 1);
+    }
+    if (a.partial_out) {
+      float* dst = a.partial_out + row * kPartStride;
+      dst[d] = acc;
+      if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+    } else {
+      a.out[l * a.o_sl + b * a.o_sb + (int64_t)(hq0 + qi) * kHeadDim + d] =
+          __half_as_ushort(__float2half_rn(acc / lsum));
+    }
   }
+  if (threadIdx.x == 0) a.counters[((int64_t)l * a.B + b) * a.H + h] = 0u;  // ready for the next launch
 }
 
 // Cross-rank merge of gathered partials [P][rows][130] -> out fp16 [rows][128].
@@ -538,8 +744,10 @@ extern "C" {
 
 int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                                    int32_t splits) {
-  if (splits <= 1) return 0;
-  return (int64_t)layers * batch * kv_heads * m * splits * kPartStride * (int64_t)sizeof(float);
+  const int64_t units = (int64_t)layers * batch * kv_heads;
+  const int64_t counters = cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256;
+  if (splits <= 1) return counters;
+  return counters + units * m * splits * kPartStride * (int64_t)sizeof(float);
 }
 
 int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
@@ -559,19 +767,27 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
   a.K = k_arena; a.V = v_arena; a.seq = seq;
   a.L = layers; a.B = batch; a.H = kv_heads; a.m = m; a.splits = splits;
   a.scale_log2 = scale * 1.4426950408889634f;
-  a.ws = reinterpret_cast<float*>(workspace);
+  const int64_t units = (int64_t)layers * batch * kv_heads;
+  a.counters = reinterpret_cast<uint32_t*>(workspace);
+  a.ws = workspace ? reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                              cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256)
+                   : nullptr;
   a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
   a.partial_out = partial_out;
+  a.zero = 0u;
   dim3 grid((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * batch));
   decode_kernel<<<grid, kDecWarps * 32, 0, as_stream(stream)>>>(a);
   CKV_LAUNCH_CHECK();
-  if (splits > 1) {
-    const int64_t rows = (int64_t)layers * batch * kv_heads * m;
-    merge_splits_kernel<<<(unsigned)rows, kHeadDim, 0, as_stream(stream)>>>(
-        a.ws, splits, rows, batch, kv_heads * m, out, o_s_layer, o_s_batch, partial_out);
-    CKV_LAUNCH_CHECK();
-  }
   return CKV_OK;
+}
+
+int32_t ckv_decode_ctas_per_sm(void) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel, kDecWarps * 32, 0) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -1;
+  }
+  return n;
 }
 
 int32_t ckv_lse_merge(const float* partials, int32_t n_parts, int64_t rows, uint16_t* out,

@@ -101,6 +101,7 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       continue;
     }
     const float qmax = tier == 0 ? 3.0f : 15.0f;
+    bool wide = false;
 #pragma unroll 2
     for (int rr = 0; rr < 16; ++rr) {
       const int r = 2 * rr + sub;
@@ -129,6 +130,8 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
         for (int e = 0; e < 8; ++e)
           packed |= exact_code(f[e], lo, hi, qinv, qmax) << (e * (tier == 0 ? 2 : 4));
       }
+      // decode's weighted fp16 dequant needs 16 * scale (and 12 * scale) in range: flag wider
+      wide |= (hi - lo) * (tier == 0 ? (1.0f / 3.0f) : (1.0f / 15.0f)) > 4000.0f;
       if (tier == 0) reinterpret_cast<uint16_t*>(s_codes[warp])[r * 16 + j] = (uint16_t)packed;
       else s_codes[warp][r * 16 + j] = packed;
       if ((j & 3) == 0) s_meta[warp][r * 4 + (j >> 2)] = h2_as_u32(__floats2half2_rn(lo, hi));
@@ -143,6 +146,8 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
     for (int i = lane; i < n16; i += 32)
       reinterpret_cast<uint4*>(codes)[i] = reinterpret_cast<const uint4*>(s_codes[warp])[i];
     reinterpret_cast<uint4*>(meta)[lane] = reinterpret_cast<const uint4*>(s_meta[warp])[lane];
+    if (__any_sync(0xffffffffu, wide) && lane == 0 && A.span_flags)
+      atomicOr(A.span_flags + unit * B + b, tier == 0 ? 1u : 2u);
     __syncwarp();
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE);

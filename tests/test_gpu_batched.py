@@ -1,0 +1,184 @@
+"""GPU: the batched fp16 hot path — fused reorder/quantize/pack (bit-exact codes, metadata,
+permutation) and mixed-precision decode attention (1e-2 abs / 1e-2 rel of the reference's
+f64 result on the same fp16 inputs), edge cases, split-KV shards, and full-size properties."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ckv_oracle as O
+from tests.conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+from paper_2503_23294_b200 import batched, distributed, retrieval  # noqa: E402
+
+TOL_ABS = 1e-2
+TOL_REL = 1e-2
+
+
+def _search_from_tiers(tiers):
+    tiers = np.asarray(tiers, np.float64)
+    return retrieval.assign_tiers_batched(tiers, np.tile([[0.5, 1.5]], (tiers.shape[0], 1)))
+
+
+def _check_unit(cache, l, b, h, k, v, tiers_b, q_rows, out_rows, ctx=None):
+    T = k.shape[2] if ctx is None else ctx
+    oc = O.build_cache(k[l, b, :T, h].astype(np.float64), v[l, b, :T, h].astype(np.float64), tiers_b, 32, 32)
+    ex = cache.export_unit(l, b, h)
+    for name in ("k_q2", "v_q2", "k_q4", "v_q4"):
+        a, w = getattr(ex, name), getattr(oc, name)
+        assert np.array_equal(a.packed, w.packed), name
+        assert np.array_equal(a.scales.view(np.uint64), w.scales.view(np.uint64)), name
+        assert np.array_equal(a.zero_points.view(np.uint64), w.zero_points.view(np.uint64)), name
+    assert np.array_equal(ex.k_fp[:oc.len_fp], oc.k_fp)
+    ref = O.mixed_decode_attention(q_rows.astype(np.float64), oc)
+    err = np.max(np.abs(out_rows.astype(np.float64) - ref))
+    scale = max(np.max(np.abs(ref)), 1e-30)
+    assert err <= TOL_ABS * max(1.0, scale) and err / scale <= TOL_REL, (err, scale)
+    return err / scale
+
+
+def test_batched_golden_case():
+    g = load_golden("batched.npz")
+    L, B, H, m, T = (int(x) for x in g["dims"])
+    k = torch.from_numpy(g["k"]).cuda()
+    v = torch.from_numpy(g["v"]).cuda()
+    q = torch.from_numpy(g["q"]).cuda()
+    cache = batched.build_cache_batched(k, v, _search_from_tiers(g["tiers"]))
+    out = cache.decode(q).float().cpu().numpy()
+    for l in range(L):
+        for b in range(B):
+            for h in range(H):
+                key = f"{l}_{b}_{h}"
+                ex = cache.export_unit(l, b, h)
+                for name in ("k_q2", "v_q2", "k_q4", "v_q4"):
+                    blk = getattr(ex, name)
+                    assert np.array_equal(blk.packed, g[f"{name}_packed_{key}"])
+                    assert np.array_equal(blk.scales.view(np.uint64), g[f"{name}_scales_{key}"].view(np.uint64))
+                    assert np.array_equal(blk.zero_points.view(np.uint64), g[f"{name}_zps_{key}"].view(np.uint64))
+                ref = g[f"out_{key}"]
+                got = out[l, b, h * m:(h + 1) * m]
+                err = np.max(np.abs(got - ref))
+                assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL
+
+
+@pytest.mark.parametrize("m", [1, 4, 8])
+@pytest.mark.parametrize("kind", ["mix", "int2", "int4", "fp16"])
+def test_decode_tiers_and_gqa(m, kind):
+    rng = np.random.default_rng(hash((m, kind)) % 2**32)
+    L, B, H, D, N, tail = 2, 3, 2, 128, 20, 9
+    T = N * 32 + tail
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    q = (rng.normal(size=(L, B, H * m, D)) * 2).astype(np.float16)
+    if kind == "mix":
+        tiers = rng.choice([0, 0, 1, 2], size=(B, N)).astype(np.uint8)
+    else:
+        tiers = np.full((B, N), {"int2": 0, "int4": 1, "fp16": 2}[kind], np.uint8)
+    kd, vd, qd = (torch.from_numpy(x).cuda() for x in (k, v, q))
+    cache = batched.build_cache_batched(kd, vd, _search_from_tiers(tiers))
+    outs = [cache.decode(qd, splits=s).float().cpu().numpy() for s in (1, 2, 5)]
+    for o in outs[1:]:
+        assert np.max(np.abs(o - outs[0])) < 2e-3  # split-KV merge is exact up to fp32 order
+    for l in range(L):
+        for b in range(B):
+            for h in range(H):
+                _check_unit(cache, l, b, h, k, v, tiers[b], q[l, b, h * m:(h + 1) * m], outs[0][l, b, h * m:(h + 1) * m])
+
+
+def test_large_values_take_the_exact_slow_path():
+    rng = np.random.default_rng(9)
+    L, B, H, D, N = 1, 2, 1, 128, 8
+    T = N * 32
+    k = (rng.normal(size=(L, B, T, H, D)) * 2000).astype(np.float16)   # spans >> 192 -> slow path
+    v = (rng.uniform(-60000, 60000, size=(L, B, T, H, D))).astype(np.float16)
+    q = (rng.normal(size=(L, B, 4 * H, D)) * 1e-3).astype(np.float16)
+    tiers = np.array([[0, 1, 0, 2, 0, 1, 0, 0], [1, 1, 0, 0, 0, 0, 2, 2]], np.uint8)
+    cache = batched.build_cache_batched(*(torch.from_numpy(x).cuda() for x in (k, v)), _search_from_tiers(tiers))
+    out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for b in range(B):
+        _check_unit(cache, 0, b, 0, k, v, tiers[b], q[0, b, :4], out[0, b, :4])
+
+
+def test_nonfinite_input_rejected():
+    k = torch.zeros((1, 1, 64, 1, 128), dtype=torch.float16, device="cuda")
+    v = torch.zeros_like(k)
+    k[0, 0, 3, 0, 7] = float("inf")
+    with pytest.raises(ValueError):
+        batched.build_cache_batched(k, v, _search_from_tiers([[0, 1]]))
+
+
+def test_ragged_contexts_and_decode_appends():
+    rng = np.random.default_rng(12)
+    L, B, H, m, D = 2, 3, 2, 4, 128
+    ctx = np.array([5 * 32 + 3, 12 * 32, 2 * 32 + 31])
+    Tmax = int(ctx.max())
+    k = rng.normal(size=(L, B, Tmax, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, Tmax, H, D)).astype(np.float16)
+    N = ctx // 32
+    tiers = np.zeros((B, int(N.max())), np.uint8)
+    for b in range(B):
+        tiers[b, :N[b]] = rng.choice([0, 1, 2], size=N[b])
+    s = retrieval.assign_tiers_batched(tiers.astype(np.float64), np.tile([[0.5, 1.5]], (B, 1)), seq_chunks=N)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), s,
+                                        context_lens=ctx, decode_capacity=20)
+    kh, vh = k.copy(), v.copy()
+    appended_k, appended_v = [], []
+    for step in range(17):
+        kn = rng.normal(size=(L, B, H, D)).astype(np.float16)
+        vn = rng.normal(size=(L, B, H, D)).astype(np.float16)
+        cache.append(torch.from_numpy(kn).cuda(), torch.from_numpy(vn).cuda())
+        appended_k.append(kn)
+        appended_v.append(vn)
+    q = (rng.normal(size=(L, B, H * m, D))).astype(np.float16)
+    out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
+    AK, AV = np.stack(appended_k, 2), np.stack(appended_v, 2)  # [L, B, steps, H, D]
+    for l in range(L):
+        for b in range(B):
+            for h in range(H):
+                oc = O.build_cache(kh[l, b, :ctx[b], h].astype(np.float64), vh[l, b, :ctx[b], h].astype(np.float64),
+                                   tiers[b, :N[b]], 32, 32)
+                for t in range(AK.shape[2]):
+                    oc.append(AK[l, b, t, h], AV[l, b, t, h])
+                ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+                err = np.max(np.abs(out[l, b, h * m:(h + 1) * m] - ref))
+                assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL
+    with pytest.raises(ValueError):  # capacity = round_up(len_fp + 20, 16) rows per sequence
+        for _ in range(64):
+            cache.append(torch.from_numpy(kn).cuda(), torch.from_numpy(vn).cuda())
+
+
+def test_sequence_split_kv_shards_merge_to_full_decode():
+    rng = np.random.default_rng(21)
+    L, B, H, m, D, N, tail = 2, 2, 2, 4, 128, 37, 11
+    T = N * 32 + tail
+    k = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    q = torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16)).cuda()
+    s = _search_from_tiers(rng.choice([0, 0, 0, 1, 2], size=(B, N)).astype(np.uint8))
+    full = batched.build_cache_batched(k, v, s).decode(q).float()
+    for world in (2, 3, 8):
+        parts = [distributed.build_sequence_shard(k, v, s, world, r).decode_partial(q) for r in range(world)]
+        merged = batched.lse_merge(torch.stack(parts)).view(q.shape).float()
+        assert torch.max(torch.abs(merged - full)).item() < 2e-3
+
+
+def test_full_size_unit_properties_32k():
+    """cfg2-sized units (32K context, reference tier maps): bit-exact codes/metadata for sampled
+    units and decode within tolerance of the reference's f64 result."""
+    import bench
+    rng = np.random.default_rng(5)
+    L, B, H, m, D, T = 1, 2, 8, 4, 128, 32768
+    wls = [bench.load_workload(T, s) for s in range(B)]
+    s = retrieval.search_batched(np.stack([w["emb"] for w in wls]), np.stack([w["norm"] for w in wls]),
+                                 np.stack([w["q"] for w in wls]), np.array([w["qnorm"] for w in wls]))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    k = torch.randn((L, B, T, H, D), generator=g, device="cuda", dtype=torch.float16)
+    v = torch.randn((L, B, T, H, D), generator=g, device="cuda", dtype=torch.float16)
+    q = torch.randn((L, B, H * m, D), generator=g, device="cuda", dtype=torch.float16)
+    cache = batched.build_cache_batched(k, v, s)
+    out = cache.decode(q).float().cpu().numpy()
+    kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
+    for b, h in ((0, 0), (1, 5)):
+        _check_unit(cache, 0, b, h, kh, vh, wls[b]["tiers"], qh[0, b, h * m:(h + 1) * m], out[0, b, h * m:(h + 1) * m])
