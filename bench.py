@@ -314,8 +314,8 @@ def main():
     step_bytes = cache.algorithmic_bytes(m)
 
     def step():
-        for l in range(L):
-            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l)
+        for l in range(L):  # per-layer launches; layer l+1 overlaps its K/V prefetch with layer l
+            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -358,7 +358,7 @@ def main():
     for _ in range(3):
         qd.copy_(qh, non_blocking=True)
         for l in range(L):
-            cache.decode(qd[l:l + 1], splits=splits, out=out[l:l + 1], layer=l)
+            cache.decode(qd[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
         oh.copy_(out, non_blocking=True)
     torch.cuda.synchronize()
     barrier()
@@ -367,7 +367,7 @@ def main():
     for _ in range(args.steps):
         qd.copy_(qh, non_blocking=True)
         for l in range(L):
-            cache.decode(qd[l:l + 1], splits=splits, out=out[l:l + 1], layer=l)
+            cache.decode(qd[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
         oh.copy_(out, non_blocking=True)
     e5.record()
     torch.cuda.synchronize()
@@ -388,7 +388,7 @@ def main():
         peak, peak_kind = measured_peak_gbs()
         per_launch_bytes = step_bytes / L
         achieved = per_launch_bytes / (ms * 1e-3 / L) / 1e9 / 1.0
-        launches_per_step = L * (2 if splits > 1 else 1)
+        launches_per_step = L  # split merge happens inside the decode launch
         counts = search.seg_counts.cpu().numpy()
         frac = counts.sum(axis=0) / counts.sum()
         line = {

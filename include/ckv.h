@@ -196,12 +196,17 @@ int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_hea
                                    int32_t splits);
 /* Resident decode CTAs per SM on the current device (for sizing `splits` to whole waves). */
 int32_t ckv_decode_ctas_per_sm(void);
+#define CKV_DECODE_PDL 1  /* flags bit: launch as a programmatic dependent of the preceding
+                             kernel, which must not write the quantized arenas or the immutable
+                             seq fields (e.g. the previous layer's decode).  The kernel prefetches
+                             its first K/V tiles, then waits on the preceding grid before it
+                             reads q, len_fp or the FP16 region. */
 int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
                              ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
                              int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                              float scale, int32_t splits, void* workspace, uint16_t* out,
                              int64_t o_s_layer, int64_t o_s_batch, float* partial_out,
-                             void* stream);
+                             int32_t flags, void* stream);
 
 /* Split-KV merge across ranks (new; the NCCL-exchanged partials of SURVEY §8e):
  * partials f32 [P][rows][128 + 2] = (acc[128] unnormalised at m, m (log2 domain), l);

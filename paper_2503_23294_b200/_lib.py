@@ -33,6 +33,7 @@ FLAG_CROSSING = 4
 FLAG_EMPTY_SCORES = 8
 
 SEQ_FIELDS = 8  # CKV_SEQ_FIELDS
+DECODE_PDL = 1  # CKV_DECODE_PDL
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -73,7 +74,7 @@ _SIGNATURES = {
     "ckv_decode_workspace_bytes": ([_i32, _i32, _i32, _i32, _i32], _i64),
     "ckv_decode_ctas_per_sm": ([], _i32),
     "ckv_decode_attention": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _f32, _i32,
-                              _vp, _vp, _i64, _i64, _vp, _vp], _i32),
+                              _vp, _vp, _i64, _i64, _vp, _i32, _vp], _i32),
     "ckv_lse_merge": ([_vp, _i32, _i64, _vp, _vp], _i32),
 }
 

@@ -161,18 +161,32 @@ class BatchedKVCache:
                 best, best_cost = s, cost
         return best
 
-    def _workspace(self, m, splits):
-        key = (m, splits)
+    def _workspace(self, m, splits, layers, layer):
+        """Zero-initialised decode workspace (split partials + self-resetting arrival counters).
+        Launches covering a single layer get a private per-layer slice, so consecutive
+        per-layer launches never share counters (required for programmatic dependent launch)."""
+        lib = _lib.load()
+        if layers == self.L:
+            key = (m, splits, "all")
+            nbytes = lib.ckv_decode_workspace_bytes(self.L, self.B, self.H, m, splits)
+            off = 0
+        else:
+            key = (m, splits, "per-layer", layers)
+            per = lib.ckv_decode_workspace_bytes(layers, self.B, self.H, m, splits)
+            per = -(-per // 256) * 256
+            nbytes = per * self.L
+            off = per * layer
         if key not in self._ws:
-            nbytes = _lib.load().ckv_decode_workspace_bytes(self.L, self.B, self.H, m, splits)
-            # zero once: the split-KV arrival counters live at the front and self-reset
             self._ws[key] = torch.zeros(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
-        return self._ws[key]
+        return self._ws[key].data_ptr() + off
 
-    def decode(self, q, splits=None, out=None, scale=None, layer=0):
+    def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False):
         """Mixed-precision decode attention for q fp16 [L', B, H*m, 128] -> fp16 same shape,
         over layers [layer, layer + L') of the cache (L' = L for the whole model in one launch,
-        1 for the per-layer launches of a real decode step)."""
+        1 for the per-layer launches of a real decode step).  pdl=True launches as a
+        programmatic dependent of the previous kernel on the stream; use it only when that
+        kernel was itself a decode of this cache (it overlaps this launch's K/V prefetch with
+        the previous launch's tail)."""
         L, B, Hq, D = q.shape
         if B != self.B or layer < 0 or layer + L > self.L or D != HEAD_DIM or Hq % self.H:
             raise ValueError("q shape does not match the cache")
@@ -184,25 +198,27 @@ class BatchedKVCache:
         splits = self.default_splits(m, L) if splits is None else int(splits)
         if out is None:
             out = torch.empty((L, B, Hq, D), dtype=torch.float16, device=q.device)
-        ws = self._workspace(m, splits)
+        ws = self._workspace(m, splits, L, layer)
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
         _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1),
                   self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H,
-                  m, scale, splits, _lib.ptr(ws), _lib.ptr(out), out.stride(0), out.stride(1), None,
-                  _lib.stream())
+                  m, scale, splits, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
+                  _lib.DECODE_PDL if pdl else 0, _lib.stream())
         return out
 
     def decode_partial(self, q, splits=None, scale=None):
         """Unnormalised split-KV partials f32 [L*B*H*m, 130] = (acc[128], m (log2), l)."""
         L, B, Hq, D = q.shape
+        if (L, B) != (self.L, self.B) or D != HEAD_DIM or Hq % self.H:
+            raise ValueError("q shape does not match the cache")
         m = Hq // self.H
         splits = self.default_splits(m) if splits is None else int(splits)
         part = torch.empty((L * B * Hq, HEAD_DIM + 2), dtype=torch.float32, device=q.device)
-        ws = self._workspace(m, splits)
+        ws = self._workspace(m, splits, L, 0)
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
         _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k"),
                   self.arena("v"), _lib.ptr(self.seq), L, B, self.H, m, scale, splits,
-                  _lib.ptr(ws), None, 0, 0, _lib.ptr(part), _lib.stream())
+                  ws, None, 0, 0, _lib.ptr(part), 0, _lib.stream())
         return part
 
     def append(self, k_new, v_new):

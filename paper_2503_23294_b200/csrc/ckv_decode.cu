@@ -477,21 +477,26 @@ __device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const Ti
   cp_commit();
 }
 
-// The tile loops of one warp: quantized tiles through the cp.async ring, then FP16 tiles.
-template <bool EXACT>
-__device__ __forceinline__ void run_tiles(int t_begin, int t_end, int n2t, int n4t, int len_fp,
-                                          const TileSrc& src, const LaneSrc& lo, const uint16_t* kf,
-                                          const uint16_t* vf, uint32_t ring_l, const QS& qs,
-                                          uint32_t mg, WarpState& st, int warp, int g, int c) {
-  const int t_q_end = min(t_end, n2t + n4t);
+// Prologue: put this warp's first kStages-1 quantized tiles in flight.
+__device__ __forceinline__ void prologue(int q_begin, int q_end, int n2t, const TileSrc& src,
+                                         const LaneSrc& lo, uint32_t ring_l, int warp) {
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s)
-    issue_tile(t_begin + warp + kDecWarps * s, t_q_end, n2t, src, lo, ring_l + s * kStageBytes);
+    issue_tile(q_begin + warp + kDecWarps * s, q_end, n2t, src, lo, ring_l + s * kStageBytes);
+}
+
+// The tile loops of one warp: quantized tiles [q_begin, q_end) through the cp.async ring
+// (prologue already issued), then FP16-region tiles [f_begin, f_end).
+template <bool EXACT>
+__device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, int f_end, int n2t,
+                                          int len_fp, const TileSrc& src, const LaneSrc& lo,
+                                          const uint16_t* kf, const uint16_t* vf, uint32_t ring_l,
+                                          const QS& qs, uint32_t mg, WarpState& st, int warp, int g,
+                                          int c) {
   uint32_t use = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
-  int t = t_begin + warp;
-  for (; t < t_q_end; t += kDecWarps) {
-    issue_tile(t + kDecWarps * (kStages - 1), t_q_end, n2t, src, lo, put);
+  for (int t = q_begin + warp; t < q_end; t += kDecWarps) {
+    issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, src, lo, put);
     put = put + kStageBytes == ring_end ? ring_l : put + kStageBytes;
     cp_wait<kStages - 1>();
     __syncwarp();
@@ -501,8 +506,8 @@ __device__ __forceinline__ void run_tiles(int t_begin, int t_end, int n2t, int n
     __syncwarp();
   }
   cp_wait<0>();
-  for (; t < t_end; t += kDecWarps) {
-    const int r = (t - n2t - n4t) * kTile;
+  for (int t = f_begin + warp; t < f_end; t += kDecWarps) {
+    const int r = t * kTile;
     tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
   }
 }
@@ -516,40 +521,52 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   const int g = lane >> 2, c = lane & 3;
   const int split = blockIdx.x, h = blockIdx.y;
   const int l = blockIdx.z / a.B, b = blockIdx.z % a.B;
-  const Seq8 sq = ld_seq(a.seq, b);
-  const int n2t = sq.len2 / kTile, n4t = sq.len4 / kTile;
-  const int nft = (sq.len_fp + kTile - 1) / kTile;
-  // byte-balanced split of the virtual tile sequence (INT2 || INT4 || FP16)
-  const int64_t c2 = 96, c4 = 160, cf = 512;
-  const int64_t tot = n2t * c2 + n4t * c4 + nft * cf;
-  auto tile_at = [&](int64_t x) -> int {  // first tile whose start cost >= x
+  // Segment lengths of the quantized arenas are immutable after the build; len_fp grows with
+  // decode appends and is read only after the programmatic-dependent-launch wait below.
+  const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
+  const int off2 = s0.x, off4 = s0.z, off_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 4];
+  const int n2t = s0.y / kTile, n4t = s0.w / kTile;
+  // time-balanced split of the quantized tiles (INT2 || INT4): an INT2 tile (1.5 KB) and an
+  // INT4 tile (2.5 KB) cost about the same issue slots (dequant-bound), so weigh them ~equally.
+  // FP16-region tiles are split separately.
+  const int64_t c2 = 100, c4 = 110;
+  const int64_t qtot = n2t * c2 + n4t * c4;
+  auto qtile_at = [&](int64_t x) -> int {  // first tile whose start cost >= x
     if (x <= n2t * c2) return (int)((x + c2 - 1) / c2);
     x -= n2t * c2;
-    if (x <= n4t * c4) return n2t + (int)((x + c4 - 1) / c4);
-    x -= n4t * c4;
-    return n2t + n4t + (int)min((int64_t)nft, (x + cf - 1) / cf);
+    return n2t + (int)min((int64_t)n4t, (x + c4 - 1) / c4);
   };
-  const int t_begin = tile_at(tot * split / a.splits);
-  const int t_end = tile_at(tot * (split + 1) / a.splits);
-
+  const int q_begin = qtile_at(qtot * split / a.splits);
+  const int q_end = qtile_at(qtot * (split + 1) / a.splits);
   const int64_t unit = (int64_t)l * a.H + h;
   TileSrc src;
-  src.k2 = reinterpret_cast<const char*>(a.K.codes2 + (unit * a.K.rows2 + sq.off2) * 8);
-  src.k2m = reinterpret_cast<const char*>(a.K.meta2 + (unit * a.K.rows2 + sq.off2) * 4);
-  src.v2 = reinterpret_cast<const char*>(a.V.codes2 + (unit * a.V.rows2 + sq.off2) * 8);
-  src.v2m = reinterpret_cast<const char*>(a.V.meta2 + (unit * a.V.rows2 + sq.off2) * 4);
-  src.k4 = reinterpret_cast<const char*>(a.K.codes4 + (unit * a.K.rows4 + sq.off4) * 16);
-  src.k4m = reinterpret_cast<const char*>(a.K.meta4 + (unit * a.K.rows4 + sq.off4) * 4);
-  src.v4 = reinterpret_cast<const char*>(a.V.codes4 + (unit * a.V.rows4 + sq.off4) * 16);
-  src.v4m = reinterpret_cast<const char*>(a.V.meta4 + (unit * a.V.rows4 + sq.off4) * 4);
-  const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + sq.off_fp) * kHeadDim;
-  const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + sq.off_fp) * kHeadDim;
+  src.k2 = reinterpret_cast<const char*>(a.K.codes2 + (unit * a.K.rows2 + off2) * 8);
+  src.k2m = reinterpret_cast<const char*>(a.K.meta2 + (unit * a.K.rows2 + off2) * 4);
+  src.v2 = reinterpret_cast<const char*>(a.V.codes2 + (unit * a.V.rows2 + off2) * 8);
+  src.v2m = reinterpret_cast<const char*>(a.V.meta2 + (unit * a.V.rows2 + off2) * 4);
+  src.k4 = reinterpret_cast<const char*>(a.K.codes4 + (unit * a.K.rows4 + off4) * 16);
+  src.k4m = reinterpret_cast<const char*>(a.K.meta4 + (unit * a.K.rows4 + off4) * 4);
+  src.v4 = reinterpret_cast<const char*>(a.V.codes4 + (unit * a.V.rows4 + off4) * 16);
+  src.v4m = reinterpret_cast<const char*>(a.V.meta4 + (unit * a.V.rows4 + off4) * 4);
+  const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
+  const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
   LaneSrc lo;
   lo.k = g * 32 + 8 * c;          // K row g, bytes of group c (INT2)
   lo.km = g * 16 + 4 * c;         // K meta row g, group c
   lo.v = 2 * c * 32 + 4 * g;      // V row 2c, word g (INT2)
   lo.vm = 2 * c * 16 + 4 * (g >> 1);
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
+  prologue(q_begin, q_end, n2t, src, lo, ring_l, warp);
+
+  // Everything above touched only build-time data.  q, the FP16 region and len_fp may come
+  // from the preceding kernel on the stream: wait for it (no-op without PDL), and let the next
+  // decode launch (next layer) start its own prologue as soon as SMs free up.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 5];
+  const int nft = (len_fp + kTile - 1) / kTile;
+  const int f_begin = (int)((int64_t)nft * split / a.splits);
+  const int f_end = (int)((int64_t)nft * (split + 1) / a.splits);
 
   // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m); warp 0 writes the
   // CTA's three sets to shared memory.
@@ -616,9 +633,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.lsum[0] = st.lsum[1] = 0.f;
 
   if (exact) {
-    run_tiles<true>(t_begin, t_end, n2t, n4t, sq.len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<true>(q_begin, q_end, f_begin, f_end, n2t, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
   } else {
-    run_tiles<false>(t_begin, t_end, n2t, n4t, sq.len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<false>(q_begin, q_end, f_begin, f_end, n2t, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
     // undo the V m-tile weights 2^(2(mt&3) - 6)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
@@ -755,7 +772,7 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
                              int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                              float scale, int32_t splits, void* workspace, uint16_t* out,
                              int64_t o_s_layer, int64_t o_s_batch, float* partial_out,
-                             void* stream) {
+                             int32_t flags, void* stream) {
   if (layers < 0 || batch < 0 || kv_heads < 0 || splits < 1) return CKV_ERR_ARG;
   if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (!q || !seq || (!out && !partial_out)) return CKV_ERR_ARG;
@@ -775,9 +792,20 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
   a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
   a.partial_out = partial_out;
   a.zero = 0u;
-  dim3 grid((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * batch));
-  decode_kernel<<<grid, kDecWarps * 32, 0, as_stream(stream)>>>(a);
-  CKV_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * batch));
+  cfg.blockDim = dim3(kDecWarps * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (flags & CKV_DECODE_PDL) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, decode_kernel, a) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return CKV_ERR_CUDA;
+  }
   return CKV_OK;
 }
 

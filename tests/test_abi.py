@@ -50,7 +50,7 @@ def test_argument_validation_without_gpu():
                           None, None, None) == _lib.CKV_ERR_ARG
     ar = _lib.Arena()
     assert lib.ckv_decode_attention(ctypes.c_void_p(16), 0, 0, ar, ar, ctypes.c_void_p(16), 1, 1, 1, 9,
-                                    0.1, 1, None, ctypes.c_void_p(16), 0, 0, None, None) == _lib.CKV_ERR_UNSUPPORTED
+                                    0.1, 1, None, ctypes.c_void_p(16), 0, 0, None, 0, None) == _lib.CKV_ERR_UNSUPPORTED
     # zero-size work is a no-op success
     assert lib.ckv_pack_codes(None, 0, 2, None, None) == _lib.CKV_OK
 

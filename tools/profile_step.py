@@ -26,7 +26,7 @@ def main():
     out = torch.empty_like(q)
     for _ in range(args.steps):
         for l in range(cache.L):
-            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l)
+            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
     torch.cuda.synchronize()
     if args.prefill:
         del cache
