@@ -31,7 +31,7 @@ namespace ckv {
 
 constexpr int kDecWarps = 4;
 constexpr int kTile = 16;
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 // Stage layout is lane-ordered: every lane's fragment data for one tile sits in 16-byte
 // slots [region][lane][16 B], filled by cp.async straight from the reference-format rows.
 //   INT2: KC @0 (tok g | tok g+8, 8 B each), VC @512 (word g of tok 2c,2c+1,2c+8,2c+9),
@@ -39,6 +39,7 @@ constexpr int kStages = 3;
 //   INT4: KC @0 (tok g, 16 B) @512 (tok g+8), VC @1024 (tok 2c|2c+1, 8 B each) @1536 (2c+8|2c+9),
 //         KM @2048, VM @2560
 constexpr int kStageBytes = 3072;
+constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 48 KB per CTA
 constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
 
@@ -164,14 +165,17 @@ struct WarpState {
 
 __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint32_t& bp0,
                                              uint32_t& bp1) {
+  // Lazy online softmax: keep the running max unless a score exceeds it by more than the
+  // threshold (then P <= 2^8 still fits fp16).  Only then reduce the tile max across the
+  // 8 row-groups and rescale; the common case needs no shuffles.
   float t0 = fmaxf(s[0], s[2]), t1 = fmaxf(s[1], s[3]);
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {
-    t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, o));
-    t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, o));
-  }
   const bool need = (t0 > st.mrun[0] + kRescaleThresh) || (t1 > st.mrun[1] + kRescaleThresh);
   if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+      t1 = fmaxf(t1, __shfl_xor_sync(0xffffffffu, t1, o));
+    }
     const float n0 = fmaxf(st.mrun[0], t0), n1 = fmaxf(st.mrun[1], t1);
     const float f0 = st.mrun[0] == -INFINITY ? 0.0f : fast_exp2(st.mrun[0] - n0);
     const float f1 = st.mrun[1] == -INFINITY ? 0.0f : fast_exp2(st.mrun[1] - n1);
@@ -215,17 +219,15 @@ __device__ __forceinline__ void lo_mma(WarpState& st, uint32_t a0, uint32_t a2, 
 
 // ---- INT2 tile from a shared-memory stage ----------------------------------------------
 template <bool EXACT>
-__device__ __forceinline__ void tile_int2(uint32_t sl, const QS& qs, uint32_t mg, WarpState& st) {
+__device__ __forceinline__ void qk_int2(uint32_t sl, const QS& qs, uint32_t mg, float (&s)[4]) {
   const uint4 kk = lds128(sl);  // (tok g: words 2c, 2c+1), (tok g+8: words 2c, 2c+1)
   const uint2 kmm = lds64(sl + 1024);
-  const uint4 vv = lds128(sl + 512);
-  const uint4 vmm = lds128(sl + 1536);
   constexpr float iq = 1.0f / 3.0f;
   const float sk0 = meta_scale(kmm.x, iq), sk1 = meta_scale(kmm.y, iq);
-  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
-  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
 
-  float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+  float s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s[e] = 0.f;
   if (!EXACT) {
     const DeqC dk0 = make_deq(sk0, sk0), dk1 = make_deq(sk1, sk1);
 #pragma unroll
@@ -256,8 +258,15 @@ __device__ __forceinline__ void tile_int2(uint32_t sl, const QS& qs, uint32_t mg
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) s[e] += s2[e];
-  uint32_t bp0, bp1;
-  softmax_tile(s, st, bp0, bp1);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void pv_int2(uint32_t sl, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+  const uint4 vv = lds128(sl + 512);
+  const uint4 vmm = lds128(sl + 1536);
+  constexpr float iq = 1.0f / 3.0f;
+  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
+  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
   const uint32_t c01lo = prmt(vv.x, vv.y, 0x5410), c01hi = prmt(vv.x, vv.y, 0x7632);
   const uint32_t c23lo = prmt(vv.z, vv.w, 0x5410), c23hi = prmt(vv.z, vv.w, 0x7632);
   if (!EXACT) {
@@ -289,17 +298,15 @@ __device__ __forceinline__ void tile_int2(uint32_t sl, const QS& qs, uint32_t mg
 
 // ---- INT4 tile from a shared-memory stage ----------------------------------------------
 template <bool EXACT>
-__device__ __forceinline__ void tile_int4(uint32_t sl, const QS& qs, uint32_t mg, WarpState& st) {
+__device__ __forceinline__ void qk_int4(uint32_t sl, const QS& qs, uint32_t mg, float (&s)[4]) {
   const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);  // group c of tok g / tok g+8
   const uint2 kmm = lds64(sl + 2048);
-  const uint4 va = lds128(sl + 1024), vb = lds128(sl + 1536);
-  const uint4 vmm = lds128(sl + 2560);
   constexpr float iq = 1.0f / 15.0f;
   const float sk0 = meta_scale(kmm.x, iq), sk1 = meta_scale(kmm.y, iq);
-  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
-  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
 
-  float s[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+  float s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s[e] = 0.f;
   const uint32_t kwa[4] = {kw0.x, kw0.y, kw0.z, kw0.w}, kwb[4] = {kw1.x, kw1.y, kw1.z, kw1.w};
   if (!EXACT) {
     const DeqC dk0 = make_deq(sk0, sk0), dk1 = make_deq(sk1, sk1);
@@ -338,8 +345,15 @@ __device__ __forceinline__ void tile_int4(uint32_t sl, const QS& qs, uint32_t mg
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) s[e] += s2[e];
-  uint32_t bp0, bp1;
-  softmax_tile(s, st, bp0, bp1);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void pv_int4(uint32_t sl, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+  const uint4 va = lds128(sl + 1024), vb = lds128(sl + 1536);
+  const uint4 vmm = lds128(sl + 2560);
+  constexpr float iq = 1.0f / 15.0f;
+  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
+  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
   // V (tok 2c | 2c+1) and (2c+8 | 2c+9) for d = 16g + mt (word 2g) and 16g + 8 + mt (word 2g+1)
   const uint32_t x01[4] = {prmt(va.x, va.z, 0x5410), prmt(va.x, va.z, 0x7632),
                            prmt(va.y, va.w, 0x5410), prmt(va.y, va.w, 0x7632)};
@@ -485,35 +499,76 @@ __device__ __forceinline__ void prologue(int q_begin, int q_end, int n2t, const 
     issue_tile(q_begin + warp + kDecWarps * s, q_end, n2t, src, lo, ring_l + s * kStageBytes);
 }
 
+template <bool EXACT>
+__device__ __forceinline__ void qk_any(bool int2, uint32_t sl, const QS& qs, uint32_t mg, float (&s)[4]) {
+  if (int2) qk_int2<EXACT>(sl, qs, mg, s);
+  else qk_int4<EXACT>(sl, qs, mg, s);
+}
+template <bool EXACT>
+__device__ __forceinline__ void pv_any(bool int2, uint32_t sl, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+  if (int2) pv_int2<EXACT>(sl, mg, st, bp0, bp1);
+  else pv_int4<EXACT>(sl, mg, st, bp0, bp1);
+}
+
 // The tile loops of one warp: quantized tiles [q_begin, q_end) through the cp.async ring
-// (prologue already issued), then FP16-region tiles [f_begin, f_end).
+// (prologue already issued), software-pipelined so that q.K^T of tile i+1 and P.V of tile i
+// form one straight-line block (independent MMA chains the scheduler can interleave); then
+// FP16-region tiles [f_begin, f_end).
 template <bool EXACT>
 __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, int f_end, int n2t,
                                           int len_fp, const TileSrc& src, const LaneSrc& lo,
                                           const uint16_t* kf, const uint16_t* vf, uint32_t ring_l,
                                           const QS& qs, uint32_t mg, WarpState& st, int warp, int g,
                                           int c) {
-  uint32_t use = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
-  for (int t = q_begin + warp; t < q_end; t += kDecWarps) {
-    issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, src, lo, put);
-    put = put + kStageBytes == ring_end ? ring_l : put + kStageBytes;
-    cp_wait<kStages - 1>();
+  auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
+  int t = q_begin + warp;
+  if (t < q_end) {
+    uint32_t cur = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
+    cp_wait<kStages - 2>();
     __syncwarp();
-    if (t < n2t) tile_int2<EXACT>(use, qs, mg, st);
-    else tile_int4<EXACT>(use, qs, mg, st);
-    use = use + kStageBytes == ring_end ? ring_l : use + kStageBytes;
-    __syncwarp();
+    float s0[4];
+    qk_any<EXACT>(t < n2t, cur, qs, mg, s0);
+    uint32_t bp0, bp1;
+    softmax_tile(s0, st, bp0, bp1);
+    while (true) {
+      const int tn = t + kDecWarps;
+      issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, src, lo, put);
+      put = next(put);
+      if (tn >= q_end) {
+        pv_any<EXACT>(t < n2t, cur, mg, st, bp0, bp1);
+        break;
+      }
+      cp_wait<kStages - 2>();
+      __syncwarp();
+      const uint32_t nx = next(cur);
+      float sn[4];
+      if (tn < n2t) {  // both INT2 (tn > t)
+        qk_int2<EXACT>(nx, qs, mg, sn);
+        pv_int2<EXACT>(cur, mg, st, bp0, bp1);
+      } else if (t >= n2t) {  // both INT4
+        qk_int4<EXACT>(nx, qs, mg, sn);
+        pv_int4<EXACT>(cur, mg, st, bp0, bp1);
+      } else {  // INT2 -> INT4 boundary
+        qk_int4<EXACT>(nx, qs, mg, sn);
+        pv_int2<EXACT>(cur, mg, st, bp0, bp1);
+      }
+      __syncwarp();  // slot `cur` may be refilled from now on
+      softmax_tile(sn, st, bp0, bp1);
+      cur = nx;
+      t = tn;
+    }
   }
   cp_wait<0>();
-  for (int t = f_begin + warp; t < f_end; t += kDecWarps) {
-    const int r = t * kTile;
+  for (int tf = f_begin + warp; tf < f_end; tf += kDecWarps) {
+    const int r = tf * kTile;
     tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
   }
 }
 
 __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs a) {
-  __shared__ __align__(128) unsigned char s_ring[kDecWarps][kStages][kStageBytes];
+  extern __shared__ __align__(128) unsigned char s_dyn[];  // ring: [warp][stage][kStageBytes]
+  unsigned char (*s_ring)[kStages][kStageBytes] = reinterpret_cast<unsigned char (*)[kStages][kStageBytes]>(s_dyn);
   __shared__ float s_ml[kDecWarps][8][2];
   __shared__ __align__(16) uint2 s_q[3][9][32];
   __shared__ int s_last, s_wide_q;
@@ -757,6 +812,18 @@ __global__ void lse_merge_kernel(const float* __restrict__ parts, int P, int64_t
 
 using namespace ckv;
 
+static bool ensure_decode_attr() {
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return false;
+    }
+    attr_set = true;
+  }
+  return true;
+}
+
 extern "C" {
 
 int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
@@ -792,10 +859,11 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
   a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
   a.partial_out = partial_out;
   a.zero = 0u;
+  if (!ensure_decode_attr()) return CKV_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * batch));
   cfg.blockDim = dim3(kDecWarps * 32);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = kDynSmem;
   cfg.stream = as_stream(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -810,8 +878,9 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
 }
 
 int32_t ckv_decode_ctas_per_sm(void) {
+  if (!ensure_decode_attr()) return -1;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel, kDecWarps * 32, 0) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel, kDecWarps * 32, kDynSmem) != cudaSuccess) {
     (void)cudaGetLastError();
     return -1;
   }
