@@ -25,6 +25,8 @@
 //   weighted form run an unweighted exact mode (code by subtraction, full affine).
 #include <math.h>
 
+#include <cuda/atomic>
+
 #include "ckv_common.cuh"
 
 namespace ckv {
@@ -42,6 +44,7 @@ constexpr int kStageBytes = 3072;
 constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 48 KB per CTA
 constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
+constexpr int kMaxSplitsFast = 16;         // split merge keeps up to 16 partials in registers
 
 struct DecArgs {
   const uint16_t* q;
@@ -757,27 +760,50 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     }
   }
   if (a.splits == 1) return;
-  // split-KV: the last CTA of this unit to arrive merges all partials (in-launch, no 2nd kernel)
-  __threadfence();
+  // split-KV: the last CTA of this unit to arrive merges all partials (in-launch, no 2nd
+  // kernel).  The CTA barrier orders every thread's partial stores before thread 0's
+  // device-scope release RMW; the acquiring side sees them after its own barrier.
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t prev = atomicAdd(a.counters + ((int64_t)l * a.B + b) * a.H + h, 1u);
+    cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[((int64_t)l * a.B + b) * a.H + h]);
+    const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
     s_last = prev == (uint32_t)(a.splits - 1);
+    if (s_last) ctr.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   for (int qi = 0; qi < a.m; ++qi) {
     const int64_t row = ((int64_t)l * a.B + b) * Hq + hq0 + qi;
     const float* p = a.ws + row * a.splits * kPartStride;
-    float ms = -INFINITY;
-    for (int s = 0; s < a.splits; ++s) ms = fmaxf(ms, __ldcg(p + s * kPartStride + kHeadDim));
-    float acc = 0.f, lsum = 0.f;
-    for (int s = 0; s < a.splits; ++s) {
-      const float mw = __ldcg(p + s * kPartStride + kHeadDim);
-      const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-      acc += f * __ldcg(p + s * kPartStride + d);
-      lsum += f * __ldcg(p + s * kPartStride + kHeadDim + 1);
+    float mv[kMaxSplitsFast], lv[kMaxSplitsFast], av[kMaxSplitsFast];
+    float ms = -INFINITY, acc = 0.f, lsum = 0.f;
+    if (a.splits <= kMaxSplitsFast) {
+#pragma unroll
+      for (int s = 0; s < kMaxSplitsFast; ++s) {  // all loads in flight at once
+        if (s < a.splits) {
+          mv[s] = __ldcg(p + s * kPartStride + kHeadDim);
+          lv[s] = __ldcg(p + s * kPartStride + kHeadDim + 1);
+          av[s] = __ldcg(p + s * kPartStride + d);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < kMaxSplitsFast; ++s) if (s < a.splits) ms = fmaxf(ms, mv[s]);
+#pragma unroll
+      for (int s = 0; s < kMaxSplitsFast; ++s) {
+        if (s < a.splits) {
+          const float f = mv[s] == -INFINITY ? 0.f : fast_exp2(mv[s] - ms);
+          acc += f * av[s];
+          lsum += f * lv[s];
+        }
+      }
+    } else {
+      for (int s = 0; s < a.splits; ++s) ms = fmaxf(ms, __ldcg(p + s * kPartStride + kHeadDim));
+      for (int s = 0; s < a.splits; ++s) {
+        const float mw = __ldcg(p + s * kPartStride + kHeadDim);
+        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+        acc += f * __ldcg(p + s * kPartStride + d);
+        lsum += f * __ldcg(p + s * kPartStride + kHeadDim + 1);
+      }
     }
     if (a.partial_out) {
       float* dst = a.partial_out + row * kPartStride;
@@ -788,7 +814,6 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
           __half_as_ushort(__float2half_rn(acc / lsum));
     }
   }
-  if (threadIdx.x == 0) a.counters[((int64_t)l * a.B + b) * a.H + h] = 0u;  // ready for the next launch
 }
 
 // Cross-rank merge of gathered partials [P][rows][130] -> out fp16 [rows][128].
