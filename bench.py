@@ -60,11 +60,7 @@ def load_workload(ctx, seed):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled (NVML, every 10 ms) during the timed region."""
 
     def __init__(self, index):
         self.index = index
@@ -73,16 +69,22 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            hdl = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                    "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                    "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                    "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4)}
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(hdl)
+                self.samples.append((sm, mx, [k for k, b in bits.items() if r & b]))
+                self._stop.wait(0.01)
+        except Exception as exc:  # no NVML: record why
+            self.samples.append((None, None, [f"unsampled: {type(exc).__name__}"]))
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -94,14 +96,12 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples if s[0] is not None]
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": sorted({r for s in self.samples for r in s[2]}) or ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples if s[1]),
+                "reasons": sorted({r for s in self.samples for r in s[2]}), "samples": len(sm)}
 
 
 def measured_peak_gbs():
@@ -226,7 +226,7 @@ def build_cfg2(torch, dev, rank):
     return cache, q, search
 
 
-def bench_prefill(torch, dev, steps=3):
+def bench_prefill(torch, dev, steps=3, profile=False):
     """cfg5-shaped prefill: search + reorder/quantize/pack of a 128K x 32-layer x 8-head cache."""
     from paper_2503_23294_b200 import batched, retrieval
 
@@ -247,6 +247,8 @@ def bench_prefill(torch, dev, steps=3):
     for i in range(steps + 2):
         flush.fill_(i)
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        if profile and i == steps + 1:
+            torch.cuda.profiler.start()
         e0.record()
         s2 = retrieval.search_batched(wl["emb"][None], wl["norm"][None], wl["q"][None],
                                       np.array([wl["qnorm"]]), check=False)
@@ -254,6 +256,8 @@ def bench_prefill(torch, dev, steps=3):
         cache.build(k, v, s2.perm, check=False)
         e2.record()
         torch.cuda.synchronize()
+        if profile and i == steps + 1:
+            torch.cuda.profiler.stop()
         if i >= 2:
             times_search.append(e0.elapsed_time(e1))
             times_build.append(e1.elapsed_time(e2))

@@ -46,6 +46,68 @@ __device__ __forceinline__ uint32_t exact_code(float x, float lo, float hi, floa
   return (uint32_t)n;
 }
 
+// One 8-element lane slice of a row (4 lanes = one 32-element group): group min/max, codes,
+// packed little-endian lane word.  Fast path per element (7 instructions):
+//   r = (x - lo) * (qmax / span)   [x - lo in one mixed f16/f32 add]
+//   y = r + 1.5*2^23               [low mantissa bits = round-half-even(r)]
+//   |r - (y - 1.5*2^23)| > 0.5 - 2^-14  -> exact IEEE f64 recomputation (near a tie)
+//   acc += bits(y) * base^e        [one IMAD; the constant offset is pre-subtracted]
+// The fp32 value of r is within 3.6e-6 of the exact rational, so away from the guard band
+// round-half-even(r) == floor(exact + 0.5) == the reference's f64 result.
+template <int BITS>
+__device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float& lo_out, float& hi_out,
+                                                   bool& bad, bool& wide) {
+  constexpr float qmax = BITS == 2 ? 3.0f : 15.0f;
+  constexpr uint32_t base = BITS == 2 ? 4u : 16u;
+  constexpr uint32_t kM = 0x4B400000u;  // bits of 1.5 * 2^23
+  constexpr uint32_t kSum = BITS == 2 ? 21845u : 0x11111111u;  // sum_e base^e, e = 0..7
+  // group min / max in fp16 with NaN propagation; (lo, -hi) travel as one half2
+  const __half2 h0 = u32_as_h2(w[0]), h1 = u32_as_h2(w[1]), h2 = u32_as_h2(w[2]), h3 = u32_as_h2(w[3]);
+  const __half2 mn = __hmin2_nan(__hmin2_nan(h0, h1), __hmin2_nan(h2, h3));
+  const __half2 mx = __hmax2_nan(__hmax2_nan(h0, h1), __hmax2_nan(h2, h3));
+  __half2 lh = __halves2half2(__hmin_nan(__low2half(mn), __high2half(mn)),
+                              __hneg(__hmax_nan(__low2half(mx), __high2half(mx))));
+  lh = __hmin2_nan(lh, u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(lh), 1)));
+  lh = __hmin2_nan(lh, u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(lh), 2)));
+  const float lo = __low2float(lh), hi = -__high2float(lh);
+  lo_out = lo;
+  hi_out = hi;
+  const float span = hi - lo;
+  bad |= !(isfinite(lo) && isfinite(hi));  // any inf / nan in the group reaches lo or hi
+  wide |= span * (1.0f / qmax) > 4000.0f;
+  if (!(span > 0.0f)) return 0u;  // constant group: codes 0 (also nan groups; flagged above)
+  const float qinv = qmax / span;
+  uint32_t acc = 0u - kM * kSum;
+  bool near = false;
+  float r[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t hb = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+    float d;
+    asm("{.reg .f16 xh; mov.b16 xh, %1; sub.rn.f32.f16 %0, xh, %2;}" : "=f"(d) : "h"((unsigned short)hb), "f"(lo));
+    r[e] = d * qinv;
+    const float y = r[e] + 12582912.0f;
+    const float dd = r[e] - (y - 12582912.0f);
+    near |= fabsf(dd) > 0.5f - (1.0f / 16384.0f);
+    uint32_t p = 1u;
+#pragma unroll
+    for (int k = 0; k < e; ++k) p *= base;
+    acc += __float_as_uint(y) * p;
+  }
+  if (near) {  // rare: redo every element of this slice exactly (IEEE f64, reference tree)
+    acc = 0u;
+    uint32_t p = 1u;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t hb = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+      const float x = __half2float(__ushort_as_half((unsigned short)hb));
+      acc += exact_code(x, lo, hi, qinv, qmax) * p;
+      p *= base;
+    }
+  }
+  return acc;
+}
+
 // One warp per (layer, sequence, kv-head, destination chunk slot).  Slot p < N takes source
 // chunk perm[p]; slot p == N is the context tail (if any).
 __global__ void __launch_bounds__(kQWarps * 32)
@@ -100,41 +162,26 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       }
       continue;
     }
-    const float qmax = tier == 0 ? 3.0f : 15.0f;
     bool wide = false;
-#pragma unroll 2
-    for (int rr = 0; rr < 16; ++rr) {
-      const int r = 2 * rr + sub;
-      const uint4 x = __ldg(reinterpret_cast<const uint4*>(src + r * sT) + j);
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-      float f[8];
+#pragma unroll 1
+    for (int r4 = 0; r4 < 16; r4 += 4) {
+      uint4 xs[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        bad |= !fp16_bits_finite(w[e] & 0xFFFF) || !fp16_bits_finite(w[e] >> 16);
-        const float2 t = __half22float2(u32_as_h2(w[e]));
-        f[2 * e] = t.x;
-        f[2 * e + 1] = t.y;
+      for (int u = 0; u < 4; ++u)  // four 16-byte loads in flight per lane
+        xs[u] = __ldg(reinterpret_cast<const uint4*>(src + (2 * (r4 + u) + sub) * sT) + j);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = 2 * (r4 + u) + sub;
+        const uint32_t w[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+        float lo, hi;
+        if (tier == 0) {
+          const uint32_t packed = quantize_slice<2>(w, lo, hi, bad, wide);
+          reinterpret_cast<uint16_t*>(s_codes[warp])[r * 16 + j] = (uint16_t)packed;
+        } else {
+          s_codes[warp][r * 16 + j] = quantize_slice<4>(w, lo, hi, bad, wide);
+        }
+        if ((j & 3) == 0) s_meta[warp][r * 4 + (j >> 2)] = h2_as_u32(__floats2half2_rn(lo, hi));
       }
-      float lo = f[0], hi = f[0];
-#pragma unroll
-      for (int e = 1; e < 8; ++e) { lo = fminf(lo, f[e]); hi = fmaxf(hi, f[e]); }
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
-      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
-      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
-      const float span = hi - lo;  // only compared against 0 and used in the guarded candidate
-      uint32_t packed = 0;
-      if (span > 0.0f) {
-        const float qinv = qmax * (1.0f / span);
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          packed |= exact_code(f[e], lo, hi, qinv, qmax) << (e * (tier == 0 ? 2 : 4));
-      }
-      // decode's weighted fp16 dequant needs 16 * scale (and 12 * scale) in range: flag wider
-      wide |= (hi - lo) * (tier == 0 ? (1.0f / 3.0f) : (1.0f / 15.0f)) > 4000.0f;
-      if (tier == 0) reinterpret_cast<uint16_t*>(s_codes[warp])[r * 16 + j] = (uint16_t)packed;
-      else s_codes[warp][r * 16 + j] = packed;
-      if ((j & 3) == 0) s_meta[warp][r * 4 + (j >> 2)] = h2_as_u32(__floats2half2_rn(lo, hi));
     }
     __syncwarp();
     // 128-bit coalesced stores of the packed chunk (1 KB INT2 / 2 KB INT4) and its metadata

@@ -182,3 +182,55 @@ def test_full_size_unit_properties_32k():
     kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
     for b, h in ((0, 0), (1, 5)):
         _check_unit(cache, 0, b, h, kh, vh, wls[b]["tiers"], qh[0, b, h * m:(h + 1) * m], out[0, b, h * m:(h + 1) * m])
+
+
+def test_per_layer_pdl_launches_match_single_launch():
+    rng = np.random.default_rng(31)
+    L, B, H, m, D, N = 4, 2, 2, 4, 128, 24
+    T = N * 32 + 5
+    k = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    q = torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16)).cuda()
+    cache = batched.build_cache_batched(k, v, _search_from_tiers(rng.choice([0, 0, 1, 2], size=(B, N)).astype(np.uint8)))
+    full = cache.decode(q).float()
+    per = torch.empty_like(q)
+    for l in range(L):
+        cache.decode(q[l:l + 1], out=per[l:l + 1], layer=l, pdl=l > 0)
+    assert torch.max(torch.abs(per.float() - full)).item() < 2e-3
+    for s in (1, 3, 16, 40):  # 40 > the merge's register fast path
+        o = cache.decode(q, splits=s).float()
+        assert torch.max(torch.abs(o - full)).item() < 2e-3
+
+
+def test_exact_mode_for_wide_scales_and_large_q():
+    rng = np.random.default_rng(33)
+    L, B, H, m, D, N = 1, 2, 2, 4, 128, 8
+    T = N * 32
+    k = (rng.normal(size=(L, B, T, H, D)) * 3).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v[0, 1, :, 1, :] *= 30000 / 4  # one unit with huge V spans
+    tiers = rng.choice([0, 1], size=(B, N)).astype(np.uint8)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search_from_tiers(tiers))
+    assert cache.wide_scale_units() >= 1
+    for qscale in (1.0, 3000.0):  # |q| * scale_log2 > 1000 forces the unweighted mode too
+        q = (rng.normal(size=(L, B, H * m, D)) * qscale).astype(np.float16)
+        out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
+        for b in range(B):
+            for h in range(H):
+                _check_unit(cache, 0, b, h, k, v, tiers[b], q[0, b, h * m:(h + 1) * m], out[0, b, h * m:(h + 1) * m])
+
+
+def test_fp16_only_and_int_only_units_with_many_splits():
+    rng = np.random.default_rng(35)
+    L, B, H, m, D, N = 1, 2, 1, 4, 128, 12
+    T = N * 32 + 3
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    tiers = np.stack([np.full(N, 2, np.uint8), np.full(N, 0, np.uint8)])
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search_from_tiers(tiers))
+    assert cache.wide_scale_units() == 0
+    q = rng.normal(size=(L, B, H * m, D)).astype(np.float16)
+    for s in (1, 7, 25):
+        out = cache.decode(torch.from_numpy(q).cuda(), splits=s).float().cpu().numpy()
+        for b in range(B):
+            _check_unit(cache, 0, b, 0, k, v, tiers[b], q[0, b, :m], out[0, b, :m])

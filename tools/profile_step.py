@@ -24,14 +24,19 @@ def main():
     m = q.shape[2] // cache.H
     splits = cache.default_splits(m, 1)
     out = torch.empty_like(q)
+    for l in range(cache.L):  # warm-up outside the profiled range
+        cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
     for _ in range(args.steps):
         for l in range(cache.L):
             cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     if args.prefill:
         del cache
         torch.cuda.empty_cache()
-        bench.bench_prefill(torch, dev, steps=1)
+        bench.bench_prefill(torch, dev, steps=1, profile=True)
     torch.cuda.synchronize()
 
 
