@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
 
   // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m); warp 0 writes the
   // CTA's three sets to shared memory.
-  if (warp == 0) {
+  {
     float qv[32];
     const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
     if (g < a.m) {
@@ -639,41 +639,41 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __half22float2(u32_as_h2(w[e]));
-          qv[8 * u + 2 * e] = f.x * a.scale_log2;
-          qv[8 * u + 2 * e + 1] = f.y * a.scale_log2;
+          qv[8 * u + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
+          qv[8 * u + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
         }
       }
     } else {
 #pragma unroll
       for (int e = 0; e < 32; ++e) qv[e] = 0.f;
     }
-    float qsum = 0.f, qmaxabs = 0.f;
+    // warp w < 3 stores q-fragment set w; warp 3 stores the zero-point entry and the range flag
+    if (warp < 3) {
 #pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      qv[e] = __half2float(__float2half_rn(qv[e]));  // exactly the fp16 operand the MMA sees
-      qsum += qv[e];
-      qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
-    }
+      for (int ks = 0; ks < 8; ++ks) {
+        const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
+        const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
+        // slot weights 2^(6-j): INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1); set 2: 1
+        const float w0 = warp == 0 ? exp2f((float)(6 - (i0 <= 4 ? 2 * i0 : 2 * (i0 - 5))))
+                                   : (warp == 1 ? exp2f((float)(6 - 4 * (i0 & 1))) : 1.0f);
+        const float w1 = warp == 0 ? exp2f((float)(6 - (i1 <= 4 ? 2 * i1 : 2 * (i1 - 5))))
+                                   : (warp == 1 ? exp2f((float)(6 - 4 * (i1 & 1))) : 1.0f);
+        s_q[warp][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * w0, qv[d0 + 8] * w0)),
+                                         h2_as_u32(__floats2half2_rn(qv[d0 + 1] * w1, qv[d0 + 9] * w1)));
+      }
+    } else {
+      float qsum = 0.f, qmaxabs = 0.f;
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
-      const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
-      // INT2 slot weight 2^(j-6): j = 2i (i <= 4) or 2(i-5); INT4: j = 4(i & 1)
-      const float w20 = exp2f((float)(6 - (i0 <= 4 ? 2 * i0 : 2 * (i0 - 5))));
-      const float w21 = exp2f((float)(6 - (i1 <= 4 ? 2 * i1 : 2 * (i1 - 5))));
-      const float w40 = exp2f((float)(6 - 4 * (i0 & 1))), w41 = exp2f((float)(6 - 4 * (i1 & 1)));
-      s_q[0][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * w20, qv[d0 + 8] * w20)),
-                                    h2_as_u32(__floats2half2_rn(qv[d0 + 1] * w21, qv[d0 + 9] * w21)));
-      s_q[1][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * w40, qv[d0 + 8] * w40)),
-                                    h2_as_u32(__floats2half2_rn(qv[d0 + 1] * w41, qv[d0 + 9] * w41)));
-      s_q[2][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0], qv[d0 + 8])),
-                                    h2_as_u32(__floats2half2_rn(qv[d0 + 1], qv[d0 + 9])));
+      for (int e = 0; e < 32; ++e) {
+        qsum += qv[e];
+        qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
+      }
+      const __half qhi = __float2half_rn(qsum);
+      const __half qlo = __float2half_rn(qsum - __half2float(qhi));
+      s_q[0][8][lane] = make_uint2(h2_as_u32(__halves2half2(qhi, qlo)), 0u);
+      const bool wide = __any_sync(0xffffffffu, qmaxabs > kWideQ);
+      if (lane == 0) s_wide_q = wide;
     }
-    const __half qhi = __float2half_rn(qsum);
-    const __half qlo = __float2half_rn(qsum - __half2float(qhi));
-    s_q[0][8][lane] = make_uint2(h2_as_u32(__halves2half2(qhi, qlo)), 0u);
-    const bool wide = __any_sync(0xffffffffu, qmaxabs > kWideQ);
-    if (lane == 0) s_wide_q = wide;
   }
   __syncthreads();
   QS qs;
@@ -908,6 +908,29 @@ int32_t ckv_decode_ctas_per_sm(void) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_kernel, kDecWarps * 32, kDynSmem) != cudaSuccess) {
     (void)cudaGetLastError();
     return -1;
+  }
+  return n;
+}
+
+// Tuning probe (not part of the ABI): resident clusters of `cluster` decode CTAs.
+int32_t ckv_probe_max_clusters(int32_t cluster, int32_t grid_x) {
+  if (!ensure_decode_attr()) return -1;
+  cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid_x, 8, 8);
+  cfg.blockDim = dim3(kDecWarps * 32);
+  cfg.dynamicSmemBytes = kDynSmem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, decode_kernel, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -2;
   }
   return n;
 }
