@@ -60,46 +60,63 @@ def load_workload(ctx, seed):
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled (NVML, every 10 ms) during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML) during the timed region: NVML is opened
+    before the region starts, one sample is taken on entry, then every 5 ms, then on exit."""
+
+    BITS = {"hw_slowdown": "nvmlClocksThrottleReasonHwSlowdown",
+            "hw_thermal_slowdown": "nvmlClocksThrottleReasonHwThermalSlowdown",
+            "sw_thermal_slowdown": "nvmlClocksThrottleReasonSwThermalSlowdown",
+            "sw_power_cap": "nvmlClocksThrottleReasonSwPowerCap"}
+    DEFAULT_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.samples = []
+        self.error = None
         self._stop = threading.Event()
         self._t = None
-
-    def _run(self):
+        self._nv = self._hdl = None
         try:
             import pynvml as nv
             nv.nvmlInit()
-            hdl = nv.nvmlDeviceGetHandleByIndex(self.index)
-            mx = nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM)
-            bits = {"hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
-                    "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
-                    "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
-                    "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4)}
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(hdl)
-                self.samples.append((sm, mx, [k for k, b in bits.items() if r & b]))
-                self._stop.wait(0.01)
+            self._nv = nv
+            self._hdl = nv.nvmlDeviceGetHandleByIndex(index)
+            self._max = nv.nvmlDeviceGetMaxClockInfo(self._hdl, nv.NVML_CLOCK_SM)
+            self._bits = {k: getattr(nv, a, self.DEFAULT_BITS[k]) for k, a in self.BITS.items()}
         except Exception as exc:  # no NVML: record why
-            self.samples.append((None, None, [f"unsampled: {type(exc).__name__}"]))
+            self.error = f"unsampled: {type(exc).__name__}"
+
+    def _sample(self):
+        nv = self._nv
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(self._hdl, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._hdl)
+            self.samples.append((sm, self._max, [k for k, b in self._bits.items() if r & b]))
+        except Exception as exc:
+            self.error = f"unsampled: {type(exc).__name__}"
+
+    def _run(self):
+        while not self._stop.wait(0.005):
+            self._sample()
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self._nv is not None:
+            self._sample()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._stop.set()
+            self._t.join(timeout=10)
+            self._sample()
 
     def summary(self):
         sm = [s[0] for s in self.samples if s[0] is not None]
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None,
-                    "reasons": sorted({r for s in self.samples for r in s[2]}) or ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.error or "unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples if s[1]),
                 "reasons": sorted({r for s in self.samples for r in s[2]}), "samples": len(sm)}
 

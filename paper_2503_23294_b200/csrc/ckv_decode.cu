@@ -42,9 +42,9 @@ constexpr int kStages = 4;
 //         KM @2048, VM @2560
 constexpr int kStageBytes = 3072;
 constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 48 KB per CTA
-constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l
+constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l (partial_out / cross-rank format)
+constexpr int kWsStride = kHeadDim + 4;    // split workspace rows: acc[128], m, l, pad (16-B rows)
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
-constexpr int kMaxSplitsFast = 16;         // split merge keeps up to 16 partials in registers
 
 struct DecArgs {
   const uint16_t* q;
@@ -60,6 +60,23 @@ struct DecArgs {
   float* partial_out;   // [L][B][H*m][130] or null
   uint32_t zero;        // runtime 0: keeps the fp16 magic exponents in registers (see Magic)
 };
+
+// Optional per-CTA timeline (tuning aid, not part of the ABI): when set, every CTA appends 16
+// int64: globaltimer at start, after the PDL wait, after q staging, after warp 0's tiles, at
+// exit; smid, linear block index, q pointer (launch id); after all warps' tiles, before the
+// arrival atomic, after it, is-last; per-warp tile end times.
+__device__ int64_t* g_trace = nullptr;
+__device__ unsigned long long g_trace_n = 0;
+__device__ __forceinline__ int64_t gtime() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 struct Seq8 {
   int off2, len2, off4, len4, off_fp, len_fp, tail_src, ctx;
@@ -129,9 +146,30 @@ struct DeqC {
   __half2 sc;  // (sc_lo_half, sc_hi_half)
   __half2 nm;  // -16 * sc  (exact: power-of-two multiple)
 };
-__device__ __forceinline__ DeqC make_deq(float s0, float s1) {
+
+// Scale constants straight from fp16 metadata with half2 arithmetic: span = hi - lo (one
+// rounding), nm = -16 sc (exact).  The rounding of fp16(1/qmax) would bias every scale by the
+// same relative amount (2.4e-4 for 1/3), and a constant bias does not average out over a long
+// context.  K: sc = span * fp16(1/qmax), and the constant factor 1 / (qmax fp16(1/qmax)) is
+// folded into that tier's q fragments.  V: sc = span * c_hi + span * c_lo (c_hi + c_lo = 1/qmax
+// to 2^-22), one rounding.  K: one (lo, hi) word -> that token's constants in both halves;
+// V: two words (tokens t0, t1) -> (t0, t1) constants.
+__device__ __forceinline__ float kscale_fold(float inv_q) {  // 1 / (qmax * fp16(1/qmax))
+  return inv_q / __half2float(__float2half_rn(inv_q));
+}
+__device__ __forceinline__ DeqC kdeq(uint32_t meta, __half2 inv_q) {
+  const __half2 h = u32_as_h2(meta);
   DeqC d;
-  d.sc = __floats2half2_rn(s0, s1);
+  d.sc = __hmul2(__hsub2(__high2half2(h), __low2half2(h)), inv_q);
+  d.nm = __hmul2(d.sc, __float2half2_rn(-16.0f));
+  return d;
+}
+__device__ __forceinline__ DeqC vdeq(uint32_t lo01, uint32_t hi01, float inv_q) {
+  const __half c_hi = __float2half_rn(inv_q);
+  const __half c_lo = __float2half_rn(inv_q - __half2float(c_hi));
+  const __half2 span = __hsub2(u32_as_h2(hi01), u32_as_h2(lo01));
+  DeqC d;
+  d.sc = __hfma2(span, __half2half2(c_hi), __hmul2(span, __half2half2(c_lo)));
   d.nm = __hmul2(d.sc, __float2half2_rn(-16.0f));
   return d;
 }
@@ -226,13 +264,13 @@ __device__ __forceinline__ void qk_int2(uint32_t sl, const QS& qs, uint32_t mg, 
   const uint4 kk = lds128(sl);  // (tok g: words 2c, 2c+1), (tok g+8: words 2c, 2c+1)
   const uint2 kmm = lds64(sl + 1024);
   constexpr float iq = 1.0f / 3.0f;
-  const float sk0 = meta_scale(kmm.x, iq), sk1 = meta_scale(kmm.y, iq);
 
   float s2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int e = 0; e < 4; ++e) s[e] = 0.f;
   if (!EXACT) {
-    const DeqC dk0 = make_deq(sk0, sk0), dk1 = make_deq(sk1, sk1);
+    const __half2 iq2 = __float2half2_rn(iq);
+    const DeqC dk0 = kdeq(kmm.x, iq2), dk1 = kdeq(kmm.y, iq2);
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
       const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
@@ -246,7 +284,7 @@ __device__ __forceinline__ void qk_int2(uint32_t sl, const QS& qs, uint32_t mg, 
     }
     mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
   } else {
-    const __half2 sc0 = __float2half2_rn(sk0), sc1 = __float2half2_rn(sk1);
+    const __half2 sc0 = __float2half2_rn(meta_scale(kmm.x, iq)), sc1 = __float2half2_rn(meta_scale(kmm.y, iq));
     const __half2 lo0 = u32_as_h2(prmt(kmm.x, kmm.x, 0x1010)), lo1 = u32_as_h2(prmt(kmm.y, kmm.y, 0x1010));
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
@@ -268,12 +306,11 @@ __device__ __forceinline__ void pv_int2(uint32_t sl, uint32_t mg, WarpState& st,
   const uint4 vv = lds128(sl + 512);
   const uint4 vmm = lds128(sl + 1536);
   constexpr float iq = 1.0f / 3.0f;
-  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
-  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
   const uint32_t c01lo = prmt(vv.x, vv.y, 0x5410), c01hi = prmt(vv.x, vv.y, 0x7632);
   const uint32_t c23lo = prmt(vv.z, vv.w, 0x5410), c23hi = prmt(vv.z, vv.w, 0x7632);
   if (!EXACT) {
-    const DeqC d01 = make_deq(sv0, sv1), d23 = make_deq(sv2, sv3);
+    const uint32_t l01 = prmt(vmm.x, vmm.y, 0x5410), l23 = prmt(vmm.z, vmm.w, 0x5410);
+    const DeqC d01 = vdeq(l01, prmt(vmm.x, vmm.y, 0x7632), iq), d23 = vdeq(l23, prmt(vmm.z, vmm.w, 0x7632), iq);
     const uint32_t a8 = c01lo >> 8, b8 = c01hi >> 8, e8 = c23lo >> 8, f8 = c23hi >> 8;
     // m-tile mt uses code mt of each 8-code half: j = 2 (mt & 3), from x (mt < 4) or x >> 8
 #define PV2(MT)                                                                                     \
@@ -284,9 +321,10 @@ __device__ __forceinline__ void pv_int2(uint32_t sl, uint32_t mg, WarpState& st,
   }
     PV2(0) PV2(1) PV2(2) PV2(3) PV2(4) PV2(5) PV2(6) PV2(7)
 #undef PV2
-    lo_mma(st, prmt(vmm.x, vmm.y, 0x5410), prmt(vmm.z, vmm.w, 0x5410), bp0, bp1);
+    lo_mma(st, l01, l23, bp0, bp1);
   } else {
-    const __half2 sc01 = __floats2half2_rn(sv0, sv1), sc23 = __floats2half2_rn(sv2, sv3);
+    const __half2 sc01 = __floats2half2_rn(meta_scale(vmm.x, iq), meta_scale(vmm.y, iq));
+    const __half2 sc23 = __floats2half2_rn(meta_scale(vmm.z, iq), meta_scale(vmm.w, iq));
     const __half2 lo01 = u32_as_h2(prmt(vmm.x, vmm.y, 0x5410)), lo23 = u32_as_h2(prmt(vmm.z, vmm.w, 0x5410));
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
@@ -305,14 +343,14 @@ __device__ __forceinline__ void qk_int4(uint32_t sl, const QS& qs, uint32_t mg, 
   const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);  // group c of tok g / tok g+8
   const uint2 kmm = lds64(sl + 2048);
   constexpr float iq = 1.0f / 15.0f;
-  const float sk0 = meta_scale(kmm.x, iq), sk1 = meta_scale(kmm.y, iq);
 
   float s2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int e = 0; e < 4; ++e) s[e] = 0.f;
   const uint32_t kwa[4] = {kw0.x, kw0.y, kw0.z, kw0.w}, kwb[4] = {kw1.x, kw1.y, kw1.z, kw1.w};
   if (!EXACT) {
-    const DeqC dk0 = make_deq(sk0, sk0), dk1 = make_deq(sk1, sk1);
+    const __half2 iq2 = __float2half2_rn(iq);
+    const DeqC dk0 = kdeq(kmm.x, iq2), dk1 = kdeq(kmm.y, iq2);
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
       // pairs (d0, d0+8) = (word 2blk code i, word 2blk+1 code i)
@@ -328,7 +366,7 @@ __device__ __forceinline__ void qk_int4(uint32_t sl, const QS& qs, uint32_t mg, 
     }
     mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
   } else {
-    const __half2 sc0 = __float2half2_rn(sk0), sc1 = __float2half2_rn(sk1);
+    const __half2 sc0 = __float2half2_rn(meta_scale(kmm.x, iq)), sc1 = __float2half2_rn(meta_scale(kmm.y, iq));
     const __half2 lo0 = u32_as_h2(prmt(kmm.x, kmm.x, 0x1010)), lo1 = u32_as_h2(prmt(kmm.y, kmm.y, 0x1010));
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
@@ -355,15 +393,14 @@ __device__ __forceinline__ void pv_int4(uint32_t sl, uint32_t mg, WarpState& st,
   const uint4 va = lds128(sl + 1024), vb = lds128(sl + 1536);
   const uint4 vmm = lds128(sl + 2560);
   constexpr float iq = 1.0f / 15.0f;
-  const float sv0 = meta_scale(vmm.x, iq), sv1 = meta_scale(vmm.y, iq);
-  const float sv2 = meta_scale(vmm.z, iq), sv3 = meta_scale(vmm.w, iq);
+  const uint32_t l01 = prmt(vmm.x, vmm.y, 0x5410), l23 = prmt(vmm.z, vmm.w, 0x5410);
   // V (tok 2c | 2c+1) and (2c+8 | 2c+9) for d = 16g + mt (word 2g) and 16g + 8 + mt (word 2g+1)
   const uint32_t x01[4] = {prmt(va.x, va.z, 0x5410), prmt(va.x, va.z, 0x7632),
                            prmt(va.y, va.w, 0x5410), prmt(va.y, va.w, 0x7632)};
   const uint32_t x23[4] = {prmt(vb.x, vb.z, 0x5410), prmt(vb.x, vb.z, 0x7632),
                            prmt(vb.y, vb.w, 0x5410), prmt(vb.y, vb.w, 0x7632)};
   if (!EXACT) {
-    const DeqC d01 = make_deq(sv0, sv1), d23 = make_deq(sv2, sv3);
+    const DeqC d01 = vdeq(l01, prmt(vmm.x, vmm.y, 0x7632), iq), d23 = vdeq(l23, prmt(vmm.z, vmm.w, 0x7632), iq);
     // m-tile mt: code k = mt & 3 of x[mt >> 2] sits at bits 4k; move it to j = 2k (>> 2k)
 #define PV4(MT)                                                                                     \
   {                                                                                                 \
@@ -374,10 +411,11 @@ __device__ __forceinline__ void pv_int4(uint32_t sl, uint32_t mg, WarpState& st,
   }
     PV4(0) PV4(1) PV4(2) PV4(3) PV4(4) PV4(5) PV4(6) PV4(7)
 #undef PV4
-    lo_mma(st, prmt(vmm.x, vmm.y, 0x5410), prmt(vmm.z, vmm.w, 0x5410), bp0, bp1);
+    lo_mma(st, l01, l23, bp0, bp1);
   } else {
-    const __half2 sc01 = __floats2half2_rn(sv0, sv1), sc23 = __floats2half2_rn(sv2, sv3);
-    const __half2 lo01 = u32_as_h2(prmt(vmm.x, vmm.y, 0x5410)), lo23 = u32_as_h2(prmt(vmm.z, vmm.w, 0x5410));
+    const __half2 sc01 = __floats2half2_rn(meta_scale(vmm.x, iq), meta_scale(vmm.y, iq));
+    const __half2 sc23 = __floats2half2_rn(meta_scale(vmm.z, iq), meta_scale(vmm.w, iq));
+    const __half2 lo01 = u32_as_h2(l01), lo23 = u32_as_h2(l23);
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
       const int k = mt & 3, u = mt >> 2;
@@ -578,34 +616,35 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   const int split = blockIdx.x, h = blockIdx.y;
+  int64_t* const trace = g_trace;
+  int64_t tr[12];
+  __shared__ int64_t s_tend[kDecWarps];
+  tr[11] = 0;
+  if (trace) tr[0] = gtime();
   const int l = blockIdx.z / a.B, b = blockIdx.z % a.B;
   // Segment lengths of the quantized arenas are immutable after the build; len_fp grows with
   // decode appends and is read only after the programmatic-dependent-launch wait below.
   const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
   const int off2 = s0.x, off4 = s0.z, off_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 4];
   const int n2t = s0.y / kTile, n4t = s0.w / kTile;
-  // time-balanced split of the quantized tiles (INT2 || INT4): an INT2 tile (1.5 KB) and an
-  // INT4 tile (2.5 KB) cost about the same issue slots (dequant-bound), so weigh them ~equally.
-  // FP16-region tiles are split separately.
-  const int64_t c2 = 100, c4 = 110;
-  const int64_t qtot = n2t * c2 + n4t * c4;
-  auto qtile_at = [&](int64_t x) -> int {  // first tile whose start cost >= x
-    if (x <= n2t * c2) return (int)((x + c2 - 1) / c2);
-    x -= n2t * c2;
-    return n2t + (int)min((int64_t)n4t, (x + c4 - 1) / c4);
-  };
-  const int q_begin = qtile_at(qtot * split / a.splits);
-  const int q_end = qtile_at(qtot * (split + 1) / a.splits);
+  // Split of the quantized tiles: every CTA takes the same 1/splits share of the INT2 tiles
+  // AND of the INT4 tiles (and of the FP16-region tiles below), so all CTAs carry the same
+  // mix and finish together whatever the relative per-tile costs are.
+  const int a2 = (int)((int64_t)n2t * split / a.splits), b2 = (int)((int64_t)n2t * (split + 1) / a.splits);
+  const int a4 = (int)((int64_t)n4t * split / a.splits), b4 = (int)((int64_t)n4t * (split + 1) / a.splits);
+  const int cnt2 = b2 - a2;               // local tiles [0, cnt2) are INT2, [cnt2, nloc) INT4
+  const int nloc = cnt2 + (b4 - a4);
   const int64_t unit = (int64_t)l * a.H + h;
   TileSrc src;
-  src.k2 = reinterpret_cast<const char*>(a.K.codes2 + (unit * a.K.rows2 + off2) * 8);
-  src.k2m = reinterpret_cast<const char*>(a.K.meta2 + (unit * a.K.rows2 + off2) * 4);
-  src.v2 = reinterpret_cast<const char*>(a.V.codes2 + (unit * a.V.rows2 + off2) * 8);
-  src.v2m = reinterpret_cast<const char*>(a.V.meta2 + (unit * a.V.rows2 + off2) * 4);
-  src.k4 = reinterpret_cast<const char*>(a.K.codes4 + (unit * a.K.rows4 + off4) * 16);
-  src.k4m = reinterpret_cast<const char*>(a.K.meta4 + (unit * a.K.rows4 + off4) * 4);
-  src.v4 = reinterpret_cast<const char*>(a.V.codes4 + (unit * a.V.rows4 + off4) * 16);
-  src.v4m = reinterpret_cast<const char*>(a.V.meta4 + (unit * a.V.rows4 + off4) * 4);
+  const int64_t r2 = off2 + (int64_t)a2 * kTile, r4 = off4 + (int64_t)a4 * kTile;  // first rows
+  src.k2 = reinterpret_cast<const char*>(a.K.codes2 + (unit * a.K.rows2 + r2) * 8);
+  src.k2m = reinterpret_cast<const char*>(a.K.meta2 + (unit * a.K.rows2 + r2) * 4);
+  src.v2 = reinterpret_cast<const char*>(a.V.codes2 + (unit * a.V.rows2 + r2) * 8);
+  src.v2m = reinterpret_cast<const char*>(a.V.meta2 + (unit * a.V.rows2 + r2) * 4);
+  src.k4 = reinterpret_cast<const char*>(a.K.codes4 + (unit * a.K.rows4 + r4) * 16);
+  src.k4m = reinterpret_cast<const char*>(a.K.meta4 + (unit * a.K.rows4 + r4) * 4);
+  src.v4 = reinterpret_cast<const char*>(a.V.codes4 + (unit * a.V.rows4 + r4) * 16);
+  src.v4m = reinterpret_cast<const char*>(a.V.meta4 + (unit * a.V.rows4 + r4) * 4);
   const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
   const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
   LaneSrc lo;
@@ -614,13 +653,14 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   lo.v = 2 * c * 32 + 4 * g;      // V row 2c, word g (INT2)
   lo.vm = 2 * c * 16 + 4 * (g >> 1);
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
-  prologue(q_begin, q_end, n2t, src, lo, ring_l, warp);
+  prologue(0, nloc, cnt2, src, lo, ring_l, warp);
 
   // Everything above touched only build-time data.  q, the FP16 region and len_fp may come
   // from the preceding kernel on the stream: wait for it (no-op without PDL), and let the next
   // decode launch (next layer) start its own prologue as soon as SMs free up.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
+  if (trace) tr[1] = gtime();
   const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 5];
   const int nft = (len_fp + kTile - 1) / kTile;
   const int f_begin = (int)((int64_t)nft * split / a.splits);
@@ -658,8 +698,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
                                    : (warp == 1 ? exp2f((float)(6 - 4 * (i0 & 1))) : 1.0f);
         const float w1 = warp == 0 ? exp2f((float)(6 - (i1 <= 4 ? 2 * i1 : 2 * (i1 - 5))))
                                    : (warp == 1 ? exp2f((float)(6 - 4 * (i1 & 1))) : 1.0f);
-        s_q[warp][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * w0, qv[d0 + 8] * w0)),
-                                         h2_as_u32(__floats2half2_rn(qv[d0 + 1] * w1, qv[d0 + 9] * w1)));
+        // INT2 / INT4 sets also carry the fold of the fp16(1/qmax) rounding (see kdeq)
+        const float fold = warp == 0 ? kscale_fold(1.0f / 3.0f) : (warp == 1 ? kscale_fold(1.0f / 15.0f) : 1.0f);
+        const float x0 = w0 * fold, x1 = w1 * fold;
+        s_q[warp][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0)),
+                                         h2_as_u32(__floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1)));
       }
     } else {
       float qsum = 0.f, qmaxabs = 0.f;
@@ -676,6 +719,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     }
   }
   __syncthreads();
+  if (trace) tr[2] = gtime();
   QS qs;
   qs.base = (uint32_t)__cvta_generic_to_shared(&s_q[0][0][0]) + 8 * lane;
   const int64_t fidx = unit * a.B + b;  // span flags are [L][H][B]
@@ -691,9 +735,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.lsum[0] = st.lsum[1] = 0.f;
 
   if (exact) {
-    run_tiles<true>(q_begin, q_end, f_begin, f_end, n2t, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<true>(0, nloc, f_begin, f_end, cnt2, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
   } else {
-    run_tiles<false>(q_begin, q_end, f_begin, f_end, n2t, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<false>(0, nloc, f_begin, f_end, cnt2, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
     // undo the V m-tile weights 2^(2(mt&3) - 6)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
@@ -702,6 +746,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     }
   }
 
+  if (trace) { tr[3] = gtime(); if (lane == 0) s_tend[warp] = tr[3]; }
   // finish the warp: fold the zero-point term, reduce row sums over the 8 row-groups
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
@@ -714,6 +759,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
   }
   __syncthreads();  // ring -> merge buffer reuse
+  if (trace) tr[8] = gtime();
   float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0][0]);
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
@@ -754,16 +800,28 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
             __half_as_ushort(__float2half_rn(acc / lsum));
       }
     } else {
-      float* dst = a.ws + (row * a.splits + split) * kPartStride;
+      float* dst = a.ws + (row * a.splits + split) * kWsStride;
       dst[d] = acc;
       if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
     }
   }
-  if (a.splits == 1) return;
+  auto trace_out = [&]() {
+    if (trace && threadIdx.x == 0) {
+      tr[4] = gtime();
+      int64_t* dst = trace + 16 * atomicAdd(&g_trace_n, 1ull);
+      for (int i = 0; i < 5; ++i) dst[i] = tr[i];
+      for (int i = 8; i < 12; ++i) dst[i] = tr[i];
+      for (int i = 0; i < kDecWarps; ++i) dst[12 + i] = s_tend[i];
+      dst[5] = smid(); dst[6] = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      dst[7] = (int64_t)a.q;
+    }
+  };
+  if (a.splits == 1) { trace_out(); return; }
   // split-KV: the last CTA of this unit to arrive merges all partials (in-launch, no 2nd
   // kernel).  The CTA barrier orders every thread's partial stores before thread 0's
   // device-scope release RMW; the acquiring side sees them after its own barrier.
   __syncthreads();
+  if (trace) tr[9] = gtime();
   if (threadIdx.x == 0) {
     cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[((int64_t)l * a.B + b) * a.H + h]);
     const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
@@ -771,39 +829,34 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     if (s_last) ctr.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
   }
   __syncthreads();
-  if (!s_last) return;
+  if (trace) { tr[10] = gtime(); tr[11] = s_last; }
+  if (!s_last) { trace_out(); return; }
+  // All m x splits partial rows of this unit are contiguous in the workspace: stage them in
+  // shared memory with every 16-B copy in flight at once (one L2 round trip), then merge.
+  const int64_t row0 = ((int64_t)l * a.B + b) * Hq + hq0;
+  const float* p0 = a.ws + row0 * a.splits * kWsStride;
+  const int nrows = a.m * a.splits;
+  float* s_part = reinterpret_cast<float*>(&s_ring[0][0][0]);
+  if (nrows * kWsStride * (int)sizeof(float) <= kDynSmem) {
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_part);
+    const int nvec = nrows * kWsStride / 4;
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) cp_async16(sbase + 16 * i, p0 + 4 * i);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+  } else {
+    s_part = nullptr;
+  }
   for (int qi = 0; qi < a.m; ++qi) {
-    const int64_t row = ((int64_t)l * a.B + b) * Hq + hq0 + qi;
-    const float* p = a.ws + row * a.splits * kPartStride;
-    float mv[kMaxSplitsFast], lv[kMaxSplitsFast], av[kMaxSplitsFast];
+    const int64_t row = row0 + qi;
+    const float* p = s_part ? s_part + qi * a.splits * kWsStride : a.ws + row * a.splits * kWsStride;
     float ms = -INFINITY, acc = 0.f, lsum = 0.f;
-    if (a.splits <= kMaxSplitsFast) {
-#pragma unroll
-      for (int s = 0; s < kMaxSplitsFast; ++s) {  // all loads in flight at once
-        if (s < a.splits) {
-          mv[s] = __ldcg(p + s * kPartStride + kHeadDim);
-          lv[s] = __ldcg(p + s * kPartStride + kHeadDim + 1);
-          av[s] = __ldcg(p + s * kPartStride + d);
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < kMaxSplitsFast; ++s) if (s < a.splits) ms = fmaxf(ms, mv[s]);
-#pragma unroll
-      for (int s = 0; s < kMaxSplitsFast; ++s) {
-        if (s < a.splits) {
-          const float f = mv[s] == -INFINITY ? 0.f : fast_exp2(mv[s] - ms);
-          acc += f * av[s];
-          lsum += f * lv[s];
-        }
-      }
-    } else {
-      for (int s = 0; s < a.splits; ++s) ms = fmaxf(ms, __ldcg(p + s * kPartStride + kHeadDim));
-      for (int s = 0; s < a.splits; ++s) {
-        const float mw = __ldcg(p + s * kPartStride + kHeadDim);
-        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-        acc += f * __ldcg(p + s * kPartStride + d);
-        lsum += f * __ldcg(p + s * kPartStride + kHeadDim + 1);
-      }
+    for (int s = 0; s < a.splits; ++s) ms = fmaxf(ms, p[s * kWsStride + kHeadDim]);
+    for (int s = 0; s < a.splits; ++s) {
+      const float mw = p[s * kWsStride + kHeadDim];
+      const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+      acc += f * p[s * kWsStride + d];
+      lsum += f * p[s * kWsStride + kHeadDim + 1];
     }
     if (a.partial_out) {
       float* dst = a.partial_out + row * kPartStride;
@@ -814,6 +867,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
           __half_as_ushort(__float2half_rn(acc / lsum));
     }
   }
+  trace_out();
 }
 
 // Cross-rank merge of gathered partials [P][rows][130] -> out fp16 [rows][128].
@@ -856,7 +910,7 @@ int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_hea
   const int64_t units = (int64_t)layers * batch * kv_heads;
   const int64_t counters = cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256;
   if (splits <= 1) return counters;
-  return counters + units * m * splits * kPartStride * (int64_t)sizeof(float);
+  return counters + units * m * splits * kWsStride * (int64_t)sizeof(float);
 }
 
 int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
@@ -910,6 +964,18 @@ int32_t ckv_decode_ctas_per_sm(void) {
     return -1;
   }
   return n;
+}
+
+// Tuning aid (not part of the ABI): point the decode timeline at buf (null disables) and
+// reset its counter.
+int32_t ckv_decode_set_trace(int64_t* buf) {
+  unsigned long long z = 0;
+  if (cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return CKV_ERR_CUDA;
+  }
+  return CKV_OK;
 }
 
 // Tuning probe (not part of the ABI): resident clusters of `cluster` decode CTAs.
