@@ -135,13 +135,17 @@ int32_t ckv_assign_tiers(const double* scores, const double* thresholds,
                          int32_t* flags, void* stream);
 
 /* Arena set for one of K or V over [layers, kv_heads]; rows are concatenated over the
- * batch (varlen).  Row formats match the reference's packing bit for bit (one D=128 row
- * packs into 8 (INT2) / 16 (INT4) little-endian u32 words, _numpy.py:70-86). */
+ * batch (varlen; every segment starts at a multiple of 32 rows).  The quantized arenas are
+ * TILE-NATIVE: each 16-row tile holds exactly the bits of the reference's row packing (one
+ * D=128 row packs into 8 (INT2) / 16 (INT4) little-endian u32 words, _numpy.py:70-86) and
+ * the rows' fp16 (lo, hi) group metadata, permuted in 16-bit pieces into the order the
+ * decode kernel's MMA fragments consume them (layout functions tile_off_* in
+ * csrc/ckv_common.cuh; K and V tiles differ).  ckv_arena_export restores reference rows. */
 typedef struct ckv_arena {
-  uint32_t* codes2;   /* u32 [L][H][rows2][8]                                   */
-  uint32_t* meta2;    /* half2 (lo, hi) [L][H][rows2][4]                         */
-  uint32_t* codes4;   /* u32 [L][H][rows4][16]                                  */
-  uint32_t* meta4;    /* half2 (lo, hi) [L][H][rows4][4]                         */
+  uint32_t* codes2;   /* [L][H][rows2 / 16] tiles of 512 B  (16 rows x 8 u32)    */
+  uint32_t* meta2;    /* [L][H][rows2 / 16] tiles of 256 B  (16 rows x 4 (lo,hi)) */
+  uint32_t* codes4;   /* [L][H][rows4 / 16] tiles of 1024 B (16 rows x 16 u32)   */
+  uint32_t* meta4;    /* [L][H][rows4 / 16] tiles of 256 B                       */
   uint16_t* fp;       /* fp16 [L][H][rows_fp][128] (FP16 chunks || tail || decode) */
   uint32_t* span_flags; /* u32 [L][H][B], zero-filled before build: bit0/bit1 set when an
                            INT2/INT4 group's scale exceeds 4000 (decode then runs that unit in
@@ -182,6 +186,13 @@ int32_t ckv_append_tokens(const uint16_t* k_new, const uint16_t* v_new, int32_t 
  * in f64.  Used to export arenas as reference QuantizedBlocks (quantizer.py:20-57). */
 int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, double* scales,
                         double* zero_points, void* stream);
+
+/* Tile-native arena rows -> reference format (export / verification, quantizer.py:20-57):
+ * `rows` (a multiple of 16) rows starting at a tile boundary of one arena (codes + meta of
+ * the K arena when is_v == 0, of the V arena otherwise) -> out_codes u32 [rows][8 or 16]
+ * (pack_codes row format, _numpy.py:70-86) and out_meta half2 (lo, hi) [rows][4]. */
+int32_t ckv_arena_export(const uint32_t* codes, const uint32_t* meta, int64_t rows, int32_t bits,
+                         int32_t is_v, uint32_t* out_codes, uint32_t* out_meta, void* stream);
 
 /* (3) Mixed-precision decode attention (attention.mixed_decode_attention, attention.py:63-90,
  * for every (layer, sequence, kv-head) unit at once).  q fp16 [L][B][H*m][128] (strides

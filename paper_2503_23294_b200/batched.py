@@ -9,12 +9,14 @@ Pipeline (one launch each, everything stays in HBM):
   cache.append(k_new, v_new)    -> decode-token append               (kv_store.py:135-148)
 
 HBM layout (per K and V, see include/ckv.h ckv_arena):
-  codes2 u32 [L][H][rows2][8]     meta2 half2(lo,hi) [L][H][rows2][4]
-  codes4 u32 [L][H][rows4][16]    meta4 half2(lo,hi) [L][H][rows4][4]
+  codes2 [L][H][rows2/16] tiles of 512 B     meta2 [L][H][rows2/16] tiles of 256 B
+  codes4 [L][H][rows4/16] tiles of 1024 B    meta4 [L][H][rows4/16] tiles of 256 B
   fp     fp16 [L][H][rows_fp][128]
 Rows of one sequence are contiguous inside each arena (varlen concatenation over the
-batch); the per-sequence table seq i32 [B][8] holds the offsets and lengths.  Packed rows
-are bit-identical to the reference's pack_codes of the same rows.
+batch); the per-sequence table seq i32 [B][8] holds the offsets and lengths.  Quantized
+tiles hold exactly the bits of the reference's pack_codes rows and (lo, hi) metadata,
+permuted into the decode kernel's fragment order (tile-native layout, csrc/ckv_common.cuh);
+export_unit restores reference rows on the device (ckv_arena_export).
 """
 
 from __future__ import annotations
@@ -249,8 +251,9 @@ class BatchedKVCache:
 
     # -- export to the reference per-head format ------------------------------------------
     def export_unit(self, layer, seq, head, perm=None):
-        """The reference-format ChunkedKVCache of one unit (kv_store.py:24-166): packed words are
-        the arena rows verbatim, f64 scale/zero_point expanded from (lo, hi) on the device."""
+        """The reference-format ChunkedKVCache of one unit (kv_store.py:24-166): packed words and
+        (lo, hi) metadata gathered back from the tile-native arenas to reference rows, f64
+        scale/zero_point expanded from (lo, hi), all on the device."""
         s = self.seq_host[seq]
         off2, len2, off4, len4, offf, lenf, _, ctx = (int(x) for x in s)
 
@@ -258,8 +261,12 @@ class BatchedKVCache:
             codes = t["codes2" if bits == 2 else "codes4"][layer, head]
             meta = t["meta2" if bits == 2 else "meta4"][layer, head]
             off, rows = (off2, len2) if bits == 2 else (off4, len4)
-            packed = codes[off:off + rows].reshape(-1).contiguous()
-            mt = meta[off:off + rows].reshape(-1).contiguous()
+            packed = torch.empty((rows, codes.shape[1]), dtype=torch.int32, device=self.device)
+            mt = torch.empty((rows, 4), dtype=torch.int32, device=self.device)
+            _lib.call("ckv_arena_export", _lib.ptr(codes[off:]), _lib.ptr(meta[off:]), rows, bits,
+                      int(which == "v"), _lib.ptr(packed), _lib.ptr(mt), _lib.stream())
+            packed = packed.reshape(-1)
+            mt = mt.reshape(-1)
             sc = torch.empty(mt.numel(), dtype=torch.float64, device=self.device)
             zp = torch.empty(mt.numel(), dtype=torch.float64, device=self.device)
             _lib.call("ckv_expand_meta", _lib.ptr(mt), mt.numel(), bits, _lib.ptr(sc), _lib.ptr(zp),

@@ -54,4 +54,47 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// ---- Tile-native arena layout ----------------------------------------------------------
+// The quantized arenas are stored in 16-row tiles whose bytes are laid out in the order the
+// decode kernel's MMA fragments consume them (lane-ordered 16-byte slots), so a tile moves
+// HBM -> shared memory with fully coalesced 16-byte copies and every fragment read is one
+// conflict-free shared load with no shuffling.  Tile t of a segment covers arena rows
+// [16t, 16t+16) (segments start at multiples of 32 rows).  Within a tile, rt = row % 16,
+// w = 32-bit word of the reference row packing (_numpy.py:70-86: INT2 w = 0..7, INT4 w =
+// 0..15), hf = 16-bit half of that word; metadata (lo, hi) of group G has hf 0 = lo, 1 = hi.
+// The functions give the byte offset of that 16-bit piece inside its tile; the reference row
+// format is recovered exactly by the inverse gather (ckv_arena_export).
+constexpr int kTileRows = 16;
+constexpr int kTileBytes2 = 512;    // INT2 codes tile (16 rows x 32 B)
+constexpr int kTileBytes4 = 1024;   // INT4 codes tile (16 rows x 64 B)
+constexpr int kTileBytesMeta = 256; // metadata tile (16 rows x 4 groups x (lo, hi))
+
+// K INT2: lane (g, c) = [tok g: w 2c, 2c+1 | tok g+8: w 2c, 2c+1]
+__host__ __device__ __forceinline__ int tile_off_k2(int rt, int w, int hf) {
+  return ((rt & 7) * 4 + (w >> 1)) * 16 + (rt >> 3) * 8 + (w & 1) * 4 + hf * 2;
+}
+// V INT2: lane (g, c) = [(w g: lo half of tok 2c, 2c+1), (hi halves), same for tok 2c+8, 2c+9]
+__host__ __device__ __forceinline__ int tile_off_v2(int rt, int w, int hf) {
+  return (w * 4 + ((rt & 7) >> 1)) * 16 + ((rt >> 3) * 2 + hf) * 4 + (rt & 1) * 2;
+}
+// K INT4: rows g / g+8 in two 512-B halves; lane (g, c) = group c as
+//   [(lo w4c, lo w4c+1), (hi w4c, hi w4c+1), (lo w4c+2, lo w4c+3), (hi w4c+2, hi w4c+3)]
+__host__ __device__ __forceinline__ int tile_off_k4(int rt, int w, int hf) {
+  const int wi = w & 3;
+  return (rt >> 3) * 512 + ((rt & 7) * 4 + (w >> 2)) * 16 + ((wi >> 1) * 2 + hf) * 4 + (wi & 1) * 2;
+}
+// V INT4: toks 2c, 2c+1 / 2c+8, 2c+9 in two 512-B halves; lane (g, c) =
+//   [(lo w2g of tok 2c, 2c+1), (hi w2g ...), (lo w2g+1 ...), (hi w2g+1 ...)]
+__host__ __device__ __forceinline__ int tile_off_v4(int rt, int w, int hf) {
+  return (rt >> 3) * 512 + ((w >> 1) * 4 + ((rt & 7) >> 1)) * 16 + ((w & 1) * 2 + hf) * 4 + (rt & 1) * 2;
+}
+// K metadata: lane (g, c) = [(lo, hi) tok g group c, (lo, hi) tok g+8 group c]
+__host__ __device__ __forceinline__ int tile_off_km(int rt, int G, int hf) {
+  return ((rt & 7) * 4 + G) * 8 + (rt >> 3) * 4 + hf * 2;
+}
+// V metadata: entry (G, c) = [(lo tok 2c, 2c+1), (hi tok 2c, 2c+1), (lo 2c+8, 2c+9), (hi ...)]
+__host__ __device__ __forceinline__ int tile_off_vm(int rt, int G, int hf) {
+  return (G * 4 + ((rt & 7) >> 1)) * 16 + ((rt >> 3) * 2 + hf) * 4 + (rt & 1) * 2;
+}
+
 }  // namespace ckv

@@ -34,14 +34,10 @@ namespace ckv {
 constexpr int kDecWarps = 4;
 constexpr int kTile = 16;
 constexpr int kStages = 4;
-// Stage layout is lane-ordered: every lane's fragment data for one tile sits in 16-byte
-// slots [region][lane][16 B], filled by cp.async straight from the reference-format rows.
-//   INT2: KC @0 (tok g | tok g+8, 8 B each), VC @512 (word g of tok 2c,2c+1,2c+8,2c+9),
-//         KM @1024 (meta tok g, g+8 of group c), VM @1536 (meta of the 4 V tokens, group g/2)
-//   INT4: KC @0 (tok g, 16 B) @512 (tok g+8), VC @1024 (tok 2c|2c+1, 8 B each) @1536 (2c+8|2c+9),
-//         KM @2048, VM @2560
-constexpr int kStageBytes = 3072;
-constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 48 KB per CTA
+// A stage holds one 16-token tile of the tile-native arenas verbatim (see the tile functions
+// below): INT2 1536 B, INT4 2560 B.
+constexpr int kStageBytes = 2560;
+constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 40 KB per CTA
 constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l (partial_out / cross-rank format)
 constexpr int kWsStride = kHeadDim + 4;    // split workspace rows: acc[128], m, l, pad (16-B rows)
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
@@ -258,11 +254,26 @@ __device__ __forceinline__ void lo_mma(WarpState& st, uint32_t a0, uint32_t a2, 
   st.lacc[1] = t[1];
 }
 
-// ---- INT2 tile from a shared-memory stage ----------------------------------------------
+// ---- quantized tiles from a shared-memory stage ---------------------------------------
+// A stage holds one tile in the tile-native arena layout (ckv_common.cuh), copied verbatim:
+//   INT2: KC @0 (512 B), VC @512 (512 B), KM @1024 (256 B), VM @1280 (256 B)
+//   INT4: KC @0 (1024 B), VC @1024 (1024 B), KM @2048, VM @2304
+// `sl` = stage + 16 * lane (this lane's code slots); metadata addresses add the per-lane
+// deltas of MetaOff (K: 8-byte entry per lane; V: 16-byte entry (g/2, c), shared by lane pairs).
+struct MetaOff {
+  int32_t k, v;  // k = -8 lane, v = 16 ((g >> 1) * 4 + c) - 16 lane
+};
+
+// exact-mode scales (f32, then fp16) of two tokens from (lo0, lo1) and (hi0, hi1) half2 words
+__device__ __forceinline__ __half2 exact_sc2(uint32_t lo01, uint32_t hi01, float inv_q) {
+  const float2 l = __half22float2(u32_as_h2(lo01)), h = __half22float2(u32_as_h2(hi01));
+  return __floats2half2_rn((h.x - l.x) * inv_q, (h.y - l.y) * inv_q);
+}
+
 template <bool EXACT>
-__device__ __forceinline__ void qk_int2(uint32_t sl, const QS& qs, uint32_t mg, float (&s)[4]) {
+__device__ __forceinline__ void qk_int2(uint32_t sl, const MetaOff& mo, const QS& qs, uint32_t mg, float (&s)[4]) {
   const uint4 kk = lds128(sl);  // (tok g: words 2c, 2c+1), (tok g+8: words 2c, 2c+1)
-  const uint2 kmm = lds64(sl + 1024);
+  const uint2 kmm = lds64(sl + 1024 + mo.k);
   constexpr float iq = 1.0f / 3.0f;
 
   float s2[4] = {0.f, 0.f, 0.f, 0.f};
@@ -302,15 +313,14 @@ __device__ __forceinline__ void qk_int2(uint32_t sl, const QS& qs, uint32_t mg, 
 }
 
 template <bool EXACT>
-__device__ __forceinline__ void pv_int2(uint32_t sl, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+__device__ __forceinline__ void pv_int2(uint32_t sl, const MetaOff& mo, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+  // codes: word g of tokens (2c | 2c+1) lo halves, hi halves, then (2c+8 | 2c+9)
   const uint4 vv = lds128(sl + 512);
-  const uint4 vmm = lds128(sl + 1536);
+  const uint4 vmm = lds128(sl + 1280 + mo.v);  // (lo 2c|2c+1), (hi ...), (lo 2c+8|2c+9), (hi ...)
   constexpr float iq = 1.0f / 3.0f;
-  const uint32_t c01lo = prmt(vv.x, vv.y, 0x5410), c01hi = prmt(vv.x, vv.y, 0x7632);
-  const uint32_t c23lo = prmt(vv.z, vv.w, 0x5410), c23hi = prmt(vv.z, vv.w, 0x7632);
+  const uint32_t c01lo = vv.x, c01hi = vv.y, c23lo = vv.z, c23hi = vv.w;
   if (!EXACT) {
-    const uint32_t l01 = prmt(vmm.x, vmm.y, 0x5410), l23 = prmt(vmm.z, vmm.w, 0x5410);
-    const DeqC d01 = vdeq(l01, prmt(vmm.x, vmm.y, 0x7632), iq), d23 = vdeq(l23, prmt(vmm.z, vmm.w, 0x7632), iq);
+    const DeqC d01 = vdeq(vmm.x, vmm.y, iq), d23 = vdeq(vmm.z, vmm.w, iq);
     const uint32_t a8 = c01lo >> 8, b8 = c01hi >> 8, e8 = c23lo >> 8, f8 = c23hi >> 8;
     // m-tile mt uses code mt of each 8-code half: j = 2 (mt & 3), from x (mt < 4) or x >> 8
 #define PV2(MT)                                                                                     \
@@ -321,11 +331,10 @@ __device__ __forceinline__ void pv_int2(uint32_t sl, uint32_t mg, WarpState& st,
   }
     PV2(0) PV2(1) PV2(2) PV2(3) PV2(4) PV2(5) PV2(6) PV2(7)
 #undef PV2
-    lo_mma(st, l01, l23, bp0, bp1);
+    lo_mma(st, vmm.x, vmm.z, bp0, bp1);
   } else {
-    const __half2 sc01 = __floats2half2_rn(meta_scale(vmm.x, iq), meta_scale(vmm.y, iq));
-    const __half2 sc23 = __floats2half2_rn(meta_scale(vmm.z, iq), meta_scale(vmm.w, iq));
-    const __half2 lo01 = u32_as_h2(prmt(vmm.x, vmm.y, 0x5410)), lo23 = u32_as_h2(prmt(vmm.z, vmm.w, 0x5410));
+    const __half2 sc01 = exact_sc2(vmm.x, vmm.y, iq), sc23 = exact_sc2(vmm.z, vmm.w, iq);
+    const __half2 lo01 = u32_as_h2(vmm.x), lo23 = u32_as_h2(vmm.z);
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
       const int j = 2 * (mt & 3);
@@ -337,11 +346,11 @@ __device__ __forceinline__ void pv_int2(uint32_t sl, uint32_t mg, WarpState& st,
   }
 }
 
-// ---- INT4 tile from a shared-memory stage ----------------------------------------------
 template <bool EXACT>
-__device__ __forceinline__ void qk_int4(uint32_t sl, const QS& qs, uint32_t mg, float (&s)[4]) {
-  const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);  // group c of tok g / tok g+8
-  const uint2 kmm = lds64(sl + 2048);
+__device__ __forceinline__ void qk_int4(uint32_t sl, const MetaOff& mo, const QS& qs, uint32_t mg, float (&s)[4]) {
+  // group c of tok g / tok g+8, words paired as (lo w0, lo w1), (hi w0, hi w1), (lo w2, lo w3), (hi ...)
+  const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);
+  const uint2 kmm = lds64(sl + 2048 + mo.k);
   constexpr float iq = 1.0f / 15.0f;
 
   float s2[4] = {0.f, 0.f, 0.f, 0.f};
@@ -354,8 +363,8 @@ __device__ __forceinline__ void qk_int4(uint32_t sl, const QS& qs, uint32_t mg, 
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
       // pairs (d0, d0+8) = (word 2blk code i, word 2blk+1 code i)
-      const uint32_t a_lo = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x5410), a_hi = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x7632);
-      const uint32_t b_lo = prmt(kwb[2 * blk], kwb[2 * blk + 1], 0x5410), b_hi = prmt(kwb[2 * blk], kwb[2 * blk + 1], 0x7632);
+      const uint32_t a_lo = kwa[2 * blk], a_hi = kwa[2 * blk + 1];
+      const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
       const uint32_t a_lo8 = a_lo >> 8, a_hi8 = a_hi >> 8, b_lo8 = b_lo >> 8, b_hi8 = b_hi >> 8;
 #define KD(X, X8, D, I) wdeq(K4<I>::hi ? X8 : X, 0x000F000Fu << K4<I>::j, mg, D)
       mma_16816(s, KD(a_lo, a_lo8, dk0, 0), KD(b_lo, b_lo8, dk1, 0), KD(a_lo, a_lo8, dk0, 1), KD(b_lo, b_lo8, dk1, 1), qs.ld(1, 4 * blk + 0));
@@ -370,8 +379,8 @@ __device__ __forceinline__ void qk_int4(uint32_t sl, const QS& qs, uint32_t mg, 
     const __half2 lo0 = u32_as_h2(prmt(kmm.x, kmm.x, 0x1010)), lo1 = u32_as_h2(prmt(kmm.y, kmm.y, 0x1010));
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
-      const uint32_t a_lo = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x5410), a_hi = prmt(kwa[2 * blk], kwa[2 * blk + 1], 0x7632);
-      const uint32_t b_lo = prmt(kwb[2 * blk], kwb[2 * blk + 1], 0x5410), b_hi = prmt(kwb[2 * blk], kwb[2 * blk + 1], 0x7632);
+      const uint32_t a_lo = kwa[2 * blk], a_hi = kwa[2 * blk + 1];
+      const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
 #pragma unroll
       for (int q2 = 0; q2 < 4; ++q2) {
         const uint32_t ca = q2 < 2 ? a_lo : a_hi, cb = q2 < 2 ? b_lo : b_hi;
@@ -389,18 +398,16 @@ __device__ __forceinline__ void qk_int4(uint32_t sl, const QS& qs, uint32_t mg, 
 }
 
 template <bool EXACT>
-__device__ __forceinline__ void pv_int4(uint32_t sl, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+__device__ __forceinline__ void pv_int4(uint32_t sl, const MetaOff& mo, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+  // V (tok 2c | 2c+1) and (2c+8 | 2c+9) for d = 16g + mt (word 2g) and 16g + 8 + mt (word 2g+1):
+  // (lo w2g), (hi w2g), (lo w2g+1), (hi w2g+1) per token pair
   const uint4 va = lds128(sl + 1024), vb = lds128(sl + 1536);
-  const uint4 vmm = lds128(sl + 2560);
+  const uint4 vmm = lds128(sl + 2304 + mo.v);
   constexpr float iq = 1.0f / 15.0f;
-  const uint32_t l01 = prmt(vmm.x, vmm.y, 0x5410), l23 = prmt(vmm.z, vmm.w, 0x5410);
-  // V (tok 2c | 2c+1) and (2c+8 | 2c+9) for d = 16g + mt (word 2g) and 16g + 8 + mt (word 2g+1)
-  const uint32_t x01[4] = {prmt(va.x, va.z, 0x5410), prmt(va.x, va.z, 0x7632),
-                           prmt(va.y, va.w, 0x5410), prmt(va.y, va.w, 0x7632)};
-  const uint32_t x23[4] = {prmt(vb.x, vb.z, 0x5410), prmt(vb.x, vb.z, 0x7632),
-                           prmt(vb.y, vb.w, 0x5410), prmt(vb.y, vb.w, 0x7632)};
+  const uint32_t x01[4] = {va.x, va.y, va.z, va.w};
+  const uint32_t x23[4] = {vb.x, vb.y, vb.z, vb.w};
   if (!EXACT) {
-    const DeqC d01 = vdeq(l01, prmt(vmm.x, vmm.y, 0x7632), iq), d23 = vdeq(l23, prmt(vmm.z, vmm.w, 0x7632), iq);
+    const DeqC d01 = vdeq(vmm.x, vmm.y, iq), d23 = vdeq(vmm.z, vmm.w, iq);
     // m-tile mt: code k = mt & 3 of x[mt >> 2] sits at bits 4k; move it to j = 2k (>> 2k)
 #define PV4(MT)                                                                                     \
   {                                                                                                 \
@@ -411,11 +418,10 @@ __device__ __forceinline__ void pv_int4(uint32_t sl, uint32_t mg, WarpState& st,
   }
     PV4(0) PV4(1) PV4(2) PV4(3) PV4(4) PV4(5) PV4(6) PV4(7)
 #undef PV4
-    lo_mma(st, l01, l23, bp0, bp1);
+    lo_mma(st, vmm.x, vmm.z, bp0, bp1);
   } else {
-    const __half2 sc01 = __floats2half2_rn(meta_scale(vmm.x, iq), meta_scale(vmm.y, iq));
-    const __half2 sc23 = __floats2half2_rn(meta_scale(vmm.z, iq), meta_scale(vmm.w, iq));
-    const __half2 lo01 = u32_as_h2(l01), lo23 = u32_as_h2(l23);
+    const __half2 sc01 = exact_sc2(vmm.x, vmm.y, iq), sc23 = exact_sc2(vmm.z, vmm.w, iq);
+    const __half2 lo01 = u32_as_h2(vmm.x), lo23 = u32_as_h2(vmm.z);
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
       const int k = mt & 3, u = mt >> 2;
@@ -478,55 +484,32 @@ __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf
   }
 }
 
+// Per-lane source pointers of tile 0 of this CTA's INT2 / INT4 ranges (codes + 16 lane,
+// metadata + 8 lane): every copy below is a warp-wide contiguous 512-B / 256-B block.
 struct TileSrc {
   const char *k2, *k2m, *v2, *v2m, *k4, *k4m, *v4, *v4m;
 };
 
-// per-lane source byte offsets inside one 16-token tile (INT2 rows; INT4 code rows are 2x)
-struct LaneSrc {
-  uint32_t k, km, v, vm;
-};
-
-// Warp-wide: stage one quantized tile into this lane's slots with cp.async.  Each lane
-// fetches exactly the bytes its MMA fragments need.  Commits a (possibly empty) group.
+// Warp-wide: stage one quantized tile (tile-native layout) into the stage whose lane slot is
+// `sl` with 16-/8-byte cp.async.  Commits a (possibly empty) group.
 __device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const TileSrc& s,
-                                           const LaneSrc& o, uint32_t sl) {
+                                           const MetaOff& mo, uint32_t sl) {
   if (t < t_q_end) {
     if (t < n2t) {
-      const char* kc = s.k2 + (int64_t)t * (kTile * 32) + o.k;
-      const char* km = s.k2m + (int64_t)t * (kTile * 16) + o.km;
-      const char* vc = s.v2 + (int64_t)t * (kTile * 32) + o.v;
-      const char* vm = s.v2m + (int64_t)t * (kTile * 16) + o.vm;
-      cp_async8(sl, kc);
-      cp_async8(sl + 8, kc + 8 * 32);
-      cp_async4(sl + 512, vc);
-      cp_async4(sl + 516, vc + 32);
-      cp_async4(sl + 520, vc + 8 * 32);
-      cp_async4(sl + 524, vc + 9 * 32);
-      cp_async4(sl + 1024, km);
-      cp_async4(sl + 1028, km + 8 * 16);
-      cp_async4(sl + 1536, vm);
-      cp_async4(sl + 1540, vm + 16);
-      cp_async4(sl + 1544, vm + 8 * 16);
-      cp_async4(sl + 1548, vm + 9 * 16);
+      cp_async16(sl, s.k2 + (int64_t)t * kTileBytes2);
+      cp_async16(sl + 512, s.v2 + (int64_t)t * kTileBytes2);
+      cp_async8(sl + 1024 + mo.k, s.k2m + (int64_t)t * kTileBytesMeta);
+      cp_async8(sl + 1280 + mo.k, s.v2m + (int64_t)t * kTileBytesMeta);
     } else {
       const int64_t t4 = t - n2t;
-      const char* kc = s.k4 + t4 * (kTile * 64) + 2 * o.k;
-      const char* km = s.k4m + t4 * (kTile * 16) + o.km;
-      const char* vc = s.v4 + t4 * (kTile * 64) + 2 * o.v;
-      const char* vm = s.v4m + t4 * (kTile * 16) + o.vm;
+      const char* kc = s.k4 + t4 * kTileBytes4;
+      const char* vc = s.v4 + t4 * kTileBytes4;
       cp_async16(sl, kc);
-      cp_async16(sl + 512, kc + 8 * 64);
-      cp_async8(sl + 1024, vc);
-      cp_async8(sl + 1032, vc + 64);
-      cp_async8(sl + 1536, vc + 8 * 64);
-      cp_async8(sl + 1544, vc + 9 * 64);
-      cp_async4(sl + 2048, km);
-      cp_async4(sl + 2052, km + 8 * 16);
-      cp_async4(sl + 2560, vm);
-      cp_async4(sl + 2564, vm + 16);
-      cp_async4(sl + 2568, vm + 8 * 16);
-      cp_async4(sl + 2572, vm + 9 * 16);
+      cp_async16(sl + 512, kc + 512);
+      cp_async16(sl + 1024, vc);
+      cp_async16(sl + 1536, vc + 512);
+      cp_async8(sl + 2048 + mo.k, s.k4m + t4 * kTileBytesMeta);
+      cp_async8(sl + 2304 + mo.k, s.v4m + t4 * kTileBytesMeta);
     }
   }
   cp_commit();
@@ -534,21 +517,21 @@ __device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const Ti
 
 // Prologue: put this warp's first kStages-1 quantized tiles in flight.
 __device__ __forceinline__ void prologue(int q_begin, int q_end, int n2t, const TileSrc& src,
-                                         const LaneSrc& lo, uint32_t ring_l, int warp) {
+                                         const MetaOff& mo, uint32_t ring_l, int warp) {
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s)
-    issue_tile(q_begin + warp + kDecWarps * s, q_end, n2t, src, lo, ring_l + s * kStageBytes);
+    issue_tile(q_begin + warp + kDecWarps * s, q_end, n2t, src, mo, ring_l + s * kStageBytes);
 }
 
 template <bool EXACT>
-__device__ __forceinline__ void qk_any(bool int2, uint32_t sl, const QS& qs, uint32_t mg, float (&s)[4]) {
-  if (int2) qk_int2<EXACT>(sl, qs, mg, s);
-  else qk_int4<EXACT>(sl, qs, mg, s);
+__device__ __forceinline__ void qk_any(bool int2, uint32_t sl, const MetaOff& mo, const QS& qs, uint32_t mg, float (&s)[4]) {
+  if (int2) qk_int2<EXACT>(sl, mo, qs, mg, s);
+  else qk_int4<EXACT>(sl, mo, qs, mg, s);
 }
 template <bool EXACT>
-__device__ __forceinline__ void pv_any(bool int2, uint32_t sl, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
-  if (int2) pv_int2<EXACT>(sl, mg, st, bp0, bp1);
-  else pv_int4<EXACT>(sl, mg, st, bp0, bp1);
+__device__ __forceinline__ void pv_any(bool int2, uint32_t sl, const MetaOff& mo, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
+  if (int2) pv_int2<EXACT>(sl, mo, mg, st, bp0, bp1);
+  else pv_int4<EXACT>(sl, mo, mg, st, bp0, bp1);
 }
 
 // The tile loops of one warp: quantized tiles [q_begin, q_end) through the cp.async ring
@@ -557,7 +540,7 @@ __device__ __forceinline__ void pv_any(bool int2, uint32_t sl, uint32_t mg, Warp
 // FP16-region tiles [f_begin, f_end).
 template <bool EXACT>
 __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, int f_end, int n2t,
-                                          int len_fp, const TileSrc& src, const LaneSrc& lo,
+                                          int len_fp, const TileSrc& src, const MetaOff& mo,
                                           const uint16_t* kf, const uint16_t* vf, uint32_t ring_l,
                                           const QS& qs, uint32_t mg, WarpState& st, int warp, int g,
                                           int c) {
@@ -569,15 +552,15 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, i
     cp_wait<kStages - 2>();
     __syncwarp();
     float s0[4];
-    qk_any<EXACT>(t < n2t, cur, qs, mg, s0);
+    qk_any<EXACT>(t < n2t, cur, mo, qs, mg, s0);
     uint32_t bp0, bp1;
     softmax_tile(s0, st, bp0, bp1);
     while (true) {
       const int tn = t + kDecWarps;
-      issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, src, lo, put);
+      issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, src, mo, put);
       put = next(put);
       if (tn >= q_end) {
-        pv_any<EXACT>(t < n2t, cur, mg, st, bp0, bp1);
+        pv_any<EXACT>(t < n2t, cur, mo, mg, st, bp0, bp1);
         break;
       }
       cp_wait<kStages - 2>();
@@ -585,14 +568,14 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, i
       const uint32_t nx = next(cur);
       float sn[4];
       if (tn < n2t) {  // both INT2 (tn > t)
-        qk_int2<EXACT>(nx, qs, mg, sn);
-        pv_int2<EXACT>(cur, mg, st, bp0, bp1);
+        qk_int2<EXACT>(nx, mo, qs, mg, sn);
+        pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
       } else if (t >= n2t) {  // both INT4
-        qk_int4<EXACT>(nx, qs, mg, sn);
-        pv_int4<EXACT>(cur, mg, st, bp0, bp1);
+        qk_int4<EXACT>(nx, mo, qs, mg, sn);
+        pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
       } else {  // INT2 -> INT4 boundary
-        qk_int4<EXACT>(nx, qs, mg, sn);
-        pv_int2<EXACT>(cur, mg, st, bp0, bp1);
+        qk_int4<EXACT>(nx, mo, qs, mg, sn);
+        pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
       }
       __syncwarp();  // slot `cur` may be refilled from now on
       softmax_tile(sn, st, bp0, bp1);
@@ -635,25 +618,23 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   const int cnt2 = b2 - a2;               // local tiles [0, cnt2) are INT2, [cnt2, nloc) INT4
   const int nloc = cnt2 + (b4 - a4);
   const int64_t unit = (int64_t)l * a.H + h;
-  TileSrc src;
   const int64_t r2 = off2 + (int64_t)a2 * kTile, r4 = off4 + (int64_t)a4 * kTile;  // first rows
-  src.k2 = reinterpret_cast<const char*>(a.K.codes2 + (unit * a.K.rows2 + r2) * 8);
-  src.k2m = reinterpret_cast<const char*>(a.K.meta2 + (unit * a.K.rows2 + r2) * 4);
-  src.v2 = reinterpret_cast<const char*>(a.V.codes2 + (unit * a.V.rows2 + r2) * 8);
-  src.v2m = reinterpret_cast<const char*>(a.V.meta2 + (unit * a.V.rows2 + r2) * 4);
-  src.k4 = reinterpret_cast<const char*>(a.K.codes4 + (unit * a.K.rows4 + r4) * 16);
-  src.k4m = reinterpret_cast<const char*>(a.K.meta4 + (unit * a.K.rows4 + r4) * 4);
-  src.v4 = reinterpret_cast<const char*>(a.V.codes4 + (unit * a.V.rows4 + r4) * 16);
-  src.v4m = reinterpret_cast<const char*>(a.V.meta4 + (unit * a.V.rows4 + r4) * 4);
+  TileSrc src;  // tile-native arenas: a row range starting at a tile is contiguous bytes
+  src.k2 = reinterpret_cast<const char*>(a.K.codes2 + (unit * a.K.rows2 + r2) * 8) + 16 * lane;
+  src.k2m = reinterpret_cast<const char*>(a.K.meta2 + (unit * a.K.rows2 + r2) * 4) + 8 * lane;
+  src.v2 = reinterpret_cast<const char*>(a.V.codes2 + (unit * a.V.rows2 + r2) * 8) + 16 * lane;
+  src.v2m = reinterpret_cast<const char*>(a.V.meta2 + (unit * a.V.rows2 + r2) * 4) + 8 * lane;
+  src.k4 = reinterpret_cast<const char*>(a.K.codes4 + (unit * a.K.rows4 + r4) * 16) + 16 * lane;
+  src.k4m = reinterpret_cast<const char*>(a.K.meta4 + (unit * a.K.rows4 + r4) * 4) + 8 * lane;
+  src.v4 = reinterpret_cast<const char*>(a.V.codes4 + (unit * a.V.rows4 + r4) * 16) + 16 * lane;
+  src.v4m = reinterpret_cast<const char*>(a.V.meta4 + (unit * a.V.rows4 + r4) * 4) + 8 * lane;
   const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
   const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
-  LaneSrc lo;
-  lo.k = g * 32 + 8 * c;          // K row g, bytes of group c (INT2)
-  lo.km = g * 16 + 4 * c;         // K meta row g, group c
-  lo.v = 2 * c * 32 + 4 * g;      // V row 2c, word g (INT2)
-  lo.vm = 2 * c * 16 + 4 * (g >> 1);
+  MetaOff mo;
+  mo.k = -8 * lane;
+  mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
-  prologue(0, nloc, cnt2, src, lo, ring_l, warp);
+  prologue(0, nloc, cnt2, src, mo, ring_l, warp);
 
   // Everything above touched only build-time data.  q, the FP16 region and len_fp may come
   // from the preceding kernel on the stream: wait for it (no-op without PDL), and let the next
@@ -735,9 +716,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.lsum[0] = st.lsum[1] = 0.f;
 
   if (exact) {
-    run_tiles<true>(0, nloc, f_begin, f_end, cnt2, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<true>(0, nloc, f_begin, f_end, cnt2, len_fp, src, mo, kf, vf, ring_l, qs, mg, st, warp, g, c);
   } else {
-    run_tiles<false>(0, nloc, f_begin, f_end, cnt2, len_fp, src, lo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<false>(0, nloc, f_begin, f_end, cnt2, len_fp, src, mo, kf, vf, ring_l, qs, mg, st, warp, g, c);
     // undo the V m-tile weights 2^(2(mt&3) - 6)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {

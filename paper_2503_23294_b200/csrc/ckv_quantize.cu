@@ -116,6 +116,7 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
                              const uint32_t* __restrict__ perm, int max_chunks,
                              const int32_t* __restrict__ seq, ckv_arena KA, ckv_arena VA,
                              int32_t* flag) {
+  // staging of one packed chunk (2 tiles) in the tile-native layout (ckv_common.cuh)
   __shared__ __align__(16) uint32_t s_codes[kQWarps][512];  // 2 KB per warp (INT4 chunk)
   __shared__ __align__(16) uint32_t s_meta[kQWarps][128];   // 512 B per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -174,17 +175,33 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
         const int r = 2 * (r4 + u) + sub;
         const uint32_t w[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
         float lo, hi;
+        const int rt = r & 15;
+        unsigned char* sc = reinterpret_cast<unsigned char*>(s_codes[warp]);
         if (tier == 0) {
           const uint32_t packed = quantize_slice<2>(w, lo, hi, bad, wide);
-          reinterpret_cast<uint16_t*>(s_codes[warp])[r * 16 + j] = (uint16_t)packed;
+          const int off = (r >> 4) * kTileBytes2 + (tsel ? tile_off_v2(rt, j >> 1, j & 1) : tile_off_k2(rt, j >> 1, j & 1));
+          *reinterpret_cast<uint16_t*>(sc + off) = (uint16_t)packed;
         } else {
-          s_codes[warp][r * 16 + j] = quantize_slice<4>(w, lo, hi, bad, wide);
+          const uint32_t packed = quantize_slice<4>(w, lo, hi, bad, wide);
+          unsigned char* t4 = sc + (r >> 4) * kTileBytes4;
+          *reinterpret_cast<uint16_t*>(t4 + (tsel ? tile_off_v4(rt, j, 0) : tile_off_k4(rt, j, 0))) = (uint16_t)packed;
+          *reinterpret_cast<uint16_t*>(t4 + (tsel ? tile_off_v4(rt, j, 1) : tile_off_k4(rt, j, 1))) = (uint16_t)(packed >> 16);
         }
-        if ((j & 3) == 0) s_meta[warp][r * 4 + (j >> 2)] = h2_as_u32(__floats2half2_rn(lo, hi));
+        if ((j & 3) == 0) {
+          unsigned char* sm = reinterpret_cast<unsigned char*>(s_meta[warp]) + (r >> 4) * kTileBytesMeta;
+          const uint32_t lh = h2_as_u32(__floats2half2_rn(lo, hi));
+          if (tsel) {
+            *reinterpret_cast<uint16_t*>(sm + tile_off_vm(rt, j >> 2, 0)) = (uint16_t)lh;
+            *reinterpret_cast<uint16_t*>(sm + tile_off_vm(rt, j >> 2, 1)) = (uint16_t)(lh >> 16);
+          } else {
+            *reinterpret_cast<uint32_t*>(sm + tile_off_km(rt, j >> 2, 0)) = lh;
+          }
+        }
       }
     }
     __syncwarp();
-    // 128-bit coalesced stores of the packed chunk (1 KB INT2 / 2 KB INT4) and its metadata
+    // 128-bit coalesced stores of the packed chunk (2 tiles: 1 KB INT2 / 2 KB INT4) and its
+    // metadata (2 x 256 B); tiles of a segment are contiguous
     uint32_t* codes = tier == 0 ? A.codes2 + (unit * A.rows2 + dst_row0) * 8
                                 : A.codes4 + (unit * A.rows4 + dst_row0) * 16;
     uint32_t* meta = tier == 0 ? A.meta2 + (unit * A.rows2 + dst_row0) * 4
@@ -232,6 +249,39 @@ __global__ void expand_meta_kernel(const uint32_t* __restrict__ meta, int64_t n,
   zps[i] = lo;
 }
 
+// Tile-native arena rows -> the reference's row-major packed words (_numpy.py:70-86) and
+// (lo, hi) metadata [rows][4]: the inverse gather of the tile layout (ckv_common.cuh).
+__global__ void arena_export_kernel(const unsigned char* __restrict__ codes,
+                                    const unsigned char* __restrict__ meta, int64_t rows, int words,
+                                    int is_v, uint32_t* __restrict__ out_codes,
+                                    uint32_t* __restrict__ out_meta) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t n_code = rows * words;
+  if (i < n_code) {
+    const int64_t r = i / words;
+    const int w = (int)(i % words), rt = (int)(r & 15);
+    const unsigned char* t = codes + (r >> 4) * (words == 8 ? kTileBytes2 : kTileBytes4);
+    int o0, o1;
+    if (words == 8) {
+      o0 = is_v ? tile_off_v2(rt, w, 0) : tile_off_k2(rt, w, 0);
+      o1 = is_v ? tile_off_v2(rt, w, 1) : tile_off_k2(rt, w, 1);
+    } else {
+      o0 = is_v ? tile_off_v4(rt, w, 0) : tile_off_k4(rt, w, 0);
+      o1 = is_v ? tile_off_v4(rt, w, 1) : tile_off_k4(rt, w, 1);
+    }
+    out_codes[i] = (uint32_t)*reinterpret_cast<const uint16_t*>(t + o0) |
+                   ((uint32_t)*reinterpret_cast<const uint16_t*>(t + o1) << 16);
+  } else if (i < n_code + rows * kGroupsPerRow) {
+    const int64_t k = i - n_code, r = k / kGroupsPerRow;
+    const int G = (int)(k % kGroupsPerRow), rt = (int)(r & 15);
+    const unsigned char* t = meta + (r >> 4) * kTileBytesMeta;
+    const int o0 = is_v ? tile_off_vm(rt, G, 0) : tile_off_km(rt, G, 0);
+    const int o1 = is_v ? tile_off_vm(rt, G, 1) : tile_off_km(rt, G, 1);
+    out_meta[k] = (uint32_t)*reinterpret_cast<const uint16_t*>(t + o0) |
+                  ((uint32_t)*reinterpret_cast<const uint16_t*>(t + o1) << 16);
+  }
+}
+
 }  // namespace ckv
 
 using namespace ckv;
@@ -277,6 +327,21 @@ int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, do
   if (n_groups == 0) return CKV_OK;
   expand_meta_kernel<<<(unsigned)cdiv(n_groups, 256), 256, 0, as_stream(stream)>>>(
       meta, n_groups, (double)((1 << bits) - 1), scales, zero_points);
+  CKV_LAUNCH_CHECK();
+  return CKV_OK;
+}
+
+int32_t ckv_arena_export(const uint32_t* codes, const uint32_t* meta, int64_t rows, int32_t bits,
+                         int32_t is_v, uint32_t* out_codes, uint32_t* out_meta, void* stream) {
+  if (bits != 2 && bits != 4) return CKV_ERR_BITS;
+  if (rows < 0 || (rows % kTileRows)) return CKV_ERR_SHAPE;
+  if (rows == 0) return CKV_OK;
+  if (!codes || !meta || !out_codes || !out_meta) return CKV_ERR_ARG;
+  const int words = bits == 2 ? 8 : 16;
+  const int64_t n = rows * (words + kGroupsPerRow);
+  arena_export_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const unsigned char*>(codes), reinterpret_cast<const unsigned char*>(meta),
+      rows, words, is_v, out_codes, out_meta);
   CKV_LAUNCH_CHECK();
   return CKV_OK;
 }
