@@ -107,6 +107,61 @@ def main():
     for v in per_sm.values():
         by_n.setdefault(len(v), []).append(np.mean(v))
     print("median layer: tile time by CTAs/SM:", {k: round(float(np.mean(v)), 1) for k, v in by_n.items()})
+    # variance decomposition over all layers: SM-level vs unit-level (CTAs of a unit share the
+    # unit's data) vs residual, for CTAs on 4-CTA SMs
+    nsplit = splits
+    res = {"sm": [], "unit": []}
+    for p_ in launches:
+        x = t[t[:, 7] == p_]
+        tt = x[:, 12:16].max(1) - x[:, 2]
+        sm = x[:, 5]
+        unit = x[:, 6] // nsplit
+        cnt = {k: v for k, v in zip(*np.unique(sm, return_counts=True))}
+        keep = np.array([cnt[k] == 4 for k in sm])
+        tt, sm, unit = tt[keep], sm[keep], unit[keep]
+        dev = tt - tt.mean()
+        sm_mean = {k: dev[sm == k].mean() for k in np.unique(sm)}
+        un_mean = {k: dev[unit == k].mean() for k in np.unique(unit)}
+        res["sm"].append(np.var([sm_mean[k] for k in sm]) / np.var(dev))
+        res["unit"].append(np.var([un_mean[k] for k in unit]) / np.var(dev))
+    print("variance share of per-SM means %.2f, of per-unit means %.2f (4-CTA SMs)" % (
+        np.mean(res["sm"]), np.mean(res["unit"])))
+    # per-tile cost regression (static split: CTA `split` of unit (b, h) takes the same share of
+    # INT2, INT4 and FP16-region tiles): CTA tile time ~ t0 + c2 n2 + c4 n4 + cf nf
+    if not args.single:
+        sh = cache.seq_host.astype(np.int64)
+        n2t, n4t, nft = sh[:, 1] // 16, sh[:, 3] // 16, (sh[:, 5] + 15) // 16
+        S, H = splits, cache.H
+        X, Y = [], []
+        for p_ in launches:
+            x = t[t[:, 7] == p_]
+            for r in x:
+                idx = int(r[6]); sp = idx % S; b = (idx // (S * H)) % cache.B
+                f = lambda n: n * (sp + 1) // S - n * sp // S  # noqa: E731
+                X.append([1.0, f(n2t[b]), f(n4t[b]), f(nft[b])])
+                Y.append((r[12:16].max() - r[2]) / 1e3)
+        X, Y = np.array(X, float), np.array(Y)
+        coef, *_ = np.linalg.lstsq(X, Y, rcond=None)
+        pred = X @ coef
+        U = np.zeros((len(launches), cache.B, H))
+        for li, p_ in enumerate(launches):
+            x = t[t[:, 7] == p_]
+            tt = x[:, 12:16].max(1) - x[:, 2]
+            for r, v in zip(x, tt):
+                idx = int(r[6]); b = (idx // (S * H)) % cache.B; h = (idx // S) % H
+                U[li, b, h] += v / S / 1e3
+        U /= U.mean(axis=(1, 2), keepdims=True)
+        half = len(launches) // 2
+        print("per-unit relative time, correlation between layer halves: %.2f" % np.corrcoef(
+            U[:half].mean(0).ravel(), U[half:].mean(0).ravel())[0, 1])
+        print("mean over layers, rows = sequence b, cols = kv head h:")
+        print(np.array2string(U.mean(0), precision=3))
+        print("per-layer std of unit means %.3f; layer-to-layer std of a unit %.3f" % (
+            U.std(axis=(1, 2)).mean(), U.std(axis=0).mean()))
+        print("tile-time model: t0 %.2f us, INT2 %.4f, INT4 %.4f, FP16 %.4f us/tile (per CTA); "
+              "ratios INT4/INT2 %.2f FP16/INT2 %.2f; R^2 %.2f" % (
+                  coef[0], coef[1], coef[2], coef[3], coef[2] / coef[1], coef[3] / coef[1],
+                  1 - np.var(Y - pred) / np.var(Y)))
 
 
 if __name__ == "__main__":
