@@ -196,19 +196,16 @@ int32_t ckv_arena_export(const uint32_t* codes, const uint32_t* meta, int64_t ro
 
 /* (3) Mixed-precision decode attention (attention.mixed_decode_attention, attention.py:63-90,
  * for every (layer, sequence, kv-head) unit at once).  q fp16 [L][B][H*m][128] (strides
- * q_s_layer, q_s_batch in elements), m = q heads per kv head (1..8), batch <= 512.  Online
- * softmax over the virtual sequence INT2 || INT4 || FP16; scale = softmax scale (1/sqrt(128)).
- * Output fp16 [L][B][H*m][128].  `ctas` = grid size (normally one per SM,
- * ckv_decode_ctas_per_sm() x SMs): the launch's quantized tiles, weighted by tier cost, are cut
- * into `ctas` equal contiguous ranges over all units (split-KV across CTAs).  Workspace:
- * ckv_decode_workspace_bytes() bytes, zero-filled once before first use (self-resetting
- * per-unit arrival counters + partial slots; a unit's last CTA merges its split partials
- * inside the same launch).  partial_out (nullable):
+ * q_s_layer, q_s_batch in elements), m = q heads per kv head (1..8).  Online softmax over the
+ * virtual sequence INT2 || INT4 || FP16 with split-KV; scale = softmax scale (1/sqrt(128)).
+ * Output fp16 [L][B][H*m][128].  Workspace: ckv_decode_workspace_bytes() bytes, zero-filled
+ * once before first use (it holds self-resetting split arrival counters; the last CTA of
+ * each unit merges the split partials inside the same launch).  partial_out (nullable):
  * write unnormalised f32 [L][B][H*m][130] = (acc[128], m (log2 domain), l) instead of out,
  * for a cross-GPU split-KV merge with ckv_lse_merge. */
 int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
-                                   int32_t ctas);
-/* Resident decode CTAs per SM on the current device (1: a CTA is 16 warps, 160 KB of stages). */
+                                   int32_t splits);
+/* Resident decode CTAs per SM on the current device (for sizing `splits` to whole waves). */
 int32_t ckv_decode_ctas_per_sm(void);
 #define CKV_DECODE_PDL 1  /* flags bit: launch as a programmatic dependent of the preceding
                              kernel, which must not write the quantized arenas or the immutable
@@ -218,7 +215,7 @@ int32_t ckv_decode_ctas_per_sm(void);
 int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
                              ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
                              int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
-                             float scale, int32_t ctas, void* workspace, uint16_t* out,
+                             float scale, int32_t splits, void* workspace, uint16_t* out,
                              int64_t o_s_layer, int64_t o_s_batch, float* partial_out,
                              int32_t flags, void* stream);
 

@@ -146,12 +146,22 @@ class BatchedKVCache:
         return (s[:, 1] + s[:, 3] + s[:, 5]).astype(np.int64)
 
     def default_splits(self, m, layers=None):
-        """CTAs per decode launch: one 16-warp CTA per SM.  The kernel cuts the launch's work
-        (all units' quantized tiles, weighted by tier cost) into that many equal contiguous
-        ranges, so every SM gets the same share; the split-KV partials of units that span
-        several CTAs are merged inside the launch."""
+        """Split-KV factor: the whole grid should fill whole waves of resident CTAs (a
+        byte-balanced split makes every CTA equally long, so the tail is the partial wave),
+        while keeping >= ~16 tiles per CTA so partial traffic stays negligible."""
+        units = (self.L if layers is None else layers) * self.B * self.H
         per_sm = _lib.load().ckv_decode_ctas_per_sm()
-        return _num_sms() * max(per_sm, 1)
+        slots = _num_sms() * max(per_sm, 1)
+        tiles = int(max(1, (self.total_tokens().max() + TILE - 1) // TILE))
+        best, best_cost = 1, None
+        for s in range(1, 65):
+            if s > 1 and tiles // s < 16:
+                break
+            waves = -(-units * s // slots)
+            cost = waves / (units * s / slots) + 0.002 * s  # tail waste + merge overhead
+            if best_cost is None or cost < best_cost - 1e-9:
+                best, best_cost = s, cost
+        return best
 
     def _workspace(self, m, splits, layers, layer):
         """Zero-initialised decode workspace (split partials + self-resetting arrival counters).

@@ -31,13 +31,13 @@
 
 namespace ckv {
 
-constexpr int kDecWarps = 16;  // one CTA of 16 warps per SM
+constexpr int kDecWarps = 4;
 constexpr int kTile = 16;
 constexpr int kStages = 4;
 // A stage holds one 16-token tile of the tile-native arenas verbatim (see the tile functions
 // below): INT2 1536 B, INT4 2560 B.
 constexpr int kStageBytes = 2560;
-constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 160 KB per CTA
+constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 40 KB per CTA
 constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l (partial_out / cross-rank format)
 constexpr int kWsStride = kHeadDim + 4;    // split workspace rows: acc[128], m, l, pad (16-B rows)
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
@@ -47,9 +47,9 @@ struct DecArgs {
   int64_t q_sl, q_sb;
   ckv_arena K, V;
   const int32_t* seq;
-  int L, B, H, m;
+  int L, B, H, m, splits;
   float scale_log2;
-  float* ws;            // partial slots [ctas + 2 units][m][132] (see the work decomposition)
+  float* ws;            // [L*B*H*m][splits][130] partials
   uint32_t* counters;   // [L*B*H] arrival counters (self-resetting)
   uint16_t* out;
   int64_t o_sl, o_sb;
@@ -58,8 +58,9 @@ struct DecArgs {
 };
 
 // Optional per-CTA timeline (tuning aid, not part of the ABI): when set, every CTA appends 16
-// int64: globaltimer at start, after the PDL wait, after the first q staging, after the last
-// segment's tiles, at exit; smid, block index, q pointer (launch id), segments, cost range.
+// int64: globaltimer at start, after the PDL wait, after q staging, after warp 0's tiles, at
+// exit; smid, linear block index, q pointer (launch id); after all warps' tiles, before the
+// arrival atomic, after it, is-last; per-warp tile end times.
 __device__ int64_t* g_trace = nullptr;
 __device__ unsigned long long g_trace_n = 0;
 __device__ __forceinline__ int64_t gtime() {
@@ -155,10 +156,8 @@ __device__ __forceinline__ float kscale_fold(float inv_q) {  // 1 / (qmax * fp16
 __device__ __forceinline__ DeqC kdeq(uint32_t meta, __half2 inv_q) {
   const __half2 h = u32_as_h2(meta);
   DeqC d;
-  // opaque: keep (sc, sc) one packed register.  Otherwise ptxas keeps the scalar, uses .H0_H0
-  // operand selects, and re-packs -16 sc with a PRMT before every HFMA2 that needs it as C.
-  d.sc = u32_as_h2(opaque(h2_as_u32(__hmul2(__hsub2(__high2half2(h), __low2half2(h)), inv_q))));
-  d.nm = u32_as_h2(opaque(h2_as_u32(__hmul2(d.sc, __float2half2_rn(-16.0f)))));
+  d.sc = __hmul2(__hsub2(__high2half2(h), __low2half2(h)), inv_q);
+  d.nm = __hmul2(d.sc, __float2half2_rn(-16.0f));
   return d;
 }
 __device__ __forceinline__ DeqC vdeq(uint32_t lo01, uint32_t hi01, float inv_q) {
@@ -166,8 +165,8 @@ __device__ __forceinline__ DeqC vdeq(uint32_t lo01, uint32_t hi01, float inv_q) 
   const __half c_lo = __float2half_rn(inv_q - __half2float(c_hi));
   const __half2 span = __hsub2(u32_as_h2(hi01), u32_as_h2(lo01));
   DeqC d;
-  d.sc = u32_as_h2(opaque(h2_as_u32(__hfma2(span, __half2half2(c_hi), __hmul2(span, __half2half2(c_lo))))));
-  d.nm = u32_as_h2(opaque(h2_as_u32(__hmul2(d.sc, __float2half2_rn(-16.0f)))));
+  d.sc = __hfma2(span, __half2half2(c_hi), __hmul2(span, __half2half2(c_lo)));
+  d.nm = __hmul2(d.sc, __float2half2_rn(-16.0f));
   return d;
 }
 
@@ -233,15 +232,24 @@ __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint3
   bp1 = movmatrix_trans(h2_as_u32(__floats2half2_rn(p2, p3)));  // (P[g][8+2c], P[g][9+2c])
 }
 
-// Q B-fragments live in shared memory as three sets ([set][9][32 lanes] x 8 B, one copy per
-// CTA): 0 = INT2 slot weights, 1 = INT4 slot weights, 2 = unweighted (FP16 tiles and the exact
-// mode).  Entry 8 of a set holds the (hi, lo) split of sum_g(q) for the zero-point MMA.
-constexpr int kQSet = 9 * 32 * 8;
+// Q B-fragments live in shared memory as three sets ([set][k-step pair][32 lanes] x 16 B, one
+// copy per CTA: k-steps 2kp, 2kp+1 of a lane side by side, so a pair is one conflict-free
+// 128-bit load): 0 = INT2 slot weights, 1 = INT4 slot weights, 2 = unweighted (FP16 tiles and
+// the exact mode).  After the sets, [32 lanes] x 4 B: the (hi, lo) split of sum_g(q) for the
+// zero-point MMA.
+constexpr int kQSet = 4 * 32 * 16;
+constexpr int kQBytes = 3 * kQSet + 32 * 4;
 struct QS {
-  uint32_t base;  // s_q + 8 * lane
-  __device__ __forceinline__ uint2 ld(int set, int ks) const { return lds64(base + set * kQSet + 256 * ks); }
-  __device__ __forceinline__ uint32_t aug() const { return lds32(base + 256 * 8); }
+  uint32_t base;  // s_q + 16 * lane
+  uint32_t aug_addr;
+  __device__ __forceinline__ uint2 ld(int set, int ks) const {
+    return lds64(base + set * kQSet + 512 * (ks >> 1) + 8 * (ks & 1));
+  }
+  __device__ __forceinline__ uint4 ld2(int set, int kp) const { return lds128(base + set * kQSet + 512 * kp); }
+  __device__ __forceinline__ uint32_t aug() const { return lds32(aug_addr); }
 };
+__device__ __forceinline__ uint2 lo2(const uint4& v) { return make_uint2(v.x, v.y); }
+__device__ __forceinline__ uint2 hi2(const uint4& v) { return make_uint2(v.z, v.w); }
 
 __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                           uint32_t a3, uint2 b) {
@@ -287,11 +295,12 @@ __device__ __forceinline__ void qk_int2(uint32_t sl, const MetaOff& mo, const QS
     for (int blk = 0; blk < 2; ++blk) {
       const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
       const uint32_t w0s = w0 >> 10, w1s = w1 >> 10;
+      const uint4 qa = qs.ld2(0, 2 * blk), qb = qs.ld2(0, 2 * blk + 1);
 #define KD(W, WS, D, I) wdeq(K2<I>::hi ? WS : W, 0x00030003u << K2<I>::j, mg, D)
-      mma_16816(s, KD(w0, w0s, dk0, 0), KD(w1, w1s, dk1, 0), KD(w0, w0s, dk0, 1), KD(w1, w1s, dk1, 1), qs.ld(0, 4 * blk + 0));
-      mma_16816(s2, KD(w0, w0s, dk0, 2), KD(w1, w1s, dk1, 2), KD(w0, w0s, dk0, 3), KD(w1, w1s, dk1, 3), qs.ld(0, 4 * blk + 1));
-      mma_16816(s, KD(w0, w0s, dk0, 4), KD(w1, w1s, dk1, 4), KD(w0, w0s, dk0, 5), KD(w1, w1s, dk1, 5), qs.ld(0, 4 * blk + 2));
-      mma_16816(s2, KD(w0, w0s, dk0, 6), KD(w1, w1s, dk1, 6), KD(w0, w0s, dk0, 7), KD(w1, w1s, dk1, 7), qs.ld(0, 4 * blk + 3));
+      mma_16816(s, KD(w0, w0s, dk0, 0), KD(w1, w1s, dk1, 0), KD(w0, w0s, dk0, 1), KD(w1, w1s, dk1, 1), lo2(qa));
+      mma_16816(s2, KD(w0, w0s, dk0, 2), KD(w1, w1s, dk1, 2), KD(w0, w0s, dk0, 3), KD(w1, w1s, dk1, 3), hi2(qa));
+      mma_16816(s, KD(w0, w0s, dk0, 4), KD(w1, w1s, dk1, 4), KD(w0, w0s, dk0, 5), KD(w1, w1s, dk1, 5), lo2(qb));
+      mma_16816(s2, KD(w0, w0s, dk0, 6), KD(w1, w1s, dk1, 6), KD(w0, w0s, dk0, 7), KD(w1, w1s, dk1, 7), hi2(qb));
 #undef KD
     }
     mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
@@ -367,11 +376,12 @@ __device__ __forceinline__ void qk_int4(uint32_t sl, const MetaOff& mo, const QS
       const uint32_t a_lo = kwa[2 * blk], a_hi = kwa[2 * blk + 1];
       const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
       const uint32_t a_lo8 = a_lo >> 8, a_hi8 = a_hi >> 8, b_lo8 = b_lo >> 8, b_hi8 = b_hi >> 8;
+      const uint4 qa = qs.ld2(1, 2 * blk), qb = qs.ld2(1, 2 * blk + 1);
 #define KD(X, X8, D, I) wdeq(K4<I>::hi ? X8 : X, 0x000F000Fu << K4<I>::j, mg, D)
-      mma_16816(s, KD(a_lo, a_lo8, dk0, 0), KD(b_lo, b_lo8, dk1, 0), KD(a_lo, a_lo8, dk0, 1), KD(b_lo, b_lo8, dk1, 1), qs.ld(1, 4 * blk + 0));
-      mma_16816(s2, KD(a_lo, a_lo8, dk0, 2), KD(b_lo, b_lo8, dk1, 2), KD(a_lo, a_lo8, dk0, 3), KD(b_lo, b_lo8, dk1, 3), qs.ld(1, 4 * blk + 1));
-      mma_16816(s, KD(a_hi, a_hi8, dk0, 0), KD(b_hi, b_hi8, dk1, 0), KD(a_hi, a_hi8, dk0, 1), KD(b_hi, b_hi8, dk1, 1), qs.ld(1, 4 * blk + 2));
-      mma_16816(s2, KD(a_hi, a_hi8, dk0, 2), KD(b_hi, b_hi8, dk1, 2), KD(a_hi, a_hi8, dk0, 3), KD(b_hi, b_hi8, dk1, 3), qs.ld(1, 4 * blk + 3));
+      mma_16816(s, KD(a_lo, a_lo8, dk0, 0), KD(b_lo, b_lo8, dk1, 0), KD(a_lo, a_lo8, dk0, 1), KD(b_lo, b_lo8, dk1, 1), lo2(qa));
+      mma_16816(s2, KD(a_lo, a_lo8, dk0, 2), KD(b_lo, b_lo8, dk1, 2), KD(a_lo, a_lo8, dk0, 3), KD(b_lo, b_lo8, dk1, 3), hi2(qa));
+      mma_16816(s, KD(a_hi, a_hi8, dk0, 0), KD(b_hi, b_hi8, dk1, 0), KD(a_hi, a_hi8, dk0, 1), KD(b_hi, b_hi8, dk1, 1), lo2(qb));
+      mma_16816(s2, KD(a_hi, a_hi8, dk0, 2), KD(b_hi, b_hi8, dk1, 2), KD(a_hi, a_hi8, dk0, 3), KD(b_hi, b_hi8, dk1, 3), hi2(qb));
 #undef KD
     }
     mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
@@ -485,28 +495,26 @@ __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf
   }
 }
 
-// Per-lane byte offsets (from the arena bases, which stay in kernel parameters) of the first
-// tile of this CTA's share of a unit's INT2 / INT4 segments: codes + 16 lane, metadata +
-// 8 lane.  K and V arenas share row offsets.  Every copy below is a warp-wide contiguous
-// 512-B / 256-B block.
-struct TileOff {
+// Per-lane byte offsets (from the arena bases, which stay in kernel parameters) of tile 0 of
+// this CTA's INT2 / INT4 ranges: codes + 16 lane, metadata + 8 lane.  K and V arenas share row
+// offsets.  Every copy below is a warp-wide contiguous 512-B / 256-B block.
+struct TileSrc {
   int64_t c2, m2, c4, m4;
 };
 
-// Warp-wide: stage local tile t of the segment (t < n2: INT2 tile t, else INT4 tile t - n2)
-// into the stage whose lane slot is `sl` with 16-/8-byte cp.async.  Commits a (possibly
-// empty) group.
-__device__ __forceinline__ void issue_tile(int t, int nq, int n2, const DecArgs& a, const TileOff& o,
-                                           const MetaOff& mo, uint32_t sl) {
-  if (t < nq) {
-    if (t < n2) {
+// Warp-wide: stage one quantized tile (tile-native layout) into the stage whose lane slot is
+// `sl` with 16-/8-byte cp.async.  Commits a (possibly empty) group.
+__device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const DecArgs& a,
+                                           const TileSrc& o, const MetaOff& mo, uint32_t sl) {
+  if (t < t_q_end) {
+    if (t < n2t) {
       const int64_t oc = o.c2 + (int64_t)t * kTileBytes2, om = o.m2 + (int64_t)t * kTileBytesMeta;
       cp_async16(sl, reinterpret_cast<const char*>(a.K.codes2) + oc);
       cp_async16(sl + 512, reinterpret_cast<const char*>(a.V.codes2) + oc);
       cp_async8(sl + 1024 + mo.k, reinterpret_cast<const char*>(a.K.meta2) + om);
       cp_async8(sl + 1280 + mo.k, reinterpret_cast<const char*>(a.V.meta2) + om);
     } else {
-      const int64_t t4 = t - n2;
+      const int64_t t4 = t - n2t;
       const int64_t oc = o.c4 + t4 * kTileBytes4, om = o.m4 + t4 * kTileBytesMeta;
       const char* kc = reinterpret_cast<const char*>(a.K.codes4) + oc;
       const char* vc = reinterpret_cast<const char*>(a.V.codes4) + oc;
@@ -521,13 +529,13 @@ __device__ __forceinline__ void issue_tile(int t, int nq, int n2, const DecArgs&
   cp_commit();
 }
 
-// ticket from the CTA's shared-memory counter, taken by the warp's leader lane only (PTX, so
-// the compiler does not turn it into a warp-aggregated atomic)
-__device__ __forceinline__ uint32_t leader_ticket(uint32_t ctr_addr, uint32_t old, uint32_t leader) {
-  uint32_t r = old;
-  asm volatile("{.reg .pred p; setp.ne.u32 p, %2, 0; @p atom.shared.add.u32 %0, [%1], 1;}"
-               : "+r"(r) : "r"(ctr_addr), "r"(leader) : "memory");
-  return r;
+// Prologue: put this warp's first kStages-1 quantized tiles in flight.
+__device__ __forceinline__ void prologue(int q_begin, int q_end, int n2t, const DecArgs& a,
+                                         const TileSrc& src, const MetaOff& mo, uint32_t ring_l,
+                                         int warp) {
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s)
+    issue_tile(q_begin + warp + kDecWarps * s, q_end, n2t, a, src, mo, ring_l + s * kStageBytes);
 }
 
 template <bool EXACT>
@@ -541,55 +549,44 @@ __device__ __forceinline__ void pv_any(bool int2, uint32_t sl, const MetaOff& mo
   else pv_int4<EXACT>(sl, mo, mg, st, bp0, bp1);
 }
 
-// The tile loop of one warp over the CTA's share of one unit: nq quantized tiles (INT2 then
-// INT4).  The prologue staged local tiles warp, warp + 16, warp + 32; every further tile is a
-// ticket from the CTA's shared-memory counter (one ATOMS per tile, requested one tile ahead),
-// so the 16 warps finish the share together whatever their scheduling priorities.  Software-
-// pipelined: q.K^T of tile i+1 and P.V of tile i form one straight-line block.  Then the
-// CTA's FP16-region tiles [f_begin, f_end), interleaved over warps.
+// The tile loops of one warp: quantized tiles [q_begin, q_end) through the cp.async ring
+// (prologue already issued), software-pipelined so that q.K^T of tile i+1 and P.V of tile i
+// form one straight-line block (independent MMA chains the scheduler can interleave); then
+// FP16-region tiles [f_begin, f_end).
 template <bool EXACT>
-__device__ __forceinline__ void run_tiles(int nq, int n2, int f_begin, int f_end, int len_fp,
-                                          const DecArgs& a, const TileOff& src, const MetaOff& mo,
+__device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, int f_end, int n2t,
+                                          int len_fp, const DecArgs& a, const TileSrc& src,
+                                          const MetaOff& mo,
                                           const uint16_t* kf, const uint16_t* vf, uint32_t ring_l,
-                                          const QS& qs, uint32_t mg, WarpState& st, uint32_t tick_addr,
-                                          int warp, int lane, int g, int c) {
-  static_assert(kStages == 4, "the tile FIFO below assumes a 4-slot ring");
+                                          const QS& qs, uint32_t mg, WarpState& st, int warp, int g,
+                                          int c) {
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
-  int t = warp, t1 = warp + kDecWarps, t2 = warp + 2 * kDecWarps;  // staged by the prologue
-  const uint32_t leader = lane == 0;
-  uint32_t pend = (uint32_t)nq;  // ticket requested one tile ahead (lane 0)
-  if (t2 < nq) pend = leader_ticket(tick_addr, pend, leader);
-  auto take = [&]() -> int {
-    const int v = (int)__shfl_sync(0xffffffffu, pend, 0);
-    if (v < nq) pend = leader_ticket(tick_addr, pend, leader);
-    return v;
-  };
-  if (t < nq) {
+  int t = q_begin + warp;
+  if (t < q_end) {
     uint32_t cur = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
     cp_wait<kStages - 2>();
     __syncwarp();
     float s0[4];
-    qk_any<EXACT>(t < n2, cur, mo, qs, mg, s0);
+    qk_any<EXACT>(t < n2t, cur, mo, qs, mg, s0);
     uint32_t bp0, bp1;
     softmax_tile(s0, st, bp0, bp1);
     while (true) {
-      const int tn = t1;
-      const int t3 = t2 < nq ? take() : nq;
-      issue_tile(t3, nq, n2, a, src, mo, put);
+      const int tn = t + kDecWarps;
+      issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, a, src, mo, put);
       put = next(put);
-      if (tn >= nq) {
-        pv_any<EXACT>(t < n2, cur, mo, mg, st, bp0, bp1);
+      if (tn >= q_end) {
+        pv_any<EXACT>(t < n2t, cur, mo, mg, st, bp0, bp1);
         break;
       }
       cp_wait<kStages - 2>();
       __syncwarp();
       const uint32_t nx = next(cur);
       float sn[4];
-      if (tn < n2) {  // both INT2 (tn > t)
+      if (tn < n2t) {  // both INT2 (tn > t)
         qk_int2<EXACT>(nx, mo, qs, mg, sn);
         pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
-      } else if (t >= n2) {  // both INT4
+      } else if (t >= n2t) {  // both INT4
         qk_int4<EXACT>(nx, mo, qs, mg, sn);
         pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
       } else {  // INT2 -> INT4 boundary
@@ -600,11 +597,8 @@ __device__ __forceinline__ void run_tiles(int nq, int n2, int f_begin, int f_end
       softmax_tile(sn, st, bp0, bp1);
       cur = nx;
       t = tn;
-      t1 = t2;
-      t2 = t3;
     }
   }
-  pend = __shfl_sync(0xffffffffu, pend, 0);  // retire the last ticket request
   cp_wait<0>();
   for (int tf = f_begin + warp; tf < f_end; tf += kDecWarps) {
     const int r = tf * kTile;
@@ -612,351 +606,185 @@ __device__ __forceinline__ void run_tiles(int nq, int n2, int f_begin, int f_end
   }
 }
 
-// ---- work decomposition ------------------------------------------------------------------
-// A launch covers units u = (l, b, h) (l-major, then sequence, then kv head).  Unit u costs
-// C_b = kCost2 n2t + kCost4 n4t + 1 (its quantized tiles, plus one virtual slot so every unit
-// has a CTA even without quantized tiles), the same for all heads and layers of sequence b.
-// CTA i of N owns the cost range [i C / N, (i+1) C / N) of the concatenation: one CTA per SM,
-// every SM the same share, a range spanning 1-3 units ("segments").  A tile belongs to the
-// CTA whose range holds its start cost.  The CTAs touching unit u ("participants") are
-// cta_of(P_u) .. cta_of(P_u + C_u - 1); each writes its partial to workspace slot i + 2u
-// (slots of one unit are contiguous and never collide), and the last to arrive merges them.
-// A unit's FP16-region tiles (whose count grows with decode appends, so they stay out of the
-// cost model) are split evenly over its participants.
-constexpr int kCost2 = 10, kCost4 = 11;  // relative issue cost of an INT2 / INT4 tile
-constexpr int kMaxSeq = 512;             // sequences per launch (cost prefix in shared memory)
-
-__device__ __forceinline__ int64_t cta_of(int64_t x, int64_t C, int64_t N) {  // CTA holding cost x
-  return ((x + 1) * N - 1) / C;
-}
-
-// The CTA's plan and current segment live in shared memory (computed by thread 0): nothing of
-// the outer loop stays in registers across the tile loop.
-struct Plan {
-  int64_t C, N, c_layer, x, hi;
-};
-struct SegDesc {
-  int64_t u, i_first;         // unit index in the launch; its first participant CTA
-  int64_t c2, m2, c4, m4;     // TileOff of the CTA's share, without the lane terms
-  int l, b, h, npart, slot, n2, nq, valid;
-};
-
-__device__ __forceinline__ void plan_segment(const DecArgs& a, const int64_t* s_pre, Plan& ps,
-                                             SegDesc& sd) {
-  if (ps.x >= ps.hi) {
-    sd.valid = 0;
-    return;
-  }
-  const int64_t x = ps.x, C = ps.C, N = ps.N, c_layer = ps.c_layer;
-  const int l = (int)(x / c_layer);
-  const int64_t r = x - (int64_t)l * c_layer;
-  int lo_b = 0, hi_b = a.B;  // largest b with H * s_pre[b] <= r
-  while (hi_b - lo_b > 1) {
-    const int mid = (lo_b + hi_b) >> 1;
-    if ((int64_t)a.H * s_pre[mid] <= r) lo_b = mid; else hi_b = mid;
-  }
-  const int b = lo_b;
-  const int64_t cb = s_pre[b + 1] - s_pre[b];
-  const int h = (int)((r - (int64_t)a.H * s_pre[b]) / cb);
-  const int64_t pu = (int64_t)l * c_layer + (int64_t)a.H * s_pre[b] + (int64_t)h * cb;
-  const int64_t ca = x - pu, ce = min(ps.hi, pu + cb) - pu;  // local cost range [ca, ce)
-  ps.x = pu + cb;
-  const int64_t i_first = cta_of(pu, C, N), i_last = cta_of(pu + cb - 1, C, N);
-  const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
-  const int n2t = s0.y / kTile, n4t = s0.w / kTile;
-  const int64_t base4 = (int64_t)kCost2 * n2t;
-  const int k0 = (int)min((int64_t)n2t, (ca + kCost2 - 1) / kCost2);
-  const int k1 = (int)min((int64_t)n2t, (ce + kCost2 - 1) / kCost2);
-  const int j0 = (int)min((int64_t)n4t, max((int64_t)0, (ca - base4 + kCost4 - 1) / kCost4));
-  const int j1 = (int)min((int64_t)n4t, max((int64_t)0, (ce - base4 + kCost4 - 1) / kCost4));
-  const int64_t unit = (int64_t)l * a.H + h;  // arena slab (layer, kv head)
-  const int64_t r2 = unit * a.K.rows2 + s0.x + (int64_t)k0 * kTile;
-  const int64_t r4 = unit * a.K.rows4 + s0.z + (int64_t)j0 * kTile;
-  sd.u = ((int64_t)l * a.B + b) * a.H + h;
-  sd.i_first = i_first;
-  sd.c2 = r2 * 32; sd.m2 = r2 * 16; sd.c4 = r4 * 64; sd.m4 = r4 * 16;
-  sd.l = l; sd.b = b; sd.h = h;
-  sd.npart = (int)(i_last - i_first + 1);
-  sd.slot = (int)((int64_t)blockIdx.x - i_first);
-  sd.n2 = k1 - k0;
-  sd.nq = (k1 - k0) + (j1 - j0);
-  sd.valid = 1;
-}
-
-__global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(const DecArgs a) {
+__global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs a) {
   extern __shared__ __align__(128) unsigned char s_dyn[];  // ring: [warp][stage][kStageBytes]
   unsigned char (*s_ring)[kStages][kStageBytes] = reinterpret_cast<unsigned char (*)[kStages][kStageBytes]>(s_dyn);
-  __shared__ int64_t s_pre[kMaxSeq + 1];  // cost prefix over sequences (one layer, one head)
   __shared__ float s_ml[kDecWarps][8][2];
-  __shared__ __align__(16) uint2 s_q[3][9][32];
-  __shared__ Plan s_plan;
-  __shared__ SegDesc s_seg;
-  __shared__ int s_tick, s_last, s_wide_q;
+  __shared__ __align__(16) unsigned char s_q[kQBytes];
+  __shared__ int s_last, s_wide_q;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
+  const int split = blockIdx.x, h = blockIdx.y;
   int64_t* const trace = g_trace;
-  int64_t tr[5];
-  tr[0] = trace ? gtime() : 0;
-  tr[1] = tr[2] = tr[3] = 0;
-
-  // ---- cost prefix over the sequences (immutable after the build: read before the PDL wait)
-  for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
-    const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
-    s_pre[b + 1] = (int64_t)kCost2 * (s0.y / kTile) + (int64_t)kCost4 * (s0.w / kTile) + 1;
-  }
-  if (threadIdx.x == 0) s_pre[0] = 0;
-  __syncthreads();
-  if (warp == 0) {  // inclusive scan of s_pre[1..B] in chunks of 32
-    int64_t carry = 0;
-    for (int base = 1; base <= a.B; base += 32) {
-      const int i = base + lane;
-      int64_t v = i <= a.B ? s_pre[i] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      if (i <= a.B) s_pre[i] = v + carry;
-      carry += __shfl_sync(0xffffffffu, v, 31);
-    }
-    if (lane == 0) {
-      Plan ps;
-      ps.c_layer = (int64_t)a.H * s_pre[a.B];
-      ps.C = (int64_t)a.L * ps.c_layer;
-      ps.N = min((int64_t)gridDim.x, ps.C);
-      const int64_t cta = blockIdx.x;
-      ps.x = cta < ps.N ? cta * ps.C / ps.N : 0;
-      ps.hi = cta < ps.N ? (cta + 1) * ps.C / ps.N : 0;
-      s_plan = ps;
-    }
-  }
-
-  const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
+  int64_t tr[12];
+  __shared__ int64_t s_tend[kDecWarps];
+  tr[11] = 0;
+  if (trace) tr[0] = gtime();
+  const int l = blockIdx.z / a.B, b = blockIdx.z % a.B;
+  // Segment lengths of the quantized arenas are immutable after the build; len_fp grows with
+  // decode appends and is read only after the programmatic-dependent-launch wait below.
+  const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
+  const int off2 = s0.x, off4 = s0.z, off_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 4];
+  const int n2t = s0.y / kTile, n4t = s0.w / kTile;
+  // Split of the quantized tiles: every CTA takes the same 1/splits share of the INT2 tiles
+  // AND of the INT4 tiles (and of the FP16-region tiles below), so all CTAs carry the same
+  // mix and finish together whatever the relative per-tile costs are.
+  const int a2 = (int)((int64_t)n2t * split / a.splits), b2 = (int)((int64_t)n2t * (split + 1) / a.splits);
+  const int a4 = (int)((int64_t)n4t * split / a.splits), b4 = (int)((int64_t)n4t * (split + 1) / a.splits);
+  const int cnt2 = b2 - a2;               // local tiles [0, cnt2) are INT2, [cnt2, nloc) INT4
+  const int nloc = cnt2 + (b4 - a4);
+  const int64_t unit = (int64_t)l * a.H + h;
+  const int64_t r2 = off2 + (int64_t)a2 * kTile, r4 = off4 + (int64_t)a4 * kTile;  // first rows
+  TileSrc src;  // tile-native arenas: a row range starting at a tile is contiguous bytes
+  src.c2 = (unit * a.K.rows2 + r2) * 32 + 16 * lane;
+  src.m2 = (unit * a.K.rows2 + r2) * 16 + 8 * lane;
+  src.c4 = (unit * a.K.rows4 + r4) * 64 + 16 * lane;
+  src.m4 = (unit * a.K.rows4 + r4) * 16 + 8 * lane;
+  const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
+  const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
   MetaOff mo;
   mo.k = -8 * lane;
   mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
-  const uint32_t mg = kMagic16 | a.zero;
-  const uint32_t tick_addr = (uint32_t)__cvta_generic_to_shared(&s_tick);
-  int nseg = 0;
+  const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
+  prologue(0, nloc, cnt2, a, src, mo, ring_l, warp);
 
-  for (;; ++nseg) {
-    __syncthreads();  // plan / previous segment's merge done: the ring and s_seg are free
-    if (threadIdx.x == 0) {
-      plan_segment(a, s_pre, s_plan, s_seg);
-      s_tick = kDecWarps * (kStages - 1);
-    }
-    __syncthreads();
-    if (!s_seg.valid) break;
-    {
-      const int n2 = s_seg.n2, nq = s_seg.nq;
-      TileOff src;
-      src.c2 = s_seg.c2 + 16 * lane; src.m2 = s_seg.m2 + 8 * lane;
-      src.c4 = s_seg.c4 + 16 * lane; src.m4 = s_seg.m4 + 8 * lane;
-#pragma unroll
-      for (int s = 0; s < kStages - 1; ++s)
-        issue_tile(warp + kDecWarps * s, nq, n2, a, src, mo, ring_l + s * kStageBytes);
-    }
-    if (nseg == 0) {
-      // Everything above touched only build-time data.  q, the FP16 region and len_fp may
-      // come from the preceding kernel on the stream: wait for it (no-op without PDL), and let
-      // the next decode launch start its own prologue as soon as SMs free up.
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      asm volatile("griddepcontrol.launch_dependents;");
-      if (trace) tr[1] = gtime();
-    }
-    // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m); warps 0-2 write the
-    // three sets, warp 3 the zero-point entry and the range flag.
-    if (warp < 4) {
-      const int l = s_seg.l, b = s_seg.b, h = s_seg.h;
-      float qv[32];
-      const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
-      if (g < a.m) {
-#pragma unroll
-        for (int uu = 0; uu < 4; ++uu) {
-          const uint4 xq = reinterpret_cast<const uint4*>(qrow)[uu];
-          const uint32_t w[4] = {xq.x, xq.y, xq.z, xq.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __half22float2(u32_as_h2(w[e]));
-            qv[8 * uu + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
-            qv[8 * uu + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) qv[e] = 0.f;
-      }
-      if (warp < 3) {
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
-          const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
-          // slot weights 2^(6-j): INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1); set 2: 1
-          const float w0 = warp == 0 ? exp2f((float)(6 - (i0 <= 4 ? 2 * i0 : 2 * (i0 - 5))))
-                                     : (warp == 1 ? exp2f((float)(6 - 4 * (i0 & 1))) : 1.0f);
-          const float w1 = warp == 0 ? exp2f((float)(6 - (i1 <= 4 ? 2 * i1 : 2 * (i1 - 5))))
-                                     : (warp == 1 ? exp2f((float)(6 - 4 * (i1 & 1))) : 1.0f);
-          // INT2 / INT4 sets also carry the fold of the fp16(1/qmax) rounding (see kdeq)
-          const float fold = warp == 0 ? kscale_fold(1.0f / 3.0f) : (warp == 1 ? kscale_fold(1.0f / 15.0f) : 1.0f);
-          const float x0 = w0 * fold, x1 = w1 * fold;
-          s_q[warp][ks][lane] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0)),
-                                           h2_as_u32(__floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1)));
-        }
-      } else {
-        float qsum = 0.f, qmaxabs = 0.f;
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          qsum += qv[e];
-          qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
-        }
-        const __half qhi = __float2half_rn(qsum);
-        const __half qlo = __float2half_rn(qsum - __half2float(qhi));
-        s_q[0][8][lane] = make_uint2(h2_as_u32(__halves2half2(qhi, qlo)), 0u);
-        const bool wide = __any_sync(0xffffffffu, qmaxabs > kWideQ);
-        if (lane == 0) s_wide_q = wide;
-      }
-    }
-    __syncthreads();
-    if (nseg == 0 && trace) tr[2] = gtime();
+  // Everything above touched only build-time data.  q, the FP16 region and len_fp may come
+  // from the preceding kernel on the stream: wait for it (no-op without PDL), and let the next
+  // decode launch (next layer) start its own prologue as soon as SMs free up.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (trace) tr[1] = gtime();
+  const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 5];
+  const int nft = (len_fp + kTile - 1) / kTile;
+  const int f_begin = (int)((int64_t)nft * split / a.splits);
+  const int f_end = (int)((int64_t)nft * (split + 1) / a.splits);
 
-    WarpState st;
+  // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m); warp 0 writes the
+  // CTA's three sets to shared memory.
+  {
+    float qv[32];
+    const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
+    if (g < a.m) {
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) st.acc[mt][0] = st.acc[mt][1] = st.acc[mt][2] = st.acc[mt][3] = 0.f;
-    st.lacc[0] = st.lacc[1] = 0.f;
-    st.mrun[0] = st.mrun[1] = -INFINITY;
-    st.lsum[0] = st.lsum[1] = 0.f;
-    {
-      const int l = s_seg.l, b = s_seg.b, h = s_seg.h, npart = s_seg.npart, slot = s_seg.slot;
-      const int n2 = s_seg.n2, nq = s_seg.nq;
-      TileOff src;
-      src.c2 = s_seg.c2 + 16 * lane; src.m2 = s_seg.m2 + 8 * lane;
-      src.c4 = s_seg.c4 + 16 * lane; src.m4 = s_seg.m4 + 8 * lane;
-      const int64_t unit = (int64_t)l * a.H + h;
-      const int off_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 4];
-      const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 5];
-      const int nft = (len_fp + kTile - 1) / kTile;
-      const int f_begin = (int)((int64_t)nft * slot / npart);
-      const int f_end = (int)((int64_t)nft * (slot + 1) / npart);
-      const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
-      const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
-      QS qs;
-      qs.base = (uint32_t)__cvta_generic_to_shared(&s_q[0][0][0]) + 8 * lane;
-      const int64_t fidx = unit * a.B + b;  // span flags are [L][H][B]
-      const bool exact = s_wide_q || (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
-                         (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
-      if (exact) {
-        run_tiles<true>(nq, n2, f_begin, f_end, len_fp, a, src, mo, kf, vf, ring_l, qs, mg, st, tick_addr, warp, lane, g, c);
-      } else {
-        run_tiles<false>(nq, n2, f_begin, f_end, len_fp, a, src, mo, kf, vf, ring_l, qs, mg, st, tick_addr, warp, lane, g, c);
-        // undo the V m-tile weights 2^(2(mt&3) - 6)
+      for (int u = 0; u < 4; ++u) {
+        const uint4 x = reinterpret_cast<const uint4*>(qrow)[u];
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          const float f = (float)(64 >> (2 * (mt & 3)));
-          st.acc[mt][0] *= f; st.acc[mt][1] *= f; st.acc[mt][2] *= f; st.acc[mt][3] *= f;
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(u32_as_h2(w[e]));
+          qv[8 * u + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
+          qv[8 * u + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
         }
       }
-    }
-    if (trace) tr[3] = gtime();
-
-    // finish the warp: fold the zero-point term, reduce row sums over the 8 row-groups
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      st.acc[mt][0] += st.lacc[0]; st.acc[mt][1] += st.lacc[1];
-      st.acc[mt][2] += st.lacc[0]; st.acc[mt][3] += st.lacc[1];
-    }
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
-      st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
-    }
-    __syncthreads();  // ring -> merge buffer reuse
-    float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0][0]);
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      s_acc[warp][2 * c][16 * g + mt] = st.acc[mt][0];
-      s_acc[warp][2 * c + 1][16 * g + mt] = st.acc[mt][1];
-      s_acc[warp][2 * c][16 * g + 8 + mt] = st.acc[mt][2];
-      s_acc[warp][2 * c + 1][16 * g + 8 + mt] = st.acc[mt][3];
-    }
-    if (g == 0) {
-      s_ml[warp][2 * c][0] = st.mrun[0]; s_ml[warp][2 * c][1] = st.lsum[0];
-      s_ml[warp][2 * c + 1][0] = st.mrun[1]; s_ml[warp][2 * c + 1][1] = st.lsum[1];
-    }
-    __syncthreads();
-    // merge the 16 warps: thread -> (q row, d)
-    const int l = s_seg.l, b = s_seg.b, h = s_seg.h, npart = s_seg.npart;
-    const int64_t u = s_seg.u, i_first = s_seg.i_first;
-    const int d = threadIdx.x & (kHeadDim - 1);
-    const int hq0 = h * a.m;
-    const int64_t row0 = ((int64_t)l * a.B + b) * (a.H * a.m) + hq0;
-    for (int qi = threadIdx.x >> 7; qi < a.m; qi += kDecWarps * 32 / kHeadDim) {
-      float ms = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < kDecWarps; ++w) ms = fmaxf(ms, s_ml[w][qi][0]);
-      float acc = 0.f, lsum = 0.f;
-#pragma unroll
-      for (int w = 0; w < kDecWarps; ++w) {
-        const float mw = s_ml[w][qi][0];
-        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-        acc += f * s_acc[w][qi][d];
-        lsum += f * s_ml[w][qi][1];
-      }
-      const int64_t row = row0 + qi;
-      if (npart == 1) {
-        if (a.partial_out) {
-          float* dst = a.partial_out + row * kPartStride;
-          dst[d] = acc;
-          if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
-        } else {
-          a.out[l * a.o_sl + b * a.o_sb + (int64_t)(hq0 + qi) * kHeadDim + d] =
-              __half_as_ushort(__float2half_rn(acc / lsum));
-        }
-      } else {  // this CTA's slot of unit u
-        float* dst = a.ws + (((int64_t)blockIdx.x + 2 * u) * a.m + qi) * kWsStride;
-        dst[d] = acc;
-        if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
-      }
-    }
-    if (npart == 1) continue;
-    // The unit's last participant merges all partials.  The CTA barrier orders every thread's
-    // partial stores before thread 0's device-scope release RMW; the acquiring side sees them
-    // after its own barrier.
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[u]);
-      const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
-      s_last = prev == (uint32_t)(npart - 1);
-      if (s_last) ctr.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
-    }
-    __syncthreads();
-    if (!s_last) continue;
-    // All participants' rows of unit u are contiguous (slots i_first + 2u ..): stage them in
-    // shared memory with every 16-B copy in flight at once (one L2 round trip), then merge.
-    const float* p0 = a.ws + ((i_first + 2 * u) * a.m) * kWsStride;
-    const int nrows = npart * a.m;  // [participant][q row]
-    float* s_part = reinterpret_cast<float*>(&s_ring[0][0][0]);
-    if (nrows * kWsStride * (int)sizeof(float) <= kDynSmem) {
-      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_part);
-      const int nvec = nrows * kWsStride / 4;
-      for (int i = threadIdx.x; i < nvec; i += blockDim.x) cp_async16(sbase + 16 * i, p0 + 4 * i);
-      cp_commit();
-      cp_wait<0>();
-      __syncthreads();
     } else {
-      s_part = nullptr;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) qv[e] = 0.f;
     }
-    for (int qi = threadIdx.x >> 7; qi < a.m; qi += kDecWarps * 32 / kHeadDim) {
-      const float* p = s_part ? s_part : p0;
-      float ms = -INFINITY, acc = 0.f, lsum = 0.f;
-      for (int s = 0; s < npart; ++s) ms = fmaxf(ms, p[(s * a.m + qi) * kWsStride + kHeadDim]);
-      for (int s = 0; s < npart; ++s) {
-        const float* q = p + (s * a.m + qi) * kWsStride;
-        const float mw = q[kHeadDim];
-        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-        acc += f * q[d];
-        lsum += f * q[kHeadDim + 1];
+    // warp w < 3 stores q-fragment set w; warp 3 stores the zero-point entry and the range flag
+    if (warp < 3) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
+        const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
+        // slot weights 2^(6-j): INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1); set 2: 1
+        const float w0 = warp == 0 ? exp2f((float)(6 - (i0 <= 4 ? 2 * i0 : 2 * (i0 - 5))))
+                                   : (warp == 1 ? exp2f((float)(6 - 4 * (i0 & 1))) : 1.0f);
+        const float w1 = warp == 0 ? exp2f((float)(6 - (i1 <= 4 ? 2 * i1 : 2 * (i1 - 5))))
+                                   : (warp == 1 ? exp2f((float)(6 - 4 * (i1 & 1))) : 1.0f);
+        // INT2 / INT4 sets also carry the fold of the fp16(1/qmax) rounding (see kdeq)
+        const float fold = warp == 0 ? kscale_fold(1.0f / 3.0f) : (warp == 1 ? kscale_fold(1.0f / 15.0f) : 1.0f);
+        const float x0 = w0 * fold, x1 = w1 * fold;
+        reinterpret_cast<uint2*>(s_q + warp * kQSet + 512 * (ks >> 1) + 16 * lane)[ks & 1] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0)),
+                                         h2_as_u32(__floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1)));
       }
-      const int64_t row = row0 + qi;
+    } else {
+      float qsum = 0.f, qmaxabs = 0.f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        qsum += qv[e];
+        qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
+      }
+      const __half qhi = __float2half_rn(qsum);
+      const __half qlo = __float2half_rn(qsum - __half2float(qhi));
+      reinterpret_cast<uint32_t*>(s_q + 3 * kQSet)[lane] = h2_as_u32(__halves2half2(qhi, qlo));
+      const bool wide = __any_sync(0xffffffffu, qmaxabs > kWideQ);
+      if (lane == 0) s_wide_q = wide;
+    }
+  }
+  __syncthreads();
+  if (trace) tr[2] = gtime();
+  QS qs;
+  qs.base = (uint32_t)__cvta_generic_to_shared(s_q) + 16 * lane;
+  qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_q) + 3 * kQSet + 4 * lane;
+  const int64_t fidx = unit * a.B + b;  // span flags are [L][H][B]
+  const bool exact = s_wide_q || (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
+                     (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
+  const uint32_t mg = kMagic16 | a.zero;
+
+  WarpState st;
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) st.acc[mt][0] = st.acc[mt][1] = st.acc[mt][2] = st.acc[mt][3] = 0.f;
+  st.lacc[0] = st.lacc[1] = 0.f;
+  st.mrun[0] = st.mrun[1] = -INFINITY;
+  st.lsum[0] = st.lsum[1] = 0.f;
+
+  if (exact) {
+    run_tiles<true>(0, nloc, f_begin, f_end, cnt2, len_fp, a, src, mo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+  } else {
+    run_tiles<false>(0, nloc, f_begin, f_end, cnt2, len_fp, a, src, mo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    // undo the V m-tile weights 2^(2(mt&3) - 6)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const float f = (float)(64 >> (2 * (mt & 3)));
+      st.acc[mt][0] *= f; st.acc[mt][1] *= f; st.acc[mt][2] *= f; st.acc[mt][3] *= f;
+    }
+  }
+
+  if (trace) { tr[3] = gtime(); if (lane == 0) s_tend[warp] = tr[3]; }
+  // finish the warp: fold the zero-point term, reduce row sums over the 8 row-groups
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    st.acc[mt][0] += st.lacc[0]; st.acc[mt][1] += st.lacc[1];
+    st.acc[mt][2] += st.lacc[0]; st.acc[mt][3] += st.lacc[1];
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
+    st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
+  }
+  __syncthreads();  // ring -> merge buffer reuse
+  if (trace) tr[8] = gtime();
+  float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0][0]);
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    s_acc[warp][2 * c][16 * g + mt] = st.acc[mt][0];
+    s_acc[warp][2 * c + 1][16 * g + mt] = st.acc[mt][1];
+    s_acc[warp][2 * c][16 * g + 8 + mt] = st.acc[mt][2];
+    s_acc[warp][2 * c + 1][16 * g + 8 + mt] = st.acc[mt][3];
+  }
+  if (g == 0) {
+    s_ml[warp][2 * c][0] = st.mrun[0]; s_ml[warp][2 * c][1] = st.lsum[0];
+    s_ml[warp][2 * c + 1][0] = st.mrun[1]; s_ml[warp][2 * c + 1][1] = st.lsum[1];
+  }
+  __syncthreads();
+  // merge the 4 warps: thread -> d
+  const int d = threadIdx.x;
+  const int hq0 = h * a.m;
+  const int Hq = a.H * a.m;
+  for (int qi = 0; qi < a.m; ++qi) {
+    float ms = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w) ms = fmaxf(ms, s_ml[w][qi][0]);
+    float acc = 0.f, lsum = 0.f;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w) {
+      const float mw = s_ml[w][qi][0];
+      const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+      acc += f * s_acc[w][qi][d];
+      lsum += f * s_ml[w][qi][1];
+    }
+    const int64_t row = ((int64_t)l * a.B + b) * Hq + hq0 + qi;
+    if (a.splits == 1) {
       if (a.partial_out) {
         float* dst = a.partial_out + row * kPartStride;
         dst[d] = acc;
@@ -965,19 +793,75 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(const DecArgs
         a.out[l * a.o_sl + b * a.o_sb + (int64_t)(hq0 + qi) * kHeadDim + d] =
             __half_as_ushort(__float2half_rn(acc / lsum));
       }
+    } else {
+      float* dst = a.ws + (row * a.splits + split) * kWsStride;
+      dst[d] = acc;
+      if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
     }
   }
-  if (trace && threadIdx.x == 0) {
-    tr[4] = gtime();
-    int64_t* dst = trace + 16 * atomicAdd(&g_trace_n, 1ull);
-    for (int i = 0; i < 5; ++i) dst[i] = tr[i];
-    dst[5] = smid();
-    dst[6] = blockIdx.x;
-    dst[7] = (int64_t)a.q;
-    dst[8] = nseg;
-    dst[9] = s_plan.x;
-    dst[10] = s_plan.hi;
+  auto trace_out = [&]() {
+    if (trace && threadIdx.x == 0) {
+      tr[4] = gtime();
+      int64_t* dst = trace + 16 * atomicAdd(&g_trace_n, 1ull);
+      for (int i = 0; i < 5; ++i) dst[i] = tr[i];
+      for (int i = 8; i < 12; ++i) dst[i] = tr[i];
+      for (int i = 0; i < kDecWarps; ++i) dst[12 + i] = s_tend[i];
+      dst[5] = smid(); dst[6] = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      dst[7] = (int64_t)a.q;
+    }
+  };
+  if (a.splits == 1) { trace_out(); return; }
+  // split-KV: the last CTA of this unit to arrive merges all partials (in-launch, no 2nd
+  // kernel).  The CTA barrier orders every thread's partial stores before thread 0's
+  // device-scope release RMW; the acquiring side sees them after its own barrier.
+  __syncthreads();
+  if (trace) tr[9] = gtime();
+  if (threadIdx.x == 0) {
+    cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[((int64_t)l * a.B + b) * a.H + h]);
+    const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
+    s_last = prev == (uint32_t)(a.splits - 1);
+    if (s_last) ctr.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
   }
+  __syncthreads();
+  if (trace) { tr[10] = gtime(); tr[11] = s_last; }
+  if (!s_last) { trace_out(); return; }
+  // All m x splits partial rows of this unit are contiguous in the workspace: stage them in
+  // shared memory with every 16-B copy in flight at once (one L2 round trip), then merge.
+  const int64_t row0 = ((int64_t)l * a.B + b) * Hq + hq0;
+  const float* p0 = a.ws + row0 * a.splits * kWsStride;
+  const int nrows = a.m * a.splits;
+  float* s_part = reinterpret_cast<float*>(&s_ring[0][0][0]);
+  if (nrows * kWsStride * (int)sizeof(float) <= kDynSmem) {
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_part);
+    const int nvec = nrows * kWsStride / 4;
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) cp_async16(sbase + 16 * i, p0 + 4 * i);
+    cp_commit();
+    cp_wait<0>();
+    __syncthreads();
+  } else {
+    s_part = nullptr;
+  }
+  for (int qi = 0; qi < a.m; ++qi) {
+    const int64_t row = row0 + qi;
+    const float* p = s_part ? s_part + qi * a.splits * kWsStride : a.ws + row * a.splits * kWsStride;
+    float ms = -INFINITY, acc = 0.f, lsum = 0.f;
+    for (int s = 0; s < a.splits; ++s) ms = fmaxf(ms, p[s * kWsStride + kHeadDim]);
+    for (int s = 0; s < a.splits; ++s) {
+      const float mw = p[s * kWsStride + kHeadDim];
+      const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+      acc += f * p[s * kWsStride + d];
+      lsum += f * p[s * kWsStride + kHeadDim + 1];
+    }
+    if (a.partial_out) {
+      float* dst = a.partial_out + row * kPartStride;
+      dst[d] = acc;
+      if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+    } else {
+      a.out[l * a.o_sl + b * a.o_sb + (int64_t)(hq0 + qi) * kHeadDim + d] =
+          __half_as_ushort(__float2half_rn(acc / lsum));
+    }
+  }
+  trace_out();
 }
 
 // Cross-rank merge of gathered partials [P][rows][130] -> out fp16 [rows][128].
@@ -1016,29 +900,29 @@ static bool ensure_decode_attr() {
 extern "C" {
 
 int64_t ckv_decode_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
-                                   int32_t ctas) {
+                                   int32_t splits) {
   const int64_t units = (int64_t)layers * batch * kv_heads;
   const int64_t counters = cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256;
-  if (ctas <= 1) return counters;
-  return counters + (ctas + 2 * units) * m * kWsStride * (int64_t)sizeof(float);
+  if (splits <= 1) return counters;
+  return counters + units * m * splits * kWsStride * (int64_t)sizeof(float);
 }
 
 int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
                              ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
                              int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
-                             float scale, int32_t ctas, void* workspace, uint16_t* out,
+                             float scale, int32_t splits, void* workspace, uint16_t* out,
                              int64_t o_s_layer, int64_t o_s_batch, float* partial_out,
                              int32_t flags, void* stream) {
-  if (layers < 0 || batch < 0 || kv_heads < 0 || ctas < 1) return CKV_ERR_ARG;
-  if (m < 1 || m > 8 || batch > kMaxSeq) return CKV_ERR_UNSUPPORTED;
+  if (layers < 0 || batch < 0 || kv_heads < 0 || splits < 1) return CKV_ERR_ARG;
+  if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (!q || !seq || (!out && !partial_out)) return CKV_ERR_ARG;
-  if (ctas > 1 && !workspace) return CKV_ERR_ARG;
+  if (splits > 1 && !workspace) return CKV_ERR_ARG;
   if ((q_s_layer % 8) || (q_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
   if (layers * batch * kv_heads == 0) return CKV_OK;
   DecArgs a;
   a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
   a.K = k_arena; a.V = v_arena; a.seq = seq;
-  a.L = layers; a.B = batch; a.H = kv_heads; a.m = m;
+  a.L = layers; a.B = batch; a.H = kv_heads; a.m = m; a.splits = splits;
   a.scale_log2 = scale * 1.4426950408889634f;
   const int64_t units = (int64_t)layers * batch * kv_heads;
   a.counters = reinterpret_cast<uint32_t*>(workspace);
@@ -1050,7 +934,7 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
   a.zero = 0u;
   if (!ensure_decode_attr()) return CKV_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)ctas);
+  cfg.gridDim = dim3((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * batch));
   cfg.blockDim = dim3(kDecWarps * 32);
   cfg.dynamicSmemBytes = kDynSmem;
   cfg.stream = as_stream(stream);
@@ -1086,6 +970,29 @@ int32_t ckv_decode_set_trace(int64_t* buf) {
     return CKV_ERR_CUDA;
   }
   return CKV_OK;
+}
+
+// Tuning probe (not part of the ABI): resident clusters of `cluster` decode CTAs.
+int32_t ckv_probe_max_clusters(int32_t cluster, int32_t grid_x) {
+  if (!ensure_decode_attr()) return -1;
+  cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid_x, 8, 8);
+  cfg.blockDim = dim3(kDecWarps * 32);
+  cfg.dynamicSmemBytes = kDynSmem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, decode_kernel, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -2;
+  }
+  return n;
 }
 
 int32_t ckv_lse_merge(const float* partials, int32_t n_parts, int64_t rows, uint16_t* out,
