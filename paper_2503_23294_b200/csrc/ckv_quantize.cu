@@ -46,6 +46,22 @@ __device__ __forceinline__ uint32_t exact_code(float x, float lo, float hi, floa
   return (uint32_t)n;
 }
 
+// Rare path: every element of a slice exactly (IEEE f64, reference tree); out of line so the
+// four quantize_chunk instantiations stay small.
+__device__ __noinline__ uint32_t exact_slice(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                             float lo, float hi, float qinv, float qmax, uint32_t base) {
+  const uint32_t w[4] = {w0, w1, w2, w3};
+  uint32_t acc = 0u, p = 1u;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t hb = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+    const float x = __half2float(__ushort_as_half((unsigned short)hb));
+    acc += exact_code(x, lo, hi, qinv, qmax) * p;
+    p *= base;
+  }
+  return acc;
+}
+
 // One 8-element lane slice of a row (4 lanes = one 32-element group): group min/max, codes,
 // packed little-endian lane word.  Fast path per element (7 instructions):
 //   r = (x - lo) * (qmax / span)   [x - lo in one mixed f16/f32 add]
@@ -94,18 +110,81 @@ __device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float
     for (int k = 0; k < e; ++k) p *= base;
     acc += __float_as_uint(y) * p;
   }
-  if (near) {  // rare: redo every element of this slice exactly (IEEE f64, reference tree)
-    acc = 0u;
-    uint32_t p = 1u;
+  if (near) acc = exact_slice(w[0], w[1], w[2], w[3], lo, hi, qinv, qmax, base);  // rare
+  return acc;
+}
+
+// One 32-row chunk of K (ISV = false) or V rows -> codes and (lo, hi) metadata staged in shared
+// memory in the tile-native layout (2 tiles).  Lanes: sub = lane / 16 picks the row of a pair,
+// j = lane % 16 the 8-element slice (4 lanes = one 32-element group).  Returns whether a group's
+// scale needs the decode's wide-scale mode.
+// Staging offsets of the tile-native layout (ckv_common.cuh tile_off_*) for row
+// r = 2 (r4 + u) + sub and slice j, decomposed as
+//   (r4 >> 3) TB + ((r4 >> 2) & 1) X + u U + L(j, sub, hf)
+// so each store costs one add (the GPU parity tests read every arena back through
+// ckv_arena_export, i.e. through tile_off_*, and compare with the reference bit for bit).
+template <int BITS, bool ISV> struct StageOff {
+  static constexpr int TB = BITS == 2 ? kTileBytes2 : kTileBytes4;
+  static constexpr int X = BITS == 2 ? 8 : 512;
+  static constexpr int U = ISV ? 16 : 128;
+  __device__ __forceinline__ static int lane(int j, int sub) {
+    if (BITS == 2) return ISV ? (j >> 1) * 64 + (j & 1) * 4 + sub * 2
+                              : sub * 64 + (j >> 2) * 16 + ((j >> 1) & 1) * 4 + (j & 1) * 2;
+    return ISV ? (j >> 1) * 64 + (j & 1) * 8 + sub * 2
+               : sub * 64 + (j >> 2) * 16 + ((j & 3) >> 1) * 8 + (j & 1) * 2;  // hf = 1: + 4
+  }
+};
+template <bool ISV> struct MetaStageOff {
+  static constexpr int TB = kTileBytesMeta;
+  static constexpr int X = ISV ? 8 : 4;
+  static constexpr int U = ISV ? 16 : 64;
+  __device__ __forceinline__ static int lane(int j, int sub) {  // lo; hi at + (ISV ? 4 : 2)
+    return ISV ? (j >> 2) * 64 + sub * 2 : sub * 32 + (j >> 2) * 8;
+  }
+};
+
+// One 32-row chunk of K (ISV = false) or V rows -> codes and (lo, hi) metadata staged in shared
+// memory in the tile-native layout (2 tiles).  Lanes: sub = lane / 16 picks the row of a pair,
+// j = lane % 16 the 8-element slice (4 lanes = one 32-element group).  Returns whether a group's
+// scale needs the decode's wide-scale mode.
+template <int BITS, bool ISV>
+__device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, int sub, int j,
+                                               unsigned char* sc, unsigned char* sm, bool& bad) {
+  using SO = StageOff<BITS, ISV>;
+  using MO = MetaStageOff<ISV>;
+  bool wide = false;
+  const int lc = SO::lane(j, sub), lm = MO::lane(j, sub);
+#pragma unroll 1
+  for (int r4 = 0; r4 < 16; r4 += 4) {
+    uint4 xs[4];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t hb = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-      const float x = __half2float(__ushort_as_half((unsigned short)hb));
-      acc += exact_code(x, lo, hi, qinv, qmax) * p;
-      p *= base;
+    for (int u = 0; u < 4; ++u)  // four 16-byte loads in flight per lane
+      xs[u] = __ldg(reinterpret_cast<const uint4*>(src + (2 * (r4 + u) + sub) * sT) + j);
+    unsigned char* cb = sc + (r4 >> 3) * SO::TB + ((r4 >> 2) & 1) * SO::X + lc;
+    unsigned char* mb = sm + (r4 >> 3) * MO::TB + ((r4 >> 2) & 1) * MO::X + lm;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+      float lo, hi;
+      const uint32_t packed = quantize_slice<BITS>(w, lo, hi, bad, wide);
+      if (BITS == 2) {
+        *reinterpret_cast<uint16_t*>(cb + u * SO::U) = (uint16_t)packed;
+      } else {
+        *reinterpret_cast<uint16_t*>(cb + u * SO::U) = (uint16_t)packed;
+        *reinterpret_cast<uint16_t*>(cb + u * SO::U + 4) = (uint16_t)(packed >> 16);
+      }
+      if ((j & 3) == 0) {
+        const uint32_t lh = h2_as_u32(__floats2half2_rn(lo, hi));
+        if (ISV) {
+          *reinterpret_cast<uint16_t*>(mb + u * MO::U) = (uint16_t)lh;
+          *reinterpret_cast<uint16_t*>(mb + u * MO::U + 4) = (uint16_t)(lh >> 16);
+        } else {
+          *reinterpret_cast<uint32_t*>(mb + u * MO::U) = lh;
+        }
+      }
     }
   }
-  return acc;
+  return wide;
 }
 
 // One warp per (layer, sequence, kv-head, destination chunk slot).  Slot p < N takes source
@@ -163,42 +242,13 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       }
       continue;
     }
-    bool wide = false;
-#pragma unroll 1
-    for (int r4 = 0; r4 < 16; r4 += 4) {
-      uint4 xs[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)  // four 16-byte loads in flight per lane
-        xs[u] = __ldg(reinterpret_cast<const uint4*>(src + (2 * (r4 + u) + sub) * sT) + j);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = 2 * (r4 + u) + sub;
-        const uint32_t w[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
-        float lo, hi;
-        const int rt = r & 15;
-        unsigned char* sc = reinterpret_cast<unsigned char*>(s_codes[warp]);
-        if (tier == 0) {
-          const uint32_t packed = quantize_slice<2>(w, lo, hi, bad, wide);
-          const int off = (r >> 4) * kTileBytes2 + (tsel ? tile_off_v2(rt, j >> 1, j & 1) : tile_off_k2(rt, j >> 1, j & 1));
-          *reinterpret_cast<uint16_t*>(sc + off) = (uint16_t)packed;
-        } else {
-          const uint32_t packed = quantize_slice<4>(w, lo, hi, bad, wide);
-          unsigned char* t4 = sc + (r >> 4) * kTileBytes4;
-          *reinterpret_cast<uint16_t*>(t4 + (tsel ? tile_off_v4(rt, j, 0) : tile_off_k4(rt, j, 0))) = (uint16_t)packed;
-          *reinterpret_cast<uint16_t*>(t4 + (tsel ? tile_off_v4(rt, j, 1) : tile_off_k4(rt, j, 1))) = (uint16_t)(packed >> 16);
-        }
-        if ((j & 3) == 0) {
-          unsigned char* sm = reinterpret_cast<unsigned char*>(s_meta[warp]) + (r >> 4) * kTileBytesMeta;
-          const uint32_t lh = h2_as_u32(__floats2half2_rn(lo, hi));
-          if (tsel) {
-            *reinterpret_cast<uint16_t*>(sm + tile_off_vm(rt, j >> 2, 0)) = (uint16_t)lh;
-            *reinterpret_cast<uint16_t*>(sm + tile_off_vm(rt, j >> 2, 1)) = (uint16_t)(lh >> 16);
-          } else {
-            *reinterpret_cast<uint32_t*>(sm + tile_off_km(rt, j >> 2, 0)) = lh;
-          }
-        }
-      }
-    }
+    unsigned char* sc = reinterpret_cast<unsigned char*>(s_codes[warp]);
+    unsigned char* sm = reinterpret_cast<unsigned char*>(s_meta[warp]);
+    bool wide;
+    if (tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, sub, j, sc, sm, bad)
+                               : quantize_chunk<2, false>(src, sT, sub, j, sc, sm, bad);
+    else wide = tsel ? quantize_chunk<4, true>(src, sT, sub, j, sc, sm, bad)
+                     : quantize_chunk<4, false>(src, sT, sub, j, sc, sm, bad);
     __syncwarp();
     // 128-bit coalesced stores of the packed chunk (2 tiles: 1 KB INT2 / 2 KB INT4) and its
     // metadata (2 x 256 B); tiles of a segment are contiguous
