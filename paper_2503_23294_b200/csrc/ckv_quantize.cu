@@ -92,24 +92,27 @@ __device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float
   bad |= !(isfinite(lo) && isfinite(hi));  // any inf / nan in the group reaches lo or hi
   wide |= span * (1.0f / qmax) > 4000.0f;
   if (!(span > 0.0f)) return 0u;  // constant group: codes 0 (also nan groups; flagged above)
-  const float qinv = qmax / span;
+  // qmax / span via the approximate reciprocal (<= 2 ulp): the candidate r below stays within
+  // 2^-17 of the exact rational, well inside the 2^-14 guard band that triggers the exact path
+  float rs;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(span));
+  const float qinv = qmax * rs;
   uint32_t acc = 0u - kM * kSum;
-  bool near = false;
-  float r[8];
+  float dmax = 0.0f;  // max |r - round(r)| over the slice
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const uint32_t hb = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
     float d;
     asm("{.reg .f16 xh; mov.b16 xh, %1; sub.rn.f32.f16 %0, xh, %2;}" : "=f"(d) : "h"((unsigned short)hb), "f"(lo));
-    r[e] = d * qinv;
-    const float y = r[e] + 12582912.0f;
-    const float dd = r[e] - (y - 12582912.0f);
-    near |= fabsf(dd) > 0.5f - (1.0f / 16384.0f);
+    const float r = d * qinv;
+    const float y = r + 12582912.0f;
+    dmax = fmaxf(dmax, fabsf(r - (y - 12582912.0f)));
     uint32_t p = 1u;
 #pragma unroll
     for (int k = 0; k < e; ++k) p *= base;
     acc += __float_as_uint(y) * p;
   }
+  const bool near = dmax > 0.5f - (1.0f / 16384.0f);
   if (near) acc = exact_slice(w[0], w[1], w[2], w[3], lo, hi, qinv, qmax, base);  // rare
   return acc;
 }

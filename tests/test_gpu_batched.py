@@ -234,3 +234,28 @@ def test_fp16_only_and_int_only_units_with_many_splits():
         out = cache.decode(torch.from_numpy(q).cuda(), splits=s).float().cpu().numpy()
         for b in range(B):
             _check_unit(cache, 0, b, 0, k, v, tiers[b], q[0, b, :m], out[0, b, :m])
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+def test_adversarial_fp16_rows_through_fused_build(bits):
+    """The reference's adversarial fp16 rows (grid midpoints, exact ties, subnormals, +-60000;
+    tests/golden/make_golden.py) through the fused reorder/quantize/pack kernel (fast fp32
+    candidate + guarded exact path, tile-native staging) and back through ckv_arena_export:
+    packed words and f64 metadata bit-identical to the reference's quantize_groups/pack_codes."""
+    g = load_golden("fp16_rows.npz")
+    x = g["x16"]
+    n = (x.shape[0] // 32) * 32
+    rows = torch.from_numpy(x[:n]).cuda()
+    k = rows.reshape(1, 1, n, 1, 128)
+    v = torch.flip(rows, dims=[0]).contiguous().reshape(1, 1, n, 1, 128)  # different V rows
+    tier = 0 if bits == 2 else 1
+    cache = batched.build_cache_batched(k, v, _search_from_tiers(np.full((1, n // 32), tier, np.uint8)))
+    ex = cache.export_unit(0, 0, 0)
+    words = n * 128 * bits // 32
+    kb, vb = (ex.k_q2, ex.v_q2) if bits == 2 else (ex.k_q4, ex.v_q4)
+    assert np.array_equal(kb.packed, g[f"packed{bits}"][:words])
+    assert np.array_equal(kb.scales.view(np.uint64), g[f"scales{bits}"][:n * 4].view(np.uint64))
+    assert np.array_equal(kb.zero_points.view(np.uint64), g[f"zps{bits}"][:n * 4].view(np.uint64))
+    want_v = O.quantize_groups(x[:n][::-1].astype(np.float64), bits, 32)
+    assert np.array_equal(vb.packed, O.pack_codes(want_v[0].reshape(-1), bits))
+    assert np.array_equal(vb.scales.view(np.uint64), want_v[1].view(np.uint64))
