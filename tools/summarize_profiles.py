@@ -24,9 +24,9 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 KEYS = [
-    ("gpu__time_duration.sum", "duration (us)"),
-    ("dram__bytes_read.sum", "DRAM read (MB)"),
-    ("dram__bytes_write.sum", "DRAM write (MB)"),
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput (% of peak)"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active (%)"),
@@ -53,11 +53,12 @@ def summarize(rep):
     r = list(csv.reader(io.StringIO(ncu(rep, "raw"))))
     hdr, units, v = r[0], r[1], r[2]
     vals = dict(zip(hdr, v))
+    unit = dict(zip(hdr, units))
     name = vals.get("Kernel Name", "?")
     metrics = {}
     for key, label in KEYS:
         if key in vals:
-            metrics[label] = vals[key]
+            metrics[label] = f"{vals[key]} {unit.get(key, '')}".strip()
     stalls = {}
     for h, x in vals.items():
         if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued"):
@@ -88,8 +89,10 @@ def summarize(rep):
             total += n
     opmix = [(op, 100 * n / total) for op, n in ops.most_common(16)] if total else []
     dram = None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     try:
-        dram = (float(vals["dram__bytes_read.sum"]) + float(vals["dram__bytes_write.sum"])) * 1e6
+        dram = sum(float(vals[k].replace(",", "")) * scale[unit[k]]
+                   for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     except (KeyError, ValueError):
         pass
     return name, metrics, stall_mix, opmix, dram
