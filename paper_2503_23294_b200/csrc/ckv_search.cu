@@ -3,7 +3,9 @@
 //   compute_thresholds  retrieval.py:222-237  (two roundings each, no FMA)
 //   assign_tiers        retrieval.py:240-250  (strict rule, ties -> INT4)
 //   stable grouping     kv_store.py:190-192,204-206 (perm = INT2 || INT4 || FP16)
-// One CTA per sequence; everything stays on the device.
+// Scores: a grid over (chunk blocks, sequences), four chunks per warp with all their loads in
+// flight (the embeddings are the only sizeable input).  Thresholds, tiers and the stable
+// partition: one CTA per sequence.  Everything stays on the device.
 #include <math.h>
 
 #include "ckv_common.cuh"
@@ -33,10 +35,47 @@ __device__ __forceinline__ double block_reduce(double v, bool is_min, double* re
   return red[0];
 }
 
+constexpr int kScoreWarps = 8, kScorePerWarp = 4;
+
+// raw cosine per chunk: q . c / (|q| |c|)  (retrieval.py:202); NaN marks zero-norm chunks
+__global__ void __launch_bounds__(kScoreWarps * 32)
+score_kernel(const double* __restrict__ emb, const double* __restrict__ emb_norm,
+             const double* __restrict__ q, const double* __restrict__ q_norm,
+             const int32_t* __restrict__ seq_chunks, int n_max, int dim, double* __restrict__ scores) {
+  const int b = blockIdx.y;
+  const int n = seq_chunks ? min(seq_chunks[b], n_max) : n_max;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = (blockIdx.x * kScoreWarps + warp) * kScorePerWarp;
+  if (i0 >= n) return;
+  const double* Q = q + (int64_t)b * dim;
+  const double* E = emb + ((int64_t)b * n_max + i0) * dim;
+  double s[kScorePerWarp];
+#pragma unroll
+  for (int k = 0; k < kScorePerWarp; ++k) s[k] = 0.0;
+#pragma unroll 4
+  for (int d = lane; d < dim; d += 32) {
+    const double qd = __ldg(Q + d);
+#pragma unroll
+    for (int k = 0; k < kScorePerWarp; ++k)
+      if (i0 + k < n) s[k] = fma(qd, __ldg(E + (int64_t)k * dim + d), s[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < kScorePerWarp; ++k)
+    for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+  if (lane < kScorePerWarp && i0 + lane < n) {
+    double v = s[0];
+#pragma unroll
+    for (int k = 1; k < kScorePerWarp; ++k) if (lane == k) v = s[k];
+    const double cn = emb_norm[(int64_t)b * n_max + i0 + lane];
+    scores[(int64_t)b * n_max + i0 + lane] = cn > 0.0 ? __ddiv_rn(v, __dmul_rn(q_norm[b], cn)) : NAN;
+  }
+}
+
+// scored != 0: `scores` holds score_kernel's raw cosines (zero-norm substitution still to do);
+// scored == 0: `scores` is caller input (compute_thresholds / assign_tiers entries).
 __global__ void __launch_bounds__(kSearchThreads)
-search_kernel(const double* __restrict__ emb, const double* __restrict__ emb_norm,
-              const double* __restrict__ q, const double* __restrict__ q_norm,
-              const int32_t* __restrict__ seq_chunks, int n_max, int dim, double alpha,
+search_kernel(int scored, const double* __restrict__ q_norm,
+              const int32_t* __restrict__ seq_chunks, int n_max, double alpha,
               double beta, int ab_gt_1, const double* __restrict__ t_in,
               double* __restrict__ scores, double* __restrict__ stats,
               uint8_t* __restrict__ tiers, uint32_t* __restrict__ perm,
@@ -46,29 +85,15 @@ search_kernel(const double* __restrict__ emb, const double* __restrict__ emb_nor
   __shared__ int tot[3];
   const int b = blockIdx.x;
   const int n = seq_chunks ? min(seq_chunks[b], n_max) : n_max;
-  const double* E = emb ? emb + (int64_t)b * n_max * dim : nullptr;
-  const double* EN = emb ? emb_norm + (int64_t)b * n_max : nullptr;
-  const double* Q = emb ? q + (int64_t)b * dim : nullptr;
-  const double qn = emb ? q_norm[b] : 1.0;
+  const double qn = scored ? q_norm[b] : 1.0;
   double* S = scores + (int64_t)b * n_max;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t flag = 0;
   if (qn == 0.0) flag |= CKV_FLAG_ZERO_QUERY;
   if (n == 0) flag |= CKV_FLAG_EMPTY_SCORES;
 
   double lo = INFINITY, hi = -INFINITY;
-  if (E != nullptr) {
-    // raw cosine per chunk: q . c / (|q| |c|)  (retrieval.py:202); NaN marks zero-norm chunks
-    for (int i = warp; i < n; i += nwarps) {
-      const double* c = E + (int64_t)i * dim;
-      double s = 0.0;
-      for (int d = lane; d < dim; d += 32) s = fma(Q[d], c[d], s);
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) {
-        const double cn = EN[i];
-        S[i] = cn > 0.0 ? __ddiv_rn(s, __dmul_rn(qn, cn)) : NAN;
-      }
-    }
+  if (scored) {
     __syncthreads();
     // zero-norm chunks score min(valid), 0.0 if none valid (retrieval.py:217-219)
     double lmin = INFINITY;
@@ -164,9 +189,15 @@ extern "C" int32_t ckv_search(const double* emb, const double* emb_norm, const d
   if (!(alpha >= 0.0 && alpha <= 1.0 && beta >= 0.0 && beta <= 1.0)) return CKV_ERR_ARG;
   if (batch == 0) return CKV_OK;
   const int ab_gt_1 = (alpha + beta) > 1.0;
+  if (emb && n_chunks > 0) {
+    const int per_cta = kScoreWarps * kScorePerWarp;
+    score_kernel<<<dim3((unsigned)cdiv(n_chunks, per_cta), (unsigned)batch), kScoreWarps * 32, 0,
+                   as_stream(stream)>>>(emb, emb_norm, q, q_norm, seq_chunks, n_chunks, dim, scores);
+    CKV_LAUNCH_CHECK();
+  }
   search_kernel<<<batch, kSearchThreads, 0, as_stream(stream)>>>(
-      emb, emb_norm, q, q_norm, seq_chunks, n_chunks, dim, alpha, beta, ab_gt_1, nullptr, scores,
-      stats, tiers, perm, seg_counts, flags);
+      emb ? 1 : 0, q_norm, seq_chunks, n_chunks, alpha, beta, ab_gt_1, nullptr, scores, stats,
+      tiers, perm, seg_counts, flags);
   CKV_LAUNCH_CHECK();
   return CKV_OK;
 }
@@ -178,8 +209,8 @@ extern "C" int32_t ckv_assign_tiers(const double* scores, const double* threshol
   if (batch < 0 || n_chunks < 0 || !scores || !thresholds) return CKV_ERR_ARG;
   if (batch == 0) return CKV_OK;
   search_kernel<<<batch, kSearchThreads, 0, as_stream(stream)>>>(
-      nullptr, nullptr, nullptr, nullptr, seq_chunks, n_chunks, 0, 0.0, 0.0, 0, thresholds,
-      const_cast<double*>(scores), stats, tiers, perm, seg_counts, flags);
+      0, nullptr, seq_chunks, n_chunks, 0.0, 0.0, 0, thresholds, const_cast<double*>(scores), stats,
+      tiers, perm, seg_counts, flags);
   CKV_LAUNCH_CHECK();
   return CKV_OK;
 }
