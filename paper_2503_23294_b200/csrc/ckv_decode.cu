@@ -196,10 +196,12 @@ template <int I> struct K4 {
 struct WarpState {
   float acc[8][4];  // O^T C-fragments, m-tile mt: rows d = 16g+mt (c0,c1), 16g+8+mt (c2,c3)
   float lacc[2];    // sum_t p_t * lo_t for the group of row g, cols 2c, 2c+1
+  float lsq[2];     // sum_t p_t over the quantized tiles (complete, from the lo MMA's ones rows)
   float mrun[2];    // running max (log2 domain) for cols 2c, 2c+1
   float lsum[2];
 };
 
+template <bool FADD_SUM>
 __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint32_t& bp0,
                                              uint32_t& bp1) {
   // Lazy online softmax: keep the running max unless a score exceeds it by more than the
@@ -221,13 +223,16 @@ __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint3
       st.acc[mt][0] *= f0; st.acc[mt][1] *= f1; st.acc[mt][2] *= f0; st.acc[mt][3] *= f1;
     }
     st.lacc[0] *= f0; st.lacc[1] *= f1;
+    st.lsq[0] *= f0; st.lsq[1] *= f1;
     st.lsum[0] *= f0; st.lsum[1] *= f1;
     st.mrun[0] = n0; st.mrun[1] = n1;
   }
   const float p0 = fast_exp2(s[0] - st.mrun[0]), p1 = fast_exp2(s[1] - st.mrun[1]);
   const float p2 = fast_exp2(s[2] - st.mrun[0]), p3 = fast_exp2(s[3] - st.mrun[1]);
-  st.lsum[0] += p0 + p2;
-  st.lsum[1] += p1 + p3;
+  if (FADD_SUM) {  // else the lo MMA of the tile's P.V sums P (rows g+8 of its A are ones)
+    st.lsum[0] += p0 + p2;
+    st.lsum[1] += p1 + p3;
+  }
   bp0 = movmatrix_trans(h2_as_u32(__floats2half2_rn(p0, p1)));  // (P[g][2c], P[g][2c+1])
   bp1 = movmatrix_trans(h2_as_u32(__floats2half2_rn(p2, p3)));  // (P[g][8+2c], P[g][9+2c])
 }
@@ -256,11 +261,16 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a
   mma_16816(d, a0, a1, a2, a3, b.x, b.y);
 }
 
+// The V zero-point term sum_t p_t lo_t (A rows g) and, on the A rows g+8 set to fp16 ones, the
+// tile's row sums sum_t p_t of the same fp16 P the P.V MMAs use.
 __device__ __forceinline__ void lo_mma(WarpState& st, uint32_t a0, uint32_t a2, uint32_t bp0, uint32_t bp1) {
-  float t[4] = {st.lacc[0], st.lacc[1], 0.f, 0.f};
-  mma_16816(t, a0, 0u, a2, 0u, bp0, bp1);
+  constexpr uint32_t kOnes = 0x3C003C00u;
+  float t[4] = {st.lacc[0], st.lacc[1], st.lsq[0], st.lsq[1]};
+  mma_16816(t, a0, kOnes, a2, kOnes, bp0, bp1);
   st.lacc[0] = t[0];
   st.lacc[1] = t[1];
+  st.lsq[0] = t[2];
+  st.lsq[1] = t[3];
 }
 
 // ---- quantized tiles from a shared-memory stage ---------------------------------------
@@ -467,7 +477,7 @@ __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf
   if (g >= valid) { s[0] = -INFINITY; s[1] = -INFINITY; }
   if (g + 8 >= valid) { s[2] = -INFINITY; s[3] = -INFINITY; }
   uint32_t bp0, bp1;
-  softmax_tile(s, st, bp0, bp1);
+  softmax_tile<true>(s, st, bp0, bp1);
   const int toks[4] = {2 * c, 2 * c + 1, 2 * c + 8, 2 * c + 9};
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
@@ -570,7 +580,7 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, i
     float s0[4];
     qk_any<EXACT>(t < n2t, cur, mo, qs, mg, s0);
     uint32_t bp0, bp1;
-    softmax_tile(s0, st, bp0, bp1);
+    softmax_tile<EXACT>(s0, st, bp0, bp1);
     while (true) {
       const int tn = t + kDecWarps;
       issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, a, src, mo, put);
@@ -594,7 +604,7 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, i
         pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
       }
       __syncwarp();  // slot `cur` may be refilled from now on
-      softmax_tile(sn, st, bp0, bp1);
+      softmax_tile<EXACT>(sn, st, bp0, bp1);
       cur = nx;
       t = tn;
     }
@@ -725,6 +735,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) st.acc[mt][0] = st.acc[mt][1] = st.acc[mt][2] = st.acc[mt][3] = 0.f;
   st.lacc[0] = st.lacc[1] = 0.f;
+  st.lsq[0] = st.lsq[1] = 0.f;
   st.mrun[0] = st.mrun[1] = -INFINITY;
   st.lsum[0] = st.lsum[1] = 0.f;
 
@@ -752,6 +763,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
     st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
   }
+  st.lsum[0] += st.lsq[0];  // already summed over the 16 tokens of every tile
+  st.lsum[1] += st.lsq[1];
   __syncthreads();  // ring -> merge buffer reuse
   if (trace) tr[8] = gtime();
   float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0][0]);
