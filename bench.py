@@ -44,6 +44,7 @@ PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
 
 CFG2 = dict(layers=32, batch=8, kv_heads=8, q_per_kv=4, context=32768, head_dim=128)
 CFG5 = dict(layers=32, batch=1, kv_heads=8, context=131072, head_dim=128)
+CFG3 = dict(layers=40, batch=1, kv_heads=40, q_per_kv=1, context=131072, head_dim=128)
 
 
 def load_workload(ctx, seed):
@@ -299,6 +300,120 @@ def bench_prefill(torch, dev, steps=3, profile=False):
     }
 
 
+def run_cfg3(args, torch, dist, dev, rank, world, local):
+    """cfg3: Llama-2-13B shape (40 layers x 40 MHA heads, d128), 128K context, batch 1.  Every
+    rank owns a chunk-aligned 1/N slice of each tier segment (sequence split-KV); a decode step
+    is 40 per-layer decode_partial launches (PDL-chained), one all_gather of all layers'
+    (acc, m, l) partials (NCCL) and the LSE merge.  Strong scaling: the cache is fixed."""
+    from paper_2503_23294_b200 import batched, distributed, retrieval
+
+    c = CFG3
+    L, B, H, m, T, D = c["layers"], c["batch"], c["kv_heads"], c["q_per_kv"], c["context"], c["head_dim"]
+    wl = load_workload(T, 0)
+    search = retrieval.search_batched(wl["emb"][None], wl["norm"][None], wl["q"][None],
+                                      np.array([wl["qnorm"]]), 0.6, 0.1)
+    if not np.array_equal(search.tiers.cpu().numpy()[0], wl["tiers"]):
+        raise SystemExit("128K tier map differs from the reference's")
+    cache, perm_r = distributed.sequence_shard_cache(search, L, H, [T], world, rank, decode_capacity=128,
+                                                     device=dev)
+    g = torch.Generator(device=dev)
+    for l in range(L):  # the full context's K/V, one layer at a time (same on every rank)
+        g.manual_seed(4321 + l)
+        k = torch.randn((1, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+        v = torch.randn((1, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+        cache.build(k, v, perm_r, layer=l)
+        del k, v
+    g.manual_seed(99)
+    q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
+    Hq = H * m
+    parts = torch.empty((L * B * Hq, D + 2), dtype=torch.float32, device=dev)
+    splits = args.splits or cache.default_splits(m, 1)
+
+    def local_decode(qq):
+        for l in range(L):
+            cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
+                                 out=parts[l * B * Hq:(l + 1) * B * Hq])
+
+    def step(qq):
+        local_decode(qq)
+        gathered = distributed.exchange_partials(parts) if world > 1 else parts[None]
+        return batched.lse_merge(gathered)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(max(args.warmup, 3)):
+        step(q)
+    with ClockSampler(local) as clk:
+        ms = timed(lambda: step(q), args.steps)
+    ms_local = timed(lambda: local_decode(q), args.steps)
+    my_bytes = cache.algorithmic_bytes(m)
+    tot = torch.tensor([float(my_bytes)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tot)
+    step_bytes = float(tot.item())
+    value = step_bytes / (ms * 1e-3) / 1e9
+
+    # end to end: pinned host q -> device, step, merged output -> pinned host
+    qh = q.cpu().pin_memory()
+    oh = torch.empty((L * B * Hq, D), dtype=torch.float16, pin_memory=True)
+    qd = torch.empty_like(q)
+
+    def e2e_step():
+        qd.copy_(qh, non_blocking=True)
+        oh.copy_(step(qd), non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    e2e_ms = timed(e2e_step, args.steps)
+    if rank == 0:
+        peak, peak_kind = measured_peak_gbs()
+        per_rank_gbs = my_bytes / (ms_local * 1e-3) / 1e9
+        counts = search.seg_counts.cpu().numpy()[0]
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
+            "data": "synthetic (fp16 N(0,1) K/V/q; reference search tier map, 128K seed 0)",
+            "config": {"workload": "cfg3: Llama-2-13B 40 layers x 40 MHA heads d128, 128K ctx, batch 1, "
+                                   "sequence split-KV across the GPUs",
+                       "global_batch": B, "seq_len": T, "parallelism": f"seq-split x{world}",
+                       "tier_fractions_int2_int4_fp16": [round(float(x) / counts.sum(), 4) for x in counts],
+                       "launch": "per-layer decode_partial (40 PDL-chained launches) + all_gather + merge",
+                       "splits": splits, "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
+            "tokens_per_s": round(B / (ms * 1e-3), 1),
+            "algorithmic_bytes_per_step": int(step_bytes),
+            "local_decode_ms": round(ms_local, 4),
+            "exchange_merge_ms": round(ms - ms_local, 4),
+            "roofline": {"bound": "hbm", "achieved": round(per_rank_gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(per_rank_gbs / peak, 4), "peak_kind": peak_kind,
+                         "traffic": None},
+            "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(oh.numel() * 2)},
+            "gpu_launches": args.steps * (L + 1),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -308,6 +423,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--splits", type=int, default=None)
+    ap.add_argument("--workload", choices=["cfg2", "cfg3"], default="cfg2",
+                    help="cfg2: batch-sharded 32K GQA decode (default); cfg3: 128K MHA decode with "
+                         "sequence split-KV across the ranks (NCCL all-gather + LSE merge)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -329,6 +447,12 @@ def main():
     def barrier():
         if world > 1:
             dist.barrier()
+
+    if args.workload == "cfg3":
+        run_cfg3(args, torch, dist, dev, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     cache, q, search = build_cfg2(torch, dev, rank)
     L, B = cache.L, cache.B

@@ -119,23 +119,25 @@ class BatchedKVCache:
         return _lib.Arena(ptr("codes2"), ptr("meta2"), ptr("codes4"), ptr("meta4"), ptr("fp"),
                           ptr("span_flags"), self.rows2, self.rows4, self.rows_fp)
 
-    def build(self, k, v, perm, check=True):
-        """ckv_reorder_quantize_pack over every unit; perm i32/u32 [B, max_chunks]."""
+    def build(self, k, v, perm, check=True, layer=0):
+        """ckv_reorder_quantize_pack over every unit of layers [layer, layer + L'); k, v fp16
+        [L', B, T, H, 128] (L' = L for the whole cache at once, or a slice so that a cache
+        larger than its fp16 source can be built layer by layer); perm i32/u32 [B, max_chunks]."""
         if k.dtype != torch.float16 or v.dtype != torch.float16:
             raise ValueError("batched build expects fp16 K/V")
         if k.shape != v.shape or k.stride() != v.stride():
             raise ValueError("k and v must have equal shape and strides")
         L, B, T, H, D = k.shape
-        if (L, B, H) != (self.L, self.B, self.H) or D != HEAD_DIM or k.stride(4) != 1:
+        if layer < 0 or layer + L > self.L or (B, H) != (self.B, self.H) or D != HEAD_DIM or k.stride(4) != 1:
             raise ValueError("K/V shape does not match the cache")
         perm = kernels.to_dev(perm, torch.int32)
-        self.k["span_flags"].zero_()
-        self.v["span_flags"].zero_()
+        self.k["span_flags"][layer:layer + L].zero_()
+        self.v["span_flags"][layer:layer + L].zero_()
         flag = torch.zeros(1, dtype=torch.int32, device=k.device)
         _lib.call("ckv_reorder_quantize_pack", _lib.ptr(k), _lib.ptr(v), L, B, H, k.stride(0),
                   k.stride(1), k.stride(2), k.stride(3), _lib.ptr(perm), perm.shape[1],
                   _lib.ptr(self.seq), int(self.seq_host[:, 7].max()) if B else 0,
-                  self.arena("k"), self.arena("v"), _lib.ptr(flag), _lib.stream())
+                  self.arena("k", layer), self.arena("v", layer), _lib.ptr(flag), _lib.stream())
         if check and int(flag.item()) & _lib.FLAG_NONFINITE:
             raise ValueError("matrix contains non-finite values")
         return self
@@ -208,19 +210,25 @@ class BatchedKVCache:
                   _lib.DECODE_PDL if pdl else 0, _lib.stream())
         return out
 
-    def decode_partial(self, q, splits=None, scale=None):
-        """Unnormalised split-KV partials f32 [L*B*H*m, 130] = (acc[128], m (log2), l)."""
+    def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None):
+        """Unnormalised split-KV partials f32 [L'*B*H*m, 130] = (acc[128], m (log2), l) for q
+        fp16 [L', B, H*m, 128] over layers [layer, layer + L') (per-layer launches: L' = 1,
+        pdl as in decode); `out` may be a preallocated [L'*B*H*m, 130] view."""
         L, B, Hq, D = q.shape
-        if (L, B) != (self.L, self.B) or D != HEAD_DIM or Hq % self.H:
+        if B != self.B or layer < 0 or layer + L > self.L or D != HEAD_DIM or Hq % self.H:
             raise ValueError("q shape does not match the cache")
         m = Hq // self.H
-        splits = self.default_splits(m) if splits is None else int(splits)
-        part = torch.empty((L * B * Hq, HEAD_DIM + 2), dtype=torch.float32, device=q.device)
-        ws = self._workspace(m, splits, L, 0)
+        splits = self.default_splits(m, L) if splits is None else int(splits)
+        part = out if out is not None else torch.empty((L * B * Hq, HEAD_DIM + 2), dtype=torch.float32,
+                                                       device=q.device)
+        if part.shape != (L * B * Hq, HEAD_DIM + 2) or not part.is_contiguous():
+            raise ValueError("partials buffer must be contiguous [L*B*Hq, 130]")
+        ws = self._workspace(m, splits, L, layer)
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
-        _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k"),
-                  self.arena("v"), _lib.ptr(self.seq), L, B, self.H, m, scale, splits,
-                  ws, None, 0, 0, _lib.ptr(part), 0, _lib.stream())
+        _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1),
+                  self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H,
+                  m, scale, splits, ws, None, 0, 0, _lib.ptr(part), _lib.DECODE_PDL if pdl else 0,
+                  _lib.stream())
         return part
 
     def append(self, k_new, v_new):

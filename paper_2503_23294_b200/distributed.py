@@ -47,18 +47,16 @@ def sequence_shard_plan(seg_counts, world, rank):
     return out, rank == world - 1
 
 
-def build_sequence_shard(k, v, search, world, rank, decode_capacity=128, check=True):
-    """This rank's BatchedKVCache for a sequence-split (split-KV) layout.
-
-    k, v fp16 [L, B, T, H, 128] (the full context, e.g. prefilled redundantly or loaded
-    per rank); search = SearchResult of the full context (tiers are global).
-    """
-    L, B, T, H, D = k.shape
+def sequence_shard_cache(search, layers, kv_heads, context, world, rank, decode_capacity=128,
+                         device=None):
+    """This rank's empty BatchedKVCache for a sequence-split (split-KV) layout and the perm of
+    its chunks (source chunk per destination slot), to be filled with ``cache.build(k, v,
+    perm_r[, layer=...])`` from the full-context K/V (all layers at once or layer by layer)."""
     counts = search.seg_counts.cpu().numpy().astype(np.int64)
+    B = counts.shape[0]
     plan, owns_tail = sequence_shard_plan(counts, world, rank)
     perm = search.perm
     n_max = perm.shape[1]
-    rows = []
     n2r = plan[:, 1] - plan[:, 0]
     n4r = plan[:, 3] - plan[:, 2]
     nfr = plan[:, 5] - plan[:, 4]
@@ -71,10 +69,23 @@ def build_sequence_shard(k, v, search, world, rank, decode_capacity=128, check=T
     idx_d = torch.from_numpy(idx).to(perm.device)
     perm_r = torch.gather(perm, 1, idx_d.clamp(max=n_max - 1)) if n_max else perm
     n_glob = counts.sum(axis=1)
-    tail = T - CHUNK * n_glob
+    tail = np.asarray(context, np.int64).reshape(-1) - CHUNK * n_glob
     ctx_r = CHUNK * (n2r + n4r + nfr) + (tail if owns_tail else 0)
-    cache = BatchedKVCache(L, B, H, n2r, n4r, nfr, ctx_r, decode_capacity if owns_tail else 0,
-                           tail_src=CHUNK * n_glob, device=k.device)
+    cache = BatchedKVCache(layers, B, kv_heads, n2r, n4r, nfr, ctx_r,
+                           decode_capacity if owns_tail else 0, tail_src=CHUNK * n_glob,
+                           device=device or perm.device)
+    return cache, perm_r
+
+
+def build_sequence_shard(k, v, search, world, rank, decode_capacity=128, check=True):
+    """This rank's BatchedKVCache for a sequence-split (split-KV) layout.
+
+    k, v fp16 [L, B, T, H, 128] (the full context, e.g. prefilled redundantly or loaded
+    per rank); search = SearchResult of the full context (tiers are global).
+    """
+    L, B, T, H, D = k.shape
+    cache, perm_r = sequence_shard_cache(search, L, H, np.full(B, T), world, rank, decode_capacity,
+                                         device=k.device)
     cache.build(k, v, perm_r, check=check)
     return cache
 
@@ -99,5 +110,5 @@ def split_kv_decode(cache: BatchedKVCache, q, group=None, splits=None):
     return out.view(q.shape)
 
 
-__all__ = ["batch_shard", "sequence_shard_plan", "build_sequence_shard", "exchange_partials",
-           "split_kv_decode"]
+__all__ = ["batch_shard", "sequence_shard_plan", "sequence_shard_cache", "build_sequence_shard",
+           "exchange_partials", "split_kv_decode"]

@@ -259,3 +259,29 @@ def test_adversarial_fp16_rows_through_fused_build(bits):
     want_v = O.quantize_groups(x[:n][::-1].astype(np.float64), bits, 32)
     assert np.array_equal(vb.packed, O.pack_codes(want_v[0].reshape(-1), bits))
     assert np.array_equal(vb.scales.view(np.uint64), want_v[1].view(np.uint64))
+
+
+def test_layer_by_layer_build_and_per_layer_partials():
+    """A cache built one layer at a time (build(..., layer=l)) equals the all-layers build, and
+    per-layer decode_partial launches into slices of one buffer equal the single launch
+    (the path bench.py's cfg3 uses for caches larger than their fp16 source)."""
+    rng = np.random.default_rng(41)
+    L, B, H, m, D, N = 3, 2, 2, 2, 128, 20
+    T = N * 32 + 7
+    k = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    q = torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16)).cuda()
+    s = _search_from_tiers(rng.choice([0, 0, 1, 2], size=(B, N)).astype(np.uint8))
+    full = batched.build_cache_batched(k, v, s)
+    counts = s.seg_counts.cpu().numpy()
+    per = batched.BatchedKVCache(L, B, H, counts[:, 0], counts[:, 1], counts[:, 2], [T] * B, device=k.device)
+    for l in range(L):
+        per.build(k[l:l + 1], v[l:l + 1], s.perm, layer=l)
+    for name in ("codes2", "meta2", "codes4", "meta4", "fp"):
+        assert torch.equal(full.k[name], per.k[name]) and torch.equal(full.v[name], per.v[name]), name
+    want = full.decode_partial(q)
+    got = torch.empty_like(want)
+    rows = B * H * m
+    for l in range(L):
+        per.decode_partial(q[l:l + 1], layer=l, pdl=l > 0, out=got[l * rows:(l + 1) * rows])
+    assert torch.max(torch.abs(batched.lse_merge(got[None]).float() - batched.lse_merge(want[None]).float())).item() < 2e-3
