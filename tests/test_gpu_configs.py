@@ -1,0 +1,142 @@
+"""GPU: BASELINE.json's five configurations as parity cases (bench.py measures cfg2, cfg3 and
+cfg5; here each config's shape, tier maps and features are checked against the CPU oracle on
+sampled units, with the tier maps from the device search asserted equal to the reference's).
+
+Bit-exact: tier maps, permutations, packed codes and f64 metadata.  Attention: 1e-2 abs and
+1e-2 of max|ref| against the reference's f64 mixed_decode_attention on the same fp16 inputs
+(north_star tolerance)."""
+
+import numpy as np
+import pytest
+import torch
+
+import bench
+from oracle import ckv_oracle as O
+from paper_2503_23294_b200 import batched, distributed, retrieval
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def _search(ctxs_seeds):
+    wls = [bench.load_workload(ctx, seed) for ctx, seed in ctxs_seeds]
+    s = retrieval.search_batched(np.stack([w["emb"] for w in wls]), np.stack([w["norm"] for w in wls]),
+                                 np.stack([w["q"] for w in wls]), np.array([w["qnorm"] for w in wls]),
+                                 0.6, 0.1)
+    tiers = s.tiers.cpu().numpy()
+    for i, w in enumerate(wls):
+        assert np.array_equal(tiers[i], w["tiers"]), "device search differs from the reference map"
+    return s, [w["tiers"] for w in wls]
+
+
+def _randn(shape, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.randn(shape, generator=g, device="cuda", dtype=torch.float16)
+
+
+def _check_unit(cache, out, kh, vh, qh, l, b, h, m, tiers, codes=True):
+    oc = O.build_cache(kh[l, b, :, h].astype(np.float64), vh[l, b, :, h].astype(np.float64), tiers, 32, 32)
+    if codes:
+        ex = cache.export_unit(l, b, h)
+        for name in ("k_q2", "v_q2", "k_q4", "v_q4"):
+            a, w = getattr(ex, name), getattr(oc, name)
+            assert np.array_equal(a.packed, w.packed), name
+            assert np.array_equal(a.scales.view(np.uint64), w.scales.view(np.uint64)), name
+            assert np.array_equal(a.zero_points.view(np.uint64), w.zero_points.view(np.uint64)), name
+    ref = O.mixed_decode_attention(qh[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+    got = out[l, b, h * m:(h + 1) * m].astype(np.float64)
+    err, scale = np.max(np.abs(got - ref)), max(np.max(np.abs(ref)), 1e-30)
+    assert err <= TOL * max(1.0, scale) and err / scale <= TOL, (l, b, h, err, scale)
+
+
+def test_cfg1_llama2_7b_single_layer_4k_mha():
+    """cfg1: 32 MHA heads x d128, 4K context, batch 1, tier map from the reference search
+    (106/20/2 chunks); every head checked."""
+    L, B, H, m, T = 1, 1, 32, 1, 4096
+    s, maps = _search([(T, 0)])
+    assert np.bincount(maps[0], minlength=3).tolist() == [106, 20, 2]
+    k, v, q = _randn((L, B, T, H, 128), 1), _randn((L, B, T, H, 128), 2), _randn((L, B, H * m, 128), 3)
+    cache = batched.build_cache_batched(k, v, s)
+    out = cache.decode(q).float().cpu().numpy()
+    kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
+    for h in range(H):
+        _check_unit(cache, out, kh, vh, qh, 0, 0, h, m, maps[0], codes=h < 4)
+
+
+def test_cfg2_llama3_8b_gqa_32k_batch8_per_layer():
+    """cfg2 shape (32 q / 8 kv heads -> m = 4, 32K, batch 8 with the reference's per-sequence
+    maps), reduced to 2 layers x 2 kv heads; per-layer PDL launches as in the bench."""
+    L, B, H, m, T = 2, 8, 2, 4, 32768
+    s, maps = _search([(T, b) for b in range(B)])
+    k, v, q = _randn((L, B, T, H, 128), 11), _randn((L, B, T, H, 128), 12), _randn((L, B, H * m, 128), 13)
+    cache = batched.build_cache_batched(k, v, s)
+    out = torch.empty_like(q)
+    for l in range(L):
+        cache.decode(q[l:l + 1], out=out[l:l + 1], layer=l, pdl=l > 0)
+    out = out.float().cpu().numpy()
+    kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
+    for b in range(B):
+        _check_unit(cache, out, kh, vh, qh, b % L, b, (b // L) % H, m, maps[b], codes=b < 2)
+
+
+def test_cfg3_llama2_13b_128k_sequence_split_kv():
+    """cfg3 shape (MHA m = 1, 128K, batch 1, the reference's 128K map) on 4 heads: the full
+    decode against the oracle, and the split-KV shards of 2 / 4 / 8 ranks merged by LSE equal
+    the full decode."""
+    L, B, H, m, T = 1, 1, 4, 1, 131072
+    s, maps = _search([(T, 0)])
+    k, v, q = _randn((L, B, T, H, 128), 21), _randn((L, B, T, H, 128), 22), _randn((L, B, H * m, 128), 23)
+    cache = batched.build_cache_batched(k, v, s)
+    full = cache.decode(q)
+    out = full.float().cpu().numpy()
+    kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
+    for h in (0, 3):
+        _check_unit(cache, out, kh, vh, qh, 0, 0, h, m, maps[0], codes=h == 0)
+    for world in (2, 4, 8):
+        parts = [distributed.build_sequence_shard(k, v, s, world, r).decode_partial(q) for r in range(world)]
+        merged = batched.lse_merge(torch.stack(parts)).view(q.shape).float()
+        assert torch.max(torch.abs(merged - full.float())).item() < 2e-3, world
+
+
+@pytest.mark.parametrize("kind", ["all_fp16", "all_int2", "skewed"])
+def test_cfg4_batch64_16k_bitwidth_mix(kind):
+    """cfg4: batch 64 x 16K (Llama-3-8B GQA m = 4, one kv head here) for the three maps of the
+    bitwidth-mix sweep; the skewed map takes the reference's 16K maps (sequence b: seed b % 8)."""
+    L, B, H, m, T = 1, 64, 1, 4, 16384
+    n = T // 32
+    if kind == "skewed":
+        maps = [bench.load_workload(T, b % 8)["tiers"] for b in range(B)]
+    else:
+        maps = [np.full(n, 2 if kind == "all_fp16" else 0, np.uint8)] * B
+    tiers = np.stack(maps).astype(np.float64)
+    s = retrieval.assign_tiers_batched(tiers, np.tile([[0.5, 1.5]], (B, 1)))
+    assert np.array_equal(s.tiers.cpu().numpy(), np.stack(maps))
+    k, v, q = _randn((L, B, T, H, 128), 31), _randn((L, B, T, H, 128), 32), _randn((L, B, H * m, 128), 33)
+    cache = batched.build_cache_batched(k, v, s)
+    out = cache.decode(q).float().cpu().numpy()
+    kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
+    for b in (0, 17, 42, 63):
+        _check_unit(cache, out, kh, vh, qh, 0, b, 0, m, maps[b], codes=b == 0)
+
+
+def test_cfg5_prefill_128k_codes_bit_exact():
+    """cfg5: search + reorder + INT4/INT2 pack of a 128K context (2 layers x 2 kv heads here):
+    permutation and every code / metadata word of sampled units bit-exact."""
+    L, B, H, T = 2, 1, 2, 131072
+    s, maps = _search([(T, 0)])
+    perm_ref, counts_ref = O.stable_perm(maps[0])
+    assert np.array_equal(s.perm.cpu().numpy()[0][:perm_ref.size], perm_ref)
+    assert np.array_equal(s.seg_counts.cpu().numpy()[0], counts_ref)
+    k, v = _randn((L, B, T, H, 128), 41), _randn((L, B, T, H, 128), 42)
+    cache = batched.build_cache_batched(k, v, s)
+    kh, vh = k.cpu().numpy(), v.cpu().numpy()
+    for l, h in ((0, 1), (1, 0)):
+        oc = O.build_cache(kh[l, 0, :, h].astype(np.float64), vh[l, 0, :, h].astype(np.float64), maps[0], 32, 32)
+        ex = cache.export_unit(l, 0, h)
+        for name in ("k_q2", "v_q2", "k_q4", "v_q4"):
+            a, w = getattr(ex, name), getattr(oc, name)
+            assert np.array_equal(a.packed, w.packed), name
+            assert np.array_equal(a.scales.view(np.uint64), w.scales.view(np.uint64)), name
+            assert np.array_equal(a.zero_points.view(np.uint64), w.zero_points.view(np.uint64)), name
+        assert np.array_equal(ex.k_fp[:oc.len_fp], oc.k_fp) and np.array_equal(ex.v_fp[:oc.len_fp], oc.v_fp)

@@ -46,7 +46,7 @@ def one(ctx, seed):
 
 def main():
     out = {}
-    for ctx, seeds in ((32768, range(8)), (131072, range(1)), (16384, range(8))):
+    for ctx, seeds in ((32768, range(8)), (131072, range(1)), (16384, range(8)), (4096, range(1))):
         for s in seeds:
             for k, v in one(ctx, s).items():
                 out[f"{ctx}_{s}_{k}"] = v
