@@ -68,10 +68,26 @@ __device__ __forceinline__ int64_t gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Probe points write shared memory and re-read g_trace each time, so nothing of the tracing
+// stays live in registers across the tile loop.
+__device__ __forceinline__ bool tracing() { return *reinterpret_cast<int64_t* volatile*>(&g_trace) != nullptr; }
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
+}
+
+// (split, kv head, layer, sequence) of this CTA, re-read from the special registers at each
+// call (volatile) so nothing derived from them stays live in registers across the tile loop.
+struct CtaIds {
+  int split, h, l, b;
+};
+__device__ __forceinline__ CtaIds cta_ids(int B) {
+  uint32_t x, y, z;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(x));
+  asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(y));
+  asm volatile("mov.u32 %0, %%ctaid.z;" : "=r"(z));
+  return CtaIds{(int)x, (int)y, (int)z / B, (int)z % B};
 }
 
 struct Seq8 {
@@ -564,12 +580,9 @@ __device__ __forceinline__ void pv_any(bool int2, uint32_t sl, const MetaOff& mo
 // form one straight-line block (independent MMA chains the scheduler can interleave); then
 // FP16-region tiles [f_begin, f_end).
 template <bool EXACT>
-__device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, int f_end, int n2t,
-                                          int len_fp, const DecArgs& a, const TileSrc& src,
-                                          const MetaOff& mo,
-                                          const uint16_t* kf, const uint16_t* vf, uint32_t ring_l,
-                                          const QS& qs, uint32_t mg, WarpState& st, int warp, int g,
-                                          int c) {
+__device__ __forceinline__ void run_tiles(int q_begin, int q_end, int n2t, const DecArgs& a,
+                                          const TileSrc& src, const MetaOff& mo, uint32_t ring_l,
+                                          const QS& qs, uint32_t mg, WarpState& st, int warp) {
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
   int t = q_begin + warp;
@@ -610,6 +623,23 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int f_begin, i
     }
   }
   cp_wait<0>();
+}
+
+// This CTA's share of its unit's FP16-region tiles (FP16-tier chunks, tail, decode tokens),
+// interleaved over the warps; pointers and ranges re-derived here (len_fp may have grown by
+// decode appends: read after the programmatic-dependent-launch wait).
+template <bool EXACT>
+__device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpState& st, int warp,
+                                           int g, int c) {
+  const CtaIds id = cta_ids(a.B);
+  const int off_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 4];
+  const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 5];
+  const int nft = (len_fp + kTile - 1) / kTile;
+  const int f_begin = (int)((int64_t)nft * id.split / a.splits);
+  const int f_end = (int)((int64_t)nft * (id.split + 1) / a.splits);
+  const int64_t unit = (int64_t)id.l * a.H + id.h;
+  const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
+  const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
   for (int tf = f_begin + warp; tf < f_end; tf += kDecWarps) {
     const int r = tf * kTile;
     tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
@@ -624,34 +654,30 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   __shared__ int s_last, s_wide_q;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
-  const int split = blockIdx.x, h = blockIdx.y;
-  int64_t* const trace = g_trace;
-  int64_t tr[12];
-  __shared__ int64_t s_tend[kDecWarps];
-  tr[11] = 0;
-  if (trace) tr[0] = gtime();
-  const int l = blockIdx.z / a.B, b = blockIdx.z % a.B;
+  __shared__ int64_t s_tr[12], s_tend[kDecWarps];
+  if (threadIdx.x == 0 && tracing()) { s_tr[0] = gtime(); s_tr[11] = 0; }
   // Segment lengths of the quantized arenas are immutable after the build; len_fp grows with
   // decode appends and is read only after the programmatic-dependent-launch wait below.
-  const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
-  const int off2 = s0.x, off4 = s0.z, off_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 4];
-  const int n2t = s0.y / kTile, n4t = s0.w / kTile;
   // Split of the quantized tiles: every CTA takes the same 1/splits share of the INT2 tiles
-  // AND of the INT4 tiles (and of the FP16-region tiles below), so all CTAs carry the same
-  // mix and finish together whatever the relative per-tile costs are.
-  const int a2 = (int)((int64_t)n2t * split / a.splits), b2 = (int)((int64_t)n2t * (split + 1) / a.splits);
-  const int a4 = (int)((int64_t)n4t * split / a.splits), b4 = (int)((int64_t)n4t * (split + 1) / a.splits);
-  const int cnt2 = b2 - a2;               // local tiles [0, cnt2) are INT2, [cnt2, nloc) INT4
-  const int nloc = cnt2 + (b4 - a4);
-  const int64_t unit = (int64_t)l * a.H + h;
-  const int64_t r2 = off2 + (int64_t)a2 * kTile, r4 = off4 + (int64_t)a4 * kTile;  // first rows
+  // AND of the INT4 tiles (and of the FP16-region tiles, fp16_tiles), so all CTAs carry the
+  // same mix and finish together whatever the relative per-tile costs are.
+  int cnt2, nloc;
   TileSrc src;  // tile-native arenas: a row range starting at a tile is contiguous bytes
-  src.c2 = (unit * a.K.rows2 + r2) * 32 + 16 * lane;
-  src.m2 = (unit * a.K.rows2 + r2) * 16 + 8 * lane;
-  src.c4 = (unit * a.K.rows4 + r4) * 64 + 16 * lane;
-  src.m4 = (unit * a.K.rows4 + r4) * 16 + 8 * lane;
-  const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
-  const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
+  {
+    const CtaIds id = cta_ids(a.B);
+    const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * id.b];
+    const int n2t = s0.y / kTile, n4t = s0.w / kTile;
+    const int a2 = (int)((int64_t)n2t * id.split / a.splits), b2 = (int)((int64_t)n2t * (id.split + 1) / a.splits);
+    const int a4 = (int)((int64_t)n4t * id.split / a.splits), b4 = (int)((int64_t)n4t * (id.split + 1) / a.splits);
+    cnt2 = b2 - a2;  // local tiles [0, cnt2) are INT2, [cnt2, nloc) INT4
+    nloc = cnt2 + (b4 - a4);
+    const int64_t unit = (int64_t)id.l * a.H + id.h;
+    const int64_t r2 = s0.x + (int64_t)a2 * kTile, r4 = s0.z + (int64_t)a4 * kTile;  // first rows
+    src.c2 = (unit * a.K.rows2 + r2) * 32 + 16 * lane;
+    src.m2 = (unit * a.K.rows2 + r2) * 16 + 8 * lane;
+    src.c4 = (unit * a.K.rows4 + r4) * 64 + 16 * lane;
+    src.m4 = (unit * a.K.rows4 + r4) * 16 + 8 * lane;
+  }
   MetaOff mo;
   mo.k = -8 * lane;
   mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
@@ -663,15 +689,14 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   // decode launch (next layer) start its own prologue as soon as SMs free up.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  if (trace) tr[1] = gtime();
-  const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 5];
-  const int nft = (len_fp + kTile - 1) / kTile;
-  const int f_begin = (int)((int64_t)nft * split / a.splits);
-  const int f_end = (int)((int64_t)nft * (split + 1) / a.splits);
+  if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
 
   // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m); warp 0 writes the
   // CTA's three sets to shared memory.
+  bool exact;
   {
+    const CtaIds id = cta_ids(a.B);
+    const int l = id.l, b = id.b, h = id.h;
     float qv[32];
     const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
     if (g < a.m) {
@@ -720,15 +745,16 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
       const bool wide = __any_sync(0xffffffffu, qmaxabs > kWideQ);
       if (lane == 0) s_wide_q = wide;
     }
+    const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // span flags are [L][H][B]
+    exact = (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
+            (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
   }
   __syncthreads();
-  if (trace) tr[2] = gtime();
+  exact = exact || s_wide_q;
+  if (threadIdx.x == 0 && tracing()) s_tr[2] = gtime();
   QS qs;
   qs.base = (uint32_t)__cvta_generic_to_shared(s_q) + 16 * lane;
   qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_q) + 3 * kQSet + 4 * lane;
-  const int64_t fidx = unit * a.B + b;  // span flags are [L][H][B]
-  const bool exact = s_wide_q || (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
-                     (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
   const uint32_t mg = kMagic16 | a.zero;
 
   WarpState st;
@@ -740,9 +766,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.lsum[0] = st.lsum[1] = 0.f;
 
   if (exact) {
-    run_tiles<true>(0, nloc, f_begin, f_end, cnt2, len_fp, a, src, mo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<true>(0, nloc, cnt2, a, src, mo, ring_l, qs, mg, st, warp);
+    fp16_tiles<true>(a, qs, st, warp, g, c);
   } else {
-    run_tiles<false>(0, nloc, f_begin, f_end, cnt2, len_fp, a, src, mo, kf, vf, ring_l, qs, mg, st, warp, g, c);
+    run_tiles<false>(0, nloc, cnt2, a, src, mo, ring_l, qs, mg, st, warp);
+    fp16_tiles<false>(a, qs, st, warp, g, c);
     // undo the V m-tile weights 2^(2(mt&3) - 6)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
@@ -751,7 +779,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     }
   }
 
-  if (trace) { tr[3] = gtime(); if (lane == 0) s_tend[warp] = tr[3]; }
+  if (lane == 0 && tracing()) s_tend[warp] = gtime();
   // finish the warp: fold the zero-point term, reduce row sums over the 8 row-groups
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
@@ -766,7 +794,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.lsum[0] += st.lsq[0];  // already summed over the 16 tokens of every tile
   st.lsum[1] += st.lsq[1];
   __syncthreads();  // ring -> merge buffer reuse
-  if (trace) tr[8] = gtime();
+  if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
   float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0][0]);
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
@@ -781,6 +809,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   }
   __syncthreads();
   // merge the 4 warps: thread -> d
+  const CtaIds id = cta_ids(a.B);
+  const int split = id.split, h = id.h, l = id.l, b = id.b;
   const int d = threadIdx.x;
   const int hq0 = h * a.m;
   const int Hq = a.H * a.m;
@@ -813,11 +843,12 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     }
   }
   auto trace_out = [&]() {
-    if (trace && threadIdx.x == 0) {
-      tr[4] = gtime();
-      int64_t* dst = trace + 16 * atomicAdd(&g_trace_n, 1ull);
-      for (int i = 0; i < 5; ++i) dst[i] = tr[i];
-      for (int i = 8; i < 12; ++i) dst[i] = tr[i];
+    if (threadIdx.x == 0 && tracing()) {
+      s_tr[3] = s_tend[0];
+      s_tr[4] = gtime();
+      int64_t* dst = g_trace + 16 * atomicAdd(&g_trace_n, 1ull);
+      for (int i = 0; i < 5; ++i) dst[i] = s_tr[i];
+      for (int i = 8; i < 12; ++i) dst[i] = s_tr[i];
       for (int i = 0; i < kDecWarps; ++i) dst[12 + i] = s_tend[i];
       dst[5] = smid(); dst[6] = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
       dst[7] = (int64_t)a.q;
@@ -828,7 +859,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   // kernel).  The CTA barrier orders every thread's partial stores before thread 0's
   // device-scope release RMW; the acquiring side sees them after its own barrier.
   __syncthreads();
-  if (trace) tr[9] = gtime();
+  if (threadIdx.x == 0 && tracing()) s_tr[9] = gtime();
   if (threadIdx.x == 0) {
     cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[((int64_t)l * a.B + b) * a.H + h]);
     const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
@@ -836,7 +867,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     if (s_last) ctr.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
   }
   __syncthreads();
-  if (trace) { tr[10] = gtime(); tr[11] = s_last; }
+  if (threadIdx.x == 0 && tracing()) { s_tr[10] = gtime(); s_tr[11] = s_last; }
   if (!s_last) { trace_out(); return; }
   // All m x splits partial rows of this unit are contiguous in the workspace: stage them in
   // shared memory with every 16-B copy in flight at once (one L2 round trip), then merge.
@@ -983,29 +1014,6 @@ int32_t ckv_decode_set_trace(int64_t* buf) {
     return CKV_ERR_CUDA;
   }
   return CKV_OK;
-}
-
-// Tuning probe (not part of the ABI): resident clusters of `cluster` decode CTAs.
-int32_t ckv_probe_max_clusters(int32_t cluster, int32_t grid_x) {
-  if (!ensure_decode_attr()) return -1;
-  cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid_x, 8, 8);
-  cfg.blockDim = dim3(kDecWarps * 32);
-  cfg.dynamicSmemBytes = kDynSmem;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, decode_kernel, &cfg) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return -2;
-  }
-  return n;
 }
 
 int32_t ckv_lse_merge(const float* partials, int32_t n_parts, int64_t rows, uint16_t* out,
