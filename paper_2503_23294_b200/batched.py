@@ -210,6 +210,53 @@ class BatchedKVCache:
                   _lib.DECODE_PDL if pdl else 0, _lib.stream())
         return out
 
+    def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=8):
+        """One decode step for all layers from HOST buffers: pinned fp16 q [L, B, H*m, 128] ->
+        pinned fp16 output of the same shape.  The q upload runs on a copy stream, layer 0
+        waits only for its own slice; the outputs go back every `d2h_every` layers while the
+        next layers compute; per-layer decode launches stay PDL-chained.  Device staging is
+        double-buffered across steps, so consecutive steps never wait on each other's copies."""
+        L, B, Hq, D = q_host.shape
+        if (L, B) != (self.L, self.B) or D != HEAD_DIM or Hq % self.H or q_host.dtype != torch.float16:
+            raise ValueError("q shape does not match the cache")
+        if out_host.shape != q_host.shape or out_host.dtype != torch.float16:
+            raise ValueError("out_host must match q_host")
+        key = tuple(q_host.shape)
+        st = getattr(self, "_host_step", None)
+        if st is None or st["key"] != key:
+            dev = self.device
+            st = dict(key=key, q=[torch.empty(key, dtype=torch.float16, device=dev) for _ in range(2)],
+                      o=[torch.empty(key, dtype=torch.float16, device=dev) for _ in range(2)],
+                      cs=torch.cuda.Stream(device=dev), i=0)
+            self._host_step = st
+        ms = torch.cuda.current_stream()
+        cs = st["cs"]
+        buf = st["i"] & 1
+        st["i"] += 1
+        qd, od = st["q"][buf], st["o"][buf]
+        cs.wait_stream(ms)  # staging buffer `buf` was last used two steps ago on ms
+        ev_q0, ev_q = torch.cuda.Event(), torch.cuda.Event()
+        with torch.cuda.stream(cs):
+            qd[0:1].copy_(q_host[0:1], non_blocking=True)
+            ev_q0.record(cs)
+            qd[1:].copy_(q_host[1:], non_blocking=True)
+            ev_q.record(cs)
+        for l in range(L):
+            if l == 0:
+                ms.wait_event(ev_q0)
+            elif l == 1:
+                ms.wait_event(ev_q)
+            self.decode(qd[l:l + 1], splits=splits, out=od[l:l + 1], scale=scale, layer=l, pdl=l > 1)
+            if (l + 1) % d2h_every == 0 or l == L - 1:
+                lo = (l // d2h_every) * d2h_every
+                ev = torch.cuda.Event()
+                ev.record(ms)
+                cs.wait_event(ev)
+                with torch.cuda.stream(cs):
+                    out_host[lo:l + 1].copy_(od[lo:l + 1], non_blocking=True)
+        ms.wait_stream(cs)
+        return out_host
+
     def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None):
         """Unnormalised split-KV partials f32 [L'*B*H*m, 130] = (acc[128], m (log2), l) for q
         fp16 [L', B, H*m, 128] over layers [layer, layer + L') (per-layer launches: L' = 1,

@@ -285,3 +285,21 @@ def test_layer_by_layer_build_and_per_layer_partials():
     for l in range(L):
         per.decode_partial(q[l:l + 1], layer=l, pdl=l > 0, out=got[l * rows:(l + 1) * rows])
     assert torch.max(torch.abs(batched.lse_merge(got[None]).float() - batched.lse_merge(want[None]).float())).item() < 2e-3
+
+
+def test_decode_step_host_matches_device_decode():
+    """decode_step_host (pinned host q -> overlapped uploads, per-layer PDL decode, overlapped
+    downloads) returns exactly the device decode's output, over consecutive steps."""
+    rng = np.random.default_rng(51)
+    L, B, H, m, D, N = 5, 2, 2, 4, 128, 12
+    T = N * 32 + 3
+    k = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    cache = batched.build_cache_batched(k, v, _search_from_tiers(rng.choice([0, 1, 2], size=(B, N)).astype(np.uint8)))
+    for step in range(3):
+        q = torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16))
+        oh = torch.empty(q.shape, dtype=torch.float16).pin_memory()
+        cache.decode_step_host(q.pin_memory(), oh, d2h_every=2)
+        torch.cuda.synchronize()
+        want = cache.decode(q.cuda()).cpu()
+        assert torch.equal(oh, want), step
