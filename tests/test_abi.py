@@ -97,3 +97,44 @@ def test_batch_shard_covers_batch():
         spans = [batch_shard(64, world, r) for r in range(world)]
         assert spans[0][0] == 0 and spans[-1][1] == 64
         assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_sequence_shard_cache_layout_partitions_the_context(world):
+    """Host planning of a sequence split-KV shard (no kernels): the ranks' caches hold every
+    chunk of every tier exactly once (perm slots), the last rank also the tail and the decode
+    capacity, and every rank's arena rows add up to the full cache's."""
+    import torch
+    from paper_2503_23294_b200.distributed import sequence_shard_cache
+    from paper_2503_23294_b200.retrieval import SearchResult
+
+    rng = np.random.default_rng(7)
+    B, N, tail = 3, 45, 11
+    tiers = rng.choice([0, 0, 0, 1, 2], size=(B, N)).astype(np.uint8)
+    perm = np.zeros((B, N), np.int32)
+    counts = np.zeros((B, 3), np.int32)
+    for b in range(B):
+        order = np.concatenate([np.nonzero(tiers[b] == t)[0] for t in range(3)])
+        perm[b] = order
+        counts[b] = np.bincount(tiers[b], minlength=3)
+    z = torch.zeros
+    s = SearchResult(z((B, N), dtype=torch.float64), z((B, 4), dtype=torch.float64),
+                     torch.from_numpy(tiers), torch.from_numpy(perm), torch.from_numpy(counts),
+                     z(B, dtype=torch.int32))
+    ctx = np.full(B, N * 32 + tail)
+    seen = [[] for _ in range(B)]
+    rows = np.zeros(3, np.int64)
+    for r in range(world):
+        cache, perm_r = sequence_shard_cache(s, 2, 2, ctx, world, r, decode_capacity=8,
+                                             device=torch.device("cpu"))
+        sh = cache.seq_host
+        rows += [cache.rows2, cache.rows4, int(sh[:, 5].sum())]
+        for b in range(B):
+            n_r = (sh[b, 1] + sh[b, 3]) // 32 + (sh[b, 5] - (tail if r == world - 1 else 0)) // 32
+            seen[b] += perm_r[b, :n_r].tolist()
+            assert (sh[b, 5] % 32 == tail % 32) if r == world - 1 else (sh[b, 5] % 32 == 0)
+            assert (cache.cap_fp[b] >= sh[b, 5] + (8 if r == world - 1 else 0))
+    for b in range(B):
+        assert sorted(seen[b]) == list(range(N))
+    assert rows.tolist() == [int(counts[:, 0].sum()) * 32, int(counts[:, 1].sum()) * 32,
+                             int(counts[:, 2].sum()) * 32 + B * tail]
