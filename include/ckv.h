@@ -150,6 +150,10 @@ typedef struct ckv_arena {
   uint32_t* span_flags; /* u32 [L][H][B], zero-filled before build: bit0/bit1 set when an
                            INT2/INT4 group's scale exceeds 4000 (decode then runs that unit in
                            its exact unweighted mode; nullable) */
+  uint32_t* span_max; /* f32 bits [L][H][B], zero-filled before build: the largest quantized
+                         group span (hi - lo) of the unit's rows, which with |q| bounds the
+                         decode's fp16 operand error (decode then takes its precise K path;
+                         nullable) */
   int64_t rows2, rows4, rows_fp;
 } ckv_arena;
 

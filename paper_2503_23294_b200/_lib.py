@@ -47,7 +47,7 @@ class Arena(ctypes.Structure):
 
     _fields_ = [
         ("codes2", _vp), ("meta2", _vp), ("codes4", _vp), ("meta4", _vp), ("fp", _vp),
-        ("span_flags", _vp), ("rows2", _i64), ("rows4", _i64), ("rows_fp", _i64),
+        ("span_flags", _vp), ("span_max", _vp), ("rows2", _i64), ("rows4", _i64), ("rows_fp", _i64),
     ]
 
 

@@ -93,7 +93,7 @@ class BatchedKVCache:
         self.k = dict(codes2=z32(L, H, self.rows2, 8), meta2=z32(L, H, self.rows2, 4),
                       codes4=z32(L, H, self.rows4, 16), meta4=z32(L, H, self.rows4, 4),
                       fp=torch.zeros((L, H, self.rows_fp, HEAD_DIM), dtype=torch.float16, device=dev),
-                      span_flags=z32(L, H, self.B))
+                      span_flags=z32(L, H, self.B), span_max=z32(L, H, self.B))
         self.v = {k: torch.zeros_like(t) for k, t in self.k.items()}
         self._ws = {}
 
@@ -117,7 +117,7 @@ class BatchedKVCache:
         t = self.k if which == "k" else self.v
         ptr = lambda name: t[name].data_ptr() + layer * t[name].stride(0) * t[name].element_size()  # noqa: E731
         return _lib.Arena(ptr("codes2"), ptr("meta2"), ptr("codes4"), ptr("meta4"), ptr("fp"),
-                          ptr("span_flags"), self.rows2, self.rows4, self.rows_fp)
+                          ptr("span_flags"), ptr("span_max"), self.rows2, self.rows4, self.rows_fp)
 
     def build(self, k, v, perm, check=True, layer=0):
         """ckv_reorder_quantize_pack over every unit of layers [layer, layer + L'); k, v fp16
@@ -131,8 +131,9 @@ class BatchedKVCache:
         if layer < 0 or layer + L > self.L or (B, H) != (self.B, self.H) or D != HEAD_DIM or k.stride(4) != 1:
             raise ValueError("K/V shape does not match the cache")
         perm = kernels.to_dev(perm, torch.int32)
-        self.k["span_flags"][layer:layer + L].zero_()
-        self.v["span_flags"][layer:layer + L].zero_()
+        for t in (self.k, self.v):
+            t["span_flags"][layer:layer + L].zero_()
+            t["span_max"][layer:layer + L].zero_()
         flag = torch.zeros(1, dtype=torch.int32, device=k.device)
         _lib.call("ckv_reorder_quantize_pack", _lib.ptr(k), _lib.ptr(v), L, B, H, k.stride(0),
                   k.stride(1), k.stride(2), k.stride(3), _lib.ptr(perm), perm.shape[1],

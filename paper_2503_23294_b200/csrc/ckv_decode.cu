@@ -145,6 +145,10 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 constexpr uint32_t kMagic16 = 0x4C004C00u;  // fp16 16.0 in both halves
 constexpr float kWideScale = 4000.0f;       // weighted mode needs 16 * sc and 12 * sc in fp16 range
 constexpr float kWideQ = 1000.0f;           // and |q| 2^6 in fp16 range
+// precise K path when (largest K group span) x max|q| (log2-scaled q) exceeds this: the normal
+// path's score error is ~2^-12 span |q| per group element (measured ~1.5e-3 relative output
+// error at a product of ~3 on N(0,1) data, 1.8e-2 at ~55 on SURVEY's outlier variant)
+constexpr float kPreciseSpanQ = 8.0f;
 
 // scale (hi - lo) / qmax of one (lo, hi) half2 metadata word (hi - lo via mixed f16/f32 add)
 __device__ __forceinline__ float meta_scale(uint32_t meta, float inv_qmax) {
@@ -470,6 +474,117 @@ __device__ __forceinline__ void pv_int4(uint32_t sl, const MetaOff& mo, uint32_t
   }
 }
 
+// ---- precise K path (wide-span units) ---------------------------------------------------
+// The normal path feeds the tensor cores fp16 values sc*code*2^(j-6), so the score error grows
+// with the K group span times |q|.  The precise path feeds the exact magic values
+// 16 + code*2^(j-6) instead and applies bias and scale per group in fp32: two MMAs per k-step
+// whose B fragments are the tier's q fragments (sets 0 / 1) masked to two groups each
+// (column n = (q row n & 3, group 2v + n / 4), m <= 4), so D holds per-(token, q row, group)
+// partial sums  sum_{d in G} q'_d (16 + code_d 2^(j-6)) = 16 Q'_G + (1/f) sum_{d in G} q_d code_d
+// (f = the set's fp16(1/qmax) fold), and S = sum_G span_G fp16(1/qmax) (D_G - 16 Q'_G) + lo term.
+// A thread holds groups c/2 and 2 + c/2 of q rows (2c)&3, (2c)&3 + 1; lanes c and c^2 hold the
+// other two groups.  Needs no shared memory beyond a 128-byte bias table.
+struct PreciseOff {
+  int32_t m0, m1;   // byte offsets (from the lane slot `sl`) of the metadata of groups G0, G1
+  uint32_t bias;    // shared-memory address of this thread's 16 Q' constants (INT2 tier)
+  int32_t qoff;     // q-fragment offset of lane ((g & 3), c) relative to this lane
+  uint32_t msk0, msk1;  // all-ones when this lane's B column takes group c in variant 0 / 1
+};
+constexpr int kBiasG = 4 * 4;              // bias table f32 16 Q' [tier][group][q row]
+constexpr int kBiasTier = 4 * kBiasG;
+
+__device__ __forceinline__ uint32_t raw_pair(uint32_t x, uint32_t mask, uint32_t magic) {
+  return (x & mask) | magic;
+}
+__device__ __forceinline__ uint2 masked(uint32_t x, uint32_t y, uint32_t m) { return make_uint2(x & m, y & m); }
+
+__device__ __forceinline__ void precise_combine(const float (&P0)[4], const float (&P1)[4], float sc0g,
+                                                float sc0g8, float sc1g, float sc1g8,
+                                                uint32_t bias_addr, float (&t)[4]) {
+  const uint2 b0 = lds64(bias_addr), b1 = lds64(bias_addr + 2 * kBiasG);  // (G0, a..a+1), (G0 + 2, ..)
+  const float b0x = __uint_as_float(b0.x), b0y = __uint_as_float(b0.y);
+  const float b1x = __uint_as_float(b1.x), b1y = __uint_as_float(b1.y);
+  t[0] = fmaf(sc1g, P1[0] - b1x, sc0g * (P0[0] - b0x));
+  t[1] = fmaf(sc1g, P1[1] - b1y, sc0g * (P0[1] - b0y));
+  t[2] = fmaf(sc1g8, P1[2] - b1x, sc0g8 * (P0[2] - b0x));
+  t[3] = fmaf(sc1g8, P1[3] - b1y, sc0g8 * (P0[3] - b0y));
+#pragma unroll
+  for (int e = 0; e < 4; ++e) t[e] += __shfl_xor_sync(0xffffffffu, t[e], 2);
+}
+
+// span * fp16(1/qmax) in fp32 from a (lo, hi) metadata word (matches the fold in the q sets)
+__device__ __forceinline__ float precise_scale(uint32_t meta, float inv_q16) {
+  const float2 lh = __half22float2(u32_as_h2(meta));
+  return (lh.y - lh.x) * inv_q16;
+}
+
+template <int BITS>
+__device__ __forceinline__ void qk_precise(uint32_t sl, const MetaOff& mo, const PreciseOff& po,
+                                           const QS& qs, uint32_t mg, float (&s)[4]) {
+  constexpr int set = BITS == 2 ? 0 : 1;
+  constexpr uint32_t meta_at = BITS == 2 ? 1024 : 2048;
+  const float inv_q16 = __half2float(__float2half_rn(BITS == 2 ? 1.0f / 3.0f : 1.0f / 15.0f));
+  float P0[4] = {0.f, 0.f, 0.f, 0.f}, P1[4] = {0.f, 0.f, 0.f, 0.f};
+  const uint32_t qsrc = qs.base + po.qoff + set * kQSet;
+  if (BITS == 2) {
+    const uint4 kk = lds128(sl);
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
+      const uint32_t w0s = w0 >> 10, w1s = w1 >> 10;
+      const uint4 qa = lds128(qsrc + 512 * (2 * blk)), qb = lds128(qsrc + 512 * (2 * blk + 1));
+#define KR(W, WS, I) raw_pair(K2<I>::hi ? WS : W, 0x00030003u << K2<I>::j, mg)
+#define KSTEP(I0, I1, X, Y)                                                        \
+      {                                                                          \
+        const uint32_t x0 = KR(w0, w0s, I0), x1 = KR(w1, w1s, I0);               \
+        const uint32_t x2 = KR(w0, w0s, I1), x3 = KR(w1, w1s, I1);               \
+        mma_16816(P0, x0, x1, x2, x3, masked(X, Y, po.msk0));                    \
+        mma_16816(P1, x0, x1, x2, x3, masked(X, Y, po.msk1));                    \
+      }
+      KSTEP(0, 1, qa.x, qa.y)
+      KSTEP(2, 3, qa.z, qa.w)
+      KSTEP(4, 5, qb.x, qb.y)
+      KSTEP(6, 7, qb.z, qb.w)
+#undef KSTEP
+#undef KR
+    }
+  } else {
+    const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);
+    const uint32_t kwa[4] = {kw0.x, kw0.y, kw0.z, kw0.w}, kwb[4] = {kw1.x, kw1.y, kw1.z, kw1.w};
+#pragma unroll
+    for (int blk = 0; blk < 2; ++blk) {
+      const uint32_t a_lo = kwa[2 * blk], a_hi = kwa[2 * blk + 1];
+      const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
+      const uint32_t a_lo8 = a_lo >> 8, a_hi8 = a_hi >> 8, b_lo8 = b_lo >> 8, b_hi8 = b_hi >> 8;
+      const uint4 qa = lds128(qsrc + 512 * (2 * blk)), qb = lds128(qsrc + 512 * (2 * blk + 1));
+#define KR(X, X8, I) raw_pair(K4<I>::hi ? X8 : X, 0x000F000Fu << K4<I>::j, mg)
+#define KSTEP(XA, XA8, XB, XB8, I0, I1, X, Y)                                      \
+      {                                                                          \
+        const uint32_t x0 = KR(XA, XA8, I0), x1 = KR(XB, XB8, I0);               \
+        const uint32_t x2 = KR(XA, XA8, I1), x3 = KR(XB, XB8, I1);               \
+        mma_16816(P0, x0, x1, x2, x3, masked(X, Y, po.msk0));                    \
+        mma_16816(P1, x0, x1, x2, x3, masked(X, Y, po.msk1));                    \
+      }
+      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 0, 1, qa.x, qa.y)
+      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 2, 3, qa.z, qa.w)
+      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 0, 1, qb.x, qb.y)
+      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 2, 3, qb.z, qb.w)
+#undef KSTEP
+#undef KR
+    }
+  }
+  const uint2 m0 = lds64(sl + meta_at + po.m0), m1 = lds64(sl + meta_at + po.m1);
+  float t[4];
+  precise_combine(P0, P1, precise_scale(m0.x, inv_q16), precise_scale(m0.y, inv_q16),
+                  precise_scale(m1.x, inv_q16), precise_scale(m1.y, inv_q16),
+                  po.bias + (BITS == 2 ? 0 : kBiasTier), t);
+  const uint2 kmm = lds64(sl + meta_at + mo.k);
+  float s2[4] = {0.f, 0.f, 0.f, 0.f};
+  mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s[e] = t[e] + s2[e];
+}
+
 // ---- FP16 tile straight from global memory (FP16 chunks, tail, decode tokens) ------------
 template <bool EXACT>
 __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf, int valid,
@@ -564,10 +679,24 @@ __device__ __forceinline__ void prologue(int q_begin, int q_end, int n2t, const 
     issue_tile(q_begin + warp + kDecWarps * s, q_end, n2t, a, src, mo, ring_l + s * kStageBytes);
 }
 
-template <bool EXACT>
-__device__ __forceinline__ void qk_any(bool int2, uint32_t sl, const MetaOff& mo, const QS& qs, uint32_t mg, float (&s)[4]) {
-  if (int2) qk_int2<EXACT>(sl, mo, qs, mg, s);
-  else qk_int4<EXACT>(sl, mo, qs, mg, s);
+// decode modes of a unit: normal; precise K (wide span x |q|, m <= 4); exact (scales or q
+// too wide for the fp16-weighted forms)
+constexpr int kModeNormal = 0, kModePrecise = 1, kModeExact = 2;
+
+template <int MODE>
+__device__ __forceinline__ void qk2(uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
+  if (MODE == kModePrecise) qk_precise<2>(sl, mo, po, qs, mg, s);
+  else qk_int2<MODE == kModeExact>(sl, mo, qs, mg, s);
+}
+template <int MODE>
+__device__ __forceinline__ void qk4(uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
+  if (MODE == kModePrecise) qk_precise<4>(sl, mo, po, qs, mg, s);
+  else qk_int4<MODE == kModeExact>(sl, mo, qs, mg, s);
+}
+template <int MODE>
+__device__ __forceinline__ void qk_any(bool int2, uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
+  if (int2) qk2<MODE>(sl, mo, po, qs, mg, s);
+  else qk4<MODE>(sl, mo, po, qs, mg, s);
 }
 template <bool EXACT>
 __device__ __forceinline__ void pv_any(bool int2, uint32_t sl, const MetaOff& mo, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
@@ -579,10 +708,12 @@ __device__ __forceinline__ void pv_any(bool int2, uint32_t sl, const MetaOff& mo
 // (prologue already issued), software-pipelined so that q.K^T of tile i+1 and P.V of tile i
 // form one straight-line block (independent MMA chains the scheduler can interleave); then
 // FP16-region tiles [f_begin, f_end).
-template <bool EXACT>
+template <int MODE>
 __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int n2t, const DecArgs& a,
-                                          const TileSrc& src, const MetaOff& mo, uint32_t ring_l,
-                                          const QS& qs, uint32_t mg, WarpState& st, int warp) {
+                                          const TileSrc& src, const MetaOff& mo, const PreciseOff& po,
+                                          uint32_t ring_l, const QS& qs, uint32_t mg, WarpState& st,
+                                          int warp) {
+  constexpr bool EXACT = MODE == kModeExact;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
   int t = q_begin + warp;
@@ -591,7 +722,7 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int n2t, const
     cp_wait<kStages - 2>();
     __syncwarp();
     float s0[4];
-    qk_any<EXACT>(t < n2t, cur, mo, qs, mg, s0);
+    qk_any<MODE>(t < n2t, cur, mo, po, qs, mg, s0);
     uint32_t bp0, bp1;
     softmax_tile<EXACT>(s0, st, bp0, bp1);
     while (true) {
@@ -607,13 +738,13 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int n2t, const
       const uint32_t nx = next(cur);
       float sn[4];
       if (tn < n2t) {  // both INT2 (tn > t)
-        qk_int2<EXACT>(nx, mo, qs, mg, sn);
+        qk2<MODE>(nx, mo, po, qs, mg, sn);
         pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
       } else if (t >= n2t) {  // both INT4
-        qk_int4<EXACT>(nx, mo, qs, mg, sn);
+        qk4<MODE>(nx, mo, po, qs, mg, sn);
         pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
       } else {  // INT2 -> INT4 boundary
-        qk_int4<EXACT>(nx, mo, qs, mg, sn);
+        qk4<MODE>(nx, mo, po, qs, mg, sn);
         pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
       }
       __syncwarp();  // slot `cur` may be refilled from now on
@@ -629,8 +760,12 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int n2t, const
 // interleaved over the warps; pointers and ranges re-derived here (len_fp may have grown by
 // decode appends: read after the programmatic-dependent-launch wait).
 template <bool EXACT>
-__device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpState& st, int warp,
-                                           int g, int c) {
+__device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpState& st) {
+  // thread coordinates re-read here (volatile): values carried from the kernel's start would be
+  // spilled across the tile loop and reloaded in every iteration of this one
+  uint32_t tid;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+  const int warp = (int)(tid >> 5), g = (int)((tid & 31) >> 2), c = (int)(tid & 3);
   const CtaIds id = cta_ids(a.B);
   const int off_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 4];
   const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 5];
@@ -651,7 +786,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   unsigned char (*s_ring)[kStages][kStageBytes] = reinterpret_cast<unsigned char (*)[kStages][kStageBytes]>(s_dyn);
   __shared__ float s_ml[kDecWarps][8][2];
   __shared__ __align__(16) unsigned char s_q[kQBytes];
-  __shared__ int s_last, s_wide_q;
+  __shared__ int s_last;
+  __shared__ __align__(16) float s_bias[2 * 16];  // precise mode: 16 Q' [tier][group][q row]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   __shared__ int64_t s_tr[12], s_tend[kDecWarps];
@@ -691,70 +827,96 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
 
-  // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m); warp 0 writes the
-  // CTA's three sets to shared memory.
-  bool exact;
+  // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m).  Every warp loads the
+  // same 8 rows and derives the unit's mode from max |q| and the K span bound; then warps 0-2
+  // write q-fragment sets 0-2 (precise mode: the group-masked INT2 / INT4 sets and their 16 Q'
+  // bias constants instead of sets 0 and 1), warp 3 the zero-point entry.
+  int mode;
   {
     const CtaIds id = cta_ids(a.B);
     const int l = id.l, b = id.b, h = id.h;
-    float qv[32];
-    const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
-    if (g < a.m) {
+    const uint16_t* qbase = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m) * kHeadDim + 32 * c;
+    auto load_q = [&](int row, float (&qv)[32]) {
+      if (row < a.m) {
+        const uint16_t* qrow = qbase + (int64_t)row * kHeadDim;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint4 x = reinterpret_cast<const uint4*>(qrow)[u];
-        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        for (int u = 0; u < 4; ++u) {
+          const uint4 x = reinterpret_cast<const uint4*>(qrow)[u];
+          const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __half22float2(u32_as_h2(w[e]));
-          qv[8 * u + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
-          qv[8 * u + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(u32_as_h2(w[e]));
+            qv[8 * u + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
+            qv[8 * u + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
+          }
         }
-      }
-    } else {
+      } else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) qv[e] = 0.f;
-    }
-    // warp w < 3 stores q-fragment set w; warp 3 stores the zero-point entry and the range flag
+        for (int e = 0; e < 32; ++e) qv[e] = 0.f;
+      }
+    };
+    float qv[32];
+    load_q(g, qv);
+    float qmaxabs = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) qmaxabs = fmaxf(qmaxabs, __shfl_xor_sync(0xffffffffu, qmaxabs, o));
+    const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // span flags are [L][H][B]
+    const bool wide = qmaxabs > kWideQ || (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
+                      (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
+    const float kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
+    mode = wide ? kModeExact
+                : (a.m <= 4 && kspan * qmaxabs > kPreciseSpanQ ? kModePrecise : kModeNormal);
+    // slot weights 2^(6-j) of K pair i: INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1)
+    auto slot_w = [&](int set, int i) {
+      return set == 0 ? exp2f((float)(6 - (i <= 4 ? 2 * i : 2 * (i - 5))))
+                      : (set == 1 ? exp2f((float)(6 - 4 * (i & 1))) : 1.0f);
+    };
     if (warp < 3) {
+      float qsw = 0.f;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
         const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
-        // slot weights 2^(6-j): INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1); set 2: 1
-        const float w0 = warp == 0 ? exp2f((float)(6 - (i0 <= 4 ? 2 * i0 : 2 * (i0 - 5))))
-                                   : (warp == 1 ? exp2f((float)(6 - 4 * (i0 & 1))) : 1.0f);
-        const float w1 = warp == 0 ? exp2f((float)(6 - (i1 <= 4 ? 2 * i1 : 2 * (i1 - 5))))
-                                   : (warp == 1 ? exp2f((float)(6 - 4 * (i1 & 1))) : 1.0f);
         // INT2 / INT4 sets also carry the fold of the fp16(1/qmax) rounding (see kdeq)
         const float fold = warp == 0 ? kscale_fold(1.0f / 3.0f) : (warp == 1 ? kscale_fold(1.0f / 15.0f) : 1.0f);
-        const float x0 = w0 * fold, x1 = w1 * fold;
-        reinterpret_cast<uint2*>(s_q + warp * kQSet + 512 * (ks >> 1) + 16 * lane)[ks & 1] = make_uint2(h2_as_u32(__floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0)),
-                                         h2_as_u32(__floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1)));
+        const float x0 = slot_w(warp, i0) * fold, x1 = slot_w(warp, i1) * fold;
+        const __half2 lo = __floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0);
+        const __half2 hi = __floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1);
+        reinterpret_cast<uint2*>(s_q + warp * kQSet + 512 * (ks >> 1) + 16 * lane)[ks & 1] =
+            make_uint2(h2_as_u32(lo), h2_as_u32(hi));
+        const float2 fl = __half22float2(lo), fh = __half22float2(hi);
+        qsw += (fl.x + fl.y) + (fh.x + fh.y);
       }
+      // precise-mode bias 16 Q'[tier][group c][q row g]: the sum of exactly the fp16 weighted
+      // values this lane's B fragments hold
+      if (warp < 2 && g < 4) s_bias[warp * 16 + c * 4 + g] = 16.0f * qsw;
     } else {
-      float qsum = 0.f, qmaxabs = 0.f;
+      float qsum = 0.f;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        qsum += qv[e];
-        qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
-      }
+      for (int e = 0; e < 32; ++e) qsum += qv[e];
       const __half qhi = __float2half_rn(qsum);
       const __half qlo = __float2half_rn(qsum - __half2float(qhi));
       reinterpret_cast<uint32_t*>(s_q + 3 * kQSet)[lane] = h2_as_u32(__halves2half2(qhi, qlo));
-      const bool wide = __any_sync(0xffffffffu, qmaxabs > kWideQ);
-      if (lane == 0) s_wide_q = wide;
     }
-    const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // span flags are [L][H][B]
-    exact = (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
-            (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
   }
   __syncthreads();
-  exact = exact || s_wide_q;
   if (threadIdx.x == 0 && tracing()) s_tr[2] = gtime();
   QS qs;
   qs.base = (uint32_t)__cvta_generic_to_shared(s_q) + 16 * lane;
   qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_q) + 3 * kQSet + 4 * lane;
+  PreciseOff po;
+  {
+    const int G0 = c >> 1, qa = (2 * c) & 3;
+    po.m0 = (g * 4 + G0) * 8 - 16 * lane;
+    po.m1 = (g * 4 + G0 + 2) * 8 - 16 * lane;
+    po.bias = (uint32_t)__cvta_generic_to_shared(s_bias) + (G0 * 4 + qa) * 4;
+    po.qoff = 16 * (((g & 3) * 4 + c) - lane);
+    const bool in = (g >> 2) == (c & 1);  // column g takes group c (variant c / 2)
+    po.msk0 = in && (c >> 1) == 0 ? 0xffffffffu : 0u;
+    po.msk1 = in && (c >> 1) == 1 ? 0xffffffffu : 0u;
+  }
   const uint32_t mg = kMagic16 | a.zero;
 
   WarpState st;
@@ -765,12 +927,13 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.mrun[0] = st.mrun[1] = -INFINITY;
   st.lsum[0] = st.lsum[1] = 0.f;
 
-  if (exact) {
-    run_tiles<true>(0, nloc, cnt2, a, src, mo, ring_l, qs, mg, st, warp);
-    fp16_tiles<true>(a, qs, st, warp, g, c);
+  if (mode == kModeExact) {
+    run_tiles<kModeExact>(0, nloc, cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    fp16_tiles<true>(a, qs, st);
   } else {
-    run_tiles<false>(0, nloc, cnt2, a, src, mo, ring_l, qs, mg, st, warp);
-    fp16_tiles<false>(a, qs, st, warp, g, c);
+    if (mode == kModePrecise) run_tiles<kModePrecise>(0, nloc, cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    else run_tiles<kModeNormal>(0, nloc, cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    fp16_tiles<false>(a, qs, st);
     // undo the V m-tile weights 2^(2(mt&3) - 6)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {

@@ -152,7 +152,8 @@ template <bool ISV> struct MetaStageOff {
 // scale needs the decode's wide-scale mode.
 template <int BITS, bool ISV>
 __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, int sub, int j,
-                                               unsigned char* sc, unsigned char* sm, bool& bad) {
+                                               unsigned char* sc, unsigned char* sm, bool& bad,
+                                               float& smax) {
   using SO = StageOff<BITS, ISV>;
   using MO = MetaStageOff<ISV>;
   bool wide = false;
@@ -170,6 +171,7 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
       const uint32_t w[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
       float lo, hi;
       const uint32_t packed = quantize_slice<BITS>(w, lo, hi, bad, wide);
+      smax = fmaxf(smax, hi - lo);
       if (BITS == 2) {
         *reinterpret_cast<uint16_t*>(cb + u * SO::U) = (uint16_t)packed;
       } else {
@@ -248,10 +250,11 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
     unsigned char* sc = reinterpret_cast<unsigned char*>(s_codes[warp]);
     unsigned char* sm = reinterpret_cast<unsigned char*>(s_meta[warp]);
     bool wide;
-    if (tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, sub, j, sc, sm, bad)
-                               : quantize_chunk<2, false>(src, sT, sub, j, sc, sm, bad);
-    else wide = tsel ? quantize_chunk<4, true>(src, sT, sub, j, sc, sm, bad)
-                     : quantize_chunk<4, false>(src, sT, sub, j, sc, sm, bad);
+    float smax = 0.0f;  // largest group span of the chunk (decode precision routing)
+    if (tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, sub, j, sc, sm, bad, smax)
+                               : quantize_chunk<2, false>(src, sT, sub, j, sc, sm, bad, smax);
+    else wide = tsel ? quantize_chunk<4, true>(src, sT, sub, j, sc, sm, bad, smax)
+                     : quantize_chunk<4, false>(src, sT, sub, j, sc, sm, bad, smax);
     __syncwarp();
     // 128-bit coalesced stores of the packed chunk (2 tiles: 1 KB INT2 / 2 KB INT4) and its
     // metadata (2 x 256 B); tiles of a segment are contiguous
@@ -265,6 +268,10 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
     reinterpret_cast<uint4*>(meta)[lane] = reinterpret_cast<const uint4*>(s_meta[warp])[lane];
     if (__any_sync(0xffffffffu, wide) && lane == 0 && A.span_flags)
       atomicOr(A.span_flags + unit * B + b, tier == 0 ? 1u : 2u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    if (lane == 0 && A.span_max)  // non-negative floats order like their bit patterns
+      atomicMax(A.span_max + unit * B + b, __float_as_uint(smax));
     __syncwarp();
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE);
