@@ -90,25 +90,9 @@ __device__ __forceinline__ CtaIds cta_ids(int B) {
   return CtaIds{(int)x, (int)y, (int)z / B, (int)z % B};
 }
 
-struct Seq8 {
-  int off2, len2, off4, len4, off_fp, len_fp, tail_src, ctx;
-};
-
-__device__ __forceinline__ Seq8 ld_seq(const int32_t* seq, int b) {
-  const int4 a = reinterpret_cast<const int4*>(seq)[2 * b];
-  const int4 c = reinterpret_cast<const int4*>(seq)[2 * b + 1];
-  return Seq8{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-}
-
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
-  return r;
-}
-// Keep a constant in a register (LOP3 takes one immediate; the magic exponent is the 2nd).
-__device__ __forceinline__ uint32_t opaque(uint32_t v) {
-  uint32_t r;
-  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
   return r;
 }
 
@@ -143,7 +127,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 
 
 constexpr uint32_t kMagic16 = 0x4C004C00u;  // fp16 16.0 in both halves
-constexpr float kWideScale = 4000.0f;       // weighted mode needs 16 * sc and 12 * sc in fp16 range
 constexpr float kWideQ = 1000.0f;           // and |q| 2^6 in fp16 range
 // precise K path when (largest K group span) x max|q| (log2-scaled q) exceeds this: the normal
 // path's score error is ~2^-12 span |q| per group element (measured ~1.5e-3 relative output
