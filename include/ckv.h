@@ -140,12 +140,19 @@ int32_t ckv_assign_tiers(const double* scores, const double* thresholds,
  * D=128 row packs into 8 (INT2) / 16 (INT4) little-endian u32 words, _numpy.py:70-86) and
  * the rows' fp16 (lo, hi) group metadata, permuted in 16-bit pieces into the order the
  * decode kernel's MMA fragments consume them (layout functions tile_off_* in
- * csrc/ckv_common.cuh; K and V tiles differ).  ckv_arena_export restores reference rows. */
+ * csrc/ckv_common.cuh; K and V tiles differ).  K and V share one interleaved tile buffer per
+ * tier: tile t of the INT2 arenas is the 1536-byte block [K codes 512 | V codes 512 | K meta
+ * 256 | V meta 256] at t * 1536 (INT4: 2560-byte blocks [K codes 1024 | V codes 1024 | K meta
+ * 256 | V meta 256]), tiles indexed ([L][H] slab) * rows / 16 + row / 16.  So the K arena's
+ * codes2 / meta2 point at block offsets 0 / 1024 and the V arena's at 512 / 1280 (INT4: 0 /
+ * 2048 and 1024 / 2304); ckv_decode_attention checks this.  A decode tile is then one
+ * contiguous block (3 / 5 coalesced 16-byte copies per lane).  ckv_arena_export restores
+ * reference rows. */
 typedef struct ckv_arena {
-  uint32_t* codes2;   /* [L][H][rows2 / 16] tiles of 512 B  (16 rows x 8 u32)    */
-  uint32_t* meta2;    /* [L][H][rows2 / 16] tiles of 256 B  (16 rows x 4 (lo,hi)) */
-  uint32_t* codes4;   /* [L][H][rows4 / 16] tiles of 1024 B (16 rows x 16 u32)   */
-  uint32_t* meta4;    /* [L][H][rows4 / 16] tiles of 256 B                       */
+  uint32_t* codes2;   /* tile t at +t*1536: 512 B (16 rows x 8 u32)             */
+  uint32_t* meta2;    /* tile t at +t*1536: 256 B (16 rows x 4 (lo, hi) half2)    */
+  uint32_t* codes4;   /* tile t at +t*2560: 1024 B (16 rows x 16 u32)            */
+  uint32_t* meta4;    /* tile t at +t*2560: 256 B                                 */
   uint16_t* fp;       /* fp16 [L][H][rows_fp][128] (FP16 chunks || tail || decode) */
   uint32_t* span_flags; /* u32 [L][H][B], zero-filled before build: bit0/bit1 set when an
                            INT2/INT4 group's scale exceeds 4000 (decode then runs that unit in
@@ -193,10 +200,12 @@ int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, do
 
 /* Tile-native arena rows -> reference format (export / verification, quantizer.py:20-57):
  * `rows` (a multiple of 16) rows starting at a tile boundary of one arena (codes + meta of
- * the K arena when is_v == 0, of the V arena otherwise) -> out_codes u32 [rows][8 or 16]
+ * the K arena when is_v == 0, of the V arena otherwise; consecutive tiles `tile_stride` bytes
+ * apart, 1536 / 2560 for the interleaved INT2 / INT4 buffers) -> out_codes u32 [rows][8 or 16]
  * (pack_codes row format, _numpy.py:70-86) and out_meta half2 (lo, hi) [rows][4]. */
 int32_t ckv_arena_export(const uint32_t* codes, const uint32_t* meta, int64_t rows, int32_t bits,
-                         int32_t is_v, uint32_t* out_codes, uint32_t* out_meta, void* stream);
+                         int32_t is_v, int64_t tile_stride, uint32_t* out_codes,
+                         uint32_t* out_meta, void* stream);
 
 /* (3) Mixed-precision decode attention (attention.mixed_decode_attention, attention.py:63-90,
  * for every (layer, sequence, kv-head) unit at once).  q fp16 [L][B][H*m][128] (strides

@@ -8,10 +8,10 @@ Pipeline (one launch each, everything stays in HBM):
   cache.decode(q)               -> attention output per q head       (attention.py:63-90)
   cache.append(k_new, v_new)    -> decode-token append               (kv_store.py:135-148)
 
-HBM layout (per K and V, see include/ckv.h ckv_arena):
-  codes2 [L][H][rows2/16] tiles of 512 B     meta2 [L][H][rows2/16] tiles of 256 B
-  codes4 [L][H][rows4/16] tiles of 1024 B    meta4 [L][H][rows4/16] tiles of 256 B
-  fp     fp16 [L][H][rows_fp][128]
+HBM layout (see include/ckv.h ckv_arena):
+  tiles2 u8 [L][H][rows2/16][1536]  = per 16-row INT2 tile [K codes | V codes | K meta | V meta]
+  tiles4 u8 [L][H][rows4/16][2560]  = the same for INT4
+  fp     fp16 [L][H][rows_fp][128]  per K and V
 Rows of one sequence are contiguous inside each arena (varlen concatenation over the
 batch); the per-sequence table seq i32 [B][8] holds the offsets and lengths.  Quantized
 tiles hold exactly the bits of the reference's pack_codes rows and (lo, hi) metadata,
@@ -34,6 +34,8 @@ HEAD_DIM = 128
 GROUP = 32
 CHUNK = 32
 TILE = 16
+BLOCK2 = 1536  # interleaved INT2 tile: K codes 512 | V codes 512 | K meta 256 | V meta 256
+BLOCK4 = 2560  # interleaved INT4 tile: K codes 1024 | V codes 1024 | K meta 256 | V meta 256
 # algorithmic bytes per token per kv-head, K+V (codes + fp16 (lo,hi) metadata)
 BYTES_INT2 = 2 * (32 + 16)
 BYTES_INT4 = 2 * (64 + 16)
@@ -90,9 +92,10 @@ class BatchedKVCache:
         self.seq = torch.from_numpy(self.seq_host.copy()).to(dev)
         L, H = self.L, self.H
         z32 = lambda *s: torch.zeros(s, dtype=torch.int32, device=dev)  # noqa: E731
-        self.k = dict(codes2=z32(L, H, self.rows2, 8), meta2=z32(L, H, self.rows2, 4),
-                      codes4=z32(L, H, self.rows4, 16), meta4=z32(L, H, self.rows4, 4),
-                      fp=torch.zeros((L, H, self.rows_fp, HEAD_DIM), dtype=torch.float16, device=dev),
+        u8 = lambda *s: torch.zeros(s, dtype=torch.uint8, device=dev)  # noqa: E731
+        self.tiles2 = u8(L, H, self.rows2 // TILE, BLOCK2)
+        self.tiles4 = u8(L, H, self.rows4 // TILE, BLOCK4)
+        self.k = dict(fp=torch.zeros((L, H, self.rows_fp, HEAD_DIM), dtype=torch.float16, device=dev),
                       span_flags=z32(L, H, self.B), span_max=z32(L, H, self.B))
         self.v = {k: torch.zeros_like(t) for k, t in self.k.items()}
         self._ws = {}
@@ -113,11 +116,16 @@ class BatchedKVCache:
         return cache
 
     def arena(self, which, layer=0):
-        """ckv_arena view starting at `layer` (per-layer launches index layers from there)."""
+        """ckv_arena view starting at `layer` (per-layer launches index layers from there):
+        codes/meta pointers into the interleaved tile buffers (K at block offsets 0 / 2x codes,
+        V one code tile / one meta tile further)."""
         t = self.k if which == "k" else self.v
-        ptr = lambda name: t[name].data_ptr() + layer * t[name].stride(0) * t[name].element_size()  # noqa: E731
-        return _lib.Arena(ptr("codes2"), ptr("meta2"), ptr("codes4"), ptr("meta4"), ptr("fp"),
-                          ptr("span_flags"), ptr("span_max"), self.rows2, self.rows4, self.rows_fp)
+        ptr = lambda x: x.data_ptr() + layer * x.stride(0) * x.element_size()  # noqa: E731
+        v = which == "v"
+        b2, b4 = ptr(self.tiles2), ptr(self.tiles4)
+        return _lib.Arena(b2 + (512 if v else 0), b2 + 1024 + (256 if v else 0),
+                          b4 + (1024 if v else 0), b4 + 2048 + (256 if v else 0), ptr(t["fp"]),
+                          ptr(t["span_flags"]), ptr(t["span_max"]), self.rows2, self.rows4, self.rows_fp)
 
     def build(self, k, v, perm, check=True, layer=0):
         """ckv_reorder_quantize_pack over every unit of layers [layer, layer + L'); k, v fp16
@@ -299,7 +307,8 @@ class BatchedKVCache:
         return int(self.L * self.H * per_unit.sum() + 2 * self.L * self.B * self.H * m * HEAD_DIM * 2)
 
     def memory_bytes(self):
-        return sum(t.numel() * t.element_size() for d in (self.k, self.v) for t in d.values())
+        return (self.tiles2.numel() + self.tiles4.numel() +
+                sum(t.numel() * t.element_size() for d in (self.k, self.v) for t in d.values()))
 
     def wide_scale_units(self):
         """Number of (layer, kv-head, sequence) units that use the exact wide-scale path."""
@@ -314,13 +323,17 @@ class BatchedKVCache:
         off2, len2, off4, len4, offf, lenf, _, ctx = (int(x) for x in s)
 
         def block(t, which, bits):
-            codes = t["codes2" if bits == 2 else "codes4"][layer, head]
-            meta = t["meta2" if bits == 2 else "meta4"][layer, head]
             off, rows = (off2, len2) if bits == 2 else (off4, len4)
-            packed = torch.empty((rows, codes.shape[1]), dtype=torch.int32, device=self.device)
+            buf = (self.tiles2 if bits == 2 else self.tiles4)[layer, head, off // TILE:]
+            stride = BLOCK2 if bits == 2 else BLOCK4
+            code_bytes = 512 if bits == 2 else 1024
+            v = which == "v"
+            packed = torch.empty((rows, 8 if bits == 2 else 16), dtype=torch.int32, device=self.device)
             mt = torch.empty((rows, 4), dtype=torch.int32, device=self.device)
-            _lib.call("ckv_arena_export", _lib.ptr(codes[off:]), _lib.ptr(meta[off:]), rows, bits,
-                      int(which == "v"), _lib.ptr(packed), _lib.ptr(mt), _lib.stream())
+            base = buf.data_ptr()
+            _lib.call("ckv_arena_export", _lib._vp(base + (code_bytes if v else 0)),
+                      _lib._vp(base + 2 * code_bytes + (256 if v else 0)), rows, bits, int(v), stride,
+                      _lib.ptr(packed), _lib.ptr(mt), _lib.stream())
             packed = packed.reshape(-1)
             mt = mt.reshape(-1)
             sc = torch.empty(mt.numel(), dtype=torch.float64, device=self.device)

@@ -68,6 +68,9 @@ constexpr int kTileRows = 16;
 constexpr int kTileBytes2 = 512;    // INT2 codes tile (16 rows x 32 B)
 constexpr int kTileBytes4 = 1024;   // INT4 codes tile (16 rows x 64 B)
 constexpr int kTileBytesMeta = 256; // metadata tile (16 rows x 4 groups x (lo, hi))
+// K and V share one interleaved buffer per tier: [K codes | V codes | K meta | V meta]
+constexpr int kBlock2 = 2 * kTileBytes2 + 2 * kTileBytesMeta;  // 1536 B per INT2 tile
+constexpr int kBlock4 = 2 * kTileBytes4 + 2 * kTileBytesMeta;  // 2560 B per INT4 tile
 
 // K INT2: lane (g, c) = [tok g: w 2c, 2c+1 | tok g+8: w 2c, 2c+1]
 __host__ __device__ __forceinline__ int tile_off_k2(int rt, int w, int hf) {

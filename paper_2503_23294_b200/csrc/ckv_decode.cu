@@ -619,35 +619,33 @@ __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf
   }
 }
 
-// Per-lane byte offsets (from the arena bases, which stay in kernel parameters) of tile 0 of
-// this CTA's INT2 / INT4 ranges: codes + 16 lane, metadata + 8 lane.  K and V arenas share row
-// offsets.  Every copy below is a warp-wide contiguous 512-B / 256-B block.
+// Per-lane byte offsets (from the interleaved tile buffers' bases, which stay in kernel
+// parameters) of tile 0 of this CTA's INT2 / INT4 ranges, + 16 lane.  A tile is one
+// contiguous block [K codes | V codes | K meta | V meta] (include/ckv.h), copied verbatim into
+// the stage with 16-byte cp.async: 3 per lane (INT2) / 5 (INT4), every one a warp-wide
+// contiguous 512-byte run.
 struct TileSrc {
-  int64_t c2, m2, c4, m4;
+  int64_t c2, c4;
 };
 
-// Warp-wide: stage one quantized tile (tile-native layout) into the stage whose lane slot is
-// `sl` with 16-/8-byte cp.async.  Commits a (possibly empty) group.
+// Warp-wide: stage one quantized tile into the stage whose lane slot is `sl`.  Commits a
+// (possibly empty) group.
 __device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const DecArgs& a,
                                            const TileSrc& o, const MetaOff& mo, uint32_t sl) {
+  (void)mo;
   if (t < t_q_end) {
     if (t < n2t) {
-      const int64_t oc = o.c2 + (int64_t)t * kTileBytes2, om = o.m2 + (int64_t)t * kTileBytesMeta;
-      cp_async16(sl, reinterpret_cast<const char*>(a.K.codes2) + oc);
-      cp_async16(sl + 512, reinterpret_cast<const char*>(a.V.codes2) + oc);
-      cp_async8(sl + 1024 + mo.k, reinterpret_cast<const char*>(a.K.meta2) + om);
-      cp_async8(sl + 1280 + mo.k, reinterpret_cast<const char*>(a.V.meta2) + om);
+      const char* p = reinterpret_cast<const char*>(a.K.codes2) + o.c2 + (int64_t)t * kBlock2;
+      cp_async16(sl, p);
+      cp_async16(sl + 512, p + 512);
+      cp_async16(sl + 1024, p + 1024);
     } else {
-      const int64_t t4 = t - n2t;
-      const int64_t oc = o.c4 + t4 * kTileBytes4, om = o.m4 + t4 * kTileBytesMeta;
-      const char* kc = reinterpret_cast<const char*>(a.K.codes4) + oc;
-      const char* vc = reinterpret_cast<const char*>(a.V.codes4) + oc;
-      cp_async16(sl, kc);
-      cp_async16(sl + 512, kc + 512);
-      cp_async16(sl + 1024, vc);
-      cp_async16(sl + 1536, vc + 512);
-      cp_async8(sl + 2048 + mo.k, reinterpret_cast<const char*>(a.K.meta4) + om);
-      cp_async8(sl + 2304 + mo.k, reinterpret_cast<const char*>(a.V.meta4) + om);
+      const char* p = reinterpret_cast<const char*>(a.K.codes4) + o.c4 + (int64_t)(t - n2t) * kBlock4;
+      cp_async16(sl, p);
+      cp_async16(sl + 512, p + 512);
+      cp_async16(sl + 1024, p + 1024);
+      cp_async16(sl + 1536, p + 1536);
+      cp_async16(sl + 2048, p + 2048);
     }
   }
   cp_commit();
@@ -792,10 +790,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     nloc = cnt2 + (b4 - a4);
     const int64_t unit = (int64_t)id.l * a.H + id.h;
     const int64_t r2 = s0.x + (int64_t)a2 * kTile, r4 = s0.z + (int64_t)a4 * kTile;  // first rows
-    src.c2 = (unit * a.K.rows2 + r2) * 32 + 16 * lane;
-    src.m2 = (unit * a.K.rows2 + r2) * 16 + 8 * lane;
-    src.c4 = (unit * a.K.rows4 + r4) * 64 + 16 * lane;
-    src.m4 = (unit * a.K.rows4 + r4) * 16 + 8 * lane;
+    src.c2 = (unit * a.K.rows2 + r2) / kTileRows * kBlock2 + 16 * lane;
+    src.c4 = (unit * a.K.rows4 + r4) / kTileRows * kBlock4 + 16 * lane;
   }
   MetaOff mo;
   mo.k = -8 * lane;
@@ -1109,6 +1105,19 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
   if (splits > 1 && !workspace) return CKV_ERR_ARG;
   if ((q_s_layer % 8) || (q_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
   if (layers * batch * kv_heads == 0) return CKV_OK;
+  {  // interleaved K/V tile buffers (include/ckv.h)
+    const char* k2 = reinterpret_cast<const char*>(k_arena.codes2);
+    const char* k4 = reinterpret_cast<const char*>(k_arena.codes4);
+    const bool ok2 = k_arena.rows2 == 0 ||
+                     (reinterpret_cast<const char*>(v_arena.codes2) == k2 + kTileBytes2 &&
+                      reinterpret_cast<const char*>(k_arena.meta2) == k2 + 2 * kTileBytes2 &&
+                      reinterpret_cast<const char*>(v_arena.meta2) == k2 + 2 * kTileBytes2 + kTileBytesMeta);
+    const bool ok4 = k_arena.rows4 == 0 ||
+                     (reinterpret_cast<const char*>(v_arena.codes4) == k4 + kTileBytes4 &&
+                      reinterpret_cast<const char*>(k_arena.meta4) == k4 + 2 * kTileBytes4 &&
+                      reinterpret_cast<const char*>(v_arena.meta4) == k4 + 2 * kTileBytes4 + kTileBytesMeta);
+    if (!ok2 || !ok4 || k_arena.rows2 != v_arena.rows2 || k_arena.rows4 != v_arena.rows4) return CKV_ERR_ARG;
+  }
   DecArgs a;
   a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
   a.K = k_arena; a.V = v_arena; a.seq = seq;

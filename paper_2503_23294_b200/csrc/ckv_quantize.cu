@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float
 // so each store costs one add (the GPU parity tests read every arena back through
 // ckv_arena_export, i.e. through tile_off_*, and compare with the reference bit for bit).
 template <int BITS, bool ISV> struct StageOff {
-  static constexpr int TB = BITS == 2 ? kTileBytes2 : kTileBytes4;
+  static constexpr int TB = BITS == 2 ? kBlock2 : kBlock4;  // staging holds whole K/V blocks
   static constexpr int X = BITS == 2 ? 8 : 512;
   static constexpr int U = ISV ? 16 : 128;
   __device__ __forceinline__ static int lane(int j, int sub) {
@@ -137,8 +137,8 @@ template <int BITS, bool ISV> struct StageOff {
                : sub * 64 + (j >> 2) * 16 + ((j & 3) >> 1) * 8 + (j & 1) * 2;  // hf = 1: + 4
   }
 };
-template <bool ISV> struct MetaStageOff {
-  static constexpr int TB = kTileBytesMeta;
+template <int BITS, bool ISV> struct MetaStageOff {
+  static constexpr int TB = BITS == 2 ? kBlock2 : kBlock4;
   static constexpr int X = ISV ? 8 : 4;
   static constexpr int U = ISV ? 16 : 64;
   __device__ __forceinline__ static int lane(int j, int sub) {  // lo; hi at + (ISV ? 4 : 2)
@@ -155,7 +155,7 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
                                                unsigned char* sc, unsigned char* sm, bool& bad,
                                                float& smax) {
   using SO = StageOff<BITS, ISV>;
-  using MO = MetaStageOff<ISV>;
+  using MO = MetaStageOff<BITS, ISV>;
   bool wide = false;
   const int lc = SO::lane(j, sub), lm = MO::lane(j, sub);
 #pragma unroll 1
@@ -194,15 +194,15 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
 
 // One warp per (layer, sequence, kv-head, destination chunk slot).  Slot p < N takes source
 // chunk perm[p]; slot p == N is the context tail (if any).
-__global__ void __launch_bounds__(kQWarps * 32)
+__global__ void __launch_bounds__(kQWarps * 32, 6)
 reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
                              int H, int B, int64_t sL, int64_t sB, int64_t sT, int64_t sH,
                              const uint32_t* __restrict__ perm, int max_chunks,
                              const int32_t* __restrict__ seq, ckv_arena KA, ckv_arena VA,
                              int32_t* flag) {
-  // staging of one packed chunk (2 tiles) in the tile-native layout (ckv_common.cuh)
-  __shared__ __align__(16) uint32_t s_codes[kQWarps][512];  // 2 KB per warp (INT4 chunk)
-  __shared__ __align__(16) uint32_t s_meta[kQWarps][128];   // 512 B per warp
+  // staging of one packed chunk: its 2 interleaved K/V tile blocks (ckv_common.cuh), written
+  // by the K pass and the V pass, then stored as one contiguous 3 KB / 5 KB run
+  __shared__ __align__(16) unsigned char s_blk[kQWarps][2 * kBlock4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x * kQWarps + warp;
   const int h = blockIdx.y;
@@ -247,8 +247,9 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       }
       continue;
     }
-    unsigned char* sc = reinterpret_cast<unsigned char*>(s_codes[warp]);
-    unsigned char* sm = reinterpret_cast<unsigned char*>(s_meta[warp]);
+    const int code_bytes = tier == 0 ? kTileBytes2 : kTileBytes4;
+    unsigned char* sc = s_blk[warp] + (tsel ? code_bytes : 0);
+    unsigned char* sm = s_blk[warp] + 2 * code_bytes + (tsel ? kTileBytesMeta : 0);
     bool wide;
     float smax = 0.0f;  // largest group span of the chunk (decode precision routing)
     if (tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, sub, j, sc, sm, bad, smax)
@@ -256,16 +257,13 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
     else wide = tsel ? quantize_chunk<4, true>(src, sT, sub, j, sc, sm, bad, smax)
                      : quantize_chunk<4, false>(src, sT, sub, j, sc, sm, bad, smax);
     __syncwarp();
-    // 128-bit coalesced stores of the packed chunk (2 tiles: 1 KB INT2 / 2 KB INT4) and its
-    // metadata (2 x 256 B); tiles of a segment are contiguous
-    uint32_t* codes = tier == 0 ? A.codes2 + (unit * A.rows2 + dst_row0) * 8
-                                : A.codes4 + (unit * A.rows4 + dst_row0) * 16;
-    uint32_t* meta = tier == 0 ? A.meta2 + (unit * A.rows2 + dst_row0) * 4
-                               : A.meta4 + (unit * A.rows4 + dst_row0) * 4;
-    const int n16 = tier == 0 ? 64 : 128;
-    for (int i = lane; i < n16; i += 32)
-      reinterpret_cast<uint4*>(codes)[i] = reinterpret_cast<const uint4*>(s_codes[warp])[i];
-    reinterpret_cast<uint4*>(meta)[lane] = reinterpret_cast<const uint4*>(s_meta[warp])[lane];
+    if (tsel) {  // both halves staged: 128-bit coalesced stores of the 2 contiguous blocks
+      const int64_t blk = tier == 0 ? kBlock2 : kBlock4;
+      const int64_t tile0 = (unit * (tier == 0 ? KA.rows2 : KA.rows4) + dst_row0) / kTileRows;
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(tier == 0 ? KA.codes2 : KA.codes4) + tile0 * blk);
+      const int n16 = (int)(2 * blk / 16);
+      for (int i = lane; i < n16; i += 32) dst[i] = reinterpret_cast<const uint4*>(s_blk[warp])[i];
+    }
     if (__any_sync(0xffffffffu, wide) && lane == 0 && A.span_flags)
       atomicOr(A.span_flags + unit * B + b, tier == 0 ? 1u : 2u);
 #pragma unroll
@@ -313,14 +311,14 @@ __global__ void expand_meta_kernel(const uint32_t* __restrict__ meta, int64_t n,
 // (lo, hi) metadata [rows][4]: the inverse gather of the tile layout (ckv_common.cuh).
 __global__ void arena_export_kernel(const unsigned char* __restrict__ codes,
                                     const unsigned char* __restrict__ meta, int64_t rows, int words,
-                                    int is_v, uint32_t* __restrict__ out_codes,
+                                    int is_v, int64_t stride, uint32_t* __restrict__ out_codes,
                                     uint32_t* __restrict__ out_meta) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t n_code = rows * words;
   if (i < n_code) {
     const int64_t r = i / words;
     const int w = (int)(i % words), rt = (int)(r & 15);
-    const unsigned char* t = codes + (r >> 4) * (words == 8 ? kTileBytes2 : kTileBytes4);
+    const unsigned char* t = codes + (r >> 4) * stride;
     int o0, o1;
     if (words == 8) {
       o0 = is_v ? tile_off_v2(rt, w, 0) : tile_off_k2(rt, w, 0);
@@ -334,7 +332,7 @@ __global__ void arena_export_kernel(const unsigned char* __restrict__ codes,
   } else if (i < n_code + rows * kGroupsPerRow) {
     const int64_t k = i - n_code, r = k / kGroupsPerRow;
     const int G = (int)(k % kGroupsPerRow), rt = (int)(r & 15);
-    const unsigned char* t = meta + (r >> 4) * kTileBytesMeta;
+    const unsigned char* t = meta + (r >> 4) * stride;
     const int o0 = is_v ? tile_off_vm(rt, G, 0) : tile_off_km(rt, G, 0);
     const int o1 = is_v ? tile_off_vm(rt, G, 1) : tile_off_km(rt, G, 1);
     out_meta[k] = (uint32_t)*reinterpret_cast<const uint16_t*>(t + o0) |
@@ -392,16 +390,17 @@ int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, do
 }
 
 int32_t ckv_arena_export(const uint32_t* codes, const uint32_t* meta, int64_t rows, int32_t bits,
-                         int32_t is_v, uint32_t* out_codes, uint32_t* out_meta, void* stream) {
+                         int32_t is_v, int64_t tile_stride, uint32_t* out_codes,
+                         uint32_t* out_meta, void* stream) {
   if (bits != 2 && bits != 4) return CKV_ERR_BITS;
   if (rows < 0 || (rows % kTileRows)) return CKV_ERR_SHAPE;
   if (rows == 0) return CKV_OK;
-  if (!codes || !meta || !out_codes || !out_meta) return CKV_ERR_ARG;
+  if (!codes || !meta || !out_codes || !out_meta || tile_stride <= 0) return CKV_ERR_ARG;
   const int words = bits == 2 ? 8 : 16;
   const int64_t n = rows * (words + kGroupsPerRow);
   arena_export_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const unsigned char*>(codes), reinterpret_cast<const unsigned char*>(meta),
-      rows, words, is_v, out_codes, out_meta);
+      rows, words, is_v, tile_stride, out_codes, out_meta);
   CKV_LAUNCH_CHECK();
   return CKV_OK;
 }

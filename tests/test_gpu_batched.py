@@ -277,8 +277,8 @@ def test_layer_by_layer_build_and_per_layer_partials():
     per = batched.BatchedKVCache(L, B, H, counts[:, 0], counts[:, 1], counts[:, 2], [T] * B, device=k.device)
     for l in range(L):
         per.build(k[l:l + 1], v[l:l + 1], s.perm, layer=l)
-    for name in ("codes2", "meta2", "codes4", "meta4", "fp"):
-        assert torch.equal(full.k[name], per.k[name]) and torch.equal(full.v[name], per.v[name]), name
+    assert torch.equal(full.tiles2, per.tiles2) and torch.equal(full.tiles4, per.tiles4)
+    assert torch.equal(full.k["fp"], per.k["fp"]) and torch.equal(full.v["fp"], per.v["fp"])
     want = full.decode_partial(q)
     got = torch.empty_like(want)
     rows = B * H * m
