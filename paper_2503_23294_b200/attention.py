@@ -64,10 +64,15 @@ class AttentionInstance:
 
 def mixed_decode_attention(inst: AttentionInstance) -> np.ndarray:
     """attention.py:63-90 on the GPU (f64)."""
-    cache = inst.cache
-    if cache.total_tokens == 0:
+    if inst.cache.total_tokens == 0:
         raise ValueError("cache holds no tokens")
-    q = kernels.to_dev(inst.q, torch.float64)
+    mask = kernels.to_dev(inst.mask, torch.float64) if inst.mask is not None else None
+    return mixed_decode_dev(kernels.to_dev(inst.q, torch.float64), inst.cache, inst.scale, mask).cpu().numpy()
+
+
+def mixed_decode_dev(q, cache: ChunkedKVCache, scale, mask=None, out=None):
+    """The blocked attention of ``mixed_decode_attention`` on device tensors (q f64 [m, d] on
+    the GPU, optional f64 mask on the GPU) -> f64 [m, d] on the GPU (into ``out`` if given)."""
     m = q.shape[0]
     n2, n4, nf = cache.len_2, cache.len_4, cache.len_fp
     total = n2 + n4 + nf
@@ -76,13 +81,13 @@ def mixed_decode_attention(inst: AttentionInstance) -> np.ndarray:
     quantizer.fqm_dev(q, cache.k_q2, True, out=att[:, :n2])            # attention.py:75
     quantizer.fqm_dev(q, cache.k_q4, True, out=att[:, n2:n2 + n4])     # attention.py:76
     kernels.matmul_dev(q, kfp, True, out=att[:, n2 + n4:])             # attention.py:77
-    mask = kernels.to_dev(inst.mask, torch.float64) if inst.mask is not None else None
-    _softmax_dev(att, inst.scale, mask)                                # attention.py:79-82
-    out = torch.empty((m, cache.head_dim), dtype=torch.float64, device=q.device)
+    _softmax_dev(att, scale, mask)                                     # attention.py:79-82
+    if out is None:
+        out = torch.empty((m, cache.head_dim), dtype=torch.float64, device=q.device)
     quantizer.fqm_dev(att[:, :n2], cache.v_q2, False, out=out)          # attention.py:90
     quantizer.fqm_dev(att[:, n2:n2 + n4], cache.v_q4, False, out=out, accumulate=True)
     kernels.matmul_dev(att[:, n2 + n4:], vfp, False, out=out, accumulate=True)
-    return out.cpu().numpy()
+    return out
 
 
 def reference_attention(q, k, v, mask=None, scale=None) -> np.ndarray:
@@ -94,18 +99,51 @@ def reference_attention(q, k, v, mask=None, scale=None) -> np.ndarray:
         raise ValueError("q, k, v must be 2D")
     if q.shape[1] != k.shape[1] or k.shape[0] != v.shape[0]:
         raise ValueError("attention shape mismatch")
-    if scale is None:
-        scale = 1.0 / math.sqrt(q.shape[1])
     if mask is not None:
         mask = np.asarray(mask, dtype=np.float64)
         if mask.shape != (q.shape[0], k.shape[0]):
             raise ValueError("mask shape must be (m, tokens)")
     qd, kd, vd = (kernels.to_dev(x, torch.float64) for x in (q, k, v))
-    att = kernels.matmul_dev(qd, kd, True)
-    _softmax_dev(att, scale, kernels.to_dev(mask, torch.float64) if mask is not None else None)
-    return kernels.matmul_dev(att, vd, False).cpu().numpy()
+    md = kernels.to_dev(mask, torch.float64) if mask is not None else None
+    return reference_attention_dev(qd, kd, vd, md, scale).cpu().numpy()
+
+
+def reference_attention_dev(q, k, v, mask=None, scale=None, out=None):
+    """``reference_attention`` on device f64 tensors (column slices allowed: rows are strided)."""
+    if scale is None:
+        scale = 1.0 / math.sqrt(q.shape[1])
+    att = kernels.matmul_dev(q, k, True)
+    _softmax_dev(att, scale, mask)
+    return kernels.matmul_dev(att, v, False, out=out)
 
 
 def causal_mask(n) -> np.ndarray:
     """attention.py:115-117."""
     return np.triu(np.full((n, n), -np.inf), k=1)
+
+
+def prefill_attention(embeddings, model, return_hidden=False):
+    """attention.py:120-145: single-layer causal self-attention over the prompt of the toy
+    model, on the GPU in f64.  Returns the full-precision K and V projections (tokens x
+    embed_dim, heads side by side), the last position's logits and optionally the hidden
+    states (embeddings + concatenated head outputs)."""
+    emb = np.ascontiguousarray(embeddings, dtype=np.float64)
+    if emb.ndim != 2 or emb.shape[1] != model.embed_dim:
+        raise ValueError("embeddings must be (tokens, embed_dim)")
+    n, d = emb.shape[0], model.head_dim
+    if n == 0:  # the reference fails on logits[-1] of an empty prompt
+        raise IndexError("index -1 is out of bounds for axis 0 with size 0")
+    w = model.device_weights()
+    e = kernels.to_dev(emb, torch.float64)
+    q, k, v = (kernels.matmul_dev(e, w[name], False) for name in ("w_q", "w_k", "w_v"))
+    mask = kernels.to_dev(causal_mask(n), torch.float64)
+    hidden = e.clone()
+    for h in range(model.n_heads):
+        cols = slice(h * d, (h + 1) * d)
+        hidden[:, cols] += reference_attention_dev(q[:, cols], k[:, cols], v[:, cols], mask)
+    logits = kernels.matmul_dev(hidden, w["w_o"], False)
+    k_h, v_h = k.cpu().numpy(), v.cpu().numpy()
+    last = logits[-1].cpu().numpy()
+    if return_hidden:
+        return k_h, v_h, last, hidden.cpu().numpy()
+    return k_h, v_h, last

@@ -9,6 +9,7 @@ here as small .npz fixtures that the oracle (tests/test_oracle.py) and the CUDA 
 
 from __future__ import annotations
 
+import hashlib
 import os
 import sys
 
@@ -21,7 +22,9 @@ from chunkkv import kernels as rk  # noqa: E402
 from chunkkv import quantizer as rq  # noqa: E402
 from chunkkv.attention import AttentionInstance, mixed_decode_attention, reference_attention  # noqa: E402
 from chunkkv.harness import RunConfig, synth_workload  # noqa: E402
-from chunkkv.kv_store import build_cache, reconstruct  # noqa: E402
+from chunkkv.attention import prefill_attention  # noqa: E402
+from chunkkv.kv_store import build_cache, reconstruct, serialize_cache  # noqa: E402
+from chunkkv.toy_model import ToyModel, generate  # noqa: E402
 from chunkkv.retrieval import (HashedBowEncoder, build_similarity_report, score_chunks,  # noqa: E402
                                segment_context)
 from chunkkv.tiers import Tier  # noqa: E402
@@ -173,8 +176,59 @@ def batched_case():
                     out[f"{name}_scales_{key}"] = blk.scales
                     out[f"{name}_zps_{key}"] = blk.zero_points
                 out[f"perm_{key}"] = cache.perm
+                wire = serialize_cache(cache)  # kv_store.py:310-360, the bit-exact wire format
+                out[f"wire_len_{key}"] = np.array(len(wire))
+                out[f"wire_sha256_{key}"] = np.frombuffer(hashlib.sha256(wire).digest(), np.uint8)
                 qq = q[l, b, h * m:(h + 1) * m].astype(np.float64)
                 out[f"out_{key}"] = mixed_decode_attention(AttentionInstance(q=qq, cache=cache))
+    return out
+
+
+# toy-model scenarios: (vocab, embed_dim, heads, seed, prompt_len, tier pattern, chunk, group, steps)
+TOY_SPECS = [
+    (64, 16, 2, 7, 24, "int2_int4", 4, 8, 10),
+    (128, 32, 4, 8, 56, "fp16", 8, 8, 16),
+    (64, 16, 2, 9, 32, "int4", 8, 8, 4),
+    (512, 64, 4, 0, 200, "random", 32, 16, 24),
+    (256, 128, 1, 3, 300, "random", 32, 32, 12),
+]
+
+
+def toy_tiers(pattern, n, rng):
+    if pattern == "int2_int4":
+        return [Tier.INT2, Tier.INT4] * (n // 2) + [Tier.INT2] * (n % 2)
+    if pattern in ("fp16", "int4"):
+        return [Tier(pattern)] * n
+    return [Tier(t) for t in rng.choice(["int2", "int4", "fp16"], size=n)]
+
+
+def toy_cases():
+    """The reference's own caller of the path (toy_model.generate over per-head caches built
+    from prefill_attention's K/V), on the tests' scenarios and two larger ones."""
+    out = {}
+    rng = np.random.default_rng(11)
+    for i, (vocab, dim, heads, seed, n_prompt, pattern, cs, gs, steps) in enumerate(TOY_SPECS):
+        model = ToyModel(vocab_size=vocab, embed_dim=dim, n_heads=heads, seed=seed)
+        prompt = [int(t) for t in rng.integers(0, vocab, size=n_prompt)]
+        emb = model.embed(prompt)
+        k, v, logits, hidden = prefill_attention(emb, model, return_hidden=True)
+        chunk_set = segment_context(prompt, cs)
+        tiers = toy_tiers(pattern, chunk_set.n, rng)
+        d = model.head_dim
+        caches = [build_cache(k[:, h * d:(h + 1) * d], v[:, h * d:(h + 1) * d], tiers, chunk_set, gs)
+                  for h in range(heads)]
+        first = int(np.argmax(logits))
+        gen = generate(model, caches, first, steps, start_pos=n_prompt)
+        out[f"spec{i}"] = np.array([vocab, dim, heads, seed, n_prompt, cs, gs, steps])
+        out[f"prompt{i}"] = np.array(prompt, np.int64)
+        out[f"tiers{i}"] = np.array([TIER_CODE[t] for t in tiers], np.uint8)
+        out[f"prefill_logits{i}"] = logits
+        out[f"prefill_hidden{i}"] = hidden[-4:]  # last rows (the fixture stays small)
+        out[f"first{i}"] = np.array(first)
+        out[f"tokens{i}"] = np.array(gen.tokens, np.int64)
+        out[f"final_hidden{i}"] = gen.final_hidden
+        out[f"w_sum{i}"] = np.array([model.w_e.sum(), model.w_q.sum(), model.w_o.sum()])
+    out["n"] = np.array(len(TOY_SPECS))
     return out
 
 
@@ -185,6 +239,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "search.npz"), **search_cases())
     np.savez_compressed(os.path.join(HERE, "attention.npz"), **attention_cases())
     np.savez_compressed(os.path.join(HERE, "batched.npz"), **batched_case())
+    np.savez_compressed(os.path.join(HERE, "toy.npz"), **toy_cases())
     print("reference backend:", rk.BACKEND, "chunkkv", chunkkv.__version__, file=sys.stderr)
 
 

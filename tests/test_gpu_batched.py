@@ -2,6 +2,8 @@
 permutation) and mixed-precision decode attention (1e-2 abs / 1e-2 rel of the reference's
 f64 result on the same fp16 inputs), edge cases, split-KV shards, and full-size properties."""
 
+import hashlib
+
 import numpy as np
 import pytest
 import torch
@@ -12,6 +14,7 @@ from tests.conftest import load_golden
 pytestmark = pytest.mark.gpu
 
 from paper_2503_23294_b200 import batched, distributed, retrieval  # noqa: E402
+from paper_2503_23294_b200.kv_store import serialize_cache  # noqa: E402
 
 TOL_ABS = 1e-2
 TOL_REL = 1e-2
@@ -51,7 +54,11 @@ def test_batched_golden_case():
         for b in range(B):
             for h in range(H):
                 key = f"{l}_{b}_{h}"
-                ex = cache.export_unit(l, b, h)
+                ex = cache.export_unit(l, b, h, perm=g[f"perm_{key}"])
+                # the reference's wire format straight from the GPU arenas
+                wire = serialize_cache(ex)
+                assert len(wire) == int(g[f"wire_len_{key}"])
+                assert hashlib.sha256(wire).digest() == g[f"wire_sha256_{key}"].tobytes(), key
                 for name in ("k_q2", "v_q2", "k_q4", "v_q4"):
                     blk = getattr(ex, name)
                     assert np.array_equal(blk.packed, g[f"{name}_packed_{key}"])
