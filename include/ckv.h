@@ -109,6 +109,25 @@ int32_t ckv_scatter_rows_f64(const double* src, int64_t rows, int64_t cols, cons
  * Batched hot path: fp16 K/V, head_dim 128, group 32, chunk 32.
  * ==================================================================== */
 
+/* (0) Text encoders upstream of the search (retrieval.py:70-138).  They replace
+ * the reference's per-text Python encode() calls (HashedBowEncoder.encode retrieval.py:87-100,
+ * TfidfEncoder.encode retrieval.py:122-138) with one launch over all texts; the output rows are
+ * ckv_search's emb / q inputs.
+ * ckv_bow_encode: text = UTF-8 bytes of n_texts texts back to back, offsets i64[n_texts + 1]
+ *   (device); key = HOST bytes of the BLAKE2b key (the seed's decimal ASCII), key_len <= 64;
+ *   -> vectors f64[n_texts, dim], norms f64[n_texts] (1.0, or 0.0 for a text without words or
+ *   with all buckets cancelled).  Words split at str.isspace() characters; dim <= 8192.
+ *   Bit-identical to the reference.
+ * ckv_tfidf_encode: vocabulary ids i32 (the caller maps words through the fitted sorted
+ *   vocabulary, dropping unknown words), offsets i64[n_texts + 1], idf f64[vocab] -> vectors
+ *   f64[n_texts, ld] (columns >= vocab zero), norms f64[n_texts].  Within a few ulp (the norm's
+ *   summation order is not BLAS's). */
+int32_t ckv_bow_encode(const uint8_t* text, const int64_t* offsets, int32_t n_texts, int32_t dim,
+                       const uint8_t* key, int32_t key_len, double* vectors, double* norms,
+                       void* stream);
+int32_t ckv_tfidf_encode(const int32_t* ids, const int64_t* offsets, int32_t n_texts, const double* idf,
+                         int32_t vocab, int32_t ld, double* vectors, double* norms, void* stream);
+
 /* (1) Chunk-level quantization search (retrieval.py:199-250 + kv_store.py:190-206).
  * Per sequence b: cosine of q[b] with each chunk embedding (zero-norm chunks take the
  * minimum valid score, retrieval.py:217-219), thresholds (retrieval.py:222-237), strict

@@ -333,3 +333,47 @@ def lse_merge(ms, ls, accs):
     den = (np.asarray(ls, np.float64) * w).sum(axis=0)
     num = (np.asarray(accs, np.float64) * w[..., None]).sum(axis=0)
     return num / den[..., None]
+
+
+# -- text encoders upstream of the search (retrieval.py:70-138) --------------------------
+
+def bow_encode(text, dim=256, seed=0):
+    """HashedBowEncoder.encode (retrieval.py:87-100): keyed BLAKE2b-64 per whitespace word
+    (hashlib, the reference's own hash), sign from bit 63, bucket h % dim, L2-normalised."""
+    import hashlib
+
+    key = str(int(seed)).encode("ascii")
+    vec = np.zeros(dim, dtype=np.float64)
+    for word in text.split():
+        h = int.from_bytes(hashlib.blake2b(word.encode("utf-8"), key=key, digest_size=8).digest(), "little")
+        vec[h % dim] += -1.0 if h >> 63 else 1.0
+    norm = float(np.linalg.norm(vec))
+    if norm > 0.0:
+        return vec / norm, 1.0
+    return vec, norm
+
+
+def tfidf_fit(texts):
+    """TfidfEncoder.fit (retrieval.py:111-120) -> (word -> index, idf)."""
+    texts = list(texts)
+    vocab = sorted({w for t in texts for w in t.split()})
+    index = {w: i for i, w in enumerate(vocab)}
+    df = np.zeros(len(vocab), dtype=np.float64)
+    for t in texts:
+        for w in set(t.split()):
+            df[index[w]] += 1.0
+    return index, np.log((1.0 + len(texts)) / (1.0 + df)) + 1.0
+
+
+def tfidf_encode(text, index, idf):
+    """TfidfEncoder.encode (retrieval.py:122-138)."""
+    vec = np.zeros(len(index), dtype=np.float64)
+    for w in text.split():
+        i = index.get(w)
+        if i is not None:
+            vec[i] += 1.0
+    vec *= idf
+    norm = float(np.linalg.norm(vec))
+    if norm > 0.0:
+        return vec / norm, 1.0
+    return vec, norm

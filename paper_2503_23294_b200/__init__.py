@@ -12,6 +12,7 @@ Per-head (reference-shaped, float64) API:
     AttentionInstance, mixed_decode_attention, reference_attention, stable_softmax
     score_chunks, cosine_similarity, compute_thresholds, assign_tiers,
     build_similarity_report, segment_context, ChunkSet, Embedding, Tier
+    HashedBowEncoder, TfidfEncoder, PrecomputedEncoder, make_encoder, encode, search_texts
     prefill_attention, ToyModel, generate, GenerationResult (the reference's toy-model caller)
 Batched fp16 hot path (all layers x sequences x kv-heads, head_dim 128):
     search_batched, BatchedKVCache, build_cache_batched, mixed_decode_attention_batched,
@@ -56,6 +57,12 @@ from .quantizer import (
 from .retrieval import (
     ChunkSet,
     Embedding,
+    HashedBowEncoder,
+    PrecomputedEncoder,
+    TfidfEncoder,
+    encode,
+    make_encoder,
+    search_texts,
     SearchResult,
     SimilarityReport,
     assign_tiers,
@@ -74,7 +81,8 @@ from .toy_model import GenerationResult, ToyModel, generate
 __version__ = "0.1.0"
 
 __all__ = [
-    "AttentionInstance", "BACKEND", "GenerationResult", "ToyModel", "generate", "prefill_attention", "BatchedKVCache", "ChunkSet", "ChunkedKVCache", "Embedding",
+    "AttentionInstance", "BACKEND", "GenerationResult", "HashedBowEncoder", "PrecomputedEncoder",
+    "TfidfEncoder", "encode", "make_encoder", "search_texts", "ToyModel", "generate", "prefill_attention", "BatchedKVCache", "ChunkSet", "ChunkedKVCache", "Embedding",
     "MemoryReport", "QuantizedBlock", "SearchResult", "SimilarityReport", "Tier",
     "append_decode_token", "assign_tiers", "assign_tiers_batched", "build_cache",
     "build_cache_batched", "build_similarity_report", "cache_layout", "causal_mask",

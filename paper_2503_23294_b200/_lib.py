@@ -66,6 +66,8 @@ _SIGNATURES = {
     "ckv_scatter_rows_f64": ([_vp, _i64, _i64, _vp, _vp, _vp], _i32),
     "ckv_search": ([_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _f64, _f64, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp], _i32),
+    "ckv_bow_encode": ([_vp, _vp, _i32, _i32, ctypes.c_char_p, _i32, _vp, _vp, _vp], _i32),
+    "ckv_tfidf_encode": ([_vp, _vp, _i32, _vp, _i32, _i32, _vp, _vp, _vp], _i32),
     "ckv_assign_tiers": ([_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "ckv_reorder_quantize_pack": ([_vp, _vp, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _vp, _i32,
                                    _vp, _i32, Arena, Arena, _vp, _vp], _i32),

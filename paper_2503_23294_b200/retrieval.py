@@ -1,10 +1,15 @@
-"""Chunk-level quantization search (Module I) — drop-in for the scoring half of
-``chunkkv.retrieval`` (retrieval.py:17-67, 199-279), computed by the ckv_search kernel.
+"""Chunk-level quantization search (Module I) — drop-in for ``chunkkv.retrieval``
+(retrieval.py:17-279): scoring, thresholds, tiers and the stable permutation in the
+ckv_search kernel, and the text encoders upstream of it.
 
-Text encoders (HashedBow/TF-IDF/precomputed, retrieval.py:70-191) produce the kernel's
-*input* embeddings on the host; they are outside this hot path and not
-rebuilt.  ``Embedding`` and ``segment_context`` are kept as plain host types because
-build_cache's signature uses them.
+Encoders (retrieval.py:70-191): ``HashedBowEncoder`` runs on the GPU (ckv_bow_encode:
+UTF-8 whitespace split, keyed BLAKE2b-64 per word, signed buckets, L2 normalisation; the
+embeddings equal the reference's bit for bit).  ``TfidfEncoder`` fits its sorted vocabulary
+and smoothed idf on the host like the reference, maps words to ids on the host, and counts,
+weights and normalises on the GPU (ckv_tfidf_encode; the norm's summation order differs
+from BLAS, so vectors agree to a few ulp).  ``PrecomputedEncoder`` reads JSON lines.
+``search_texts`` goes from chunk/query texts to tiers and permutations with the embeddings
+never leaving the device.
 
 ``search_batched`` is the batched device form: B sequences x N chunks in one launch,
 returning scores, thresholds, tiers, the stable INT2||INT4||FP16 permutation and
@@ -62,6 +67,176 @@ class Embedding:
     def from_vector(cls, vector) -> "Embedding":
         v = np.asarray(vector, dtype=np.float64).reshape(-1)
         return cls(vector=v, norm=float(np.linalg.norm(v)))
+
+
+# -- encoders (retrieval.py:70-196) ---------------------------------------------------
+
+def _pack_texts(texts):
+    """UTF-8 bytes of all texts back to back + int64 offsets [n + 1], on the device."""
+    bufs = [t.encode("utf-8") for t in texts]
+    offsets = np.zeros(len(bufs) + 1, dtype=np.int64)
+    np.cumsum([len(b) for b in bufs], out=offsets[1:])
+    data = b"".join(bufs) or b"\0"
+    dev = _lib.device()
+    text = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
+    return text, torch.from_numpy(offsets).to(dev)
+
+
+class HashedBowEncoder:
+    """retrieval.py:70-100: order-free hashed bag of words with a hash-derived sign, L2
+    normalised, keyed BLAKE2b (key = the seed's decimal digits), on the GPU."""
+
+    def __init__(self, dim=256, seed=0):
+        if dim < 1:
+            raise ValueError("dim must be >= 1")
+        self.dim = dim
+        self._key = str(int(seed)).encode("ascii")
+
+    def fit(self, texts):
+        pass  # stateless
+
+    def encode_batch_dev(self, texts, out=None, norms=None):
+        """All texts in one launch -> (vectors f64 [n, dim], norms f64 [n]) on the GPU."""
+        texts = list(texts)
+        dev = _lib.device()
+        n = len(texts)
+        if out is None:
+            out = torch.empty((n, self.dim), dtype=torch.float64, device=dev)
+        if norms is None:
+            norms = torch.empty(n, dtype=torch.float64, device=dev)
+        if n:
+            text, offsets = _pack_texts(texts)
+            _lib.call("ckv_bow_encode", _lib.ptr(text), _lib.ptr(offsets), n, self.dim, self._key,
+                      len(self._key), _lib.ptr(out), _lib.ptr(norms), _lib.stream())
+        return out, norms
+
+    def encode(self, text) -> Embedding:
+        v, n = self.encode_batch_dev([text])
+        return Embedding(vector=v[0].cpu().numpy(), norm=float(n[0].item()))
+
+
+class TfidfEncoder:
+    """retrieval.py:103-138: TF-IDF over the texts of one run; sorted vocabulary, smoothed
+    idf ln((1 + n_docs) / (1 + df)) + 1.  fit() on the host (the reference's algorithm);
+    counting, weighting and normalisation on the GPU."""
+
+    def __init__(self):
+        self._index = None
+        self._idf = None
+        self._idf_dev = None
+
+    def fit(self, texts):
+        texts = list(texts)
+        vocab = sorted({w for t in texts for w in t.split()})
+        self._index = {w: i for i, w in enumerate(vocab)}
+        df = np.zeros(len(vocab), dtype=np.float64)
+        for t in texts:
+            for w in set(t.split()):
+                df[self._index[w]] += 1.0
+        self._idf = np.log((1.0 + len(texts)) / (1.0 + df)) + 1.0
+        self._idf_dev = None
+
+    @property
+    def dim(self):
+        return len(self._index) if self._index is not None else 0
+
+    def encode_batch_dev(self, texts, out=None, norms=None):
+        if self._index is None:
+            raise RuntimeError("TfidfEncoder.encode called before fit")
+        texts = list(texts)
+        dev = _lib.device()
+        if self._idf_dev is None:
+            self._idf_dev = kernels.to_dev(self._idf, torch.float64)
+        get = self._index.get
+        ids = [[i for i in map(get, t.split()) if i is not None] for t in texts]
+        offsets = np.zeros(len(ids) + 1, dtype=np.int64)
+        np.cumsum([len(x) for x in ids], out=offsets[1:])
+        flat = np.fromiter((i for x in ids for i in x), dtype=np.int32, count=int(offsets[-1]))
+        n, dim = len(texts), max(self.dim, 1)
+        if out is None:
+            out = torch.empty((n, dim), dtype=torch.float64, device=dev)
+        if norms is None:
+            norms = torch.empty(n, dtype=torch.float64, device=dev)
+        if n:
+            ids_d = kernels.to_dev(flat if flat.size else np.zeros(1, np.int32), torch.int32)
+            _lib.call("ckv_tfidf_encode", _lib.ptr(ids_d), _lib.ptr(kernels.to_dev(offsets, torch.int64)), n,
+                      _lib.ptr(self._idf_dev), self.dim, out.stride(0), _lib.ptr(out), _lib.ptr(norms),
+                      _lib.stream())
+        return out, norms
+
+    def encode(self, text) -> Embedding:
+        v, n = self.encode_batch_dev([text])
+        return Embedding(vector=v[0, :self.dim].cpu().numpy(), norm=float(n[0].item()))
+
+
+class PrecomputedEncoder:
+    """retrieval.py:141-181: vectors injected from a JSON-lines file of {"id", "vector"}."""
+
+    def __init__(self, path):
+        import json
+
+        self.path = path
+        self._vectors = {}
+        dim = None
+        with open(path, "r", encoding="utf-8") as fh:
+            for lineno, line in enumerate(fh, start=1):
+                if not line.strip():
+                    continue
+                try:
+                    record = json.loads(line)
+                    key = record["id"]
+                    vec = np.asarray(record["vector"], dtype=np.float64).reshape(-1)
+                except (json.JSONDecodeError, KeyError, TypeError, ValueError) as exc:
+                    raise ValueError(f"{path}:{lineno}: bad embedding record: {exc}") from exc
+                if dim is None:
+                    dim = vec.shape[0]
+                elif vec.shape[0] != dim:
+                    raise ValueError(f"{path}:{lineno}: vector dimension {vec.shape[0]} != {dim}")
+                if key in self._vectors:
+                    raise ValueError(f"{path}:{lineno}: duplicate id {key!r}")
+                self._vectors[key] = vec
+        if not self._vectors:
+            raise ValueError(f"{path}: no embedding records")
+        self.dim = dim
+
+    def fit(self, texts):
+        pass  # vectors are fixed
+
+    def encode(self, key) -> Embedding:
+        try:
+            vec = self._vectors[key]
+        except KeyError:
+            raise KeyError(f"no precomputed embedding for id {key!r} in {self.path}") from None
+        return Embedding.from_vector(vec)
+
+    def encode_batch_dev(self, keys, out=None, norms=None):
+        embs = [self.encode(k) for k in keys]
+        dev = _lib.device()
+        v = kernels.to_dev(np.stack([e.vector for e in embs]) if embs else np.zeros((0, self.dim)), torch.float64)
+        nm = kernels.to_dev(np.array([e.norm for e in embs], np.float64), torch.float64)
+        if out is not None:
+            out.copy_(v)
+            v = out
+        if norms is not None:
+            norms.copy_(nm)
+            nm = norms
+        return v.to(dev), nm.to(dev)
+
+
+def make_encoder(spec, seed=0):
+    """retrieval.py:184-192: bow, tfidf, or file:PATH."""
+    if spec == "bow":
+        return HashedBowEncoder(seed=seed)
+    if spec == "tfidf":
+        return TfidfEncoder()
+    if spec.startswith("file:"):
+        return PrecomputedEncoder(spec[len("file:"):])
+    raise ValueError(f"unknown encoder {spec!r} (expected bow, tfidf, or file:PATH)")
+
+
+def encode(text, encoder) -> Embedding:
+    """retrieval.py:195-196."""
+    return encoder.encode(text)
 
 
 @dataclass
@@ -122,6 +297,32 @@ def search_batched(emb, emb_norm, q, q_norm, alpha=0.6, beta=0.1, seq_chunks=Non
     if check:
         res.raise_on_error()
     return res
+
+
+def search_texts(chunk_texts, query_texts, alpha=0.6, beta=0.1, encoder=None, fit=True,
+                 check=True) -> SearchResult:
+    """Texts to tiers for B sequences: ``chunk_texts`` a list (per sequence) of chunk strings,
+    ``query_texts`` one string per sequence.  All chunks and queries are encoded in one launch
+    (default ``HashedBowEncoder()``) into a [B, N_max, dim] embedding block that ckv_search
+    reads in place (ragged sequences: padded rows are empty texts, excluded via seq_chunks).
+    ``fit`` calls ``encoder.fit`` on every chunk and query text first, as the harness does
+    (harness.py:181-190; a no-op for bow)."""
+    encoder = HashedBowEncoder() if encoder is None else encoder
+    chunk_texts = [list(c) for c in chunk_texts]
+    query_texts = list(query_texts)
+    B = len(chunk_texts)
+    if B != len(query_texts):
+        raise ValueError("one query text per sequence")
+    n = [len(c) for c in chunk_texts]
+    N = max(n) if n else 0
+    if fit:
+        encoder.fit([t for c in chunk_texts for t in c] + query_texts)
+    flat = [t for c in chunk_texts for t in c + [""] * (N - len(c))] + query_texts
+    vec, norms = encoder.encode_batch_dev(flat)
+    d = vec.shape[1]
+    emb, emb_norm = vec[:B * N].view(B, N, d), norms[:B * N].view(B, N)
+    return search_batched(emb, emb_norm, vec[B * N:], norms[B * N:], alpha, beta,
+                          np.array(n, np.int32), check)
 
 
 def tiers_from_scores_batched(scores, alpha, beta, check=True) -> SearchResult:

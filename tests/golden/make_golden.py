@@ -25,8 +25,8 @@ from chunkkv.harness import RunConfig, synth_workload  # noqa: E402
 from chunkkv.attention import prefill_attention  # noqa: E402
 from chunkkv.kv_store import build_cache, reconstruct, serialize_cache  # noqa: E402
 from chunkkv.toy_model import ToyModel, generate  # noqa: E402
-from chunkkv.retrieval import (HashedBowEncoder, build_similarity_report, score_chunks,  # noqa: E402
-                               segment_context)
+from chunkkv.retrieval import (HashedBowEncoder, TfidfEncoder, build_similarity_report,  # noqa: E402
+                               score_chunks, segment_context)
 from chunkkv.tiers import Tier  # noqa: E402
 
 TIER_CODE = {Tier.INT2: 0, Tier.INT4: 1, Tier.FP16: 2}
@@ -232,6 +232,62 @@ def toy_cases():
     return out
 
 
+def _blob(texts):
+    bufs = [t.encode("utf-8") for t in texts]
+    off = np.zeros(len(bufs) + 1, np.int64)
+    np.cumsum([len(b) for b in bufs], out=off[1:])
+    return np.frombuffer(b"".join(bufs) or b"\0", np.uint8).copy(), off
+
+
+def encoder_cases():
+    """HashedBowEncoder / TfidfEncoder on edge-case texts (every str.isspace() separator,
+    non-ASCII words, words longer than one 128-byte BLAKE2b block, empty and blank texts, a
+    cancelling pair) and on synthetic workloads' chunk texts with their search results."""
+    spaces = [c for c in map(chr, range(0x110000)) if c.isspace()]
+    rng = np.random.default_rng(31)
+    texts = ["", "   ", "\t\n\x0b\x0c\r\x1c", "word", "a b c a", "x" * 128, "y" * 129, "z" * 300 + " q",
+             "caf\u00e9 \u4e2d\u6587 \U0001f600 na\u00efve", "a\u00a0b", "\u00a0lead trail\u3000",
+             "\u0085\u0085x\u2028y\u2029z"]
+    for c in spaces:
+        texts.append(f"alpha{c}beta{c}{c}gamma")
+    # a word pair landing in the same dim-256 bucket with opposite signs: the bucket cancels
+    enc = HashedBowEncoder(seed=0)
+    import hashlib
+    seen = {}
+    for i in range(100000):
+        w = f"w{i}"
+        h = int.from_bytes(hashlib.blake2b(w.encode(), key=b"0", digest_size=8).digest(), "little")
+        b, sgn = h % 256, h >> 63
+        if (b, 1 - sgn) in seen:
+            texts.append(f"{seen[(b, 1 - sgn)]} {w}")
+            break
+        seen[(b, sgn)] = w
+    for _ in range(40):
+        n = int(rng.integers(1, 60))
+        texts.append(" ".join(f"w{int(x):05d}" for x in rng.integers(0, 3000, size=n)))
+    out = {"spaces": np.array([ord(c) for c in spaces], np.int64)}
+    out["text"], out["offsets"] = _blob(texts)
+    for seed in (0, 7, 123456789):
+        for dim in (256, 100, 1, 4096):
+            enc = HashedBowEncoder(dim=dim, seed=seed)
+            embs = [enc.encode(t) for t in texts]
+            out[f"bow_{seed}_{dim}"] = np.stack([e.vector for e in embs])
+            out[f"bow_norm_{seed}_{dim}"] = np.array([e.norm for e in embs])
+    tf = TfidfEncoder()
+    tf.fit(texts)
+    embs = [tf.encode(t) for t in texts]
+    out["tfidf"] = np.stack([e.vector for e in embs])
+    out["tfidf_norm"] = np.array([e.norm for e in embs])
+    # texts -> tiers: the synthetic workloads of search.npz (4K, seeds 0-3) as texts
+    for s in (0, 1, 2, 3):
+        cfg = RunConfig(context_len=4096, seed=s)
+        words, query = synth_workload(cfg)
+        cs = segment_context(words, cfg.chunk_size)
+        chunk_texts = [" ".join(c) for c in cs.chunks]
+        out[f"wl_text{s}"], out[f"wl_offsets{s}"] = _blob(chunk_texts + [" ".join(query)])
+    return out
+
+
 def main():
     assert rk.BACKEND in ("numpy", "compiled")
     np.savez_compressed(os.path.join(HERE, "quantize.npz"), **quantize_cases())
@@ -240,6 +296,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "attention.npz"), **attention_cases())
     np.savez_compressed(os.path.join(HERE, "batched.npz"), **batched_case())
     np.savez_compressed(os.path.join(HERE, "toy.npz"), **toy_cases())
+    np.savez_compressed(os.path.join(HERE, "encoders.npz"), **encoder_cases())
     print("reference backend:", rk.BACKEND, "chunkkv", chunkkv.__version__, file=sys.stderr)
 
 
