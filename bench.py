@@ -287,6 +287,7 @@ def bench_prefill(torch, dev, steps=3, profile=False):
     ach = (read + write) / tb / 1e9
     del k, v, cache
     torch.cuda.empty_cache()
+    text = bench_text_search(torch, T // 32)
     return {
         "workload": "cfg5: prefill search + reorder/quantize/pack, 128K ctx x 32 layers x 8 kv heads, b1",
         "tier_fractions": [round(x / (n2 + n4 + nf), 4) for x in (n2, n4, nf)],
@@ -297,7 +298,42 @@ def bench_prefill(torch, dev, steps=3, profile=False):
         "bytes_read": read, "bytes_written": write,
         "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(ach / peak, 4), "traffic": profile_traffic("reorder_quantize_pack")},
+        "text_search": text,
     }
+
+
+def bench_text_search(torch, n_chunks, reps=5):
+    """Texts -> tiers for one 128K context (n_chunks chunk texts of 32 synthetic words + a
+    64-word query): the public search_texts call (UTF-8 packing, host-to-device copy, GPU
+    hashed-BoW encode, search), wall clock with a device sync, beside the CPU restatement of
+    the reference's per-text encoder on a sample of the same texts (extrapolated)."""
+    from paper_2503_23294_b200 import retrieval
+
+    rng = np.random.default_rng(5)
+    words = rng.integers(0, 4096, size=(n_chunks, 32))
+    chunks = [" ".join(f"w{int(x):05d}" for x in row) for row in words]
+    query = " ".join(f"w{int(x):05d}" for x in rng.integers(0, 1024, size=64))
+    enc = retrieval.HashedBowEncoder(seed=0)
+    times = []
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = retrieval.search_texts([chunks], [query], 0.6, 0.1, enc, check=False)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    gpu_ms = statistics.median(times[1:]) * 1e3
+    from oracle import ckv_oracle as O  # CPU baseline leg only
+
+    sample = chunks[:512]
+    t0 = time.perf_counter()
+    for t in sample:
+        O.bow_encode(t, 256, 0)
+    cpu_ms = (time.perf_counter() - t0) * 1e3 * (n_chunks + 1) / len(sample)
+    del r
+    return {"chunks": n_chunks, "gpu_ms": round(gpu_ms, 3), "cpu_encode_ms": round(cpu_ms, 1),
+            "note": "gpu_ms: search_texts from host strings to device tiers (encode + search); "
+                    "cpu_encode_ms: the oracle port of HashedBowEncoder.encode (hashlib, 1 core) on "
+                    "512 of the texts, scaled to all of them (encoding only)"}
 
 
 def run_cfg3(args, torch, dist, dev, rank, world, local):
