@@ -70,6 +70,26 @@ __device__ __noinline__ uint32_t exact_slice(uint32_t w0, uint32_t w1, uint32_t 
 //   acc += bits(y) * base^e        [one IMAD; the constant offset is pre-subtracted]
 // The fp32 value of r is within 3.6e-6 of the exact rational, so away from the guard band
 // round-half-even(r) == floor(exact + 0.5) == the reference's f64 result.
+// packed fp32x2 arithmetic (sm_100: FADD2 / FFMA2, two lanes of f32 per instruction)
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 template <int BITS>
 __device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float& lo_out, float& hi_out,
                                                    bool& bad, bool& wide) {
@@ -99,18 +119,25 @@ __device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float
   const float qinv = qmax * rs;
   uint32_t acc = 0u - kM * kSum;
   float dmax = 0.0f;  // max |r - round(r)| over the slice
+  // element pairs in packed f32x2 arithmetic (FADD2 / FFMA2: half the issue slots):
+  //   d = x - lo;  y = RN(d qinv + 1.5 2^23) (the code lands in y's low mantissa bits);
+  //   e = d qinv - (y - 1.5 2^23) (one rounding)
+  const uint64_t nlo = f2pack(-lo, -lo), qi = f2pack(qinv, qinv), mm = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t neg1 = f2pack(-1.0f, -1.0f);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const uint32_t hb = (w[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-    float d;
-    asm("{.reg .f16 xh; mov.b16 xh, %1; sub.rn.f32.f16 %0, xh, %2;}" : "=f"(d) : "h"((unsigned short)hb), "f"(lo));
-    const float r = d * qinv;
-    const float y = r + 12582912.0f;
-    dmax = fmaxf(dmax, fabsf(r - (y - 12582912.0f)));
-    uint32_t p = 1u;
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __half22float2(u32_as_h2(w[i]));
+    const uint64_t d = fadd2(f2pack(x.x, x.y), nlo);
+    const uint64_t y = ffma2(d, qi, mm);
+    const uint64_t e = ffma2(d, qi, ffma2(y, neg1, mm));
+    float e0, e1, y0, y1;
+    f2unpack(e, e0, e1);
+    f2unpack(y, y0, y1);
+    dmax = fmaxf(dmax, fmaxf(fabsf(e0), fabsf(e1)));
+    uint32_t p0 = 1u;
 #pragma unroll
-    for (int k = 0; k < e; ++k) p *= base;
-    acc += __float_as_uint(y) * p;
+    for (int k = 0; k < 2 * i; ++k) p0 *= base;
+    acc += __float_as_uint(y0) * p0 + __float_as_uint(y1) * (p0 * base);
   }
   const bool near = dmax > 0.5f - (1.0f / 16384.0f);
   if (near) acc = exact_slice(w[0], w[1], w[2], w[3], lo, hi, qinv, qmax, base);  // rare
