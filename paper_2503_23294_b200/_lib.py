@@ -15,7 +15,7 @@ import re
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libckv.so")
+LIB_PATH = os.environ.get("CKV_LIB_PATH") or os.path.join(_HERE, "_lib", "libckv.so")  # override: A/B builds (tuning aid)
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "ckv.h")
 
 CKV_OK = 0

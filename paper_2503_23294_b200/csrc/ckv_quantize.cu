@@ -221,7 +221,7 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
 
 // One warp per (layer, sequence, kv-head, destination chunk slot).  Slot p < N takes source
 // chunk perm[p]; slot p == N is the context tail (if any).
-__global__ void __launch_bounds__(kQWarps * 32, 6)
+__global__ void __launch_bounds__(kQWarps * 32, 8)
 reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
                              int H, int B, int64_t sL, int64_t sB, int64_t sT, int64_t sH,
                              const uint32_t* __restrict__ perm, int max_chunks,
