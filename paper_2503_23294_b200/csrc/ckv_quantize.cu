@@ -70,6 +70,22 @@ __device__ __noinline__ uint32_t exact_slice(uint32_t w0, uint32_t w1, uint32_t 
 //   acc += bits(y) * base^e        [one IMAD; the constant offset is pre-subtracted]
 // The fp32 value of r is within 3.6e-6 of the exact rational, so away from the guard band
 // round-half-even(r) == floor(exact + 0.5) == the reference's f64 result.
+__device__ __forceinline__ uint32_t hmin2_nan(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("min.NaN.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hmax2_nan(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.NaN.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t prmt_q(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
 // packed fp32x2 arithmetic (sm_100: FADD2 / FFMA2, two lanes of f32 per instruction)
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
   uint64_t r;
@@ -97,20 +113,20 @@ __device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float
   constexpr uint32_t base = BITS == 2 ? 4u : 16u;
   constexpr uint32_t kM = 0x4B400000u;  // bits of 1.5 * 2^23
   constexpr uint32_t kSum = BITS == 2 ? 21845u : 0x11111111u;  // sum_e base^e, e = 0..7
-  // group min / max in fp16 with NaN propagation; (lo, -hi) travel as one half2
-  const __half2 h0 = u32_as_h2(w[0]), h1 = u32_as_h2(w[1]), h2 = u32_as_h2(w[2]), h3 = u32_as_h2(w[3]);
-  const __half2 mn = __hmin2_nan(__hmin2_nan(h0, h1), __hmin2_nan(h2, h3));
-  const __half2 mx = __hmax2_nan(__hmax2_nan(h0, h1), __hmax2_nan(h2, h3));
-  __half2 lh = __halves2half2(__hmin_nan(__low2half(mn), __high2half(mn)),
-                              __hneg(__hmax_nan(__low2half(mx), __high2half(mx))));
-  lh = __hmin2_nan(lh, u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(lh), 1)));
-  lh = __hmin2_nan(lh, u32_as_h2(__shfl_xor_sync(0xffffffffu, h2_as_u32(lh), 2)));
-  const float lo = __low2float(lh), hi = -__high2float(lh);
+  // group min / max in fp16 with NaN propagation; (lo, -hi) travel as one half2 so that one
+  // min per butterfly step reduces both over the group's 4 lanes
+  const uint32_t mn = hmin2_nan(hmin2_nan(w[0], w[1]), hmin2_nan(w[2], w[3]));
+  const uint32_t nmx = hmax2_nan(hmax2_nan(w[0], w[1]), hmax2_nan(w[2], w[3])) ^ 0x80008000u;
+  uint32_t lh = hmin2_nan(prmt_q(mn, nmx, 0x5410), prmt_q(mn, nmx, 0x7632));
+  lh = hmin2_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 1));
+  lh = hmin2_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 2));
+  const float2 lhf = __half22float2(u32_as_h2(lh));
+  const float lo = lhf.x, hi = -lhf.y;
   lo_out = lo;
   hi_out = hi;
   const float span = hi - lo;
-  bad |= !(isfinite(lo) && isfinite(hi));  // any inf / nan in the group reaches lo or hi
-  wide |= span * (1.0f / qmax) > 4000.0f;
+  bad |= !(span < INFINITY);  // an inf / nan anywhere in the group makes the span inf or nan
+  wide |= span > 4000.0f * qmax;
   if (!(span > 0.0f)) return 0u;  // constant group: codes 0 (also nan groups; flagged above)
   // qmax / span via the approximate reciprocal (<= 2 ulp): the candidate r below stays within
   // 2^-17 of the exact rational, well inside the 2^-14 guard band that triggers the exact path
