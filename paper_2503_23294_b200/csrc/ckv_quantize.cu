@@ -235,6 +235,27 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
   return wide;
 }
 
+struct QTask {
+  int tier, rows, src_tok0, dst_row0;
+};
+__device__ __forceinline__ QTask read_task(uint32_t addr) {
+  QTask t;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(t.tier), "=r"(t.rows), "=r"(t.src_tok0), "=r"(t.dst_row0) : "r"(addr));
+  return t;
+}
+struct CtaPos {
+  int l, b, h;
+};
+// (layer, sequence, kv-head) of this CTA from the special registers (volatile: re-read where
+// used instead of occupying registers across the loops)
+__device__ __forceinline__ CtaPos cta_pos(int B) {
+  uint32_t y, z;
+  asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(y));
+  asm volatile("mov.u32 %0, %%ctaid.z;" : "=r"(z));
+  return CtaPos{(int)z / B, (int)z % B, (int)y};
+}
+
 // One warp per (layer, sequence, kv-head, destination chunk slot).  Slot p < N takes source
 // chunk perm[p]; slot p == N is the context tail (if any).
 __global__ void __launch_bounds__(kQWarps * 32, 8)
@@ -246,40 +267,51 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
   // staging of one packed chunk: its 2 interleaved K/V tile blocks (ckv_common.cuh), written
   // by the K pass and the V pass, then stored as one contiguous 3 KB / 5 KB run
   __shared__ __align__(16) unsigned char s_blk[kQWarps][2 * kBlock4];
+  // the warp's task (tier, rows, first source token, first destination row), re-read from
+  // shared memory where used: kept in registers across the quantize loops these would be
+  // spilled to local memory at 64 registers
+  __shared__ __align__(16) int s_task[kQWarps][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * kQWarps + warp;
-  const int h = blockIdx.y;
-  const int l = blockIdx.z / B, b = blockIdx.z % B;
-  const SeqRow sr = load_seq(seq, b);
-  const int N = sr.ctx / kChunk;
-  const int tail = sr.ctx - N * kChunk;
-  if (p > N || (p == N && tail == 0)) return;
-  const int n2 = sr.len2 / kChunk, n4 = sr.len4 / kChunk;
-  int tier, rows, src_tok0, dst_row0;
-  if (p < N) {
-    const int src = (int)perm[(int64_t)b * max_chunks + p];
-    src_tok0 = src * kChunk;
-    rows = kChunk;
-    if (p < n2) { tier = 0; dst_row0 = sr.off2 + p * kChunk; }
-    else if (p < n2 + n4) { tier = 1; dst_row0 = sr.off4 + (p - n2) * kChunk; }
-    else { tier = 2; dst_row0 = sr.off_fp + (p - n2 - n4) * kChunk; }
-  } else {
-    tier = 2; rows = tail; src_tok0 = sr.tail_src;
-    dst_row0 = sr.off_fp + (N - n2 - n4) * kChunk;
+  {
+    const int p = blockIdx.x * kQWarps + warp;
+    const int b = blockIdx.z % B;
+    const SeqRow sr = load_seq(seq, b);
+    const int N = sr.ctx / kChunk;
+    const int tail = sr.ctx - N * kChunk;
+    if (p > N || (p == N && tail == 0)) return;
+    const int n2 = sr.len2 / kChunk, n4 = sr.len4 / kChunk;
+    int tier, rows, src_tok0, dst_row0;
+    if (p < N) {
+      const int src = (int)perm[(int64_t)b * max_chunks + p];
+      src_tok0 = src * kChunk;
+      rows = kChunk;
+      if (p < n2) { tier = 0; dst_row0 = sr.off2 + p * kChunk; }
+      else if (p < n2 + n4) { tier = 1; dst_row0 = sr.off4 + (p - n2) * kChunk; }
+      else { tier = 2; dst_row0 = sr.off_fp + (p - n2 - n4) * kChunk; }
+    } else {
+      tier = 2; rows = tail; src_tok0 = sr.tail_src;
+      dst_row0 = sr.off_fp + (N - n2 - n4) * kChunk;
+    }
+    if (lane == 0) *reinterpret_cast<int4*>(s_task[warp]) = make_int4(tier, rows, src_tok0, dst_row0);
+    __syncwarp();
   }
+  const uint32_t task_addr = (uint32_t)__cvta_generic_to_shared(s_task[warp]);
   const int sub = lane >> 4, j = lane & 15;  // 2 rows per warp step, 8 fp16 per lane
   bool bad = false;
-  const int64_t unit = (int64_t)l * H + h;
 #pragma unroll 1
   for (int tsel = 0; tsel < 2; ++tsel) {
-    const uint16_t* src = (tsel ? v : k) + l * sL + b * sB + h * sH + (int64_t)src_tok0 * sT;
-    const ckv_arena& A = tsel ? VA : KA;
-    if (tier == 2) {
-      uint16_t* dst = A.fp + (unit * A.rows_fp + dst_row0) * kHeadDim;
+    const QTask t = read_task(task_addr);
+    const CtaPos c = cta_pos(B);
+    const int64_t unit = (int64_t)c.l * H + c.h;
+    const uint16_t* src = (tsel ? v : k) + c.l * sL + c.b * sB + c.h * sH + (int64_t)t.src_tok0 * sT;
+    if (t.tier == 2) {
+      // arena fields by explicit selects (a reference to either parameter struct would put
+      // both in local memory)
+      uint16_t* dst = (tsel ? VA.fp : KA.fp) + (unit * (tsel ? VA.rows_fp : KA.rows_fp) + t.dst_row0) * kHeadDim;
 #pragma unroll 4
       for (int rr = 0; rr < 16; ++rr) {
         const int r = 2 * rr + sub;
-        if (r < rows) {
+        if (r < t.rows) {
           const uint4 x = __ldg(reinterpret_cast<const uint4*>(src + r * sT) + j);
           const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -290,29 +322,34 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       }
       continue;
     }
-    const int code_bytes = tier == 0 ? kTileBytes2 : kTileBytes4;
+    const int code_bytes = t.tier == 0 ? kTileBytes2 : kTileBytes4;
     unsigned char* sc = s_blk[warp] + (tsel ? code_bytes : 0);
     unsigned char* sm = s_blk[warp] + 2 * code_bytes + (tsel ? kTileBytesMeta : 0);
     bool wide;
     float smax = 0.0f;  // largest group span of the chunk (decode precision routing)
-    if (tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, sub, j, sc, sm, bad, smax)
-                               : quantize_chunk<2, false>(src, sT, sub, j, sc, sm, bad, smax);
+    if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, sub, j, sc, sm, bad, smax)
+                                 : quantize_chunk<2, false>(src, sT, sub, j, sc, sm, bad, smax);
     else wide = tsel ? quantize_chunk<4, true>(src, sT, sub, j, sc, sm, bad, smax)
                      : quantize_chunk<4, false>(src, sT, sub, j, sc, sm, bad, smax);
     __syncwarp();
+    const QTask t2 = read_task(task_addr);
+    const CtaPos c2 = cta_pos(B);
+    const int64_t unit2 = (int64_t)c2.l * H + c2.h;
     if (tsel) {  // both halves staged: 128-bit coalesced stores of the 2 contiguous blocks
-      const int64_t blk = tier == 0 ? kBlock2 : kBlock4;
-      const int64_t tile0 = (unit * (tier == 0 ? KA.rows2 : KA.rows4) + dst_row0) / kTileRows;
-      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(tier == 0 ? KA.codes2 : KA.codes4) + tile0 * blk);
+      const int64_t blk = t2.tier == 0 ? kBlock2 : kBlock4;
+      const int64_t tile0 = (unit2 * (t2.tier == 0 ? KA.rows2 : KA.rows4) + t2.dst_row0) / kTileRows;
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(t2.tier == 0 ? KA.codes2 : KA.codes4) + tile0 * blk);
       const int n16 = (int)(2 * blk / 16);
       for (int i = lane; i < n16; i += 32) dst[i] = reinterpret_cast<const uint4*>(s_blk[warp])[i];
     }
-    if (__any_sync(0xffffffffu, wide) && lane == 0 && A.span_flags)
-      atomicOr(A.span_flags + unit * B + b, tier == 0 ? 1u : 2u);
+    uint32_t* span_flags = tsel ? VA.span_flags : KA.span_flags;
+    uint32_t* span_max = tsel ? VA.span_max : KA.span_max;
+    if (__any_sync(0xffffffffu, wide) && lane == 0 && span_flags)
+      atomicOr(span_flags + unit2 * B + c2.b, t2.tier == 0 ? 1u : 2u);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
-    if (lane == 0 && A.span_max)  // non-negative floats order like their bit patterns
-      atomicMax(A.span_max + unit * B + b, __float_as_uint(smax));
+    if (lane == 0 && span_max)  // non-negative floats order like their bit patterns
+      atomicMax(span_max + unit2 * B + c2.b, __float_as_uint(smax));
     __syncwarp();
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE);
