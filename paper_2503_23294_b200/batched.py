@@ -219,12 +219,16 @@ class BatchedKVCache:
                   _lib.DECODE_PDL if pdl else 0, _lib.stream())
         return out
 
-    def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=8):
+    def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=16, order_current=True):
         """One decode step for all layers from HOST buffers: pinned fp16 q [L, B, H*m, 128] ->
-        pinned fp16 output of the same shape.  The q upload runs on a copy stream, layer 0
-        waits only for its own slice; the outputs go back every `d2h_every` layers while the
-        next layers compute; per-layer decode launches stay PDL-chained.  Device staging is
-        double-buffered across steps, so consecutive steps never wait on each other's copies."""
+        pinned fp16 output of the same shape.  The q upload runs on its own copy stream (it
+        overlaps the previous step's last layers), layer 0 waits only for its own slice; the
+        outputs go back on a second copy stream every `d2h_every` layers while the next layers
+        compute; per-layer decode launches stay PDL-chained between those points.  Device
+        staging is double-buffered across steps, so consecutive steps never wait on each
+        other's copies.  With ``order_current`` the current stream is ordered after the last
+        download on return; without it the downloads stay on the copy stream (they overlap the
+        next step's layers) and ``self.host_step_ready`` is the event that completes them."""
         L, B, Hq, D = q_host.shape
         if (L, B) != (self.L, self.B) or D != HEAD_DIM or Hq % self.H or q_host.dtype != torch.float16:
             raise ValueError("q shape does not match the cache")
@@ -236,20 +240,24 @@ class BatchedKVCache:
             dev = self.device
             st = dict(key=key, q=[torch.empty(key, dtype=torch.float16, device=dev) for _ in range(2)],
                       o=[torch.empty(key, dtype=torch.float16, device=dev) for _ in range(2)],
-                      cs=torch.cuda.Stream(device=dev), i=0)
+                      cin=torch.cuda.Stream(device=dev), cout=torch.cuda.Stream(device=dev),
+                      q_free=[None, None], o_free=[None, None], i=0)
             self._host_step = st
         ms = torch.cuda.current_stream()
-        cs = st["cs"]
+        cin, cout = st["cin"], st["cout"]
         buf = st["i"] & 1
         st["i"] += 1
         qd, od = st["q"][buf], st["o"][buf]
-        cs.wait_stream(ms)  # staging buffer `buf` was last used two steps ago on ms
         ev_q0, ev_q = torch.cuda.Event(), torch.cuda.Event()
-        with torch.cuda.stream(cs):
+        with torch.cuda.stream(cin):
+            if st["q_free"][buf] is not None:  # the step two back has read this staging buffer
+                cin.wait_event(st["q_free"][buf])
             qd[0:1].copy_(q_host[0:1], non_blocking=True)
-            ev_q0.record(cs)
+            ev_q0.record(cin)
             qd[1:].copy_(q_host[1:], non_blocking=True)
-            ev_q.record(cs)
+            ev_q.record(cin)
+        if st["o_free"][buf] is not None:  # ... and its outputs have left this staging buffer
+            ms.wait_event(st["o_free"][buf])
         for l in range(L):
             if l == 0:
                 ms.wait_event(ev_q0)
@@ -260,10 +268,16 @@ class BatchedKVCache:
                 lo = (l // d2h_every) * d2h_every
                 ev = torch.cuda.Event()
                 ev.record(ms)
-                cs.wait_event(ev)
-                with torch.cuda.stream(cs):
+                cout.wait_event(ev)
+                with torch.cuda.stream(cout):
                     out_host[lo:l + 1].copy_(od[lo:l + 1], non_blocking=True)
-        ms.wait_stream(cs)
+        q_free, o_free = torch.cuda.Event(), torch.cuda.Event()
+        q_free.record(ms)
+        o_free.record(cout)
+        st["q_free"][buf], st["o_free"][buf] = q_free, o_free
+        self.host_step_ready = o_free
+        if order_current:
+            ms.wait_stream(cout)
         return out_host
 
     def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None):

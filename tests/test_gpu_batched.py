@@ -306,7 +306,9 @@ def test_decode_step_host_matches_device_decode():
     for step in range(3):
         q = torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16))
         oh = torch.empty(q.shape, dtype=torch.float16).pin_memory()
-        cache.decode_step_host(q.pin_memory(), oh, d2h_every=2)
+        cache.decode_step_host(q.pin_memory(), oh, d2h_every=2, order_current=step == 0)
+        if step:
+            cache.host_step_ready.synchronize()
         torch.cuda.synchronize()
         want = cache.decode(q.cuda()).cpu()
         assert torch.equal(oh, want), step
