@@ -45,6 +45,7 @@ PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
 CFG2 = dict(layers=32, batch=8, kv_heads=8, q_per_kv=4, context=32768, head_dim=128)
 CFG5 = dict(layers=32, batch=1, kv_heads=8, context=131072, head_dim=128)
 CFG3 = dict(layers=40, batch=1, kv_heads=40, q_per_kv=1, context=131072, head_dim=128)
+CFG4 = dict(layers=32, batch=64, kv_heads=8, q_per_kv=4, context=16384, head_dim=128)
 
 
 def load_workload(ctx, seed):
@@ -471,6 +472,114 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def run_cfg4(args, torch, dist, dev, rank, world, local):
+    """cfg4: batch 64 x 16K, Llama-3-8B GQA shape (32 layers, 8 kv heads, m = 4), the global
+    batch sharded over the ranks (64/N whole sequences per GPU, no data-path collective; strong
+    scaling of the fixed batch).  Tier maps (--cfg4-map): the reference's 16K maps (sequence
+    b: seed b % 8, "skewed"), all-INT2 or all-FP16 — SURVEY's bitwidth-mix sweep.  The cache is
+    built one layer at a time (the fp16 source of one layer is 4.3 GB)."""
+    from paper_2503_23294_b200 import batched, distributed, retrieval
+
+    c = CFG4
+    L, Bg, H, m, T, D = c["layers"], c["batch"], c["kv_heads"], c["q_per_kv"], c["context"], c["head_dim"]
+    lo, hi = distributed.batch_shard(Bg, world, rank)
+    B = hi - lo
+    n = T // 32
+    if args.cfg4_map == "skewed":
+        maps = np.stack([load_workload(T, b % 8)["tiers"] for b in range(lo, hi)])
+    else:
+        maps = np.full((B, n), 2 if args.cfg4_map == "all_fp16" else 0, np.uint8)
+    search = retrieval.assign_tiers_batched(maps.astype(np.float64), np.tile([[0.5, 1.5]], (B, 1)))
+    if not np.array_equal(search.tiers.cpu().numpy(), maps):
+        raise SystemExit("cfg4 tier maps not reproduced")
+    counts = search.seg_counts.cpu().numpy()
+    cache = batched.BatchedKVCache(L, B, H, counts[:, 0], counts[:, 1], counts[:, 2], [T] * B, 128, device=dev)
+    g = torch.Generator(device=dev)
+    for l in range(L):
+        g.manual_seed(7000 + 100 * rank + l)
+        k = torch.randn((1, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+        v = torch.randn((1, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+        cache.build(k, v, search.perm, layer=l)
+        del k, v
+    torch.cuda.empty_cache()
+    g.manual_seed(11 + rank)
+    q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
+    out = torch.empty_like(q)
+    splits = args.splits or cache.default_splits(m, 1)
+    my_bytes = cache.algorithmic_bytes(m)
+
+    def step():
+        for l in range(L):
+            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
+
+    def sync_max(ms):
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    ms = sync_max(e0.elapsed_time(e1) / args.steps)
+    qh = q.cpu().pin_memory()
+    oh = torch.empty(q.shape, dtype=torch.float16, pin_memory=True)
+    for _ in range(3):
+        cache.decode_step_host(qh, oh, splits=splits, order_current=False)
+    torch.cuda.synchronize()
+    barrier()
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record()
+    for _ in range(args.steps):
+        cache.decode_step_host(qh, oh, splits=splits, order_current=False)
+    torch.cuda.current_stream().wait_event(cache.host_step_ready)
+    e5.record()
+    torch.cuda.synchronize()
+    e2e_ms = sync_max(e4.elapsed_time(e5) / args.steps)
+    tot = torch.tensor([float(my_bytes)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tot)
+    step_bytes = float(tot.item())
+    if rank == 0:
+        peak, peak_kind = measured_peak_gbs()
+        frac = counts.sum(axis=0) / counts.sum()
+        line = {
+            "metric": METRIC, "value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
+            "data": f"synthetic (fp16 N(0,1) K/V/q; tier maps: {args.cfg4_map})",
+            "config": {"workload": f"cfg4: batch 64 x 16K, Llama-3-8B GQA 32q/8kv d128, 32 layers, map {args.cfg4_map}",
+                       "global_batch": Bg, "seq_len": T, "parallelism": f"batch-shard x{world}",
+                       "tier_fractions_int2_int4_fp16": [round(float(x), 4) for x in frac],
+                       "launch": "per-layer (32 launches per step)", "splits": splits,
+                       "l2": "inputs larger than L2"},
+            "tokens_per_s": round(Bg / (ms * 1e-3), 1),
+            "algorithmic_bytes_per_step": int(step_bytes),
+            "roofline": {"bound": "hbm", "achieved": round(my_bytes / (ms * 1e-3) / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(my_bytes / (ms * 1e-3) / 1e9 / peak, 4),
+                         "peak_kind": peak_kind, "traffic": None},
+            "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(q.numel() * 2)},
+            "gpu_launches": args.steps * L,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -480,9 +589,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--splits", type=int, default=None)
-    ap.add_argument("--workload", choices=["cfg2", "cfg3"], default="cfg2",
+    ap.add_argument("--workload", choices=["cfg2", "cfg3", "cfg4"], default="cfg2",
                     help="cfg2: batch-sharded 32K GQA decode (default); cfg3: 128K MHA decode with "
-                         "sequence split-KV across the ranks (NCCL all-gather + LSE merge)")
+                         "sequence split-KV across the ranks (NCCL all-gather + LSE merge); cfg4: "
+                         "batch 64 x 16K GQA decode sharded over the ranks (--cfg4-map)")
+    ap.add_argument("--cfg4-map", choices=["skewed", "all_int2", "all_fp16"], default="skewed")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -505,8 +616,8 @@ def main():
         if world > 1:
             dist.barrier()
 
-    if args.workload == "cfg3":
-        run_cfg3(args, torch, dist, dev, rank, world, local)
+    if args.workload in ("cfg3", "cfg4"):
+        (run_cfg3 if args.workload == "cfg3" else run_cfg4)(args, torch, dist, dev, rank, world, local)
         if world > 1:
             dist.destroy_process_group()
         return
