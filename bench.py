@@ -46,6 +46,7 @@ CFG2 = dict(layers=32, batch=8, kv_heads=8, q_per_kv=4, context=32768, head_dim=
 CFG5 = dict(layers=32, batch=1, kv_heads=8, context=131072, head_dim=128)
 CFG3 = dict(layers=40, batch=1, kv_heads=40, q_per_kv=1, context=131072, head_dim=128)
 CFG4 = dict(layers=32, batch=64, kv_heads=8, q_per_kv=4, context=16384, head_dim=128)
+CFG1 = dict(layers=1, batch=1, kv_heads=32, q_per_kv=1, context=4096, head_dim=128)
 
 
 def load_workload(ctx, seed):
@@ -580,6 +581,81 @@ def run_cfg4(args, torch, dist, dev, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def run_cfg1(args, torch, dist, dev, rank, world, local):
+    """cfg1: Llama-2-7B single layer (32 MHA heads, d128), 4K context, batch 1, the reference's
+    4K tier map (106/20/2 chunks).  15 MB of arenas: L2-resident and launch-latency bound, so
+    every timed launch follows an L2 flush (256 MB write) and is timed alone with its own event
+    pair.  Not a roofline target; replicas only at N > 1."""
+    from paper_2503_23294_b200 import batched, retrieval
+
+    c = CFG1
+    L, B, H, m, T, D = c["layers"], c["batch"], c["kv_heads"], c["q_per_kv"], c["context"], c["head_dim"]
+    wl = load_workload(T, 0)
+    search = retrieval.search_batched(wl["emb"][None], wl["norm"][None], wl["q"][None],
+                                      np.array([wl["qnorm"]]), 0.6, 0.1)
+    if not np.array_equal(search.tiers.cpu().numpy()[0], wl["tiers"]):
+        raise SystemExit("4K tier map differs from the reference's")
+    g = torch.Generator(device=dev)
+    g.manual_seed(17)
+    k = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    v = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    cache = batched.build_cache_batched(k, v, search)
+    del k, v
+    q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
+    out = torch.empty_like(q)
+    splits = args.splits or cache.default_splits(m)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        cache.decode(q, splits=splits, out=out)
+    times = []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            cache.decode(q, splits=splits, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    qh = q.cpu().pin_memory()
+    oh = torch.empty(q.shape, dtype=torch.float16, pin_memory=True)
+    et = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cache.decode_step_host(qh, oh, splits=splits)
+        e1.record()
+        torch.cuda.synchronize()
+        et.append(e0.elapsed_time(e1))
+    e2e_ms = statistics.median(et)
+    nbytes = cache.algorithmic_bytes(m)
+    if rank == 0:
+        peak, peak_kind = measured_peak_gbs(sustained=False)
+        counts = search.seg_counts.cpu().numpy()[0]
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(world * gbs, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+            "data": "synthetic (fp16 N(0,1) K/V/q; reference search tier map, 4K seed 0)",
+            "config": {"workload": "cfg1: Llama-2-7B 1 layer x 32 MHA heads d128, 4K ctx, batch 1",
+                       "global_batch": B * world, "seq_len": T, "parallelism": f"replicas x{world}",
+                       "tier_chunks_int2_int4_fp16": [int(x) for x in counts], "splits": splits,
+                       "l2": "L2 flushed (256 MB write) before every timed launch"},
+            "us_per_decode": round(ms * 1e3, 2),
+            "algorithmic_bytes_per_step": int(nbytes),
+            "roofline": {"bound": "latency", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "peak_kind": peak_kind, "traffic": None},
+            "e2e": {"value": round(world * nbytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(q.numel() * 2)},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -589,10 +665,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--splits", type=int, default=None)
-    ap.add_argument("--workload", choices=["cfg2", "cfg3", "cfg4"], default="cfg2",
+    ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4"], default="cfg2",
                     help="cfg2: batch-sharded 32K GQA decode (default); cfg3: 128K MHA decode with "
                          "sequence split-KV across the ranks (NCCL all-gather + LSE merge); cfg4: "
-                         "batch 64 x 16K GQA decode sharded over the ranks (--cfg4-map)")
+                         "batch 64 x 16K GQA decode sharded over the ranks (--cfg4-map); cfg1: the "
+                         "4K single-layer MHA parity config (L2-flushed, latency bound)")
     ap.add_argument("--cfg4-map", choices=["skewed", "all_int2", "all_fp16"], default="skewed")
     args = ap.parse_args()
 
@@ -616,8 +693,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    if args.workload in ("cfg3", "cfg4"):
-        (run_cfg3 if args.workload == "cfg3" else run_cfg4)(args, torch, dist, dev, rank, world, local)
+    if args.workload in ("cfg1", "cfg3", "cfg4"):
+        fn = {"cfg1": run_cfg1, "cfg3": run_cfg3, "cfg4": run_cfg4}[args.workload]
+        fn(args, torch, dist, dev, rank, world, local)
         if world > 1:
             dist.destroy_process_group()
         return
