@@ -106,38 +106,17 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   return r;
 }
 
+// Codes of 8 elements (4 half2 words) for a group with lower bound lo and qinv = qmax / span,
+// packed as the reference's little-endian sub-word codes; element pairs in packed f32x2
+// arithmetic (FADD2 / FFMA2: half the issue slots):
+//   d = x - lo;  y = RN(d qinv + 1.5 2^23) (the code lands in y's low mantissa bits);
+//   e = d qinv - (y - 1.5 2^23) (one rounding);  dmax = max |e| (the guard test)
 template <int BITS>
-__device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float& lo_out, float& hi_out,
-                                                   bool& bad, bool& wide) {
-  constexpr float qmax = BITS == 2 ? 3.0f : 15.0f;
+__device__ __forceinline__ uint32_t codes8(const uint32_t* w, float lo, float qinv, float& dmax) {
   constexpr uint32_t base = BITS == 2 ? 4u : 16u;
   constexpr uint32_t kM = 0x4B400000u;  // bits of 1.5 * 2^23
   constexpr uint32_t kSum = BITS == 2 ? 21845u : 0x11111111u;  // sum_e base^e, e = 0..7
-  // group min / max in fp16 with NaN propagation; (lo, -hi) travel as one half2 so that one
-  // min per butterfly step reduces both over the group's 4 lanes
-  const uint32_t mn = hmin2_nan(hmin2_nan(w[0], w[1]), hmin2_nan(w[2], w[3]));
-  const uint32_t nmx = hmax2_nan(hmax2_nan(w[0], w[1]), hmax2_nan(w[2], w[3])) ^ 0x80008000u;
-  uint32_t lh = hmin2_nan(prmt_q(mn, nmx, 0x5410), prmt_q(mn, nmx, 0x7632));
-  lh = hmin2_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 1));
-  lh = hmin2_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 2));
-  const float2 lhf = __half22float2(u32_as_h2(lh));
-  const float lo = lhf.x, hi = -lhf.y;
-  lo_out = lo;
-  hi_out = hi;
-  const float span = hi - lo;
-  bad |= !(span < INFINITY);  // an inf / nan anywhere in the group makes the span inf or nan
-  wide |= span > 4000.0f * qmax;
-  if (!(span > 0.0f)) return 0u;  // constant group: codes 0 (also nan groups; flagged above)
-  // qmax / span via the approximate reciprocal (<= 2 ulp): the candidate r below stays within
-  // 2^-17 of the exact rational, well inside the 2^-14 guard band that triggers the exact path
-  float rs;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(span));
-  const float qinv = qmax * rs;
   uint32_t acc = 0u - kM * kSum;
-  float dmax = 0.0f;  // max |r - round(r)| over the slice
-  // element pairs in packed f32x2 arithmetic (FADD2 / FFMA2: half the issue slots):
-  //   d = x - lo;  y = RN(d qinv + 1.5 2^23) (the code lands in y's low mantissa bits);
-  //   e = d qinv - (y - 1.5 2^23) (one rounding)
   const uint64_t nlo = f2pack(-lo, -lo), qi = f2pack(qinv, qinv), mm = f2pack(12582912.0f, 12582912.0f);
   const uint64_t neg1 = f2pack(-1.0f, -1.0f);
 #pragma unroll
@@ -155,15 +134,49 @@ __device__ __forceinline__ uint32_t quantize_slice(const uint32_t (&w)[4], float
     for (int k = 0; k < 2 * i; ++k) p0 *= base;
     acc += __float_as_uint(y0) * p0 + __float_as_uint(y1) * (p0 * base);
   }
-  const bool near = dmax > 0.5f - (1.0f / 16384.0f);
-  if (near) acc = exact_slice(w[0], w[1], w[2], w[3], lo, hi, qinv, qmax, base);  // rare
   return acc;
 }
 
-// One 32-row chunk of K (ISV = false) or V rows -> codes and (lo, hi) metadata staged in shared
-// memory in the tile-native layout (2 tiles).  Lanes: sub = lane / 16 picks the row of a pair,
-// j = lane % 16 the 8-element slice (4 lanes = one 32-element group).  Returns whether a group's
-// scale needs the decode's wide-scale mode.
+// One 16-element lane slice of a row (2 lanes = one 32-element group): group min / max in fp16
+// with NaN propagation ((lo, -hi) travel as one half2, so one min reduces both across the lane
+// pair), one scale, and the codes of both 8-element halves (c[0]: elements 0-7, c[1]: 8-15),
+// each packed like the reference's words.  A half whose candidate lies within 2^-14 of a
+// rounding boundary is recomputed in IEEE f64 (exact_slice, rare).
+template <int BITS>
+__device__ __forceinline__ void quantize_slice16(const uint32_t (&w)[8], uint32_t (&c)[2], float& lo_out,
+                                                 float& hi_out, bool& bad, bool& wide) {
+  constexpr float qmax = BITS == 2 ? 3.0f : 15.0f;
+  constexpr uint32_t base = BITS == 2 ? 4u : 16u;
+  const uint32_t mn = hmin2_nan(hmin2_nan(hmin2_nan(w[0], w[1]), hmin2_nan(w[2], w[3])),
+                                hmin2_nan(hmin2_nan(w[4], w[5]), hmin2_nan(w[6], w[7])));
+  const uint32_t nmx = hmax2_nan(hmax2_nan(hmax2_nan(w[0], w[1]), hmax2_nan(w[2], w[3])),
+                                 hmax2_nan(hmax2_nan(w[4], w[5]), hmax2_nan(w[6], w[7]))) ^ 0x80008000u;
+  uint32_t lh = hmin2_nan(prmt_q(mn, nmx, 0x5410), prmt_q(mn, nmx, 0x7632));
+  lh = hmin2_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 1));
+  const float2 lhf = __half22float2(u32_as_h2(lh));
+  const float lo = lhf.x, hi = -lhf.y;
+  lo_out = lo;
+  hi_out = hi;
+  const float span = hi - lo;
+  bad |= !(span < INFINITY);  // an inf / nan anywhere in the group makes the span inf or nan
+  wide |= span > 4000.0f * qmax;
+  if (!(span > 0.0f)) {  // constant group: codes 0 (also nan groups; flagged above)
+    c[0] = c[1] = 0u;
+    return;
+  }
+  // qmax / span via the approximate reciprocal (<= 2 ulp): the candidate stays within 2^-17 of
+  // the exact rational, well inside the 2^-14 guard band that triggers the exact path
+  float rs;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(span));
+  const float qinv = qmax * rs;
+  float d0 = 0.0f, d1 = 0.0f;
+  c[0] = codes8<BITS>(w, lo, qinv, d0);
+  c[1] = codes8<BITS>(w + 4, lo, qinv, d1);
+  constexpr float kNear = 0.5f - (1.0f / 16384.0f);
+  if (d0 > kNear) c[0] = exact_slice(w[0], w[1], w[2], w[3], lo, hi, qinv, qmax, base);  // rare
+  if (d1 > kNear) c[1] = exact_slice(w[4], w[5], w[6], w[7], lo, hi, qinv, qmax, base);
+}
+
 // Staging offsets of the tile-native layout (ckv_common.cuh tile_off_*) for row
 // r = 2 (r4 + u) + sub and slice j, decomposed as
 //   (r4 >> 3) TB + ((r4 >> 2) & 1) X + u U + L(j, sub, hf)
@@ -190,44 +203,59 @@ template <int BITS, bool ISV> struct MetaStageOff {
 };
 
 // One 32-row chunk of K (ISV = false) or V rows -> codes and (lo, hi) metadata staged in shared
-// memory in the tile-native layout (2 tiles).  Lanes: sub = lane / 16 picks the row of a pair,
-// j = lane % 16 the 8-element slice (4 lanes = one 32-element group).  Returns whether a group's
-// scale needs the decode's wide-scale mode.
+// memory in the tile-native layout (2 tiles).  Lanes: rs = lane / 8 picks the row of a quad
+// (rows 4q + rs), jj = lane % 8 the 16-element slice (2 lanes = one 32-element group); each
+// lane covers the reference's 8-element slices j = 2 jj, 2 jj + 1 of StageOff.  Row r of the
+// chunk sits at StageOff's (r4, u, sub) = ((r >> 3) << 2, (r >> 1) & 3, r & 1).  Returns
+// whether a group's scale needs the decode's wide-scale mode.
 template <int BITS, bool ISV>
-__device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, int sub, int j,
+__device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, int lane,
                                                unsigned char* sc, unsigned char* sm, bool& bad,
                                                float& smax) {
   using SO = StageOff<BITS, ISV>;
   using MO = MetaStageOff<BITS, ISV>;
   bool wide = false;
-  const int lc = SO::lane(j, sub), lm = MO::lane(j, sub);
+  const int rs = lane >> 3, jj = lane & 7;
+  const int sub = rs & 1, j0 = 2 * jj;
+  // per-lane parts of the two slices' code offsets and the group's metadata offset
+  const int lc0 = SO::lane(j0, sub) + (rs >> 1) * SO::U, lc1 = SO::lane(j0 + 1, sub) + (rs >> 1) * SO::U;
+  const int lm = MO::lane(j0, sub) + (rs >> 1) * MO::U;
+  const uint4* srow = reinterpret_cast<const uint4*>(src + rs * sT) + 2 * jj;
 #pragma unroll 1
-  for (int r4 = 0; r4 < 16; r4 += 4) {
+  for (int it = 0; it < 4; ++it) {  // rows 4q + rs, q = 2 it + h
     uint4 xs[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)  // four 16-byte loads in flight per lane
-      xs[u] = __ldg(reinterpret_cast<const uint4*>(src + (2 * (r4 + u) + sub) * sT) + j);
-    unsigned char* cb = sc + (r4 >> 3) * SO::TB + ((r4 >> 2) & 1) * SO::X + lc;
-    unsigned char* mb = sm + (r4 >> 3) * MO::TB + ((r4 >> 2) & 1) * MO::X + lm;
+    for (int h = 0; h < 2; ++h) {  // four 16-byte loads in flight per lane
+      const uint4* p = srow + (int64_t)(4 * (2 * it + h)) * sT / 8;
+      xs[2 * h] = __ldg(p);
+      xs[2 * h + 1] = __ldg(p + 1);
+    }
+    const int tq = (it >> 1) * SO::TB + (it & 1) * SO::X;
+    const int tm = (it >> 1) * MO::TB + (it & 1) * MO::X;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t w[4] = {xs[u].x, xs[u].y, xs[u].z, xs[u].w};
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
+                             xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
       float lo, hi;
-      const uint32_t packed = quantize_slice<BITS>(w, lo, hi, bad, wide);
+      uint32_t c[2];
+      quantize_slice16<BITS>(w, c, lo, hi, bad, wide);
       smax = fmaxf(smax, hi - lo);
-      if (BITS == 2) {
-        *reinterpret_cast<uint16_t*>(cb + u * SO::U) = (uint16_t)packed;
-      } else {
-        *reinterpret_cast<uint16_t*>(cb + u * SO::U) = (uint16_t)packed;
-        *reinterpret_cast<uint16_t*>(cb + u * SO::U + 4) = (uint16_t)(packed >> 16);
+      unsigned char* c0 = sc + tq + 2 * h * SO::U + lc0;
+      unsigned char* c1 = sc + tq + 2 * h * SO::U + lc1;
+      *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
+      *reinterpret_cast<uint16_t*>(c1) = (uint16_t)c[1];
+      if (BITS == 4) {
+        *reinterpret_cast<uint16_t*>(c0 + 4) = (uint16_t)(c[0] >> 16);
+        *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
       }
-      if ((j & 3) == 0) {
-        const uint32_t lh = h2_as_u32(__floats2half2_rn(lo, hi));
+      if ((jj & 1) == 0) {
+        unsigned char* mb = sm + tm + 2 * h * MO::U + lm;
+        const uint32_t lhw = h2_as_u32(__floats2half2_rn(lo, hi));
         if (ISV) {
-          *reinterpret_cast<uint16_t*>(mb + u * MO::U) = (uint16_t)lh;
-          *reinterpret_cast<uint16_t*>(mb + u * MO::U + 4) = (uint16_t)(lh >> 16);
+          *reinterpret_cast<uint16_t*>(mb) = (uint16_t)lhw;
+          *reinterpret_cast<uint16_t*>(mb + 4) = (uint16_t)(lhw >> 16);
         } else {
-          *reinterpret_cast<uint32_t*>(mb + u * MO::U) = lh;
+          *reinterpret_cast<uint32_t*>(mb) = lhw;
         }
       }
     }
@@ -327,10 +355,10 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
     unsigned char* sm = s_blk[warp] + 2 * code_bytes + (tsel ? kTileBytesMeta : 0);
     bool wide;
     float smax = 0.0f;  // largest group span of the chunk (decode precision routing)
-    if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, sub, j, sc, sm, bad, smax)
-                                 : quantize_chunk<2, false>(src, sT, sub, j, sc, sm, bad, smax);
-    else wide = tsel ? quantize_chunk<4, true>(src, sT, sub, j, sc, sm, bad, smax)
-                     : quantize_chunk<4, false>(src, sT, sub, j, sc, sm, bad, smax);
+    if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, lane, sc, sm, bad, smax)
+                                 : quantize_chunk<2, false>(src, sT, lane, sc, sm, bad, smax);
+    else wide = tsel ? quantize_chunk<4, true>(src, sT, lane, sc, sm, bad, smax)
+                     : quantize_chunk<4, false>(src, sT, lane, sc, sm, bad, smax);
     __syncwarp();
     const QTask t2 = read_task(task_addr);
     const CtaPos c2 = cta_pos(B);
