@@ -241,12 +241,20 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
       quantize_slice16<BITS>(w, c, lo, hi, bad, wide);
       smax = fmaxf(smax, hi - lo);
       unsigned char* c0 = sc + tq + 2 * h * SO::U + lc0;
-      unsigned char* c1 = sc + tq + 2 * h * SO::U + lc1;
-      *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
-      *reinterpret_cast<uint16_t*>(c1) = (uint16_t)c[1];
-      if (BITS == 4) {
-        *reinterpret_cast<uint16_t*>(c0 + 4) = (uint16_t)(c[0] >> 16);
-        *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
+      if (!ISV) {  // K: the two slices' 16-bit pieces are adjacent (SO::lane(j0 + 1) = + 2)
+        if (BITS == 2) {
+          *reinterpret_cast<uint32_t*>(c0) = prmt_q(c[0], c[1], 0x5410);
+        } else {
+          *reinterpret_cast<uint2*>(c0) = make_uint2(prmt_q(c[0], c[1], 0x5410), prmt_q(c[0], c[1], 0x7632));
+        }
+      } else {
+        unsigned char* c1 = sc + tq + 2 * h * SO::U + lc1;
+        *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
+        *reinterpret_cast<uint16_t*>(c1) = (uint16_t)c[1];
+        if (BITS == 4) {
+          *reinterpret_cast<uint16_t*>(c0 + 4) = (uint16_t)(c[0] >> 16);
+          *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
+        }
       }
       if ((jj & 1) == 0) {
         unsigned char* mb = sm + tm + 2 * h * MO::U + lm;
