@@ -203,8 +203,8 @@ template <int BITS, bool ISV> struct MetaStageOff {
 };
 
 // One 32-row chunk of K (ISV = false) or V rows -> codes and (lo, hi) metadata staged in shared
-// memory in the tile-native layout (2 tiles).  Lanes: rs = lane / 8 picks the row of a quad
-// (rows 4q + rs), jj = lane % 8 the 16-element slice (2 lanes = one 32-element group); each
+// memory in the tile-native layout (2 tiles).  Lanes: rs = lane / 8 picks the row
+// (rows 2 it + 16 h + (rs & 1) + 8 (rs >> 1)), jj = lane % 8 the 16-element slice (2 lanes = one 32-element group); each
 // lane covers the reference's 8-element slices j = 2 jj, 2 jj + 1 of StageOff.  Row r of the
 // chunk sits at StageOff's (r4, u, sub) = ((r >> 3) << 2, (r >> 1) & 3, r & 1).  Returns
 // whether a group's scale needs the decode's wide-scale mode.
@@ -217,21 +217,23 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
   bool wide = false;
   const int rs = lane >> 3, jj = lane & 7;
   const int sub = rs & 1, j0 = 2 * jj;
-  // per-lane parts of the two slices' code offsets and the group's metadata offset
-  const int lc0 = SO::lane(j0, sub) + (rs >> 1) * SO::U, lc1 = SO::lane(j0 + 1, sub) + (rs >> 1) * SO::U;
-  const int lm = MO::lane(j0, sub) + (rs >> 1) * MO::U;
-  const uint4* srow = reinterpret_cast<const uint4*>(src + rs * sT) + 2 * jj;
+  // per-lane parts of the two slices' code offsets and the group's metadata offset: the
+  // lane's rows differ from its step's first row in bits 0 and 3 (sub, X), which keeps the
+  // K stores of a warp in distinct banks (bits 1-2 (U) would alias them)
+  const int lc0 = SO::lane(j0, sub) + (rs >> 1) * SO::X, lc1 = SO::lane(j0 + 1, sub) + (rs >> 1) * SO::X;
+  const int lm = MO::lane(j0, sub) + (rs >> 1) * MO::X;
+  const uint4* srow = reinterpret_cast<const uint4*>(src + (sub + 8 * (rs >> 1)) * sT) + 2 * jj;
 #pragma unroll 1
-  for (int it = 0; it < 4; ++it) {  // rows 4q + rs, q = 2 it + h
+  for (int it = 0; it < 4; ++it) {  // rows 2 it + 16 h + sub + 8 (rs >> 1)
     uint4 xs[4];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // four 16-byte loads in flight per lane
-      const uint4* p = srow + (int64_t)(4 * (2 * it + h)) * sT / 8;
+      const uint4* p = srow + (int64_t)(2 * it + 16 * h) * sT / 8;
       xs[2 * h] = __ldg(p);
       xs[2 * h + 1] = __ldg(p + 1);
     }
-    const int tq = (it >> 1) * SO::TB + (it & 1) * SO::X;
-    const int tm = (it >> 1) * MO::TB + (it & 1) * MO::X;
+    const int tq = it * SO::U;
+    const int tm = it * MO::U;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
@@ -240,7 +242,7 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
       uint32_t c[2];
       quantize_slice16<BITS>(w, c, lo, hi, bad, wide);
       smax = fmaxf(smax, hi - lo);
-      unsigned char* c0 = sc + tq + 2 * h * SO::U + lc0;
+      unsigned char* c0 = sc + tq + h * SO::TB + lc0;
       if (!ISV) {  // K: the two slices' 16-bit pieces are adjacent (SO::lane(j0 + 1) = + 2)
         if (BITS == 2) {
           *reinterpret_cast<uint32_t*>(c0) = prmt_q(c[0], c[1], 0x5410);
@@ -248,7 +250,7 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
           *reinterpret_cast<uint2*>(c0) = make_uint2(prmt_q(c[0], c[1], 0x5410), prmt_q(c[0], c[1], 0x7632));
         }
       } else {
-        unsigned char* c1 = sc + tq + 2 * h * SO::U + lc1;
+        unsigned char* c1 = sc + tq + h * SO::TB + lc1;
         *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
         *reinterpret_cast<uint16_t*>(c1) = (uint16_t)c[1];
         if (BITS == 4) {
@@ -257,7 +259,7 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
         }
       }
       if ((jj & 1) == 0) {
-        unsigned char* mb = sm + tm + 2 * h * MO::U + lm;
+        unsigned char* mb = sm + tm + h * MO::TB + lm;
         const uint32_t lhw = h2_as_u32(__floats2half2_rn(lo, hi));
         if (ISV) {
           *reinterpret_cast<uint16_t*>(mb) = (uint16_t)lhw;
