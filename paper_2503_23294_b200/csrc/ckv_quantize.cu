@@ -208,10 +208,65 @@ template <int BITS, bool ISV> struct MetaStageOff {
 // lane covers the reference's 8-element slices j = 2 jj, 2 jj + 1 of StageOff.  Row r of the
 // chunk sits at StageOff's (r4, u, sub) = ((r >> 3) << 2, (r >> 1) & 3, r & 1).  Returns
 // whether a group's scale needs the decode's wide-scale mode.
+// V rows: lanes over 16 rows x the 2 halves of one group, so that a warp's V code and
+// metadata stores fall in distinct banks (lanes over slices, as for K, would put the 64-byte
+// slice stride of the V tile layout on 2 banks).  lane = 2 rr + hg: rows rr (+16 h), group it;
+// elements 32 it + 8 hg + [0, 8) and 32 it + 16 + 8 hg + [0, 8), i.e. the reference's
+// 8-element slices j = 4 it + hg and 4 it + 2 + hg (each load instruction reads a row's 32
+// contiguous bytes with the lane pair).
+template <int BITS>
+__device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int64_t sT, int lane,
+                                                 unsigned char* sc, unsigned char* sm, bool& bad,
+                                                 float& smax) {
+  using SO = StageOff<BITS, true>;
+  using MO = MetaStageOff<BITS, true>;
+  bool wide = false;
+  const int rr = lane >> 1, hg = lane & 1, sub = rr & 1;
+  const int rowc = ((rr >> 3) & 1) * SO::X + ((rr >> 1) & 3) * SO::U;
+  const int rowm = ((rr >> 3) & 1) * MO::X + ((rr >> 1) & 3) * MO::U;
+  const uint4* srow = reinterpret_cast<const uint4*>(src + rr * sT) + hg;
+#pragma unroll 1
+  for (int it = 0; it < 4; ++it) {  // group it, rows rr and rr + 16
+    uint4 xs[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // four 16-byte loads in flight per lane
+      const uint4* p = srow + (int64_t)(16 * h) * sT / 8 + 4 * it;
+      xs[2 * h] = __ldg(p);
+      xs[2 * h + 1] = __ldg(p + 2);
+    }
+    const int j0 = 4 * it + hg, j1 = j0 + 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
+                             xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
+      float lo, hi;
+      uint32_t c[2];
+      quantize_slice16<BITS>(w, c, lo, hi, bad, wide);
+      smax = fmaxf(smax, hi - lo);
+      unsigned char* c0 = sc + h * SO::TB + rowc + SO::lane(j0, sub);
+      unsigned char* c1 = sc + h * SO::TB + rowc + SO::lane(j1, sub);
+      *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
+      *reinterpret_cast<uint16_t*>(c1) = (uint16_t)c[1];
+      if (BITS == 4) {
+        *reinterpret_cast<uint16_t*>(c0 + 4) = (uint16_t)(c[0] >> 16);
+        *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
+      }
+      if (hg == 0) {
+        unsigned char* mb = sm + h * MO::TB + rowm + MO::lane(j0, sub);
+        const uint32_t lhw = h2_as_u32(__floats2half2_rn(lo, hi));
+        *reinterpret_cast<uint16_t*>(mb) = (uint16_t)lhw;
+        *reinterpret_cast<uint16_t*>(mb + 4) = (uint16_t)(lhw >> 16);
+      }
+    }
+  }
+  return wide;
+}
+
 template <int BITS, bool ISV>
 __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, int lane,
                                                unsigned char* sc, unsigned char* sm, bool& bad,
                                                float& smax) {
+  if (ISV) return quantize_chunk_v<BITS>(src, sT, lane, sc, sm, bad, smax);
   using SO = StageOff<BITS, ISV>;
   using MO = MetaStageOff<BITS, ISV>;
   bool wide = false;
