@@ -108,8 +108,8 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
 
 // Codes of 8 elements (4 half2 words) for a group with lower bound lo and qinv = qmax / span,
 // packed as the reference's little-endian sub-word codes; element pairs in packed f32x2
-// arithmetic (FADD2 / FFMA2: half the issue slots):
-//   d = x - lo;  y = RN(d qinv + 1.5 2^23) (the code lands in y's low mantissa bits);
+// arithmetic (FFMA2: half the issue slots):
+//   d = x - lo (fp16 - fp32, one rounding);  y = RN(d qinv + 1.5 2^23) (the code lands in y's low mantissa bits);
 //   e = d qinv - (y - 1.5 2^23) (one rounding);  dmax = max |e| (the guard test)
 template <int BITS>
 __device__ __forceinline__ uint32_t codes8(const uint32_t* w, float lo, float qinv, float& dmax) {
@@ -117,12 +117,14 @@ __device__ __forceinline__ uint32_t codes8(const uint32_t* w, float lo, float qi
   constexpr uint32_t kM = 0x4B400000u;  // bits of 1.5 * 2^23
   constexpr uint32_t kSum = BITS == 2 ? 21845u : 0x11111111u;  // sum_e base^e, e = 0..7
   uint32_t acc = 0u - kM * kSum;
-  const uint64_t nlo = f2pack(-lo, -lo), qi = f2pack(qinv, qinv), mm = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t qi = f2pack(qinv, qinv), mm = f2pack(12582912.0f, 12582912.0f);
   const uint64_t neg1 = f2pack(-1.0f, -1.0f);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float2 x = __half22float2(u32_as_h2(w[i]));
-    const uint64_t d = fadd2(f2pack(x.x, x.y), nlo);
+    float dx, dy;  // x - lo straight from the fp16 halves (mixed f16 - f32 subtract, one rounding)
+    asm("{.reg .f16 a, b; mov.b32 {a, b}, %2; sub.rn.f32.f16 %0, a, %3; sub.rn.f32.f16 %1, b, %3;}"
+        : "=f"(dx), "=f"(dy) : "r"(w[i]), "f"(lo));
+    const uint64_t d = f2pack(dx, dy);
     const uint64_t y = ffma2(d, qi, mm);
     const uint64_t e = ffma2(d, qi, ffma2(y, neg1, mm));
     float e0, e1, y0, y1;
