@@ -145,8 +145,8 @@ __device__ __forceinline__ uint32_t codes8(const uint32_t* w, float lo, float qi
 // each packed like the reference's words.  A half whose candidate lies within 2^-14 of a
 // rounding boundary is recomputed in IEEE f64 (exact_slice, rare).
 template <int BITS>
-__device__ __forceinline__ void quantize_slice16(const uint32_t (&w)[8], uint32_t (&c)[2], float& lo_out,
-                                                 float& hi_out, bool& bad, bool& wide) {
+__device__ __forceinline__ void quantize_slice16(const uint32_t (&w)[8], uint32_t (&c)[2], uint32_t& meta,
+                                                 float& smax) {
   constexpr float qmax = BITS == 2 ? 3.0f : 15.0f;
   constexpr uint32_t base = BITS == 2 ? 4u : 16u;
   const uint32_t mn = hmin2_nan(hmin2_nan(hmin2_nan(w[0], w[1]), hmin2_nan(w[2], w[3])),
@@ -155,14 +155,14 @@ __device__ __forceinline__ void quantize_slice16(const uint32_t (&w)[8], uint32_
                                  hmax2_nan(hmax2_nan(w[4], w[5]), hmax2_nan(w[6], w[7]))) ^ 0x80008000u;
   uint32_t lh = hmin2_nan(prmt_q(mn, nmx, 0x5410), prmt_q(mn, nmx, 0x7632));
   lh = hmin2_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 1));
+  meta = lh ^ 0x80000000u;  // the group's fp16 (lo, hi)
   const float2 lhf = __half22float2(u32_as_h2(lh));
   const float lo = lhf.x, hi = -lhf.y;
-  lo_out = lo;
-  hi_out = hi;
   const float span = hi - lo;
-  bad |= !(span < INFINITY);  // an inf / nan anywhere in the group makes the span inf or nan
-  wide |= span > 4000.0f * qmax;
-  if (!(span > 0.0f)) {  // constant group: codes 0 (also nan groups; flagged above)
+  // NaN-propagating max: an inf / nan anywhere in a group makes its span inf or nan, so the
+  // chunk's non-finite and wide-scale tests are on smax after the loop
+  asm("max.NaN.f32 %0, %0, %1;" : "+f"(smax) : "f"(span));
+  if (!(span > 0.0f)) {  // constant group: codes 0 (also nan groups; flagged from smax)
     c[0] = c[1] = 0u;
     return;
   }
@@ -210,6 +210,13 @@ template <int BITS, bool ISV> struct MetaStageOff {
 // lane covers the reference's 8-element slices j = 2 jj, 2 jj + 1 of StageOff.  Row r of the
 // chunk sits at StageOff's (r4, u, sub) = ((r >> 3) << 2, (r >> 1) & 3, r & 1).  Returns
 // whether a group's scale needs the decode's wide-scale mode.
+// After a chunk half: non-finite input anywhere (its span max is inf or nan) and the decode's
+// wide-scale test (some group scale span / qmax above 4000).
+__device__ __forceinline__ bool chunk_flags(float smax, float qmax, bool& bad) {
+  bad |= !(smax < INFINITY);
+  return smax > 4000.0f * qmax;
+}
+
 // V rows: lanes over 16 rows x the 2 halves of one group, so that a warp's V code and
 // metadata stores fall in distinct banks (lanes over slices, as for K, would put the 64-byte
 // slice stride of the V tile layout on 2 banks).  lane = 2 rr + hg: rows rr (+16 h), group it;
@@ -222,7 +229,6 @@ __device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int64_t sT
                                                  float& smax) {
   using SO = StageOff<BITS, true>;
   using MO = MetaStageOff<BITS, true>;
-  bool wide = false;
   const int rr = lane >> 1, hg = lane & 1, sub = rr & 1;
   const int rowc = ((rr >> 3) & 1) * SO::X + ((rr >> 1) & 3) * SO::U;
   const int rowm = ((rr >> 3) & 1) * MO::X + ((rr >> 1) & 3) * MO::U;
@@ -241,10 +247,8 @@ __device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int64_t sT
     for (int h = 0; h < 2; ++h) {
       const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
                              xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
-      float lo, hi;
-      uint32_t c[2];
-      quantize_slice16<BITS>(w, c, lo, hi, bad, wide);
-      smax = fmaxf(smax, hi - lo);
+      uint32_t c[2], meta;
+      quantize_slice16<BITS>(w, c, meta, smax);
       unsigned char* c0 = sc + h * SO::TB + rowc + SO::lane(j0, sub);
       unsigned char* c1 = sc + h * SO::TB + rowc + SO::lane(j1, sub);
       *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
@@ -253,15 +257,13 @@ __device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int64_t sT
         *reinterpret_cast<uint16_t*>(c0 + 4) = (uint16_t)(c[0] >> 16);
         *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
       }
-      if (hg == 0) {
-        unsigned char* mb = sm + h * MO::TB + rowm + MO::lane(j0, sub);
-        const uint32_t lhw = h2_as_u32(__floats2half2_rn(lo, hi));
-        *reinterpret_cast<uint16_t*>(mb) = (uint16_t)lhw;
-        *reinterpret_cast<uint16_t*>(mb + 4) = (uint16_t)(lhw >> 16);
-      }
+      // both lanes of the group hold the same (lo, hi): duplicate stores, no branch
+      unsigned char* mb = sm + h * MO::TB + rowm + MO::lane(j0, sub);
+      *reinterpret_cast<uint16_t*>(mb) = (uint16_t)meta;
+      *reinterpret_cast<uint16_t*>(mb + 4) = (uint16_t)(meta >> 16);
     }
   }
-  return wide;
+  return chunk_flags(smax, BITS == 2 ? 3.0f : 15.0f, bad);
 }
 
 template <int BITS, bool ISV>
@@ -271,7 +273,6 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
   if (ISV) return quantize_chunk_v<BITS>(src, sT, lane, sc, sm, bad, smax);
   using SO = StageOff<BITS, ISV>;
   using MO = MetaStageOff<BITS, ISV>;
-  bool wide = false;
   const int rs = lane >> 3, jj = lane & 7;
   const int sub = rs & 1, j0 = 2 * jj;
   // per-lane parts of the two slices' code offsets and the group's metadata offset: the
@@ -295,10 +296,8 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
     for (int h = 0; h < 2; ++h) {
       const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
                              xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
-      float lo, hi;
-      uint32_t c[2];
-      quantize_slice16<BITS>(w, c, lo, hi, bad, wide);
-      smax = fmaxf(smax, hi - lo);
+      uint32_t c[2], meta;
+      quantize_slice16<BITS>(w, c, meta, smax);
       unsigned char* c0 = sc + tq + h * SO::TB + lc0;
       if (!ISV) {  // K: the two slices' 16-bit pieces are adjacent (SO::lane(j0 + 1) = + 2)
         if (BITS == 2) {
@@ -315,19 +314,11 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
           *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
         }
       }
-      if ((jj & 1) == 0) {
-        unsigned char* mb = sm + tm + h * MO::TB + lm;
-        const uint32_t lhw = h2_as_u32(__floats2half2_rn(lo, hi));
-        if (ISV) {
-          *reinterpret_cast<uint16_t*>(mb) = (uint16_t)lhw;
-          *reinterpret_cast<uint16_t*>(mb + 4) = (uint16_t)(lhw >> 16);
-        } else {
-          *reinterpret_cast<uint32_t*>(mb) = lhw;
-        }
-      }
+      // both lanes of the group hold the same (lo, hi): duplicate stores, no branch
+      *reinterpret_cast<uint32_t*>(sm + tm + h * MO::TB + lm) = meta;
     }
   }
-  return wide;
+  return chunk_flags(smax, BITS == 2 ? 3.0f : 15.0f, bad);
 }
 
 struct QTask {
