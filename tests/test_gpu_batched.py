@@ -312,3 +312,28 @@ def test_decode_step_host_matches_device_decode():
         torch.cuda.synchronize()
         want = cache.decode(q.cuda()).cpu()
         assert torch.equal(oh, want), step
+
+
+def test_context_shorter_than_one_chunk():
+    """A sequence with no full chunk (everything rides in the FP16 tail, harness.py:196-199)
+    next to a normal one, built through the layout constructor (no search for the short one)."""
+    rng = np.random.default_rng(61)
+    L, B, H, m, D = 1, 2, 2, 4, 128
+    ctx = np.array([20, 3 * 32 + 1])
+    Tmax = int(ctx.max())
+    k = rng.normal(size=(L, B, Tmax, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, Tmax, H, D)).astype(np.float16)
+    tiers1 = np.array([0, 2, 1], np.uint8)
+    counts = np.array([[0, 0, 0], np.bincount(tiers1, minlength=3)])
+    perm = np.zeros((B, 3), np.int32)
+    perm[1] = np.concatenate([np.nonzero(tiers1 == t)[0] for t in (0, 1, 2)])
+    cache = batched.BatchedKVCache(L, B, H, counts[:, 0], counts[:, 1], counts[:, 2], ctx, 8, device=torch.device("cuda"))
+    cache.build(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(perm).cuda())
+    q = rng.normal(size=(L, B, H * m, D)).astype(np.float16)
+    out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for b, tl in ((0, np.zeros(0, np.uint8)), (1, tiers1)):
+        for h in range(H):
+            oc = O.build_cache(k[0, b, :ctx[b], h].astype(np.float64), v[0, b, :ctx[b], h].astype(np.float64), tl, 32, 32)
+            ref = O.mixed_decode_attention(q[0, b, h * m:(h + 1) * m].astype(np.float64), oc)
+            err = np.max(np.abs(out[0, b, h * m:(h + 1) * m] - ref))
+            assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (b, h, err)
