@@ -222,9 +222,10 @@ class BatchedKVCache:
     def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=16, order_current=True):
         """One decode step for all layers from HOST buffers: pinned fp16 q [L, B, H*m, 128] ->
         pinned fp16 output of the same shape.  The q upload runs on its own copy stream (it
-        overlaps the previous step's last layers), layer 0 waits only for its own slice; the
-        outputs go back on a second copy stream every `d2h_every` layers while the next layers
-        compute; per-layer decode launches stay PDL-chained between those points.  Device
+        overlaps the previous step's layers); the layers run as CUDA-graph segments of
+        `d2h_every` PDL-chained per-layer launches (captured once per staging buffer, so the
+        host enqueues one replay per segment instead of one launch per layer); each segment's
+        outputs go back on a second copy stream while the next segment computes.  Device
         staging is double-buffered across steps, so consecutive steps never wait on each
         other's copies.  With ``order_current`` the current stream is ordered after the last
         download on return; without it the downloads stay on the copy stream (they overlap the
@@ -234,43 +235,41 @@ class BatchedKVCache:
             raise ValueError("q shape does not match the cache")
         if out_host.shape != q_host.shape or out_host.dtype != torch.float16:
             raise ValueError("out_host must match q_host")
-        key = tuple(q_host.shape)
+        seg = max(1, min(int(d2h_every), L))
+        key = (tuple(q_host.shape), splits, scale, seg)
         st = getattr(self, "_host_step", None)
         if st is None or st["key"] != key:
             dev = self.device
-            st = dict(key=key, q=[torch.empty(key, dtype=torch.float16, device=dev) for _ in range(2)],
-                      o=[torch.empty(key, dtype=torch.float16, device=dev) for _ in range(2)],
+            shape = tuple(q_host.shape)
+            st = dict(key=key, q=[torch.empty(shape, dtype=torch.float16, device=dev) for _ in range(2)],
+                      o=[torch.empty(shape, dtype=torch.float16, device=dev) for _ in range(2)],
                       cin=torch.cuda.Stream(device=dev), cout=torch.cuda.Stream(device=dev),
-                      q_free=[None, None], o_free=[None, None], i=0)
+                      q_free=[None, None], o_free=[None, None], i=0, graphs=[None, None])
+            for b in range(2):
+                st["graphs"][b] = self._segment_graphs(st["q"][b], st["o"][b], seg, splits, scale)
             self._host_step = st
         ms = torch.cuda.current_stream()
         cin, cout = st["cin"], st["cout"]
         buf = st["i"] & 1
         st["i"] += 1
         qd, od = st["q"][buf], st["o"][buf]
-        ev_q0, ev_q = torch.cuda.Event(), torch.cuda.Event()
+        ev_q = torch.cuda.Event()
         with torch.cuda.stream(cin):
             if st["q_free"][buf] is not None:  # the step two back has read this staging buffer
                 cin.wait_event(st["q_free"][buf])
-            qd[0:1].copy_(q_host[0:1], non_blocking=True)
-            ev_q0.record(cin)
-            qd[1:].copy_(q_host[1:], non_blocking=True)
+            qd.copy_(q_host, non_blocking=True)
             ev_q.record(cin)
         if st["o_free"][buf] is not None:  # ... and its outputs have left this staging buffer
             ms.wait_event(st["o_free"][buf])
-        for l in range(L):
-            if l == 0:
-                ms.wait_event(ev_q0)
-            elif l == 1:
-                ms.wait_event(ev_q)
-            self.decode(qd[l:l + 1], splits=splits, out=od[l:l + 1], scale=scale, layer=l, pdl=l > 1)
-            if (l + 1) % d2h_every == 0 or l == L - 1:
-                lo = (l // d2h_every) * d2h_every
-                ev = torch.cuda.Event()
-                ev.record(ms)
-                cout.wait_event(ev)
-                with torch.cuda.stream(cout):
-                    out_host[lo:l + 1].copy_(od[lo:l + 1], non_blocking=True)
+        ms.wait_event(ev_q)
+        for i, g in enumerate(st["graphs"][buf]):
+            g.replay()
+            lo, hi = i * seg, min(L, (i + 1) * seg)
+            ev = torch.cuda.Event()
+            ev.record(ms)
+            cout.wait_event(ev)
+            with torch.cuda.stream(cout):
+                out_host[lo:hi].copy_(od[lo:hi], non_blocking=True)
         q_free, o_free = torch.cuda.Event(), torch.cuda.Event()
         q_free.record(ms)
         o_free.record(cout)
@@ -279,6 +278,50 @@ class BatchedKVCache:
         if order_current:
             ms.wait_stream(cout)
         return out_host
+
+    def _segment_graphs(self, q, out, seg, splits, scale):
+        """CUDA graphs of layers [i seg, (i+1) seg): per-layer launches, PDL-chained inside a
+        segment, over the fixed staging buffers q / out."""
+        graphs = []
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        for lo in range(0, self.L, seg):
+            hi = min(self.L, lo + seg)
+
+            def run(lo=lo, hi=hi):
+                for l in range(lo, hi):
+                    self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l, pdl=l > lo)
+
+            with torch.cuda.stream(side):
+                run()  # warm-up: workspace, launch attributes
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                run()
+            graphs.append(g)
+        return graphs
+
+    def decode_graph(self, q, out, splits=None, scale=None):
+        """Capture one decode step — every layer as its own PDL-chained launch, as in
+        ``decode(q[l:l+1], layer=l, pdl=l > 0)`` — into a CUDA graph over the fixed device
+        buffers q / out (fp16 [L, B, H*m, 128]).  ``graph.replay()`` runs a step; refill q in
+        place between replays.  The workspace is allocated by an eager warm-up step first."""
+        if q.shape != out.shape or q.shape[0] != self.L:
+            raise ValueError("q and out must be [L, B, H*m, 128] for all layers")
+
+        def step():
+            for l in range(self.L):
+                self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l, pdl=l > 0)
+
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()  # warm-up: workspace, launch attributes
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        return graph
 
     def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None):
         """Unnormalised split-KV partials f32 [L'*B*H*m, 130] = (acc[128], m (log2), l) for q

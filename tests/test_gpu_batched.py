@@ -337,3 +337,25 @@ def test_context_shorter_than_one_chunk():
             ref = O.mixed_decode_attention(q[0, b, h * m:(h + 1) * m].astype(np.float64), oc)
             err = np.max(np.abs(out[0, b, h * m:(h + 1) * m] - ref))
             assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (b, h, err)
+
+
+def test_decode_graph_replay_matches_eager():
+    """decode_graph: the per-layer PDL-chained step captured in a CUDA graph gives the eager
+    launches' output bit for bit, and follows in-place updates of q between replays."""
+    rng = np.random.default_rng(71)
+    L, B, H, m, D, N = 3, 2, 2, 4, 128, 10
+    T = N * 32 + 5
+    k = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    cache = batched.build_cache_batched(k, v, _search_from_tiers(rng.choice([0, 1, 2], size=(B, N)).astype(np.uint8)))
+    q = torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16)).cuda()
+    out = torch.empty_like(q)
+    g = cache.decode_graph(q, out, splits=3)
+    for _ in range(2):
+        g.replay()
+        want = torch.empty_like(q)
+        for l in range(L):
+            cache.decode(q[l:l + 1], splits=3, out=want[l:l + 1], layer=l, pdl=l > 0)
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
+        q.copy_(torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16)))
