@@ -98,7 +98,9 @@ class BatchedKVCache:
         self.k = dict(fp=torch.zeros((L, H, self.rows_fp, HEAD_DIM), dtype=torch.float16, device=dev),
                       span_flags=z32(L, H, self.B), span_max=z32(L, H, self.B))
         self.v = {k: torch.zeros_like(t) for k, t in self.k.items()}
-        self._ws = {}
+        self._ws, self._ws_ptr = {}, {}
+        self._arenas = {}
+        self._any_empty = bool((self.total_tokens() == 0).any())
 
     # -- construction ------------------------------------------------------------------
     @classmethod
@@ -118,7 +120,14 @@ class BatchedKVCache:
     def arena(self, which, layer=0):
         """ckv_arena view starting at `layer` (per-layer launches index layers from there):
         codes/meta pointers into the interleaved tile buffers (K at block offsets 0 / 2x codes,
-        V one code tile / one meta tile further)."""
+        V one code tile / one meta tile further).  Cached: the buffers never move."""
+        key = (which, layer)
+        cached = self._arenas.get(key)
+        if cached is None:
+            cached = self._arenas[key] = self._make_arena(which, layer)
+        return cached
+
+    def _make_arena(self, which, layer):
         t = self.k if which == "k" else self.v
         ptr = lambda x: x.data_ptr() + layer * x.stride(0) * x.element_size()  # noqa: E731
         v = which == "v"
@@ -178,6 +187,10 @@ class BatchedKVCache:
         """Zero-initialised decode workspace (split partials + self-resetting arrival counters).
         Launches covering a single layer get a private per-layer slice, so consecutive
         per-layer launches never share counters (required for programmatic dependent launch)."""
+        wkey = (m, splits, layers, layer)
+        hit = self._ws_ptr.get(wkey)
+        if hit is not None:
+            return hit
         lib = _lib.load()
         if layers == self.L:
             key = (m, splits, "all")
@@ -191,7 +204,8 @@ class BatchedKVCache:
             off = per * layer
         if key not in self._ws:
             self._ws[key] = torch.zeros(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
-        return self._ws[key].data_ptr() + off
+        self._ws_ptr[wkey] = ptr = self._ws[key].data_ptr() + off
+        return ptr
 
     def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False):
         """Mixed-precision decode attention for q fp16 [L', B, H*m, 128] -> fp16 same shape,
@@ -205,7 +219,7 @@ class BatchedKVCache:
             raise ValueError("q shape does not match the cache")
         if q.dtype != torch.float16 or q.stride(3) != 1 or q.stride(2) != HEAD_DIM:
             raise ValueError("q must be fp16 with contiguous heads")
-        if (self.total_tokens() == 0).any():
+        if self._any_empty:
             raise ValueError("cache holds no tokens")  # attention.py:71-72
         m = Hq // self.H
         splits = self.default_splits(m, L) if splits is None else int(splits)
@@ -219,13 +233,14 @@ class BatchedKVCache:
                   _lib.DECODE_PDL if pdl else 0, _lib.stream())
         return out
 
-    def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=16, order_current=True):
+    def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=None, order_current=True):
         """One decode step for all layers from HOST buffers: pinned fp16 q [L, B, H*m, 128] ->
         pinned fp16 output of the same shape.  The q upload runs on its own copy stream (it
         overlaps the previous step's layers); the layers run as CUDA-graph segments of
-        `d2h_every` PDL-chained per-layer launches (captured once per staging buffer, so the
-        host enqueues one replay per segment instead of one launch per layer); each segment's
-        outputs go back on a second copy stream while the next segment computes.  Device
+        `d2h_every` (default: all) PDL-chained per-layer launches (captured once per staging
+        buffer, so the host enqueues one replay per segment instead of one launch per layer);
+        each segment's outputs go back on a second copy stream while the next segment (or, for
+        the last one, the next step) computes.  Device
         staging is double-buffered across steps, so consecutive steps never wait on each
         other's copies.  With ``order_current`` the current stream is ordered after the last
         download on return; without it the downloads stay on the copy stream (they overlap the
@@ -235,7 +250,7 @@ class BatchedKVCache:
             raise ValueError("q shape does not match the cache")
         if out_host.shape != q_host.shape or out_host.dtype != torch.float16:
             raise ValueError("out_host must match q_host")
-        seg = max(1, min(int(d2h_every), L))
+        seg = L if d2h_every is None else max(1, min(int(d2h_every), L))
         key = (tuple(q_host.shape), splits, scale, seg)
         st = getattr(self, "_host_step", None)
         if st is None or st["key"] != key:
@@ -355,6 +370,7 @@ class BatchedKVCache:
         _lib.call("ckv_append_tokens", _lib.ptr(k_new), _lib.ptr(v_new), self.L, self.B, self.H,
                   _lib.ptr(self.seq), self.arena("k"), self.arena("v"), _lib.stream())
         self.seq_host[:, 5] += 1
+        self._any_empty = bool((self.total_tokens() == 0).any())
 
     # -- accounting --------------------------------------------------------------------
     def algorithmic_bytes(self, m):
