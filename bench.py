@@ -393,8 +393,21 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
             cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
                                  out=parts[l * B * Hq:(l + 1) * B * Hq])
 
+    # the 40 PDL-chained decode_partial launches over the resident q buffer, captured once
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        local_decode(q)
+    torch.cuda.current_stream().wait_stream(side)
+    local_graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(local_graph):
+        local_decode(q)
+
     def step(qq):
-        local_decode(qq)
+        if qq is q:
+            local_graph.replay()
+        else:
+            local_decode(qq)
         gathered = distributed.exchange_partials(parts) if world > 1 else parts[None]
         return batched.lse_merge(gathered)
 
@@ -423,7 +436,7 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
         step(q)
     with ClockSampler(local) as clk:
         ms = timed(lambda: step(q), args.steps)
-    ms_local = timed(lambda: local_decode(q), args.steps)
+    ms_local = timed(local_graph.replay, args.steps)
     my_bytes = cache.algorithmic_bytes(m)
     tot = torch.tensor([float(my_bytes)], device=dev, dtype=torch.float64)
     if world > 1:
@@ -434,11 +447,10 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
     # end to end: pinned host q -> device, step, merged output -> pinned host
     qh = q.cpu().pin_memory()
     oh = torch.empty((L * B * Hq, D), dtype=torch.float16, pin_memory=True)
-    qd = torch.empty_like(q)
 
-    def e2e_step():
-        qd.copy_(qh, non_blocking=True)
-        oh.copy_(step(qd), non_blocking=True)
+    def e2e_step():  # the upload lands in the graph's q buffer
+        q.copy_(qh, non_blocking=True)
+        oh.copy_(step(q), non_blocking=True)
 
     for _ in range(3):
         e2e_step()
@@ -456,7 +468,7 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
                                    "sequence split-KV across the GPUs",
                        "global_batch": B, "seq_len": T, "parallelism": f"seq-split x{world}",
                        "tier_fractions_int2_int4_fp16": [round(float(x) / counts.sum(), 4) for x in counts],
-                       "launch": "per-layer decode_partial (40 PDL-chained launches) + all_gather + merge",
+                       "launch": "per-layer decode_partial (40 PDL-chained launches, one CUDA graph) + all_gather + merge",
                        "splits": splits, "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
             "tokens_per_s": round(B / (ms * 1e-3), 1),
             "algorithmic_bytes_per_step": int(step_bytes),
