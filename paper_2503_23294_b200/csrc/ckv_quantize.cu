@@ -47,7 +47,7 @@ __device__ __forceinline__ uint32_t exact_code(float x, float lo, float hi, floa
 }
 
 // Rare path: every element of a slice exactly (IEEE f64, reference tree); out of line so the
-// four quantize_chunk instantiations stay small.
+// quantize_chunk instantiations stay small.
 __device__ __noinline__ uint32_t exact_slice(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
                                              float lo, float hi, float qinv, float qmax, uint32_t base) {
   const uint32_t w[4] = {w0, w1, w2, w3};
@@ -62,14 +62,13 @@ __device__ __noinline__ uint32_t exact_slice(uint32_t w0, uint32_t w1, uint32_t 
   return acc;
 }
 
-// One 8-element lane slice of a row (4 lanes = one 32-element group): group min/max, codes,
-// packed little-endian lane word.  Fast path per element (7 instructions):
-//   r = (x - lo) * (qmax / span)   [x - lo in one mixed f16/f32 add]
-//   y = r + 1.5*2^23               [low mantissa bits = round-half-even(r)]
-//   |r - (y - 1.5*2^23)| > 0.5 - 2^-14  -> exact IEEE f64 recomputation (near a tie)
+// Codes per element, fast path (codes8 below, two elements per packed instruction):
+//   d = x - lo                     [one mixed f16 - f32 subtract]
+//   y = RN(d * qmax / span + 1.5*2^23)   [low mantissa bits = round-half-even]
+//   |d * qmax / span - (y - 1.5*2^23)| > 0.5 - 2^-14  -> exact IEEE f64 recomputation (near a tie)
 //   acc += bits(y) * base^e        [one IMAD; the constant offset is pre-subtracted]
-// The fp32 value of r is within 3.6e-6 of the exact rational, so away from the guard band
-// round-half-even(r) == floor(exact + 0.5) == the reference's f64 result.
+// The fp32 value is within 3.6e-6 of the exact rational, so away from the guard band
+// round-half-even == floor(exact + 0.5) == the reference's f64 result.
 __device__ __forceinline__ uint32_t hmin2_nan(uint32_t a, uint32_t b) {
   uint32_t d;
   asm("min.NaN.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
