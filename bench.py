@@ -668,6 +668,75 @@ def run_cfg1(args, torch, dist, dev, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def run_cfg5(args, torch, dist, dev, rank, world, local):
+    """cfg5 prefill sharded by layer: every rank runs the 128K search (its tier map
+    is the reference's) and reorders / quantizes / packs its 32/N layers x 8 kv heads; no
+    exchange.  Strong scaling of the fixed 32-layer build; max-over-ranks device time."""
+    from paper_2503_23294_b200 import batched, distributed, retrieval
+
+    c = CFG5
+    L, B, H, T, D = c["layers"], c["batch"], c["kv_heads"], c["context"], c["head_dim"]
+    lo, hi = distributed.layer_shard(L, world, rank)
+    Ll = hi - lo
+    wl = load_workload(T, 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77 + rank)
+    k = torch.randn((Ll, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    v = torch.randn((Ll, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
+    s = retrieval.search_batched(wl["emb"][None], wl["norm"][None], wl["q"][None], np.array([wl["qnorm"]]))
+    if not np.array_equal(s.tiers.cpu().numpy()[0], wl["tiers"]):
+        raise SystemExit("128K tier map differs from the reference's")
+    counts = s.seg_counts.cpu().numpy()
+    # search inputs resident on the device like the K/V (the timed region is device work only)
+    dev_emb = [torch.as_tensor(x, device=dev) for x in (wl["emb"][None], wl["norm"][None], wl["q"][None],
+                                                      np.array([wl["qnorm"]]))]
+    cache = batched.BatchedKVCache(Ll, B, H, counts[:, 0], counts[:, 1], counts[:, 2], [T], 0, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    times = []
+    with ClockSampler(local) as clk:
+        for i in range(max(args.warmup, 3) + args.steps):
+            flush.fill_(i & 0xFF)
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            s2 = retrieval.search_batched(*dev_emb, check=False)
+            cache.build(k, v, s2.perm, check=False)
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= max(args.warmup, 3):
+                times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n2, n4, nf = (int(x) for x in counts[0])
+    read = 2 * L * H * T * D * 2
+    write = 2 * L * H * (n2 * 32 * 48 + n4 * 32 * 80 + (nf * 32 + (T - 32 * (n2 + n4 + nf))) * 256)
+    if rank == 0:
+        peak, peak_kind = measured_peak_gbs(sustained=False)
+        per_rank = (read + write) * Ll / L / (ms * 1e-3) / 1e9
+        line = {
+            "metric": "cfg5 prefill search + reorder/quantize/pack GB/s (% HBM peak)",
+            "value": round((read + write) / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
+            "data": "synthetic (fp16 N(0,1) K/V; reference search tier map, 128K seed 0)",
+            "config": {"workload": "cfg5: prefill search + reorder/quantize/pack, 128K ctx x 32 layers x 8 kv heads, b1",
+                       "global_batch": B, "seq_len": T, "parallelism": f"layer-shard x{world}",
+                       "l2": "L2 flushed (256 MB write) before every timed build"},
+            "bytes_read": read, "bytes_written": write,
+            "roofline": {"bound": "hbm", "achieved": round(per_rank, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(per_rank / peak, 4), "peak_kind": peak_kind,
+                         "traffic": profile_traffic("reorder_quantize_pack")},
+            "e2e": None,
+            "gpu_launches": args.steps * 3,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -677,11 +746,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--splits", type=int, default=None)
-    ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4"], default="cfg2",
+    ap.add_argument("--workload", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"], default="cfg2",
                     help="cfg2: batch-sharded 32K GQA decode (default); cfg3: 128K MHA decode with "
                          "sequence split-KV across the ranks (NCCL all-gather + LSE merge); cfg4: "
                          "batch 64 x 16K GQA decode sharded over the ranks (--cfg4-map); cfg1: the "
-                         "4K single-layer MHA parity config (L2-flushed, latency bound)")
+                         "4K single-layer MHA parity config (L2-flushed, latency bound); cfg5: the "
+                         "128K prefill build with its layers sharded over the ranks")
     ap.add_argument("--cfg4-map", choices=["skewed", "all_int2", "all_fp16"], default="skewed")
     args = ap.parse_args()
 
@@ -705,8 +775,8 @@ def main():
         if world > 1:
             dist.barrier()
 
-    if args.workload in ("cfg1", "cfg3", "cfg4"):
-        fn = {"cfg1": run_cfg1, "cfg3": run_cfg3, "cfg4": run_cfg4}[args.workload]
+    if args.workload in ("cfg1", "cfg3", "cfg4", "cfg5"):
+        fn = {"cfg1": run_cfg1, "cfg3": run_cfg3, "cfg4": run_cfg4, "cfg5": run_cfg5}[args.workload]
         fn(args, torch, dist, dev, rank, world, local)
         if world > 1:
             dist.destroy_process_group()

@@ -27,6 +27,13 @@ def batch_shard(batch, world, rank):
     return lo, hi
 
 
+def layer_shard(layers, world, rank):
+    """Contiguous slice of layers built by `rank` (cfg5 prefill sharded by layer, SURVEY §8e:
+    every rank runs the search for the sequence — N bytes of tier map — and quantizes its own
+    layers; no exchange)."""
+    return _split(layers, world, rank)
+
+
 def _split(n, world, rank):
     return rank * n // world, (rank + 1) * n // world
 

@@ -66,3 +66,15 @@ def test_split_kv_exchange_world2(tmp_path):
     cache = O.build_cache(k, v, tiers, 32, 32)
     want = O.reference_attention(q, *O.reconstruct(cache))
     assert np.max(np.abs(got - want)) < 1e-5  # f32 partials
+
+
+def test_layer_and_batch_shards_partition():
+    from paper_2503_23294_b200.distributed import batch_shard, layer_shard
+
+    for n in (1, 7, 32, 40, 64):
+        for world in (1, 2, 3, 4, 8):
+            for fn in (layer_shard, batch_shard):
+                parts = [fn(n, world, r) for r in range(world)]
+                assert parts[0][0] == 0 and parts[-1][1] == n
+                assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+                assert max(b - a for a, b in parts) - min(b - a for a, b in parts) <= 1

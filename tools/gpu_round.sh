@@ -8,6 +8,7 @@ cat gpurun_out/bench.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -1 gpurun_out/bench_ref.json
 timeout 900 python bench.py --workload cfg3 --steps 10 --warmup 3 2>/dev/null | tail -1 > gpurun_out/bench_cfg3.json
 timeout 600 python bench.py --workload cfg1 --steps 30 --warmup 5 2>/dev/null | tail -1 > gpurun_out/bench_cfg1.json
+timeout 600 python bench.py --workload cfg5 --steps 5 --warmup 3 2>/dev/null | tail -1 > gpurun_out/bench_cfg5.json
 for mp in skewed all_int2 all_fp16; do timeout 900 python bench.py --workload cfg4 --cfg4-map $mp --steps 10 --warmup 3 2>/dev/null | tail -1; done > gpurun_out/bench_cfg4.jsonl
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches.csv python tools/profile_step.py --steps 1 --prefill > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:decode_kernel -s 8 -c 1 -o gpurun_out/decode_prof -f python tools/profile_step.py --steps 1 > gpurun_out/ncu_decode.log 2>&1
