@@ -628,22 +628,18 @@ struct TileSrc {
   int64_t c2, c4;
 };
 
-// Warp-wide: stage one quantized tile into the stage whose lane slot is `sl`.  Commits a
-// (possibly empty) group.
-__device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const DecArgs& a,
-                                           const TileSrc& o, const MetaOff& mo, uint32_t sl) {
-  (void)mo;
-  if (t < t_q_end) {
-    if (t < n2t) {
-      const char* p = reinterpret_cast<const char*>(a.K.codes2) + o.c2 + (int64_t)t * kBlock2;
-      cp_async16(sl, p);
-      cp_async16(sl + 512, p + 512);
-      cp_async16(sl + 1024, p + 1024);
-    } else {
-      const char* p = reinterpret_cast<const char*>(a.K.codes4) + o.c4 + (int64_t)(t - n2t) * kBlock4;
-      cp_async16(sl, p);
-      cp_async16(sl + 512, p + 512);
-      cp_async16(sl + 1024, p + 1024);
+// Warp-wide: stage tile t (< n) of one kind's range into the stage whose lane slot is `sl`.
+// Commits a (possibly empty) group.  The INT2 and INT4 ranges run as separate phases, so
+// every issue is of a known kind: one address and 3 / 5 copies, nothing predicated off.
+template <int BITS>
+__device__ __forceinline__ void issue_tile(int t, int n, const DecArgs& a, const TileSrc& o, uint32_t sl) {
+  if (t < n) {
+    const char* p = BITS == 2 ? reinterpret_cast<const char*>(a.K.codes2) + o.c2 + (int64_t)t * kBlock2
+                              : reinterpret_cast<const char*>(a.K.codes4) + o.c4 + (int64_t)t * kBlock4;
+    cp_async16(sl, p);
+    cp_async16(sl + 512, p + 512);
+    cp_async16(sl + 1024, p + 1024);
+    if (BITS == 4) {
       cp_async16(sl + 1536, p + 1536);
       cp_async16(sl + 2048, p + 2048);
     }
@@ -651,13 +647,11 @@ __device__ __forceinline__ void issue_tile(int t, int t_q_end, int n2t, const De
   cp_commit();
 }
 
-// Prologue: put this warp's first kStages-1 quantized tiles in flight.
-__device__ __forceinline__ void prologue(int q_begin, int q_end, int n2t, const DecArgs& a,
-                                         const TileSrc& src, const MetaOff& mo, uint32_t ring_l,
-                                         int warp) {
+// Prologue of a phase: put this warp's first kStages-1 tiles of the range in flight.
+template <int BITS>
+__device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc& src, uint32_t ring_l, int warp) {
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s)
-    issue_tile(q_begin + warp + kDecWarps * s, q_end, n2t, a, src, mo, ring_l + s * kStageBytes);
+  for (int s = 0; s < kStages - 1; ++s) issue_tile<BITS>(warp + kDecWarps * s, n, a, src, ring_l + s * kStageBytes);
 }
 
 // decode modes of a unit: normal; precise K (wide span x |q|, m <= 4); exact (scales or q
@@ -674,59 +668,46 @@ __device__ __forceinline__ void qk4(uint32_t sl, const MetaOff& mo, const Precis
   if (MODE == kModePrecise) qk_precise<4>(sl, mo, po, qs, mg, s);
   else qk_int4<MODE == kModeExact>(sl, mo, qs, mg, s);
 }
-template <int MODE>
-__device__ __forceinline__ void qk_any(bool int2, uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
-  if (int2) qk2<MODE>(sl, mo, po, qs, mg, s);
-  else qk4<MODE>(sl, mo, po, qs, mg, s);
-}
-template <bool EXACT>
-__device__ __forceinline__ void pv_any(bool int2, uint32_t sl, const MetaOff& mo, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
-  if (int2) pv_int2<EXACT>(sl, mo, mg, st, bp0, bp1);
-  else pv_int4<EXACT>(sl, mo, mg, st, bp0, bp1);
-}
-
-// The tile loops of one warp: quantized tiles [q_begin, q_end) through the cp.async ring
-// (prologue already issued), software-pipelined so that q.K^T of tile i+1 and P.V of tile i
-// form one straight-line block (independent MMA chains the scheduler can interleave); then
-// FP16-region tiles [f_begin, f_end).
-template <int MODE>
-__device__ __forceinline__ void run_tiles(int q_begin, int q_end, int n2t, const DecArgs& a,
-                                          const TileSrc& src, const MetaOff& mo, const PreciseOff& po,
-                                          uint32_t ring_l, const QS& qs, uint32_t mg, WarpState& st,
-                                          int warp) {
+// The tile loop of one warp over one kind's range [0, n) (tiles warp, warp + 4, ...) through
+// the cp.async ring (prologue already issued), software-pipelined so that q.K^T of tile i+1
+// and P.V of tile i form one straight-line block (independent MMA chains the scheduler can
+// interleave).
+template <int MODE, int BITS>
+__device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc& src, const MetaOff& mo,
+                                          const PreciseOff& po, uint32_t ring_l, const QS& qs, uint32_t mg,
+                                          WarpState& st, int warp) {
   constexpr bool EXACT = MODE == kModeExact;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
-  int t = q_begin + warp;
-  if (t < q_end) {
+  int t = warp;
+  if (t < n) {
     uint32_t cur = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
     cp_wait<kStages - 2>();
     __syncwarp();
     float s0[4];
-    qk_any<MODE>(t < n2t, cur, mo, po, qs, mg, s0);
+    if (BITS == 2) qk2<MODE>(cur, mo, po, qs, mg, s0);
+    else qk4<MODE>(cur, mo, po, qs, mg, s0);
     uint32_t bp0, bp1;
     softmax_tile<EXACT>(s0, st, bp0, bp1);
     while (true) {
       const int tn = t + kDecWarps;
-      issue_tile(t + kDecWarps * (kStages - 1), q_end, n2t, a, src, mo, put);
+      issue_tile<BITS>(t + kDecWarps * (kStages - 1), n, a, src, put);
       put = next(put);
-      if (tn >= q_end) {
-        pv_any<EXACT>(t < n2t, cur, mo, mg, st, bp0, bp1);
+      if (tn >= n) {
+        if (BITS == 2) pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
+        else pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
         break;
       }
       cp_wait<kStages - 2>();
       __syncwarp();
       const uint32_t nx = next(cur);
       float sn[4];
-      if (tn < n2t) {  // both INT2 (tn > t)
+      if (BITS == 2) {
         qk2<MODE>(nx, mo, po, qs, mg, sn);
         pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
-      } else if (t >= n2t) {  // both INT4
+      } else {
         qk4<MODE>(nx, mo, po, qs, mg, sn);
         pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
-      } else {  // INT2 -> INT4 boundary
-        qk4<MODE>(nx, mo, po, qs, mg, sn);
-        pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
       }
       __syncwarp();  // slot `cur` may be refilled from now on
       softmax_tile<EXACT>(sn, st, bp0, bp1);
@@ -735,6 +716,22 @@ __device__ __forceinline__ void run_tiles(int q_begin, int q_end, int n2t, const
     }
   }
   cp_wait<0>();
+}
+
+// Both phases of a CTA's quantized tiles: INT2 (its prologue issued before the PDL wait), then
+// INT4 (prologue here, or before the wait when the CTA has no INT2 tiles).
+template <int MODE>
+__device__ __forceinline__ void quantized_tiles(int n2, int n4, const DecArgs& a, const TileSrc& src,
+                                                const MetaOff& mo, const PreciseOff& po, uint32_t ring_l,
+                                                const QS& qs, uint32_t mg, WarpState& st, int warp) {
+  if (n2 > 0) {
+    run_tiles<MODE, 2>(n2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    if (n4 > 0) {
+      __syncwarp();
+      prologue<4>(n4, a, src, ring_l, warp);
+    }
+  }
+  if (n4 > 0) run_tiles<MODE, 4>(n4, a, src, mo, po, ring_l, qs, mg, st, warp);
 }
 
 // This CTA's share of its unit's FP16-region tiles (FP16-tier chunks, tail, decode tokens),
@@ -786,7 +783,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     const int n2t = s0.y / kTile, n4t = s0.w / kTile;
     const int a2 = (int)((int64_t)n2t * id.split / a.splits), b2 = (int)((int64_t)n2t * (id.split + 1) / a.splits);
     const int a4 = (int)((int64_t)n4t * id.split / a.splits), b4 = (int)((int64_t)n4t * (id.split + 1) / a.splits);
-    cnt2 = b2 - a2;  // local tiles [0, cnt2) are INT2, [cnt2, nloc) INT4
+    cnt2 = b2 - a2;  // INT2 tiles [0, cnt2) of this CTA, then INT4 tiles [0, nloc - cnt2)
     nloc = cnt2 + (b4 - a4);
     const int64_t unit = (int64_t)id.l * a.H + id.h;
     const int64_t r2 = s0.x + (int64_t)a2 * kTile, r4 = s0.z + (int64_t)a4 * kTile;  // first rows
@@ -797,7 +794,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   mo.k = -8 * lane;
   mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
-  prologue(0, nloc, cnt2, a, src, mo, ring_l, warp);
+  if (cnt2 > 0) prologue<2>(cnt2, a, src, ring_l, warp);
+  else prologue<4>(nloc, a, src, ring_l, warp);
 
   // Everything above touched only build-time data.  q, the FP16 region and len_fp may come
   // from the preceding kernel on the stream: wait for it (no-op without PDL), and let the next
@@ -907,11 +905,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.lsum[0] = st.lsum[1] = 0.f;
 
   if (mode == kModeExact) {
-    run_tiles<kModeExact>(0, nloc, cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    quantized_tiles<kModeExact>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
     fp16_tiles<true>(a, qs, st);
   } else {
-    if (mode == kModePrecise) run_tiles<kModePrecise>(0, nloc, cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
-    else run_tiles<kModeNormal>(0, nloc, cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    if (mode == kModePrecise) quantized_tiles<kModePrecise>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    else quantized_tiles<kModeNormal>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
     fp16_tiles<false>(a, qs, st);
     // undo the V m-tile weights 2^(2(mt&3) - 6)
 #pragma unroll
