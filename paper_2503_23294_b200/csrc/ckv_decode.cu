@@ -628,14 +628,17 @@ struct TileSrc {
   int64_t c2, c4;
 };
 
-// Warp-wide: stage tile t (< n) of one kind's range into the stage whose lane slot is `sl`.
+// Warp-wide: stage tile t (< n) of one kind's range (tile 0 at `base`) into the stage whose lane slot is `sl`.
 // Commits a (possibly empty) group.  The INT2 and INT4 ranges run as separate phases, so
 // every issue is of a known kind: one address and 3 / 5 copies, nothing predicated off.
 template <int BITS>
-__device__ __forceinline__ void issue_tile(int t, int n, const DecArgs& a, const TileSrc& o, uint32_t sl) {
+__device__ __forceinline__ const char* tile_base(const DecArgs& a, const TileSrc& o) {
+  return BITS == 2 ? reinterpret_cast<const char*>(a.K.codes2) + o.c2 : reinterpret_cast<const char*>(a.K.codes4) + o.c4;
+}
+template <int BITS>
+__device__ __forceinline__ void issue_at(int t, int n, const char* base, uint32_t sl) {
   if (t < n) {
-    const char* p = BITS == 2 ? reinterpret_cast<const char*>(a.K.codes2) + o.c2 + (int64_t)t * kBlock2
-                              : reinterpret_cast<const char*>(a.K.codes4) + o.c4 + (int64_t)t * kBlock4;
+    const char* p = base + (int64_t)t * (BITS == 2 ? kBlock2 : kBlock4);
     cp_async16(sl, p);
     cp_async16(sl + 512, p + 512);
     cp_async16(sl + 1024, p + 1024);
@@ -650,8 +653,9 @@ __device__ __forceinline__ void issue_tile(int t, int n, const DecArgs& a, const
 // Prologue of a phase: put this warp's first kStages-1 tiles of the range in flight.
 template <int BITS>
 __device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc& src, uint32_t ring_l, int warp) {
+  const char* base = tile_base<BITS>(a, src);
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue_tile<BITS>(warp + kDecWarps * s, n, a, src, ring_l + s * kStageBytes);
+  for (int s = 0; s < kStages - 1; ++s) issue_at<BITS>(warp + kDecWarps * s, n, base, ring_l + s * kStageBytes);
 }
 
 // decode modes of a unit: normal; precise K (wide span x |q|, m <= 4); exact (scales or q
@@ -680,6 +684,10 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
   int t = warp;
+  constexpr int64_t kStep = (int64_t)kDecWarps * (BITS == 2 ? kBlock2 : kBlock4);
+  // address of the next tile to issue (kStages-1 ahead of the one consumed), advanced by one
+  // warp stride per iteration: a loop-carried pointer instead of base + t * block each time
+  const char* pn = tile_base<BITS>(a, src) + (int64_t)(warp + kDecWarps * (kStages - 1)) * (kStep / kDecWarps);
   if (t < n) {
     uint32_t cur = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
     cp_wait<kStages - 2>();
@@ -691,7 +699,8 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
     softmax_tile<EXACT>(s0, st, bp0, bp1);
     while (true) {
       const int tn = t + kDecWarps;
-      issue_tile<BITS>(t + kDecWarps * (kStages - 1), n, a, src, put);
+      issue_at<BITS>(t + kDecWarps * (kStages - 1) < n ? 0 : 1, 1, pn, put);
+      pn += kStep;
       put = next(put);
       if (tn >= n) {
         if (BITS == 2) pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
