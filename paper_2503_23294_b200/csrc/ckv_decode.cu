@@ -701,7 +701,6 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
       const int tn = t + kDecWarps;
       issue_at<BITS>(t + kDecWarps * (kStages - 1) < n ? 0 : 1, 1, pn, put);
       pn += kStep;
-      put = next(put);
       if (tn >= n) {
         if (BITS == 2) pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
         else pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
@@ -720,6 +719,7 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
       }
       __syncwarp();  // slot `cur` may be refilled from now on
       softmax_tile<EXACT>(sn, st, bp0, bp1);
+      put = cur;  // the refill slot trails the consumed one by a full ring (kStages - 1 ahead)
       cur = nx;
       t = tn;
     }
