@@ -210,9 +210,11 @@ __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint3
   // Lazy online softmax: keep the running max unless a score exceeds it by more than the
   // threshold (then P <= 2^8 still fits fp16).  Only then reduce the tile max across the
   // 8 row-groups and rescale; the common case needs no shuffles.
-  float t0 = fmaxf(s[0], s[2]), t1 = fmaxf(s[1], s[3]);
-  const bool need = (t0 > st.mrun[0] + kRescaleThresh) || (t1 > st.mrun[1] + kRescaleThresh);
+  // scores relative to the running max (the exp2 arguments; the threshold test reuses them)
+  float d0 = s[0] - st.mrun[0], d1 = s[1] - st.mrun[1], d2 = s[2] - st.mrun[0], d3 = s[3] - st.mrun[1];
+  const bool need = (fmaxf(d0, d2) > kRescaleThresh) || (fmaxf(d1, d3) > kRescaleThresh);
   if (__any_sync(0xffffffffu, need)) {
+    float t0 = fmaxf(s[0], s[2]), t1 = fmaxf(s[1], s[3]);
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
       t0 = fmaxf(t0, __shfl_xor_sync(0xffffffffu, t0, o));
@@ -229,9 +231,9 @@ __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint3
     st.lsq[0] *= f0; st.lsq[1] *= f1;
     st.lsum[0] *= f0; st.lsum[1] *= f1;
     st.mrun[0] = n0; st.mrun[1] = n1;
+    d0 = s[0] - n0; d1 = s[1] - n1; d2 = s[2] - n0; d3 = s[3] - n1;
   }
-  const float p0 = fast_exp2(s[0] - st.mrun[0]), p1 = fast_exp2(s[1] - st.mrun[1]);
-  const float p2 = fast_exp2(s[2] - st.mrun[0]), p3 = fast_exp2(s[3] - st.mrun[1]);
+  const float p0 = fast_exp2(d0), p1 = fast_exp2(d1), p2 = fast_exp2(d2), p3 = fast_exp2(d3);
   if (FADD_SUM) {  // else the lo MMA of the tile's P.V sums P (rows g+8 of its A are ones)
     st.lsum[0] += p0 + p2;
     st.lsum[1] += p1 + p3;
