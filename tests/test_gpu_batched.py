@@ -359,3 +359,25 @@ def test_decode_graph_replay_matches_eager():
         torch.cuda.synchronize()
         assert torch.equal(out, want)
         q.copy_(torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16)))
+
+
+def test_decode_graph_sees_decode_appends():
+    """A captured decode step keeps working across decode-token appends: the graph's launches
+    read the sequence table (len_fp) on the device, so replays attend over the new tokens."""
+    rng = np.random.default_rng(72)
+    L, B, H, m, D, N = 2, 2, 2, 4, 128, 6
+    T = N * 32 + 3
+    k = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    cache = batched.build_cache_batched(k, v, _search_from_tiers(rng.choice([0, 1, 2], size=(B, N)).astype(np.uint8)),
+                                        decode_capacity=16)
+    q = torch.from_numpy(rng.normal(size=(L, B, H * m, D)).astype(np.float16)).cuda()
+    out = torch.empty_like(q)
+    g = cache.decode_graph(q, out, splits=2)
+    for _ in range(5):
+        cache.append(torch.from_numpy(rng.normal(size=(L, B, H, D)).astype(np.float16)).cuda(),
+                     torch.from_numpy(rng.normal(size=(L, B, H, D)).astype(np.float16)).cuda())
+        g.replay()
+        want = cache.decode(q, splits=2)
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
