@@ -85,7 +85,7 @@ __device__ __forceinline__ uint32_t prmt_q(uint32_t a, uint32_t b, uint32_t sel)
   return d;
 }
 
-// packed fp32x2 arithmetic (sm_100: FADD2 / FFMA2, two lanes of f32 per instruction)
+// packed fp32x2 arithmetic (sm_100: FFMA2, two lanes of f32 per instruction)
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
   uint64_t r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
@@ -93,11 +93,6 @@ __device__ __forceinline__ uint64_t f2pack(float a, float b) {
 }
 __device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
 }
 __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   uint64_t r;
