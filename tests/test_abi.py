@@ -138,3 +138,26 @@ def test_sequence_shard_cache_layout_partitions_the_context(world):
         assert sorted(seen[b]) == list(range(N))
     assert rows.tolist() == [int(counts[:, 0].sum()) * 32, int(counts[:, 1].sum()) * 32,
                              int(counts[:, 2].sum()) * 32 + B * tail]
+
+
+def test_product_path_fails_loudly_without_gpu_or_library():
+    """No CPU fallback: without a visible CUDA device the public API raises instead of
+    computing, and a missing libckv.so is an error at load time (not a silent substitute)."""
+    import subprocess
+    import sys
+
+    import numpy as np
+    import torch
+
+    import paper_2503_23294_b200 as P
+
+    if not torch.cuda.is_available():
+        with pytest.raises(RuntimeError, match="CUDA"):
+            P.quantize(np.ones((2, 4)), 4, group_size=4)
+        with pytest.raises(RuntimeError, match="CUDA"):
+            P.HashedBowEncoder().encode("a b c")
+    code = ("import os; os.environ['CKV_LIB_PATH'] = '/nonexistent/libckv.so'\n"
+            "from paper_2503_23294_b200 import _lib\n"
+            "try:\n    _lib.load()\nexcept RuntimeError as e:\n    print('raised', 'missing' in str(e))\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=_build.ROOT)
+    assert "raised True" in out.stdout, out.stdout + out.stderr
