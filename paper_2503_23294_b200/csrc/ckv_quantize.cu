@@ -204,6 +204,11 @@ template <int BITS, bool ISV> struct MetaStageOff {
 // lane covers the reference's 8-element slices j = 2 jj, 2 jj + 1 of StageOff.  Row r of the
 // chunk sits at StageOff's (r4, u, sub) = ((r >> 3) << 2, (r >> 1) & 3, r & 1).  Returns
 // whether a group's scale needs the decode's wide-scale mode.
+// L2 prefetch of the line holding p (no registers held; the demand load a step later hits L2)
+__device__ __forceinline__ void l2_prefetch(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // After a chunk half: non-finite input anywhere (its span max is inf or nan) and the decode's
 // wide-scale test (some group scale span / qmax above 4000).
 __device__ __forceinline__ bool chunk_flags(float smax, float qmax, bool& bad) {
@@ -235,6 +240,7 @@ __device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int64_t sT
       const uint4* p = srow + (int64_t)(16 * h) * sT / 8 + 4 * it;
       xs[2 * h] = __ldg(p);
       xs[2 * h + 1] = __ldg(p + 2);
+      if (it == 0) l2_prefetch(p + 8);  // the row's second 128-byte line (steps 2, 3)
     }
     const int j0 = 4 * it + hg, j1 = j0 + 2;
 #pragma unroll
@@ -283,6 +289,7 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
       const uint4* p = srow + (int64_t)(2 * it + 16 * h) * sT / 8;
       xs[2 * h] = __ldg(p);
       xs[2 * h + 1] = __ldg(p + 1);
+      if (it < 3) l2_prefetch(p + 2 * sT / 8);  // this lane's piece of the next step's row
     }
     const int tq = it * SO::U;
     const int tm = it * MO::U;
