@@ -209,6 +209,18 @@ __device__ __forceinline__ void l2_prefetch(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// 32-bit shared-memory stores (staging addresses are 32-bit shared-window offsets: no 64-bit
+// generic pointer arithmetic in the quantize loops)
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t v0, uint32_t v1) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v0), "r"(v1) : "memory");
+}
+
 // After a chunk half: non-finite input anywhere (its span max is inf or nan) and the decode's
 // wide-scale test (some group scale span / qmax above 4000).
 __device__ __forceinline__ bool chunk_flags(float smax, float qmax, bool& bad) {
@@ -223,15 +235,14 @@ __device__ __forceinline__ bool chunk_flags(float smax, float qmax, bool& bad) {
 // 8-element slices j = 4 it + hg and 4 it + 2 + hg (each load instruction reads a row's 32
 // contiguous bytes with the lane pair).
 template <int BITS>
-__device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int64_t sT, int lane,
-                                                 unsigned char* sc, unsigned char* sm, bool& bad,
-                                                 float& smax) {
+__device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int sT, int lane,
+                                                 uint32_t sc, uint32_t sm, bool& bad, float& smax) {
   using SO = StageOff<BITS, true>;
   using MO = MetaStageOff<BITS, true>;
   const int rr = lane >> 1, hg = lane & 1, sub = rr & 1;
-  const int rowc = ((rr >> 3) & 1) * SO::X + ((rr >> 1) & 3) * SO::U;
-  const int rowm = ((rr >> 3) & 1) * MO::X + ((rr >> 1) & 3) * MO::U;
-  const uint4* srow = reinterpret_cast<const uint4*>(src + rr * sT) + hg;
+  const uint32_t cb = sc + ((rr >> 3) & 1) * SO::X + ((rr >> 1) & 3) * SO::U + SO::lane(hg, sub);
+  const uint32_t mbase = sm + ((rr >> 3) & 1) * MO::X + ((rr >> 1) & 3) * MO::U + MO::lane(0, sub);
+  const uint4* srow = reinterpret_cast<const uint4*>(src + (int64_t)rr * sT) + hg;
 #pragma unroll 1
   for (int it = 0; it < 4; ++it) {  // group it, rows rr and rr + 16
     uint4 xs[4];
@@ -242,45 +253,43 @@ __device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int64_t sT
       xs[2 * h + 1] = __ldg(p + 2);
       if (it == 0) l2_prefetch(p + 8);  // the row's second 128-byte line (steps 2, 3)
     }
-    const int j0 = 4 * it + hg, j1 = j0 + 2;
+    // slices j0 = 4 it + hg and j0 + 2: SO::lane(j, sub) = SO::lane(j mod 2, sub) + (j / 2) * 64
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
                              xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
       uint32_t c[2], meta;
       quantize_slice16<BITS>(w, c, meta, smax);
-      unsigned char* c0 = sc + h * SO::TB + rowc + SO::lane(j0, sub);
-      unsigned char* c1 = sc + h * SO::TB + rowc + SO::lane(j1, sub);
-      *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
-      *reinterpret_cast<uint16_t*>(c1) = (uint16_t)c[1];
+      const uint32_t c0 = cb + h * SO::TB + it * 128, c1 = c0 + 64;
+      sts16(c0, c[0]);
+      sts16(c1, c[1]);
       if (BITS == 4) {
-        *reinterpret_cast<uint16_t*>(c0 + 4) = (uint16_t)(c[0] >> 16);
-        *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
+        sts16(c0 + 4, c[0] >> 16);
+        sts16(c1 + 4, c[1] >> 16);
       }
       // both lanes of the group hold the same (lo, hi): duplicate stores, no branch
-      unsigned char* mb = sm + h * MO::TB + rowm + MO::lane(j0, sub);
-      *reinterpret_cast<uint16_t*>(mb) = (uint16_t)meta;
-      *reinterpret_cast<uint16_t*>(mb + 4) = (uint16_t)(meta >> 16);
+      const uint32_t mb = mbase + h * MO::TB + it * 64;
+      sts16(mb, meta);
+      sts16(mb + 4, meta >> 16);
     }
   }
   return chunk_flags(smax, BITS == 2 ? 3.0f : 15.0f, bad);
 }
 
 template <int BITS, bool ISV>
-__device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, int lane,
-                                               unsigned char* sc, unsigned char* sm, bool& bad,
-                                               float& smax) {
+__device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int sT, int lane, uint32_t sc, uint32_t sm,
+                                               bool& bad, float& smax) {
   if (ISV) return quantize_chunk_v<BITS>(src, sT, lane, sc, sm, bad, smax);
   using SO = StageOff<BITS, ISV>;
   using MO = MetaStageOff<BITS, ISV>;
   const int rs = lane >> 3, jj = lane & 7;
   const int sub = rs & 1, j0 = 2 * jj;
-  // per-lane parts of the two slices' code offsets and the group's metadata offset: the
-  // lane's rows differ from its step's first row in bits 0 and 3 (sub, X), which keeps the
-  // K stores of a warp in distinct banks (bits 1-2 (U) would alias them)
-  const int lc0 = SO::lane(j0, sub) + (rs >> 1) * SO::X, lc1 = SO::lane(j0 + 1, sub) + (rs >> 1) * SO::X;
-  const int lm = MO::lane(j0, sub) + (rs >> 1) * MO::X;
-  const uint4* srow = reinterpret_cast<const uint4*>(src + (sub + 8 * (rs >> 1)) * sT) + 2 * jj;
+  // per-lane parts of the code and metadata offsets: the lane's rows differ from its step's
+  // first row in bits 0 and 3 (sub, X), which keeps the K stores of a warp in distinct banks
+  // (bits 1-2 (U) would alias them)
+  const uint32_t cb = sc + SO::lane(j0, sub) + (rs >> 1) * SO::X;
+  const uint32_t mbase = sm + MO::lane(j0, sub) + (rs >> 1) * MO::X;
+  const uint4* srow = reinterpret_cast<const uint4*>(src + (int64_t)(sub + 8 * (rs >> 1)) * sT) + 2 * jj;
 #pragma unroll 1
   for (int it = 0; it < 4; ++it) {  // rows 2 it + 16 h + sub + 8 (rs >> 1)
     uint4 xs[4];
@@ -291,32 +300,18 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int64_t sT, 
       xs[2 * h + 1] = __ldg(p + 1);
       if (it < 3) l2_prefetch(p + 2 * sT / 8);  // this lane's piece of the next step's row
     }
-    const int tq = it * SO::U;
-    const int tm = it * MO::U;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
                              xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
       uint32_t c[2], meta;
       quantize_slice16<BITS>(w, c, meta, smax);
-      unsigned char* c0 = sc + tq + h * SO::TB + lc0;
-      if (!ISV) {  // K: the two slices' 16-bit pieces are adjacent (SO::lane(j0 + 1) = + 2)
-        if (BITS == 2) {
-          *reinterpret_cast<uint32_t*>(c0) = prmt_q(c[0], c[1], 0x5410);
-        } else {
-          *reinterpret_cast<uint2*>(c0) = make_uint2(prmt_q(c[0], c[1], 0x5410), prmt_q(c[0], c[1], 0x7632));
-        }
-      } else {
-        unsigned char* c1 = sc + tq + h * SO::TB + lc1;
-        *reinterpret_cast<uint16_t*>(c0) = (uint16_t)c[0];
-        *reinterpret_cast<uint16_t*>(c1) = (uint16_t)c[1];
-        if (BITS == 4) {
-          *reinterpret_cast<uint16_t*>(c0 + 4) = (uint16_t)(c[0] >> 16);
-          *reinterpret_cast<uint16_t*>(c1 + 4) = (uint16_t)(c[1] >> 16);
-        }
-      }
+      // the two slices' 16-bit pieces are adjacent (SO::lane(j0 + 1) = + 2)
+      const uint32_t c0 = cb + h * SO::TB + it * SO::U;
+      if (BITS == 2) sts32(c0, prmt_q(c[0], c[1], 0x5410));
+      else sts64(c0, prmt_q(c[0], c[1], 0x5410), prmt_q(c[0], c[1], 0x7632));
       // both lanes of the group hold the same (lo, hi): duplicate stores, no branch
-      *reinterpret_cast<uint32_t*>(sm + tm + h * MO::TB + lm) = meta;
+      sts32(mbase + h * MO::TB + it * MO::U, meta);
     }
   }
   return chunk_flags(smax, BITS == 2 ? 3.0f : 15.0f, bad);
@@ -410,14 +405,15 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       continue;
     }
     const int code_bytes = t.tier == 0 ? kTileBytes2 : kTileBytes4;
-    unsigned char* sc = s_blk[warp] + (tsel ? code_bytes : 0);
-    unsigned char* sm = s_blk[warp] + 2 * code_bytes + (tsel ? kTileBytesMeta : 0);
+    const uint32_t sblk = (uint32_t)__cvta_generic_to_shared(s_blk[warp]);
+    const uint32_t sc = sblk + (tsel ? code_bytes : 0);
+    const uint32_t sm = sblk + 2 * code_bytes + (tsel ? kTileBytesMeta : 0);
     bool wide;
     float smax = 0.0f;  // largest group span of the chunk (decode precision routing)
-    if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, sT, lane, sc, sm, bad, smax)
-                                 : quantize_chunk<2, false>(src, sT, lane, sc, sm, bad, smax);
-    else wide = tsel ? quantize_chunk<4, true>(src, sT, lane, sc, sm, bad, smax)
-                     : quantize_chunk<4, false>(src, sT, lane, sc, sm, bad, smax);
+    if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, (int)sT, lane, sc, sm, bad, smax)
+                                 : quantize_chunk<2, false>(src, (int)sT, lane, sc, sm, bad, smax);
+    else wide = tsel ? quantize_chunk<4, true>(src, (int)sT, lane, sc, sm, bad, smax)
+                     : quantize_chunk<4, false>(src, (int)sT, lane, sc, sm, bad, smax);
     __syncwarp();
     const QTask t2 = read_task(task_addr);
     const CtaPos c2 = cta_pos(B);
@@ -522,6 +518,7 @@ int32_t ckv_reorder_quantize_pack(const uint16_t* k, const uint16_t* v, int32_t 
   if (layers < 0 || batch < 0 || kv_heads < 0 || max_chunks < 0 || max_ctx < 0) return CKV_ERR_ARG;
   if (!k || !v || !seq || !flag) return CKV_ERR_ARG;
   if ((s_token % 8) || (s_head % 8) || (s_batch % 8) || (s_layer % 8)) return CKV_ERR_UNSUPPORTED;
+  if (s_token <= 0 || s_token > INT32_MAX) return CKV_ERR_UNSUPPORTED;  // the kernel's row stride is 32-bit
   if (layers == 0 || batch == 0 || kv_heads == 0) return CKV_OK;
   const int slots = (int)(cdiv(max_ctx, kChunk)) + 1;
   dim3 grid((unsigned)cdiv(slots, kQWarps), (unsigned)kv_heads, (unsigned)(layers * batch));
