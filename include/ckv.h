@@ -192,7 +192,8 @@ typedef struct ckv_arena {
 
 /* (2) Chunk-level reorder + quantize + pack (kv_store.build_cache, kv_store.py:169-219 with
  * quantizer.quantize / kernels.quantize_groups / pack_codes).  One pass over fp16 K and V:
- *   k, v fp16 element strides (layer, batch, token, head); head_dim contiguous.
+ *   k, v fp16 element strides (layer, batch, token, head), all multiples of 8 (16-byte rows);
+ *   head_dim contiguous; 0 < s_token <= INT32_MAX (CKV_ERR_UNSUPPORTED otherwise).
  *   perm u32[B, max_chunks] (from ckv_search), seq i32[B][8].
  * Writes codes/meta to the INT arenas and verbatim rows to the FP16 region (FP16-tier
  * chunks, then the context tail).  Sets CKV_FLAG_NONFINITE on inf/nan input. */
