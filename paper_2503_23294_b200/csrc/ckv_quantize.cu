@@ -405,15 +405,20 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       continue;
     }
     const int code_bytes = t.tier == 0 ? kTileBytes2 : kTileBytes4;
-    const uint32_t sblk = (uint32_t)__cvta_generic_to_shared(s_blk[warp]);
+    // thread coordinates re-read here (volatile): hoisted out of the pass loop, the addresses
+    // derived from them would be spilled to local memory at 64 registers
+    uint32_t tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    const int lane_v = (int)(tid & 31);
+    const uint32_t sblk = (uint32_t)__cvta_generic_to_shared(s_blk[tid >> 5]);
     const uint32_t sc = sblk + (tsel ? code_bytes : 0);
     const uint32_t sm = sblk + 2 * code_bytes + (tsel ? kTileBytesMeta : 0);
     bool wide;
     float smax = 0.0f;  // largest group span of the chunk (decode precision routing)
-    if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, (int)sT, lane, sc, sm, bad, smax)
-                                 : quantize_chunk<2, false>(src, (int)sT, lane, sc, sm, bad, smax);
-    else wide = tsel ? quantize_chunk<4, true>(src, (int)sT, lane, sc, sm, bad, smax)
-                     : quantize_chunk<4, false>(src, (int)sT, lane, sc, sm, bad, smax);
+    if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, (int)sT, lane_v, sc, sm, bad, smax)
+                                 : quantize_chunk<2, false>(src, (int)sT, lane_v, sc, sm, bad, smax);
+    else wide = tsel ? quantize_chunk<4, true>(src, (int)sT, lane_v, sc, sm, bad, smax)
+                     : quantize_chunk<4, false>(src, (int)sT, lane_v, sc, sm, bad, smax);
     __syncwarp();
     const QTask t2 = read_task(task_addr);
     const CtaPos c2 = cta_pos(B);
