@@ -42,6 +42,9 @@ BYTES_INT4 = 2 * (64 + 16)
 BYTES_FP16 = 2 * 256
 
 
+MAX_Q_PER_KV = 8  # q rows per kv head in one decode launch (the MMA's N columns)
+
+
 def _round_up(x, m):
     return -(-x // m) * m
 
@@ -222,9 +225,19 @@ class BatchedKVCache:
         if self._any_empty:
             raise ValueError("cache holds no tokens")  # attention.py:71-72
         m = Hq // self.H
-        splits = self.default_splits(m, L) if splits is None else int(splits)
         if out is None:
             out = torch.empty((L, B, Hq, D), dtype=torch.float16, device=q.device)
+        if m > MAX_Q_PER_KV:
+            # more q heads per kv head than one CTA's MMA columns hold: groups of <= 8 rows,
+            # each a separate launch over the same cache (K/V read once per group)
+            qv, ov = q.view(L, B, self.H, m, D), out.view(L, B, self.H, m, D)
+            for r0 in range(0, m, MAX_Q_PER_KV):
+                r1 = min(m, r0 + MAX_Q_PER_KV)
+                og = self.decode(qv[:, :, :, r0:r1].reshape(L, B, self.H * (r1 - r0), D),
+                                 splits=splits, scale=scale, layer=layer, pdl=False)
+                ov[:, :, :, r0:r1] = og.view(L, B, self.H, r1 - r0, D)
+            return out
+        splits = self.default_splits(m, L) if splits is None else int(splits)
         ws = self._workspace(m, splits, L, layer)
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
         _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1),

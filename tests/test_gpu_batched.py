@@ -381,3 +381,21 @@ def test_decode_graph_sees_decode_appends():
         want = cache.decode(q, splits=2)
         torch.cuda.synchronize()
         assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("m", [12, 16])
+def test_decode_more_than_eight_q_heads_per_kv_head(m):
+    """GQA ratios above 8 (q rows per kv head beyond one launch's MMA columns) run as groups
+    of <= 8 rows over the same cache."""
+    rng = np.random.default_rng(80 + m)
+    L, B, H, D, N = 1, 2, 2, 128, 9
+    T = N * 32 + 4
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    tiers = rng.choice([0, 1, 2], size=(B, N)).astype(np.uint8)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search_from_tiers(tiers))
+    q = rng.normal(size=(L, B, H * m, D)).astype(np.float16)
+    out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            _check_unit(cache, 0, b, h, k, v, tiers[b], q[0, b, h * m:(h + 1) * m], out[0, b, h * m:(h + 1) * m])
