@@ -729,21 +729,25 @@ template <int MODE>
 __device__ __forceinline__ void quantized_tiles(int n2, int n4, const DecArgs& a, const TileSrc& src,
                                                 const MetaOff& mo, const PreciseOff& po, uint32_t ring_l,
                                                 const QS& qs, uint32_t mg, WarpState& st, int warp) {
+  // the INT4 phase starts at the warp after the one that took the last INT2 tile, so every
+  // warp's tile count over both phases is within one of the others' (the CTA's warps meet at
+  // the merge barrier)
+  const int w4 = (warp - n2) & (kDecWarps - 1);
   if (n2 > 0) {
     run_tiles<MODE, 2>(n2, a, src, mo, po, ring_l, qs, mg, st, warp);
     if (n4 > 0) {
       __syncwarp();
-      prologue<4>(n4, a, src, ring_l, warp);
+      prologue<4>(n4, a, src, ring_l, w4);
     }
   }
-  if (n4 > 0) run_tiles<MODE, 4>(n4, a, src, mo, po, ring_l, qs, mg, st, warp);
+  if (n4 > 0) run_tiles<MODE, 4>(n4, a, src, mo, po, ring_l, qs, mg, st, w4);
 }
 
 // This CTA's share of its unit's FP16-region tiles (FP16-tier chunks, tail, decode tokens),
 // interleaved over the warps; pointers and ranges re-derived here (len_fp may have grown by
 // decode appends: read after the programmatic-dependent-launch wait).
 template <bool EXACT>
-__device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpState& st) {
+__device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpState& st, int nq) {
   // thread coordinates re-read here (volatile): values carried from the kernel's start would be
   // spilled across the tile loop and reloaded in every iteration of this one
   uint32_t tid;
@@ -758,7 +762,8 @@ __device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpS
   const int64_t unit = (int64_t)id.l * a.H + id.h;
   const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
   const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
-  for (int tf = f_begin + warp; tf < f_end; tf += kDecWarps) {
+  // continue the quantized phases' rotation over the warps (nq quantized tiles before)
+  for (int tf = f_begin + ((warp - nq) & (kDecWarps - 1)); tf < f_end; tf += kDecWarps) {
     const int r = tf * kTile;
     tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
   }
@@ -911,11 +916,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
 
   if (mode == kModeExact) {
     quantized_tiles<kModeExact>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
-    fp16_tiles<true>(a, qs, st);
+    fp16_tiles<true>(a, qs, st, nloc);
   } else {
     if (mode == kModePrecise) quantized_tiles<kModePrecise>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
     else quantized_tiles<kModeNormal>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
-    fp16_tiles<false>(a, qs, st);
+    fp16_tiles<false>(a, qs, st, nloc);
     // undo the V m-tile weights 2^(2(mt&3) - 6)
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
