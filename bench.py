@@ -753,6 +753,10 @@ def main():
                          "4K single-layer MHA parity config (L2-flushed, latency bound); cfg5: the "
                          "128K prefill build with its layers sharded over the ranks")
     ap.add_argument("--cfg4-map", choices=["skewed", "all_int2", "all_fp16"], default="skewed")
+    ap.add_argument("--chains", type=int, default=1,
+                    help="micro-batch chains per decode step (cfg2/cfg4): the batch is split into this "
+                         "many sequence ranges, each its own chain of per-layer launches on its own "
+                         "stream, so one range's layer boundary overlaps the others' work")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -789,13 +793,14 @@ def main():
     out = torch.empty_like(q)
     step_bytes = cache.algorithmic_bytes(m)
 
-    def eager_step():
-        for l in range(L):  # per-layer launches; layer l+1 overlaps its K/V prefetch with layer l
-            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
+    chain_streams = [torch.cuda.Stream(device=dev) for _ in range(args.chains)]
+
+    def eager_step():  # per-layer launches; layer l+1 overlaps its K/V prefetch with layer l
+        cache._launch_layers(q, out, 0, L, splits, None, args.chains, chain_streams)
 
     # the same 32 PDL-chained launches captured once in a CUDA graph (a serving loop's decode
     # step); the eager figure is reported beside it
-    graph = cache.decode_graph(q, out, splits=splits)
+    graph = cache.decode_graph(q, out, splits=splits, chains=args.chains)
     step = graph.replay
     for _ in range(max(args.warmup, 3)):
         step()
@@ -826,13 +831,13 @@ def main():
     qh = q.cpu().pin_memory()
     oh = torch.empty(q.shape, dtype=torch.float16, pin_memory=True)
     for _ in range(3):
-        cache.decode_step_host(qh, oh, splits=splits, order_current=False)
+        cache.decode_step_host(qh, oh, splits=splits, order_current=False, chains=args.chains)
     torch.cuda.synchronize()
     barrier()
     e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e4.record()
     for _ in range(args.steps):  # a step's downloads overlap the next step's first layers
-        cache.decode_step_host(qh, oh, splits=splits, order_current=False)
+        cache.decode_step_host(qh, oh, splits=splits, order_current=False, chains=args.chains)
     torch.cuda.current_stream().wait_event(cache.host_step_ready)  # the last download is timed
     e5.record()
     torch.cuda.synchronize()

@@ -251,6 +251,17 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
                              float scale, int32_t splits, void* workspace, uint16_t* out,
                              int64_t o_s_layer, int64_t o_s_batch, float* partial_out,
                              int32_t flags, void* stream);
+/* The same over sequences [seq_begin, seq_begin + seq_count) of the cache's `batch` only
+ * (q, out, partial_out and the workspace keep their full-batch layout; a launch touches only
+ * its sequences' rows and counters, so launches over disjoint sequence ranges may run
+ * concurrently on different streams, e.g. two micro-batch chains of per-layer launches whose
+ * layer boundaries overlap each other's work). */
+int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                                  ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                                  int32_t layers, int32_t batch, int32_t seq_begin, int32_t seq_count,
+                                  int32_t kv_heads, int32_t m, float scale, int32_t splits,
+                                  void* workspace, uint16_t* out, int64_t o_s_layer, int64_t o_s_batch,
+                                  float* partial_out, int32_t flags, void* stream);
 
 /* Split-KV merge across ranks (new; the NCCL-exchanged partials of SURVEY §8e):
  * partials f32 [P][rows][128 + 2] = (acc[128] unnormalised at m, m (log2 domain), l);

@@ -34,13 +34,16 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in _inputs())
 
 
-def build(force=False, verbose=False):
-    """Compile every .cu under csrc/ into _lib/libckv.so (sm_100a)."""
-    if not force and not needs_build():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile every .cu under csrc/ into _lib/libckv.so (sm_100a).  `out` / `defines` build a
+    tuning variant elsewhere (e.g. -DCKV_DEC_MIN_CTAS=4), loaded through CKV_LIB_PATH."""
+    out = out or OUT
+    if out == OUT and not defines and not force and not needs_build():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *sources()]
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           "-o", out + ".tmp", *sources()]
     if verbose:
         print(" ".join(cmd))
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -48,8 +51,8 @@ def build(force=False, verbose=False):
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     if verbose and res.stderr:
         print(res.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -78,6 +78,8 @@ _SIGNATURES = {
     "ckv_decode_ctas_per_sm": ([], _i32),
     "ckv_decode_attention": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _f32, _i32,
                               _vp, _vp, _i64, _i64, _vp, _i32, _vp], _i32),
+    "ckv_decode_attention_seqs": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
+                                   _f32, _i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp], _i32),
     "ckv_lse_merge": ([_vp, _i32, _i64, _vp, _vp], _i32),
 }
 

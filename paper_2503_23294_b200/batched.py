@@ -210,13 +210,15 @@ class BatchedKVCache:
         self._ws_ptr[wkey] = ptr = self._ws[key].data_ptr() + off
         return ptr
 
-    def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False):
+    def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False, seqs=None):
         """Mixed-precision decode attention for q fp16 [L', B, H*m, 128] -> fp16 same shape,
         over layers [layer, layer + L') of the cache (L' = L for the whole model in one launch,
         1 for the per-layer launches of a real decode step).  pdl=True launches as a
         programmatic dependent of the previous kernel on the stream; use it only when that
         kernel was itself a decode of this cache (it overlaps this launch's K/V prefetch with
-        the previous launch's tail)."""
+        the previous launch's tail).  seqs=(b0, b1) computes sequences [b0, b1) only (q / out
+        keep the full batch; the other rows of out are left untouched), so disjoint sequence
+        ranges can run as concurrent micro-batch chains."""
         L, B, Hq, D = q.shape
         if B != self.B or layer < 0 or layer + L > self.L or D != HEAD_DIM or Hq % self.H:
             raise ValueError("q shape does not match the cache")
@@ -224,29 +226,36 @@ class BatchedKVCache:
             raise ValueError("q must be fp16 with contiguous heads")
         if self._any_empty:
             raise ValueError("cache holds no tokens")  # attention.py:71-72
+        b0, b1 = (0, B) if seqs is None else (int(seqs[0]), int(seqs[1]))
+        if not 0 <= b0 <= b1 <= B:
+            raise ValueError("seqs must be a range inside the batch")
         m = Hq // self.H
         if out is None:
             out = torch.empty((L, B, Hq, D), dtype=torch.float16, device=q.device)
+        elif (out.shape != q.shape or out.dtype != torch.float16 or out.device != q.device
+              or out.stride(3) != 1 or out.stride(2) != HEAD_DIM):
+            raise ValueError("out must be fp16 [L', B, H*m, 128] with contiguous heads on q's device")
         if m > MAX_Q_PER_KV:
             # more q heads per kv head than one CTA's MMA columns hold: groups of <= 8 rows,
             # each a separate launch over the same cache (K/V read once per group)
-            qv, ov = q.view(L, B, self.H, m, D), out.view(L, B, self.H, m, D)
+            qv = q.view(L, B, self.H, m, D)
             for r0 in range(0, m, MAX_Q_PER_KV):
                 r1 = min(m, r0 + MAX_Q_PER_KV)
                 og = self.decode(qv[:, :, :, r0:r1].reshape(L, B, self.H * (r1 - r0), D),
-                                 splits=splits, scale=scale, layer=layer, pdl=False)
-                ov[:, :, :, r0:r1] = og.view(L, B, self.H, r1 - r0, D)
+                                 splits=splits, scale=scale, layer=layer, pdl=False, seqs=(b0, b1))
+                out.view(L, B, self.H, m, D)[:, b0:b1, :, r0:r1] = og.view(L, B, self.H, r1 - r0, D)[:, b0:b1]
             return out
         splits = self.default_splits(m, L) if splits is None else int(splits)
         ws = self._workspace(m, splits, L, layer)
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
-        _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1),
-                  self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H,
-                  m, scale, splits, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
+        _lib.call("ckv_decode_attention_seqs", _lib.ptr(q), q.stride(0), q.stride(1),
+                  self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, b0, b1 - b0,
+                  self.H, m, scale, splits, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
                   _lib.DECODE_PDL if pdl else 0, _lib.stream())
         return out
 
-    def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=None, order_current=True):
+    def decode_step_host(self, q_host, out_host, splits=None, scale=None, d2h_every=None, order_current=True,
+                         chains=1):
         """One decode step for all layers from HOST buffers: pinned fp16 q [L, B, H*m, 128] ->
         pinned fp16 output of the same shape.  The q upload runs on its own copy stream (it
         overlaps the previous step's layers); the layers run as CUDA-graph segments of
@@ -264,7 +273,7 @@ class BatchedKVCache:
         if out_host.shape != q_host.shape or out_host.dtype != torch.float16:
             raise ValueError("out_host must match q_host")
         seg = L if d2h_every is None else max(1, min(int(d2h_every), L))
-        key = (tuple(q_host.shape), splits, scale, seg)
+        key = (tuple(q_host.shape), splits, scale, seg, chains)
         st = getattr(self, "_host_step", None)
         if st is None or st["key"] != key:
             dev = self.device
@@ -274,7 +283,7 @@ class BatchedKVCache:
                       cin=torch.cuda.Stream(device=dev), cout=torch.cuda.Stream(device=dev),
                       q_free=[None, None], o_free=[None, None], i=0, graphs=[None, None])
             for b in range(2):
-                st["graphs"][b] = self._segment_graphs(st["q"][b], st["o"][b], seg, splits, scale)
+                st["graphs"][b] = self._segment_graphs(st["q"][b], st["o"][b], seg, splits, scale, chains)
             self._host_step = st
         ms = torch.cuda.current_stream()
         cin, cout = st["cin"], st["cout"]
@@ -307,49 +316,59 @@ class BatchedKVCache:
             ms.wait_stream(cout)
         return out_host
 
-    def _segment_graphs(self, q, out, seg, splits, scale):
+    def _chain_ranges(self, chains):
+        chains = max(1, min(int(chains), self.B))
+        return [(c * self.B // chains, (c + 1) * self.B // chains) for c in range(chains)]
+
+    def _launch_layers(self, q, out, lo, hi, splits, scale, chains, streams):
+        """Per-layer launches of layers [lo, hi): one PDL chain per micro-batch (sequence range),
+        each on its own stream forked from (and joined back into) the current stream."""
+        ranges = self._chain_ranges(chains)
+        if len(ranges) == 1:
+            for l in range(lo, hi):
+                self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l, pdl=l > lo)
+            return
+        cur = torch.cuda.current_stream()
+        for st in streams:
+            st.wait_stream(cur)
+        for (b0, b1), st in zip(ranges, streams):
+            with torch.cuda.stream(st):
+                for l in range(lo, hi):
+                    self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l,
+                                pdl=l > lo, seqs=(b0, b1))
+        for st in streams:
+            cur.wait_stream(st)
+
+    def _segment_graphs(self, q, out, seg, splits, scale, chains=1):
         """CUDA graphs of layers [i seg, (i+1) seg): per-layer launches, PDL-chained inside a
-        segment, over the fixed staging buffers q / out."""
+        segment (one chain per micro-batch), over the fixed staging buffers q / out."""
         graphs = []
         side = torch.cuda.Stream(device=self.device)
+        streams = [torch.cuda.Stream(device=self.device) for _ in self._chain_ranges(chains)]
         side.wait_stream(torch.cuda.current_stream())
         for lo in range(0, self.L, seg):
             hi = min(self.L, lo + seg)
-
-            def run(lo=lo, hi=hi):
-                for l in range(lo, hi):
-                    self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l, pdl=l > lo)
-
-            with torch.cuda.stream(side):
-                run()  # warm-up: workspace, launch attributes
+            with torch.cuda.stream(side):  # warm-up: workspace, launch attributes
+                self._launch_layers(q, out, lo, hi, splits, scale, chains, streams)
             torch.cuda.current_stream().wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                run()
+                self._launch_layers(q, out, lo, hi, splits, scale, chains, streams)
             graphs.append(g)
         return graphs
 
-    def decode_graph(self, q, out, splits=None, scale=None):
+    def decode_graph(self, q, out, splits=None, scale=None, chains=1):
         """Capture one decode step — every layer as its own PDL-chained launch, as in
         ``decode(q[l:l+1], layer=l, pdl=l > 0)`` — into a CUDA graph over the fixed device
         buffers q / out (fp16 [L, B, H*m, 128]).  ``graph.replay()`` runs a step; refill q in
-        place between replays.  The workspace is allocated by an eager warm-up step first."""
+        place between replays.  chains > 1 splits the batch into that many micro-batches, each
+        its own chain of per-layer launches on its own stream inside the graph: a sequence's
+        layer l+1 still waits for its layer l, but one micro-batch's layer boundary (the tail
+        of layer l and the ramp of layer l+1) overlaps the other micro-batches' work.  The
+        workspace is allocated by an eager warm-up step first."""
         if q.shape != out.shape or q.shape[0] != self.L:
             raise ValueError("q and out must be [L, B, H*m, 128] for all layers")
-
-        def step():
-            for l in range(self.L):
-                self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l, pdl=l > 0)
-
-        side = torch.cuda.Stream(device=self.device)
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            step()  # warm-up: workspace, launch attributes
-        torch.cuda.current_stream().wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step()
-        return graph
+        return self._segment_graphs(q, out, self.L, splits, scale, chains)[0]
 
     def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None):
         """Unnormalised split-KV partials f32 [L'*B*H*m, 130] = (acc[128], m (log2), l) for q

@@ -33,11 +33,26 @@ namespace ckv {
 
 constexpr int kDecWarps = 4;
 constexpr int kTile = 16;
-constexpr int kStages = 4;
-// A stage holds one 16-token tile of the tile-native arenas verbatim (see the tile functions
-// below): INT2 1536 B, INT4 2560 B.
-constexpr int kStageBytes = 2560;
-constexpr int kDynSmem = kDecWarps * kStages * kStageBytes;  // 40 KB per CTA
+// Per-warp cp.async ring.  A stage holds one 16-token tile of the tile-native arenas verbatim
+// (see the tile functions below): INT2 1536 B, INT4 2560 B.  The INT2 and INT4 phases reuse
+// the same per-warp region, each with its own stage count.
+#ifndef CKV_DEC_MIN_CTAS
+#define CKV_DEC_MIN_CTAS 4
+#endif
+#ifndef CKV_DEC_STAGES2
+#define CKV_DEC_STAGES2 4
+#endif
+#ifndef CKV_DEC_STAGES4
+#define CKV_DEC_STAGES4 4
+#endif
+constexpr int kMinCtas = CKV_DEC_MIN_CTAS;
+template <int BITS> struct Ring {
+  static constexpr int stages = BITS == 2 ? CKV_DEC_STAGES2 : CKV_DEC_STAGES4;
+  static constexpr int bytes = BITS == 2 ? 1536 : 2560;
+};
+constexpr int kWarpRing = Ring<2>::stages * Ring<2>::bytes > Ring<4>::stages * Ring<4>::bytes
+                              ? Ring<2>::stages * Ring<2>::bytes : Ring<4>::stages * Ring<4>::bytes;
+constexpr int kDynSmem = kDecWarps * kWarpRing;  // 40 KB per CTA (4 x 2560 B per warp)
 constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l (partial_out / cross-rank format)
 constexpr int kWsStride = kHeadDim + 4;    // split workspace rows: acc[128], m, l, pad (16-B rows)
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
@@ -48,6 +63,7 @@ struct DecArgs {
   ckv_arena K, V;
   const int32_t* seq;
   int L, B, H, m, splits;
+  int b0, Bc;           // this launch's sequences [b0, b0 + Bc) of the B in the cache
   float scale_log2;
   float* ws;            // [L*B*H*m][splits][130] partials
   uint32_t* counters;   // [L*B*H] arrival counters (self-resetting)
@@ -82,12 +98,12 @@ __device__ __forceinline__ uint32_t smid() {
 struct CtaIds {
   int split, h, l, b;
 };
-__device__ __forceinline__ CtaIds cta_ids(int B) {
+__device__ __forceinline__ CtaIds cta_ids(int Bc, int b0) {
   uint32_t x, y, z;
   asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(x));
   asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(y));
   asm volatile("mov.u32 %0, %%ctaid.z;" : "=r"(z));
-  return CtaIds{(int)x, (int)y, (int)z / B, (int)z % B};
+  return CtaIds{(int)x, (int)y, (int)z / Bc, b0 + (int)z % Bc};
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -651,7 +667,7 @@ template <int BITS>
 __device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc& src, uint32_t ring_l, int warp) {
   const char* base = tile_base<BITS>(a, src);
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue_at<BITS>(warp + kDecWarps * s, n, base, ring_l + s * kStageBytes);
+  for (int s = 0; s < Ring<BITS>::stages - 1; ++s) issue_at<BITS>(warp + kDecWarps * s, n, base, ring_l + s * Ring<BITS>::bytes);
 }
 
 // decode modes of a unit: normal; precise K (wide span x |q|, m <= 4); exact (scales or q
@@ -677,6 +693,7 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
                                           const PreciseOff& po, uint32_t ring_l, const QS& qs, uint32_t mg,
                                           WarpState& st, int warp) {
   constexpr bool EXACT = MODE == kModeExact;
+  constexpr int kStages = Ring<BITS>::stages, kStageBytes = Ring<BITS>::bytes;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
   int t = warp;
@@ -753,7 +770,7 @@ __device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpS
   uint32_t tid;
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
   const int warp = (int)(tid >> 5), g = (int)((tid & 31) >> 2), c = (int)(tid & 3);
-  const CtaIds id = cta_ids(a.B);
+  const CtaIds id = cta_ids(a.Bc, a.b0);
   const int off_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 4];
   const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 5];
   const int nft = (len_fp + kTile - 1) / kTile;
@@ -769,9 +786,9 @@ __device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpS
   }
 }
 
-__global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs a) {
-  extern __shared__ __align__(128) unsigned char s_dyn[];  // ring: [warp][stage][kStageBytes]
-  unsigned char (*s_ring)[kStages][kStageBytes] = reinterpret_cast<unsigned char (*)[kStages][kStageBytes]>(s_dyn);
+__global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const DecArgs a) {
+  extern __shared__ __align__(128) unsigned char s_dyn[];  // ring: [warp][kWarpRing]
+  unsigned char (*s_ring)[kWarpRing] = reinterpret_cast<unsigned char (*)[kWarpRing]>(s_dyn);
   __shared__ float s_ml[kDecWarps][8][2];
   __shared__ __align__(16) unsigned char s_q[kQBytes];
   __shared__ int s_last;
@@ -788,7 +805,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   int cnt2, nloc;
   TileSrc src;  // tile-native arenas: a row range starting at a tile is contiguous bytes
   {
-    const CtaIds id = cta_ids(a.B);
+    const CtaIds id = cta_ids(a.Bc, a.b0);
     const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * id.b];
     const int n2t = s0.y / kTile, n4t = s0.w / kTile;
     const int a2 = (int)((int64_t)n2t * id.split / a.splits), b2 = (int)((int64_t)n2t * (id.split + 1) / a.splits);
@@ -803,13 +820,23 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   MetaOff mo;
   mo.k = -8 * lane;
   mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
-  const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0][0]) + 16 * lane;
+  const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0]) + 16 * lane;
   if (cnt2 > 0) prologue<2>(cnt2, a, src, ring_l, warp);
   else prologue<4>(nloc, a, src, ring_l, warp);
 
   // Everything above touched only build-time data.  q, the FP16 region and len_fp may come
   // from the preceding kernel on the stream: wait for it (no-op without PDL), and let the next
   // decode launch (next layer) start its own prologue as soon as SMs free up.
+  // the unit's span bounds are build-time data too: read them before the wait
+  bool span_wide;
+  float kspan;
+  {
+    const CtaIds id = cta_ids(a.Bc, a.b0);
+    const int64_t fidx = ((int64_t)id.l * a.H + id.h) * a.B + id.b;  // span flags are [L][H][B]
+    span_wide = (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
+                (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
+    kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
@@ -820,7 +847,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   // bias constants instead of sets 0 and 1), warp 3 the zero-point entry.
   int mode;
   {
-    const CtaIds id = cta_ids(a.B);
+    const CtaIds id = cta_ids(a.Bc, a.b0);
     const int l = id.l, b = id.b, h = id.h;
     const uint16_t* qbase = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m) * kHeadDim + 32 * c;
     auto load_q = [&](int row, float (&qv)[32]) {
@@ -849,10 +876,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
     for (int e = 0; e < 32; ++e) qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) qmaxabs = fmaxf(qmaxabs, __shfl_xor_sync(0xffffffffu, qmaxabs, o));
-    const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // span flags are [L][H][B]
-    const bool wide = qmaxabs > kWideQ || (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
-                      (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
-    const float kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
+    const bool wide = qmaxabs > kWideQ || span_wide;
     mode = wide ? kModeExact
                 : (a.m <= 4 && kspan * qmaxabs > kPreciseSpanQ ? kModePrecise : kModeNormal);
     // slot weights 2^(6-j) of K pair i: INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1)
@@ -945,7 +969,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   st.lsum[1] += st.lsq[1];
   __syncthreads();  // ring -> merge buffer reuse
   if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
-  float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0][0]);
+  float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0]);
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
     s_acc[warp][2 * c][16 * g + mt] = st.acc[mt][0];
@@ -959,7 +983,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   }
   __syncthreads();
   // merge the 4 warps: thread -> d
-  const CtaIds id = cta_ids(a.B);
+  const CtaIds id = cta_ids(a.Bc, a.b0);
   const int split = id.split, h = id.h, l = id.l, b = id.b;
   const int d = threadIdx.x;
   const int hq0 = h * a.m;
@@ -1000,7 +1024,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
       for (int i = 0; i < 5; ++i) dst[i] = s_tr[i];
       for (int i = 8; i < 12; ++i) dst[i] = s_tr[i];
       for (int i = 0; i < kDecWarps; ++i) dst[12 + i] = s_tend[i];
-      dst[5] = smid(); dst[6] = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      // launch position | split << 20 | (sequence * H + kv head) << 40
+      dst[5] = smid();
+      dst[6] = (int64_t)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) | ((int64_t)split << 20) |
+               ((int64_t)(b * a.H + h) << 40);
       dst[7] = (int64_t)a.q;
     }
   };
@@ -1024,7 +1051,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 4) decode_kernel(const DecArgs
   const int64_t row0 = ((int64_t)l * a.B + b) * Hq + hq0;
   const float* p0 = a.ws + row0 * a.splits * kWsStride;
   const int nrows = a.m * a.splits;
-  float* s_part = reinterpret_cast<float*>(&s_ring[0][0][0]);
+  float* s_part = reinterpret_cast<float*>(&s_ring[0][0]);
   if (nrows * kWsStride * (int)sizeof(float) <= kDynSmem) {
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_part);
     const int nvec = nrows * kWsStride / 4;
@@ -1107,12 +1134,24 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
                              float scale, int32_t splits, void* workspace, uint16_t* out,
                              int64_t o_s_layer, int64_t o_s_batch, float* partial_out,
                              int32_t flags, void* stream) {
+  return ckv_decode_attention_seqs(q, q_s_layer, q_s_batch, k_arena, v_arena, seq, layers, batch, 0,
+                                   batch, kv_heads, m, scale, splits, workspace, out, o_s_layer,
+                                   o_s_batch, partial_out, flags, stream);
+}
+
+int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                                  ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                                  int32_t layers, int32_t batch, int32_t seq_begin, int32_t seq_count,
+                                  int32_t kv_heads, int32_t m, float scale, int32_t splits,
+                                  void* workspace, uint16_t* out, int64_t o_s_layer, int64_t o_s_batch,
+                                  float* partial_out, int32_t flags, void* stream) {
   if (layers < 0 || batch < 0 || kv_heads < 0 || splits < 1) return CKV_ERR_ARG;
+  if (seq_begin < 0 || seq_count < 0 || seq_begin + seq_count > batch) return CKV_ERR_ARG;
   if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (!q || !seq || (!out && !partial_out)) return CKV_ERR_ARG;
   if (splits > 1 && !workspace) return CKV_ERR_ARG;
   if ((q_s_layer % 8) || (q_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
-  if (layers * batch * kv_heads == 0) return CKV_OK;
+  if (layers * seq_count * kv_heads == 0) return CKV_OK;
   {  // interleaved K/V tile buffers (include/ckv.h)
     const char* k2 = reinterpret_cast<const char*>(k_arena.codes2);
     const char* k4 = reinterpret_cast<const char*>(k_arena.codes4);
@@ -1130,6 +1169,7 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
   a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
   a.K = k_arena; a.V = v_arena; a.seq = seq;
   a.L = layers; a.B = batch; a.H = kv_heads; a.m = m; a.splits = splits;
+  a.b0 = seq_begin; a.Bc = seq_count;
   a.scale_log2 = scale * 1.4426950408889634f;
   const int64_t units = (int64_t)layers * batch * kv_heads;
   a.counters = reinterpret_cast<uint32_t*>(workspace);
@@ -1141,7 +1181,7 @@ int32_t ckv_decode_attention(const uint16_t* q, int64_t q_s_layer, int64_t q_s_b
   a.zero = 0u;
   if (!ensure_decode_attr()) return CKV_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * batch));
+  cfg.gridDim = dim3((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * seq_count));
   cfg.blockDim = dim3(kDecWarps * 32);
   cfg.dynamicSmemBytes = kDynSmem;
   cfg.stream = as_stream(stream);

@@ -115,7 +115,7 @@ def main():
         x = t[t[:, 7] == p_]
         tt = x[:, 12:16].max(1) - x[:, 2]
         sm = x[:, 5]
-        unit = x[:, 6] // nsplit
+        unit = x[:, 6] >> 40
         cnt = {k: v for k, v in zip(*np.unique(sm, return_counts=True))}
         keep = np.array([cnt[k] == 4 for k in sm])
         tt, sm, unit = tt[keep], sm[keep], unit[keep]
@@ -136,7 +136,7 @@ def main():
         for p_ in launches:
             x = t[t[:, 7] == p_]
             for r in x:
-                idx = int(r[6]); sp = idx % S; b = (idx // (S * H)) % cache.B
+                sp = (int(r[6]) >> 20) & 0xFFFFF; b = (int(r[6]) >> 40) // H
                 f = lambda n: n * (sp + 1) // S - n * sp // S  # noqa: E731
                 X.append([1.0, f(n2t[b]), f(n4t[b]), f(nft[b])])
                 Y.append((r[12:16].max() - r[2]) / 1e3)
@@ -148,7 +148,7 @@ def main():
             x = t[t[:, 7] == p_]
             tt = x[:, 12:16].max(1) - x[:, 2]
             for r, v in zip(x, tt):
-                idx = int(r[6]); b = (idx // (S * H)) % cache.B; h = (idx // S) % H
+                u = int(r[6]) >> 40; b, h = u // H, u % H
                 U[li, b, h] += v / S / 1e3
         U /= U.mean(axis=(1, 2), keepdims=True)
         half = len(launches) // 2
@@ -158,6 +158,16 @@ def main():
         print(np.array2string(U.mean(0), precision=3))
         print("per-layer std of unit means %.3f; layer-to-layer std of a unit %.3f" % (
             U.std(axis=(1, 2)).mean(), U.std(axis=0).mean()))
+        # relative CTA tile time by launch position (bins of 64 positions), median over layers
+        P = []
+        for p_ in launches:
+            x = t[t[:, 7] == p_]
+            tt = x[:, 12:16].max(1) - x[:, 2]
+            P.append((x[:, 6] & 0xFFFFF, tt / np.median(tt)))
+        pos = np.concatenate([a for a, _ in P]); rv = np.concatenate([b for _, b in P])
+        nb = int(pos.max()) // 64 + 1
+        print("relative CTA tile time by launch position / 64:",
+              [round(float(np.mean(rv[pos // 64 == k])), 3) for k in range(nb)])
         print("tile-time model: t0 %.2f us, INT2 %.4f, INT4 %.4f, FP16 %.4f us/tile (per CTA); "
               "ratios INT4/INT2 %.2f FP16/INT2 %.2f; R^2 %.2f" % (
                   coef[0], coef[1], coef[2], coef[3], coef[2] / coef[1], coef[3] / coef[1],
