@@ -13,8 +13,13 @@ kernel against MEASURED_PEAKS.json, an end-to-end figure through the public API 
 buffers, the CPU baseline (oracle restatement of the reference, timed on host cores), and a
 prefill sub-object (cfg5-shaped search + reorder/quantize/pack, 128K x 32 layers x 8 kv heads).
 
-Under torchrun (N>1) every rank owns its own batch of 8 sequences (batch-sharded, weak scaling,
-no data-path collective); time is the max over ranks.
+N>1 (`--gpus N`: re-launches itself under torch.distributed.run when WORLD_SIZE is unset, one
+rank per GPU): every rank owns its own batch of 8 sequences (batch-sharded, weak scaling, no
+data-path collective); time is the max over ranks.  The N>1 line adds a `split_kv` object: cfg3
+(128K, 40 layers x 40 heads) strong-scaled over the same ranks with sequence split-KV (per-layer
+decode_partial launches, one NCCL all_gather of the (acc, m, l) partials, ckv_lse_merge; with
+the local / exchange+merge split of the step time and the latency of one layer's exchange +
+merge) and `head_shard`, the KV-head partition of the same cache (no collective).
 
 --impl reference: the reference's CPU algorithm (oracle port of attention.py:63-90 over
 quantizer.fqm / _numpy.py) on all host cores, same metric, bounded sample per step.
@@ -359,13 +364,19 @@ def bench_text_search(torch, n_chunks, reps=5):
                     "512 of the texts, scaled to all of them (encoding only)"}
 
 
-def run_cfg3(args, torch, dist, dev, rank, world, local):
-    """cfg3: Llama-2-13B shape (40 layers x 40 MHA heads, d128), 128K context, batch 1.  Every
-    rank owns a chunk-aligned 1/N slice of each tier segment (sequence split-KV); a decode step
-    is 40 per-layer decode_partial launches (PDL-chained), one all_gather of all layers'
-    (acc, m, l) partials (NCCL) and the LSE merge.  Strong scaling: the cache is fixed."""
+def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, warmup=None):
+    """cfg3: Llama-2-13B shape (40 layers x 40 MHA heads, d128), 128K context, batch 1, strong
+    scaling of the fixed cache over the ranks (max-over-ranks device time).
+
+    split="seq": sequence split-KV — every rank owns a chunk-aligned 1/N slice of each tier
+    segment; a step is 40 per-layer decode_partial launches (PDL-chained, one CUDA graph), one
+    all_gather of all layers' (acc, m, l) partials (NCCL over NVLink/NVSwitch) and the LSE merge.
+    split="head": KV-head partition — every rank owns 40/N whole heads (all tokens); a step is
+    40 per-layer decode launches; no collective.  Returns a dict of measurements (rank 0)."""
     from paper_2503_23294_b200 import batched, distributed, retrieval
 
+    steps = args.steps if steps is None else steps
+    warmup = max(args.warmup if warmup is None else warmup, 3)
     c = CFG3
     L, B, H, m, T, D = c["layers"], c["batch"], c["kv_heads"], c["q_per_kv"], c["context"], c["head_dim"]
     wl = load_workload(T, 0)
@@ -373,115 +384,186 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
                                       np.array([wl["qnorm"]]), 0.6, 0.1)
     if not np.array_equal(search.tiers.cpu().numpy()[0], wl["tiers"]):
         raise SystemExit("128K tier map differs from the reference's")
-    cache, perm_r = distributed.sequence_shard_cache(search, L, H, [T], world, rank, decode_capacity=128,
-                                                     device=dev)
+    counts = search.seg_counts.cpu().numpy()
+    h0, h1 = distributed.head_shard(H, world, rank) if split == "head" else (0, H)
+    if split == "seq":
+        cache, perm_r = distributed.sequence_shard_cache(search, L, H, [T], world, rank, decode_capacity=128,
+                                                         device=dev)
+    else:
+        cache = batched.BatchedKVCache(L, B, h1 - h0, counts[:, 0], counts[:, 1], counts[:, 2], [T], 128,
+                                       device=dev)
+        perm_r = search.perm
     g = torch.Generator(device=dev)
-    for l in range(L):  # the full context's K/V, one layer at a time (same on every rank)
+    for l in range(L):  # the full context's K/V, one layer at a time (same data on every rank)
         g.manual_seed(4321 + l)
         k = torch.randn((1, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
         v = torch.randn((1, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
-        cache.build(k, v, perm_r, layer=l)
+        cache.build(k[:, :, :, h0:h1], v[:, :, :, h0:h1], perm_r, layer=l)
         del k, v
+    torch.cuda.empty_cache()
     g.manual_seed(99)
-    q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
-    Hq = H * m
-    parts = torch.empty((L * B * Hq, D + 2), dtype=torch.float32, device=dev)
+    q_all = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
+    q = q_all[:, :, h0 * m:h1 * m].contiguous()
+    Hq = (h1 - h0) * m
     splits = args.splits or cache.default_splits(m, 1)
-
-    def local_decode(qq):
-        for l in range(L):
-            cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
-                                 out=parts[l * B * Hq:(l + 1) * B * Hq])
-
-    # the 40 PDL-chained decode_partial launches over the resident q buffer, captured once
-    side = torch.cuda.Stream(device=dev)
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        local_decode(q)
-    torch.cuda.current_stream().wait_stream(side)
-    local_graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(local_graph):
-        local_decode(q)
-
-    def step(qq):
-        if qq is q:
-            local_graph.replay()
-        else:
-            local_decode(qq)
-        gathered = distributed.exchange_partials(parts) if world > 1 else parts[None]
-        return batched.lse_merge(gathered)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    def timed(fn, steps):
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            fn()
-        e1.record()
-        torch.cuda.synchronize()
-        barrier()
-        ms = e0.elapsed_time(e1) / steps
+    def sync_max(ms):
         if world > 1:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
 
-    for _ in range(max(args.warmup, 3)):
-        step(q)
-    with ClockSampler(local) as clk:
-        ms = timed(lambda: step(q), args.steps)
-    ms_local = timed(local_graph.replay, args.steps)
+    def timed(fn, n):
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        return sync_max(e0.elapsed_time(e1) / n)
+
+    res = {}
+    if split == "seq":
+        parts = torch.empty((L * B * Hq, D + 2), dtype=torch.float32, device=dev)
+
+        def local_decode(qq):
+            for l in range(L):
+                cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
+                                     out=parts[l * B * Hq:(l + 1) * B * Hq])
+
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            local_decode(q)
+        torch.cuda.current_stream().wait_stream(side)
+        local_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(local_graph):
+            local_decode(q)
+
+        def step():
+            local_graph.replay()
+            gathered = distributed.exchange_partials(parts) if world > 1 else parts[None]
+            return batched.lse_merge(gathered)
+
+        layer_rows = parts[:B * Hq]
+
+        def layer_merge():  # one layer's exchange + merge (the per-layer latency of SURVEY §7.8)
+            gathered = distributed.exchange_partials(layer_rows) if world > 1 else layer_rows[None]
+            return batched.lse_merge(gathered)
+
+        for _ in range(warmup):
+            step()
+            layer_merge()
+        # one layer's exchange + merge, 20 times in a CUDA graph (NCCL collectives capture), so
+        # the figure is device latency, not Python launch overhead; eager when capture fails
+        merge_fn, merge_reps = layer_merge, 1
+        try:
+            side2 = torch.cuda.Stream(device=dev)
+            side2.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side2):
+                layer_merge()
+            torch.cuda.current_stream().wait_stream(side2)
+            mg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(mg):
+                for _ in range(20):
+                    layer_merge()
+            mg.replay()
+            merge_fn, merge_reps = mg.replay, 20
+        except Exception:  # noqa: BLE001 (gloo test mode: no capture)
+            torch.cuda.synchronize()
+        with ClockSampler(dev.index or 0) as clk:
+            ms = timed(step, steps)
+        res["local_decode_ms"] = round(timed(local_graph.replay, steps), 4)
+        res["exchange_merge_ms"] = round(ms - res["local_decode_ms"], 4)
+        res["per_layer_merge_us"] = round(1e3 * timed(merge_fn, max(steps, 20)) / merge_reps, 2)
+        res["per_layer_merge_note"] = ("one layer's all_gather + ckv_lse_merge, " +
+                                       ("CUDA-graph replayed" if merge_reps > 1 else "eager launches"))
+        out_rows = L * B * Hq
+        e2e_out = step
+    else:
+        out = torch.empty_like(q)
+        graph = cache.decode_graph(q, out, splits=splits)
+        for _ in range(warmup):
+            graph.replay()
+        with ClockSampler(dev.index or 0) as clk:
+            ms = timed(graph.replay, steps)
+        out_rows = L * B * Hq
+
+        def e2e_out():
+            graph.replay()
+            return out
+
     my_bytes = cache.algorithmic_bytes(m)
     tot = torch.tensor([float(my_bytes)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(tot)
     step_bytes = float(tot.item())
-    value = step_bytes / (ms * 1e-3) / 1e9
 
-    # end to end: pinned host q -> device, step, merged output -> pinned host
+    # end to end: pinned host q -> device (this rank's q heads), step, output -> pinned host
     qh = q.cpu().pin_memory()
-    oh = torch.empty((L * B * Hq, D), dtype=torch.float16, pin_memory=True)
+    oh = torch.empty((out_rows, D), dtype=torch.float16, pin_memory=True)
 
-    def e2e_step():  # the upload lands in the graph's q buffer
+    def e2e_step():
         q.copy_(qh, non_blocking=True)
-        oh.copy_(step(q), non_blocking=True)
+        oh.copy_(e2e_out().reshape(out_rows, D), non_blocking=True)
 
     for _ in range(3):
         e2e_step()
-    e2e_ms = timed(e2e_step, args.steps)
+    e2e_ms = timed(e2e_step, steps)
+    counts0 = counts[0]
+    res.update({
+        "value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
+        "tokens_per_s": round(B / (ms * 1e-3), 1), "algorithmic_bytes_per_step": int(step_bytes),
+        "splits": splits, "split": split,
+        "parallelism": f"{'seq-split' if split == 'seq' else 'head-shard'} x{world}",
+        "per_rank_gbs": round(my_bytes / (ms * 1e-3) / 1e9, 1),
+        "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                "h2d_bytes_per_step": int(q.numel() * 2 * world), "d2h_bytes_per_step": int(oh.numel() * 2 * world)},
+        "tier_fractions_int2_int4_fp16": [round(float(x) / counts0.sum(), 4) for x in counts0],
+        "clocks": clk.summary(),
+        "gpu_launches": steps * (L + (1 if split == "seq" else 0)),
+    })
+    del cache
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_cfg3(args, torch, dist, dev, rank, world, local):
+    """cfg3 line: --cfg3-split seq (sequence split-KV, default) or head (KV-head partition)."""
+    r = measure_cfg3(args, torch, dist, dev, rank, world, split=args.cfg3_split)
     if rank == 0:
         peak, peak_kind = measured_peak_gbs()
-        per_rank_gbs = my_bytes / (ms_local * 1e-3) / 1e9
-        counts = search.seg_counts.cpu().numpy()[0]
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
             "data": "synthetic (fp16 N(0,1) K/V/q; reference search tier map, 128K seed 0)",
             "config": {"workload": "cfg3: Llama-2-13B 40 layers x 40 MHA heads d128, 128K ctx, batch 1, "
-                                   "sequence split-KV across the GPUs",
-                       "global_batch": B, "seq_len": T, "parallelism": f"seq-split x{world}",
-                       "tier_fractions_int2_int4_fp16": [round(float(x) / counts.sum(), 4) for x in counts],
-                       "launch": "per-layer decode_partial (40 PDL-chained launches, one CUDA graph) + all_gather + merge",
-                       "splits": splits, "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
-            "tokens_per_s": round(B / (ms * 1e-3), 1),
-            "algorithmic_bytes_per_step": int(step_bytes),
-            "local_decode_ms": round(ms_local, 4),
-            "exchange_merge_ms": round(ms - ms_local, 4),
-            "roofline": {"bound": "hbm", "achieved": round(per_rank_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(per_rank_gbs / peak, 4), "peak_kind": peak_kind,
-                         "traffic": None},
-            "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
-                    "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(oh.numel() * 2)},
-            "gpu_launches": args.steps * (L + 1),
-            "clocks": clk.summary(),
+                                   + ("sequence split-KV across the GPUs" if r["split"] == "seq"
+                                      else "KV heads partitioned across the GPUs"),
+                       "global_batch": CFG3["batch"], "seq_len": CFG3["context"], "parallelism": r["parallelism"],
+                       "tier_fractions_int2_int4_fp16": r["tier_fractions_int2_int4_fp16"],
+                       "launch": ("per-layer decode_partial (40 PDL-chained launches, one CUDA graph) + all_gather "
+                                  "+ merge" if r["split"] == "seq" else
+                                  "per-layer decode (40 PDL-chained launches, one CUDA graph), no collective"),
+                       "splits": r["splits"], "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
+            "tokens_per_s": r["tokens_per_s"],
+            "algorithmic_bytes_per_step": r["algorithmic_bytes_per_step"],
+            "roofline": {"bound": "hbm", "achieved": r["per_rank_gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": round(r["per_rank_gbs"] / peak, 4), "peak_kind": peak_kind, "traffic": None},
+            "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
         }
+        for key in ("local_decode_ms", "exchange_merge_ms", "per_layer_merge_us", "per_layer_merge_note"):
+            if key in r:
+                line[key] = r[key]
         print(json.dumps(line), flush=True)
 
 
@@ -753,15 +835,36 @@ def main():
                          "4K single-layer MHA parity config (L2-flushed, latency bound); cfg5: the "
                          "128K prefill build with its layers sharded over the ranks")
     ap.add_argument("--cfg4-map", choices=["skewed", "all_int2", "all_fp16"], default="skewed")
+    ap.add_argument("--cfg3-split", choices=["seq", "head"], default="seq",
+                    help="cfg3 partition: sequence split-KV with NCCL LSE merge, or whole KV heads per GPU")
+    ap.add_argument("--no-split-kv", action="store_true",
+                    help="N>1 default line: skip the cfg3 split_kv / head_shard sub-objects")
     ap.add_argument("--chains", type=int, default=1,
                     help="micro-batch chains per decode step (cfg2/cfg4): the batch is split into this "
                          "many sequence ranges, each its own chain of per-layer launches on its own "
                          "stream, so one range's layer boundary overlaps the others' work")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched without torchrun: start one rank per GPU ourselves (127.0.0.1 rendezvous)
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus and os.environ.get("CKV_BENCH_SHARE_GPU") != "1":
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {n} GPU(s) visible")
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: WORLD_SIZE {world} != --gpus {args.gpus}; using {world} ranks", file=sys.stderr)
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
@@ -770,10 +873,18 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # CKV_BENCH_SHARE_GPU=1 (test aid): every rank on cuda:0 over gloo, to exercise the N>1
+    # control flow on a one-GPU box (its numbers are not measurements)
+    share = os.environ.get("CKV_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if world > 1:
@@ -869,6 +980,22 @@ def main():
     torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
 
+    split_kv = None
+    if world > 1 and not args.no_split_kv:
+        # cfg3 (128K, 40 layers x 40 heads) on the same ranks: sequence split-KV with the NCCL
+        # exchange + LSE merge, and the KV-head partition beside it (no collective)
+        sk_steps = max(3, min(args.steps, 10))
+        seq = measure_cfg3(args, torch, dist, dev, rank, world, "seq", steps=sk_steps)
+        head = measure_cfg3(args, torch, dist, dev, rank, world, "head", steps=sk_steps)
+        split_kv = {"workload": "cfg3: Llama-2-13B 40 layers x 40 MHA heads d128, 128K ctx, batch 1 (strong scaling)",
+                    "value": seq["value"], "unit": "GB/s", "ms_per_step": seq["ms_per_step"],
+                    "local_decode_ms": seq["local_decode_ms"], "exchange_merge_ms": seq["exchange_merge_ms"],
+                    "per_layer_merge_us": seq["per_layer_merge_us"],
+                    "per_layer_merge_note": seq["per_layer_merge_note"], "splits": seq["splits"],
+                    "parallelism": seq["parallelism"], "e2e": seq["e2e"],
+                    "head_shard": {"value": head["value"], "unit": "GB/s", "ms_per_step": head["ms_per_step"],
+                                   "parallelism": head["parallelism"], "e2e": head["e2e"]}}
+
     prefill = None
     if rank == 0 and world == 1 and not args.no_prefill:
         del cache
@@ -906,6 +1033,8 @@ def main():
         }
         if prefill is not None:
             line["prefill"] = prefill
+        if split_kv is not None:
+            line["split_kv"] = split_kv
         if world == 1 and not args.no_cpu_baseline:
             gbs, n, busy = cpu_baseline(seconds=12.0, processes=1)
             line["cpu_baseline"] = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",

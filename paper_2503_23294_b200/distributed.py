@@ -1,6 +1,9 @@
 """Multi-GPU partitioning of the hot path.  One process per GPU.
 
-* Batch x kv-head sharding (cfg4): independent units, no exchange -> ``batch_shard``.
+* Batch sharding (cfg2/cfg4): independent units, no exchange -> ``batch_shard``.
+* KV-head sharding (cfg3 alternative to split-KV): every rank owns whole kv heads (all
+  layers, all tokens) -> ``head_shard`` / ``build_head_shard``; no exchange either (the
+  q heads of a kv head stay on its rank, as in tensor-parallel attention).
 * Sequence split-KV (cfg3, long contexts): every rank owns a chunk-aligned 1/P slice of
   each tier segment (INT2, INT4 and FP16 chunks separately, so bytes are balanced); the
   last rank also owns the context tail and the decode tokens.  Each rank computes
@@ -25,6 +28,21 @@ def batch_shard(batch, world, rank):
     lo = rank * batch // world
     hi = (rank + 1) * batch // world
     return lo, hi
+
+
+def head_shard(kv_heads, world, rank):
+    """Contiguous slice of kv heads owned by `rank` (head-parallel decode: no collective)."""
+    return _split(kv_heads, world, rank)
+
+
+def build_head_shard(k, v, search, world, rank, decode_capacity=128, check=True):
+    """This rank's BatchedKVCache over its kv heads [lo, hi): k, v fp16 [L, B, T, H, 128] (the
+    full model's K/V or any view holding at least those heads).  Decode it with the matching q
+    heads, q[:, :, lo*m:hi*m]."""
+    L, B, T, H, D = k.shape
+    lo, hi = head_shard(H, world, rank)
+    return BatchedKVCache.from_search(k[:, :, :, lo:hi], v[:, :, :, lo:hi], search,
+                                      decode_capacity=decode_capacity, check=check)
 
 
 def layer_shard(layers, world, rank):
@@ -98,13 +116,21 @@ def build_sequence_shard(k, v, search, world, rank, decode_capacity=128, check=T
 
 
 def exchange_partials(part, group=None):
-    """all_gather of f32 partials [rows, 130] -> [P, rows, 130] (NCCL on GPU, gloo on CPU)."""
+    """all_gather of f32 partials [rows, 130] -> [P, rows, 130] on part's device: NCCL for CUDA
+    tensors (NVLink / NVSwitch), gloo for host tensors; CUDA partials over a gloo group are
+    staged through pinned host memory (e.g. several ranks sharing one GPU in a test)."""
     world = dist.get_world_size(group)
     part = part.contiguous()
+    dev = part.device
+    if dev.type == "cuda" and dist.get_backend(group) == "gloo":
+        part = part.to("cpu")
     out = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype,
                       device=part.device)
-    dist.all_gather_into_tensor(out, part, group=group)
-    return out.view((world,) + tuple(part.shape))
+    if dist.get_backend(group) == "gloo":
+        dist.all_gather(list(out.chunk(world)), part, group=group)
+    else:
+        dist.all_gather_into_tensor(out, part, group=group)
+    return out.view((world,) + tuple(part.shape)).to(dev)
 
 
 def split_kv_decode(cache: BatchedKVCache, q, group=None, splits=None):
@@ -117,5 +143,5 @@ def split_kv_decode(cache: BatchedKVCache, q, group=None, splits=None):
     return out.view(q.shape)
 
 
-__all__ = ["batch_shard", "sequence_shard_plan", "sequence_shard_cache", "build_sequence_shard",
-           "exchange_partials", "split_kv_decode"]
+__all__ = ["batch_shard", "head_shard", "build_head_shard", "layer_shard", "sequence_shard_plan",
+           "sequence_shard_cache", "build_sequence_shard", "exchange_partials", "split_kv_decode"]

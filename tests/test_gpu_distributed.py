@@ -1,0 +1,110 @@
+"""Multi-process GPU paths of distributed.py, run with two ranks that share cuda:0 (gpurun gives
+one GPU): sequence split-KV (real decode_partial partials -> gloo exchange through host memory
+-> ckv_lse_merge) against the unsharded decode and the reference oracle; KV-head sharding
+against the unsharded decode, bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import ckv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_ABS = 1e-2
+TOL_REL = 1e-2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case(seed=41, L=2, B=2, H=2, m=4, N=29, tail=9):
+    rng = np.random.default_rng(seed)
+    T = N * 32 + tail
+    k = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
+    q = rng.normal(size=(L, B, H * m, 128)).astype(np.float16)
+    tiers = rng.choice([0, 0, 0, 1, 2], size=(B, N)).astype(np.uint8)
+    return k, v, q, tiers
+
+
+def _search(tiers):
+    from paper_2503_23294_b200 import retrieval
+
+    # scores that reproduce the given tier map under thresholds (0.5, 1.5)
+    return retrieval.assign_tiers_batched(tiers.astype(np.float64), np.tile([[0.5, 1.5]], (tiers.shape[0], 1)))
+
+
+def _split_kv_worker(rank, world, port, k, v, q, tiers, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_23294_b200 import distributed
+
+        s = _search(tiers)
+        kd, vd, qd = (torch.from_numpy(x).cuda() for x in (k, v, q))
+        cache = distributed.build_sequence_shard(kd, vd, s, world, rank)
+        for splits in (None, 1, 3):  # in-launch split merge on top of the cross-rank merge
+            out = distributed.split_kv_decode(cache, qd, splits=splits)
+            if rank == 0:
+                np.save(out_path + f".{splits}.npy", out.float().cpu().numpy())
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_split_kv_decode_two_processes(tmp_path):
+    """distributed.split_kv_decode across 2 processes: the GPU decode_partial partials of each
+    rank's chunk-aligned slice, exchanged (gloo, host-staged) and merged by ckv_lse_merge, equal
+    the unsharded decode and the reference's f64 attention within the decode tolerance."""
+    from paper_2503_23294_b200 import batched
+
+    k, v, q, tiers = _case()
+    L, B, T, H, D = k.shape
+    m = q.shape[2] // H
+    path = str(tmp_path / "out")
+    mp.spawn(_split_kv_worker, args=(2, _free_port(), k, v, q, tiers, path), nprocs=2, join=True)
+    full = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                                       _search(tiers)).decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
+    for splits in (None, 1, 3):
+        got = np.load(path + f".{splits}.npy")
+        assert np.max(np.abs(got - full)) < 2e-3, splits
+        for l in range(L):
+            for b in range(B):
+                for h in range(H):
+                    oc = O.build_cache(k[l, b, :, h].astype(np.float64), v[l, b, :, h].astype(np.float64),
+                                       tiers[b], 32, 32)
+                    ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+                    err = np.max(np.abs(got[l, b, h * m:(h + 1) * m] - ref))
+                    assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (splits, l, b, h, err)
+
+
+def test_head_shards_equal_unsharded_decode():
+    """KV-head sharding: each rank's cache over its kv heads, decoded with the matching q heads,
+    gives exactly the unsharded decode's rows for those heads (same split count)."""
+    from paper_2503_23294_b200 import batched, distributed
+
+    k, v, q, tiers = _case(seed=43, H=5, N=20)
+    L, B, T, H, D = k.shape
+    m = q.shape[2] // H
+    kd, vd, qd = (torch.from_numpy(x).cuda() for x in (k, v, q))
+    s = _search(tiers)
+    full = batched.build_cache_batched(kd, vd, s).decode(qd, splits=2)
+    for world in (2, 3, 5):
+        for r in range(world):
+            lo, hi = distributed.head_shard(H, world, r)
+            cache = distributed.build_head_shard(kd, vd, s, world, r)
+            out = cache.decode(qd[:, :, lo * m:hi * m].contiguous(), splits=2)
+            assert torch.equal(out, full[:, :, lo * m:hi * m]), (world, r)
