@@ -167,21 +167,22 @@ def profile_traffic(key):
 # ---------------------------------------------------------------------------------------
 # CPU legs (oracle restatement of the reference; test infrastructure used as the baseline)
 
-def _cpu_unit(args):
-    q, k, v, tiers = args
+_CPU_UNITS = []  # prebuilt oracle caches of the CPU legs (inherited by forked pool workers)
+
+
+def _cpu_decode(i):
+    """Decode-only time of prebuilt unit i (the reference's mixed_decode_attention algorithm)."""
     from oracle import ckv_oracle as O
+    q, cache = _CPU_UNITS[i]
     t0 = time.perf_counter()
-    cache = O.build_cache(k, v, tiers, 32, 32)
-    t1 = time.perf_counter()
     O.mixed_decode_attention(q, cache)
-    t2 = time.perf_counter()
-    s = cache
-    nbytes = s.len_2 * 96 + s.len_4 * 160 + s.len_fp * 512 + 2 * q.size * 2
-    return t2 - t1, nbytes
+    t1 = time.perf_counter()
+    nbytes = cache.len_2 * 96 + cache.len_4 * 160 + cache.len_fp * 512 + 2 * q.size * 2
+    return t1 - t0, nbytes
 
 
-def _cpu_sample_units(n_units, ctx, m, rng):
-    from oracle import ckv_oracle as O  # noqa: F401
+def _cpu_build_units(n_units, ctx, m, rng):
+    from oracle import ckv_oracle as O
     units = []
     for u in range(n_units):
         wl = load_workload(32768, u % 8) if ctx == 32768 else None
@@ -189,58 +190,86 @@ def _cpu_sample_units(n_units, ctx, m, rng):
         k = rng.standard_normal((ctx, 128)).astype(np.float16).astype(np.float64)
         v = rng.standard_normal((ctx, 128)).astype(np.float16).astype(np.float64)
         q = rng.standard_normal((m, 128)).astype(np.float16).astype(np.float64)
-        units.append((q, k, v, tiers))
+        units.append((q, O.build_cache(k, v, tiers, 32, 32)))
     return units
 
 
-def cpu_baseline(seconds=12.0, processes=1):
-    """Time the oracle's restatement of mixed_decode_attention on cfg2 units (32K, m=4)."""
-    rng = np.random.default_rng(0)
-    per = 2 if processes == 1 else processes
-    done_bytes, busy, n_done = 0, 0.0, 0
-    t_start = time.perf_counter()
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_kernels():
+    """Select the CPU leg's kernels: the reference's own compiled module (oracle/_ref, built by
+    oracle/Makefile from /root/reference's _core.pyx) when present — kind "reference" — else
+    the oracle's numpy restatement of the reference (kind "port")."""
+    from oracle import ckv_oracle as O, ref_core
+    mod = ref_core.load()
+    O.use_reference_kernels(mod)
+    return ("reference", "chunkkv.kernels._core (compiled reference, -O3 -ffp-contract=off) under the oracle's "
+            "restatement of attention.py") if mod is not None else ("port", "oracle numpy restatement")
+
+
+def cpu_baseline(seconds=12.0, processes=1, n_units=None):
+    """Time the reference algorithm of mixed_decode_attention over cfg2 units (32K, m = 4):
+    units prebuilt (build_cache is outside the timing), then decoded repeatedly — one process,
+    or a fork pool of `processes` workers timed by the pool's wall clock — until `seconds`."""
+    global _CPU_UNITS
+    kind, kernels = cpu_kernels()
+    n_units = n_units or max(2, processes)
+    if len(_CPU_UNITS) < n_units:  # built once per process, reused by later calls
+        _CPU_UNITS = _cpu_build_units(n_units, CFG2["context"], CFG2["q_per_kv"], np.random.default_rng(0))
+    pool = None
     if processes > 1:
         import multiprocessing as mpx
         pool = mpx.get_context("fork").Pool(processes)
-    else:
-        pool = None
-    while time.perf_counter() - t_start < seconds:
-        units = _cpu_sample_units(per, CFG2["context"], CFG2["q_per_kv"], rng)
-        res = pool.map(_cpu_unit, units) if pool else [_cpu_unit(u) for u in units]
-        # decode-only time per unit; with P processes the aggregate rate is P x the per-process
-        # rate (optimistic for the CPU: assumes perfect scaling across cores)
-        busy += sum(r[0] for r in res) / max(processes, 1)
+        pool.map(_cpu_decode, range(n_units))  # warm the workers
+    done_bytes, wall, n_done = 0, 0.0, 0
+    while wall < seconds:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_decode, range(n_units), chunksize=1) if pool else [_cpu_decode(i) for i in range(n_units)]
+        wall += time.perf_counter() - t0
         done_bytes += sum(r[1] for r in res)
         n_done += len(res)
     if pool:
         pool.close()
-    return done_bytes / busy / 1e9, n_done, busy
+        pool.join()
+    return done_bytes / wall / 1e9, n_done, wall, kind, kernels
 
-
-# ---------------------------------------------------------------------------------------
 
 def run_reference_arm(args, rank, world):
-    """--impl reference: the reference's CPU algorithm on all host cores; rank 0 only."""
+    """--impl reference: the reference's CPU implementation on all host cores; rank 0 only."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     steps_gbs = []
+    kind = kernels = None
     for _ in range(args.warmup):
         cpu_baseline(seconds=0.5, processes=cores)
     for _ in range(args.steps):
-        gbs, n, busy = cpu_baseline(seconds=max(2.0, 20.0 / max(args.steps, 1)), processes=cores)
+        gbs, n, wall, kind, kernels = cpu_baseline(seconds=max(2.0, 20.0 / max(args.steps, 1)), processes=cores)
         steps_gbs.append(gbs)
     value = statistics.median(steps_gbs)
-    sample = f"{cores}-process fan-out over cfg2 units (32K ctx, m=4, reference tier maps), per step >= 2 s"
+    sample = (f"{cores}-process fork pool over {cores} prebuilt cfg2 units (32K ctx, m=4, reference tier maps), "
+              f"decode timed by the pool's wall clock, >= 2 s per step; kernels: {kernels}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg2: Llama-3-8B GQA 32q/8kv d128, 32 layers, 32K ctx, batch 8",
-                   "sampled_units": True},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                   "sampled_units": True,
+                   "same_config_note": "per-byte rate over sampled cfg2 units (BASELINE.md section 3 plan); "
+                                       "the full step would take minutes on the CPU"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -837,6 +866,7 @@ def main():
     ap.add_argument("--cfg4-map", choices=["skewed", "all_int2", "all_fp16"], default="skewed")
     ap.add_argument("--cfg3-split", choices=["seq", "head"], default="seq",
                     help="cfg3 partition: sequence split-KV with NCCL LSE merge, or whole KV heads per GPU")
+    ap.add_argument("--no-tpot", action="store_true", help="skip the 128-step decode loop (TPOT)")
     ap.add_argument("--no-split-kv", action="store_true",
                     help="N>1 default line: skip the cfg3 split_kv / head_shard sub-objects")
     ap.add_argument("--chains", type=int, default=1,
@@ -896,6 +926,8 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+
+    from paper_2503_23294_b200 import batched as batched_mod
 
     cache, q, search = build_cfg2(torch, dev, rank)
     L, B = cache.L, cache.B
@@ -980,6 +1012,41 @@ def main():
     torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
 
+    # serving decode loop (TPOT): per step one appended token per (layer, sequence, kv head)
+    # and the per-layer decode launches, all in one CUDA graph (batched.DecodeLoop); the cache
+    # grows by 128 tokens per sequence, so this runs after the fixed-size measurements
+    memory = cache.memory_footprint().as_dict()
+    tpot = None
+    if not args.no_tpot:
+        n_tok = min(128, int((cache.cap_fp - cache.seq_host[:, 5]).min()))
+        gt = torch.Generator(device=dev)
+        gt.manual_seed(555 + rank)
+        kn = torch.randn((n_tok, L, B, cache.H, 128), generator=gt, device=dev, dtype=torch.float16)
+        vn = torch.randn((n_tok, L, B, cache.H, 128), generator=gt, device=dev, dtype=torch.float16)
+        loop = batched_mod.DecodeLoop(cache, m, splits=splits, chains=args.chains)
+        bytes0 = cache.algorithmic_bytes(m)
+        torch.cuda.synchronize()
+        barrier()
+        e8, e9 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e8.record()
+        for i in range(n_tok):
+            loop.step(q, kn[i], vn[i])
+        e9.record()
+        torch.cuda.synchronize()
+        tp_ms = e8.elapsed_time(e9) / n_tok
+        if world > 1:
+            t = torch.tensor([tp_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tp_ms = float(t.item())
+        mean_bytes = (bytes0 + cache.algorithmic_bytes(m)) / 2
+        tpot = {"steps": n_tok, "ms_per_token": round(tp_ms, 4),
+                "tokens_per_s": round(world * B / (tp_ms * 1e-3), 1),
+                "gbs": round(world * mean_bytes / (tp_ms * 1e-3) / 1e9, 2),
+                "note": "batched.DecodeLoop: per step ckv_append_tokens (one new K/V row per unit) + 32 "
+                        "PDL-chained per-layer decode launches, one CUDA graph replay; the context grows "
+                        f"from {CFG2['context']} to {CFG2['context'] + n_tok} tokens"}
+        del kn, vn, loop
+
     split_kv = None
     if world > 1 and not args.no_split_kv:
         # cfg3 (128K, 40 layers x 40 heads) on the same ranks: sequence split-KV with the NCCL
@@ -1035,11 +1102,15 @@ def main():
             line["prefill"] = prefill
         if split_kv is not None:
             line["split_kv"] = split_kv
+        line["memory"] = memory
+        if tpot is not None:
+            line["tpot"] = tpot
         if world == 1 and not args.no_cpu_baseline:
-            gbs, n, busy = cpu_baseline(seconds=12.0, processes=1)
-            line["cpu_baseline"] = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-                                    "sample": f"{n} cfg2 units (32K ctx, m=4) through the oracle restatement "
-                                              f"of mixed_decode_attention, {busy:.1f} s single process"}
+            gbs, n, wall, kind, kernels = cpu_baseline(seconds=12.0, processes=1, n_units=4)
+            line["cpu_baseline"] = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": kind,
+                                    "cpu_model": cpu_model(),
+                                    "sample": f"{n} decodes of 4 prebuilt cfg2 units (32K ctx, m=4) through "
+                                              f"mixed_decode_attention, {wall:.1f} s single process; kernels: {kernels}"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -103,8 +103,23 @@ def dequantize_codes(packed, scales, zero_points, rows, cols, bits, group_size):
     return z + s * codes
 
 
+# Optional compiled backend: the reference's own chunkkv.kernels._core (oracle/ref_core.py),
+# the "compiled" side of the reference's import-time backend choice (kernels/__init__.py:18-39).
+_KERNELS = None
+
+
+def use_reference_kernels(mod):
+    """Route matmul_packed (the decode's hot op, attention.py:75-90) through the reference's
+    compiled module `mod` (None: the numpy restatement)."""
+    global _KERNELS
+    _KERNELS = mod
+
+
 def matmul_packed(a, packed, scales, zero_points, rows, cols, bits, group_size, transpose):
-    """kernels/_numpy.py:115-125."""
+    """kernels/_numpy.py:115-125 (or the reference's compiled _core.pyx:148-192 when selected)."""
+    if _KERNELS is not None:
+        return _KERNELS.matmul_packed(np.ascontiguousarray(a, dtype=np.float64), packed, scales, zero_points,
+                                      rows, cols, bits, group_size, bool(transpose))
     a = np.ascontiguousarray(a, dtype=np.float64)
     inner = cols if transpose else rows
     if a.ndim != 2 or a.shape[1] != inner:

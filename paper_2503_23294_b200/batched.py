@@ -22,6 +22,7 @@ export_unit restores reference rows on the device (ckv_arena_export).
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -395,14 +396,20 @@ class BatchedKVCache:
         """Append one decode token per (layer, sequence, kv-head): fp16 [L, B, H, 128]."""
         if k_new.shape != (self.L, self.B, self.H, HEAD_DIM) or k_new.shape != v_new.shape:
             raise ValueError(f"decode vectors must have shape {(self.L, self.B, self.H, HEAD_DIM)}")
+        self._reserve_decode_token()
+        self._append_device(k_new.to(torch.float16).contiguous(), v_new.to(torch.float16).contiguous())
+
+    def _reserve_decode_token(self):
+        """Host mirror of one append (kv_store.py:135-148: capacity is a host decision)."""
         if (self.seq_host[:, 5] + 1 > self.cap_fp).any():
             raise ValueError("decode capacity exhausted; rebuild with a larger decode_capacity")
-        k_new = k_new.to(torch.float16).contiguous()
-        v_new = v_new.to(torch.float16).contiguous()
-        _lib.call("ckv_append_tokens", _lib.ptr(k_new), _lib.ptr(v_new), self.L, self.B, self.H,
-                  _lib.ptr(self.seq), self.arena("k"), self.arena("v"), _lib.stream())
         self.seq_host[:, 5] += 1
         self._any_empty = bool((self.total_tokens() == 0).any())
+
+    def _append_device(self, k_new, v_new):
+        """ckv_append_tokens on the current stream (device side only; graph-capturable)."""
+        _lib.call("ckv_append_tokens", _lib.ptr(k_new), _lib.ptr(v_new), self.L, self.B, self.H,
+                  _lib.ptr(self.seq), self.arena("k"), self.arena("v"), _lib.stream())
 
     # -- accounting --------------------------------------------------------------------
     def algorithmic_bytes(self, m):
@@ -414,6 +421,36 @@ class BatchedKVCache:
     def memory_bytes(self):
         return (self.tiles2.numel() + self.tiles4.numel() +
                 sum(t.numel() * t.element_size() for d in (self.k, self.v) for t in d.values()))
+
+    def memory_footprint(self):
+        """Byte accounting of the whole cache (kv_store.memory_footprint, kv_store.py:256-307,
+        summed over the (layer, sequence, kv-head) units), for the tile-native device format:
+        INT2 / INT4 tiles carry packed codes plus fp16 (lo, hi) metadata (96 / 160 B per
+        token-head, K+V); the FP16 region 512 B per token-head (FP16-tier chunks, tail and
+        decode tokens); metadata = the per-sequence table and the per-unit span words.
+        ``reference`` is the same cache under the reference's accounting (float64 scale and
+        zero point per group, the serialized header and chunk permutation per unit)."""
+        s = self.seq_host.astype(np.int64)
+        len2, len4, lenf, ctx = s[:, 1], s[:, 3], s[:, 5], s[:, 7]
+        units = self.L * self.H
+        total = len2 + len4 + lenf
+        n_chunks = ctx // CHUNK
+        from .kv_store import MemoryReport, _HEADER
+        ref = MemoryReport(
+            int2_bytes=int(units * (2 * (32 + 64) * len2).sum()),   # u32 words + f64 scale/zp, K and V
+            int4_bytes=int(units * (2 * (64 + 64) * len4).sum()),
+            fp16_bytes=int(units * (BYTES_FP16 * lenf).sum()),
+            metadata_bytes=int(units * (_HEADER.size + 4 * n_chunks).sum()),
+            fp16_baseline_bytes=int(units * (BYTES_FP16 * total).sum()))
+        return BatchedMemoryReport(
+            int2_bytes=int(units * (BYTES_INT2 * len2).sum()),
+            int4_bytes=int(units * (BYTES_INT4 * len4).sum()),
+            fp16_bytes=int(units * (BYTES_FP16 * lenf).sum()),
+            metadata_bytes=int(self.seq.numel() * 4 + 4 * sum(self.k[x].numel() + self.v[x].numel()
+                                                               for x in ("span_flags", "span_max"))),
+            fp16_baseline_bytes=int(units * (BYTES_FP16 * total).sum()),
+            fp16_capacity_bytes=int(units * (BYTES_FP16 * self.cap_fp).sum()),
+            reference=ref)
 
     def wide_scale_units(self):
         """Number of (layer, kv-head, sequence) units that use the exact wide-scale path."""
@@ -455,6 +492,76 @@ class BatchedKVCache:
         return ChunkedKVCache(CHUNK, HEAD_DIM, GROUP, ctx, np.asarray(perm, np.uint32)[:n_chunks],
                               block(self.k, "k", 2), block(self.v, "v", 2), block(self.k, "k", 4),
                               block(self.v, "v", 4), kf, vf)
+
+
+@dataclass(frozen=True)
+class BatchedMemoryReport:
+    """Bytes of a BatchedKVCache at its device precision (see BatchedKVCache.memory_footprint);
+    same fields and derived values as the reference's MemoryReport (kv_store.py:256-292)."""
+
+    int2_bytes: int
+    int4_bytes: int
+    fp16_bytes: int
+    metadata_bytes: int
+    fp16_baseline_bytes: int
+    fp16_capacity_bytes: int = 0   # the FP16 region as allocated (decode capacity included)
+    reference: object = None       # kv_store.MemoryReport of the same cache, reference accounting
+
+    @property
+    def total_bytes(self) -> int:
+        return self.int2_bytes + self.int4_bytes + self.fp16_bytes + self.metadata_bytes
+
+    @property
+    def compression_ratio(self) -> float:
+        return self.total_bytes / self.fp16_baseline_bytes if self.fp16_baseline_bytes else 0.0
+
+    def as_dict(self) -> dict:
+        d = {"int2_bytes": self.int2_bytes, "int4_bytes": self.int4_bytes, "fp16_bytes": self.fp16_bytes,
+             "metadata_bytes": self.metadata_bytes, "fp16_baseline_bytes": self.fp16_baseline_bytes,
+             "total_bytes": self.total_bytes, "compression_ratio": self.compression_ratio,
+             "fp16_capacity_bytes": self.fp16_capacity_bytes}
+        if self.reference is not None:
+            d["reference"] = self.reference.as_dict()
+        return d
+
+
+class DecodeLoop:
+    """Serving-style decode loop on the device (the reference's generate loop, toy_model.py:
+    89-108, with its per-head attention replaced by the batched cache): every step appends the
+    step's new K/V (one token per (layer, sequence, kv head), ckv_append_tokens) and runs each
+    layer as its own PDL-chained decode launch; the whole step (append + L launches) is one CUDA
+    graph over fixed staging buffers.  ``step(q, k_new, v_new)`` copies the inputs into the
+    staging buffers (any device), replays the graph and returns the output buffer
+    (fp16 [L, B, H*m, 128], valid until the next step)."""
+
+    def __init__(self, cache, m, splits=None, chains=1):
+        self.cache = cache
+        L, B, H, dev = cache.L, cache.B, cache.H, cache.device
+        self.q = torch.zeros((L, B, H * m, HEAD_DIM), dtype=torch.float16, device=dev)
+        self.out = torch.empty_like(self.q)
+        self.k_new = torch.zeros((L, B, H, HEAD_DIM), dtype=torch.float16, device=dev)
+        self.v_new = torch.zeros_like(self.k_new)
+        streams = [torch.cuda.Stream(device=dev) for _ in cache._chain_ranges(chains)]
+        splits = cache.default_splits(m, 1) if splits is None else splits
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up (workspaces, attributes) without appending
+            cache._launch_layers(self.q, self.out, 0, L, splits, None, chains, streams)
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            cache._append_device(self.k_new, self.v_new)
+            cache._launch_layers(self.q, self.out, 0, L, splits, None, chains, streams)
+        self.steps = 0
+
+    def step(self, q=None, k_new=None, v_new=None):
+        self.cache._reserve_decode_token()
+        for dst, src in ((self.q, q), (self.k_new, k_new), (self.v_new, v_new)):
+            if src is not None:
+                dst.copy_(src, non_blocking=True)
+        self.graph.replay()
+        self.steps += 1
+        return self.out
 
 
 def build_cache_batched(k, v, search, context_lens=None, decode_capacity=128, check=True):

@@ -1,0 +1,88 @@
+"""The serving decode loop (append + per-layer decode graph per step) and the tile-native
+memory accounting, against the reference algorithm (oracle) and the reference's own
+memory_footprint of the exported units."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ckv_oracle as O
+from paper_2503_23294_b200 import batched, kv_store, retrieval
+
+pytestmark = pytest.mark.gpu
+
+TOL_ABS = 1e-2
+TOL_REL = 1e-2
+
+
+def _search(tiers):
+    return retrieval.assign_tiers_batched(tiers.astype(np.float64), np.tile([[0.5, 1.5]], (tiers.shape[0], 1)))
+
+
+@pytest.mark.parametrize("chains", [1, 2])
+def test_decode_loop_matches_oracle_each_step(chains):
+    """DecodeLoop: N steps of (append one token per unit, per-layer decode graph) track the
+    reference ChunkedKVCache.append + mixed_decode_attention unit by unit (toy_model.py:89-108,
+    kv_store.py:135-148, attention.py:63-90)."""
+    rng = np.random.default_rng(90 + chains)
+    L, B, H, m, D, N, steps = 2, 3, 2, 4, 128, 11, 6
+    T = N * 32 + 7
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    tiers = rng.choice([0, 0, 1, 2], size=(B, N)).astype(np.uint8)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers),
+                                        decode_capacity=steps)
+    loop = batched.DecodeLoop(cache, m, splits=3, chains=chains)
+    refs = {(l, b, h): O.build_cache(k[l, b, :, h].astype(np.float64), v[l, b, :, h].astype(np.float64),
+                                     tiers[b], 32, 32)
+            for l in range(L) for b in range(B) for h in range(H)}
+    for _ in range(steps):
+        q = rng.normal(size=(L, B, H * m, D)).astype(np.float16)
+        kn = rng.normal(size=(L, B, H, D)).astype(np.float16)
+        vn = rng.normal(size=(L, B, H, D)).astype(np.float16)
+        out = loop.step(torch.from_numpy(q).cuda(), torch.from_numpy(kn).cuda(),
+                        torch.from_numpy(vn).cuda()).float().cpu().numpy()
+        for (l, b, h), oc in refs.items():
+            oc.append(kn[l, b, h].astype(np.float64), vn[l, b, h].astype(np.float64))
+            ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+            err = np.max(np.abs(out[l, b, h * m:(h + 1) * m] - ref))
+            assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (l, b, h, err)
+    for _ in range(int((cache.cap_fp - cache.seq_host[:, 5]).min())):  # the rounded-up capacity
+        loop.step()
+    with pytest.raises(ValueError):  # capacity is a host decision, as in the reference
+        loop.step()
+
+
+def test_memory_footprint_matches_reference_accounting():
+    """BatchedKVCache.memory_footprint().reference equals the sum of the reference's
+    memory_footprint over the exported units; the tile-native figures are the device format's
+    96 / 160 / 512 B per token-head."""
+    rng = np.random.default_rng(95)
+    L, B, H, D, N = 2, 2, 3, 128, 9
+    T = N * 32 + 5
+    k = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    v = torch.from_numpy(rng.normal(size=(L, B, T, H, D)).astype(np.float16)).cuda()
+    tiers = rng.choice([0, 1, 2], size=(B, N)).astype(np.uint8)
+    s = _search(tiers)
+    cache = batched.build_cache_batched(k, v, s, decode_capacity=4)
+    cache.append(torch.zeros((L, B, H, D), dtype=torch.float16, device="cuda"),
+                 torch.zeros((L, B, H, D), dtype=torch.float16, device="cuda"))
+    rep = cache.memory_footprint()
+    perm = s.perm.cpu().numpy()
+    tot = dict(int2_bytes=0, int4_bytes=0, fp16_bytes=0, metadata_bytes=0, fp16_baseline_bytes=0)
+    for l in range(L):
+        for b in range(B):
+            for h in range(H):
+                r = kv_store.memory_footprint(cache.export_unit(l, b, h, perm=perm[b])).as_dict()
+                for key in tot:
+                    tot[key] += r[key]
+    ref = rep.reference.as_dict()
+    for key, val in tot.items():
+        assert ref[key] == val, key
+    cnt = s.seg_counts.cpu().numpy()
+    units = L * H
+    assert rep.int2_bytes == units * 96 * 32 * int(cnt[:, 0].sum())
+    assert rep.int4_bytes == units * 160 * 32 * int(cnt[:, 1].sum())
+    assert rep.fp16_bytes == units * 512 * int((32 * cnt[:, 2] + 5 + 1).sum())
+    assert rep.fp16_baseline_bytes == units * 512 * B * (T + 1)
+    assert 0 < rep.compression_ratio < rep.reference.compression_ratio
