@@ -41,6 +41,8 @@ extern "C" {
 #define CKV_FLAG_ZERO_QUERY 2    /* retrieval.py:212-213                    */
 #define CKV_FLAG_CROSSING 4      /* retrieval.py:231-234                    */
 #define CKV_FLAG_EMPTY_SCORES 8  /* retrieval.py:225-226                    */
+#define CKV_FLAG_NONFINITE_FP16 16 /* informational: inf/nan in a row copied to the FP16
+                                      region (the reference accepts those, kv_store.py:199-202) */
 
 /* tier codes (tiers.py:6-15) */
 #define CKV_TIER_INT2 0
@@ -196,7 +198,9 @@ typedef struct ckv_arena {
  *   head_dim contiguous; 0 < s_token <= INT32_MAX (CKV_ERR_UNSUPPORTED otherwise).
  *   perm u32[B, max_chunks] (from ckv_search), seq i32[B][8].
  * Writes codes/meta to the INT arenas and verbatim rows to the FP16 region (FP16-tier
- * chunks, then the context tail).  Sets CKV_FLAG_NONFINITE on inf/nan input. */
+ * chunks, then the context tail).  Sets CKV_FLAG_NONFINITE on inf/nan in a quantized (INT2 /
+ * INT4) row, as quantizer.quantize does (quantizer.py:71-72); inf/nan in FP16-region rows only
+ * sets the informational CKV_FLAG_NONFINITE_FP16. */
 int32_t ckv_reorder_quantize_pack(const uint16_t* k, const uint16_t* v, int32_t layers,
                                   int32_t batch, int32_t kv_heads, int64_t s_layer,
                                   int64_t s_batch, int64_t s_token, int64_t s_head,

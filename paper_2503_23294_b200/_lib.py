@@ -31,6 +31,7 @@ FLAG_NONFINITE = 1
 FLAG_ZERO_QUERY = 2
 FLAG_CROSSING = 4
 FLAG_EMPTY_SCORES = 8
+FLAG_NONFINITE_FP16 = 16
 
 SEQ_FIELDS = 8  # CKV_SEQ_FIELDS
 DECODE_PDL = 1  # CKV_DECODE_PDL

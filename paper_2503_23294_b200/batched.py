@@ -104,6 +104,7 @@ class BatchedKVCache:
         self.v = {k: torch.zeros_like(t) for k, t in self.k.items()}
         self._ws, self._ws_ptr = {}, {}
         self._arenas = {}
+        self._perm = None
         self._any_empty = bool((self.total_tokens() == 0).any())
 
     # -- construction ------------------------------------------------------------------
@@ -152,6 +153,7 @@ class BatchedKVCache:
         if layer < 0 or layer + L > self.L or (B, H) != (self.B, self.H) or D != HEAD_DIM or k.stride(4) != 1:
             raise ValueError("K/V shape does not match the cache")
         perm = kernels.to_dev(perm, torch.int32)
+        self._perm = perm  # the build permutation (source chunk per slot), for export_unit
         for t in (self.k, self.v):
             t["span_flags"][layer:layer + L].zero_()
             t["span_max"][layer:layer + L].zero_()
@@ -485,8 +487,13 @@ class BatchedKVCache:
             return QuantizedBlock._from_device(rows, HEAD_DIM, bits, GROUP, packed, sc, zp)
 
         n_chunks = ctx // CHUNK
-        if perm is None:
-            perm = np.arange(n_chunks, dtype=np.uint32)
+        if perm is None:  # the permutation this cache was built with
+            if getattr(self, "_perm", None) is None:
+                raise ValueError("cache was not built here: pass the build perm to export_unit")
+            perm = self._perm[seq].cpu().numpy()
+        perm = np.asarray(perm)
+        if perm.shape[0] < n_chunks:
+            raise ValueError("perm shorter than the sequence's chunk count")
         kf = self.k["fp"][layer, head, offf:offf + lenf].double().cpu().numpy()
         vf = self.v["fp"][layer, head, offf:offf + lenf].double().cpu().numpy()
         return ChunkedKVCache(CHUNK, HEAD_DIM, GROUP, ctx, np.asarray(perm, np.uint32)[:n_chunks],

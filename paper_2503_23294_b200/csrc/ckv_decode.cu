@@ -474,18 +474,24 @@ __device__ __forceinline__ void pv_int4(uint32_t sl, const MetaOff& mo, uint32_t
 // with the K group span times |q|.  The precise path feeds the exact magic values
 // 16 + code*2^(j-6) instead and applies bias and scale per group in fp32: two MMAs per k-step
 // whose B fragments are the tier's q fragments (sets 0 / 1) masked to two groups each
-// (column n = (q row n & 3, group 2v + n / 4), m <= 4), so D holds per-(token, q row, group)
+// (column n = (q row n & 3, group 2v + n / 4)), so D holds per-(token, q row, group)
 // partial sums  sum_{d in G} q'_d (16 + code_d 2^(j-6)) = 16 Q'_G + (1/f) sum_{d in G} q_d code_d
 // (f = the set's fp16(1/qmax) fold), and S = sum_G span_G fp16(1/qmax) (D_G - 16 Q'_G) + lo term.
 // A thread holds groups c/2 and 2 + c/2 of q rows (2c)&3, (2c)&3 + 1; lanes c and c^2 hold the
 // other two groups.  Needs no shared memory beyond a 128-byte bias table.
+// With 5-8 q rows (ROWS8) a second pass over the same raw K operands covers q rows 4-7 (q
+// fragments of lane ((g & 3) + 4, c)); lanes c >= 2 keep its sums (their S columns are rows
+// 2c, 2c+1), lanes c < 2 the first pass's.
 struct PreciseOff {
   int32_t m0, m1;   // byte offsets (from the lane slot `sl`) of the metadata of groups G0, G1
   uint32_t bias;    // shared-memory address of this thread's 16 Q' constants (INT2 tier)
   int32_t qoff;     // q-fragment offset of lane ((g & 3), c) relative to this lane
+  int32_t qoff2;    // ... of lane ((g & 3) + 4, c) (q rows 4-7)
   uint32_t msk0, msk1;  // all-ones when this lane's B column takes group c in variant 0 / 1
+  bool hi_rows;     // c >= 2: this lane's S columns are q rows 4-7 when m > 4
 };
-constexpr int kBiasG = 4 * 4;              // bias table f32 16 Q' [tier][group][q row]
+constexpr int kBiasRows = 8;
+constexpr int kBiasG = kBiasRows * 4;      // bias table f32 16 Q' [tier][group][q row]
 constexpr int kBiasTier = 4 * kBiasG;
 
 __device__ __forceinline__ uint32_t raw_pair(uint32_t x, uint32_t mask, uint32_t magic) {
@@ -513,14 +519,25 @@ __device__ __forceinline__ float precise_scale(uint32_t meta, float inv_q16) {
   return (lh.y - lh.x) * inv_q16;
 }
 
-template <int BITS>
+template <int BITS, bool ROWS8>
 __device__ __forceinline__ void qk_precise(uint32_t sl, const MetaOff& mo, const PreciseOff& po,
                                            const QS& qs, uint32_t mg, float (&s)[4]) {
   constexpr int set = BITS == 2 ? 0 : 1;
   constexpr uint32_t meta_at = BITS == 2 ? 1024 : 2048;
   const float inv_q16 = __half2float(__float2half_rn(BITS == 2 ? 1.0f / 3.0f : 1.0f / 15.0f));
   float P0[4] = {0.f, 0.f, 0.f, 0.f}, P1[4] = {0.f, 0.f, 0.f, 0.f};
+  float R0[4] = {0.f, 0.f, 0.f, 0.f}, R1[4] = {0.f, 0.f, 0.f, 0.f};  // q rows 4-7 (ROWS8)
   const uint32_t qsrc = qs.base + po.qoff + set * kQSet;
+  const uint32_t qsrc2 = qs.base + po.qoff2 + set * kQSet;
+#define PSTEP(X, Y, X2, Y2)                                                        \
+  {                                                                                \
+    mma_16816(P0, x0, x1, x2, x3, masked(X, Y, po.msk0));                          \
+    mma_16816(P1, x0, x1, x2, x3, masked(X, Y, po.msk1));                          \
+    if (ROWS8) {                                                                   \
+      mma_16816(R0, x0, x1, x2, x3, masked(X2, Y2, po.msk0));                      \
+      mma_16816(R1, x0, x1, x2, x3, masked(X2, Y2, po.msk1));                      \
+    }                                                                              \
+  }
   if (BITS == 2) {
     const uint4 kk = lds128(sl);
 #pragma unroll
@@ -528,18 +545,22 @@ __device__ __forceinline__ void qk_precise(uint32_t sl, const MetaOff& mo, const
       const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
       const uint32_t w0s = w0 >> 10, w1s = w1 >> 10;
       const uint4 qa = lds128(qsrc + 512 * (2 * blk)), qb = lds128(qsrc + 512 * (2 * blk + 1));
+      uint4 qa2 = qa, qb2 = qb;
+      if (ROWS8) {
+        qa2 = lds128(qsrc2 + 512 * (2 * blk));
+        qb2 = lds128(qsrc2 + 512 * (2 * blk + 1));
+      }
 #define KR(W, WS, I) raw_pair(K2<I>::hi ? WS : W, 0x00030003u << K2<I>::j, mg)
-#define KSTEP(I0, I1, X, Y)                                                        \
+#define KSTEP(I0, I1, X, Y, X2, Y2)                                                \
       {                                                                          \
         const uint32_t x0 = KR(w0, w0s, I0), x1 = KR(w1, w1s, I0);               \
         const uint32_t x2 = KR(w0, w0s, I1), x3 = KR(w1, w1s, I1);               \
-        mma_16816(P0, x0, x1, x2, x3, masked(X, Y, po.msk0));                    \
-        mma_16816(P1, x0, x1, x2, x3, masked(X, Y, po.msk1));                    \
+        PSTEP(X, Y, X2, Y2)                                                      \
       }
-      KSTEP(0, 1, qa.x, qa.y)
-      KSTEP(2, 3, qa.z, qa.w)
-      KSTEP(4, 5, qb.x, qb.y)
-      KSTEP(6, 7, qb.z, qb.w)
+      KSTEP(0, 1, qa.x, qa.y, qa2.x, qa2.y)
+      KSTEP(2, 3, qa.z, qa.w, qa2.z, qa2.w)
+      KSTEP(4, 5, qb.x, qb.y, qb2.x, qb2.y)
+      KSTEP(6, 7, qb.z, qb.w, qb2.z, qb2.w)
 #undef KSTEP
 #undef KR
     }
@@ -552,27 +573,38 @@ __device__ __forceinline__ void qk_precise(uint32_t sl, const MetaOff& mo, const
       const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
       const uint32_t a_lo8 = a_lo >> 8, a_hi8 = a_hi >> 8, b_lo8 = b_lo >> 8, b_hi8 = b_hi >> 8;
       const uint4 qa = lds128(qsrc + 512 * (2 * blk)), qb = lds128(qsrc + 512 * (2 * blk + 1));
+      uint4 qa2 = qa, qb2 = qb;
+      if (ROWS8) {
+        qa2 = lds128(qsrc2 + 512 * (2 * blk));
+        qb2 = lds128(qsrc2 + 512 * (2 * blk + 1));
+      }
 #define KR(X, X8, I) raw_pair(K4<I>::hi ? X8 : X, 0x000F000Fu << K4<I>::j, mg)
-#define KSTEP(XA, XA8, XB, XB8, I0, I1, X, Y)                                      \
+#define KSTEP(XA, XA8, XB, XB8, I0, I1, X, Y, X2, Y2)                              \
       {                                                                          \
         const uint32_t x0 = KR(XA, XA8, I0), x1 = KR(XB, XB8, I0);               \
         const uint32_t x2 = KR(XA, XA8, I1), x3 = KR(XB, XB8, I1);               \
-        mma_16816(P0, x0, x1, x2, x3, masked(X, Y, po.msk0));                    \
-        mma_16816(P1, x0, x1, x2, x3, masked(X, Y, po.msk1));                    \
+        PSTEP(X, Y, X2, Y2)                                                      \
       }
-      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 0, 1, qa.x, qa.y)
-      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 2, 3, qa.z, qa.w)
-      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 0, 1, qb.x, qb.y)
-      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 2, 3, qb.z, qb.w)
+      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 0, 1, qa.x, qa.y, qa2.x, qa2.y)
+      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 2, 3, qa.z, qa.w, qa2.z, qa2.w)
+      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 0, 1, qb.x, qb.y, qb2.x, qb2.y)
+      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 2, 3, qb.z, qb.w, qb2.z, qb2.w)
 #undef KSTEP
 #undef KR
     }
   }
+#undef PSTEP
   const uint2 m0 = lds64(sl + meta_at + po.m0), m1 = lds64(sl + meta_at + po.m1);
+  const float s0g = precise_scale(m0.x, inv_q16), s0g8 = precise_scale(m0.y, inv_q16);
+  const float s1g = precise_scale(m1.x, inv_q16), s1g8 = precise_scale(m1.y, inv_q16);
   float t[4];
-  precise_combine(P0, P1, precise_scale(m0.x, inv_q16), precise_scale(m0.y, inv_q16),
-                  precise_scale(m1.x, inv_q16), precise_scale(m1.y, inv_q16),
-                  po.bias + (BITS == 2 ? 0 : kBiasTier), t);
+  precise_combine(P0, P1, s0g, s0g8, s1g, s1g8, po.bias + (BITS == 2 ? 0 : kBiasTier), t);
+  if (ROWS8) {
+    float t2[4];
+    precise_combine(R0, R1, s0g, s0g8, s1g, s1g8, po.bias + (BITS == 2 ? 0 : kBiasTier) + 16, t2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) t[e] = po.hi_rows ? t2[e] : t[e];
+  }
   const uint2 kmm = lds64(sl + meta_at + mo.k);
   float s2[4] = {0.f, 0.f, 0.f, 0.f};
   mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
@@ -670,18 +702,19 @@ __device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc&
   for (int s = 0; s < Ring<BITS>::stages - 1; ++s) issue_at<BITS>(warp + kDecWarps * s, n, base, ring_l + s * Ring<BITS>::bytes);
 }
 
-// decode modes of a unit: normal; precise K (wide span x |q|, m <= 4); exact (scales or q
+// decode modes of a unit: normal; precise K (wide span x |q|; m <= 4, or m <= 8 in two passes);
+// exact (scales or q
 // too wide for the fp16-weighted forms)
-constexpr int kModeNormal = 0, kModePrecise = 1, kModeExact = 2;
+constexpr int kModeNormal = 0, kModePrecise = 1, kModeExact = 2, kModePrecise8 = 3;
 
 template <int MODE>
 __device__ __forceinline__ void qk2(uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
-  if (MODE == kModePrecise) qk_precise<2>(sl, mo, po, qs, mg, s);
+  if (MODE == kModePrecise || MODE == kModePrecise8) qk_precise<2, MODE == kModePrecise8>(sl, mo, po, qs, mg, s);
   else qk_int2<MODE == kModeExact>(sl, mo, qs, mg, s);
 }
 template <int MODE>
 __device__ __forceinline__ void qk4(uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
-  if (MODE == kModePrecise) qk_precise<4>(sl, mo, po, qs, mg, s);
+  if (MODE == kModePrecise || MODE == kModePrecise8) qk_precise<4, MODE == kModePrecise8>(sl, mo, po, qs, mg, s);
   else qk_int4<MODE == kModeExact>(sl, mo, qs, mg, s);
 }
 // The tile loop of one warp over one kind's range [0, n) (tiles warp, warp + 4, ...) through
@@ -792,7 +825,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   __shared__ float s_ml[kDecWarps][8][2];
   __shared__ __align__(16) unsigned char s_q[kQBytes];
   __shared__ int s_last;
-  __shared__ __align__(16) float s_bias[2 * 16];  // precise mode: 16 Q' [tier][group][q row]
+  __shared__ __align__(16) float s_bias[2 * 4 * kBiasRows];  // precise modes: 16 Q' [tier][group][q row]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   __shared__ int64_t s_tr[12], s_tend[kDecWarps];
@@ -878,7 +911,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     for (int o = 1; o < 32; o <<= 1) qmaxabs = fmaxf(qmaxabs, __shfl_xor_sync(0xffffffffu, qmaxabs, o));
     const bool wide = qmaxabs > kWideQ || span_wide;
     mode = wide ? kModeExact
-                : (a.m <= 4 && kspan * qmaxabs > kPreciseSpanQ ? kModePrecise : kModeNormal);
+                : (kspan * qmaxabs > kPreciseSpanQ ? (a.m <= 4 ? kModePrecise : kModePrecise8) : kModeNormal);
     // slot weights 2^(6-j) of K pair i: INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1)
     auto slot_w = [&](int set, int i) {
       return set == 0 ? exp2f((float)(6 - (i <= 4 ? 2 * i : 2 * (i - 5))))
@@ -902,7 +935,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
       }
       // precise-mode bias 16 Q'[tier][group c][q row g]: the sum of exactly the fp16 weighted
       // values this lane's B fragments hold
-      if (warp < 2 && g < 4) s_bias[warp * 16 + c * 4 + g] = 16.0f * qsw;
+      if (warp < 2) s_bias[warp * 4 * kBiasRows + c * kBiasRows + g] = 16.0f * qsw;
     } else {
       float qsum = 0.f;
 #pragma unroll
@@ -922,8 +955,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     const int G0 = c >> 1, qa = (2 * c) & 3;
     po.m0 = (g * 4 + G0) * 8 - 16 * lane;
     po.m1 = (g * 4 + G0 + 2) * 8 - 16 * lane;
-    po.bias = (uint32_t)__cvta_generic_to_shared(s_bias) + (G0 * 4 + qa) * 4;
+    po.bias = (uint32_t)__cvta_generic_to_shared(s_bias) + (G0 * kBiasRows + qa) * 4;
     po.qoff = 16 * (((g & 3) * 4 + c) - lane);
+    po.qoff2 = 16 * ((((g & 3) + 4) * 4 + c) - lane);
+    po.hi_rows = c >= 2;
     const bool in = (g >> 2) == (c & 1);  // column g takes group c (variant c / 2)
     po.msk0 = in && (c >> 1) == 0 ? 0xffffffffu : 0u;
     po.msk1 = in && (c >> 1) == 1 ? 0xffffffffu : 0u;
@@ -943,6 +978,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     fp16_tiles<true>(a, qs, st, nloc);
   } else {
     if (mode == kModePrecise) quantized_tiles<kModePrecise>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    else if (mode == kModePrecise8) quantized_tiles<kModePrecise8>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
     else quantized_tiles<kModeNormal>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
     fp16_tiles<false>(a, qs, st, nloc);
     // undo the V m-tile weights 2^(2(mt&3) - 6)

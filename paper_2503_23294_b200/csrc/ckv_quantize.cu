@@ -379,7 +379,7 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
   }
   const uint32_t task_addr = (uint32_t)__cvta_generic_to_shared(s_task[warp]);
   const int sub = lane >> 4, j = lane & 15;  // 2 rows per warp step, 8 fp16 per lane
-  bool bad = false;
+  bool bad = false, bad_fp = false;  // non-finite input in a quantized / an FP16-region row
 #pragma unroll 1
   for (int tsel = 0; tsel < 2; ++tsel) {
     const QTask t = read_task(task_addr);
@@ -398,7 +398,7 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
           const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            bad |= !fp16_bits_finite(w[e] & 0xFFFF) || !fp16_bits_finite(w[e] >> 16);
+            bad_fp |= !fp16_bits_finite(w[e] & 0xFFFF) || !fp16_bits_finite(w[e] >> 16);
           reinterpret_cast<uint4*>(dst + (int64_t)r * kHeadDim)[j] = x;
         }
       }
@@ -440,7 +440,10 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       atomicMax(span_max + unit2 * B + c2.b, __float_as_uint(smax));
     __syncwarp();
   }
+  // the reference rejects non-finite values only where it quantizes (build_cache ->
+  // quantizer.quantize, quantizer.py:71-72); FP16-region rows are copied as they are
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE);
+  if (__any_sync(0xffffffffu, bad_fp) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE_FP16);
 }
 
 // Decode append: row (l, b, h) of k_new/v_new -> FP16 region row off_fp + len_fp.
