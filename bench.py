@@ -295,9 +295,28 @@ def build_cfg2(torch, dev, rank):
     k = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
     v = torch.randn((L, B, T, H, D), generator=g, device=dev, dtype=torch.float16)
     cache = batched.build_cache_batched(k, v, search, decode_capacity=128)
+    # a few units' fp16 K/V kept on the host for the parity check of the timed cache
+    samples = [(l, b, h, k[l, b, :, h].cpu().numpy(), v[l, b, :, h].cpu().numpy(), ref_tiers[b])
+               for (l, b, h) in ((0, 0, 0), (L // 2, B - 1, H // 2), (L - 1, B // 2, H - 1))]
     del k, v
     q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
+    cache.parity_samples = samples
     return cache, q, search
+
+
+def sampled_parity(cache, q, out, m):
+    """max relative error (|got - ref| / max|ref|) of sampled units of the timed cache's output
+    against the reference algorithm (oracle) in f64 on the same fp16 inputs; outside the timed
+    region."""
+    from oracle import ckv_oracle as O
+    qh, oh = q.cpu().numpy(), out.float().cpu().numpy()
+    worst = 0.0
+    for l, b, h, kh, vh, tiers in cache.parity_samples:
+        oc = O.build_cache(kh.astype(np.float64), vh.astype(np.float64), tiers, 32, 32)
+        ref = O.mixed_decode_attention(qh[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+        got = oh[l, b, h * m:(h + 1) * m].astype(np.float64)
+        worst = max(worst, float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))
+    return worst
 
 
 def bench_prefill(torch, dev, steps=3, profile=False):
@@ -1012,6 +1031,11 @@ def main():
     torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
 
+    # parity of the timed cache: the graph step's output for sampled units vs the reference
+    graph.replay()
+    torch.cuda.synchronize()
+    parity = sampled_parity(cache, q, out, m)
+
     # serving decode loop (TPOT): per step one appended token per (layer, sequence, kv head)
     # and the per-layer decode launches, all in one CUDA graph (batched.DecodeLoop); the cache
     # grows by 128 tokens per sequence, so this runs after the fixed-size measurements
@@ -1103,6 +1127,9 @@ def main():
         if split_kv is not None:
             line["split_kv"] = split_kv
         line["memory"] = memory
+        line["parity_sampled_max_rel"] = round(parity, 6)
+        line["parity_note"] = ("3 units (layer, sequence, kv head) of the timed cfg2 cache, graph-step output vs "
+                               "the reference algorithm in f64 (oracle), tolerance 1e-2")
         if tpot is not None:
             line["tpot"] = tpot
         if world == 1 and not args.no_cpu_baseline:
