@@ -1023,10 +1023,10 @@ def main():
     # single-launch (all 32 layers in one grid) figure for the same cache
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(3):
-        cache.decode(q, out=out)
+        cache.decode(q, out=out, splits=args.splits)
     e2.record()
     for _ in range(args.steps):
-        cache.decode(q, out=out)
+        cache.decode(q, out=out, splits=args.splits)
     e3.record()
     torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9

@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   const float* p0 = a.ws + row0 * a.splits * kWsStride;
   const int nrows = a.m * a.splits;
   float* s_part = reinterpret_cast<float*>(&s_ring[0][0]);
-  if (nrows * kWsStride * (int)sizeof(float) <= kDynSmem) {
+  if ((nrows * (kWsStride + 1) + 2 * a.m) * (int)sizeof(float) <= kDynSmem) {
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_part);
     const int nvec = nrows * kWsStride / 4;
     for (int i = threadIdx.x; i < nvec; i += blockDim.x) cp_async16(sbase + 16 * i, p0 + 4 * i);
@@ -1097,6 +1097,46 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     __syncthreads();
   } else {
     s_part = nullptr;
+  }
+  if (s_part != nullptr && nrows <= (int)blockDim.x) {
+    // weights first, one thread per partial row: w = 2^(m_row - max over the q row's splits),
+    // then each thread (d) sums every q row's splits independently (no serial max pass per d)
+    float* s_w = s_part + nrows * kWsStride;  // [nrows] weights, then [m] (max, sum) pairs
+    float* s_ml2 = s_w + nrows;
+    const int r = threadIdx.x;
+    if (r < nrows) {
+      const float* pq = s_part + (r / a.splits) * a.splits * kWsStride;
+      float ms = -INFINITY;
+      for (int s = 0; s < a.splits; ++s) ms = fmaxf(ms, pq[s * kWsStride + kHeadDim]);
+      const float mw = s_part[r * kWsStride + kHeadDim];
+      const float w = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+      s_w[r] = w;
+      if (r % a.splits == 0) s_ml2[2 * (r / a.splits)] = ms;
+    }
+    __syncthreads();
+    if (r < a.m) {
+      float lsum = 0.f;
+      for (int s = 0; s < a.splits; ++s) lsum += s_w[r * a.splits + s] * s_part[(r * a.splits + s) * kWsStride + kHeadDim + 1];
+      s_ml2[2 * r + 1] = lsum;
+    }
+    __syncthreads();
+    for (int qi = 0; qi < a.m; ++qi) {
+      const float* pq = s_part + qi * a.splits * kWsStride + d;
+      const float* wq = s_w + qi * a.splits;
+      float acc = 0.f;
+      for (int s = 0; s < a.splits; ++s) acc += wq[s] * pq[s * kWsStride];
+      const int64_t row = row0 + qi;
+      if (a.partial_out) {
+        float* dst = a.partial_out + row * kPartStride;
+        dst[d] = acc;
+        if (d == 0) { dst[kHeadDim] = s_ml2[2 * qi]; dst[kHeadDim + 1] = s_ml2[2 * qi + 1]; }
+      } else {
+        a.out[l * a.o_sl + b * a.o_sb + (int64_t)(hq0 + qi) * kHeadDim + d] =
+            __half_as_ushort(__float2half_rn(acc / s_ml2[2 * qi + 1]));
+      }
+    }
+    trace_out();
+    return;
   }
   for (int qi = 0; qi < a.m; ++qi) {
     const int64_t row = row0 + qi;
