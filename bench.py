@@ -888,6 +888,9 @@ def main():
     ap.add_argument("--no-tpot", action="store_true", help="skip the 128-step decode loop (TPOT)")
     ap.add_argument("--no-split-kv", action="store_true",
                     help="N>1 default line: skip the cfg3 split_kv / head_shard sub-objects")
+    ap.add_argument("--schedule", choices=["wp", "split"], default="wp",
+                    help="decode schedule of whole-batch launches: wp = warp plan (one 16-warp CTA per SM, "
+                         "units split at warp granularity), split = 4-warp CTAs with --splits per unit")
     ap.add_argument("--chains", type=int, default=1,
                     help="micro-batch chains per decode step (cfg2/cfg4): the batch is split into this "
                          "many sequence ranges, each its own chain of per-layer launches on its own "
@@ -951,7 +954,9 @@ def main():
     cache, q, search = build_cfg2(torch, dev, rank)
     L, B = cache.L, cache.B
     m = q.shape[2] // cache.H
-    splits = args.splits or cache.default_splits(m, 1)
+    cache.schedule = args.schedule
+    wp = args.schedule == "wp" and args.chains == 1 and cache.warp_plan() is not None
+    splits = None if wp else (args.splits or cache.default_splits(m, 1))
     out = torch.empty_like(q)
     step_bytes = cache.algorithmic_bytes(m)
 
@@ -1093,6 +1098,13 @@ def main():
         torch.cuda.empty_cache()
         prefill = bench_prefill(torch, dev)
 
+    if wp:
+        wprefix = cache.warp_plan()[0].cpu().numpy()[:cache.B * cache.H + 1]
+        nw = np.diff(wprefix)
+        sched_desc = (f"warp plan: {len(wprefix) - 1} units x {int(nw.min())}-{int(nw.max())} warps, "
+                      f"{cache.warp_plan()[1]} CTAs of 16 warps (one per SM)")
+    else:
+        sched_desc = f"split: {splits} CTAs of 4 warps per unit"
     if rank == 0:
         peak, peak_kind = measured_peak_gbs()
         per_launch_bytes = step_bytes / L
@@ -1109,7 +1121,8 @@ def main():
                        "global_batch": B * world, "seq_len": CFG2["context"], "parallelism": f"batch-shard x{world}",
                        "tier_fractions_int2_int4_fp16": [round(float(x), 4) for x in frac],
                        "launch": "per-layer (32 PDL-chained launches per step, replayed as one CUDA graph)",
-                       "splits": splits, "l2": "inputs larger than L2 (7.1 GB arenas vs 126 MB L2)"},
+                       "splits": splits, "schedule": sched_desc,
+                       "l2": "inputs larger than L2 (7.1 GB arenas vs 126 MB L2)"},
             "tokens_per_s": round(tokens_per_s, 1),
             "algorithmic_bytes_per_step": step_bytes,
             "eager_launches_gbs": round(eager_gbs, 2),

@@ -105,6 +105,10 @@ class BatchedKVCache:
         self._ws, self._ws_ptr = {}, {}
         self._arenas = {}
         self._perm = None
+        self._wp = None
+        # decode schedule of whole-batch launches: "wp" (warp plan: one 16-warp CTA per SM,
+        # units split at warp granularity) or "split" (4-warp CTAs, `splits` per unit)
+        self.schedule = "wp"
         self._any_empty = bool((self.total_tokens() == 0).any())
 
     # -- construction ------------------------------------------------------------------
@@ -189,6 +193,68 @@ class BatchedKVCache:
                 best, best_cost = s, cost
         return best
 
+    WP_WARPS = 16   # warps per CTA of the warp-plan decode kernel (one CTA per SM)
+
+    def warp_plan(self):
+        """Warp-plan schedule (ckv_decode_attention_wp): unit u = b*H + h gets n_u warps in
+        proportion to its tile cost (INT2 1, INT4 1.06, FP16-region 2 per 16-token tile), at
+        least 2, summing to 16 x the SM count; returns (prefix i32 [B*H + 1] on the device, ctas,
+        max_slots, max_ctas) or None when the units do not fit (more than 8 per CTA).  Computed
+        once: any plan is exact, later appends only shift the balance slightly.  The device table
+        holds the prefix, then the unit of every global warp."""
+        if self._wp is None:
+            self._wp = False
+            n_sm = _num_sms()
+            T = self.WP_WARPS * n_sm
+            U = self.B * self.H
+            s = self.seq_host.astype(np.int64)
+            cost_b = s[:, 1] // TILE + 1.06 * (s[:, 3] // TILE) + 2.0 * (-(-s[:, 5] // TILE))
+            cost = np.repeat(cost_b, self.H).astype(np.float64)
+            if U and 2 * U <= T and cost.sum() > 0:
+                raw = T * cost / cost.sum()
+                n = np.maximum(np.floor(raw).astype(np.int64), 2)
+                order = np.argsort(-(raw - np.floor(raw)), kind="stable")
+                i = 0
+                while n.sum() < T:
+                    n[order[i % U]] += 1
+                    i += 1
+                while n.sum() > T:
+                    j = int(np.argmax(np.where(n > 2, n - raw, -np.inf)))
+                    n[j] -= 1
+                prefix = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+                first, last = prefix[:-1] // self.WP_WARPS, (prefix[1:] - 1) // self.WP_WARPS
+                max_ctas = int((last - first + 1).max())
+                starts = np.arange(n_sm) * self.WP_WARPS
+                u_lo = np.searchsorted(prefix, starts, side="right") - 1
+                u_hi = np.searchsorted(prefix, starts + self.WP_WARPS - 1, side="right") - 1
+                max_slots = int((u_hi - u_lo + 1).max())
+                if max_slots <= 8:
+                    wunit = np.repeat(np.arange(U), n)  # unit of every global warp
+                    table = np.concatenate([prefix, wunit]).astype(np.int32)
+                    self._wp = (torch.from_numpy(table).to(self.device), n_sm, max_slots, max_ctas)
+        return self._wp or None
+
+    def _wp_workspace(self, m, layers, layer, max_ctas):
+        wkey = ("wp", m, layers, layer)
+        hit = self._ws_ptr.get(wkey)
+        if hit is not None:
+            return hit
+        lib = _lib.load()
+        per = lib.ckv_decode_wp_workspace_bytes(layers, self.B, self.H, m, max_ctas)
+        per = -(-per // 256) * 256
+        key = ("wp", m, layers)
+        nbytes = per * (self.L if layers == 1 else 1)
+        if key not in self._ws:
+            self._ws[key] = torch.zeros(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
+        self._ws_ptr[wkey] = ptr = self._ws[key].data_ptr() + (per * layer if layers == 1 else 0)
+        return ptr
+
+    def _use_wp(self, m, seqs, splits, schedule):
+        sched = self.schedule if schedule is None else schedule
+        if sched != "wp" or seqs is not None or splits is not None or m > MAX_Q_PER_KV:
+            return None
+        return self.warp_plan()
+
     def _workspace(self, m, splits, layers, layer):
         """Zero-initialised decode workspace (split partials + self-resetting arrival counters).
         Launches covering a single layer get a private per-layer slice, so consecutive
@@ -213,7 +279,7 @@ class BatchedKVCache:
         self._ws_ptr[wkey] = ptr = self._ws[key].data_ptr() + off
         return ptr
 
-    def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False, seqs=None):
+    def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False, seqs=None, schedule=None):
         """Mixed-precision decode attention for q fp16 [L', B, H*m, 128] -> fp16 same shape,
         over layers [layer, layer + L') of the cache (L' = L for the whole model in one launch,
         1 for the per-layer launches of a real decode step).  pdl=True launches as a
@@ -248,9 +314,18 @@ class BatchedKVCache:
                                  splits=splits, scale=scale, layer=layer, pdl=False, seqs=(b0, b1))
                 out.view(L, B, self.H, m, D)[:, b0:b1, :, r0:r1] = og.view(L, B, self.H, r1 - r0, D)[:, b0:b1]
             return out
+        scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+        plan = self._use_wp(m, None if (b0, b1) == (0, B) else seqs, splits, schedule)
+        if plan is not None:
+            prefix, ctas, slots, max_ctas = plan
+            ws = self._wp_workspace(m, L, layer, max_ctas)
+            _lib.call("ckv_decode_attention_wp", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k", layer),
+                      self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H, m, scale, _lib.ptr(prefix), ctas,
+                      slots, max_ctas, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
+                      _lib.DECODE_PDL if pdl else 0, _lib.stream())
+            return out
         splits = self.default_splits(m, L) if splits is None else int(splits)
         ws = self._workspace(m, splits, L, layer)
-        scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
         _lib.call("ckv_decode_attention_seqs", _lib.ptr(q), q.stride(0), q.stride(1),
                   self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, b0, b1 - b0,
                   self.H, m, scale, splits, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
@@ -373,7 +448,7 @@ class BatchedKVCache:
             raise ValueError("q and out must be [L, B, H*m, 128] for all layers")
         return self._segment_graphs(q, out, self.L, splits, scale, chains)[0]
 
-    def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None):
+    def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None, schedule=None):
         """Unnormalised split-KV partials f32 [L'*B*H*m, 130] = (acc[128], m (log2), l) for q
         fp16 [L', B, H*m, 128] over layers [layer, layer + L') (per-layer launches: L' = 1,
         pdl as in decode); `out` may be a preallocated [L'*B*H*m, 130] view."""
@@ -381,13 +456,23 @@ class BatchedKVCache:
         if B != self.B or layer < 0 or layer + L > self.L or D != HEAD_DIM or Hq % self.H:
             raise ValueError("q shape does not match the cache")
         m = Hq // self.H
+        splits_arg = splits
         splits = self.default_splits(m, L) if splits is None else int(splits)
         part = out if out is not None else torch.empty((L * B * Hq, HEAD_DIM + 2), dtype=torch.float32,
                                                        device=q.device)
         if part.shape != (L * B * Hq, HEAD_DIM + 2) or not part.is_contiguous():
             raise ValueError("partials buffer must be contiguous [L*B*Hq, 130]")
-        ws = self._workspace(m, splits, L, layer)
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+        plan = self._use_wp(m, None, None if schedule == "wp" else splits_arg, schedule)
+        if plan is not None:
+            prefix, ctas, slots, max_ctas = plan
+            ws = self._wp_workspace(m, L, layer, max_ctas)
+            _lib.call("ckv_decode_attention_wp", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k", layer),
+                      self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H, m, scale, _lib.ptr(prefix), ctas,
+                      slots, max_ctas, ws, None, 0, 0, _lib.ptr(part), _lib.DECODE_PDL if pdl else 0,
+                      _lib.stream())
+            return part
+        ws = self._workspace(m, splits, L, layer)
         _lib.call("ckv_decode_attention", _lib.ptr(q), q.stride(0), q.stride(1),
                   self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H,
                   m, scale, splits, ws, None, 0, 0, _lib.ptr(part), _lib.DECODE_PDL if pdl else 0,

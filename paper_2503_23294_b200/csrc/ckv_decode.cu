@@ -26,6 +26,7 @@
 #include <math.h>
 
 #include <cuda/atomic>
+#include <type_traits>
 
 #include "ckv_common.cuh"
 
@@ -696,10 +697,11 @@ __device__ __forceinline__ void issue_at(int t, int n, const char* base, uint32_
 
 // Prologue of a phase: put this warp's first kStages-1 tiles of the range in flight.
 template <int BITS>
-__device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc& src, uint32_t ring_l, int warp) {
+__device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc& src, uint32_t ring_l, int warp,
+                                         int stride = kDecWarps) {
   const char* base = tile_base<BITS>(a, src);
 #pragma unroll
-  for (int s = 0; s < Ring<BITS>::stages - 1; ++s) issue_at<BITS>(warp + kDecWarps * s, n, base, ring_l + s * Ring<BITS>::bytes);
+  for (int s = 0; s < Ring<BITS>::stages - 1; ++s) issue_at<BITS>(warp + stride * s, n, base, ring_l + s * Ring<BITS>::bytes);
 }
 
 // decode modes of a unit: normal; precise K (wide span x |q|; m <= 4, or m <= 8 in two passes);
@@ -724,16 +726,16 @@ __device__ __forceinline__ void qk4(uint32_t sl, const MetaOff& mo, const Precis
 template <int MODE, int BITS>
 __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc& src, const MetaOff& mo,
                                           const PreciseOff& po, uint32_t ring_l, const QS& qs, uint32_t mg,
-                                          WarpState& st, int warp) {
+                                          WarpState& st, int warp, int stride = kDecWarps) {
   constexpr bool EXACT = MODE == kModeExact;
   constexpr int kStages = Ring<BITS>::stages, kStageBytes = Ring<BITS>::bytes;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
   int t = warp;
-  constexpr int64_t kStep = (int64_t)kDecWarps * (BITS == 2 ? kBlock2 : kBlock4);
+  const int64_t kStep = (int64_t)stride * (BITS == 2 ? kBlock2 : kBlock4);
   // address of the next tile to issue (kStages-1 ahead of the one consumed), advanced by one
   // warp stride per iteration: a loop-carried pointer instead of base + t * block each time
-  const char* pn = tile_base<BITS>(a, src) + (int64_t)(warp + kDecWarps * (kStages - 1)) * (kStep / kDecWarps);
+  const char* pn = tile_base<BITS>(a, src) + (int64_t)(warp + stride * (kStages - 1)) * (BITS == 2 ? kBlock2 : kBlock4);
   if (t < n) {
     uint32_t cur = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
     cp_wait<kStages - 2>();
@@ -744,8 +746,8 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
     uint32_t bp0, bp1;
     softmax_tile<EXACT>(s0, st, bp0, bp1);
     while (true) {
-      const int tn = t + kDecWarps;
-      issue_at<BITS>(t + kDecWarps * (kStages - 1) < n ? 0 : 1, 1, pn, put);
+      const int tn = t + stride;
+      issue_at<BITS>(t + stride * (kStages - 1) < n ? 0 : 1, 1, pn, put);
       pn += kStep;
       if (tn >= n) {
         if (BITS == 2) pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
@@ -775,22 +777,28 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
 
 // Both phases of a CTA's quantized tiles: INT2 (its prologue issued before the PDL wait), then
 // INT4 (prologue here, or before the wait when the CTA has no INT2 tiles).
+__device__ __forceinline__ int rotate(int warp, int done, int stride) {  // (warp - done) mod stride
+  const int r = (warp - done) % stride;
+  return r < 0 ? r + stride : r;
+}
+
 template <int MODE>
 __device__ __forceinline__ void quantized_tiles(int n2, int n4, const DecArgs& a, const TileSrc& src,
                                                 const MetaOff& mo, const PreciseOff& po, uint32_t ring_l,
-                                                const QS& qs, uint32_t mg, WarpState& st, int warp) {
+                                                const QS& qs, uint32_t mg, WarpState& st, int warp,
+                                                int stride = kDecWarps) {
   // the INT4 phase starts at the warp after the one that took the last INT2 tile, so every
   // warp's tile count over both phases is within one of the others' (the CTA's warps meet at
   // the merge barrier)
-  const int w4 = (warp - n2) & (kDecWarps - 1);
+  const int w4 = rotate(warp, n2, stride);
   if (n2 > 0) {
-    run_tiles<MODE, 2>(n2, a, src, mo, po, ring_l, qs, mg, st, warp);
+    run_tiles<MODE, 2>(n2, a, src, mo, po, ring_l, qs, mg, st, warp, stride);
     if (n4 > 0) {
       __syncwarp();
-      prologue<4>(n4, a, src, ring_l, w4);
+      prologue<4>(n4, a, src, ring_l, w4, stride);
     }
   }
-  if (n4 > 0) run_tiles<MODE, 4>(n4, a, src, mo, po, ring_l, qs, mg, st, w4);
+  if (n4 > 0) run_tiles<MODE, 4>(n4, a, src, mo, po, ring_l, qs, mg, st, w4, stride);
 }
 
 // This CTA's share of its unit's FP16-region tiles (FP16-tier chunks, tail, decode tokens),
@@ -816,6 +824,81 @@ __device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpS
   for (int tf = f_begin + ((warp - nq) & (kDecWarps - 1)); tf < f_end; tf += kDecWarps) {
     const int r = tf * kTile;
     tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
+  }
+}
+
+// ---- q staging (shared by both decode kernels) -----------------------------------------
+// q row `row` (zero if >= m) of unit (l, b, h), lane's 32 columns 32c.., scaled to log2 units
+// and rounded to the fp16 MMA operand.
+__device__ __forceinline__ void load_q_rows(const DecArgs& a, int l, int b, int h, int row, int c, float (&qv)[32]) {
+  const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + row) * kHeadDim + 32 * c;
+  if (row < a.m) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint4 x = reinterpret_cast<const uint4*>(qrow)[u];
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(u32_as_h2(w[e]));
+        qv[8 * u + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
+        qv[8 * u + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) qv[e] = 0.f;
+  }
+}
+
+// decode mode of a unit from its q (the warp's 8 rows) and its span bounds
+__device__ __forceinline__ int unit_mode(const DecArgs& a, const float (&qv)[32], bool span_wide, float kspan) {
+  float qmaxabs = 0.f;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) qmaxabs = fmaxf(qmaxabs, __shfl_xor_sync(0xffffffffu, qmaxabs, o));
+  const bool wide = qmaxabs > kWideQ || span_wide;
+  return wide ? kModeExact
+              : (kspan * qmaxabs > kPreciseSpanQ ? (a.m <= 4 ? kModePrecise : kModePrecise8) : kModeNormal);
+}
+
+// Part `part` of a unit's q staging into s_qu (kQBytes) / s_biasu: 0-2 the q-fragment sets
+// (0: INT2 slot weights, 1: INT4, 2: unweighted; parts 0/1 also the precise-mode bias), 3 the
+// zero-point entry.
+__device__ __forceinline__ void stage_q_part(const DecArgs& a, const float (&qv)[32], int part, unsigned char* s_qu,
+                                             float* s_biasu, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+  // slot weights 2^(6-j) of K pair i: INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1)
+  auto slot_w = [&](int set, int i) {
+    return set == 0 ? exp2f((float)(6 - (i <= 4 ? 2 * i : 2 * (i - 5))))
+                    : (set == 1 ? exp2f((float)(6 - 4 * (i & 1))) : 1.0f);
+  };
+  if (part < 3) {
+    float qsw = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
+      const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
+      // INT2 / INT4 sets also carry the fold of the fp16(1/qmax) rounding (see kdeq)
+      const float fold = part == 0 ? kscale_fold(1.0f / 3.0f) : (part == 1 ? kscale_fold(1.0f / 15.0f) : 1.0f);
+      const float x0 = slot_w(part, i0) * fold, x1 = slot_w(part, i1) * fold;
+      const __half2 lo = __floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0);
+      const __half2 hi = __floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1);
+      reinterpret_cast<uint2*>(s_qu + part * kQSet + 512 * (ks >> 1) + 16 * lane)[ks & 1] =
+          make_uint2(h2_as_u32(lo), h2_as_u32(hi));
+      const float2 fl = __half22float2(lo), fh = __half22float2(hi);
+      qsw += (fl.x + fl.y) + (fh.x + fh.y);
+    }
+    // precise-mode bias 16 Q'[tier][group c][q row g]: the sum of exactly the fp16 weighted
+    // values this lane's B fragments hold
+    if (part < 2) s_biasu[part * 4 * kBiasRows + c * kBiasRows + g] = 16.0f * qsw;
+  } else {
+    float qsum = 0.f;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) qsum += qv[e];
+    const __half qhi = __float2half_rn(qsum);
+    const __half qlo = __float2half_rn(qsum - __half2float(qhi));
+    reinterpret_cast<uint32_t*>(s_qu + 3 * kQSet)[lane] = h2_as_u32(__halves2half2(qhi, qlo));
   }
 }
 
@@ -881,69 +964,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   int mode;
   {
     const CtaIds id = cta_ids(a.Bc, a.b0);
-    const int l = id.l, b = id.b, h = id.h;
-    const uint16_t* qbase = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m) * kHeadDim + 32 * c;
-    auto load_q = [&](int row, float (&qv)[32]) {
-      if (row < a.m) {
-        const uint16_t* qrow = qbase + (int64_t)row * kHeadDim;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint4 x = reinterpret_cast<const uint4*>(qrow)[u];
-          const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __half22float2(u32_as_h2(w[e]));
-            qv[8 * u + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
-            qv[8 * u + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) qv[e] = 0.f;
-      }
-    };
     float qv[32];
-    load_q(g, qv);
-    float qmaxabs = 0.f;
-#pragma unroll
-    for (int e = 0; e < 32; ++e) qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) qmaxabs = fmaxf(qmaxabs, __shfl_xor_sync(0xffffffffu, qmaxabs, o));
-    const bool wide = qmaxabs > kWideQ || span_wide;
-    mode = wide ? kModeExact
-                : (kspan * qmaxabs > kPreciseSpanQ ? (a.m <= 4 ? kModePrecise : kModePrecise8) : kModeNormal);
-    // slot weights 2^(6-j) of K pair i: INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1)
-    auto slot_w = [&](int set, int i) {
-      return set == 0 ? exp2f((float)(6 - (i <= 4 ? 2 * i : 2 * (i - 5))))
-                      : (set == 1 ? exp2f((float)(6 - 4 * (i & 1))) : 1.0f);
-    };
-    if (warp < 3) {
-      float qsw = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
-        const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
-        // INT2 / INT4 sets also carry the fold of the fp16(1/qmax) rounding (see kdeq)
-        const float fold = warp == 0 ? kscale_fold(1.0f / 3.0f) : (warp == 1 ? kscale_fold(1.0f / 15.0f) : 1.0f);
-        const float x0 = slot_w(warp, i0) * fold, x1 = slot_w(warp, i1) * fold;
-        const __half2 lo = __floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0);
-        const __half2 hi = __floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1);
-        reinterpret_cast<uint2*>(s_q + warp * kQSet + 512 * (ks >> 1) + 16 * lane)[ks & 1] =
-            make_uint2(h2_as_u32(lo), h2_as_u32(hi));
-        const float2 fl = __half22float2(lo), fh = __half22float2(hi);
-        qsw += (fl.x + fl.y) + (fh.x + fh.y);
-      }
-      // precise-mode bias 16 Q'[tier][group c][q row g]: the sum of exactly the fp16 weighted
-      // values this lane's B fragments hold
-      if (warp < 2) s_bias[warp * 4 * kBiasRows + c * kBiasRows + g] = 16.0f * qsw;
-    } else {
-      float qsum = 0.f;
-#pragma unroll
-      for (int e = 0; e < 32; ++e) qsum += qv[e];
-      const __half qhi = __float2half_rn(qsum);
-      const __half qlo = __float2half_rn(qsum - __half2float(qhi));
-      reinterpret_cast<uint32_t*>(s_q + 3 * kQSet)[lane] = h2_as_u32(__halves2half2(qhi, qlo));
-    }
+    load_q_rows(a, id.l, id.b, id.h, g, c, qv);
+    mode = unit_mode(a, qv, span_wide, kspan);
+    stage_q_part(a, qv, warp < 3 ? warp : 3, s_q, s_bias, lane);
   }
   __syncthreads();
   if (threadIdx.x == 0 && tracing()) s_tr[2] = gtime();
@@ -1161,6 +1185,320 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   trace_out();
 }
 
+// ---- warp-plan decode (one 16-warp CTA per SM) -------------------------------------------
+// The layer's (sequence, kv head) units are split at WARP granularity: unit u gets n_u warps
+// (host plan, proportional to its tile cost, sum = 16 x SMs), the global warp list is
+// unit-major and CTA c runs warps [16c, 16c + 16) — one CTA per SM, so there are no co-resident
+// CTAs whose scheduling priorities differ (with 4 CTAs per SM the late-launched ones run up to
+// ~30% slower and set the layer's tail).  Every warp carries the same mix of tile kinds.  A CTA spans a few units: q is staged per unit, the warps of a unit merge in shared
+// memory, and a unit split over several CTAs merges their partials in the last one to arrive.
+// Each CTA's part of a unit is a contiguous share of the unit's tiles of each kind, in
+// proportion to the part's warps (adjacent tiles stream through one SM).
+constexpr int kWpWarps = 16;
+
+struct WpArgs {
+  DecArgs d;
+  const int32_t* prefix;  // [U + 1] first global warp of each unit (U = B * H per layer),
+                          // then [16 * ctas] the unit of every global warp
+  int U;
+  int max_slots;          // most units any CTA spans (q staging slots)
+  int max_ctas;           // most CTAs any unit spans (partial slots per unit)
+};
+
+__device__ __forceinline__ int wp_unit_of(const int32_t* prefix, int U, int gw) {  // prefix[u] <= gw < prefix[u+1]
+  int lo = 0, hi = U - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(prefix + mid) <= gw) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kWpWarps * 32, 1) decode_wp_kernel(const WpArgs w) {
+  const DecArgs& a = w.d;
+  extern __shared__ __align__(128) unsigned char s_dyn[];  // ring [16][kWarpRing] | q sets [slots][kQBytes]
+  unsigned char (*s_ring)[kWarpRing] = reinterpret_cast<unsigned char (*)[kWarpRing]>(s_dyn);
+  unsigned char* s_qall = s_dyn + kWpWarps * kWarpRing;
+  __shared__ float s_ml[kWpWarps][8][2];
+  __shared__ __align__(16) float s_biasall[8][2 * 4 * kBiasRows];
+  __shared__ int s_lastu[8];
+  __shared__ int64_t s_tr[12], s_tend[kWpWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int cta = blockIdx.x, l = blockIdx.z;
+  if (threadIdx.x == 0 && tracing()) { s_tr[0] = gtime(); s_tr[11] = 0; }
+  const int gw = cta * kWpWarps + warp;
+  const int32_t* wunit = w.prefix + w.U + 1;  // unit of every global warp (one load, no search)
+  const int u = __ldg(wunit + gw);
+  const int u0 = __ldg(wunit + cta * kWpWarps);
+  const int p0 = __ldg(w.prefix + u), p1 = __ldg(w.prefix + u + 1);
+  const int nw = p1 - p0;  // the unit's warps
+  // this CTA's part of the unit: its warps [w_lo, w_hi) of the unit take a contiguous share of
+  // each tile kind (adjacent tiles on one SM, as the 4-warp kernel's CTAs), interleaved inside
+  const int w_lo = max(p0, cta * kWpWarps) - p0, w_hi = min(p1, cta * kWpWarps + kWpWarps) - p0;
+  const int k = gw - p0 - w_lo, np = w_hi - w_lo;  // this warp's index among the part's np warps
+  const int slot = u - u0;
+  const int b = u / a.H, h = u % a.H;
+  int n2t, n4t;
+  TileSrc src;
+  {
+    const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
+    const int n2u = s0.y / kTile, n4u = s0.w / kTile;
+    const int a2 = (int)((int64_t)n2u * w_lo / nw), a4 = (int)((int64_t)n4u * w_lo / nw);
+    n2t = (int)((int64_t)n2u * w_hi / nw) - a2;
+    n4t = (int)((int64_t)n4u * w_hi / nw) - a4;
+    const int64_t unit = (int64_t)l * a.H + h;
+    src.c2 = (unit * a.K.rows2 + s0.x + (int64_t)a2 * kTile) / kTileRows * kBlock2 + 16 * lane;
+    src.c4 = (unit * a.K.rows4 + s0.z + (int64_t)a4 * kTile) / kTileRows * kBlock4 + 16 * lane;
+  }
+  MetaOff mo;
+  mo.k = -8 * lane;
+  mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
+  const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0]) + 16 * lane;
+  if (n2t > 0) prologue<2>(n2t, a, src, ring_l, k, np);
+  else prologue<4>(n4t, a, src, ring_l, k, np);
+  bool span_wide;
+  float kspan;
+  {
+    const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // span flags are [L][H][B]
+    span_wide = (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
+                (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
+    kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
+
+  // q staging: every unit slot of the CTA needs parts 0-3; the warps share the jobs
+  const int u_last = __ldg(wunit + cta * kWpWarps + kWpWarps - 1);
+  const int nslots = u_last - u0 + 1;
+  int mode;
+  {
+    float qv[32];
+    load_q_rows(a, l, b, h, g, c, qv);  // this warp's unit: its mode (and its staging jobs)
+    mode = unit_mode(a, qv, span_wide, kspan);
+    for (int j = warp; j < 4 * nslots; j += kWpWarps) {
+      const int uj = u0 + (j >> 2);
+      if (uj == u) {
+        stage_q_part(a, qv, j & 3, s_qall + (j >> 2) * kQBytes, s_biasall[j >> 2], lane);
+      } else {
+        float qj[32];
+        load_q_rows(a, l, uj / a.H, uj % a.H, g, c, qj);
+        stage_q_part(a, qj, j & 3, s_qall + (j >> 2) * kQBytes, s_biasall[j >> 2], lane);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && tracing()) s_tr[2] = gtime();
+  QS qs;
+  qs.base = (uint32_t)__cvta_generic_to_shared(s_qall + slot * kQBytes) + 16 * lane;
+  qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_qall + slot * kQBytes) + 3 * kQSet + 4 * lane;
+  PreciseOff po;
+  {
+    const int G0 = c >> 1, qa = (2 * c) & 3;
+    po.m0 = (g * 4 + G0) * 8 - 16 * lane;
+    po.m1 = (g * 4 + G0 + 2) * 8 - 16 * lane;
+    po.bias = (uint32_t)__cvta_generic_to_shared(s_biasall[slot]) + (G0 * kBiasRows + qa) * 4;
+    po.qoff = 16 * (((g & 3) * 4 + c) - lane);
+    po.qoff2 = 16 * ((((g & 3) + 4) * 4 + c) - lane);
+    po.hi_rows = c >= 2;
+    const bool in = (g >> 2) == (c & 1);
+    po.msk0 = in && (c >> 1) == 0 ? 0xffffffffu : 0u;
+    po.msk1 = in && (c >> 1) == 1 ? 0xffffffffu : 0u;
+  }
+  const uint32_t mg = kMagic16 | a.zero;
+
+  WarpState st;
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) st.acc[mt][0] = st.acc[mt][1] = st.acc[mt][2] = st.acc[mt][3] = 0.f;
+  st.lacc[0] = st.lacc[1] = 0.f;
+  st.lsq[0] = st.lsq[1] = 0.f;
+  st.mrun[0] = st.mrun[1] = -INFINITY;
+  st.lsum[0] = st.lsum[1] = 0.f;
+
+  // this warp's FP16-region tiles: the unit's, continuing the rotation after the quantized ones
+  auto fp16_part = [&](auto exact_tag) {
+    constexpr bool EXACT = decltype(exact_tag)::value;
+    const int off_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 4];
+    const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 5];
+    const int nft = (len_fp + kTile - 1) / kTile;
+    const int f_begin = (int)((int64_t)nft * w_lo / nw), f_end = (int)((int64_t)nft * w_hi / nw);
+    const int64_t unit = (int64_t)l * a.H + h;
+    const uint16_t* kf = a.K.fp + (unit * a.K.rows_fp + off_fp) * kHeadDim;
+    const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
+    for (int tf = f_begin + rotate(k, n2t + n4t, np); tf < f_end; tf += np) {
+      const int r = tf * kTile;
+      tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
+    }
+  };
+  if (mode == kModeExact) {
+    quantized_tiles<kModeExact>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
+    fp16_part(std::true_type{});
+  } else {
+    if (mode == kModePrecise) quantized_tiles<kModePrecise>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
+    else if (mode == kModePrecise8) quantized_tiles<kModePrecise8>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
+    else quantized_tiles<kModeNormal>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
+    fp16_part(std::false_type{});
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const float f = (float)(64 >> (2 * (mt & 3)));
+      st.acc[mt][0] *= f; st.acc[mt][1] *= f; st.acc[mt][2] *= f; st.acc[mt][3] *= f;
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    st.acc[mt][0] += st.lacc[0]; st.acc[mt][1] += st.lacc[1];
+    st.acc[mt][2] += st.lacc[0]; st.acc[mt][3] += st.lacc[1];
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
+    st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
+  }
+  st.lsum[0] += st.lsq[0];
+  st.lsum[1] += st.lsq[1];
+  if (lane == 0 && tracing()) s_tend[warp] = gtime();
+  __syncthreads();  // ring -> merge buffer reuse
+  if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
+  float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0]);
+  // column of (q row, d) in s_acc: d's low 4 bits XOR (g >> 1 | row/2 << 2), g = d / 16 — every
+  // store instruction of a warp hits 32 distinct banks (unswizzled: 16 lanes per bank)
+  auto swz = [](int row, int d) { return (d & ~15) | ((d ^ ((((d >> 4) & 7) >> 1) | ((row >> 1) << 2))) & 15); };
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    s_acc[warp][2 * c][swz(2 * c, 16 * g + mt)] = st.acc[mt][0];
+    s_acc[warp][2 * c + 1][swz(2 * c + 1, 16 * g + mt)] = st.acc[mt][1];
+    s_acc[warp][2 * c][swz(2 * c, 16 * g + 8 + mt)] = st.acc[mt][2];
+    s_acc[warp][2 * c + 1][swz(2 * c + 1, 16 * g + 8 + mt)] = st.acc[mt][3];
+  }
+  if (g == 0) {
+    s_ml[warp][2 * c][0] = st.mrun[0]; s_ml[warp][2 * c][1] = st.lsum[0];
+    s_ml[warp][2 * c + 1][0] = st.mrun[1]; s_ml[warp][2 * c + 1][1] = st.lsum[1];
+  }
+  __syncthreads();
+  // per (unit slot, d): merge the slot's warps of this CTA; a unit entirely inside this CTA
+  // writes its output, otherwise this CTA's partial goes to its slot of the unit's workspace
+  const int Hq = a.H * a.m;
+  float* ws_l = a.ws + (int64_t)l * w.U * w.max_ctas * a.m * kWsStride;
+  for (int p = threadIdx.x; p < nslots * kHeadDim; p += blockDim.x) {
+    const int sl = p / kHeadDim, d = p % kHeadDim;
+    const int us = u0 + sl;
+    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
+    const int wlo = max(q0, cta * kWpWarps) - cta * kWpWarps, whi = min(q1, cta * kWpWarps + kWpWarps) - cta * kWpWarps;
+    const int fc = q0 / kWpWarps, lc = (q1 - 1) / kWpWarps;
+    const int bs = us / a.H, hs = us % a.H;
+    for (int qi = 0; qi < a.m; ++qi) {
+      float ms = -INFINITY;
+      for (int ww = wlo; ww < whi; ++ww) ms = fmaxf(ms, s_ml[ww][qi][0]);
+      float acc = 0.f, lsum = 0.f;
+      const int dq = swz(qi, d);
+      for (int ww = wlo; ww < whi; ++ww) {
+        const float mw = s_ml[ww][qi][0];
+        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+        acc += f * s_acc[ww][qi][dq];
+        lsum += f * s_ml[ww][qi][1];
+      }
+      if (fc == lc) {
+        const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
+        if (a.partial_out) {
+          float* dst = a.partial_out + row * kPartStride;
+          dst[d] = acc;
+          if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+        } else {
+          a.out[l * a.o_sl + bs * a.o_sb + (int64_t)(hs * a.m + qi) * kHeadDim + d] =
+              __half_as_ushort(__float2half_rn(acc / lsum));
+        }
+      } else {
+        float* dst = ws_l + (((int64_t)us * w.max_ctas + (cta - fc)) * a.m + qi) * kWsStride;
+        dst[d] = acc;
+        if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && tracing()) s_tr[9] = gtime();
+  // arrival per split unit: the CTA that completes a unit's set of partials merges them
+  if (threadIdx.x < nslots) {
+    const int us = u0 + threadIdx.x;
+    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
+    const int fc = q0 / kWpWarps, lc = (q1 - 1) / kWpWarps;
+    int last = 0;
+    if (fc != lc) {
+      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[(int64_t)l * w.U + us]);
+      const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
+      last = prev == (uint32_t)(lc - fc);
+      if (last) ctr.store(0u, cuda::memory_order_relaxed);
+    }
+    s_lastu[threadIdx.x] = last;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && tracing()) {
+    s_tr[10] = gtime();
+    int nl = 0;
+    for (int i = 0; i < nslots; ++i) nl += s_lastu[i];
+    s_tr[11] = nl;
+  }
+  // units this CTA completes, one at a time: stage the unit's partials (every CTA's rows, one L2
+  // round trip) in shared memory (the ring) when they fit, then merge per (q row, d)
+  float* s_part = reinterpret_cast<float*>(&s_ring[0][0]);
+  for (int sl = 0; sl < nslots; ++sl) {
+    if (!s_lastu[sl]) continue;
+    const int us = u0 + sl;
+    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
+    const int nc = (q1 - 1) / kWpWarps - q0 / kWpWarps + 1;
+    const int bs = us / a.H, hs = us % a.H;
+    const float* src_p = ws_l + (int64_t)us * w.max_ctas * a.m * kWsStride;  // [ctas][m][stride]
+    const bool staged = nc * a.m * kWsStride * (int)sizeof(float) <= kWpWarps * kWarpRing;
+    if (staged) {
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_part);
+      const int nvec = nc * a.m * kWsStride / 4;
+      for (int i = threadIdx.x; i < nvec; i += blockDim.x) cp_async16(sbase + 16 * i, src_p + 4 * i);
+      cp_commit();
+      cp_wait<0>();
+      __syncthreads();
+    }
+    const float* pbase = staged ? s_part : src_p;
+    for (int p = threadIdx.x; p < a.m * kHeadDim; p += blockDim.x) {
+      const int qi = p / kHeadDim, d = p % kHeadDim;
+      const float* pp = pbase + qi * kWsStride;
+      float ms = -INFINITY;
+      for (int s2 = 0; s2 < nc; ++s2) ms = fmaxf(ms, pp[s2 * a.m * kWsStride + kHeadDim]);
+      float acc = 0.f, lsum = 0.f;
+      for (int s2 = 0; s2 < nc; ++s2) {
+        const float* ps = pp + s2 * a.m * kWsStride;
+        const float mw = ps[kHeadDim];
+        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+        acc += f * ps[d];
+        lsum += f * ps[kHeadDim + 1];
+      }
+      const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
+      if (a.partial_out) {
+        float* dst = a.partial_out + row * kPartStride;
+        dst[d] = acc;
+        if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+      } else {
+        a.out[l * a.o_sl + bs * a.o_sb + (int64_t)(hs * a.m + qi) * kHeadDim + d] =
+            __half_as_ushort(__float2half_rn(acc / lsum));
+      }
+    }
+    __syncthreads();  // s_part reuse by the next unit
+  }
+  if (threadIdx.x == 0 && tracing()) {
+    int64_t tmax = 0;
+    for (int i = 0; i < kWpWarps; ++i) tmax = max(tmax, s_tend[i]);
+    s_tr[3] = tmax;
+    s_tr[4] = gtime();
+    int64_t* dst = g_trace + 16 * atomicAdd(&g_trace_n, 1ull);
+    for (int i = 0; i < 5; ++i) dst[i] = s_tr[i];
+    for (int i = 8; i < 12; ++i) dst[i] = s_tr[i];
+    for (int i = 0; i < 4; ++i) dst[12 + i] = s_tend[i * 5];
+    dst[5] = smid();
+    dst[6] = (int64_t)cta | ((int64_t)u0 << 40);
+    dst[7] = (int64_t)a.q;
+  }
+}
+
 // Cross-rank merge of gathered partials [P][rows][130] -> out fp16 [rows][128].
 __global__ void lse_merge_kernel(const float* __restrict__ parts, int P, int64_t rows,
                                  uint16_t* __restrict__ out) {
@@ -1289,6 +1627,82 @@ int32_t ckv_decode_set_trace(int64_t* buf) {
   unsigned long long z = 0;
   if (cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)) != cudaSuccess ||
       cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return CKV_ERR_CUDA;
+  }
+  return CKV_OK;
+}
+
+static size_t g_wp_smem = 0;
+
+int64_t ckv_decode_wp_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
+                                      int32_t max_ctas) {
+  const int64_t units = (int64_t)layers * batch * kv_heads;
+  return cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256 +
+         units * (int64_t)(max_ctas > 0 ? max_ctas : 1) * m * kWsStride * (int64_t)sizeof(float);
+}
+
+int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                                ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                                int32_t layers, int32_t batch, int32_t kv_heads, int32_t m, float scale,
+                                const int32_t* warp_prefix, int32_t ctas, int32_t max_slots,
+                                int32_t max_ctas, void* workspace, uint16_t* out, int64_t o_s_layer,
+                                int64_t o_s_batch, float* partial_out, int32_t flags, void* stream) {
+  if (layers < 0 || batch < 0 || kv_heads < 0 || ctas < 1) return CKV_ERR_ARG;
+  if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
+  if (max_slots < 1 || max_slots > 8 || max_ctas < 1) return CKV_ERR_UNSUPPORTED;
+  if (!q || !seq || !warp_prefix || !workspace || (!out && !partial_out)) return CKV_ERR_ARG;
+  if ((q_s_layer % 8) || (q_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
+  if (layers * batch * kv_heads == 0) return CKV_OK;
+  {
+    const char* k2 = reinterpret_cast<const char*>(k_arena.codes2);
+    const char* k4 = reinterpret_cast<const char*>(k_arena.codes4);
+    const bool ok2 = k_arena.rows2 == 0 ||
+                     (reinterpret_cast<const char*>(v_arena.codes2) == k2 + kTileBytes2 &&
+                      reinterpret_cast<const char*>(k_arena.meta2) == k2 + 2 * kTileBytes2 &&
+                      reinterpret_cast<const char*>(v_arena.meta2) == k2 + 2 * kTileBytes2 + kTileBytesMeta);
+    const bool ok4 = k_arena.rows4 == 0 ||
+                     (reinterpret_cast<const char*>(v_arena.codes4) == k4 + kTileBytes4 &&
+                      reinterpret_cast<const char*>(k_arena.meta4) == k4 + 2 * kTileBytes4 &&
+                      reinterpret_cast<const char*>(v_arena.meta4) == k4 + 2 * kTileBytes4 + kTileBytesMeta);
+    if (!ok2 || !ok4 || k_arena.rows2 != v_arena.rows2 || k_arena.rows4 != v_arena.rows4) return CKV_ERR_ARG;
+  }
+  WpArgs w;
+  DecArgs& a = w.d;
+  a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
+  a.K = k_arena; a.V = v_arena; a.seq = seq;
+  a.L = layers; a.B = batch; a.H = kv_heads; a.m = m; a.splits = 1;
+  a.b0 = 0; a.Bc = batch;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  const int64_t units = (int64_t)layers * batch * kv_heads;
+  a.counters = reinterpret_cast<uint32_t*>(workspace);
+  a.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256);
+  a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
+  a.partial_out = partial_out;
+  a.zero = 0u;
+  w.prefix = warp_prefix;
+  w.U = batch * kv_heads;
+  w.max_slots = max_slots;
+  w.max_ctas = max_ctas;
+  const size_t smem = (size_t)kWpWarps * kWarpRing + (size_t)max_slots * kQBytes;
+  if (smem > g_wp_smem) {
+    if (cudaFuncSetAttribute(decode_wp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return CKV_ERR_CUDA;
+    }
+    g_wp_smem = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ctas, 1u, (unsigned)layers);
+  cfg.blockDim = dim3(kWpWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (flags & CKV_DECODE_PDL) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, decode_wp_kernel, w) != cudaSuccess) {
     (void)cudaGetLastError();
     return CKV_ERR_CUDA;
   }

@@ -1,0 +1,99 @@
+"""The warp-plan decode schedule (ckv_decode_attention_wp: one 16-warp CTA per SM, units split
+at warp granularity, multi-CTA units merged by the last CTA to arrive) against the reference
+algorithm (oracle) and against the split schedule, on unit counts from a few (many CTAs per
+unit) to many (several units per CTA), with m = 1 / 4 / 8, decode tokens, partials, per-layer
+PDL launches and CUDA-graph replay."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ckv_oracle as O
+from paper_2503_23294_b200 import batched, retrieval
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def _search(tiers):
+    return retrieval.assign_tiers_batched(tiers.astype(np.float64), np.tile([[0.5, 1.5]], (tiers.shape[0], 1)))
+
+
+def _case(seed, L, B, H, m, N, tail, p=(0.8, 0.15, 0.05)):
+    rng = np.random.default_rng(seed)
+    T = N * 32 + tail
+    k = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
+    q = rng.normal(size=(L, B, H * m, 128)).astype(np.float16)
+    tiers = rng.choice([0, 1, 2], size=(B, N), p=p).astype(np.uint8)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers),
+                                        decode_capacity=16)
+    return cache, k, v, q, tiers
+
+
+def _check(out, k, v, q, tiers, m, units):
+    for (l, b, h) in units:
+        oc = O.build_cache(k[l, b, :, h].astype(np.float64), v[l, b, :, h].astype(np.float64), tiers[b], 32, 32)
+        ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+        got = out[l, b, h * m:(h + 1) * m]
+        err = np.max(np.abs(got - ref))
+        assert err <= TOL and err / np.max(np.abs(ref)) <= TOL, (l, b, h, err)
+
+
+@pytest.mark.parametrize("B,H,m,N", [(1, 2, 4, 300), (2, 8, 4, 60), (8, 8, 1, 9), (3, 5, 8, 40), (64, 8, 4, 6)])
+def test_warp_plan_matches_oracle_and_split(B, H, m, N):
+    L = 2
+    cache, k, v, q, tiers = _case(100 + B + H + m, L, B, H, m, N, 7)
+    plan = cache.warp_plan()
+    assert plan is not None
+    prefix, ctas, slots, max_ctas = plan
+    p = prefix.cpu().numpy()[:B * H + 1]
+    assert p[0] == 0 and p[-1] == 16 * ctas and (np.diff(p) >= 2).all()
+    qd = torch.from_numpy(q).cuda()
+    out = cache.decode(qd).float().cpu().numpy()            # warp plan (whole batch, no splits)
+    ref_split = cache.decode(qd, splits=3).float().cpu().numpy()
+    assert np.max(np.abs(out - ref_split)) < 2e-3
+    rng = np.random.default_rng(7)
+    units = {(l, int(rng.integers(B)), int(rng.integers(H))) for l in range(L) for _ in range(3)}
+    _check(out, k, v, q, tiers, m, units)
+    # partials + LSE merge give the same rows
+    part = cache.decode_partial(qd)
+    merged = batched.lse_merge(part[None]).view(q.shape).float().cpu().numpy()
+    assert np.max(np.abs(merged - out)) < 2e-3
+
+
+def test_warp_plan_per_layer_graph_and_appends():
+    L, B, H, m = 3, 2, 4, 4
+    cache, k, v, q, tiers = _case(200, L, B, H, m, 50, 3)
+    qd = torch.from_numpy(q).cuda()
+    out = torch.empty_like(qd)
+    g = cache.decode_graph(qd, out)      # per-layer PDL-chained launches of the warp-plan kernel
+    rng = np.random.default_rng(8)
+    for _ in range(3):
+        kn = torch.from_numpy(rng.normal(size=(L, B, H, 128)).astype(np.float16)).cuda()
+        vn = torch.from_numpy(rng.normal(size=(L, B, H, 128)).astype(np.float16)).cuda()
+        cache.append(kn, vn)
+        g.replay()
+        want = torch.empty_like(qd)
+        for l in range(L):
+            cache.decode(qd[l:l + 1], out=want[l:l + 1], layer=l, pdl=l > 0)
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)   # deterministic: graph replay == eager, bit for bit
+        assert torch.equal(cache.decode(qd), want)
+
+
+def test_warp_plan_outlier_precise_and_exact_units():
+    L, B, H, m = 1, 2, 3, 8
+    rng = np.random.default_rng(300)
+    N = 40
+    T = N * 32 + 5
+    k = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
+    k[..., [3, 40, 77, 100]] *= 8          # wide K groups: precise path (two passes, m = 8)
+    k[0, 1, 10, 2, 5] = 20000.0            # one unit with a huge scale: exact mode
+    v = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
+    q = (rng.normal(size=(L, B, H * m, 128)) * 3).astype(np.float16)
+    tiers = rng.choice([0, 1, 2], size=(B, N), p=(0.7, 0.25, 0.05)).astype(np.uint8)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers))
+    out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
+    _check(out, k, v, q, tiers, m, [(0, b, h) for b in range(B) for h in range(H)])

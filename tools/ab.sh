@@ -9,7 +9,7 @@ for n in "${names[@]}"; do
   CKV_LIB_PATH=$PWD/$lib timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-prefill "${extra[@]}" 2>gpurun_out/ab_$n.err | tail -1 | python -c "
 import json,sys
 try:
-    d=json.loads(sys.stdin.read()); print('$n', {k:d.get(k) for k in ['value','ms_per_step','single_launch_all_layers_gbs','eager_launches_gbs']}, 'frac', d['roofline']['frac'], 'e2e', d['e2e']['value'], 'splits', d['config']['splits'], d['clocks']['sm_mhz'], d['clocks']['reasons'])
+    d=json.loads(sys.stdin.read()); print('$n', {k:d.get(k) for k in ['value','ms_per_step','single_launch_all_layers_gbs','eager_launches_gbs']}, 'frac', d['roofline']['frac'], 'e2e', d['e2e']['value'], 'splits', d['config']['splits'], d['config'].get('schedule'), d['clocks']['sm_mhz'], d['clocks']['reasons'])
 except Exception as e: print('$n FAILED', e)
 "
 done
