@@ -275,6 +275,23 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def pick_splits(args, cache, m, layers=1):
+    """Decode schedule for a bench run: the warp plan (splits None) unless --schedule split or
+    --splits is given, or the cache has no warp plan."""
+    cache.schedule = args.schedule
+    if args.schedule == "wp" and args.splits is None and getattr(args, "chains", 1) == 1 and cache.warp_plan() is not None:
+        return None
+    return args.splits or cache.default_splits(m, layers)
+
+
+def schedule_desc(cache, splits):
+    if splits is None:
+        p = cache.warp_plan()
+        nw = np.diff(p[0].cpu().numpy()[:cache.B * cache.H + 1])
+        return f"warp plan: {len(nw)} units x {int(nw.min())}-{int(nw.max())} warps, {p[1]} CTAs"
+    return f"split: {splits} CTAs of 4 warps per unit"
+
+
 def build_cfg2(torch, dev, rank):
     from paper_2503_23294_b200 import batched, retrieval
 
@@ -453,7 +470,7 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
     q_all = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
     q = q_all[:, :, h0 * m:h1 * m].contiguous()
     Hq = (h1 - h0) * m
-    splits = args.splits or cache.default_splits(m, 1)
+    splits = pick_splits(args, cache, m)
 
     def barrier():
         if world > 1:
@@ -570,7 +587,7 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
     res.update({
         "value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
         "tokens_per_s": round(B / (ms * 1e-3), 1), "algorithmic_bytes_per_step": int(step_bytes),
-        "splits": splits, "split": split,
+        "splits": splits, "split": split, "schedule": schedule_desc(cache, splits),
         "parallelism": f"{'seq-split' if split == 'seq' else 'head-shard'} x{world}",
         "per_rank_gbs": round(my_bytes / (ms * 1e-3) / 1e9, 1),
         "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
@@ -602,7 +619,8 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
                        "launch": ("per-layer decode_partial (40 PDL-chained launches, one CUDA graph) + all_gather "
                                   "+ merge" if r["split"] == "seq" else
                                   "per-layer decode (40 PDL-chained launches, one CUDA graph), no collective"),
-                       "splits": r["splits"], "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
+                       "splits": r["splits"], "schedule": r["schedule"],
+                       "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
             "tokens_per_s": r["tokens_per_s"],
             "algorithmic_bytes_per_step": r["algorithmic_bytes_per_step"],
             "roofline": {"bound": "hbm", "achieved": r["per_rank_gbs"], "peak": peak, "unit": "GB/s",
@@ -648,7 +666,7 @@ def run_cfg4(args, torch, dist, dev, rank, world, local):
     g.manual_seed(11 + rank)
     q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
     out = torch.empty_like(q)
-    splits = args.splits or cache.default_splits(m, 1)
+    splits = pick_splits(args, cache, m)
     my_bytes = cache.algorithmic_bytes(m)
 
     graph = cache.decode_graph(q, out, splits=splits)  # the step's 32 PDL-chained launches
@@ -708,7 +726,7 @@ def run_cfg4(args, torch, dist, dev, rank, world, local):
                        "global_batch": Bg, "seq_len": T, "parallelism": f"batch-shard x{world}",
                        "tier_fractions_int2_int4_fp16": [round(float(x), 4) for x in frac],
                        "launch": "per-layer (32 PDL-chained launches per step, replayed as one CUDA graph)",
-                       "splits": splits,
+                       "splits": splits, "schedule": schedule_desc(cache, splits),
                        "l2": "inputs larger than L2"},
             "tokens_per_s": round(Bg / (ms * 1e-3), 1),
             "algorithmic_bytes_per_step": int(step_bytes),
@@ -745,7 +763,7 @@ def run_cfg1(args, torch, dist, dev, rank, world, local):
     del k, v
     q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
     out = torch.empty_like(q)
-    splits = args.splits or cache.default_splits(m)
+    splits = pick_splits(args, cache, m, 1)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(max(args.warmup, 3)):
         cache.decode(q, splits=splits, out=out)
@@ -785,6 +803,7 @@ def run_cfg1(args, torch, dist, dev, rank, world, local):
             "config": {"workload": "cfg1: Llama-2-7B 1 layer x 32 MHA heads d128, 4K ctx, batch 1",
                        "global_batch": B * world, "seq_len": T, "parallelism": f"replicas x{world}",
                        "tier_chunks_int2_int4_fp16": [int(x) for x in counts], "splits": splits,
+                       "schedule": schedule_desc(cache, splits),
                        "l2": "L2 flushed (256 MB write) before every timed launch"},
             "us_per_decode": round(ms * 1e3, 2),
             "algorithmic_bytes_per_step": int(nbytes),
@@ -954,9 +973,8 @@ def main():
     cache, q, search = build_cfg2(torch, dev, rank)
     L, B = cache.L, cache.B
     m = q.shape[2] // cache.H
-    cache.schedule = args.schedule
-    wp = args.schedule == "wp" and args.chains == 1 and cache.warp_plan() is not None
-    splits = None if wp else (args.splits or cache.default_splits(m, 1))
+    splits = pick_splits(args, cache, m)
+    wp = splits is None
     out = torch.empty_like(q)
     step_bytes = cache.algorithmic_bytes(m)
 
@@ -1027,11 +1045,12 @@ def main():
 
     # single-launch (all 32 layers in one grid) figure for the same cache
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    single_splits = args.splits or cache.default_splits(m, L)  # split schedule: the faster one in one launch
     for _ in range(3):
-        cache.decode(q, out=out, splits=args.splits)
+        cache.decode(q, out=out, splits=single_splits)
     e2.record()
     for _ in range(args.steps):
-        cache.decode(q, out=out, splits=args.splits)
+        cache.decode(q, out=out, splits=single_splits)
     e3.record()
     torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
@@ -1098,13 +1117,7 @@ def main():
         torch.cuda.empty_cache()
         prefill = bench_prefill(torch, dev)
 
-    if wp:
-        wprefix = cache.warp_plan()[0].cpu().numpy()[:cache.B * cache.H + 1]
-        nw = np.diff(wprefix)
-        sched_desc = (f"warp plan: {len(wprefix) - 1} units x {int(nw.min())}-{int(nw.max())} warps, "
-                      f"{cache.warp_plan()[1]} CTAs of 16 warps (one per SM)")
-    else:
-        sched_desc = f"split: {splits} CTAs of 4 warps per unit"
+    sched_desc = schedule_desc(cache, splits)
     if rank == 0:
         peak, peak_kind = measured_peak_gbs()
         per_launch_bytes = step_bytes / L

@@ -276,6 +276,8 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
  * zero-filled once.  Outputs as ckv_decode_attention (out or partial_out). */
 int64_t ckv_decode_wp_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                                       int32_t max_ctas);
+/* Warps per CTA of the warp-plan kernel (16: one CTA per SM). */
+int32_t ckv_decode_wp_cta_warps(void);
 int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
                                 ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
                                 int32_t layers, int32_t batch, int32_t kv_heads, int32_t m, float scale,

@@ -193,8 +193,6 @@ class BatchedKVCache:
                 best, best_cost = s, cost
         return best
 
-    WP_WARPS = 16   # warps per CTA of the warp-plan decode kernel (one CTA per SM)
-
     def warp_plan(self):
         """Warp-plan schedule (ckv_decode_attention_wp): unit u = b*H + h gets n_u warps in
         proportion to its tile cost (INT2 1, INT4 1.06, FP16-region 2 per 16-token tile), at
@@ -204,8 +202,10 @@ class BatchedKVCache:
         holds the prefix, then the unit of every global warp."""
         if self._wp is None:
             self._wp = False
+            cw = _lib.load().ckv_decode_wp_cta_warps()  # warps per CTA (16 / cw CTAs per SM)
             n_sm = _num_sms()
-            T = self.WP_WARPS * n_sm
+            T = 16 * n_sm
+            n_cta = T // cw
             U = self.B * self.H
             s = self.seq_host.astype(np.int64)
             cost_b = s[:, 1] // TILE + 1.06 * (s[:, 3] // TILE) + 2.0 * (-(-s[:, 5] // TILE))
@@ -222,16 +222,16 @@ class BatchedKVCache:
                     j = int(np.argmax(np.where(n > 2, n - raw, -np.inf)))
                     n[j] -= 1
                 prefix = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
-                first, last = prefix[:-1] // self.WP_WARPS, (prefix[1:] - 1) // self.WP_WARPS
+                first, last = prefix[:-1] // cw, (prefix[1:] - 1) // cw
                 max_ctas = int((last - first + 1).max())
-                starts = np.arange(n_sm) * self.WP_WARPS
+                starts = np.arange(n_cta) * cw
                 u_lo = np.searchsorted(prefix, starts, side="right") - 1
-                u_hi = np.searchsorted(prefix, starts + self.WP_WARPS - 1, side="right") - 1
+                u_hi = np.searchsorted(prefix, starts + cw - 1, side="right") - 1
                 max_slots = int((u_hi - u_lo + 1).max())
                 if max_slots <= 8:
                     wunit = np.repeat(np.arange(U), n)  # unit of every global warp
                     table = np.concatenate([prefix, wunit]).astype(np.int32)
-                    self._wp = (torch.from_numpy(table).to(self.device), n_sm, max_slots, max_ctas)
+                    self._wp = (torch.from_numpy(table).to(self.device), n_cta, max_slots, max_ctas)
         return self._wp or None
 
     def _wp_workspace(self, m, layers, layer, max_ctas):
@@ -634,7 +634,6 @@ class DecodeLoop:
         self.k_new = torch.zeros((L, B, H, HEAD_DIM), dtype=torch.float16, device=dev)
         self.v_new = torch.zeros_like(self.k_new)
         streams = [torch.cuda.Stream(device=dev) for _ in cache._chain_ranges(chains)]
-        splits = cache.default_splits(m, 1) if splits is None else splits
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm-up (workspaces, attributes) without appending

@@ -1194,7 +1194,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
 // memory, and a unit split over several CTAs merges their partials in the last one to arrive.
 // Each CTA's part of a unit is a contiguous share of the unit's tiles of each kind, in
 // proportion to the part's warps (adjacent tiles stream through one SM).
-constexpr int kWpWarps = 16;
+#ifndef CKV_WP_WARPS
+#define CKV_WP_WARPS 16
+#endif
+constexpr int kWpWarps = CKV_WP_WARPS;  // warps per CTA; 16 / kWpWarps CTAs per SM
 
 struct WpArgs {
   DecArgs d;
@@ -1215,7 +1218,7 @@ __device__ __forceinline__ int wp_unit_of(const int32_t* prefix, int U, int gw) 
   return lo;
 }
 
-__global__ void __launch_bounds__(kWpWarps * 32, 1) decode_wp_kernel(const WpArgs w) {
+__global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel(const WpArgs w) {
   const DecArgs& a = w.d;
   extern __shared__ __align__(128) unsigned char s_dyn[];  // ring [16][kWarpRing] | q sets [slots][kQBytes]
   unsigned char (*s_ring)[kWarpRing] = reinterpret_cast<unsigned char (*)[kWarpRing]>(s_dyn);
@@ -1634,6 +1637,8 @@ int32_t ckv_decode_set_trace(int64_t* buf) {
 }
 
 static size_t g_wp_smem = 0;
+
+int32_t ckv_decode_wp_cta_warps(void) { return kWpWarps; }
 
 int64_t ckv_decode_wp_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                                       int32_t max_ctas) {

@@ -49,7 +49,8 @@ def test_warp_plan_matches_oracle_and_split(B, H, m, N):
     assert plan is not None
     prefix, ctas, slots, max_ctas = plan
     p = prefix.cpu().numpy()[:B * H + 1]
-    assert p[0] == 0 and p[-1] == 16 * ctas and (np.diff(p) >= 2).all()
+    from paper_2503_23294_b200 import _lib
+    assert p[0] == 0 and p[-1] == _lib.load().ckv_decode_wp_cta_warps() * ctas and (np.diff(p) >= 2).all()
     qd = torch.from_numpy(q).cuda()
     out = cache.decode(qd).float().cpu().numpy()            # warp plan (whole batch, no splits)
     ref_split = cache.decode(qd, splits=3).float().cpu().numpy()
