@@ -279,7 +279,8 @@ def pick_splits(args, cache, m, layers=1):
     """Decode schedule for a bench run: the warp plan (splits None) unless --schedule split or
     --splits is given, or the cache has no warp plan."""
     cache.schedule = args.schedule
-    if args.schedule == "wp" and args.splits is None and getattr(args, "chains", 1) == 1 and cache.warp_plan() is not None:
+    if (args.schedule != "split" and args.splits is None and getattr(args, "chains", 1) == 1
+            and cache._use_wp(m, None, None, None) is not None):
         return None
     return args.splits or cache.default_splits(m, layers)
 
@@ -907,9 +908,10 @@ def main():
     ap.add_argument("--no-tpot", action="store_true", help="skip the 128-step decode loop (TPOT)")
     ap.add_argument("--no-split-kv", action="store_true",
                     help="N>1 default line: skip the cfg3 split_kv / head_shard sub-objects")
-    ap.add_argument("--schedule", choices=["wp", "split"], default="wp",
+    ap.add_argument("--schedule", choices=["auto", "wp", "split"], default="auto",
                     help="decode schedule of whole-batch launches: wp = warp plan (one 16-warp CTA per SM, "
-                         "units split at warp granularity), split = 4-warp CTAs with --splits per unit")
+                         "units split at warp granularity), split = 4-warp CTAs with --splits per unit, "
+                         "auto = the warp plan unless the cache has fewer than 8 tiles per warp")
     ap.add_argument("--chains", type=int, default=1,
                     help="micro-batch chains per decode step (cfg2/cfg4): the batch is split into this "
                          "many sequence ranges, each its own chain of per-layer launches on its own "

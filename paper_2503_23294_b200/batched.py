@@ -107,8 +107,9 @@ class BatchedKVCache:
         self._perm = None
         self._wp = None
         # decode schedule of whole-batch launches: "wp" (warp plan: one 16-warp CTA per SM,
-        # units split at warp granularity) or "split" (4-warp CTAs, `splits` per unit)
-        self.schedule = "wp"
+        # units split at warp granularity), "split" (4-warp CTAs, `splits` per unit) or "auto"
+        # (the warp plan unless the cache is small: fewer than 8 tiles per warp)
+        self.schedule = "auto"
         self._any_empty = bool((self.total_tokens() == 0).any())
 
     # -- construction ------------------------------------------------------------------
@@ -251,9 +252,16 @@ class BatchedKVCache:
 
     def _use_wp(self, m, seqs, splits, schedule):
         sched = self.schedule if schedule is None else schedule
-        if sched != "wp" or seqs is not None or splits is not None or m > MAX_Q_PER_KV:
+        if sched == "split" or seqs is not None or splits is not None or m > MAX_Q_PER_KV:
             return None
+        if sched == "auto" and self._tiles_per_warp() < 8:
+            return None  # small caches (a few tiles per warp): the split schedule's latency wins
         return self.warp_plan()
+
+    def _tiles_per_warp(self):
+        s = self.seq_host.astype(np.int64)
+        tiles = self.H * int((s[:, 1] // TILE + s[:, 3] // TILE + -(-s[:, 5] // TILE)).sum())
+        return tiles / (16 * _num_sms())
 
     def _workspace(self, m, splits, layers, layer):
         """Zero-initialised decode workspace (split partials + self-resetting arrival counters).

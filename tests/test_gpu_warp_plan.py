@@ -29,6 +29,7 @@ def _case(seed, L, B, H, m, N, tail, p=(0.8, 0.15, 0.05)):
     tiers = rng.choice([0, 1, 2], size=(B, N), p=p).astype(np.uint8)
     cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers),
                                         decode_capacity=16)
+    cache.schedule = "wp"  # force the warp plan (these caches are below the "auto" size threshold)
     return cache, k, v, q, tiers
 
 
@@ -96,5 +97,6 @@ def test_warp_plan_outlier_precise_and_exact_units():
     q = (rng.normal(size=(L, B, H * m, 128)) * 3).astype(np.float16)
     tiers = rng.choice([0, 1, 2], size=(B, N), p=(0.7, 0.25, 0.05)).astype(np.uint8)
     cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers))
+    cache.schedule = "wp"
     out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
     _check(out, k, v, q, tiers, m, [(0, b, h) for b in range(B) for h in range(H)])

@@ -17,12 +17,14 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--prefill", action="store_true")
     ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--schedule", choices=["auto", "wp", "split"], default="auto")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     bench.CFG2["layers"] = args.layers
     cache, q, _ = bench.build_cfg2(torch, dev, 0)
     m = q.shape[2] // cache.H
-    splits = cache.default_splits(m, 1)
+    splits = None if args.schedule != "split" else cache.default_splits(m, 1)  # None: the cache's schedule
+    cache.schedule = args.schedule
     out = torch.empty_like(q)
     for l in range(cache.L):  # warm-up outside the profiled range
         cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
