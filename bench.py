@@ -1057,6 +1057,7 @@ def main():
     torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
 
+    sched_desc = schedule_desc(cache, splits)
     # parity of the timed cache: the graph step's output for sampled units vs the reference
     graph.replay()
     torch.cuda.synchronize()
@@ -1119,7 +1120,6 @@ def main():
         torch.cuda.empty_cache()
         prefill = bench_prefill(torch, dev)
 
-    sched_desc = schedule_desc(cache, splits)
     if rank == 0:
         peak, peak_kind = measured_peak_gbs()
         per_launch_bytes = step_bytes / L

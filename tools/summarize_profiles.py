@@ -106,7 +106,8 @@ def main():
              "(`tools/gpu_round.sh`); one launch each.  Launch list: "
              f"`{tag}_launches.csv` (`--metrics gpu__time_duration.sum`).", ""]
     traffic = {}
-    for rep, key in (("decode_prof.ncu-rep", "decode_kernel"), ("quant_prof.ncu-rep", "reorder_quantize_pack")):
+    for rep, key in (("decode_prof.ncu-rep", "decode_kernel"), ("decode_split_prof.ncu-rep", "decode_kernel_split"),
+                     ("quant_prof.ncu-rep", "reorder_quantize_pack")):
         path = os.path.join(OUT, rep)
         if not os.path.exists(path):
             continue
