@@ -108,7 +108,8 @@ class BatchedKVCache:
         self._wp = None
         # decode schedule of whole-batch launches: "wp" (warp plan: one 16-warp CTA per SM,
         # units split at warp granularity), "split" (4-warp CTAs, `splits` per unit) or "auto"
-        # (the warp plan unless the cache is small: fewer than 8 tiles per warp)
+        # (the warp plan unless the cache is small, fewer than 8 tiles per warp, or more than half
+        # of its bytes are FP16)
         self.schedule = "auto"
         self._any_empty = bool((self.total_tokens() == 0).any())
 
@@ -254,9 +255,18 @@ class BatchedKVCache:
         sched = self.schedule if schedule is None else schedule
         if sched == "split" or seqs is not None or splits is not None or m > MAX_Q_PER_KV:
             return None
-        if sched == "auto" and self._tiles_per_warp() < 8:
-            return None  # small caches (a few tiles per warp): the split schedule's latency wins
+        if sched == "auto" and (self._tiles_per_warp() < 8 or self._fp16_byte_share() > 0.5):
+            # small caches (a few tiles per warp): the split schedule's latency wins; mostly-FP16
+            # caches are HBM bound, where SMs stream at unequal rates and the split schedule's
+            # waves of CTAs rebalance dynamically (cfg4 all-FP16: split 6375 vs warp plan 5823 GB/s)
+            return None
         return self.warp_plan()
+
+    def _fp16_byte_share(self):
+        s = self.seq_host.astype(np.float64)
+        fp = 512.0 * s[:, 5].sum()
+        tot = 96.0 * s[:, 1].sum() + 160.0 * s[:, 3].sum() + fp
+        return fp / tot if tot > 0 else 0.0
 
     def _tiles_per_warp(self):
         s = self.seq_host.astype(np.int64)

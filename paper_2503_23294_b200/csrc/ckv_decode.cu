@@ -1224,6 +1224,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   unsigned char (*s_ring)[kWarpRing] = reinterpret_cast<unsigned char (*)[kWarpRing]>(s_dyn);
   unsigned char* s_qall = s_dyn + kWpWarps * kWarpRing;
   __shared__ float s_ml[kWpWarps][8][2];
+  __shared__ float s_wf[kWpWarps][8], s_sm[8][8][2];
   __shared__ __align__(16) float s_biasall[8][2 * 4 * kBiasRows];
   __shared__ int s_lastu[8];
   __shared__ int64_t s_tr[12], s_tend[kWpWarps];
@@ -1268,6 +1269,13 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     span_wide = (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
                 (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
     kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
+  }
+  // pull this warp's q rows into L2 while the previous launch drains (L2 is the point of
+  // coherence: a producer writing q before the wait below still wins; a prefetch reads nothing
+  // into this SM)
+  if (g < a.m) {
+    const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow));
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
@@ -1380,43 +1388,63 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     s_ml[warp][2 * c + 1][0] = st.mrun[1]; s_ml[warp][2 * c + 1][1] = st.lsum[1];
   }
   __syncthreads();
-  // per (unit slot, d): merge the slot's warps of this CTA; a unit entirely inside this CTA
-  // writes its output, otherwise this CTA's partial goes to its slot of the unit's workspace
+  // in-CTA merge of each unit slot's warps, in two parallel passes: (slot, q row) -> the slot's
+  // running max, its warps' weights and the weighted l sum; then (slot, q row, d) -> the
+  // weighted acc sum (independent shared loads, no per-thread serial max pass).  A unit entirely
+  // inside this CTA writes its output, otherwise this CTA's partial goes to its slot of the
+  // unit's workspace.
   const int Hq = a.H * a.m;
   float* ws_l = a.ws + (int64_t)l * w.U * w.max_ctas * a.m * kWsStride;
-  for (int p = threadIdx.x; p < nslots * kHeadDim; p += blockDim.x) {
-    const int sl = p / kHeadDim, d = p % kHeadDim;
+  if (threadIdx.x < nslots * a.m) {
+    const int sl = threadIdx.x / a.m, qi = threadIdx.x % a.m;
+    const int us = u0 + sl;
+    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
+    const int wlo = max(q0, cta * kWpWarps) - cta * kWpWarps, whi = min(q1, cta * kWpWarps + kWpWarps) - cta * kWpWarps;
+    float ms = -INFINITY;
+    for (int ww = wlo; ww < whi; ++ww) ms = fmaxf(ms, s_ml[ww][qi][0]);
+    float lsum = 0.f;
+    for (int ww = wlo; ww < whi; ++ww) {
+      const float mw = s_ml[ww][qi][0];
+      const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
+      s_wf[ww][qi] = f;
+      lsum += f * s_ml[ww][qi][1];
+    }
+    s_sm[sl][qi][0] = ms;
+    s_sm[sl][qi][1] = lsum;
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < nslots * a.m * kHeadDim; p += blockDim.x) {
+    const int d = p % kHeadDim, r = p / kHeadDim;
+    const int sl = r / a.m, qi = r % a.m;
     const int us = u0 + sl;
     const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
     const int wlo = max(q0, cta * kWpWarps) - cta * kWpWarps, whi = min(q1, cta * kWpWarps + kWpWarps) - cta * kWpWarps;
     const int fc = q0 / kWpWarps, lc = (q1 - 1) / kWpWarps;
     const int bs = us / a.H, hs = us % a.H;
-    for (int qi = 0; qi < a.m; ++qi) {
-      float ms = -INFINITY;
-      for (int ww = wlo; ww < whi; ++ww) ms = fmaxf(ms, s_ml[ww][qi][0]);
-      float acc = 0.f, lsum = 0.f;
-      const int dq = swz(qi, d);
-      for (int ww = wlo; ww < whi; ++ww) {
-        const float mw = s_ml[ww][qi][0];
-        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-        acc += f * s_acc[ww][qi][dq];
-        lsum += f * s_ml[ww][qi][1];
-      }
-      if (fc == lc) {
-        const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
-        if (a.partial_out) {
-          float* dst = a.partial_out + row * kPartStride;
-          dst[d] = acc;
-          if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
-        } else {
-          a.out[l * a.o_sl + bs * a.o_sb + (int64_t)(hs * a.m + qi) * kHeadDim + d] =
-              __half_as_ushort(__float2half_rn(acc / lsum));
-        }
-      } else {
-        float* dst = ws_l + (((int64_t)us * w.max_ctas + (cta - fc)) * a.m + qi) * kWsStride;
+    const int dq = swz(qi, d);
+    float acc0 = 0.f, acc1 = 0.f;
+    int ww = wlo;
+    for (; ww + 1 < whi; ww += 2) {
+      acc0 += s_wf[ww][qi] * s_acc[ww][qi][dq];
+      acc1 += s_wf[ww + 1][qi] * s_acc[ww + 1][qi][dq];
+    }
+    if (ww < whi) acc0 += s_wf[ww][qi] * s_acc[ww][qi][dq];
+    const float acc = acc0 + acc1;
+    const float ms = s_sm[sl][qi][0], lsum = s_sm[sl][qi][1];
+    if (fc == lc) {
+      const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
+      if (a.partial_out) {
+        float* dst = a.partial_out + row * kPartStride;
         dst[d] = acc;
         if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+      } else {
+        a.out[l * a.o_sl + bs * a.o_sb + (int64_t)(hs * a.m + qi) * kHeadDim + d] =
+            __half_as_ushort(__float2half_rn(acc / lsum));
       }
+    } else {
+      float* dst = ws_l + (((int64_t)us * w.max_ctas + (cta - fc)) * a.m + qi) * kWsStride;
+      dst[d] = acc;
+      if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
     }
   }
   __syncthreads();

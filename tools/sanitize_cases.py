@@ -34,11 +34,21 @@ def main():
                 cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
             part = cache.decode_partial(q, splits=splits)
             batched.lse_merge(torch.stack([part, part]))
+        # warp-plan schedule: whole batch, per-layer PDL chain, partials
+        cache.decode(q, schedule="wp")
+        for l in range(L):
+            cache.decode(q[l:l + 1], out=out[l:l + 1], layer=l, pdl=l > 0, schedule="wp")
+        cache.decode_partial(q, schedule="wp")
     q = torch.from_numpy(rng.normal(size=(L, B, H * 4, D)).astype(np.float16)).to(dev)
     out = torch.empty_like(q)
     g = cache.decode_graph(q, out, splits=2, chains=2)
     g.replay()
     g.replay()
+    cache.schedule = "wp"
+    g = cache.decode_graph(q, out)
+    g.replay()
+    g.replay()
+    cache.schedule = "auto"
     loop = batched.DecodeLoop(cache, 4, splits=2)
     for _ in range(3):
         loop.step(q, k[:, :, 0], v[:, :, 0])
@@ -48,10 +58,12 @@ def main():
     k2[..., ::32] *= 40
     cache2 = batched.build_cache_batched(k2, v, s)
     cache2.decode(q * 3, splits=2)
+    cache2.decode(q * 3, schedule="wp")
     k3 = k.clone()
     k3[0, 0, :, 0, 5] = 30000
     cache3 = batched.build_cache_batched(k3, v, s)
     cache3.decode(q, splits=2)
+    cache3.decode(q, schedule="wp")
     # per-head f64 API (kernels facade, quantizer round trip)
     x = rng.normal(size=(40, 70))
     codes, sc, zp = kernels.quantize_groups(x, 4, 32)
