@@ -511,7 +511,7 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
             local_decode(q)
         torch.cuda.current_stream().wait_stream(side)
         local_graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(local_graph):
+        with torch.cuda.graph(local_graph, stream=side):  # the warm-up's stream: same workspaces
             local_decode(q)
 
         def step():

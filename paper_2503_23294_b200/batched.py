@@ -237,14 +237,15 @@ class BatchedKVCache:
         return self._wp or None
 
     def _wp_workspace(self, m, layers, layer, max_ctas):
-        wkey = ("wp", m, layers, layer)
+        sid = torch.cuda.current_stream(self.device).cuda_stream
+        wkey = ("wp", m, layers, layer, sid)
         hit = self._ws_ptr.get(wkey)
         if hit is not None:
             return hit
         lib = _lib.load()
         per = lib.ckv_decode_wp_workspace_bytes(layers, self.B, self.H, m, max_ctas)
         per = -(-per // 256) * 256
-        key = ("wp", m, layers)
+        key = ("wp", m, layers, sid)
         nbytes = per * (self.L if layers == 1 else 1)
         if key not in self._ws:
             self._ws[key] = torch.zeros(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
@@ -276,18 +277,21 @@ class BatchedKVCache:
     def _workspace(self, m, splits, layers, layer):
         """Zero-initialised decode workspace (split partials + self-resetting arrival counters).
         Launches covering a single layer get a private per-layer slice, so consecutive
-        per-layer launches never share counters (required for programmatic dependent launch)."""
-        wkey = (m, splits, layers, layer)
+        per-layer launches never share counters (required for programmatic dependent launch).
+        Keyed by the current stream as well: decodes of one cache on concurrent streams never
+        share counters (the C-ABI's re-entrancy is per stream, include/ckv.h)."""
+        sid = torch.cuda.current_stream(self.device).cuda_stream
+        wkey = (m, splits, layers, layer, sid)
         hit = self._ws_ptr.get(wkey)
         if hit is not None:
             return hit
         lib = _lib.load()
         if layers == self.L:
-            key = (m, splits, "all")
+            key = (m, splits, "all", sid)
             nbytes = lib.ckv_decode_workspace_bytes(self.L, self.B, self.H, m, splits)
             off = 0
         else:
-            key = (m, splits, "per-layer", layers)
+            key = (m, splits, "per-layer", layers, sid)
             per = lib.ckv_decode_workspace_bytes(layers, self.B, self.H, m, splits)
             per = -(-per // 256) * 256
             nbytes = per * self.L
@@ -448,7 +452,7 @@ class BatchedKVCache:
                 self._launch_layers(q, out, lo, hi, splits, scale, chains, streams)
             torch.cuda.current_stream().wait_stream(side)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=side):  # the warm-up's stream: same workspaces
                 self._launch_layers(q, out, lo, hi, splits, scale, chains, streams)
             graphs.append(g)
         return graphs
@@ -658,7 +662,7 @@ class DecodeLoop:
             cache._launch_layers(self.q, self.out, 0, L, splits, None, chains, streams)
         torch.cuda.current_stream().wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with torch.cuda.graph(self.graph, stream=side):  # the warm-up's stream: same workspaces
             cache._append_device(self.k_new, self.v_new)
             cache._launch_layers(self.q, self.out, 0, L, splits, None, chains, streams)
         self.steps = 0

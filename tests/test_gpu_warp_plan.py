@@ -100,3 +100,32 @@ def test_warp_plan_outlier_precise_and_exact_units():
     cache.schedule = "wp"
     out = cache.decode(torch.from_numpy(q).cuda()).float().cpu().numpy()
     _check(out, k, v, q, tiers, m, [(0, b, h) for b in range(B) for h in range(H)])
+
+
+@pytest.mark.parametrize("schedule", ["wp", "split"])
+def test_concurrent_streams_use_private_workspaces(schedule):
+    """Decodes of one cache on two concurrent streams: each stream gets its own workspace
+    (self-resetting arrival counters + partials), so interleaved launches on both streams give
+    the serial result (include/ckv.h: re-entrant per stream)."""
+    L, B, H, m = 2, 2, 8, 4
+    cache, k, v, q, tiers = _case(11, L, B, H, m, 60, 5)
+    cache.schedule = schedule
+    splits = 3 if schedule == "split" else None
+    qd = torch.from_numpy(q).cuda()
+    ref = cache.decode(qd, splits=splits).clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = {s: [torch.empty_like(qd) for _ in range(20)] for s in (s1, s2)}
+    for st in (s1, s2):
+        st.wait_stream(torch.cuda.current_stream())
+    for i in range(20):  # interleaved: both streams' launches are in flight together
+        for st in (s1, s2):
+            with torch.cuda.stream(st):
+                for l in range(L):
+                    cache.decode(qd[l:l + 1], splits=splits, out=outs[st][i][l:l + 1], layer=l, pdl=l > 0)
+    torch.cuda.synchronize()
+    ws = cache._ws_ptr
+    ptrs = {v for key, v in ws.items() if key[-1] in (s1.cuda_stream, s2.cuda_stream)}
+    assert len(ptrs) == 2 * L  # one per-layer slice per stream
+    for st in (s1, s2):
+        for o in outs[st]:
+            assert torch.equal(o, ref) or (o.float() - ref.float()).abs().max().item() < 2e-3

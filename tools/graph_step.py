@@ -33,7 +33,7 @@ def main():
             step()
     torch.cuda.current_stream().wait_stream(s)
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    with torch.cuda.graph(g, stream=s):
         step()
     res = {}
     for name, fn in (("eager", step), ("graph", g.replay)):

@@ -36,6 +36,6 @@ for b in sorted(hot, key=len)[:3]:
     c = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", i).split()[0].split(".")[0] for i in b)
     print(len(b), "instrs:", dict(c.most_common()))
 if "-v" in sys.argv:
-    b = sorted(hot, key=len)[1]
+    b = sorted(hot, key=len)[int(sys.argv[sys.argv.index("-v") + 1]) if len(sys.argv) > sys.argv.index("-v") + 1 else 1]
     for i in b:
         print("   ", i)
