@@ -1224,9 +1224,10 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   unsigned char (*s_ring)[kWarpRing] = reinterpret_cast<unsigned char (*)[kWarpRing]>(s_dyn);
   unsigned char* s_qall = s_dyn + kWpWarps * kWarpRing;
   __shared__ float s_ml[kWpWarps][8][2];
-  __shared__ float s_wf[kWpWarps][8], s_sm[8][8][2];
   __shared__ __align__(16) float s_biasall[8][2 * 4 * kBiasRows];
   __shared__ int s_lastu[8];
+  __shared__ int4 s_slot[8];             // per unit slot: warps [x, y) of this CTA, first / last CTA of the unit
+  __shared__ unsigned short s_rtab[64];  // merge row r -> (slot << 8 | q row)
   __shared__ int64_t s_tr[12], s_tend[kWpWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
@@ -1270,6 +1271,18 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
                 (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
     kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
   }
+  // per-slot facts for the merge (build-time plan data: before the wait)
+  const int u_last = __ldg(wunit + cta * kWpWarps + kWpWarps - 1);
+  const int nslots = u_last - u0 + 1;
+  if ((int)threadIdx.x < nslots) {
+    const int us = u0 + threadIdx.x;
+    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
+    s_slot[threadIdx.x] = make_int4(max(q0, cta * kWpWarps) - cta * kWpWarps,
+                                    min(q1, cta * kWpWarps + kWpWarps) - cta * kWpWarps, q0 / kWpWarps,
+                                    (q1 - 1) / kWpWarps);
+  }
+  if ((int)threadIdx.x < nslots * a.m)
+    s_rtab[threadIdx.x] = (unsigned short)(((threadIdx.x / a.m) << 8) | (threadIdx.x % a.m));
   // pull this warp's q rows into L2 while the previous launch drains (L2 is the point of
   // coherence: a producer writing q before the wait below still wins; a prefetch reads nothing
   // into this SM)
@@ -1282,8 +1295,6 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
 
   // q staging: every unit slot of the CTA needs parts 0-3; the warps share the jobs
-  const int u_last = __ldg(wunit + cta * kWpWarps + kWpWarps - 1);
-  const int nslots = u_last - u0 + 1;
   int mode;
   {
     float qv[32];
@@ -1370,68 +1381,57 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   st.lsum[0] += st.lsq[0];
   st.lsum[1] += st.lsq[1];
   if (lane == 0 && tracing()) s_tend[warp] = gtime();
-  __syncthreads();  // ring -> merge buffer reuse
-  if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
-  float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0]);
-  // column of (q row, d) in s_acc: d's low 4 bits XOR (g >> 1 | row/2 << 2), g = d / 16 — every
-  // store instruction of a warp hits 32 distinct banks (unswizzled: 16 lanes per bank)
+  // Park this warp's partial (rows < m) in its own ring region (its copies are all waited:
+  // no barrier needed before the stores).  Column of (q row, d): d's low 4 bits XOR
+  // (g >> 1 | row/2 << 2), g = d / 16 — every store instruction of a warp hits 32 distinct
+  // banks (unswizzled: 16 lanes per bank).
   auto swz = [](int row, int d) { return (d & ~15) | ((d ^ ((((d >> 4) & 7) >> 1) | ((row >> 1) << 2))) & 15); };
+  {
+    __syncwarp();
+    float (*s_accw)[kHeadDim] = reinterpret_cast<float (*)[kHeadDim]>(&s_ring[warp][0]);
+    const bool r0 = 2 * c < a.m, r1 = 2 * c + 1 < a.m;
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    s_acc[warp][2 * c][swz(2 * c, 16 * g + mt)] = st.acc[mt][0];
-    s_acc[warp][2 * c + 1][swz(2 * c + 1, 16 * g + mt)] = st.acc[mt][1];
-    s_acc[warp][2 * c][swz(2 * c, 16 * g + 8 + mt)] = st.acc[mt][2];
-    s_acc[warp][2 * c + 1][swz(2 * c + 1, 16 * g + 8 + mt)] = st.acc[mt][3];
-  }
-  if (g == 0) {
-    s_ml[warp][2 * c][0] = st.mrun[0]; s_ml[warp][2 * c][1] = st.lsum[0];
-    s_ml[warp][2 * c + 1][0] = st.mrun[1]; s_ml[warp][2 * c + 1][1] = st.lsum[1];
+    for (int mt = 0; mt < 8; ++mt) {
+      if (r0) {
+        s_accw[2 * c][swz(2 * c, 16 * g + mt)] = st.acc[mt][0];
+        s_accw[2 * c][swz(2 * c, 16 * g + 8 + mt)] = st.acc[mt][2];
+      }
+      if (r1) {
+        s_accw[2 * c + 1][swz(2 * c + 1, 16 * g + mt)] = st.acc[mt][1];
+        s_accw[2 * c + 1][swz(2 * c + 1, 16 * g + 8 + mt)] = st.acc[mt][3];
+      }
+    }
+    if (g == 0) {
+      s_ml[warp][2 * c][0] = st.mrun[0]; s_ml[warp][2 * c][1] = st.lsum[0];
+      s_ml[warp][2 * c + 1][0] = st.mrun[1]; s_ml[warp][2 * c + 1][1] = st.lsum[1];
+    }
   }
   __syncthreads();
-  // in-CTA merge of each unit slot's warps, in two parallel passes: (slot, q row) -> the slot's
-  // running max, its warps' weights and the weighted l sum; then (slot, q row, d) -> the
-  // weighted acc sum (independent shared loads, no per-thread serial max pass).  A unit entirely
-  // inside this CTA writes its output, otherwise this CTA's partial goes to its slot of the
-  // unit's workspace.
+  if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
+  // in-CTA merge, one pass: thread item (slot, q row, d) -> the slot's running max over its
+  // warps, then the weighted acc and l sums.  A unit entirely inside this CTA writes its output,
+  // otherwise this CTA's partial goes to its slot of the unit's workspace.
   const int Hq = a.H * a.m;
   float* ws_l = a.ws + (int64_t)l * w.U * w.max_ctas * a.m * kWsStride;
-  if (threadIdx.x < nslots * a.m) {
-    const int sl = threadIdx.x / a.m, qi = threadIdx.x % a.m;
-    const int us = u0 + sl;
-    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
-    const int wlo = max(q0, cta * kWpWarps) - cta * kWpWarps, whi = min(q1, cta * kWpWarps + kWpWarps) - cta * kWpWarps;
+  for (int p = threadIdx.x; p < nslots * a.m * kHeadDim; p += blockDim.x) {
+    const int d = p & (kHeadDim - 1), rt = s_rtab[p >> 7];
+    const int sl = rt >> 8, qi = rt & 255;
+    const int4 si = s_slot[sl];
     float ms = -INFINITY;
-    for (int ww = wlo; ww < whi; ++ww) ms = fmaxf(ms, s_ml[ww][qi][0]);
-    float lsum = 0.f;
-    for (int ww = wlo; ww < whi; ++ww) {
+    for (int ww = si.x; ww < si.y; ++ww) ms = fmaxf(ms, s_ml[ww][qi][0]);
+    const int dq = qi * kHeadDim + swz(qi, d);
+    float acc0 = 0.f, acc1 = 0.f, lsum = 0.f;
+    for (int ww = si.x; ww < si.y; ++ww) {
       const float mw = s_ml[ww][qi][0];
       const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-      s_wf[ww][qi] = f;
-      lsum += f * s_ml[ww][qi][1];
+      const float x = reinterpret_cast<const float*>(&s_ring[ww][0])[dq];
+      if (ww & 1) acc1 = fmaf(f, x, acc1);
+      else acc0 = fmaf(f, x, acc0);
+      lsum = fmaf(f, s_ml[ww][qi][1], lsum);
     }
-    s_sm[sl][qi][0] = ms;
-    s_sm[sl][qi][1] = lsum;
-  }
-  __syncthreads();
-  for (int p = threadIdx.x; p < nslots * a.m * kHeadDim; p += blockDim.x) {
-    const int d = p % kHeadDim, r = p / kHeadDim;
-    const int sl = r / a.m, qi = r % a.m;
-    const int us = u0 + sl;
-    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
-    const int wlo = max(q0, cta * kWpWarps) - cta * kWpWarps, whi = min(q1, cta * kWpWarps + kWpWarps) - cta * kWpWarps;
-    const int fc = q0 / kWpWarps, lc = (q1 - 1) / kWpWarps;
-    const int bs = us / a.H, hs = us % a.H;
-    const int dq = swz(qi, d);
-    float acc0 = 0.f, acc1 = 0.f;
-    int ww = wlo;
-    for (; ww + 1 < whi; ww += 2) {
-      acc0 += s_wf[ww][qi] * s_acc[ww][qi][dq];
-      acc1 += s_wf[ww + 1][qi] * s_acc[ww + 1][qi][dq];
-    }
-    if (ww < whi) acc0 += s_wf[ww][qi] * s_acc[ww][qi][dq];
     const float acc = acc0 + acc1;
-    const float ms = s_sm[sl][qi][0], lsum = s_sm[sl][qi][1];
-    if (fc == lc) {
+    const int us = u0 + sl, bs = us / a.H, hs = us - bs * a.H;
+    if (si.z == si.w) {
       const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
       if (a.partial_out) {
         float* dst = a.partial_out + row * kPartStride;
@@ -1442,23 +1442,22 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
             __half_as_ushort(__float2half_rn(acc / lsum));
       }
     } else {
-      float* dst = ws_l + (((int64_t)us * w.max_ctas + (cta - fc)) * a.m + qi) * kWsStride;
+      float* dst = ws_l + (((int64_t)us * w.max_ctas + (cta - si.z)) * a.m + qi) * kWsStride;
       dst[d] = acc;
       if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0 && tracing()) s_tr[9] = gtime();
-  // arrival per split unit: the CTA that completes a unit's set of partials merges them
-  if (threadIdx.x < nslots) {
-    const int us = u0 + threadIdx.x;
-    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
-    const int fc = q0 / kWpWarps, lc = (q1 - 1) / kWpWarps;
+  // arrival per split unit: the CTA that completes a unit's set of partials merges them.  The
+  // barrier above orders every thread's partial stores before the device-scope release RMW.
+  if ((int)threadIdx.x < nslots) {
+    const int4 si = s_slot[threadIdx.x];
     int last = 0;
-    if (fc != lc) {
-      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[(int64_t)l * w.U + us]);
+    if (si.z != si.w) {
+      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[(int64_t)l * w.U + u0 + threadIdx.x]);
       const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
-      last = prev == (uint32_t)(lc - fc);
+      last = prev == (uint32_t)(si.w - si.z);
       if (last) ctr.store(0u, cuda::memory_order_relaxed);
     }
     s_lastu[threadIdx.x] = last;
@@ -1476,9 +1475,9 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   for (int sl = 0; sl < nslots; ++sl) {
     if (!s_lastu[sl]) continue;
     const int us = u0 + sl;
-    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
-    const int nc = (q1 - 1) / kWpWarps - q0 / kWpWarps + 1;
-    const int bs = us / a.H, hs = us % a.H;
+    const int4 si = s_slot[sl];
+    const int nc = si.w - si.z + 1;
+    const int bs = us / a.H, hs = us - bs * a.H;
     const float* src_p = ws_l + (int64_t)us * w.max_ctas * a.m * kWsStride;  // [ctas][m][stride]
     const bool staged = nc * a.m * kWsStride * (int)sizeof(float) <= kWpWarps * kWarpRing;
     if (staged) {
@@ -1491,7 +1490,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     }
     const float* pbase = staged ? s_part : src_p;
     for (int p = threadIdx.x; p < a.m * kHeadDim; p += blockDim.x) {
-      const int qi = p / kHeadDim, d = p % kHeadDim;
+      const int qi = p >> 7, d = p & (kHeadDim - 1);
       const float* pp = pbase + qi * kWsStride;
       float ms = -INFINITY;
       for (int s2 = 0; s2 < nc; ++s2) ms = fmaxf(ms, pp[s2 * a.m * kWsStride + kHeadDim]);
@@ -1500,8 +1499,8 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
         const float* ps = pp + s2 * a.m * kWsStride;
         const float mw = ps[kHeadDim];
         const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-        acc += f * ps[d];
-        lsum += f * ps[kHeadDim + 1];
+        acc = fmaf(f, ps[d], acc);
+        lsum = fmaf(f, ps[kHeadDim + 1], lsum);
       }
       const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
       if (a.partial_out) {
