@@ -159,8 +159,9 @@ int32_t ckv_assign_tiers(const double* scores, const double* thresholds,
  * batch (varlen; every segment starts at a multiple of 32 rows).  The quantized arenas are
  * TILE-NATIVE: each 16-row tile holds exactly the bits of the reference's row packing (one
  * D=128 row packs into 8 (INT2) / 16 (INT4) little-endian u32 words, _numpy.py:70-86) and
- * the rows' fp16 (lo, hi) group metadata, permuted in 16-bit pieces into the order the
- * decode kernel's MMA fragments consume them (layout functions tile_off_* in
+ * the rows' fp16 (lo, hi) group metadata, permuted (INT2: in bytes, INT4: in 16-bit pieces)
+ * into the order the decode kernel's MMA fragments consume them: every 32-element group is its
+ * own pair of k-steps (K) / m-tiles (V) (layout functions tile_byte_* / tile_off_* in
  * csrc/ckv_common.cuh; K and V tiles differ).  K and V share one interleaved tile buffer per
  * tier: tile t of the INT2 arenas is the 1536-byte block [K codes 512 | V codes 512 | K meta
  * 256 | V meta 256] at t * 1536 (INT4: 2560-byte blocks [K codes 1024 | V codes 1024 | K meta
@@ -176,12 +177,11 @@ typedef struct ckv_arena {
   uint32_t* meta4;    /* tile t at +t*2560: 256 B                                 */
   uint16_t* fp;       /* fp16 [L][H][rows_fp][128] (FP16 chunks || tail || decode) */
   uint32_t* span_flags; /* u32 [L][H][B], zero-filled before build: bit0/bit1 set when an
-                           INT2/INT4 group's scale exceeds 4000 (decode then runs that unit in
-                           its exact unweighted mode; nullable) */
+                           INT2/INT4 group's scale exceeds 4000 (diagnostic; nullable) */
   uint32_t* span_max; /* f32 bits [L][H][B], zero-filled before build: the largest quantized
-                         group span (hi - lo) of the unit's rows, which with |q| bounds the
-                         decode's fp16 operand error (decode then takes its precise K path;
-                         nullable) */
+                         group span (hi - lo) of the unit's rows.  Decode sizes the unit's V
+                         operand scaling 2^F from the V arena's (required there when the
+                         arenas hold quantized rows; the K arena's is informational) */
   int64_t rows2, rows4, rows_fp;
 } ckv_arena;
 

@@ -59,11 +59,18 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // decode kernel's MMA fragments consume them (lane-ordered 16-byte slots), so a tile moves
 // HBM -> shared memory with fully coalesced 16-byte copies and every fragment read is one
 // conflict-free shared load with no shuffling.  Tile t of a segment covers arena rows
-// [16t, 16t+16) (segments start at multiples of 32 rows).  Within a tile, rt = row % 16,
-// w = 32-bit word of the reference row packing (_numpy.py:70-86: INT2 w = 0..7, INT4 w =
-// 0..15), hf = 16-bit half of that word; metadata (lo, hi) of group G has hf 0 = lo, 1 = hi.
-// The functions give the byte offset of that 16-bit piece inside its tile; the reference row
-// format is recovered exactly by the inverse gather (ckv_arena_export).
+// [16t, 16t+16) (segments start at multiples of 32 rows).  Within a tile, rt = row % 16.  The
+// reference row packing (_numpy.py:70-86) puts element i at bits [i b, (i+1) b) of LE word
+// i b / 32: an INT2 row is 32 bytes (byte B = elements 4B..4B+3), an INT4 row 16 words (16-bit
+// piece P = elements 4P..4P+3).  The decode takes every 32-element group G as its own k-steps
+// (K) / m-tiles (V), so lane (g, c) of a tile holds, per group:
+//   K: elements 32G + 8c + [0, 8) of tokens g and g+8 (INT2: bytes 8G+2c, 8G+2c+1 of both
+//      tokens interleaved in one word; INT4: the reference's word 4G + c of each token);
+//   V: elements 32G + 4g + [0, 4) of tokens 2c, 2c+1 (and 2c+8, 2c+9), the two tokens in the
+//      two halves of a word (INT2: bytes 8G + g, one per half; INT4: pieces 8G + g).
+// The functions give the byte offset of that byte (INT2) / 16-bit piece (INT4) inside its
+// tile; metadata (lo, hi) of group G has hf 0 = lo, 1 = hi.  The reference row format is
+// recovered exactly by the inverse gather (ckv_arena_export).
 constexpr int kTileRows = 16;
 constexpr int kTileBytes2 = 512;    // INT2 codes tile (16 rows x 32 B)
 constexpr int kTileBytes4 = 1024;   // INT4 codes tile (16 rows x 64 B)
@@ -72,24 +79,25 @@ constexpr int kTileBytesMeta = 256; // metadata tile (16 rows x 4 groups x (lo, 
 constexpr int kBlock2 = 2 * kTileBytes2 + 2 * kTileBytesMeta;  // 1536 B per INT2 tile
 constexpr int kBlock4 = 2 * kTileBytes4 + 2 * kTileBytesMeta;  // 2560 B per INT4 tile
 
-// K INT2: lane (g, c) = [tok g: w 2c, 2c+1 | tok g+8: w 2c, 2c+1]
-__host__ __device__ __forceinline__ int tile_off_k2(int rt, int w, int hf) {
-  return ((rt & 7) * 4 + (w >> 1)) * 16 + (rt >> 3) * 8 + (w & 1) * 4 + hf * 2;
+// K INT2 byte B of row rt: lane (rt & 7, c = (B & 7) / 2), word G = B / 8,
+// byte [tok rt < 8: 0 | rt >= 8: 1] + 2 (B & 1)
+__host__ __device__ __forceinline__ int tile_byte_k2(int rt, int B) {
+  return 16 * (4 * (rt & 7) + ((B & 7) >> 1)) + 4 * (B >> 3) + (rt >> 3) + 2 * (B & 1);
 }
-// V INT2: lane (g, c) = [(w g: lo half of tok 2c, 2c+1), (hi halves), same for tok 2c+8, 2c+9]
-__host__ __device__ __forceinline__ int tile_off_v2(int rt, int w, int hf) {
-  return (w * 4 + ((rt & 7) >> 1)) * 16 + ((rt >> 3) * 2 + hf) * 4 + (rt & 1) * 2;
+// V INT2 byte B: lane (g = B & 7, c = (rt & 7) / 2), word 2 (rt >= 8) + G / 2 (G = B / 8),
+// byte 2 (rt & 1) + (G & 1)
+__host__ __device__ __forceinline__ int tile_byte_v2(int rt, int B) {
+  return 16 * (4 * (B & 7) + ((rt & 7) >> 1)) + 4 * (2 * (rt >> 3) + (B >> 4)) + 2 * (rt & 1) + ((B >> 3) & 1);
 }
-// K INT4: rows g / g+8 in two 512-B halves; lane (g, c) = group c as
-//   [(lo w4c, lo w4c+1), (hi w4c, hi w4c+1), (lo w4c+2, lo w4c+3), (hi w4c+2, hi w4c+3)]
+// K INT4 piece hf of word w: rows g / g+8 in two 512-B halves; lane (rt & 7, w & 3), word w / 4
 __host__ __device__ __forceinline__ int tile_off_k4(int rt, int w, int hf) {
-  const int wi = w & 3;
-  return (rt >> 3) * 512 + ((rt & 7) * 4 + (w >> 2)) * 16 + ((wi >> 1) * 2 + hf) * 4 + (wi & 1) * 2;
+  return 512 * (rt >> 3) + 16 * (4 * (rt & 7) + (w & 3)) + 4 * (w >> 2) + 2 * hf;
 }
-// V INT4: toks 2c, 2c+1 / 2c+8, 2c+9 in two 512-B halves; lane (g, c) =
-//   [(lo w2g of tok 2c, 2c+1), (hi w2g ...), (lo w2g+1 ...), (hi w2g+1 ...)]
+// V INT4 piece P = 2w + hf: tokens 2c, 2c+1 / 2c+8, 2c+9 in two 512-B halves; lane
+// (P & 7, (rt & 7) / 2), word G = P / 8, half rt & 1
 __host__ __device__ __forceinline__ int tile_off_v4(int rt, int w, int hf) {
-  return (rt >> 3) * 512 + ((w >> 1) * 4 + ((rt & 7) >> 1)) * 16 + ((w & 1) * 2 + hf) * 4 + (rt & 1) * 2;
+  const int P = 2 * w + hf;
+  return 512 * (rt >> 3) + 16 * (4 * (P & 7) + ((rt & 7) >> 1)) + 4 * (P >> 3) + 2 * (rt & 1);
 }
 // K metadata: lane (g, c) = [(lo, hi) tok g group c, (lo, hi) tok g+8 group c]
 __host__ __device__ __forceinline__ int tile_off_km(int rt, int G, int hf) {

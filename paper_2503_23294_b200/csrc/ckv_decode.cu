@@ -137,79 +137,50 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 }
 
 
-constexpr uint32_t kMagic16 = 0x4C004C00u;  // fp16 16.0 in both halves
-constexpr float kWideQ = 1000.0f;           // and |q| 2^6 in fp16 range
-// precise K path when (largest K group span) x max|q| (log2-scaled q) exceeds this: the normal
-// path's score error is ~2^-12 span |q| per group element (measured ~1.5e-3 relative output
-// error at a product of ~3 on N(0,1) data, 1.8e-2 at ~55 on SURVEY's outlier variant)
-constexpr float kPreciseSpanQ = 8.0f;
+// ---- operand scaling -------------------------------------------------------------------
+// Quantized codes enter the tensor cores as fp16 SUBNORMALS: a code c at bits [j, j+b) of a
+// 16-bit lane (no exponent bits) is the fp16 value c * 2^(j-24) exactly, so extracting a pair
+// of codes is one AND and there is no bias term.  HMMA multiplies subnormal operands exactly
+// (tools/subnormal_probe.cu).  The per-slot power of two 2^(j-24) is folded into q (K side) and
+// into the output rows (V side); the group scales are applied per (token, group) outside the
+// per-element path: K in fp32 on the per-group q.K^T partial sums, V folded into P.
+//   q side: q' = q 2^(E - j) in fp16, E per unit so max|q| 2^E is in [2^14, 2^15) (no overflow,
+//           no fp16 range limit on q); S = lo-term + sum_G sigma_G X_G, sigma = span 2^(24-E)/qmax.
+//   V side: p'_G = fp16(p span_G 2^F), F per unit from the unit's largest V group span so that
+//           p' <= 2^15; O accumulates sum_t p'_G code 2^(j-24) and is brought back to value
+//           units (x 2^(24-F-j) / qmax per accumulator row) when a phase ends.
+__device__ __forceinline__ int q_exponent(float maxabs) {  // E: max|q| 2^E in [2^14, 2^15)
+  if (!(maxabs > 0.f) || !(maxabs < INFINITY)) return 0;
+  int x;
+  (void)frexpf(maxabs, &x);  // maxabs = m 2^x, m in [0.5, 1)
+  return 15 - x;
+}
+__device__ __forceinline__ int v_exponent(float span_max) {  // F: span_max 2^F < 2^7
+  if (!(span_max > 0.f) || !(span_max < INFINITY)) return 0;
+  int x;
+  (void)frexpf(span_max, &x);
+  return min(7 - x, 15);  // 2^F stays an fp16 normal
+}
 
-// scale (hi - lo) / qmax of one (lo, hi) half2 metadata word (hi - lo via mixed f16/f32 add)
-__device__ __forceinline__ float meta_scale(uint32_t meta, float inv_qmax) {
+// scale (hi - lo) * k of one (lo, hi) half2 metadata word (hi - lo exact: mixed f16/f32 subtract)
+__device__ __forceinline__ float meta_scale(uint32_t meta, float k) {
   float d;
   asm("{.reg .f16 lo, hi; .reg .f32 a; mov.b32 {lo, hi}, %1; cvt.f32.f16 a, lo; sub.rn.f32.f16 %0, hi, a;}"
       : "=f"(d) : "r"(meta));
-  return d * inv_qmax;
+  return d * k;
 }
-
-struct DeqC {
-  __half2 sc;  // (sc_lo_half, sc_hi_half)
-  __half2 nm;  // -16 * sc  (exact: power-of-two multiple)
-};
-
-// Scale constants straight from fp16 metadata with half2 arithmetic: span = hi - lo (one
-// rounding), nm = -16 sc (exact).  The rounding of fp16(1/qmax) would bias every scale by the
-// same relative amount (2.4e-4 for 1/3), and a constant bias does not average out over a long
-// context.  K: sc = span * fp16(1/qmax), and the constant factor 1 / (qmax fp16(1/qmax)) is
-// folded into that tier's q fragments.  V: sc = span * c_hi + span * c_lo (c_hi + c_lo = 1/qmax
-// to 2^-22), one rounding.  K: one (lo, hi) word -> that token's constants in both halves;
-// V: two words (tokens t0, t1) -> (t0, t1) constants.
-__device__ __forceinline__ float kscale_fold(float inv_q) {  // 1 / (qmax * fp16(1/qmax))
-  return inv_q / __half2float(__float2half_rn(inv_q));
+// (hi - lo) 2^F of two groups in one rounding: hi 2^F - lo 2^F (the scaled operands cannot
+// overflow where hi - lo itself would, e.g. lo = -60000, hi = 60000)
+__device__ __forceinline__ uint32_t span2(uint32_t hi, uint32_t lo, uint32_t f2) {
+  const __half2 f = u32_as_h2(f2);
+  return h2_as_u32(__hfma2(u32_as_h2(hi), f, __hneg2(__hmul2(u32_as_h2(lo), f))));
 }
-__device__ __forceinline__ DeqC kdeq(uint32_t meta, __half2 inv_q) {
-  const __half2 h = u32_as_h2(meta);
-  DeqC d;
-  d.sc = __hmul2(__hsub2(__high2half2(h), __low2half2(h)), inv_q);
-  d.nm = __hmul2(d.sc, __float2half2_rn(-16.0f));
-  return d;
-}
-__device__ __forceinline__ DeqC vdeq(uint32_t lo01, uint32_t hi01, float inv_q) {
-  const __half c_hi = __float2half_rn(inv_q);
-  const __half c_lo = __float2half_rn(inv_q - __half2float(c_hi));
-  const __half2 span = __hsub2(u32_as_h2(hi01), u32_as_h2(lo01));
-  DeqC d;
-  d.sc = __hfma2(span, __half2half2(c_hi), __hmul2(span, __half2half2(c_lo)));
-  d.nm = __hmul2(d.sc, __float2half2_rn(-16.0f));
-  return d;
-}
-
-// weighted dequant of a pair of codes at bits (j, 16 + j) of x (mask = code mask << j)
-__device__ __forceinline__ uint32_t wdeq(uint32_t x, uint32_t mask, uint32_t magic, const DeqC& d) {
-  const uint32_t raw = (x & mask) | magic;
-  return h2_as_u32(__hfma2(u32_as_h2(raw), d.sc, d.nm));
-}
-// exact (unweighted) dequant: code by subtraction, full affine v = code * sc + lo
-__device__ __forceinline__ uint32_t edeq(uint32_t x, int j, uint32_t cmask, __half2 sc, __half2 lo) {
-  const uint32_t raw = (x & (cmask << j)) | (((uint32_t)(25 - j) << 10) * 0x10001u);
-  const __half2 code = __hsub2(u32_as_h2(raw), __float2half2_rn((float)(1 << (10 - j))));
-  return h2_as_u32(__hfma2(code, sc, lo));
-}
-
-// INT2 K pair i of a word: bits (2i, 16+2i) for i <= 4, (2(i-5), ...) of w >> 10 for i >= 5
-template <int I> struct K2 {
-  static constexpr int j = I <= 4 ? 2 * I : 2 * (I - 5);
-  static constexpr bool hi = I >= 5;
-};
-// INT4 K pair i (of a 4-pair PRMT word): bits (4(i&1), ...) of x or x >> 8
-template <int I> struct K4 {
-  static constexpr int j = 4 * (I & 1);
-  static constexpr bool hi = (I & 3) >= 2;
-};
+__device__ __forceinline__ uint32_t hmul2u(uint32_t a, uint32_t b) { return h2_as_u32(__hmul2(u32_as_h2(a), u32_as_h2(b))); }
 
 struct WarpState {
-  float acc[8][4];  // O^T C-fragments, m-tile mt: rows d = 16g+mt (c0,c1), 16g+8+mt (c2,c3)
-  float lacc[2];    // sum_t p_t * lo_t for the group of row g, cols 2c, 2c+1
+  float acc[8][4];  // O^T C-fragments, m-tile mt (group mt / 2): rows d = 32 (mt >> 1) + 4 g + 2 (mt & 1)
+                    // (c0, c1) and d + 1 (c2, c3), columns (q rows) 2c, 2c+1
+  float lacc[2];    // sum_t p_t lo_{t,G} for G = g (lanes g < 4; rows g >= 4 duplicate), cols 2c, 2c+1
   float lsq[2];     // sum_t p_t over the quantized tiles (complete, from the lo MMA's ones rows)
   float mrun[2];    // running max (log2 domain) for cols 2c, 2c+1
   float lsum[2];
@@ -253,11 +224,13 @@ __device__ __forceinline__ void softmax_tile(float (&s)[4], WarpState& st, uint3
   bp1 = movmatrix_trans(h2_as_u32(__floats2half2_rn(p2, p3)));  // (P[g][8+2c], P[g][9+2c])
 }
 
-// Q B-fragments live in shared memory as three sets ([set][k-step pair][32 lanes] x 16 B, one
-// copy per CTA: k-steps 2kp, 2kp+1 of a lane side by side, so a pair is one conflict-free
-// 128-bit load): 0 = INT2 slot weights, 1 = INT4 slot weights, 2 = unweighted (FP16 tiles and
-// the exact mode).  After the sets, [32 lanes] x 4 B: the (hi, lo) split of sum_g(q) for the
-// zero-point MMA.
+// Q B-fragments live in shared memory as three sets ([set][group G][32 lanes] x 16 B, one
+// copy per CTA: the fragments of k-steps 2G, 2G+1 of a lane side by side, one conflict-free
+// 128-bit load): 0 = INT2 slot weights, 1 = INT4 slot weights, 2 = unweighted (FP16 tiles).
+// K-step 2G + h, lane (g, c): b0 = q'[g][32G + 8c + 2h], q'[g][32G + 8c + 4 + 2h];
+// b1 = q'[g][32G + 8c + 2h + 1], q'[g][32G + 8c + 5 + 2h] — the d order of the tile layouts
+// (ckv_common.cuh).  After the sets, [32 lanes] x 4 B: the (hi, lo) fp16 split of
+// Q[g][G = c] = sum_{d in G} q[g][d] for the zero-point MMA.
 constexpr int kQSet = 4 * 32 * 16;
 constexpr int kQBytes = 3 * kQSet + 32 * 4;
 struct QS {
@@ -276,9 +249,15 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a
                                           uint32_t a3, uint2 b) {
   mma_16816(d, a0, a1, a2, a3, b.x, b.y);
 }
+__device__ __forceinline__ void sts32d(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts64d(uint32_t a, uint32_t v0, uint32_t v1) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v0), "r"(v1) : "memory");
+}
 
-// The V zero-point term sum_t p_t lo_t (A rows g) and, on the A rows g+8 set to fp16 ones, the
-// tile's row sums sum_t p_t of the same fp16 P the P.V MMAs use.
+// The V zero-point term sum_t p_t lo_{t,G} (A rows g: group g & 3) and, on the A rows g+8 set
+// to fp16 ones, the tile's row sums sum_t p_t of the same fp16 P the P.V MMAs use.
 __device__ __forceinline__ void lo_mma(WarpState& st, uint32_t a0, uint32_t a2, uint32_t bp0, uint32_t bp1) {
   constexpr uint32_t kOnes = 0x3C003C00u;
   float t[4] = {st.lacc[0], st.lacc[1], st.lsq[0], st.lsq[1]};
@@ -293,345 +272,143 @@ __device__ __forceinline__ void lo_mma(WarpState& st, uint32_t a0, uint32_t a2, 
 // A stage holds one tile in the tile-native arena layout (ckv_common.cuh), copied verbatim:
 //   INT2: KC @0 (512 B), VC @512 (512 B), KM @1024 (256 B), VM @1280 (256 B)
 //   INT4: KC @0 (1024 B), VC @1024 (1024 B), KM @2048, VM @2304
-// `sl` = stage + 16 * lane (this lane's code slots); metadata addresses add the per-lane
-// deltas of MetaOff (K: 8-byte entry per lane; V: 16-byte entry (g/2, c), shared by lane pairs).
-struct MetaOff {
-  int32_t k, v;  // k = -8 lane, v = 16 ((g >> 1) * 4 + c) - 16 lane
+// `sl` = stage + 16 * lane (this lane's code slots).  Per-lane constants:
+struct LaneOff {
+  int32_t mk;   // K meta entry (tok g, g+8; group c) relative to sl: -8 lane
+  int32_t mv;   // V meta entry (group g & 3, c) relative to sl
+  uint32_t sk;  // this warp's scale scratch + 4 lane: K sigma of (tok g, group c); +128: tok g+8
+  uint32_t kc;  // scratch + 16 g: the sigmas of tok g, groups 0-3; +128: tok g+8
+  uint32_t vp;  // scratch + 256 + 8 (4 c + (g & 3)): span pairs of group g & 3
+  uint32_t vc;  // scratch + 256 + 32 c: span pairs of groups 0-3 for this lane's tokens
+};
+constexpr int kScratch = 384;  // per warp: K sigmas [16 tok][4 G] f32 | V span pairs [4 c][4 G][2] half2
+
+template <int BITS> struct TL {
+  static constexpr uint32_t vc = BITS == 2 ? 512 : 1024;
+  static constexpr uint32_t km = BITS == 2 ? 1024 : 2048;
+  static constexpr uint32_t vm = km + 256;
+  static constexpr int set = BITS == 2 ? 0 : 1;
 };
 
-// exact-mode scales (f32, then fp16) of two tokens from (lo0, lo1) and (hi0, hi1) half2 words
-__device__ __forceinline__ __half2 exact_sc2(uint32_t lo01, uint32_t hi01, float inv_q) {
-  const float2 l = __half22float2(u32_as_h2(lo01)), h = __half22float2(u32_as_h2(hi01));
-  return __floats2half2_rn((h.x - l.x) * inv_q, (h.y - l.y) * inv_q);
-}
-
-template <bool EXACT>
-__device__ __forceinline__ void qk_int2(uint32_t sl, const MetaOff& mo, const QS& qs, uint32_t mg, float (&s)[4]) {
-  const uint4 kk = lds128(sl);  // (tok g: words 2c, 2c+1), (tok g+8: words 2c, 2c+1)
-  const uint2 kmm = lds64(sl + 1024 + mo.k);
-  constexpr float iq = 1.0f / 3.0f;
-
-  float s2[4] = {0.f, 0.f, 0.f, 0.f};
+// S^T[16 tok x 8 q] of a quantized tile: zero-point MMA (lo x Q), then per group G two MMAs on
+// the raw subnormal codes into the group's own accumulator X_G, combined in fp32 with the
+// (token, group) sigmas shared through the warp's scratch.  kappa = 2^(24-E) / qmax.
+template <int BITS>
+__device__ __forceinline__ void qk_tile(uint32_t sl, const LaneOff& lo, const QS& qs, float kappa, float (&s)[4]) {
+  const uint2 kmm = lds64(sl + TL<BITS>::km + lo.mk);  // (lo, hi) of (tok g, G = c), (tok g+8, G = c)
+  sts32d(lo.sk, __float_as_uint(meta_scale(kmm.x, kappa)));
+  sts32d(lo.sk + 128, __float_as_uint(meta_scale(kmm.y, kappa)));
 #pragma unroll
   for (int e = 0; e < 4; ++e) s[e] = 0.f;
-  if (!EXACT) {
-    const __half2 iq2 = __float2half2_rn(iq);
-    const DeqC dk0 = kdeq(kmm.x, iq2), dk1 = kdeq(kmm.y, iq2);
-#pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
-      const uint32_t w0s = w0 >> 10, w1s = w1 >> 10;
-      const uint4 qa = qs.ld2(0, 2 * blk), qb = qs.ld2(0, 2 * blk + 1);
-#define KD(W, WS, D, I) wdeq(K2<I>::hi ? WS : W, 0x00030003u << K2<I>::j, mg, D)
-      mma_16816(s, KD(w0, w0s, dk0, 0), KD(w1, w1s, dk1, 0), KD(w0, w0s, dk0, 1), KD(w1, w1s, dk1, 1), lo2(qa));
-      mma_16816(s2, KD(w0, w0s, dk0, 2), KD(w1, w1s, dk1, 2), KD(w0, w0s, dk0, 3), KD(w1, w1s, dk1, 3), hi2(qa));
-      mma_16816(s, KD(w0, w0s, dk0, 4), KD(w1, w1s, dk1, 4), KD(w0, w0s, dk0, 5), KD(w1, w1s, dk1, 5), lo2(qb));
-      mma_16816(s2, KD(w0, w0s, dk0, 6), KD(w1, w1s, dk1, 6), KD(w0, w0s, dk0, 7), KD(w1, w1s, dk1, 7), hi2(qb));
-#undef KD
-    }
-    mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
-  } else {
-    const __half2 sc0 = __float2half2_rn(meta_scale(kmm.x, iq)), sc1 = __float2half2_rn(meta_scale(kmm.y, iq));
-    const __half2 lo0 = u32_as_h2(prmt(kmm.x, kmm.x, 0x1010)), lo1 = u32_as_h2(prmt(kmm.y, kmm.y, 0x1010));
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int blk = ks >> 2, i0 = 2 * (ks & 3), i1 = i0 + 1;
-      const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
-      const int j0 = i0 <= 4 ? 2 * i0 : 2 * (i0 - 5), j1 = i1 <= 4 ? 2 * i1 : 2 * (i1 - 5);
-      const uint32_t x00 = i0 <= 4 ? w0 : w0 >> 10, x10 = i0 <= 4 ? w1 : w1 >> 10;
-      const uint32_t x01 = i1 <= 4 ? w0 : w0 >> 10, x11 = i1 <= 4 ? w1 : w1 >> 10;
-      mma_16816(s, edeq(x00, j0, 0x00030003u, sc0, lo0), edeq(x10, j0, 0x00030003u, sc1, lo1),
-                edeq(x01, j1, 0x00030003u, sc0, lo0), edeq(x11, j1, 0x00030003u, sc1, lo1), qs.ld(2, ks));
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < 4; ++e) s[e] += s2[e];
-}
-
-template <bool EXACT>
-__device__ __forceinline__ void pv_int2(uint32_t sl, const MetaOff& mo, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
-  // codes: word g of tokens (2c | 2c+1) lo halves, hi halves, then (2c+8 | 2c+9)
-  const uint4 vv = lds128(sl + 512);
-  const uint4 vmm = lds128(sl + 1280 + mo.v);  // (lo 2c|2c+1), (hi ...), (lo 2c+8|2c+9), (hi ...)
-  constexpr float iq = 1.0f / 3.0f;
-  const uint32_t c01lo = vv.x, c01hi = vv.y, c23lo = vv.z, c23hi = vv.w;
-  if (!EXACT) {
-    const DeqC d01 = vdeq(vmm.x, vmm.y, iq), d23 = vdeq(vmm.z, vmm.w, iq);
-    const uint32_t a8 = c01lo >> 8, b8 = c01hi >> 8, e8 = c23lo >> 8, f8 = c23hi >> 8;
-    // m-tile mt uses code mt of each 8-code half: j = 2 (mt & 3), from x (mt < 4) or x >> 8
-#define PV2(MT)                                                                                     \
-  {                                                                                                 \
-    constexpr uint32_t m_ = 0x00030003u << (2 * ((MT) & 3));                                       \
-    mma_16816(st.acc[MT], wdeq((MT) < 4 ? c01lo : a8, m_, mg, d01), wdeq((MT) < 4 ? c01hi : b8, m_, mg, d01), \
-              wdeq((MT) < 4 ? c23lo : e8, m_, mg, d23), wdeq((MT) < 4 ? c23hi : f8, m_, mg, d23), bp0, bp1); \
-  }
-    PV2(0) PV2(1) PV2(2) PV2(3) PV2(4) PV2(5) PV2(6) PV2(7)
-#undef PV2
-    lo_mma(st, vmm.x, vmm.z, bp0, bp1);
-  } else {
-    const __half2 sc01 = exact_sc2(vmm.x, vmm.y, iq), sc23 = exact_sc2(vmm.z, vmm.w, iq);
-    const __half2 lo01 = u32_as_h2(vmm.x), lo23 = u32_as_h2(vmm.z);
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int j = 2 * (mt & 3);
-      const uint32_t x0 = mt < 4 ? c01lo : c01lo >> 8, x1 = mt < 4 ? c01hi : c01hi >> 8;
-      const uint32_t x2 = mt < 4 ? c23lo : c23lo >> 8, x3 = mt < 4 ? c23hi : c23hi >> 8;
-      mma_16816(st.acc[mt], edeq(x0, j, 0x00030003u, sc01, lo01), edeq(x1, j, 0x00030003u, sc01, lo01),
-                edeq(x2, j, 0x00030003u, sc23, lo23), edeq(x3, j, 0x00030003u, sc23, lo23), bp0, bp1);
-    }
-  }
-}
-
-template <bool EXACT>
-__device__ __forceinline__ void qk_int4(uint32_t sl, const MetaOff& mo, const QS& qs, uint32_t mg, float (&s)[4]) {
-  // group c of tok g / tok g+8, words paired as (lo w0, lo w1), (hi w0, hi w1), (lo w2, lo w3), (hi ...)
-  const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);
-  const uint2 kmm = lds64(sl + 2048 + mo.k);
-  constexpr float iq = 1.0f / 15.0f;
-
-  float s2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int e = 0; e < 4; ++e) s[e] = 0.f;
-  const uint32_t kwa[4] = {kw0.x, kw0.y, kw0.z, kw0.w}, kwb[4] = {kw1.x, kw1.y, kw1.z, kw1.w};
-  if (!EXACT) {
-    const __half2 iq2 = __float2half2_rn(iq);
-    const DeqC dk0 = kdeq(kmm.x, iq2), dk1 = kdeq(kmm.y, iq2);
-#pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      // pairs (d0, d0+8) = (word 2blk code i, word 2blk+1 code i)
-      const uint32_t a_lo = kwa[2 * blk], a_hi = kwa[2 * blk + 1];
-      const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
-      const uint32_t a_lo8 = a_lo >> 8, a_hi8 = a_hi >> 8, b_lo8 = b_lo >> 8, b_hi8 = b_hi >> 8;
-      const uint4 qa = qs.ld2(1, 2 * blk), qb = qs.ld2(1, 2 * blk + 1);
-#define KD(X, X8, D, I) wdeq(K4<I>::hi ? X8 : X, 0x000F000Fu << K4<I>::j, mg, D)
-      mma_16816(s, KD(a_lo, a_lo8, dk0, 0), KD(b_lo, b_lo8, dk1, 0), KD(a_lo, a_lo8, dk0, 1), KD(b_lo, b_lo8, dk1, 1), lo2(qa));
-      mma_16816(s2, KD(a_lo, a_lo8, dk0, 2), KD(b_lo, b_lo8, dk1, 2), KD(a_lo, a_lo8, dk0, 3), KD(b_lo, b_lo8, dk1, 3), hi2(qa));
-      mma_16816(s, KD(a_hi, a_hi8, dk0, 0), KD(b_hi, b_hi8, dk1, 0), KD(a_hi, a_hi8, dk0, 1), KD(b_hi, b_hi8, dk1, 1), lo2(qb));
-      mma_16816(s2, KD(a_hi, a_hi8, dk0, 2), KD(b_hi, b_hi8, dk1, 2), KD(a_hi, a_hi8, dk0, 3), KD(b_hi, b_hi8, dk1, 3), hi2(qb));
-#undef KD
-    }
-    mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
-  } else {
-    const __half2 sc0 = __float2half2_rn(meta_scale(kmm.x, iq)), sc1 = __float2half2_rn(meta_scale(kmm.y, iq));
-    const __half2 lo0 = u32_as_h2(prmt(kmm.x, kmm.x, 0x1010)), lo1 = u32_as_h2(prmt(kmm.y, kmm.y, 0x1010));
-#pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      const uint32_t a_lo = kwa[2 * blk], a_hi = kwa[2 * blk + 1];
-      const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
-#pragma unroll
-      for (int q2 = 0; q2 < 4; ++q2) {
-        const uint32_t ca = q2 < 2 ? a_lo : a_hi, cb = q2 < 2 ? b_lo : b_hi;
-        const int i = 2 * (q2 & 1);  // pairs i, i+1 of the 4-pair word
-        const uint32_t xa0 = i < 2 ? ca : ca >> 8, xb0 = i < 2 ? cb : cb >> 8;
-        const uint32_t xa1 = (i + 1) < 2 ? ca : ca >> 8, xb1 = (i + 1) < 2 ? cb : cb >> 8;
-        mma_16816(s, edeq(xa0, 4 * (i & 1), 0x000F000Fu, sc0, lo0), edeq(xb0, 4 * (i & 1), 0x000F000Fu, sc1, lo1),
-                  edeq(xa1, 4 * ((i + 1) & 1), 0x000F000Fu, sc0, lo0), edeq(xb1, 4 * ((i + 1) & 1), 0x000F000Fu, sc1, lo1),
-                  qs.ld(2, 4 * blk + q2));
-      }
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < 4; ++e) s[e] += s2[e];
-}
-
-template <bool EXACT>
-__device__ __forceinline__ void pv_int4(uint32_t sl, const MetaOff& mo, uint32_t mg, WarpState& st, uint32_t bp0, uint32_t bp1) {
-  // V (tok 2c | 2c+1) and (2c+8 | 2c+9) for d = 16g + mt (word 2g) and 16g + 8 + mt (word 2g+1):
-  // (lo w2g), (hi w2g), (lo w2g+1), (hi w2g+1) per token pair
-  const uint4 va = lds128(sl + 1024), vb = lds128(sl + 1536);
-  const uint4 vmm = lds128(sl + 2304 + mo.v);
-  constexpr float iq = 1.0f / 15.0f;
-  const uint32_t x01[4] = {va.x, va.y, va.z, va.w};
-  const uint32_t x23[4] = {vb.x, vb.y, vb.z, vb.w};
-  if (!EXACT) {
-    const DeqC d01 = vdeq(vmm.x, vmm.y, iq), d23 = vdeq(vmm.z, vmm.w, iq);
-    // m-tile mt: code k = mt & 3 of x[mt >> 2] sits at bits 4k; move it to j = 2k (>> 2k)
-#define PV4(MT)                                                                                     \
-  {                                                                                                 \
-    constexpr int k_ = (MT) & 3, u_ = (MT) >> 2;                                                    \
-    constexpr uint32_t m_ = 0x000F000Fu << (2 * k_);                                               \
-    mma_16816(st.acc[MT], wdeq(x01[u_] >> (2 * k_), m_, mg, d01), wdeq(x01[2 + u_] >> (2 * k_), m_, mg, d01), \
-              wdeq(x23[u_] >> (2 * k_), m_, mg, d23), wdeq(x23[2 + u_] >> (2 * k_), m_, mg, d23), bp0, bp1); \
-  }
-    PV4(0) PV4(1) PV4(2) PV4(3) PV4(4) PV4(5) PV4(6) PV4(7)
-#undef PV4
-    lo_mma(st, vmm.x, vmm.z, bp0, bp1);
-  } else {
-    const __half2 sc01 = exact_sc2(vmm.x, vmm.y, iq), sc23 = exact_sc2(vmm.z, vmm.w, iq);
-    const __half2 lo01 = u32_as_h2(vmm.x), lo23 = u32_as_h2(vmm.z);
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int k = mt & 3, u = mt >> 2;
-      const int j = 4 * (k & 1);
-      const uint32_t sh = k < 2 ? 0 : 8;
-      mma_16816(st.acc[mt], edeq(x01[u] >> sh, j, 0x000F000Fu, sc01, lo01), edeq(x01[2 + u] >> sh, j, 0x000F000Fu, sc01, lo01),
-                edeq(x23[u] >> sh, j, 0x000F000Fu, sc23, lo23), edeq(x23[2 + u] >> sh, j, 0x000F000Fu, sc23, lo23), bp0, bp1);
-    }
-  }
-}
-
-// ---- precise K path (wide-span units) ---------------------------------------------------
-// The normal path feeds the tensor cores fp16 values sc*code*2^(j-6), so the score error grows
-// with the K group span times |q|.  The precise path feeds the exact magic values
-// 16 + code*2^(j-6) instead and applies bias and scale per group in fp32: two MMAs per k-step
-// whose B fragments are the tier's q fragments (sets 0 / 1) masked to two groups each
-// (column n = (q row n & 3, group 2v + n / 4)), so D holds per-(token, q row, group)
-// partial sums  sum_{d in G} q'_d (16 + code_d 2^(j-6)) = 16 Q'_G + (1/f) sum_{d in G} q_d code_d
-// (f = the set's fp16(1/qmax) fold), and S = sum_G span_G fp16(1/qmax) (D_G - 16 Q'_G) + lo term.
-// A thread holds groups c/2 and 2 + c/2 of q rows (2c)&3, (2c)&3 + 1; lanes c and c^2 hold the
-// other two groups.  Needs no shared memory beyond a 128-byte bias table.
-// With 5-8 q rows (ROWS8) a second pass over the same raw K operands covers q rows 4-7 (q
-// fragments of lane ((g & 3) + 4, c)); lanes c >= 2 keep its sums (their S columns are rows
-// 2c, 2c+1), lanes c < 2 the first pass's.
-struct PreciseOff {
-  int32_t m0, m1;   // byte offsets (from the lane slot `sl`) of the metadata of groups G0, G1
-  uint32_t bias;    // shared-memory address of this thread's 16 Q' constants (INT2 tier)
-  int32_t qoff;     // q-fragment offset of lane ((g & 3), c) relative to this lane
-  int32_t qoff2;    // ... of lane ((g & 3) + 4, c) (q rows 4-7)
-  uint32_t msk0, msk1;  // all-ones when this lane's B column takes group c in variant 0 / 1
-  bool hi_rows;     // c >= 2: this lane's S columns are q rows 4-7 when m > 4
-};
-constexpr int kBiasRows = 8;
-constexpr int kBiasG = kBiasRows * 4;      // bias table f32 16 Q' [tier][group][q row]
-constexpr int kBiasTier = 4 * kBiasG;
-
-__device__ __forceinline__ uint32_t raw_pair(uint32_t x, uint32_t mask, uint32_t magic) {
-  return (x & mask) | magic;
-}
-__device__ __forceinline__ uint2 masked(uint32_t x, uint32_t y, uint32_t m) { return make_uint2(x & m, y & m); }
-
-__device__ __forceinline__ void precise_combine(const float (&P0)[4], const float (&P1)[4], float sc0g,
-                                                float sc0g8, float sc1g, float sc1g8,
-                                                uint32_t bias_addr, float (&t)[4]) {
-  const uint2 b0 = lds64(bias_addr), b1 = lds64(bias_addr + 2 * kBiasG);  // (G0, a..a+1), (G0 + 2, ..)
-  const float b0x = __uint_as_float(b0.x), b0y = __uint_as_float(b0.y);
-  const float b1x = __uint_as_float(b1.x), b1y = __uint_as_float(b1.y);
-  t[0] = fmaf(sc1g, P1[0] - b1x, sc0g * (P0[0] - b0x));
-  t[1] = fmaf(sc1g, P1[1] - b1y, sc0g * (P0[1] - b0y));
-  t[2] = fmaf(sc1g8, P1[2] - b1x, sc0g8 * (P0[2] - b0x));
-  t[3] = fmaf(sc1g8, P1[3] - b1y, sc0g8 * (P0[3] - b0y));
-#pragma unroll
-  for (int e = 0; e < 4; ++e) t[e] += __shfl_xor_sync(0xffffffffu, t[e], 2);
-}
-
-// span * fp16(1/qmax) in fp32 from a (lo, hi) metadata word (matches the fold in the q sets)
-__device__ __forceinline__ float precise_scale(uint32_t meta, float inv_q16) {
-  const float2 lh = __half22float2(u32_as_h2(meta));
-  return (lh.y - lh.x) * inv_q16;
-}
-
-template <int BITS, bool ROWS8>
-__device__ __forceinline__ void qk_precise(uint32_t sl, const MetaOff& mo, const PreciseOff& po,
-                                           const QS& qs, uint32_t mg, float (&s)[4]) {
-  constexpr int set = BITS == 2 ? 0 : 1;
-  constexpr uint32_t meta_at = BITS == 2 ? 1024 : 2048;
-  const float inv_q16 = __half2float(__float2half_rn(BITS == 2 ? 1.0f / 3.0f : 1.0f / 15.0f));
-  float P0[4] = {0.f, 0.f, 0.f, 0.f}, P1[4] = {0.f, 0.f, 0.f, 0.f};
-  float R0[4] = {0.f, 0.f, 0.f, 0.f}, R1[4] = {0.f, 0.f, 0.f, 0.f};  // q rows 4-7 (ROWS8)
-  const uint32_t qsrc = qs.base + po.qoff + set * kQSet;
-  const uint32_t qsrc2 = qs.base + po.qoff2 + set * kQSet;
-#define PSTEP(X, Y, X2, Y2)                                                        \
-  {                                                                                \
-    mma_16816(P0, x0, x1, x2, x3, masked(X, Y, po.msk0));                          \
-    mma_16816(P1, x0, x1, x2, x3, masked(X, Y, po.msk1));                          \
-    if (ROWS8) {                                                                   \
-      mma_16816(R0, x0, x1, x2, x3, masked(X2, Y2, po.msk0));                      \
-      mma_16816(R1, x0, x1, x2, x3, masked(X2, Y2, po.msk1));                      \
-    }                                                                              \
-  }
+  mma_16816(s, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
+  float X[4][4];
   if (BITS == 2) {
+    // word G = [tok g: byte 8G+2c | tok g+8: 8G+2c | tok g: 8G+2c+1 | tok g+8: 8G+2c+1]
     const uint4 kk = lds128(sl);
+    const uint32_t w[4] = {kk.x, kk.y, kk.z, kk.w};
 #pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      const uint32_t w0 = blk ? kk.y : kk.x, w1 = blk ? kk.w : kk.z;
-      const uint32_t w0s = w0 >> 10, w1s = w1 >> 10;
-      const uint4 qa = lds128(qsrc + 512 * (2 * blk)), qb = lds128(qsrc + 512 * (2 * blk + 1));
-      uint4 qa2 = qa, qb2 = qb;
-      if (ROWS8) {
-        qa2 = lds128(qsrc2 + 512 * (2 * blk));
-        qb2 = lds128(qsrc2 + 512 * (2 * blk + 1));
-      }
-#define KR(W, WS, I) raw_pair(K2<I>::hi ? WS : W, 0x00030003u << K2<I>::j, mg)
-#define KSTEP(I0, I1, X, Y, X2, Y2)                                                \
-      {                                                                          \
-        const uint32_t x0 = KR(w0, w0s, I0), x1 = KR(w1, w1s, I0);               \
-        const uint32_t x2 = KR(w0, w0s, I1), x3 = KR(w1, w1s, I1);               \
-        PSTEP(X, Y, X2, Y2)                                                      \
-      }
-      KSTEP(0, 1, qa.x, qa.y, qa2.x, qa2.y)
-      KSTEP(2, 3, qa.z, qa.w, qa2.z, qa2.w)
-      KSTEP(4, 5, qb.x, qb.y, qb2.x, qb2.y)
-      KSTEP(6, 7, qb.z, qb.w, qb2.z, qb2.w)
-#undef KSTEP
-#undef KR
+    for (int G = 0; G < 4; ++G) {
+      const uint32_t W = w[G], W8 = W >> 8;
+      const uint4 q = qs.ld2(0, G);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) X[G][e] = 0.f;
+      mma_16816(X[G], W & 0x00030003u, W8 & 0x00030003u, W & 0x000C000Cu, W8 & 0x000C000Cu, lo2(q));
+      mma_16816(X[G], W & 0x00300030u, W8 & 0x00300030u, W & 0x00C000C0u, W8 & 0x00C000C0u, hi2(q));
     }
   } else {
-    const uint4 kw0 = lds128(sl), kw1 = lds128(sl + 512);
-    const uint32_t kwa[4] = {kw0.x, kw0.y, kw0.z, kw0.w}, kwb[4] = {kw1.x, kw1.y, kw1.z, kw1.w};
+    // tok g: the reference's words 4G + c (G = 0..3); +512: tok g+8
+    const uint4 ka = lds128(sl), kb = lds128(sl + 512);
+    const uint32_t wa[4] = {ka.x, ka.y, ka.z, ka.w}, wb[4] = {kb.x, kb.y, kb.z, kb.w};
 #pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      const uint32_t a_lo = kwa[2 * blk], a_hi = kwa[2 * blk + 1];
-      const uint32_t b_lo = kwb[2 * blk], b_hi = kwb[2 * blk + 1];
-      const uint32_t a_lo8 = a_lo >> 8, a_hi8 = a_hi >> 8, b_lo8 = b_lo >> 8, b_hi8 = b_hi >> 8;
-      const uint4 qa = lds128(qsrc + 512 * (2 * blk)), qb = lds128(qsrc + 512 * (2 * blk + 1));
-      uint4 qa2 = qa, qb2 = qb;
-      if (ROWS8) {
-        qa2 = lds128(qsrc2 + 512 * (2 * blk));
-        qb2 = lds128(qsrc2 + 512 * (2 * blk + 1));
-      }
-#define KR(X, X8, I) raw_pair(K4<I>::hi ? X8 : X, 0x000F000Fu << K4<I>::j, mg)
-#define KSTEP(XA, XA8, XB, XB8, I0, I1, X, Y, X2, Y2)                              \
-      {                                                                          \
-        const uint32_t x0 = KR(XA, XA8, I0), x1 = KR(XB, XB8, I0);               \
-        const uint32_t x2 = KR(XA, XA8, I1), x3 = KR(XB, XB8, I1);               \
-        PSTEP(X, Y, X2, Y2)                                                      \
-      }
-      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 0, 1, qa.x, qa.y, qa2.x, qa2.y)
-      KSTEP(a_lo, a_lo8, b_lo, b_lo8, 2, 3, qa.z, qa.w, qa2.z, qa2.w)
-      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 0, 1, qb.x, qb.y, qb2.x, qb2.y)
-      KSTEP(a_hi, a_hi8, b_hi, b_hi8, 2, 3, qb.z, qb.w, qb2.z, qb2.w)
-#undef KSTEP
-#undef KR
+    for (int G = 0; G < 4; ++G) {
+      const uint32_t A = wa[G], B = wb[G], A8 = A >> 8, B8 = B >> 8;
+      const uint4 q = qs.ld2(1, G);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) X[G][e] = 0.f;
+      mma_16816(X[G], A & 0x000F000Fu, B & 0x000F000Fu, A & 0x00F000F0u, B & 0x00F000F0u, lo2(q));
+      mma_16816(X[G], A8 & 0x000F000Fu, B8 & 0x000F000Fu, A8 & 0x00F000F0u, B8 & 0x00F000F0u, hi2(q));
     }
   }
-#undef PSTEP
-  const uint2 m0 = lds64(sl + meta_at + po.m0), m1 = lds64(sl + meta_at + po.m1);
-  const float s0g = precise_scale(m0.x, inv_q16), s0g8 = precise_scale(m0.y, inv_q16);
-  const float s1g = precise_scale(m1.x, inv_q16), s1g8 = precise_scale(m1.y, inv_q16);
-  float t[4];
-  precise_combine(P0, P1, s0g, s0g8, s1g, s1g8, po.bias + (BITS == 2 ? 0 : kBiasTier), t);
-  if (ROWS8) {
-    float t2[4];
-    precise_combine(R0, R1, s0g, s0g8, s1g, s1g8, po.bias + (BITS == 2 ? 0 : kBiasTier) + 16, t2);
+  __syncwarp();
+  const uint4 ga = lds128(lo.kc), gb = lds128(lo.kc + 128);  // sigma (tok g | tok g+8, G = 0..3)
+  const float sa[4] = {__uint_as_float(ga.x), __uint_as_float(ga.y), __uint_as_float(ga.z), __uint_as_float(ga.w)};
+  const float sb[4] = {__uint_as_float(gb.x), __uint_as_float(gb.y), __uint_as_float(gb.z), __uint_as_float(gb.w)};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) t[e] = po.hi_rows ? t2[e] : t[e];
+  for (int G = 0; G < 4; ++G) {
+    s[0] = fmaf(sa[G], X[G][0], s[0]);
+    s[1] = fmaf(sa[G], X[G][1], s[1]);
+    s[2] = fmaf(sb[G], X[G][2], s[2]);
+    s[3] = fmaf(sb[G], X[G][3], s[3]);
   }
-  const uint2 kmm = lds64(sl + meta_at + mo.k);
-  float s2[4] = {0.f, 0.f, 0.f, 0.f};
-  mma_16816(s2, prmt(kmm.x, kmm.x, 0x1010), prmt(kmm.y, kmm.y, 0x1010), 0u, 0u, qs.aug(), 0u);
+}
+
+// O^T += V^T P' of a quantized tile: the group's span pairs x 2^F (from lanes g < 4 through the
+// scratch) fold the V scales into P per group; m-tiles 2G, 2G+1 take group G's codes, rows
+// (mt, g) / (mt, g+8) = code e = 2 (mt & 1) / 2 (mt & 1) + 1 of the lane's byte (INT2) or
+// 16-bit piece (INT4) of that group.  f2 = 2^F in both halves.
+template <int BITS>
+__device__ __forceinline__ void pv_tile(uint32_t sl, const LaneOff& lo, WarpState& st, uint32_t bp0, uint32_t bp1,
+                                        uint32_t f2) {
+  // entry (G = g & 3, c): (lo 2c | 2c+1), (hi 2c | 2c+1), (lo 2c+8 | 2c+9), (hi 2c+8 | 2c+9)
+  const uint4 vmm = lds128(sl + TL<BITS>::vm + lo.mv);
+  sts64d(lo.vp, span2(vmm.y, vmm.x, f2), span2(vmm.w, vmm.z, f2));
+  lo_mma(st, vmm.x, vmm.z, bp0, bp1);
+  __syncwarp();
+  const uint4 ga = lds128(lo.vc), gb = lds128(lo.vc + 16);  // (G0: 2c|2c+1, 2c+8|2c+9), (G1 ..), (G2), (G3)
+  const uint32_t pa[4] = {hmul2u(bp0, ga.x), hmul2u(bp0, ga.z), hmul2u(bp0, gb.x), hmul2u(bp0, gb.z)};
+  const uint32_t pb[4] = {hmul2u(bp1, ga.y), hmul2u(bp1, ga.w), hmul2u(bp1, gb.y), hmul2u(bp1, gb.w)};
+  if (BITS == 2) {
+    // words: (tok 2c | 2c+1) x (G0, G1), (tok 2c | 2c+1) x (G2, G3), then tokens 2c+8 | 2c+9
+    const uint4 vv = lds128(sl + TL<2>::vc);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) s[e] = t[e] + s2[e];
+    for (int G = 0; G < 4; ++G) {
+      const uint32_t ua = ((G >> 1) ? vv.y : vv.x) >> (8 * (G & 1));
+      const uint32_t ub = ((G >> 1) ? vv.w : vv.z) >> (8 * (G & 1));
+      mma_16816(st.acc[2 * G], ua & 0x00030003u, ua & 0x000C000Cu, ub & 0x00030003u, ub & 0x000C000Cu, pa[G], pb[G]);
+      mma_16816(st.acc[2 * G + 1], ua & 0x00300030u, ua & 0x00C000C0u, ub & 0x00300030u, ub & 0x00C000C0u, pa[G], pb[G]);
+    }
+  } else {
+    // words G: (tok 2c | 2c+1) 16-bit pieces of group G; +512: tokens 2c+8 | 2c+9
+    const uint4 va = lds128(sl + TL<4>::vc), vb = lds128(sl + TL<4>::vc + 512);
+    const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+    for (int G = 0; G < 4; ++G) {
+      const uint32_t ua = wa[G], ub = wb[G], ua8 = ua >> 8, ub8 = ub >> 8;
+      mma_16816(st.acc[2 * G], ua & 0x000F000Fu, ua & 0x00F000F0u, ub & 0x000F000Fu, ub & 0x00F000F0u, pa[G], pb[G]);
+      mma_16816(st.acc[2 * G + 1], ua8 & 0x000F000Fu, ua8 & 0x00F000F0u, ub8 & 0x000F000Fu, ub8 & 0x00F000F0u, pa[G], pb[G]);
+    }
+  }
+}
+
+// Accumulator row weights of a phase: O_acc = W(e) O (value units), code e = 2 (mt & 1) + (row
+// half), W(e) = qmax 2^(F + j(e) - 24) with the code's bit position j: INT2 j = 2e, INT4
+// j = 4 (e & 1).  Scaling by w_next / w_prev per row class moves the accumulator between phases.
+__device__ __forceinline__ void phase_weights(int bits, int F, float (&w)[4]) {
+  const float qmax = bits == 2 ? 3.0f : 15.0f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) w[e] = qmax * exp2f((float)(F + (bits == 2 ? 2 * e : 4 * (e & 1)) - 24));
+}
+__device__ __forceinline__ void scale_acc(WarpState& st, const float (&f)[4]) {
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    const float a = f[2 * (mt & 1)], b = f[2 * (mt & 1) + 1];
+    st.acc[mt][0] *= a; st.acc[mt][1] *= a; st.acc[mt][2] *= b; st.acc[mt][3] *= b;
+  }
 }
 
 // ---- FP16 tile straight from global memory (FP16 chunks, tail, decode tokens) ------------
-template <bool EXACT>
+// Same d order as the quantized tiles (q set 2 = unweighted q); V in value units.
 __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf, int valid,
                                           const QS& qs, WarpState& st, int g, int c) {
   float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int blk = 0; blk < 2; ++blk) {
-    // tokens g, g+8; d 32c + 16 blk .. +16 (8 words each)
-    const uint4* p0 = reinterpret_cast<const uint4*>(kf + g * kHeadDim + 32 * c + 16 * blk);
-    const uint4* p1 = reinterpret_cast<const uint4*>(kf + (g + 8) * kHeadDim + 32 * c + 16 * blk);
-    const uint4 x0 = __ldg(p0), x1 = __ldg(p0 + 1), y0 = __ldg(p1), y1 = __ldg(p1 + 1);
-    const uint32_t ka[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-    const uint32_t kb[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      // pair (d0, d0+8), d0 = 16blk + 2kk: words kk and kk+4 of the block
-      mma_16816(s, prmt(ka[kk], ka[kk + 4], 0x5410), prmt(kb[kk], kb[kk + 4], 0x5410),
-                prmt(ka[kk], ka[kk + 4], 0x7632), prmt(kb[kk], kb[kk + 4], 0x7632), qs.ld(2, 4 * blk + kk));
-    }
+  for (int G = 0; G < 4; ++G) {
+    // tokens g, g+8: d = 32G + 8c + [0, 8)
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(kf + g * kHeadDim + 32 * G + 8 * c));
+    const uint4 y = __ldg(reinterpret_cast<const uint4*>(kf + (g + 8) * kHeadDim + 32 * G + 8 * c));
+    const uint4 q = qs.ld2(2, G);
+    mma_16816(s, prmt(x.x, x.z, 0x5410), prmt(y.x, y.z, 0x5410), prmt(x.x, x.z, 0x7632), prmt(y.x, y.z, 0x7632), lo2(q));
+    mma_16816(s, prmt(x.y, x.w, 0x5410), prmt(y.y, y.w, 0x5410), prmt(x.y, x.w, 0x7632), prmt(y.y, y.w, 0x7632), hi2(q));
   }
   if (g >= valid) { s[0] = -INFINITY; s[1] = -INFINITY; }
   if (g + 8 >= valid) { s[2] = -INFINITY; s[3] = -INFINITY; }
@@ -640,26 +417,20 @@ __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf
   const int toks[4] = {2 * c, 2 * c + 1, 2 * c + 8, 2 * c + 9};
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    uint32_t w[4][4];
+    uint2 w[4][2];  // [token][G - 2 half]: d = 32G + 4g + [0, 4)
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint2 a = __ldg(reinterpret_cast<const uint2*>(vf + toks[t] * kHeadDim + 16 * g) + half);
-      const uint2 b = __ldg(reinterpret_cast<const uint2*>(vf + toks[t] * kHeadDim + 16 * g + 8) + half);
-      w[t][0] = a.x; w[t][1] = a.y; w[t][2] = b.x; w[t][3] = b.y;
-    }
+    for (int t = 0; t < 4; ++t)
 #pragma unroll
-    for (int mm = 0; mm < 4; ++mm) {
-      const int mt = 4 * half + mm;
-      const uint32_t sel = (mm & 1) ? 0x7632 : 0x5410;
-      const int w0 = mm >> 1, w1 = 2 + (mm >> 1);
-      uint32_t a0 = prmt(w[0][w0], w[1][w0], sel), a1 = prmt(w[0][w1], w[1][w1], sel);
-      uint32_t a2 = prmt(w[2][w0], w[3][w0], sel), a3 = prmt(w[2][w1], w[3][w1], sel);
-      if (!EXACT) {  // match the quantized tiles' m-tile weight 2^(2(mt&3) - 6)
-        const __half2 wt = __float2half2_rn((float)(1 << (2 * (mt & 3))) * (1.0f / 64.0f));
-        a0 = h2_as_u32(__hmul2(u32_as_h2(a0), wt)); a1 = h2_as_u32(__hmul2(u32_as_h2(a1), wt));
-        a2 = h2_as_u32(__hmul2(u32_as_h2(a2), wt)); a3 = h2_as_u32(__hmul2(u32_as_h2(a3), wt));
-      }
-      mma_16816(st.acc[mt], a0, a1, a2, a3, bp0, bp1);
+      for (int i = 0; i < 2; ++i)
+        w[t][i] = __ldg(reinterpret_cast<const uint2*>(vf + toks[t] * kHeadDim + 32 * (2 * half + i) + 4 * g));
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int G = 2 * half + i;
+      // m-tile 2G: rows (e 0 | e 1); 2G+1: (e 2 | e 3); tokens (2c | 2c+1) and (2c+8 | 2c+9)
+      mma_16816(st.acc[2 * G], prmt(w[0][i].x, w[1][i].x, 0x5410), prmt(w[0][i].x, w[1][i].x, 0x7632),
+                prmt(w[2][i].x, w[3][i].x, 0x5410), prmt(w[2][i].x, w[3][i].x, 0x7632), bp0, bp1);
+      mma_16816(st.acc[2 * G + 1], prmt(w[0][i].y, w[1][i].y, 0x5410), prmt(w[0][i].y, w[1][i].y, 0x7632),
+                prmt(w[2][i].y, w[3][i].y, 0x5410), prmt(w[2][i].y, w[3][i].y, 0x7632), bp0, bp1);
     }
   }
 }
@@ -704,30 +475,19 @@ __device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc&
   for (int s = 0; s < Ring<BITS>::stages - 1; ++s) issue_at<BITS>(warp + stride * s, n, base, ring_l + s * Ring<BITS>::bytes);
 }
 
-// decode modes of a unit: normal; precise K (wide span x |q|; m <= 4, or m <= 8 in two passes);
-// exact (scales or q
-// too wide for the fp16-weighted forms)
-constexpr int kModeNormal = 0, kModePrecise = 1, kModeExact = 2, kModePrecise8 = 3;
+// Per-unit operand scaling of a warp (E: q, F: V; see "operand scaling").
+struct UnitScale {
+  int E, F;
+};
 
-template <int MODE>
-__device__ __forceinline__ void qk2(uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
-  if (MODE == kModePrecise || MODE == kModePrecise8) qk_precise<2, MODE == kModePrecise8>(sl, mo, po, qs, mg, s);
-  else qk_int2<MODE == kModeExact>(sl, mo, qs, mg, s);
-}
-template <int MODE>
-__device__ __forceinline__ void qk4(uint32_t sl, const MetaOff& mo, const PreciseOff& po, const QS& qs, uint32_t mg, float (&s)[4]) {
-  if (MODE == kModePrecise || MODE == kModePrecise8) qk_precise<4, MODE == kModePrecise8>(sl, mo, po, qs, mg, s);
-  else qk_int4<MODE == kModeExact>(sl, mo, qs, mg, s);
-}
 // The tile loop of one warp over one kind's range [0, n) (tiles warp, warp + 4, ...) through
 // the cp.async ring (prologue already issued), software-pipelined so that q.K^T of tile i+1
 // and P.V of tile i form one straight-line block (independent MMA chains the scheduler can
 // interleave).
-template <int MODE, int BITS>
-__device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc& src, const MetaOff& mo,
-                                          const PreciseOff& po, uint32_t ring_l, const QS& qs, uint32_t mg,
+template <int BITS>
+__device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc& src, const LaneOff& lo,
+                                          uint32_t ring_l, const QS& qs, const UnitScale& us,
                                           WarpState& st, int warp, int stride = kDecWarps) {
-  constexpr bool EXACT = MODE == kModeExact;
   constexpr int kStages = Ring<BITS>::stages, kStageBytes = Ring<BITS>::bytes;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
@@ -736,37 +496,32 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
   // address of the next tile to issue (kStages-1 ahead of the one consumed), advanced by one
   // warp stride per iteration: a loop-carried pointer instead of base + t * block each time
   const char* pn = tile_base<BITS>(a, src) + (int64_t)(warp + stride * (kStages - 1)) * (BITS == 2 ? kBlock2 : kBlock4);
+  const float kappa = exp2f((float)(24 - us.E)) * (BITS == 2 ? 1.0f / 3.0f : 1.0f / 15.0f);
+  const uint32_t f2 = h2_as_u32(__float2half2_rn(exp2f((float)us.F)));
   if (t < n) {
     uint32_t cur = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
     cp_wait<kStages - 2>();
     __syncwarp();
     float s0[4];
-    if (BITS == 2) qk2<MODE>(cur, mo, po, qs, mg, s0);
-    else qk4<MODE>(cur, mo, po, qs, mg, s0);
+    qk_tile<BITS>(cur, lo, qs, kappa, s0);
     uint32_t bp0, bp1;
-    softmax_tile<EXACT>(s0, st, bp0, bp1);
+    softmax_tile<false>(s0, st, bp0, bp1);
     while (true) {
       const int tn = t + stride;
       issue_at<BITS>(t + stride * (kStages - 1) < n ? 0 : 1, 1, pn, put);
       pn += kStep;
       if (tn >= n) {
-        if (BITS == 2) pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
-        else pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
+        pv_tile<BITS>(cur, lo, st, bp0, bp1, f2);
         break;
       }
       cp_wait<kStages - 2>();
       __syncwarp();
       const uint32_t nx = next(cur);
       float sn[4];
-      if (BITS == 2) {
-        qk2<MODE>(nx, mo, po, qs, mg, sn);
-        pv_int2<EXACT>(cur, mo, mg, st, bp0, bp1);
-      } else {
-        qk4<MODE>(nx, mo, po, qs, mg, sn);
-        pv_int4<EXACT>(cur, mo, mg, st, bp0, bp1);
-      }
-      __syncwarp();  // slot `cur` may be refilled from now on
-      softmax_tile<EXACT>(sn, st, bp0, bp1);
+      qk_tile<BITS>(nx, lo, qs, kappa, sn);
+      pv_tile<BITS>(cur, lo, st, bp0, bp1, f2);
+      __syncwarp();  // slot `cur` (and the scratch) may be refilled from now on
+      softmax_tile<false>(sn, st, bp0, bp1);
       put = cur;  // the refill slot trails the consumed one by a full ring (kStages - 1 ahead)
       cur = nx;
       t = tn;
@@ -776,35 +531,48 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
 }
 
 // Both phases of a CTA's quantized tiles: INT2 (its prologue issued before the PDL wait), then
-// INT4 (prologue here, or before the wait when the CTA has no INT2 tiles).
+// INT4 (prologue here, or before the wait when the CTA has no INT2 tiles).  The accumulator
+// moves from INT2 to INT4 row weights between the phases and to value units after them.
 __device__ __forceinline__ int rotate(int warp, int done, int stride) {  // (warp - done) mod stride
   const int r = (warp - done) % stride;
   return r < 0 ? r + stride : r;
 }
 
-template <int MODE>
 __device__ __forceinline__ void quantized_tiles(int n2, int n4, const DecArgs& a, const TileSrc& src,
-                                                const MetaOff& mo, const PreciseOff& po, uint32_t ring_l,
-                                                const QS& qs, uint32_t mg, WarpState& st, int warp,
+                                                const LaneOff& lo, uint32_t ring_l, const QS& qs,
+                                                const UnitScale& us, WarpState& st, int warp,
                                                 int stride = kDecWarps) {
   // the INT4 phase starts at the warp after the one that took the last INT2 tile, so every
   // warp's tile count over both phases is within one of the others' (the CTA's warps meet at
   // the merge barrier)
   const int w4 = rotate(warp, n2, stride);
   if (n2 > 0) {
-    run_tiles<MODE, 2>(n2, a, src, mo, po, ring_l, qs, mg, st, warp, stride);
+    run_tiles<2>(n2, a, src, lo, ring_l, qs, us, st, warp, stride);
     if (n4 > 0) {
       __syncwarp();
       prologue<4>(n4, a, src, ring_l, w4, stride);
     }
   }
-  if (n4 > 0) run_tiles<MODE, 4>(n4, a, src, mo, po, ring_l, qs, mg, st, w4, stride);
+  float w2[4], w4w[4], f[4];
+  phase_weights(2, us.F, w2);
+  phase_weights(4, us.F, w4w);
+  if (n4 > 0) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) f[e] = w4w[e] / w2[e];
+    scale_acc(st, f);
+    run_tiles<4>(n4, a, src, lo, ring_l, qs, us, st, w4, stride);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) f[e] = 1.0f / w4w[e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) f[e] = 1.0f / w2[e];
+  }
+  scale_acc(st, f);
 }
 
 // This CTA's share of its unit's FP16-region tiles (FP16-tier chunks, tail, decode tokens),
 // interleaved over the warps; pointers and ranges re-derived here (len_fp may have grown by
 // decode appends: read after the programmatic-dependent-launch wait).
-template <bool EXACT>
 __device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpState& st, int nq) {
   // thread coordinates re-read here (volatile): values carried from the kernel's start would be
   // spilled across the tile loop and reloaded in every iteration of this one
@@ -823,25 +591,49 @@ __device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpS
   // continue the quantized phases' rotation over the warps (nq quantized tiles before)
   for (int tf = f_begin + ((warp - nq) & (kDecWarps - 1)); tf < f_end; tf += kDecWarps) {
     const int r = tf * kTile;
-    tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
+    tile_fp16(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
   }
 }
 
+// Finish a warp: add the V zero-point sums of each m-tile's group (held by lanes (G, c)) and
+// reduce the row sums over the 8 row-groups.
+__device__ __forceinline__ void finish_warp(WarpState& st, int c) {
+#pragma unroll
+  for (int G = 0; G < 4; ++G) {
+    const float l0 = __shfl_sync(0xffffffffu, st.lacc[0], 4 * G + c);
+    const float l1 = __shfl_sync(0xffffffffu, st.lacc[1], 4 * G + c);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      st.acc[2 * G + h][0] += l0; st.acc[2 * G + h][1] += l1;
+      st.acc[2 * G + h][2] += l0; st.acc[2 * G + h][3] += l1;
+    }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
+    st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
+  }
+  st.lsum[0] += st.lsq[0];  // already summed over the 16 tokens of every tile
+  st.lsum[1] += st.lsq[1];
+}
+// head-dim index of accumulator element (mt, e2 = element >> 1) of lane row-group g
+__device__ __forceinline__ int acc_d(int mt, int e2, int g) { return 32 * (mt >> 1) + 4 * g + 2 * (mt & 1) + e2; }
+
 // ---- q staging (shared by both decode kernels) -----------------------------------------
-// q row `row` (zero if >= m) of unit (l, b, h), lane's 32 columns 32c.., scaled to log2 units
-// and rounded to the fp16 MMA operand.
+// q row `row` (zero if >= m) of unit (l, b, h): the lane's 32 elements d = 32G + 8c + k
+// (qv[8G + k]), scaled to log2 units and rounded to the fp16 MMA operand.
 __device__ __forceinline__ void load_q_rows(const DecArgs& a, int l, int b, int h, int row, int c, float (&qv)[32]) {
-  const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + row) * kHeadDim + 32 * c;
+  const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + row) * kHeadDim + 8 * c;
   if (row < a.m) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint4 x = reinterpret_cast<const uint4*>(qrow)[u];
+    for (int G = 0; G < 4; ++G) {
+      const uint4 x = reinterpret_cast<const uint4*>(qrow + 32 * G)[0];
       const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = __half22float2(u32_as_h2(w[e]));
-        qv[8 * u + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
-        qv[8 * u + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
+        qv[8 * G + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
+        qv[8 * G + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
       }
     }
   } else {
@@ -850,56 +642,67 @@ __device__ __forceinline__ void load_q_rows(const DecArgs& a, int l, int b, int 
   }
 }
 
-// decode mode of a unit from its q (the warp's 8 rows) and its span bounds
-__device__ __forceinline__ int unit_mode(const DecArgs& a, const float (&qv)[32], bool span_wide, float kspan) {
+// the unit's q exponent E from its q rows (all 8 row-groups of the warp)
+__device__ __forceinline__ int unit_q_exponent(const float (&qv)[32]) {
   float qmaxabs = 0.f;
 #pragma unroll
   for (int e = 0; e < 32; ++e) qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) qmaxabs = fmaxf(qmaxabs, __shfl_xor_sync(0xffffffffu, qmaxabs, o));
-  const bool wide = qmaxabs > kWideQ || span_wide;
-  return wide ? kModeExact
-              : (kspan * qmaxabs > kPreciseSpanQ ? (a.m <= 4 ? kModePrecise : kModePrecise8) : kModeNormal);
+  return q_exponent(qmaxabs);
+}
+// the unit's V exponent F (span_max is build-time data: readable before the PDL wait)
+__device__ __forceinline__ int unit_v_exponent(const DecArgs& a, int l, int b, int h) {
+  const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // [L][H][B]
+  return a.V.span_max ? v_exponent(__uint_as_float(a.V.span_max[fidx])) : 0;
 }
 
-// Part `part` of a unit's q staging into s_qu (kQBytes) / s_biasu: 0-2 the q-fragment sets
-// (0: INT2 slot weights, 1: INT4, 2: unweighted; parts 0/1 also the precise-mode bias), 3 the
-// zero-point entry.
-__device__ __forceinline__ void stage_q_part(const DecArgs& a, const float (&qv)[32], int part, unsigned char* s_qu,
-                                             float* s_biasu, int lane) {
-  const int g = lane >> 2, c = lane & 3;
-  // slot weights 2^(6-j) of K pair i: INT2 j = 2i (i <= 4) or 2(i-5); INT4 j = 4(i & 1)
-  auto slot_w = [&](int set, int i) {
-    return set == 0 ? exp2f((float)(6 - (i <= 4 ? 2 * i : 2 * (i - 5))))
-                    : (set == 1 ? exp2f((float)(6 - 4 * (i & 1))) : 1.0f);
-  };
+// Part `part` of a unit's q staging into s_qu (kQBytes): 0-2 the q-fragment sets (0: INT2 slot
+// weights 2^(E - j), 1: INT4, 2: unweighted), 3 the zero-point entry.  Whole warp.
+__device__ __forceinline__ void stage_q_part(const float (&qv)[32], int part, int E, unsigned char* s_qu, int lane) {
+  const int c = lane & 3;
   if (part < 3) {
-    float qsw = 0.f;
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const int i0 = 2 * (ks & 3), i1 = i0 + 1;  // K pair index inside the 16-d block
-      const int d0 = 16 * (ks >> 2) + i0;        // lane-local index within group c
-      // INT2 / INT4 sets also carry the fold of the fp16(1/qmax) rounding (see kdeq)
-      const float fold = part == 0 ? kscale_fold(1.0f / 3.0f) : (part == 1 ? kscale_fold(1.0f / 15.0f) : 1.0f);
-      const float x0 = slot_w(part, i0) * fold, x1 = slot_w(part, i1) * fold;
-      const __half2 lo = __floats2half2_rn(qv[d0] * x0, qv[d0 + 8] * x0);
-      const __half2 hi = __floats2half2_rn(qv[d0 + 1] * x1, qv[d0 + 9] * x1);
-      reinterpret_cast<uint2*>(s_qu + part * kQSet + 512 * (ks >> 1) + 16 * lane)[ks & 1] =
-          make_uint2(h2_as_u32(lo), h2_as_u32(hi));
-      const float2 fl = __half22float2(lo), fh = __half22float2(hi);
-      qsw += (fl.x + fl.y) + (fh.x + fh.y);
+    for (int G = 0; G < 4; ++G) {
+      uint32_t v[4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        // b0: cols 2c, 2c+1 (code e = 2h: INT2 j = 4h, INT4 j = 0); b1: cols 2c+8, 2c+9 (e = 2h+1)
+        const int j0 = part == 0 ? 4 * h : 0, j1 = part == 0 ? 4 * h + 2 : 4;
+        const float w0 = part == 2 ? 1.0f : exp2f((float)(E - j0)), w1 = part == 2 ? 1.0f : exp2f((float)(E - j1));
+        v[2 * h] = h2_as_u32(__floats2half2_rn(qv[8 * G + 2 * h] * w0, qv[8 * G + 4 + 2 * h] * w0));
+        v[2 * h + 1] = h2_as_u32(__floats2half2_rn(qv[8 * G + 2 * h + 1] * w1, qv[8 * G + 5 + 2 * h] * w1));
+      }
+      reinterpret_cast<uint4*>(s_qu + part * kQSet + 512 * G)[lane] = make_uint4(v[0], v[1], v[2], v[3]);
     }
-    // precise-mode bias 16 Q'[tier][group c][q row g]: the sum of exactly the fp16 weighted
-    // values this lane's B fragments hold
-    if (part < 2) s_biasu[part * 4 * kBiasRows + c * kBiasRows + g] = 16.0f * qsw;
   } else {
-    float qsum = 0.f;
+    float P[4];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) qsum += qv[e];
+    for (int G = 0; G < 4; ++G) {
+      P[G] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) P[G] += qv[8 * G + k];
+      P[G] += __shfl_xor_sync(0xffffffffu, P[G], 1);
+      P[G] += __shfl_xor_sync(0xffffffffu, P[G], 2);
+    }
+    const float qsum = c == 0 ? P[0] : (c == 1 ? P[1] : (c == 2 ? P[2] : P[3]));
     const __half qhi = __float2half_rn(qsum);
     const __half qlo = __float2half_rn(qsum - __half2float(qhi));
     reinterpret_cast<uint32_t*>(s_qu + 3 * kQSet)[lane] = h2_as_u32(__halves2half2(qhi, qlo));
   }
+}
+
+// per-lane constants of the tile functions; `scratch` = this warp's kScratch bytes
+__device__ __forceinline__ LaneOff lane_offsets(uint32_t scratch, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+  LaneOff lo;
+  lo.mk = -8 * lane;
+  lo.mv = 16 * (4 * (g & 3) + c) - 16 * lane;
+  lo.sk = scratch + 4 * lane;
+  lo.kc = scratch + 16 * g;
+  lo.vp = scratch + 256 + 8 * (4 * c + (g & 3));
+  lo.vc = scratch + 256 + 32 * c;
+  return lo;
 }
 
 __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const DecArgs a) {
@@ -908,7 +711,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   __shared__ float s_ml[kDecWarps][8][2];
   __shared__ __align__(16) unsigned char s_q[kQBytes];
   __shared__ int s_last;
-  __shared__ __align__(16) float s_bias[2 * 4 * kBiasRows];  // precise modes: 16 Q' [tier][group][q row]
+  __shared__ __align__(16) unsigned char s_scr[kDecWarps][kScratch];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   __shared__ int64_t s_tr[12], s_tend[kDecWarps];
@@ -933,9 +736,6 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     src.c2 = (unit * a.K.rows2 + r2) / kTileRows * kBlock2 + 16 * lane;
     src.c4 = (unit * a.K.rows4 + r4) / kTileRows * kBlock4 + 16 * lane;
   }
-  MetaOff mo;
-  mo.k = -8 * lane;
-  mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0]) + 16 * lane;
   if (cnt2 > 0) prologue<2>(cnt2, a, src, ring_l, warp);
   else prologue<4>(nloc, a, src, ring_l, warp);
@@ -943,51 +743,32 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   // Everything above touched only build-time data.  q, the FP16 region and len_fp may come
   // from the preceding kernel on the stream: wait for it (no-op without PDL), and let the next
   // decode launch (next layer) start its own prologue as soon as SMs free up.
-  // the unit's span bounds are build-time data too: read them before the wait
-  bool span_wide;
-  float kspan;
+  // the unit's V span bound is build-time data too: read it before the wait
+  UnitScale us;
   {
     const CtaIds id = cta_ids(a.Bc, a.b0);
-    const int64_t fidx = ((int64_t)id.l * a.H + id.h) * a.B + id.b;  // span flags are [L][H][B]
-    span_wide = (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
-                (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
-    kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
+    us.F = unit_v_exponent(a, id.l, id.b, id.h);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
 
   // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m).  Every warp loads the
-  // same 8 rows and derives the unit's mode from max |q| and the K span bound; then warps 0-2
-  // write q-fragment sets 0-2 (precise mode: the group-masked INT2 / INT4 sets and their 16 Q'
-  // bias constants instead of sets 0 and 1), warp 3 the zero-point entry.
-  int mode;
+  // same 8 rows and derives the unit's q exponent from max |q|; then warps 0-2 write q-fragment
+  // sets 0-2, warp 3 the zero-point entry.
   {
     const CtaIds id = cta_ids(a.Bc, a.b0);
     float qv[32];
     load_q_rows(a, id.l, id.b, id.h, g, c, qv);
-    mode = unit_mode(a, qv, span_wide, kspan);
-    stage_q_part(a, qv, warp < 3 ? warp : 3, s_q, s_bias, lane);
+    us.E = unit_q_exponent(qv);
+    stage_q_part(qv, warp < 3 ? warp : 3, us.E, s_q, lane);
   }
   __syncthreads();
   if (threadIdx.x == 0 && tracing()) s_tr[2] = gtime();
   QS qs;
   qs.base = (uint32_t)__cvta_generic_to_shared(s_q) + 16 * lane;
   qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_q) + 3 * kQSet + 4 * lane;
-  PreciseOff po;
-  {
-    const int G0 = c >> 1, qa = (2 * c) & 3;
-    po.m0 = (g * 4 + G0) * 8 - 16 * lane;
-    po.m1 = (g * 4 + G0 + 2) * 8 - 16 * lane;
-    po.bias = (uint32_t)__cvta_generic_to_shared(s_bias) + (G0 * kBiasRows + qa) * 4;
-    po.qoff = 16 * (((g & 3) * 4 + c) - lane);
-    po.qoff2 = 16 * ((((g & 3) + 4) * 4 + c) - lane);
-    po.hi_rows = c >= 2;
-    const bool in = (g >> 2) == (c & 1);  // column g takes group c (variant c / 2)
-    po.msk0 = in && (c >> 1) == 0 ? 0xffffffffu : 0u;
-    po.msk1 = in && (c >> 1) == 1 ? 0xffffffffu : 0u;
-  }
-  const uint32_t mg = kMagic16 | a.zero;
+  const LaneOff lo = lane_offsets((uint32_t)__cvta_generic_to_shared(&s_scr[warp][0]), lane);
 
   WarpState st;
 #pragma unroll
@@ -997,45 +778,20 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   st.mrun[0] = st.mrun[1] = -INFINITY;
   st.lsum[0] = st.lsum[1] = 0.f;
 
-  if (mode == kModeExact) {
-    quantized_tiles<kModeExact>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
-    fp16_tiles<true>(a, qs, st, nloc);
-  } else {
-    if (mode == kModePrecise) quantized_tiles<kModePrecise>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
-    else if (mode == kModePrecise8) quantized_tiles<kModePrecise8>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
-    else quantized_tiles<kModeNormal>(cnt2, nloc - cnt2, a, src, mo, po, ring_l, qs, mg, st, warp);
-    fp16_tiles<false>(a, qs, st, nloc);
-    // undo the V m-tile weights 2^(2(mt&3) - 6)
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const float f = (float)(64 >> (2 * (mt & 3)));
-      st.acc[mt][0] *= f; st.acc[mt][1] *= f; st.acc[mt][2] *= f; st.acc[mt][3] *= f;
-    }
-  }
+  quantized_tiles(cnt2, nloc - cnt2, a, src, lo, ring_l, qs, us, st, warp);
+  fp16_tiles(a, qs, st, nloc);
 
   if (lane == 0 && tracing()) s_tend[warp] = gtime();
-  // finish the warp: fold the zero-point term, reduce row sums over the 8 row-groups
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    st.acc[mt][0] += st.lacc[0]; st.acc[mt][1] += st.lacc[1];
-    st.acc[mt][2] += st.lacc[0]; st.acc[mt][3] += st.lacc[1];
-  }
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {
-    st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
-    st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
-  }
-  st.lsum[0] += st.lsq[0];  // already summed over the 16 tokens of every tile
-  st.lsum[1] += st.lsq[1];
+  finish_warp(st, c);
   __syncthreads();  // ring -> merge buffer reuse
   if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
   float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0]);
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
-    s_acc[warp][2 * c][16 * g + mt] = st.acc[mt][0];
-    s_acc[warp][2 * c + 1][16 * g + mt] = st.acc[mt][1];
-    s_acc[warp][2 * c][16 * g + 8 + mt] = st.acc[mt][2];
-    s_acc[warp][2 * c + 1][16 * g + 8 + mt] = st.acc[mt][3];
+    s_acc[warp][2 * c][acc_d(mt, 0, g)] = st.acc[mt][0];
+    s_acc[warp][2 * c + 1][acc_d(mt, 0, g)] = st.acc[mt][1];
+    s_acc[warp][2 * c][acc_d(mt, 1, g)] = st.acc[mt][2];
+    s_acc[warp][2 * c + 1][acc_d(mt, 1, g)] = st.acc[mt][3];
   }
   if (g == 0) {
     s_ml[warp][2 * c][0] = st.mrun[0]; s_ml[warp][2 * c][1] = st.lsum[0];
@@ -1224,7 +980,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   unsigned char (*s_ring)[kWarpRing] = reinterpret_cast<unsigned char (*)[kWarpRing]>(s_dyn);
   unsigned char* s_qall = s_dyn + kWpWarps * kWarpRing;
   __shared__ float s_ml[kWpWarps][8][2];
-  __shared__ __align__(16) float s_biasall[8][2 * 4 * kBiasRows];
+  __shared__ __align__(16) unsigned char s_scr[kWpWarps][kScratch];
   __shared__ int s_lastu[8];
   __shared__ int4 s_slot[8];             // per unit slot: warps [x, y) of this CTA, first / last CTA of the unit
   __shared__ unsigned short s_rtab[64];  // merge row r -> (slot << 8 | q row)
@@ -1257,20 +1013,11 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     src.c2 = (unit * a.K.rows2 + s0.x + (int64_t)a2 * kTile) / kTileRows * kBlock2 + 16 * lane;
     src.c4 = (unit * a.K.rows4 + s0.z + (int64_t)a4 * kTile) / kTileRows * kBlock4 + 16 * lane;
   }
-  MetaOff mo;
-  mo.k = -8 * lane;
-  mo.v = 16 * ((g >> 1) * 4 + c) - 16 * lane;
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0]) + 16 * lane;
   if (n2t > 0) prologue<2>(n2t, a, src, ring_l, k, np);
   else prologue<4>(n4t, a, src, ring_l, k, np);
-  bool span_wide;
-  float kspan;
-  {
-    const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // span flags are [L][H][B]
-    span_wide = (a.K.span_flags != nullptr && a.K.span_flags[fidx] != 0u) ||
-                (a.V.span_flags != nullptr && a.V.span_flags[fidx] != 0u);
-    kspan = a.K.span_max != nullptr ? __uint_as_float(a.K.span_max[fidx]) : 0.f;
-  }
+  UnitScale us;
+  us.F = unit_v_exponent(a, l, b, h);
   // per-slot facts for the merge (build-time plan data: before the wait)
   const int u_last = __ldg(wunit + cta * kWpWarps + kWpWarps - 1);
   const int nslots = u_last - u0 + 1;
@@ -1288,26 +1035,25 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   // into this SM)
   if (g < a.m) {
     const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * c;
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow));  // the row's 4 lanes cover its 256 B
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
 
   // q staging: every unit slot of the CTA needs parts 0-3; the warps share the jobs
-  int mode;
   {
     float qv[32];
-    load_q_rows(a, l, b, h, g, c, qv);  // this warp's unit: its mode (and its staging jobs)
-    mode = unit_mode(a, qv, span_wide, kspan);
+    load_q_rows(a, l, b, h, g, c, qv);  // this warp's unit: its q exponent (and its staging jobs)
+    us.E = unit_q_exponent(qv);
     for (int j = warp; j < 4 * nslots; j += kWpWarps) {
       const int uj = u0 + (j >> 2);
       if (uj == u) {
-        stage_q_part(a, qv, j & 3, s_qall + (j >> 2) * kQBytes, s_biasall[j >> 2], lane);
+        stage_q_part(qv, j & 3, us.E, s_qall + (j >> 2) * kQBytes, lane);
       } else {
         float qj[32];
         load_q_rows(a, l, uj / a.H, uj % a.H, g, c, qj);
-        stage_q_part(a, qj, j & 3, s_qall + (j >> 2) * kQBytes, s_biasall[j >> 2], lane);
+        stage_q_part(qj, j & 3, unit_q_exponent(qj), s_qall + (j >> 2) * kQBytes, lane);
       }
     }
   }
@@ -1316,20 +1062,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   QS qs;
   qs.base = (uint32_t)__cvta_generic_to_shared(s_qall + slot * kQBytes) + 16 * lane;
   qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_qall + slot * kQBytes) + 3 * kQSet + 4 * lane;
-  PreciseOff po;
-  {
-    const int G0 = c >> 1, qa = (2 * c) & 3;
-    po.m0 = (g * 4 + G0) * 8 - 16 * lane;
-    po.m1 = (g * 4 + G0 + 2) * 8 - 16 * lane;
-    po.bias = (uint32_t)__cvta_generic_to_shared(s_biasall[slot]) + (G0 * kBiasRows + qa) * 4;
-    po.qoff = 16 * (((g & 3) * 4 + c) - lane);
-    po.qoff2 = 16 * ((((g & 3) + 4) * 4 + c) - lane);
-    po.hi_rows = c >= 2;
-    const bool in = (g >> 2) == (c & 1);
-    po.msk0 = in && (c >> 1) == 0 ? 0xffffffffu : 0u;
-    po.msk1 = in && (c >> 1) == 1 ? 0xffffffffu : 0u;
-  }
-  const uint32_t mg = kMagic16 | a.zero;
+  const LaneOff lo = lane_offsets((uint32_t)__cvta_generic_to_shared(&s_scr[warp][0]), lane);
 
   WarpState st;
 #pragma unroll
@@ -1340,8 +1073,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   st.lsum[0] = st.lsum[1] = 0.f;
 
   // this warp's FP16-region tiles: the unit's, continuing the rotation after the quantized ones
-  auto fp16_part = [&](auto exact_tag) {
-    constexpr bool EXACT = decltype(exact_tag)::value;
+  auto fp16_part = [&]() {
     const int off_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 4];
     const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * b + 5];
     const int nft = (len_fp + kTile - 1) / kTile;
@@ -1351,41 +1083,17 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     const uint16_t* vf = a.V.fp + (unit * a.V.rows_fp + off_fp) * kHeadDim;
     for (int tf = f_begin + rotate(k, n2t + n4t, np); tf < f_end; tf += np) {
       const int r = tf * kTile;
-      tile_fp16<EXACT>(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
+      tile_fp16(kf + (int64_t)r * kHeadDim, vf + (int64_t)r * kHeadDim, len_fp - r, qs, st, g, c);
     }
   };
-  if (mode == kModeExact) {
-    quantized_tiles<kModeExact>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
-    fp16_part(std::true_type{});
-  } else {
-    if (mode == kModePrecise) quantized_tiles<kModePrecise>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
-    else if (mode == kModePrecise8) quantized_tiles<kModePrecise8>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
-    else quantized_tiles<kModeNormal>(n2t, n4t, a, src, mo, po, ring_l, qs, mg, st, k, np);
-    fp16_part(std::false_type{});
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const float f = (float)(64 >> (2 * (mt & 3)));
-      st.acc[mt][0] *= f; st.acc[mt][1] *= f; st.acc[mt][2] *= f; st.acc[mt][3] *= f;
-    }
-  }
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    st.acc[mt][0] += st.lacc[0]; st.acc[mt][1] += st.lacc[1];
-    st.acc[mt][2] += st.lacc[0]; st.acc[mt][3] += st.lacc[1];
-  }
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {
-    st.lsum[0] += __shfl_xor_sync(0xffffffffu, st.lsum[0], o);
-    st.lsum[1] += __shfl_xor_sync(0xffffffffu, st.lsum[1], o);
-  }
-  st.lsum[0] += st.lsq[0];
-  st.lsum[1] += st.lsq[1];
+  quantized_tiles(n2t, n4t, a, src, lo, ring_l, qs, us, st, k, np);
+  fp16_part();
+  finish_warp(st, c);
   if (lane == 0 && tracing()) s_tend[warp] = gtime();
   // Park this warp's partial (rows < m) in its own ring region (its copies are all waited:
-  // no barrier needed before the stores).  Column of (q row, d): d's low 4 bits XOR
-  // (g >> 1 | row/2 << 2), g = d / 16 — every store instruction of a warp hits 32 distinct
-  // banks (unswizzled: 16 lanes per bank).
-  auto swz = [](int row, int d) { return (d & ~15) | ((d ^ ((((d >> 4) & 7) >> 1) | ((row >> 1) << 2))) & 15); };
+  // no barrier needed before the stores).  Column of (q row, d): d XOR (row / 2) in its low 2
+  // bits — a store instruction writes rows 2c (+1) x d = 32G + 4g + e: 32 distinct banks.
+  auto swz = [](int row, int d) { return d ^ ((row >> 1) & 3); };
   {
     __syncwarp();
     float (*s_accw)[kHeadDim] = reinterpret_cast<float (*)[kHeadDim]>(&s_ring[warp][0]);
@@ -1393,12 +1101,12 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
       if (r0) {
-        s_accw[2 * c][swz(2 * c, 16 * g + mt)] = st.acc[mt][0];
-        s_accw[2 * c][swz(2 * c, 16 * g + 8 + mt)] = st.acc[mt][2];
+        s_accw[2 * c][swz(2 * c, acc_d(mt, 0, g))] = st.acc[mt][0];
+        s_accw[2 * c][swz(2 * c, acc_d(mt, 1, g))] = st.acc[mt][2];
       }
       if (r1) {
-        s_accw[2 * c + 1][swz(2 * c + 1, 16 * g + mt)] = st.acc[mt][1];
-        s_accw[2 * c + 1][swz(2 * c + 1, 16 * g + 8 + mt)] = st.acc[mt][3];
+        s_accw[2 * c + 1][swz(2 * c + 1, acc_d(mt, 0, g))] = st.acc[mt][1];
+        s_accw[2 * c + 1][swz(2 * c + 1, acc_d(mt, 1, g))] = st.acc[mt][3];
       }
     }
     if (g == 0) {
@@ -1608,6 +1316,7 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
                       reinterpret_cast<const char*>(k_arena.meta4) == k4 + 2 * kTileBytes4 &&
                       reinterpret_cast<const char*>(v_arena.meta4) == k4 + 2 * kTileBytes4 + kTileBytesMeta);
     if (!ok2 || !ok4 || k_arena.rows2 != v_arena.rows2 || k_arena.rows4 != v_arena.rows4) return CKV_ERR_ARG;
+    if (!v_arena.span_max && (v_arena.rows2 || v_arena.rows4)) return CKV_ERR_ARG;  // sizes the V operand scaling
   }
   DecArgs a;
   a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
@@ -1698,6 +1407,7 @@ int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_
                       reinterpret_cast<const char*>(k_arena.meta4) == k4 + 2 * kTileBytes4 &&
                       reinterpret_cast<const char*>(v_arena.meta4) == k4 + 2 * kTileBytes4 + kTileBytesMeta);
     if (!ok2 || !ok4 || k_arena.rows2 != v_arena.rows2 || k_arena.rows4 != v_arena.rows4) return CKV_ERR_ARG;
+    if (!v_arena.span_max && (v_arena.rows2 || v_arena.rows4)) return CKV_ERR_ARG;  // sizes the V operand scaling
   }
   WpArgs w;
   DecArgs& a = w.d;

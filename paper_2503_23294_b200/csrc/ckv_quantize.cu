@@ -173,21 +173,12 @@ __device__ __forceinline__ void quantize_slice16(const uint32_t (&w)[8], uint32_
   if (d1 > kNear) c[1] = exact_slice(w[4], w[5], w[6], w[7], lo, hi, qinv, qmax, base);
 }
 
-// Staging offsets of the tile-native layout (ckv_common.cuh tile_off_*) for row
-// r = 2 (r4 + u) + sub and slice j, decomposed as
-//   (r4 >> 3) TB + ((r4 >> 2) & 1) X + u U + L(j, sub, hf)
-// so each store costs one add (the GPU parity tests read every arena back through
-// ckv_arena_export, i.e. through tile_off_*, and compare with the reference bit for bit).
-template <int BITS, bool ISV> struct StageOff {
+// Staging offsets of the tile-native layout (ckv_common.cuh tile_byte_* / tile_off_*): each
+// pass computes a per-lane base once and adds (tile h) TB + (step it) part per store (the GPU
+// parity tests read every arena back through ckv_arena_export, i.e. through the layout
+// functions, and compare with the reference bit for bit).
+template <int BITS> struct StageTB {
   static constexpr int TB = BITS == 2 ? kBlock2 : kBlock4;  // staging holds whole K/V blocks
-  static constexpr int X = BITS == 2 ? 8 : 512;
-  static constexpr int U = ISV ? 16 : 128;
-  __device__ __forceinline__ static int lane(int j, int sub) {
-    if (BITS == 2) return ISV ? (j >> 1) * 64 + (j & 1) * 4 + sub * 2
-                              : sub * 64 + (j >> 2) * 16 + ((j >> 1) & 1) * 4 + (j & 1) * 2;
-    return ISV ? (j >> 1) * 64 + (j & 1) * 8 + sub * 2
-               : sub * 64 + (j >> 2) * 16 + ((j & 3) >> 1) * 8 + (j & 1) * 2;  // hf = 1: + 4
-  }
 };
 template <int BITS, bool ISV> struct MetaStageOff {
   static constexpr int TB = BITS == 2 ? kBlock2 : kBlock4;
@@ -211,6 +202,9 @@ __device__ __forceinline__ void l2_prefetch(const void* p) {
 
 // 32-bit shared-memory stores (staging addresses are 32-bit shared-window offsets: no 64-bit
 // generic pointer arithmetic in the quantize loops)
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)(v & 0xFFu)) : "memory");
+}
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
@@ -237,10 +231,13 @@ __device__ __forceinline__ bool chunk_flags(float smax, float qmax, bool& bad) {
 template <int BITS>
 __device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int sT, int lane,
                                                  uint32_t sc, uint32_t sm, bool& bad, float& smax) {
-  using SO = StageOff<BITS, true>;
   using MO = MetaStageOff<BITS, true>;
+  constexpr int TB = StageTB<BITS>::TB;
   const int rr = lane >> 1, hg = lane & 1, sub = rr & 1;
-  const uint32_t cb = sc + ((rr >> 3) & 1) * SO::X + ((rr >> 1) & 3) * SO::U + SO::lane(hg, sub);
+  // row rr of tile h: lane (g = 2 hg (+1, +4, +5), c = (rr & 7) / 2); INT2 byte 2 (rr & 1) of
+  // word 2 (rr >= 8) + it / 2 (+ it & 1 per step), INT4 half rr & 1 of word it in half rr >= 8
+  const uint32_t cb = BITS == 2 ? sc + 128 * hg + 16 * ((rr & 7) >> 1) + 8 * (rr >> 3) + 2 * (rr & 1)
+                                : sc + 512 * (rr >> 3) + 128 * hg + 16 * ((rr & 7) >> 1) + 2 * (rr & 1);
   const uint32_t mbase = sm + ((rr >> 3) & 1) * MO::X + ((rr >> 1) & 3) * MO::U + MO::lane(0, sub);
   const uint4* srow = reinterpret_cast<const uint4*>(src + (int64_t)rr * sT) + hg;
 #pragma unroll 1
@@ -253,19 +250,26 @@ __device__ __forceinline__ bool quantize_chunk_v(const uint16_t* src, int sT, in
       xs[2 * h + 1] = __ldg(p + 2);
       if (it == 0) l2_prefetch(p + 8);  // the row's second 128-byte line (steps 2, 3)
     }
-    // slices j0 = 4 it + hg and j0 + 2: SO::lane(j, sub) = SO::lane(j mod 2, sub) + (j / 2) * 64
+    // slices j0 = 4 it + hg and j0 + 2 (elements 32 it + 8 hg + [0, 8) and + 16)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t w[8] = {xs[2 * h].x, xs[2 * h].y, xs[2 * h].z, xs[2 * h].w,
                              xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
       uint32_t c[2], meta;
       quantize_slice16<BITS>(w, c, meta, smax);
-      const uint32_t c0 = cb + h * SO::TB + it * 128, c1 = c0 + 64;
-      sts16(c0, c[0]);
-      sts16(c1, c[1]);
-      if (BITS == 4) {
-        sts16(c0 + 4, c[0] >> 16);
-        sts16(c1 + 4, c[1] >> 16);
+      // c[0]: elements 32 it + 8 hg + [0, 8) -> lanes g = 2 hg, 2 hg + 1; c[1]: +16 -> g + 4
+      if (BITS == 2) {
+        const uint32_t c0 = cb + h * TB + 4 * (it >> 1) + (it & 1);
+        sts8(c0, c[0]);
+        sts8(c0 + 64, c[0] >> 8);
+        sts8(c0 + 256, c[1]);
+        sts8(c0 + 320, c[1] >> 8);
+      } else {
+        const uint32_t c0 = cb + h * TB + 4 * it;
+        sts16(c0, c[0]);
+        sts16(c0 + 64, c[0] >> 16);
+        sts16(c0 + 256, c[1]);
+        sts16(c0 + 320, c[1] >> 16);
       }
       // both lanes of the group hold the same (lo, hi): duplicate stores, no branch
       const uint32_t mb = mbase + h * MO::TB + it * 64;
@@ -280,14 +284,18 @@ template <int BITS, bool ISV>
 __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int sT, int lane, uint32_t sc, uint32_t sm,
                                                bool& bad, float& smax) {
   if (ISV) return quantize_chunk_v<BITS>(src, sT, lane, sc, sm, bad, smax);
-  using SO = StageOff<BITS, ISV>;
   using MO = MetaStageOff<BITS, ISV>;
+  constexpr int TB = StageTB<BITS>::TB;
   const int rs = lane >> 3, jj = lane & 7;
-  const int sub = rs & 1, j0 = 2 * jj;
-  // per-lane parts of the code and metadata offsets: the lane's rows differ from its step's
-  // first row in bits 0 and 3 (sub, X), which keeps the K stores of a warp in distinct banks
-  // (bits 1-2 (U) would alias them)
-  const uint32_t cb = sc + SO::lane(j0, sub) + (rs >> 1) * SO::X;
+  const int sub = rs & 1, j0 = 2 * jj, hi8 = rs >> 1;
+  // the lane's row rt = 2 it + sub + 8 hi8 of tile h, reference word jj (INT2: bytes 4 jj ..
+  // 4 jj + 3; INT4: words 2 jj, 2 jj + 1).  INT2: the rows rt and rt + 8 of a word interleave
+  // byte by byte in the tile (lanes l, l ^ 16 hold them): one shuffle, then each lane stores
+  // one whole 32-bit word (c = 2 (jj & 1) + hi8, group jj / 2).  INT4: word 2 jj + k -> lane
+  // c = 2 (jj & 1) + k, group jj / 2, half hi8.  Every store instruction: distinct banks.
+  const uint32_t cb = BITS == 2 ? sc + 64 * sub + 16 * (2 * (jj & 1) + hi8) + 4 * (jj >> 1)
+                                : sc + 512 * hi8 + 64 * sub + 32 * (jj & 1) + 4 * (jj >> 1);
+  const uint32_t sel = hi8 ? 0x3726u : 0x5140u;  // [lo.b0 hi.b0 lo.b1 hi.b1] / [lo.b2 hi.b2 lo.b3 hi.b3]
   const uint32_t mbase = sm + MO::lane(j0, sub) + (rs >> 1) * MO::X;
   const uint4* srow = reinterpret_cast<const uint4*>(src + (int64_t)(sub + 8 * (rs >> 1)) * sT) + 2 * jj;
 #pragma unroll 1
@@ -306,10 +314,15 @@ __device__ __forceinline__ bool quantize_chunk(const uint16_t* src, int sT, int 
                              xs[2 * h + 1].x, xs[2 * h + 1].y, xs[2 * h + 1].z, xs[2 * h + 1].w};
       uint32_t c[2], meta;
       quantize_slice16<BITS>(w, c, meta, smax);
-      // the two slices' 16-bit pieces are adjacent (SO::lane(j0 + 1) = + 2)
-      const uint32_t c0 = cb + h * SO::TB + it * SO::U;
-      if (BITS == 2) sts32(c0, prmt_q(c[0], c[1], 0x5410));
-      else sts64(c0, prmt_q(c[0], c[1], 0x5410), prmt_q(c[0], c[1], 0x7632));
+      const uint32_t c0 = cb + h * TB + it * 128;
+      if (BITS == 2) {
+        const uint32_t v = prmt_q(c[0], c[1], 0x5410);  // the reference's word jj of row rt
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v, 16);  // ... of row rt ^ 8
+        sts32(c0, prmt_q(v, o, sel));
+      } else {
+        sts32(c0, c[0]);
+        sts32(c0 + 16, c[1]);
+      }
       // both lanes of the group hold the same (lo, hi): duplicate stores, no branch
       sts32(mbase + h * MO::TB + it * MO::U, meta);
     }
@@ -490,16 +503,18 @@ __global__ void arena_export_kernel(const unsigned char* __restrict__ codes,
     const int64_t r = i / words;
     const int w = (int)(i % words), rt = (int)(r & 15);
     const unsigned char* t = codes + (r >> 4) * stride;
-    int o0, o1;
-    if (words == 8) {
-      o0 = is_v ? tile_off_v2(rt, w, 0) : tile_off_k2(rt, w, 0);
-      o1 = is_v ? tile_off_v2(rt, w, 1) : tile_off_k2(rt, w, 1);
+    if (words == 8) {  // INT2: bytes 4w .. 4w+3
+      uint32_t x = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        x |= (uint32_t)t[is_v ? tile_byte_v2(rt, 4 * w + k) : tile_byte_k2(rt, 4 * w + k)] << (8 * k);
+      out_codes[i] = x;
     } else {
-      o0 = is_v ? tile_off_v4(rt, w, 0) : tile_off_k4(rt, w, 0);
-      o1 = is_v ? tile_off_v4(rt, w, 1) : tile_off_k4(rt, w, 1);
+      const int o0 = is_v ? tile_off_v4(rt, w, 0) : tile_off_k4(rt, w, 0);
+      const int o1 = is_v ? tile_off_v4(rt, w, 1) : tile_off_k4(rt, w, 1);
+      out_codes[i] = (uint32_t)*reinterpret_cast<const uint16_t*>(t + o0) |
+                     ((uint32_t)*reinterpret_cast<const uint16_t*>(t + o1) << 16);
     }
-    out_codes[i] = (uint32_t)*reinterpret_cast<const uint16_t*>(t + o0) |
-                   ((uint32_t)*reinterpret_cast<const uint16_t*>(t + o1) << 16);
   } else if (i < n_code + rows * kGroupsPerRow) {
     const int64_t k = i - n_code, r = k / kGroupsPerRow;
     const int G = (int)(k % kGroupsPerRow), rt = (int)(r & 15);
