@@ -233,7 +233,8 @@ int32_t ckv_arena_export(const uint32_t* codes, const uint32_t* meta, int64_t ro
 
 /* (3) Mixed-precision decode attention (attention.mixed_decode_attention, attention.py:63-90,
  * for every (layer, sequence, kv-head) unit at once).  q fp16 [L][B][H*m][128] (strides
- * q_s_layer, q_s_batch in elements), m = q heads per kv head (1..8).  Online softmax over the
+ * q_s_layer, q_s_batch in elements; out strides o_s_layer, o_s_batch likewise multiples of 8,
+ * out 16-byte aligned), m = q heads per kv head (1..8).  Online softmax over the
  * virtual sequence INT2 || INT4 || FP16 with split-KV; scale = softmax scale (1/sqrt(128)).
  * Output fp16 [L][B][H*m][128].  Workspace: ckv_decode_workspace_bytes() bytes, zero-filled
  * once before first use (it holds self-resetting split arrival counters; the last CTA of

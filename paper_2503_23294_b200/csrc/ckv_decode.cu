@@ -9,20 +9,17 @@
 // last CTA of a unit merges).  fp16 operands, fp32 accumulation.
 //
 // Tile = 16 tokens.  Per warp and tile:
-//   S^T[16 tok x 8 q] = K_tile[16 x 128] . Q^T          mma.m16n8k16 x 8  (+1 for the lo term)
+//   S^T[16 tok x 8 q] = lo.Q + sum_G sigma_G (K_G . Q'_G^T)   mma.m16n8k16: 1 + 2 per group G
 //   P = exp2(S - m) (online, lazy rescale), P^T -> P via movmatrix
-//   O^T[128 d x 8 q] += V_tile^T[128 x 16] . P^T        mma.m16n8k16 x 8  (+1 for the lo term)
-// Quantized tiles stream through a per-warp 4-stage cp.async ring in shared memory (rows
-// permuted inside the tile so every fragment read is bank-conflict free); FP16 tiles (<4% of
-// bytes) are read straight from global memory.  Operands are rebuilt in registers from the
-// reference-format packed words:
-//   fp16 magic: (code << j) | exp(16)  ==  16 + code * 2^(j-6)  exactly, then
-//   v = fma(x, sc, -16 sc) = sc * code * 2^(j-6)  (one rounding, one constant per scale).
-//   The per-slot power-of-two weight 2^(j-6) is folded into q (K side: q' = q 2^(6-j) per
-//   d-slot) and into the output rows (V side: j depends only on the m-tile, undone once at
-//   the end).  The per-(token, group) zero point lo goes through one extra MMA per side
-//   (K: lo x sum_g(q); V: sum_t p_t lo_t).  Units whose scales (or q) are too wide for the
-//   weighted form run an unweighted exact mode (code by subtraction, full affine).
+//   O^T[128 d x 8 q] += V_G^T[32 x 16] . (P x span_G)^T      mma.m16n8k16: 2 per group (+1 lo term)
+// Quantized tiles stream through a per-warp 4-stage cp.async ring in shared memory (tile bytes
+// permuted so every fragment read is one conflict-free shared load); FP16 tiles (<4% of bytes)
+// are read straight from global memory.  The packed codes enter the tensor cores as fp16
+// subnormals (code << j is the fp16 value code * 2^(j-24): one AND per pair of codes, no
+// bias), every 32-element group forms its own k-steps (K) / m-tiles (V), and the group scales
+// are applied per (token, group) instead of per element: on the K side to the group's fp32
+// partial sums, on the V side folded into the P operand.  Per-unit powers of two keep every
+// fp16 operand in range (see "operand scaling").
 #include <math.h>
 
 #include <cuda/atomic>
@@ -71,23 +68,21 @@ struct DecArgs {
   uint16_t* out;
   int64_t o_sl, o_sb;
   float* partial_out;   // [L][B][H*m][130] or null
-  uint32_t zero;        // runtime 0: keeps the fp16 magic exponents in registers (see Magic)
+  int64_t* trace;       // per-CTA timeline buffer (tuning aid) or null
 };
 
 // Optional per-CTA timeline (tuning aid, not part of the ABI): when set, every CTA appends 16
 // int64: globaltimer at start, after the PDL wait, after q staging, after warp 0's tiles, at
 // exit; smid, linear block index, q pointer (launch id); after all warps' tiles, before the
 // arrival atomic, after it, is-last; per-warp tile end times.
-__device__ int64_t* g_trace = nullptr;
 __device__ unsigned long long g_trace_n = 0;
 __device__ __forceinline__ int64_t gtime() {
   int64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Probe points write shared memory and re-read g_trace each time, so nothing of the tracing
-// stays live in registers across the tile loop.
-__device__ __forceinline__ bool tracing() { return *reinterpret_cast<int64_t* volatile*>(&g_trace) != nullptr; }
+// The trace buffer is a kernel parameter (DecArgs::trace, null unless ckv_decode_set_trace
+// armed it): the probe points cost no memory round trip when tracing is off.
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -715,7 +710,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   __shared__ int64_t s_tr[12], s_tend[kDecWarps];
-  if (threadIdx.x == 0 && tracing()) { s_tr[0] = gtime(); s_tr[11] = 0; }
+  if (threadIdx.x == 0 && (a.trace != nullptr)) { s_tr[0] = gtime(); s_tr[11] = 0; }
   // Segment lengths of the quantized arenas are immutable after the build; len_fp grows with
   // decode appends and is read only after the programmatic-dependent-launch wait below.
   // Split of the quantized tiles: every CTA takes the same 1/splits share of the INT2 tiles
@@ -751,7 +746,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[1] = gtime();
 
   // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m).  Every warp loads the
   // same 8 rows and derives the unit's q exponent from max |q|; then warps 0-2 write q-fragment
@@ -764,7 +759,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     stage_q_part(qv, warp < 3 ? warp : 3, us.E, s_q, lane);
   }
   __syncthreads();
-  if (threadIdx.x == 0 && tracing()) s_tr[2] = gtime();
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[2] = gtime();
   QS qs;
   qs.base = (uint32_t)__cvta_generic_to_shared(s_q) + 16 * lane;
   qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_q) + 3 * kQSet + 4 * lane;
@@ -781,10 +776,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   quantized_tiles(cnt2, nloc - cnt2, a, src, lo, ring_l, qs, us, st, warp);
   fp16_tiles(a, qs, st, nloc);
 
-  if (lane == 0 && tracing()) s_tend[warp] = gtime();
+  if (lane == 0 && (a.trace != nullptr)) s_tend[warp] = gtime();
   finish_warp(st, c);
   __syncthreads();  // ring -> merge buffer reuse
-  if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[8] = gtime();
   float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0]);
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
@@ -833,10 +828,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     }
   }
   auto trace_out = [&]() {
-    if (threadIdx.x == 0 && tracing()) {
+    if (threadIdx.x == 0 && (a.trace != nullptr)) {
       s_tr[3] = s_tend[0];
       s_tr[4] = gtime();
-      int64_t* dst = g_trace + 16 * atomicAdd(&g_trace_n, 1ull);
+      int64_t* dst = a.trace + 16 * atomicAdd(&g_trace_n, 1ull);
       for (int i = 0; i < 5; ++i) dst[i] = s_tr[i];
       for (int i = 8; i < 12; ++i) dst[i] = s_tr[i];
       for (int i = 0; i < kDecWarps; ++i) dst[12 + i] = s_tend[i];
@@ -852,7 +847,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   // kernel).  The CTA barrier orders every thread's partial stores before thread 0's
   // device-scope release RMW; the acquiring side sees them after its own barrier.
   __syncthreads();
-  if (threadIdx.x == 0 && tracing()) s_tr[9] = gtime();
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[9] = gtime();
   if (threadIdx.x == 0) {
     cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[((int64_t)l * a.B + b) * a.H + h]);
     const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
@@ -860,7 +855,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     if (s_last) ctr.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
   }
   __syncthreads();
-  if (threadIdx.x == 0 && tracing()) { s_tr[10] = gtime(); s_tr[11] = s_last; }
+  if (threadIdx.x == 0 && (a.trace != nullptr)) { s_tr[10] = gtime(); s_tr[11] = s_last; }
   if (!s_last) { trace_out(); return; }
   // All m x splits partial rows of this unit are contiguous in the workspace: stage them in
   // shared memory with every 16-B copy in flight at once (one L2 round trip), then merge.
@@ -988,7 +983,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   const int cta = blockIdx.x, l = blockIdx.z;
-  if (threadIdx.x == 0 && tracing()) { s_tr[0] = gtime(); s_tr[11] = 0; }
+  if (threadIdx.x == 0 && (a.trace != nullptr)) { s_tr[0] = gtime(); s_tr[11] = 0; }
   const int gw = cta * kWpWarps + warp;
   const int32_t* wunit = w.prefix + w.U + 1;  // unit of every global warp (one load, no search)
   const int u = __ldg(wunit + gw);
@@ -1039,7 +1034,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  if (threadIdx.x == 0 && tracing()) s_tr[1] = gtime();
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[1] = gtime();
 
   // q staging: every unit slot of the CTA needs parts 0-3; the warps share the jobs
   {
@@ -1058,7 +1053,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && tracing()) s_tr[2] = gtime();
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[2] = gtime();
   QS qs;
   qs.base = (uint32_t)__cvta_generic_to_shared(s_qall + slot * kQBytes) + 16 * lane;
   qs.aug_addr = (uint32_t)__cvta_generic_to_shared(s_qall + slot * kQBytes) + 3 * kQSet + 4 * lane;
@@ -1089,7 +1084,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   quantized_tiles(n2t, n4t, a, src, lo, ring_l, qs, us, st, k, np);
   fp16_part();
   finish_warp(st, c);
-  if (lane == 0 && tracing()) s_tend[warp] = gtime();
+  if (lane == 0 && (a.trace != nullptr)) s_tend[warp] = gtime();
   // Park this warp's partial (rows < m) in its own ring region (its copies are all waited:
   // no barrier needed before the stores).  Column of (q row, d): d XOR (row / 2) in its low 2
   // bits — a store instruction writes rows 2c (+1) x d = 32G + 4g + e: 32 distinct banks.
@@ -1115,100 +1110,158 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0 && tracing()) s_tr[8] = gtime();
-  // in-CTA merge, one pass: thread item (slot, q row, d) -> the slot's running max over its
-  // warps, then the weighted acc and l sums.  A unit entirely inside this CTA writes its output,
-  // otherwise this CTA's partial goes to its slot of the unit's workspace.
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[8] = gtime();
+  // Split units: every CTA of the unit draws an arrival ticket now (tiles done); the one with the
+  // last ticket merges.  It keeps its own partial in shared memory and waits only for CTAs that
+  // have already arrived (no co-residency assumption); the others publish their partial and
+  // signal.  Counters per (layer, unit): [0] tickets, [1] published partials; the merger resets
+  // both.  The ticket's round trip overlaps the in-CTA merge below.
+  uint32_t* ctr_l = a.counters + 2 * (int64_t)l * w.U;
+  const int tick_t = blockDim.x - 1 - threadIdx.x;  // the last threads draw the tickets
+  int ticket = -1;
+  if (tick_t < nslots) {
+    const int4 si = s_slot[tick_t];
+    if (si.z != si.w) ticket = (int)atomicAdd(ctr_l + 2 * (u0 + tick_t), 1u);  // consumed after the merge
+  }
+  // in-CTA merge, one warp per merged row (slot, q row): lanes 0-15 read the slot's warps'
+  // (m, l) and form the weights 2^(m_w - max); every lane then sums 4 columns d = 4 lane + k
+  // over the slot's warps (one 128-bit shared load per warp: the parking swizzle only permutes
+  // inside aligned groups of 4).  A unit entirely inside this CTA writes its output row, otherwise
+  // this CTA's partial goes to shared memory (slot sl: ring region of warp sl, past the parked
+  // warp partials; rows of kWsStride floats: acc, m, l).
   const int Hq = a.H * a.m;
   float* ws_l = a.ws + (int64_t)l * w.U * w.max_ctas * a.m * kWsStride;
-  for (int p = threadIdx.x; p < nslots * a.m * kHeadDim; p += blockDim.x) {
-    const int d = p & (kHeadDim - 1), rt = s_rtab[p >> 7];
-    const int sl = rt >> 8, qi = rt & 255;
+  auto s_own = [&](int sl) { return reinterpret_cast<float*>(&s_ring[sl][8 * kHeadDim * 4]); };
+  for (int r = warp; r < nslots * a.m; r += kWpWarps) {
+    const int rt = s_rtab[r], sl = rt >> 8, qi = rt & 255;
     const int4 si = s_slot[sl];
-    float ms = -INFINITY;
-    for (int ww = si.x; ww < si.y; ++ww) ms = fmaxf(ms, s_ml[ww][qi][0]);
-    const int dq = qi * kHeadDim + swz(qi, d);
-    float acc0 = 0.f, acc1 = 0.f, lsum = 0.f;
+    const bool mine = lane >= si.x && lane < si.y;  // lane v <-> the CTA's warp v
+    const float mw = mine ? s_ml[lane & (kWpWarps - 1)][qi][0] : -INFINITY;
+    float ms = mw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+    const float f = mine && mw != -INFINITY ? fast_exp2(mw - ms) : 0.f;
+    float lsum = mine ? f * s_ml[lane & (kWpWarps - 1)][qi][1] : 0.f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    float ac[4] = {0.f, 0.f, 0.f, 0.f};
+    const uint32_t col = (uint32_t)__cvta_generic_to_shared(&s_ring[0][0]) + (qi * kHeadDim + 4 * lane) * 4;
     for (int ww = si.x; ww < si.y; ++ww) {
-      const float mw = s_ml[ww][qi][0];
-      const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-      const float x = reinterpret_cast<const float*>(&s_ring[ww][0])[dq];
-      if (ww & 1) acc1 = fmaf(f, x, acc1);
-      else acc0 = fmaf(f, x, acc0);
-      lsum = fmaf(f, s_ml[ww][qi][1], lsum);
+      const float fw = __shfl_sync(0xffffffffu, f, ww);
+      const uint4 x = lds128(col + ww * kWarpRing);
+      ac[0] = fmaf(fw, __uint_as_float(x.x), ac[0]);
+      ac[1] = fmaf(fw, __uint_as_float(x.y), ac[1]);
+      ac[2] = fmaf(fw, __uint_as_float(x.z), ac[2]);
+      ac[3] = fmaf(fw, __uint_as_float(x.w), ac[3]);
     }
-    const float acc = acc0 + acc1;
-    const int us = u0 + sl, bs = us / a.H, hs = us - bs * a.H;
+    // stored column 4 lane + k holds d = 4 lane + (k ^ sw)
+    const int sw = (qi >> 1) & 3;
+    float o4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o4[k] = ac[k ^ sw];
     if (si.z == si.w) {
+      const int us = u0 + sl, bs = us / a.H, hs = us - bs * a.H;
       const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
       if (a.partial_out) {
         float* dst = a.partial_out + row * kPartStride;
-        dst[d] = acc;
-        if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst[4 * lane + k] = o4[k];
+        if (lane == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
       } else {
-        a.out[l * a.o_sl + bs * a.o_sb + (int64_t)(hs * a.m + qi) * kHeadDim + d] =
-            __half_as_ushort(__float2half_rn(acc / lsum));
+        const __half2 h0 = __floats2half2_rn(o4[0] / lsum, o4[1] / lsum), h1 = __floats2half2_rn(o4[2] / lsum, o4[3] / lsum);
+        *reinterpret_cast<uint2*>(a.out + l * a.o_sl + bs * a.o_sb + (int64_t)(hs * a.m + qi) * kHeadDim + 4 * lane) =
+            make_uint2(h2_as_u32(h0), h2_as_u32(h1));
       }
     } else {
-      float* dst = ws_l + (((int64_t)us * w.max_ctas + (cta - si.z)) * a.m + qi) * kWsStride;
-      dst[d] = acc;
-      if (d == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+      float* dst = s_own(sl) + qi * kWsStride;
+      *reinterpret_cast<float4*>(dst + 4 * lane) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+      if (lane == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
     }
   }
+  if (tick_t < nslots) s_lastu[tick_t] = ticket;
   __syncthreads();
-  if (threadIdx.x == 0 && tracing()) s_tr[9] = gtime();
-  // arrival per split unit: the CTA that completes a unit's set of partials merges them.  The
-  // barrier above orders every thread's partial stores before the device-scope release RMW.
-  if ((int)threadIdx.x < nslots) {
-    const int4 si = s_slot[threadIdx.x];
-    int last = 0;
-    if (si.z != si.w) {
-      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> ctr(a.counters[(int64_t)l * w.U + u0 + threadIdx.x]);
-      const uint32_t prev = ctr.fetch_add(1u, cuda::memory_order_acq_rel);
-      last = prev == (uint32_t)(si.w - si.z);
-      if (last) ctr.store(0u, cuda::memory_order_relaxed);
-    }
-    s_lastu[threadIdx.x] = last;
+  if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[9] = gtime();
+  // publish: split slots whose ticket is not the unit's last
+  bool any_pub = false, any_last = false;
+  for (int sl = 0; sl < nslots; ++sl) {
+    const int4 si = s_slot[sl];
+    const int tk = s_lastu[sl];
+    if (tk < 0) continue;
+    if (tk == si.w - si.z) { any_last = true; continue; }
+    any_pub = true;
+    float* dst = ws_l + ((int64_t)(u0 + sl) * w.max_ctas + (cta - si.z)) * a.m * kWsStride;
+    for (int i = threadIdx.x; i < a.m * kWsStride; i += blockDim.x) __stcg(dst + i, s_own(sl)[i]);
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && tracing()) {
+  if (any_pub) {
+    __syncthreads();  // orders every thread's partial stores before the device-scope release
+    if ((int)threadIdx.x < nslots) {
+      const int4 si = s_slot[threadIdx.x];
+      const int tk = s_lastu[threadIdx.x];
+      if (tk >= 0 && tk != si.w - si.z) {
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> done(ctr_l[2 * (u0 + threadIdx.x) + 1]);
+        done.fetch_add(1u, cuda::memory_order_release);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && (a.trace != nullptr)) {
     s_tr[10] = gtime();
     int nl = 0;
-    for (int i = 0; i < nslots; ++i) nl += s_lastu[i];
+    for (int i = 0; i < nslots; ++i) nl += s_lastu[i] >= 0 && s_lastu[i] == s_slot[i].w - s_slot[i].z;
     s_tr[11] = nl;
   }
-  // units this CTA completes, one at a time: stage the unit's partials (every CTA's rows, one L2
-  // round trip) in shared memory (the ring) when they fit, then merge per (q row, d)
-  float* s_part = reinterpret_cast<float*>(&s_ring[0][0]);
-  for (int sl = 0; sl < nslots; ++sl) {
-    if (!s_lastu[sl]) continue;
-    const int us = u0 + sl;
+  // units this CTA completes: wait for the other CTAs' published partials (they arrived before
+  // this CTA's ticket, so they are running or done), then merge per (q row, d) with its own
+  for (int sl = 0; any_last && sl < nslots; ++sl) {
     const int4 si = s_slot[sl];
+    if (s_lastu[sl] != si.w - si.z) continue;
+    const int us = u0 + sl;
     const int nc = si.w - si.z + 1;
+    if (threadIdx.x == 0) {
+      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> done(ctr_l[2 * us + 1]);
+      while (done.load(cuda::memory_order_acquire) != (uint32_t)(nc - 1)) __nanosleep(32);
+      done.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
+      ctr_l[2 * us] = 0u;
+    }
+    __syncthreads();
     const int bs = us / a.H, hs = us - bs * a.H;
     const float* src_p = ws_l + (int64_t)us * w.max_ctas * a.m * kWsStride;  // [ctas][m][stride]
-    const bool staged = nc * a.m * kWsStride * (int)sizeof(float) <= kWpWarps * kWarpRing;
-    if (staged) {
-      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_part);
-      const int nvec = nc * a.m * kWsStride / 4;
-      for (int i = threadIdx.x; i < nvec; i += blockDim.x) cp_async16(sbase + 16 * i, src_p + 4 * i);
-      cp_commit();
-      cp_wait<0>();
-      __syncthreads();
-    }
-    const float* pbase = staged ? s_part : src_p;
     for (int p = threadIdx.x; p < a.m * kHeadDim; p += blockDim.x) {
       const int qi = p >> 7, d = p & (kHeadDim - 1);
-      const float* pp = pbase + qi * kWsStride;
+      const float* own = s_own(sl) + qi * kWsStride;
+      // every CTA's (m, acc, l) in CTA order (the merger's own from shared memory; the sum order
+      // does not depend on which CTA arrived last): one L2 round trip
+      constexpr int kMaxParts = 8;
+      float mv[kMaxParts], xv[kMaxParts], lv[kMaxParts];
+      const int np0 = min(nc, kMaxParts);
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxParts; ++s2) {
+        if (s2 >= np0) break;
+        const float* ps = si.z + s2 == cta ? own : src_p + (s2 * a.m + qi) * kWsStride;
+        mv[s2] = si.z + s2 == cta ? ps[kHeadDim] : __ldcg(ps + kHeadDim);
+        xv[s2] = si.z + s2 == cta ? ps[d] : __ldcg(ps + d);
+        lv[s2] = si.z + s2 == cta ? ps[kHeadDim + 1] : __ldcg(ps + kHeadDim + 1);
+      }
       float ms = -INFINITY;
-      for (int s2 = 0; s2 < nc; ++s2) ms = fmaxf(ms, pp[s2 * a.m * kWsStride + kHeadDim]);
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxParts; ++s2)
+        if (s2 < np0) ms = fmaxf(ms, mv[s2]);
       float acc = 0.f, lsum = 0.f;
-      for (int s2 = 0; s2 < nc; ++s2) {
-        const float* ps = pp + s2 * a.m * kWsStride;
-        const float mw = ps[kHeadDim];
-        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-        acc = fmaf(f, ps[d], acc);
-        lsum = fmaf(f, ps[kHeadDim + 1], lsum);
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxParts; ++s2) {
+        if (s2 >= np0) break;
+        const float f = mv[s2] == -INFINITY ? 0.f : fast_exp2(mv[s2] - ms);
+        acc = fmaf(f, xv[s2], acc);
+        lsum = fmaf(f, lv[s2], lsum);
+      }
+      for (int s2 = kMaxParts; s2 < nc; ++s2) {  // units over more than 8 CTAs: the rest streamed
+        const float* ps = si.z + s2 == cta ? own : src_p + (s2 * a.m + qi) * kWsStride;
+        const float mw = si.z + s2 == cta ? ps[kHeadDim] : __ldcg(ps + kHeadDim);
+        const float mn = fmaxf(ms, mw);
+        const float fo = ms == -INFINITY ? 0.f : fast_exp2(ms - mn);
+        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - mn);
+        acc = fmaf(f, si.z + s2 == cta ? ps[d] : __ldcg(ps + d), acc * fo);
+        lsum = fmaf(f, si.z + s2 == cta ? ps[kHeadDim + 1] : __ldcg(ps + kHeadDim + 1), lsum * fo);
+        ms = mn;
       }
       const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
       if (a.partial_out) {
@@ -1220,14 +1273,13 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
             __half_as_ushort(__float2half_rn(acc / lsum));
       }
     }
-    __syncthreads();  // s_part reuse by the next unit
   }
-  if (threadIdx.x == 0 && tracing()) {
+  if (threadIdx.x == 0 && (a.trace != nullptr)) {
     int64_t tmax = 0;
     for (int i = 0; i < kWpWarps; ++i) tmax = max(tmax, s_tend[i]);
     s_tr[3] = tmax;
     s_tr[4] = gtime();
-    int64_t* dst = g_trace + 16 * atomicAdd(&g_trace_n, 1ull);
+    int64_t* dst = a.trace + 16 * atomicAdd(&g_trace_n, 1ull);
     for (int i = 0; i < 5; ++i) dst[i] = s_tr[i];
     for (int i = 8; i < 12; ++i) dst[i] = s_tr[i];
     for (int i = 0; i < 4; ++i) dst[12 + i] = s_tend[i * 5];
@@ -1257,6 +1309,8 @@ __global__ void lse_merge_kernel(const float* __restrict__ parts, int P, int64_t
 }  // namespace ckv
 
 using namespace ckv;
+
+static int64_t* g_trace_host = nullptr;  // ckv_decode_set_trace: copied into every launch's DecArgs
 
 static bool ensure_decode_attr() {
   static bool attr_set = false;
@@ -1302,7 +1356,8 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
   if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (!q || !seq || (!out && !partial_out)) return CKV_ERR_ARG;
   if (splits > 1 && !workspace) return CKV_ERR_ARG;
-  if ((q_s_layer % 8) || (q_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
+  if ((q_s_layer % 8) || (q_s_batch % 8) || (o_s_layer % 8) || (o_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
+  if (out && (reinterpret_cast<uintptr_t>(out) & 15)) return CKV_ERR_UNSUPPORTED;
   if (layers * seq_count * kv_heads == 0) return CKV_OK;
   {  // interleaved K/V tile buffers (include/ckv.h)
     const char* k2 = reinterpret_cast<const char*>(k_arena.codes2);
@@ -1331,7 +1386,7 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
                    : nullptr;
   a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
   a.partial_out = partial_out;
-  a.zero = 0u;
+  a.trace = g_trace_host;
   if (!ensure_decode_attr()) return CKV_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * seq_count));
@@ -1364,8 +1419,8 @@ int32_t ckv_decode_ctas_per_sm(void) {
 // reset its counter.
 int32_t ckv_decode_set_trace(int64_t* buf) {
   unsigned long long z = 0;
-  if (cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)) != cudaSuccess ||
-      cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z)) != cudaSuccess) {
+  g_trace_host = buf;
+  if (cudaMemcpyToSymbol(g_trace_n, &z, sizeof(z)) != cudaSuccess) {
     (void)cudaGetLastError();
     return CKV_ERR_CUDA;
   }
@@ -1379,7 +1434,7 @@ int32_t ckv_decode_wp_cta_warps(void) { return kWpWarps; }
 int64_t ckv_decode_wp_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                                       int32_t max_ctas) {
   const int64_t units = (int64_t)layers * batch * kv_heads;
-  return cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256 +
+  return cdiv(2 * units * (int64_t)sizeof(uint32_t), 256) * 256 +
          units * (int64_t)(max_ctas > 0 ? max_ctas : 1) * m * kWsStride * (int64_t)sizeof(float);
 }
 
@@ -1393,7 +1448,8 @@ int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_
   if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (max_slots < 1 || max_slots > 8 || max_ctas < 1) return CKV_ERR_UNSUPPORTED;
   if (!q || !seq || !warp_prefix || !workspace || (!out && !partial_out)) return CKV_ERR_ARG;
-  if ((q_s_layer % 8) || (q_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
+  if ((q_s_layer % 8) || (q_s_batch % 8) || (o_s_layer % 8) || (o_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
+  if (out && (reinterpret_cast<uintptr_t>(out) & 15)) return CKV_ERR_UNSUPPORTED;
   if (layers * batch * kv_heads == 0) return CKV_OK;
   {
     const char* k2 = reinterpret_cast<const char*>(k_arena.codes2);
@@ -1418,10 +1474,10 @@ int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_
   a.scale_log2 = scale * 1.4426950408889634f;
   const int64_t units = (int64_t)layers * batch * kv_heads;
   a.counters = reinterpret_cast<uint32_t*>(workspace);
-  a.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + cdiv(units * (int64_t)sizeof(uint32_t), 256) * 256);
+  a.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + cdiv(2 * units * (int64_t)sizeof(uint32_t), 256) * 256);
   a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
   a.partial_out = partial_out;
-  a.zero = 0u;
+  a.trace = g_trace_host;
   w.prefix = warp_prefix;
   w.U = batch * kv_heads;
   w.max_slots = max_slots;

@@ -65,6 +65,18 @@ def main():
     te = np.array([[rel(v) for v in t[t[:, 7] == p, 3]] for p in launches[1:-1]], dtype=object)
     spans = [max(x) - min(x) for x in te]
     print("per layer: last - first CTA tiles_end, median %.1f us" % np.median(spans))
+    # release: earliest post-wait time of layer i+1 minus the last exit of layer i; late
+    # starters: post-wait minus start of the 10% latest-starting CTAs
+    rel_lat, late = [], []
+    for i in range(1, len(launches) - 1):
+        x, px = t[t[:, 7] == launches[i]], t[t[:, 7] == launches[i - 1]]
+        rel_lat.append((x[:, 1].min() - px[:, 4].max()) / 1e3)
+        k = max(1, len(x) // 10)
+        idx = np.argsort(x[:, 0])[-k:]
+        late.append(np.median(x[idx, 1] - x[idx, 0]) / 1e3)
+    print("PDL release after the previous layer's last exit, median %.1f us; late starters start->wait %.1f us"
+          % (np.median(rel_lat), np.median(late)))
+    print("q staging (wait -> staged) per CTA p50 %.1f max %.1f us" % tuple(np.percentile((t[:, 2] - t[:, 1]) / 1e3, [50, 100])))
 
 
 if __name__ == "__main__":
