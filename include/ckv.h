@@ -269,20 +269,27 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
                                   float* partial_out, int32_t flags, void* stream);
 
 /* Warp-plan schedule of the same computation (whole-batch launches): unit u = b * kv_heads + h
- * of every layer takes n_u warps, warp_prefix i32[B*H + 1] their exclusive prefix sum (device
- * memory; the total 16 * ctas); CTA c (16 warps, one per SM) runs warps [16c, 16c + 16).
- * max_slots = the most units one CTA spans (<= 8), max_ctas = the most CTAs one unit spans.
- * Warp k of unit u takes the unit's tiles k, k + n_u, ... of each kind; a unit split over
- * several CTAs is merged by the last to arrive.  Workspace: ckv_decode_wp_workspace_bytes(),
- * zero-filled once.  Outputs as ckv_decode_attention (out or partial_out). */
+ * of every layer takes unit_warps[u] >= 1 warps (their sum = 16 * ctas); CTA c (16 warps, one
+ * per SM) runs warps [16c, 16c + 16).  ckv_decode_wp_plan builds, on the host from the host
+ * copy of the seq table, the plan table the kernel reads (ckv_decode_wp_plan_ints(ctas) int32:
+ * per-warp tile ranges, per-CTA unit slots; upload it to device memory) and returns max_slots
+ * (the most units one CTA spans, <= 8; CKV_ERR_UNSUPPORTED above) and max_ctas (the most CTAs
+ * one unit spans).  A warp's part of unit u is a contiguous share of the unit's tiles of each
+ * kind; a unit split over several CTAs is merged by the CTA with the last arrival ticket.
+ * Workspace: ckv_decode_wp_workspace_bytes(), zero-filled once.  Outputs as
+ * ckv_decode_attention (out or partial_out). */
 int64_t ckv_decode_wp_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
                                       int32_t max_ctas);
 /* Warps per CTA of the warp-plan kernel (16: one CTA per SM). */
 int32_t ckv_decode_wp_cta_warps(void);
+int64_t ckv_decode_wp_plan_ints(int32_t ctas);
+int32_t ckv_decode_wp_plan(const int32_t* seq_host, int32_t batch, int32_t kv_heads,
+                           const int32_t* unit_warps, int32_t ctas, int32_t* plan_host,
+                           int32_t* max_slots, int32_t* max_ctas);
 int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
                                 ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
                                 int32_t layers, int32_t batch, int32_t kv_heads, int32_t m, float scale,
-                                const int32_t* warp_prefix, int32_t ctas, int32_t max_slots,
+                                const int32_t* plan, int32_t ctas, int32_t max_slots,
                                 int32_t max_ctas, void* workspace, uint16_t* out, int64_t o_s_layer,
                                 int64_t o_s_batch, float* partial_out, int32_t flags, void* stream);
 

@@ -24,6 +24,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -198,10 +200,11 @@ class BatchedKVCache:
     def warp_plan(self):
         """Warp-plan schedule (ckv_decode_attention_wp): unit u = b*H + h gets n_u warps in
         proportion to its tile cost (INT2 1, INT4 1.06, FP16-region 2 per 16-token tile), at
-        least 2, summing to 16 x the SM count; returns (prefix i32 [B*H + 1] on the device, ctas,
+        least 2, summing to 16 x the SM count; returns (plan table i32 on the device, ctas,
         max_slots, max_ctas) or None when the units do not fit (more than 8 per CTA).  Computed
-        once: any plan is exact, later appends only shift the balance slightly.  The device table
-        holds the prefix, then the unit of every global warp."""
+        once: any plan is exact, later appends only shift the balance slightly.  The table
+        (ckv_decode_wp_plan, include/ckv.h) holds every warp's tile ranges and every CTA's unit
+        slots, so a CTA's prologue needs no dependent loads."""
         if self._wp is None:
             self._wp = False
             cw = _lib.load().ckv_decode_wp_cta_warps()  # warps per CTA (16 / cw CTAs per SM)
@@ -223,17 +226,15 @@ class BatchedKVCache:
                 while n.sum() > T:
                     j = int(np.argmax(np.where(n > 2, n - raw, -np.inf)))
                     n[j] -= 1
-                prefix = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
-                first, last = prefix[:-1] // cw, (prefix[1:] - 1) // cw
-                max_ctas = int((last - first + 1).max())
-                starts = np.arange(n_cta) * cw
-                u_lo = np.searchsorted(prefix, starts, side="right") - 1
-                u_hi = np.searchsorted(prefix, starts + cw - 1, side="right") - 1
-                max_slots = int((u_hi - u_lo + 1).max())
-                if max_slots <= 8:
-                    wunit = np.repeat(np.arange(U), n)  # unit of every global warp
-                    table = np.concatenate([prefix, wunit]).astype(np.int32)
-                    self._wp = (torch.from_numpy(table).to(self.device), n_cta, max_slots, max_ctas)
+                lib = _lib.load()
+                plan = np.zeros(int(lib.ckv_decode_wp_plan_ints(n_cta)), dtype=np.int32)
+                seq = np.ascontiguousarray(self.seq_host, dtype=np.int32)
+                nw = np.ascontiguousarray(n, dtype=np.int32)
+                ms, mc = ctypes.c_int32(0), ctypes.c_int32(0)
+                st = lib.ckv_decode_wp_plan(seq.ctypes.data, self.B, self.H, nw.ctypes.data, n_cta,
+                                            plan.ctypes.data, ctypes.byref(ms), ctypes.byref(mc))
+                if st == 0:
+                    self._wp = (torch.from_numpy(plan).to(self.device), n_cta, ms.value, mc.value)
         return self._wp or None
 
     def _wp_workspace(self, m, layers, layer, max_ctas):

@@ -23,6 +23,8 @@
 #include <math.h>
 
 #include <cuda/atomic>
+#include <algorithm>
+#include <vector>
 #include <type_traits>
 
 #include "ckv_common.cuh"
@@ -950,10 +952,18 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
 #endif
 constexpr int kWpWarps = CKV_WP_WARPS;  // warps per CTA; 16 / kWpWarps CTAs per SM
 
+// Plan table (ckv_decode_wp_plan, device memory), int32:
+//   warp records [16 * ctas][8]: unit u, k | np << 16 (the warp's index in its CTA's part of
+//     the unit, the part's warps), INT2 / INT4 tiles of the warp's part, first INT2 / INT4 row
+//     of the part in the unit's segment (seq off + tile share), w_lo | w_hi << 16 (the part's
+//     warps within the unit's nw), nw;
+//   CTA records [ctas][4]: first unit u0, unit slots;
+//   slot records [ctas][8][4]: the slot unit's warps [x, y) within the CTA, first / last CTA.
+// Every CTA reads its records with independent loads (no dependent chain before its prologue).
+constexpr int kPlanWarpInts = 8, kPlanCtaInts = 4, kPlanSlots = 8;
 struct WpArgs {
   DecArgs d;
-  const int32_t* prefix;  // [U + 1] first global warp of each unit (U = B * H per layer),
-                          // then [16 * ctas] the unit of every global warp
+  const int32_t* plan;
   int U;
   int max_slots;          // most units any CTA spans (q staging slots)
   int max_ctas;           // most CTAs any unit spans (partial slots per unit)
@@ -985,28 +995,23 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   const int cta = blockIdx.x, l = blockIdx.z;
   if (threadIdx.x == 0 && (a.trace != nullptr)) { s_tr[0] = gtime(); s_tr[11] = 0; }
   const int gw = cta * kWpWarps + warp;
-  const int32_t* wunit = w.prefix + w.U + 1;  // unit of every global warp (one load, no search)
-  const int u = __ldg(wunit + gw);
-  const int u0 = __ldg(wunit + cta * kWpWarps);
-  const int p0 = __ldg(w.prefix + u), p1 = __ldg(w.prefix + u + 1);
-  const int nw = p1 - p0;  // the unit's warps
-  // this CTA's part of the unit: its warps [w_lo, w_hi) of the unit take a contiguous share of
-  // each tile kind (adjacent tiles on one SM, as the 4-warp kernel's CTAs), interleaved inside
-  const int w_lo = max(p0, cta * kWpWarps) - p0, w_hi = min(p1, cta * kWpWarps + kWpWarps) - p0;
-  const int k = gw - p0 - w_lo, np = w_hi - w_lo;  // this warp's index among the part's np warps
+  const int nctas = gridDim.x;
+  const int4* wrec = reinterpret_cast<const int4*>(w.plan) + 2 * gw;
+  const int4 r0 = __ldg(wrec), r1 = __ldg(wrec + 1);
+  const int4 crec = __ldg(reinterpret_cast<const int4*>(w.plan + kPlanWarpInts * kWpWarps * nctas) + cta);
+  const int u = r0.x, u0 = crec.x, nslots = crec.y;
+  // this CTA's part of the unit: its warps [w_lo, w_hi) of the unit's nw take a contiguous share
+  // of each tile kind (adjacent tiles on one SM), interleaved inside
+  const int k = r0.y & 0xffff, np = r0.y >> 16;  // this warp's index among the part's np warps
+  const int w_lo = r1.z & 0xffff, w_hi = r1.z >> 16, nw = r1.w;
   const int slot = u - u0;
-  const int b = u / a.H, h = u % a.H;
-  int n2t, n4t;
+  const int b = u / a.H, h = u - b * a.H;
+  const int n2t = r0.z, n4t = r0.w;
   TileSrc src;
   {
-    const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * b];
-    const int n2u = s0.y / kTile, n4u = s0.w / kTile;
-    const int a2 = (int)((int64_t)n2u * w_lo / nw), a4 = (int)((int64_t)n4u * w_lo / nw);
-    n2t = (int)((int64_t)n2u * w_hi / nw) - a2;
-    n4t = (int)((int64_t)n4u * w_hi / nw) - a4;
     const int64_t unit = (int64_t)l * a.H + h;
-    src.c2 = (unit * a.K.rows2 + s0.x + (int64_t)a2 * kTile) / kTileRows * kBlock2 + 16 * lane;
-    src.c4 = (unit * a.K.rows4 + s0.z + (int64_t)a4 * kTile) / kTileRows * kBlock4 + 16 * lane;
+    src.c2 = (unit * a.K.rows2 + r1.x) / kTileRows * kBlock2 + 16 * lane;
+    src.c4 = (unit * a.K.rows4 + r1.y) / kTileRows * kBlock4 + 16 * lane;
   }
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0]) + 16 * lane;
   if (n2t > 0) prologue<2>(n2t, a, src, ring_l, k, np);
@@ -1014,15 +1019,9 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   UnitScale us;
   us.F = unit_v_exponent(a, l, b, h);
   // per-slot facts for the merge (build-time plan data: before the wait)
-  const int u_last = __ldg(wunit + cta * kWpWarps + kWpWarps - 1);
-  const int nslots = u_last - u0 + 1;
-  if ((int)threadIdx.x < nslots) {
-    const int us = u0 + threadIdx.x;
-    const int q0 = __ldg(w.prefix + us), q1 = __ldg(w.prefix + us + 1);
-    s_slot[threadIdx.x] = make_int4(max(q0, cta * kWpWarps) - cta * kWpWarps,
-                                    min(q1, cta * kWpWarps + kWpWarps) - cta * kWpWarps, q0 / kWpWarps,
-                                    (q1 - 1) / kWpWarps);
-  }
+  if ((int)threadIdx.x < nslots)
+    s_slot[threadIdx.x] = __ldg(reinterpret_cast<const int4*>(w.plan + (kPlanWarpInts * kWpWarps + kPlanCtaInts) * nctas) +
+                                kPlanSlots * cta + threadIdx.x);
   if ((int)threadIdx.x < nslots * a.m)
     s_rtab[threadIdx.x] = (unsigned short)(((threadIdx.x / a.m) << 8) | (threadIdx.x % a.m));
   // pull this warp's q rows into L2 while the previous launch drains (L2 is the point of
@@ -1111,17 +1110,18 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   }
   __syncthreads();
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[8] = gtime();
-  // Split units: every CTA of the unit draws an arrival ticket now (tiles done); the one with the
-  // last ticket merges.  It keeps its own partial in shared memory and waits only for CTAs that
-  // have already arrived (no co-residency assumption); the others publish their partial and
-  // signal.  Counters per (layer, unit): [0] tickets, [1] published partials; the merger resets
-  // both.  The ticket's round trip overlaps the in-CTA merge below.
+  // Split units: every CTA of the unit draws an arrival ticket now (its tiles are done); the one
+  // with the last ticket merges the unit.  It keeps its own partial in shared memory and waits
+  // only for CTAs that drew earlier tickets, i.e. that are running or done (no co-residency
+  // assumption); the others publish their partial and signal.  Counters per (layer, unit):
+  // [0] tickets, [1] published partials; the merger resets both.  The tickets' round trip
+  // overlaps the in-CTA merge (stored just before its barrier).
   uint32_t* ctr_l = a.counters + 2 * (int64_t)l * w.U;
   const int tick_t = blockDim.x - 1 - threadIdx.x;  // the last threads draw the tickets
   int ticket = -1;
   if (tick_t < nslots) {
     const int4 si = s_slot[tick_t];
-    if (si.z != si.w) ticket = (int)atomicAdd(ctr_l + 2 * (u0 + tick_t), 1u);  // consumed after the merge
+    if (si.z != si.w) ticket = (int)atomicAdd(ctr_l + 2 * (u0 + tick_t), 1u);
   }
   // in-CTA merge, one warp per merged row (slot, q row): lanes 0-15 read the slot's warps'
   // (m, l) and form the weights 2^(m_w - max); every lane then sums 4 columns d = 4 lane + k
@@ -1438,16 +1438,80 @@ int64_t ckv_decode_wp_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_
          units * (int64_t)(max_ctas > 0 ? max_ctas : 1) * m * kWsStride * (int64_t)sizeof(float);
 }
 
+int64_t ckv_decode_wp_plan_ints(int32_t ctas) {
+  return ctas < 1 ? 0 : (int64_t)ctas * (kPlanWarpInts * kWpWarps + kPlanCtaInts + 4 * kPlanSlots);
+}
+
+int32_t ckv_decode_wp_plan(const int32_t* seq_host, int32_t batch, int32_t kv_heads,
+                           const int32_t* unit_warps, int32_t ctas, int32_t* plan_host,
+                           int32_t* max_slots, int32_t* max_ctas) {
+  if (!seq_host || !unit_warps || !plan_host || !max_slots || !max_ctas) return CKV_ERR_ARG;
+  if (batch < 1 || kv_heads < 1 || ctas < 1) return CKV_ERR_ARG;
+  const int U = batch * kv_heads, T = kWpWarps * ctas;
+  int64_t total = 0;
+  for (int u = 0; u < U; ++u) {
+    if (unit_warps[u] < 1) return CKV_ERR_ARG;
+    total += unit_warps[u];
+  }
+  if (total != T || U > T) return CKV_ERR_ARG;
+  std::vector<int> prefix(U + 1, 0), wunit(T);
+  for (int u = 0; u < U; ++u) prefix[u + 1] = prefix[u] + unit_warps[u];
+  for (int u = 0; u < U; ++u)
+    for (int x = prefix[u]; x < prefix[u + 1]; ++x) wunit[x] = u;
+  int32_t* wr = plan_host;
+  int32_t* cr = plan_host + (int64_t)kPlanWarpInts * T;
+  int32_t* sr = cr + (int64_t)kPlanCtaInts * ctas;
+  std::fill(plan_host, plan_host + ckv_decode_wp_plan_ints(ctas), 0);
+  int ms = 0, mc = 0;
+  for (int u = 0; u < U; ++u) mc = std::max(mc, (prefix[u + 1] - 1) / kWpWarps - prefix[u] / kWpWarps + 1);
+  for (int c = 0; c < ctas; ++c) {
+    const int u0 = wunit[c * kWpWarps], u1 = wunit[c * kWpWarps + kWpWarps - 1];
+    const int ns = u1 - u0 + 1;
+    if (ns > kPlanSlots) return CKV_ERR_UNSUPPORTED;
+    ms = std::max(ms, ns);
+    cr[kPlanCtaInts * c] = u0;
+    cr[kPlanCtaInts * c + 1] = ns;
+    for (int sl = 0; sl < ns; ++sl) {
+      const int us = u0 + sl, q0 = prefix[us], q1 = prefix[us + 1];
+      int32_t* x = sr + 4 * (kPlanSlots * c + sl);
+      x[0] = std::max(q0, c * kWpWarps) - c * kWpWarps;
+      x[1] = std::min(q1, c * kWpWarps + kWpWarps) - c * kWpWarps;
+      x[2] = q0 / kWpWarps;
+      x[3] = (q1 - 1) / kWpWarps;
+    }
+  }
+  for (int gw = 0; gw < T; ++gw) {
+    const int u = wunit[gw], c = gw / kWpWarps, b = u / kv_heads;
+    const int p0 = prefix[u], p1 = prefix[u + 1], nw = p1 - p0;
+    const int w_lo = std::max(p0, c * kWpWarps) - p0, w_hi = std::min(p1, c * kWpWarps + kWpWarps) - p0;
+    const int32_t* s0 = seq_host + CKV_SEQ_FIELDS * b;
+    const int64_t n2u = s0[1] / kTile, n4u = s0[3] / kTile;
+    const int a2 = (int)(n2u * w_lo / nw), a4 = (int)(n4u * w_lo / nw);
+    int32_t* x = wr + kPlanWarpInts * gw;
+    x[0] = u;
+    x[1] = (gw - p0 - w_lo) | ((w_hi - w_lo) << 16);
+    x[2] = (int)(n2u * w_hi / nw) - a2;
+    x[3] = (int)(n4u * w_hi / nw) - a4;
+    x[4] = s0[0] + a2 * kTile;
+    x[5] = s0[2] + a4 * kTile;
+    x[6] = w_lo | (w_hi << 16);
+    x[7] = nw;
+  }
+  *max_slots = ms;
+  *max_ctas = mc;
+  return CKV_OK;
+}
+
 int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
                                 ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
                                 int32_t layers, int32_t batch, int32_t kv_heads, int32_t m, float scale,
-                                const int32_t* warp_prefix, int32_t ctas, int32_t max_slots,
+                                const int32_t* plan, int32_t ctas, int32_t max_slots,
                                 int32_t max_ctas, void* workspace, uint16_t* out, int64_t o_s_layer,
                                 int64_t o_s_batch, float* partial_out, int32_t flags, void* stream) {
   if (layers < 0 || batch < 0 || kv_heads < 0 || ctas < 1) return CKV_ERR_ARG;
   if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (max_slots < 1 || max_slots > 8 || max_ctas < 1) return CKV_ERR_UNSUPPORTED;
-  if (!q || !seq || !warp_prefix || !workspace || (!out && !partial_out)) return CKV_ERR_ARG;
+  if (!q || !seq || !plan || !workspace || (!out && !partial_out)) return CKV_ERR_ARG;
   if ((q_s_layer % 8) || (q_s_batch % 8) || (o_s_layer % 8) || (o_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
   if (out && (reinterpret_cast<uintptr_t>(out) & 15)) return CKV_ERR_UNSUPPORTED;
   if (layers * batch * kv_heads == 0) return CKV_OK;
@@ -1478,7 +1542,7 @@ int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_
   a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
   a.partial_out = partial_out;
   a.trace = g_trace_host;
-  w.prefix = warp_prefix;
+  w.plan = plan;
   w.U = batch * kv_heads;
   w.max_slots = max_slots;
   w.max_ctas = max_ctas;

@@ -48,10 +48,16 @@ def test_warp_plan_matches_oracle_and_split(B, H, m, N):
     cache, k, v, q, tiers = _case(100 + B + H + m, L, B, H, m, N, 7)
     plan = cache.warp_plan()
     assert plan is not None
-    prefix, ctas, slots, max_ctas = plan
-    p = prefix.cpu().numpy()[:B * H + 1]
+    table, ctas, slots, max_ctas = plan
     from paper_2503_23294_b200 import _lib
-    assert p[0] == 0 and p[-1] == _lib.load().ckv_decode_wp_cta_warps() * ctas and (np.diff(p) >= 2).all()
+    cw = _lib.load().ckv_decode_wp_cta_warps()
+    rec = table.cpu().numpy()[:8 * cw * ctas].reshape(cw * ctas, 8)   # per-warp records
+    counts = np.bincount(rec[:, 0], minlength=B * H)
+    assert counts.sum() == cw * ctas and (counts >= 2).all() and (np.diff(rec[:, 0]) >= 0).all()
+    assert (rec[:, 7] == counts[rec[:, 0]]).all()                      # nw = the unit's warps
+    n2 = np.zeros(B * H, np.int64)
+    np.add.at(n2, rec[:, 0], np.where((rec[:, 1] & 0xffff) == 0, rec[:, 2], 0))  # INT2 tiles, once per part
+    assert (n2 == np.repeat(cache.seq_host[:, 1] // 16, H)).all()      # the parts cover every tile
     qd = torch.from_numpy(q).cuda()
     out = cache.decode(qd).float().cpu().numpy()            # warp plan (whole batch, no splits)
     ref_split = cache.decode(qd, splits=3).float().cpu().numpy()
