@@ -1209,24 +1209,30 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     for (int i = 0; i < nslots; ++i) nl += s_lastu[i] >= 0 && s_lastu[i] == s_slot[i].w - s_slot[i].z;
     s_tr[11] = nl;
   }
-  // units this CTA completes: wait for the other CTAs' published partials (they arrived before
-  // this CTA's ticket, so they are running or done), then merge per (q row, d) with its own
-  for (int sl = 0; any_last && sl < nslots; ++sl) {
-    const int4 si = s_slot[sl];
-    if (s_lastu[sl] != si.w - si.z) continue;
-    const int us = u0 + sl;
-    const int nc = si.w - si.z + 1;
-    if (threadIdx.x == 0) {
-      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> done(ctr_l[2 * us + 1]);
-      while (done.load(cuda::memory_order_acquire) != (uint32_t)(nc - 1)) __nanosleep(32);
-      done.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
-      ctr_l[2 * us] = 0u;
+  // units this CTA completes: wait for the other CTAs' published partials (they drew earlier
+  // tickets, so they are running or done), then merge every completed unit's rows at once
+  if (any_last) {
+    if ((int)threadIdx.x < nslots) {
+      const int4 si = s_slot[threadIdx.x];
+      if (s_lastu[threadIdx.x] == si.w - si.z) {
+        const int us = u0 + threadIdx.x;
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> done(ctr_l[2 * us + 1]);
+        while (done.load(cuda::memory_order_acquire) != (uint32_t)(si.w - si.z)) __nanosleep(32);
+        done.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
+        ctr_l[2 * us] = 0u;
+      }
     }
     __syncthreads();
+  }
+  for (int p = threadIdx.x; any_last && p < nslots * a.m * kHeadDim; p += blockDim.x) {
+    const int d = p & (kHeadDim - 1), rt = s_rtab[p >> 7];
+    const int sl = rt >> 8, qi = rt & 255;
+    const int4 si = s_slot[sl];
+    if (s_lastu[sl] != si.w - si.z) continue;
+    const int us = u0 + sl, nc = si.w - si.z + 1;
     const int bs = us / a.H, hs = us - bs * a.H;
     const float* src_p = ws_l + (int64_t)us * w.max_ctas * a.m * kWsStride;  // [ctas][m][stride]
-    for (int p = threadIdx.x; p < a.m * kHeadDim; p += blockDim.x) {
-      const int qi = p >> 7, d = p & (kHeadDim - 1);
+    {
       const float* own = s_own(sl) + qi * kWsStride;
       // every CTA's (m, acc, l) in CTA order (the merger's own from shared memory; the sum order
       // does not depend on which CTA arrived last): one L2 round trip

@@ -23,3 +23,9 @@ def load_golden(name):
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+# Two decode schedules (warp plan, split-KV with any split count, cross-rank shards) partition
+# the online softmax differently, so the fp16 P operand (and P x group span on the V side) is
+# rounded at different running maxima: outputs agree to ~1e-3, not to fp32 order.  Each
+# schedule is separately held to the reference tolerance (1e-2) against the oracle.
+SCHED_TOL = 4e-3

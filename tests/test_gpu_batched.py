@@ -3,13 +3,14 @@ permutation) and mixed-precision decode attention (1e-2 abs / 1e-2 rel of the re
 f64 result on the same fp16 inputs), edge cases, split-KV shards, and full-size properties."""
 
 import hashlib
+import zlib
 
 import numpy as np
 import pytest
 import torch
 
 from oracle import ckv_oracle as O
-from tests.conftest import load_golden
+from tests.conftest import SCHED_TOL, load_golden
 
 pytestmark = pytest.mark.gpu
 
@@ -73,7 +74,7 @@ def test_batched_golden_case():
 @pytest.mark.parametrize("m", [1, 4, 8])
 @pytest.mark.parametrize("kind", ["mix", "int2", "int4", "fp16"])
 def test_decode_tiers_and_gqa(m, kind):
-    rng = np.random.default_rng(hash((m, kind)) % 2**32)
+    rng = np.random.default_rng(zlib.crc32(f"{m}-{kind}".encode()))
     L, B, H, D, N, tail = 2, 3, 2, 128, 20, 9
     T = N * 32 + tail
     k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
@@ -87,7 +88,7 @@ def test_decode_tiers_and_gqa(m, kind):
     cache = batched.build_cache_batched(kd, vd, _search_from_tiers(tiers))
     outs = [cache.decode(qd, splits=s).float().cpu().numpy() for s in (1, 2, 5)]
     for o in outs[1:]:
-        assert np.max(np.abs(o - outs[0])) < 2e-3  # split-KV merge is exact up to fp32 order
+        assert np.max(np.abs(o - outs[0])) < SCHED_TOL  # schedules agree to ~1e-3 (conftest.SCHED_TOL)
     for l in range(L):
         for b in range(B):
             for h in range(H):
@@ -168,7 +169,7 @@ def test_sequence_split_kv_shards_merge_to_full_decode():
     for world in (2, 3, 8):
         parts = [distributed.build_sequence_shard(k, v, s, world, r).decode_partial(q) for r in range(world)]
         merged = batched.lse_merge(torch.stack(parts)).view(q.shape).float()
-        assert torch.max(torch.abs(merged - full)).item() < 2e-3
+        assert torch.max(torch.abs(merged - full)).item() < SCHED_TOL
 
 
 def test_full_size_unit_properties_32k():
@@ -203,10 +204,10 @@ def test_per_layer_pdl_launches_match_single_launch():
     per = torch.empty_like(q)
     for l in range(L):
         cache.decode(q[l:l + 1], out=per[l:l + 1], layer=l, pdl=l > 0)
-    assert torch.max(torch.abs(per.float() - full)).item() < 2e-3
+    assert torch.max(torch.abs(per.float() - full)).item() < SCHED_TOL
     for s in (1, 3, 16, 40):  # 40 > the merge's register fast path
         o = cache.decode(q, splits=s).float()
-        assert torch.max(torch.abs(o - full)).item() < 2e-3
+        assert torch.max(torch.abs(o - full)).item() < SCHED_TOL
 
 
 def test_exact_mode_for_wide_scales_and_large_q():
@@ -291,7 +292,7 @@ def test_layer_by_layer_build_and_per_layer_partials():
     rows = B * H * m
     for l in range(L):
         per.decode_partial(q[l:l + 1], layer=l, pdl=l > 0, out=got[l * rows:(l + 1) * rows])
-    assert torch.max(torch.abs(batched.lse_merge(got[None]).float() - batched.lse_merge(want[None]).float())).item() < 2e-3
+    assert torch.max(torch.abs(batched.lse_merge(got[None]).float() - batched.lse_merge(want[None]).float())).item() < SCHED_TOL
 
 
 def test_decode_step_host_matches_device_decode():

@@ -13,6 +13,7 @@ import torch
 import bench
 from oracle import ckv_oracle as O
 from paper_2503_23294_b200 import batched, distributed, retrieval
+from tests.conftest import SCHED_TOL  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -96,7 +97,7 @@ def test_cfg3_llama2_13b_128k_sequence_split_kv():
     for world in (2, 4, 8):
         parts = [distributed.build_sequence_shard(k, v, s, world, r).decode_partial(q) for r in range(world)]
         merged = batched.lse_merge(torch.stack(parts)).view(q.shape).float()
-        assert torch.max(torch.abs(merged - full.float())).item() < 2e-3, world
+        assert torch.max(torch.abs(merged - full.float())).item() < SCHED_TOL, world
 
 
 @pytest.mark.parametrize("kind", ["all_fp16", "all_int2", "skewed"])

@@ -77,6 +77,17 @@ def main():
     print("PDL release after the previous layer's last exit, median %.1f us; late starters start->wait %.1f us"
           % (np.median(rel_lat), np.median(late)))
     print("q staging (wait -> staged) per CTA p50 %.1f max %.1f us" % tuple(np.percentile((t[:, 2] - t[:, 1]) / 1e3, [50, 100])))
+    # the critical CTA of each layer (latest exit): its phases relative to its own tiles end
+    crit = []
+    for i in range(1, len(launches) - 1):
+        x = t[t[:, 7] == launches[i]]
+        r = x[np.argmax(x[:, 4])]
+        tmax = x[:, 3].max()
+        crit.append([(r[3] - tmax) / 1e3, (r[8] - r[3]) / 1e3, (r[9] - r[8]) / 1e3, (r[10] - r[9]) / 1e3,
+                     (r[4] - r[10]) / 1e3, r[11]])
+    c = np.median(np.array(crit), axis=0)
+    print("critical CTA (median over layers): tiles_end - layer tiles_end max %.1f, -> merge start %.1f, merge %.1f, "
+          "publish %.1f, final %.1f us, completes %.0f units" % tuple(c))
 
 
 if __name__ == "__main__":
