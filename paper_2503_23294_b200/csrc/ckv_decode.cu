@@ -961,6 +961,7 @@ constexpr int kWpWarps = CKV_WP_WARPS;  // warps per CTA; 16 / kWpWarps CTAs per
 //   slot records [ctas][8][4]: the slot unit's warps [x, y) within the CTA, first / last CTA.
 // Every CTA reads its records with independent loads (no dependent chain before its prologue).
 constexpr int kPlanWarpInts = 8, kPlanCtaInts = 4, kPlanSlots = 8;
+constexpr int64_t kMergeSpin = 20000;  // ns a designated merger waits for its unit's partners
 struct WpArgs {
   DecArgs d;
   const int32_t* plan;
@@ -986,7 +987,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   unsigned char* s_qall = s_dyn + kWpWarps * kWarpRing;
   __shared__ float s_ml[kWpWarps][8][2];
   __shared__ __align__(16) unsigned char s_scr[kWpWarps][kScratch];
-  __shared__ int s_lastu[8];
+  __shared__ int s_lastu[8], s_do[8];
   __shared__ int4 s_slot[8];             // per unit slot: warps [x, y) of this CTA, first / last CTA of the unit
   __shared__ unsigned short s_rtab[64];  // merge row r -> (slot << 8 | q row)
   __shared__ int64_t s_tr[12], s_tend[kWpWarps];
@@ -1019,9 +1020,11 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   UnitScale us;
   us.F = unit_v_exponent(a, l, b, h);
   // per-slot facts for the merge (build-time plan data: before the wait)
-  if ((int)threadIdx.x < nslots)
+  if ((int)threadIdx.x < nslots) {
     s_slot[threadIdx.x] = __ldg(reinterpret_cast<const int4*>(w.plan + (kPlanWarpInts * kWpWarps + kPlanCtaInts) * nctas) +
                                 kPlanSlots * cta + threadIdx.x);
+    s_do[threadIdx.x] = 0;
+  }
   if ((int)threadIdx.x < nslots * a.m)
     s_rtab[threadIdx.x] = (unsigned short)(((threadIdx.x / a.m) << 8) | (threadIdx.x % a.m));
   // pull this warp's q rows into L2 while the previous launch drains (L2 is the point of
@@ -1172,63 +1175,84 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
         *reinterpret_cast<uint2*>(a.out + l * a.o_sl + bs * a.o_sb + (int64_t)(hs * a.m + qi) * kHeadDim + 4 * lane) =
             make_uint2(h2_as_u32(h0), h2_as_u32(h1));
       }
-    } else {
+    } else {  // the partial: shared memory (a merging CTA's own) and its workspace slot (published)
       float* dst = s_own(sl) + qi * kWsStride;
-      *reinterpret_cast<float4*>(dst + 4 * lane) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-      if (lane == 0) { dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum; }
+      float* gdst = ws_l + (((int64_t)(u0 + sl) * w.max_ctas + (cta - si.z)) * a.m + qi) * kWsStride;
+      const float4 v4 = make_float4(o4[0], o4[1], o4[2], o4[3]);
+      *reinterpret_cast<float4*>(dst + 4 * lane) = v4;
+      __stcg(reinterpret_cast<float4*>(gdst + 4 * lane), v4);
+      if (lane == 0) {
+        dst[kHeadDim] = ms; dst[kHeadDim + 1] = lsum;
+        __stcg(gdst + kHeadDim, ms); __stcg(gdst + kHeadDim + 1, lsum);
+      }
     }
   }
   if (tick_t < nslots) s_lastu[tick_t] = ticket;
   __syncthreads();
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[9] = gtime();
-  // publish: split slots whose ticket is not the unit's last
-  bool any_pub = false, any_last = false;
+  // Roles per split unit: the CTA with ticket 0 (the first to finish its tiles) is the designated
+  // merger: it keeps its partial in shared memory and waits for the others' published partials,
+  // for at most kMergeSpin ns; the others publish theirs and count them in the unit's done
+  // counter.  A merger that times out (e.g. a partner CTA not yet resident because a concurrent
+  // launch holds the SMs) publishes its own partial and leaves; then the CTA whose count completes
+  // the set (old value nc - 1) merges.  Exactly one CTA merges, no CTA waits unboundedly.
+  // (every split partial is already in its workspace slot: the merge above wrote it there too)
+  bool any_pub = false, any_mrg = false;
   for (int sl = 0; sl < nslots; ++sl) {
-    const int4 si = s_slot[sl];
     const int tk = s_lastu[sl];
-    if (tk < 0) continue;
-    if (tk == si.w - si.z) { any_last = true; continue; }
-    any_pub = true;
-    float* dst = ws_l + ((int64_t)(u0 + sl) * w.max_ctas + (cta - si.z)) * a.m * kWsStride;
-    for (int i = threadIdx.x; i < a.m * kWsStride; i += blockDim.x) __stcg(dst + i, s_own(sl)[i]);
+    any_mrg |= tk == 0;
+    any_pub |= tk > 0;
   }
   if (any_pub) {
-    __syncthreads();  // orders every thread's partial stores before the device-scope release
+    // (the barrier above ordered every thread's partial stores before the device-scope release)
     if ((int)threadIdx.x < nslots) {
       const int4 si = s_slot[threadIdx.x];
       const int tk = s_lastu[threadIdx.x];
-      if (tk >= 0 && tk != si.w - si.z) {
+      if (tk > 0) {
         cuda::atomic_ref<uint32_t, cuda::thread_scope_device> done(ctr_l[2 * (u0 + threadIdx.x) + 1]);
-        done.fetch_add(1u, cuda::memory_order_release);
+        s_do[threadIdx.x] = done.fetch_add(1u, cuda::memory_order_acq_rel) == (uint32_t)(si.w - si.z);
       }
     }
   }
   if (threadIdx.x == 0 && (a.trace != nullptr)) {
     s_tr[10] = gtime();
     int nl = 0;
-    for (int i = 0; i < nslots; ++i) nl += s_lastu[i] >= 0 && s_lastu[i] == s_slot[i].w - s_slot[i].z;
+    for (int i = 0; i < nslots; ++i) nl += s_lastu[i] == 0;
     s_tr[11] = nl;
   }
-  // units this CTA completes: wait for the other CTAs' published partials (they drew earlier
-  // tickets, so they are running or done), then merge every completed unit's rows at once
-  if (any_last) {
-    if ((int)threadIdx.x < nslots) {
-      const int4 si = s_slot[threadIdx.x];
-      if (s_lastu[threadIdx.x] == si.w - si.z) {
-        const int us = u0 + threadIdx.x;
-        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> done(ctr_l[2 * us + 1]);
-        while (done.load(cuda::memory_order_acquire) != (uint32_t)(si.w - si.z)) __nanosleep(32);
-        done.store(0u, cuda::memory_order_relaxed);  // ready for the next launch
-        ctr_l[2 * us] = 0u;
+  // designated mergers: warp sl waits for slot sl's partners (bounded), or resigns
+  if (any_mrg && warp < nslots && s_lastu[warp] == 0) {
+    const int4 si = s_slot[warp];
+    const uint32_t others = (uint32_t)(si.w - si.z);
+    cuda::atomic_ref<uint32_t, cuda::thread_scope_device> done(ctr_l[2 * (u0 + warp) + 1]);
+    int got = 0;
+    if (lane == 0) {
+      const int64_t t0 = gtime();
+      while (true) {
+        if (done.load(cuda::memory_order_acquire) == others) { got = 1; break; }
+        if (gtime() - t0 > kMergeSpin) break;
+        __nanosleep(64);
       }
     }
-    __syncthreads();
+    got = __shfl_sync(0xffffffffu, got, 0);
+    if (!got) {  // resign: count the own partial (already in its workspace slot)
+      if (lane == 0) got = done.fetch_add(1u, cuda::memory_order_acq_rel) == others;
+      got = __shfl_sync(0xffffffffu, got, 0);
+    }
+    if (lane == 0) s_do[warp] = got;
   }
-  for (int p = threadIdx.x; any_last && p < nslots * a.m * kHeadDim; p += blockDim.x) {
+  if (any_pub || any_mrg) __syncthreads();
+  if ((int)threadIdx.x < nslots && s_do[threadIdx.x]) {  // the merging CTA resets the unit's counters
+    ctr_l[2 * (u0 + threadIdx.x) + 1] = 0u;
+    ctr_l[2 * (u0 + threadIdx.x)] = 0u;
+  }
+  // every unit this CTA merges: all partials in CTA order (its own from shared memory, the
+  // others from L2), all units' rows at once
+  for (int p = threadIdx.x; (any_pub || any_mrg) && p < nslots * a.m * kHeadDim; p += blockDim.x) {
     const int d = p & (kHeadDim - 1), rt = s_rtab[p >> 7];
     const int sl = rt >> 8, qi = rt & 255;
     const int4 si = s_slot[sl];
-    if (s_lastu[sl] != si.w - si.z) continue;
+    if (!s_do[sl]) continue;
     const int us = u0 + sl, nc = si.w - si.z + 1;
     const int bs = us / a.H, hs = us - bs * a.H;
     const float* src_p = ws_l + (int64_t)us * w.max_ctas * a.m * kWsStride;  // [ctas][m][stride]
