@@ -288,7 +288,7 @@ def pick_splits(args, cache, m, layers=1):
 def schedule_desc(cache, splits):
     if splits is None:
         p = cache.warp_plan()
-        nw = np.diff(p[0].cpu().numpy()[:cache.B * cache.H + 1])
+        nw = cache.wp_unit_warps
         return f"warp plan: {len(nw)} units x {int(nw.min())}-{int(nw.max())} warps, {p[1]} CTAs"
     return f"split: {splits} CTAs of 4 warps per unit"
 
@@ -547,8 +547,22 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
             torch.cuda.synchronize()
         with ClockSampler(dev.index or 0) as clk:
             ms = timed(step, steps)
-        res["local_decode_ms"] = round(timed(local_graph.replay, steps), 4)
-        res["exchange_merge_ms"] = round(ms - res["local_decode_ms"], 4)
+        # the step's two parts measured inside the same kind of step (events between them, not a
+        # difference of two separately timed loops): local decode | exchange + merge
+        torch.cuda.synchronize()
+        barrier()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        for e in ev:
+            e[0].record()
+            local_graph.replay()
+            e[1].record()
+            gathered = distributed.exchange_partials(parts) if world > 1 else parts[None]
+            batched.lse_merge(gathered)
+            e[2].record()
+        torch.cuda.synchronize()
+        barrier()
+        res["local_decode_ms"] = round(sync_max(sum(e[0].elapsed_time(e[1]) for e in ev) / steps), 4)
+        res["exchange_merge_ms"] = round(sync_max(sum(e[1].elapsed_time(e[2]) for e in ev) / steps), 4)
         res["per_layer_merge_us"] = round(1e3 * timed(merge_fn, max(steps, 20)) / merge_reps, 2)
         res["per_layer_merge_note"] = ("one layer's all_gather + ckv_lse_merge, " +
                                        ("CUDA-graph replayed" if merge_reps > 1 else "eager launches"))

@@ -235,6 +235,7 @@ class BatchedKVCache:
                                             plan.ctypes.data, ctypes.byref(ms), ctypes.byref(mc))
                 if st == 0:
                     self._wp = (torch.from_numpy(plan).to(self.device), n_cta, ms.value, mc.value)
+                    self.wp_unit_warps = n  # warps per unit (host copy, for reports)
         return self._wp or None
 
     def _wp_workspace(self, m, layers, layer, max_ctas):

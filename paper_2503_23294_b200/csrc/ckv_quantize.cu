@@ -203,7 +203,7 @@ __device__ __forceinline__ void l2_prefetch(const void* p) {
 // 32-bit shared-memory stores (staging addresses are 32-bit shared-window offsets: no 64-bit
 // generic pointer arithmetic in the quantize loops)
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)(v & 0xFFu)) : "memory");
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");  // low byte of v
 }
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
@@ -353,7 +353,10 @@ __device__ __forceinline__ CtaPos cta_pos(int B) {
 
 // One warp per (layer, sequence, kv-head, destination chunk slot).  Slot p < N takes source
 // chunk perm[p]; slot p == N is the context tail (if any).
-__global__ void __launch_bounds__(kQWarps * 32, 8)
+#ifndef CKV_Q_MIN_CTAS
+#define CKV_Q_MIN_CTAS 8
+#endif
+__global__ void __launch_bounds__(kQWarps * 32, CKV_Q_MIN_CTAS)
 reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
                              int H, int B, int64_t sL, int64_t sB, int64_t sT, int64_t sH,
                              const uint32_t* __restrict__ perm, int max_chunks,
@@ -390,16 +393,22 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
     if (lane == 0) *reinterpret_cast<int4*>(s_task[warp]) = make_int4(tier, rows, src_tok0, dst_row0);
     __syncwarp();
   }
-  const uint32_t task_addr = (uint32_t)__cvta_generic_to_shared(s_task[warp]);
-  const int sub = lane >> 4, j = lane & 15;  // 2 rows per warp step, 8 fp16 per lane
-  bool bad = false, bad_fp = false;  // non-finite input in a quantized / an FP16-region row
+  // nothing but tsel lives across the passes: the thread coordinates, the task and the
+  // non-finite flags are re-derived / reported inside each pass (held across the quantize
+  // loops, they were spilled at 64 registers, and the spill stores reached DRAM)
 #pragma unroll 1
   for (int tsel = 0; tsel < 2; ++tsel) {
+    uint32_t tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    const int lane_v = (int)(tid & 31);
+    const uint32_t task_addr = (uint32_t)__cvta_generic_to_shared(s_task[tid >> 5]);
     const QTask t = read_task(task_addr);
     const CtaPos c = cta_pos(B);
     const int64_t unit = (int64_t)c.l * H + c.h;
     const uint16_t* src = (tsel ? v : k) + c.l * sL + c.b * sB + c.h * sH + (int64_t)t.src_tok0 * sT;
     if (t.tier == 2) {
+      const int sub = lane_v >> 4, j = lane_v & 15;  // 2 rows per warp step, 8 fp16 per lane
+      bool bad_fp = false;  // non-finite input in an FP16-region row
       // arena fields by explicit selects (a reference to either parameter struct would put
       // both in local memory)
       uint16_t* dst = (tsel ? VA.fp : KA.fp) + (unit * (tsel ? VA.rows_fp : KA.rows_fp) + t.dst_row0) * kHeadDim;
@@ -415,24 +424,24 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
           reinterpret_cast<uint4*>(dst + (int64_t)r * kHeadDim)[j] = x;
         }
       }
+      // the reference rejects non-finite values only where it quantizes (build_cache ->
+      // quantizer.quantize, quantizer.py:71-72); FP16-region rows are copied as they are
+      if (__any_sync(0xffffffffu, bad_fp) && lane_v == 0) atomicOr(flag, CKV_FLAG_NONFINITE_FP16);
       continue;
     }
     const int code_bytes = t.tier == 0 ? kTileBytes2 : kTileBytes4;
-    // thread coordinates re-read here (volatile): hoisted out of the pass loop, the addresses
-    // derived from them would be spilled to local memory at 64 registers
-    uint32_t tid;
-    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
-    const int lane_v = (int)(tid & 31);
     const uint32_t sblk = (uint32_t)__cvta_generic_to_shared(s_blk[tid >> 5]);
     const uint32_t sc = sblk + (tsel ? code_bytes : 0);
     const uint32_t sm = sblk + 2 * code_bytes + (tsel ? kTileBytesMeta : 0);
-    bool wide;
+    bool wide, bad = false;  // bad: non-finite input in a quantized row
     float smax = 0.0f;  // largest group span of the chunk (decode precision routing)
     if (t.tier == 0) wide = tsel ? quantize_chunk<2, true>(src, (int)sT, lane_v, sc, sm, bad, smax)
                                  : quantize_chunk<2, false>(src, (int)sT, lane_v, sc, sm, bad, smax);
     else wide = tsel ? quantize_chunk<4, true>(src, (int)sT, lane_v, sc, sm, bad, smax)
                      : quantize_chunk<4, false>(src, (int)sT, lane_v, sc, sm, bad, smax);
     __syncwarp();
+    if (__any_sync(0xffffffffu, bad) && lane_v == 0) atomicOr(flag, CKV_FLAG_NONFINITE);
+    const int lane = lane_v;
     const QTask t2 = read_task(task_addr);
     const CtaPos c2 = cta_pos(B);
     const int64_t unit2 = (int64_t)c2.l * H + c2.h;
@@ -441,7 +450,7 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       const int64_t tile0 = (unit2 * (t2.tier == 0 ? KA.rows2 : KA.rows4) + t2.dst_row0) / kTileRows;
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(t2.tier == 0 ? KA.codes2 : KA.codes4) + tile0 * blk);
       const int n16 = (int)(2 * blk / 16);
-      for (int i = lane; i < n16; i += 32) dst[i] = reinterpret_cast<const uint4*>(s_blk[warp])[i];
+      for (int i = lane; i < n16; i += 32) dst[i] = reinterpret_cast<const uint4*>(s_blk[tid >> 5])[i];
     }
     uint32_t* span_flags = tsel ? VA.span_flags : KA.span_flags;
     uint32_t* span_max = tsel ? VA.span_max : KA.span_max;
@@ -453,10 +462,6 @@ reorder_quantize_pack_kernel(const uint16_t* __restrict__ k, const uint16_t* __r
       atomicMax(span_max + unit2 * B + c2.b, __float_as_uint(smax));
     __syncwarp();
   }
-  // the reference rejects non-finite values only where it quantizes (build_cache ->
-  // quantizer.quantize, quantizer.py:71-72); FP16-region rows are copied as they are
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE);
-  if (__any_sync(0xffffffffu, bad_fp) && lane == 0) atomicOr(flag, CKV_FLAG_NONFINITE_FP16);
 }
 
 // Decode append: row (l, b, h) of k_new/v_new -> FP16 region row off_fp + len_fp.

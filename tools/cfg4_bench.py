@@ -27,6 +27,7 @@ def run(kind, L=2, B=64, H=8, m=4, T=16384, steps=10):
     k = torch.randn((L, B, T, H, 128), generator=g, device="cuda", dtype=torch.float16)
     v = torch.randn((L, B, T, H, 128), generator=g, device="cuda", dtype=torch.float16)
     cache = batched.build_cache_batched(k, v, s)
+    cache.schedule = os.environ.get("CKV_SCHEDULE", "auto")
     del k, v
     q = torch.randn((L, B, H * m, 128), generator=g, device="cuda", dtype=torch.float16)
     out = torch.empty_like(q)
@@ -50,5 +51,7 @@ def run(kind, L=2, B=64, H=8, m=4, T=16384, steps=10):
 
 
 if __name__ == "__main__":
-    for kind in ("all_fp16", "all_int2", "skewed"):
-        print(json.dumps(run(kind)))
+    for kind in sys.argv[1:] or ("all_fp16", "all_int2", "skewed"):
+        r = run(kind)
+        r["schedule"] = os.environ.get("CKV_SCHEDULE", "auto")
+        print(json.dumps(r))
