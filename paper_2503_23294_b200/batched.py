@@ -564,7 +564,8 @@ class BatchedKVCache:
             reference=ref)
 
     def wide_scale_units(self):
-        """Number of (layer, kv-head, sequence) units that use the exact wide-scale path."""
+        """Number of (layer, kv-head, sequence) units with a group scale above 4000 (diagnostic
+        span flag of the quantize kernel; the decode has one path for every unit)."""
         return int(((self.k["span_flags"] | self.v["span_flags"]) != 0).sum().item())
 
     # -- export to the reference per-head format ------------------------------------------

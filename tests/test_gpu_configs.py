@@ -146,12 +146,11 @@ def test_cfg5_prefill_128k_codes_bit_exact():
 @pytest.mark.parametrize("m", [4, 6, 8])
 def test_cfg2_outlier_variant_32k(m):
     """SURVEY §8d's outlier variant of cfg2: K x8 on 4 channels (one per 32-wide group, so every
-    K group of every token is ~8x wider), q x3 (peaky softmax) at 32K with reference maps.  The
-    normal path's fp16 K operands would miss 1e-2 here (1.8e-2 measured: the error grows with
-    K group span x |q|); the unit's span bound routes it to the precise K path (exact magic
-    values in the MMA, per-group bias and scale in fp32), which must meet the north_star
-    tolerance — for m <= 4 q rows per kv head in one pass, for 5-8 rows in two passes over the
-    same K operands.  Codes and metadata stay bit-exact."""
+    K group of every token is ~8x wider), q x3 (peaky softmax) at 32K with reference maps.  A
+    decode that dequantizes K into fp16 operands misses 1e-2 here (round 1 measured 1.8e-2: the
+    error grows with K group span x |q|); with the codes exact in the MMA and the group scales
+    applied in fp32 the single path must meet the north_star tolerance for 4, 6 and 8 q rows
+    per kv head.  Codes and metadata stay bit-exact."""
     L, B, H, T = 1, 2, 2, 32768
     s, maps = _search([(T, 3), (T, 6)])
     k, v = _randn((L, B, T, H, 128), 61), _randn((L, B, T, H, 128), 62)

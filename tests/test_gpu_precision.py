@@ -1,8 +1,10 @@
-"""Decode precision routing at its boundaries (ckv_decode.cu: kPreciseSpanQ = 8 on
-span_max x max|q| (log2-scaled q), kWideQ = 1000 on max|q|, and the 4000 scale cutoff of the
-quantize kernel's span flags).  On both sides of every boundary the output must meet the
-north_star tolerance (1e-2 abs and 1e-2 of max|ref|) against the reference's f64
-mixed_decode_attention on the same fp16 inputs, with a peaky softmax (q aligned with a few keys)."""
+"""Decode precision across wide groups and large q.  Round 1's kernel routed units by
+span_max x max|q| (log2-scaled q; a precise K path above 8), by max|q| (an exact mode above
+1000) and by the quantize kernel's 4000 scale cutoff; the current kernel has one path (codes as
+exact fp16 subnormals in the MMA, group scales in fp32: DESIGN §3 K3), and these former
+boundaries stay as test points.  On both sides of each the output must meet the north_star
+tolerance (1e-2 abs and 1e-2 of max|ref|) against the reference's f64 mixed_decode_attention on
+the same fp16 inputs, with a peaky softmax (q aligned with a few keys)."""
 
 import math
 
@@ -68,8 +70,7 @@ def _run(k, v, q16, tiers, m):
 @pytest.mark.parametrize("m", [4, 8])
 @pytest.mark.parametrize("product", [7.5, 8.5, 60.0])
 def test_precise_threshold_both_sides(product, m):
-    """span_max x max|q| just under kPreciseSpanQ (normal path at its widest admitted span),
-    just over it and far over it (precise K path)."""
+    """span_max x max|q| just under, just over and far over round 1's precise-path threshold (8)."""
     k, v, q, tiers = _unit_case(11 + m, m=m)
     cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers))
     span = cache.k["span_max"].view(torch.float32)[0, :, 0].cpu().numpy()
@@ -82,7 +83,7 @@ def test_precise_threshold_both_sides(product, m):
 
 @pytest.mark.parametrize("qmax", [990.0, 1010.0])
 def test_wide_q_boundary(qmax):
-    """max|q| (log2-scaled) just under / over kWideQ: the weighted paths vs the exact mode."""
+    """max|q| (log2-scaled) just under / over round 1's exact-mode threshold (1000)."""
     k, v, q, tiers = _unit_case(21, outlier=1.0)
     f = qmax / max(_q_log2_max(q.astype(np.float16), h, 4) for h in range(2))
     _run(k, v, _scaled_q(q, f), tiers, 4)
@@ -91,7 +92,7 @@ def test_wide_q_boundary(qmax):
 @pytest.mark.parametrize("scale", [3990.0, 4010.0])
 def test_scale_cutoff_boundary(scale):
     """An INT2 group whose scale (span / 3) sits just under / over the 4000 cutoff: the unit's
-    span flag decides between the weighted forms and the exact mode."""
+    (diagnostic) span flag is set exactly above it, and the output meets the gate on both sides."""
     k, v, q, tiers = _unit_case(31, outlier=1.0)
     tiers[:] = 0  # all INT2 except the FP16 chunks the map would have: all quantized
     k[0, 0, 100, 0, 0] = np.float16(3 * scale + float(k[0, 0, 100, 0, 1:32].min()))

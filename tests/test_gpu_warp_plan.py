@@ -98,8 +98,8 @@ def test_warp_plan_outlier_precise_and_exact_units():
     N = 40
     T = N * 32 + 5
     k = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
-    k[..., [3, 40, 77, 100]] *= 8          # wide K groups: precise path (two passes, m = 8)
-    k[0, 1, 10, 2, 5] = 20000.0            # one unit with a huge scale: exact mode
+    k[..., [3, 40, 77, 100]] *= 8          # wide K groups (round 1: the precise path)
+    k[0, 1, 10, 2, 5] = 20000.0            # one unit with a huge scale (round 1: the exact mode)
     v = rng.normal(size=(L, B, T, H, 128)).astype(np.float16)
     q = (rng.normal(size=(L, B, H * m, 128)) * 3).astype(np.float16)
     tiers = rng.choice([0, 1, 2], size=(B, N), p=(0.7, 0.25, 0.05)).astype(np.uint8)
