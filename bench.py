@@ -279,17 +279,28 @@ def pick_splits(args, cache, m, layers=1):
     """Decode schedule for a bench run: the warp plan (splits None) unless --schedule split or
     --splits is given, or the cache has no warp plan."""
     cache.schedule = args.schedule
-    if (args.schedule != "split" and args.splits is None and getattr(args, "chains", 1) == 1
-            and cache._use_wp(m, None, None, None) is not None):
+    chains = getattr(args, "chains", 1)
+    first = None if chains == 1 else cache._chain_ranges(chains)[0]
+    if args.schedule != "split" and args.splits is None and cache._use_wp(m, first, None, None) is not None:
         return None
     return args.splits or cache.default_splits(m, layers)
 
 
-def schedule_desc(cache, splits):
+def launch_desc(chains):
+    if chains == 1:
+        return "per-layer (32 PDL-chained launches per step, replayed as one CUDA graph)"
+    return (f"per-layer: {chains} micro-batch chains (sequence ranges) on their own streams, each 32 "
+            f"PDL-chained per-layer launches (layer l+1 of a chain waits for its layer l); one CUDA graph per step")
+
+
+def schedule_desc(cache, splits, chains=1):
     if splits is None:
         p = cache.warp_plan()
         nw = cache.wp_unit_warps
-        return f"warp plan: {len(nw)} units x {int(nw.min())}-{int(nw.max())} warps, {p[1]} CTAs"
+        desc = f"warp plan: {len(nw)} units x {int(nw.min())}-{int(nw.max())} warps, {p[1]} CTAs"
+        if chains > 1:
+            desc += f"; {chains} micro-batch chains, each its own warp plan per launch"
+        return desc
     return f"split: {splits} CTAs of 4 warps per unit"
 
 
@@ -684,7 +695,7 @@ def run_cfg4(args, torch, dist, dev, rank, world, local):
     splits = pick_splits(args, cache, m)
     my_bytes = cache.algorithmic_bytes(m)
 
-    graph = cache.decode_graph(q, out, splits=splits)  # the step's 32 PDL-chained launches
+    graph = cache.decode_graph(q, out, splits=splits, chains=args.chains)  # the step's per-layer PDL-chained launches
     step = graph.replay
 
     def sync_max(ms):
@@ -740,8 +751,8 @@ def run_cfg4(args, torch, dist, dev, rank, world, local):
             "config": {"workload": f"cfg4: batch 64 x 16K, Llama-3-8B GQA 32q/8kv d128, 32 layers, map {args.cfg4_map}",
                        "global_batch": Bg, "seq_len": T, "parallelism": f"batch-shard x{world}",
                        "tier_fractions_int2_int4_fp16": [round(float(x), 4) for x in frac],
-                       "launch": "per-layer (32 PDL-chained launches per step, replayed as one CUDA graph)",
-                       "splits": splits, "schedule": schedule_desc(cache, splits),
+                       "launch": launch_desc(args.chains),
+                       "splits": splits, "schedule": schedule_desc(cache, splits, args.chains),
                        "l2": "inputs larger than L2"},
             "tokens_per_s": round(Bg / (ms * 1e-3), 1),
             "algorithmic_bytes_per_step": int(step_bytes),
@@ -1071,7 +1082,7 @@ def main():
     torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
 
-    sched_desc = schedule_desc(cache, splits)
+    sched_desc = schedule_desc(cache, splits, args.chains)
     # parity of the timed cache: the graph step's output for sampled units vs the reference
     graph.replay()
     torch.cuda.synchronize()
@@ -1149,7 +1160,7 @@ def main():
             "config": {"workload": "cfg2: Llama-3-8B GQA 32q/8kv d128, 32 layers, 32K ctx, batch 8 per GPU",
                        "global_batch": B * world, "seq_len": CFG2["context"], "parallelism": f"batch-shard x{world}",
                        "tier_fractions_int2_int4_fp16": [round(float(x), 4) for x in frac],
-                       "launch": "per-layer (32 PDL-chained launches per step, replayed as one CUDA graph)",
+                       "launch": launch_desc(args.chains),
                        "splits": splits, "schedule": sched_desc,
                        "l2": "inputs larger than L2 (7.1 GB arenas vs 126 MB L2)"},
             "tokens_per_s": round(tokens_per_s, 1),

@@ -275,7 +275,8 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
  * per-warp tile ranges, per-CTA unit slots; upload it to device memory) and returns max_slots
  * (the most units one CTA spans, <= 8; CKV_ERR_UNSUPPORTED above) and max_ctas (the most CTAs
  * one unit spans).  A warp's part of unit u is a contiguous share of the unit's tiles of each
- * kind; a unit split over several CTAs is merged by the CTA with the last arrival ticket.
+ * kind; a unit split over several CTAs is merged by the first of its CTAs to finish its tiles
+ * (bounded wait; on timeout the CTA completing the set merges).
  * Workspace: ckv_decode_wp_workspace_bytes(), zero-filled once.  Outputs as
  * ckv_decode_attention (out or partial_out). */
 int64_t ckv_decode_wp_workspace_bytes(int32_t layers, int32_t batch, int32_t kv_heads, int32_t m,
@@ -292,6 +293,17 @@ int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_
                                 const int32_t* plan, int32_t ctas, int32_t max_slots,
                                 int32_t max_ctas, void* workspace, uint16_t* out, int64_t o_s_layer,
                                 int64_t o_s_batch, float* partial_out, int32_t flags, void* stream);
+/* The same over sequences [b0, b0 + n_seqs) of the cache (micro-batch chains: each range its own
+ * chain of per-layer launches on its own stream): the plan is built from those rows of the seq
+ * table (seq_host + 8 b0, batch n_seqs), the workspace sized for n_seqs; q / out keep the whole
+ * batch's strides, rows outside the range are left untouched. */
+int32_t ckv_decode_attention_wp_seqs(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                                     ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                                     int32_t layers, int32_t batch, int32_t b0, int32_t n_seqs,
+                                     int32_t kv_heads, int32_t m, float scale, const int32_t* plan,
+                                     int32_t ctas, int32_t max_slots, int32_t max_ctas, void* workspace,
+                                     uint16_t* out, int64_t o_s_layer, int64_t o_s_batch,
+                                     float* partial_out, int32_t flags, void* stream);
 
 /* Split-KV merge across ranks (new; the NCCL-exchanged partials of SURVEY §8e):
  * partials f32 [P][rows][128 + 2] = (acc[128] unnormalised at m, m (log2 domain), l);

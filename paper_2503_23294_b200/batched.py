@@ -107,7 +107,7 @@ class BatchedKVCache:
         self._ws, self._ws_ptr = {}, {}
         self._arenas = {}
         self._perm = None
-        self._wp = None
+        self._wp = {}  # warp plans per sequence range (b0, b1)
         # decode schedule of whole-batch launches: "wp" (warp plan: one 16-warp CTA per SM,
         # units split at warp granularity), "split" (4-warp CTAs, `splits` per unit) or "auto"
         # (the warp plan unless the cache is small, fewer than 8 tiles per warp, or more than half
@@ -197,57 +197,66 @@ class BatchedKVCache:
                 best, best_cost = s, cost
         return best
 
-    def warp_plan(self):
+    def warp_plan(self, seqs=None):
         """Warp-plan schedule (ckv_decode_attention_wp): unit u = b*H + h gets n_u warps in
         proportion to its tile cost (INT2 1, INT4 1.06, FP16-region 2 per 16-token tile), at
         least 2, summing to 16 x the SM count; returns (plan table i32 on the device, ctas,
         max_slots, max_ctas) or None when the units do not fit (more than 8 per CTA).  Computed
-        once: any plan is exact, later appends only shift the balance slightly.  The table
-        (ckv_decode_wp_plan, include/ckv.h) holds every warp's tile ranges and every CTA's unit
-        slots, so a CTA's prologue needs no dependent loads."""
-        if self._wp is None:
-            self._wp = False
-            cw = _lib.load().ckv_decode_wp_cta_warps()  # warps per CTA (16 / cw CTAs per SM)
-            n_sm = _num_sms()
-            T = 16 * n_sm
-            n_cta = T // cw
-            U = self.B * self.H
-            s = self.seq_host.astype(np.int64)
-            cost_b = s[:, 1] // TILE + 1.06 * (s[:, 3] // TILE) + 2.0 * (-(-s[:, 5] // TILE))
-            cost = np.repeat(cost_b, self.H).astype(np.float64)
-            if U and 2 * U <= T and cost.sum() > 0:
-                raw = T * cost / cost.sum()
-                n = np.maximum(np.floor(raw).astype(np.int64), 2)
-                order = np.argsort(-(raw - np.floor(raw)), kind="stable")
-                i = 0
-                while n.sum() < T:
-                    n[order[i % U]] += 1
-                    i += 1
-                while n.sum() > T:
-                    j = int(np.argmax(np.where(n > 2, n - raw, -np.inf)))
-                    n[j] -= 1
-                lib = _lib.load()
-                plan = np.zeros(int(lib.ckv_decode_wp_plan_ints(n_cta)), dtype=np.int32)
-                seq = np.ascontiguousarray(self.seq_host, dtype=np.int32)
-                nw = np.ascontiguousarray(n, dtype=np.int32)
-                ms, mc = ctypes.c_int32(0), ctypes.c_int32(0)
-                st = lib.ckv_decode_wp_plan(seq.ctypes.data, self.B, self.H, nw.ctypes.data, n_cta,
-                                            plan.ctypes.data, ctypes.byref(ms), ctypes.byref(mc))
-                if st == 0:
-                    self._wp = (torch.from_numpy(plan).to(self.device), n_cta, ms.value, mc.value)
-                    self.wp_unit_warps = n  # warps per unit (host copy, for reports)
-        return self._wp or None
+        once per sequence range (``seqs`` = (b0, b1), default the whole batch; a range is one
+        micro-batch chain's launches): any plan is exact, later appends only shift the balance
+        slightly.  The table (ckv_decode_wp_plan, include/ckv.h) holds every warp's tile ranges
+        and every CTA's unit slots, so a CTA's prologue needs no dependent loads."""
+        key = (0, self.B) if seqs is None else (int(seqs[0]), int(seqs[1]))
+        if key not in self._wp:
+            plan, n = self._build_wp_plan(*key)
+            self._wp[key] = plan
+            if key == (0, self.B) and plan is not None:
+                self.wp_unit_warps = n  # warps per unit (host copy, for reports)
+        return self._wp[key]
 
-    def _wp_workspace(self, m, layers, layer, max_ctas):
+    def _build_wp_plan(self, b0, b1):
+        """(plan, warps per unit) for sequences [b0, b1), or (None, None)."""
+        cw = _lib.load().ckv_decode_wp_cta_warps()  # warps per CTA (16 / cw CTAs per SM)
+        T = 16 * _num_sms()
+        n_cta = T // cw
+        U = (b1 - b0) * self.H
+        s = self.seq_host[b0:b1].astype(np.int64)
+        cost_b = s[:, 1] // TILE + 1.06 * (s[:, 3] // TILE) + 2.0 * (-(-s[:, 5] // TILE))
+        cost = np.repeat(cost_b, self.H).astype(np.float64)
+        if not (U and 2 * U <= T and cost.sum() > 0):
+            return None, None
+        raw = T * cost / cost.sum()
+        n = np.maximum(np.floor(raw).astype(np.int64), 2)
+        order = np.argsort(-(raw - np.floor(raw)), kind="stable")
+        i = 0
+        while n.sum() < T:
+            n[order[i % U]] += 1
+            i += 1
+        while n.sum() > T:
+            j = int(np.argmax(np.where(n > 2, n - raw, -np.inf)))
+            n[j] -= 1
+        lib = _lib.load()
+        plan = np.zeros(int(lib.ckv_decode_wp_plan_ints(n_cta)), dtype=np.int32)
+        seq = np.ascontiguousarray(self.seq_host[b0:b1], dtype=np.int32)
+        nw = np.ascontiguousarray(n, dtype=np.int32)
+        ms, mc = ctypes.c_int32(0), ctypes.c_int32(0)
+        st = lib.ckv_decode_wp_plan(seq.ctypes.data, b1 - b0, self.H, nw.ctypes.data, n_cta,
+                                    plan.ctypes.data, ctypes.byref(ms), ctypes.byref(mc))
+        if st != 0:
+            return None, None
+        return (torch.from_numpy(plan).to(self.device), n_cta, ms.value, mc.value), n
+
+    def _wp_workspace(self, m, layers, layer, max_ctas, seqs=None):
         sid = torch.cuda.current_stream(self.device).cuda_stream
-        wkey = ("wp", m, layers, layer, sid)
+        b0, b1 = (0, self.B) if seqs is None else seqs
+        wkey = ("wp", m, layers, layer, b0, b1, sid)
         hit = self._ws_ptr.get(wkey)
         if hit is not None:
             return hit
         lib = _lib.load()
-        per = lib.ckv_decode_wp_workspace_bytes(layers, self.B, self.H, m, max_ctas)
+        per = lib.ckv_decode_wp_workspace_bytes(layers, b1 - b0, self.H, m, max_ctas)
         per = -(-per // 256) * 256
-        key = ("wp", m, layers, sid)
+        key = ("wp", m, layers, b0, b1, sid)
         nbytes = per * (self.L if layers == 1 else 1)
         if key not in self._ws:
             self._ws[key] = torch.zeros(max(nbytes // 4, 1), dtype=torch.float32, device=self.device)
@@ -256,14 +265,15 @@ class BatchedKVCache:
 
     def _use_wp(self, m, seqs, splits, schedule):
         sched = self.schedule if schedule is None else schedule
-        if sched == "split" or seqs is not None or splits is not None or m > MAX_Q_PER_KV:
+        if sched == "split" or splits is not None or m > MAX_Q_PER_KV:
             return None
-        if sched == "auto" and (self._tiles_per_warp() < 8 or self._fp16_byte_share() > 0.5):
+        frac = 1.0 if seqs is None else (seqs[1] - seqs[0]) / max(self.B, 1)
+        if sched == "auto" and (self._tiles_per_warp() * frac < 8 or self._fp16_byte_share() > 0.5):
             # small caches (a few tiles per warp): the split schedule's latency wins; mostly-FP16
             # caches are HBM bound, where SMs stream at unequal rates and the split schedule's
             # waves of CTAs rebalance dynamically (cfg4 all-FP16: split 6375 vs warp plan 5823 GB/s)
             return None
-        return self.warp_plan()
+        return self.warp_plan(seqs)
 
     def _fp16_byte_share(self):
         s = self.seq_host.astype(np.float64)
@@ -339,14 +349,15 @@ class BatchedKVCache:
                 out.view(L, B, self.H, m, D)[:, b0:b1, :, r0:r1] = og.view(L, B, self.H, r1 - r0, D)[:, b0:b1]
             return out
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
-        plan = self._use_wp(m, None if (b0, b1) == (0, B) else seqs, splits, schedule)
+        rng = None if (b0, b1) == (0, B) else (b0, b1)
+        plan = self._use_wp(m, rng, splits, schedule) if b1 > b0 else None
         if plan is not None:
             prefix, ctas, slots, max_ctas = plan
-            ws = self._wp_workspace(m, L, layer, max_ctas)
-            _lib.call("ckv_decode_attention_wp", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k", layer),
-                      self.arena("v", layer), _lib.ptr(self.seq), L, B, self.H, m, scale, _lib.ptr(prefix), ctas,
-                      slots, max_ctas, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
-                      _lib.DECODE_PDL if pdl else 0, _lib.stream())
+            ws = self._wp_workspace(m, L, layer, max_ctas, rng)
+            _lib.call("ckv_decode_attention_wp_seqs", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k", layer),
+                      self.arena("v", layer), _lib.ptr(self.seq), L, B, b0, b1 - b0, self.H, m, scale,
+                      _lib.ptr(prefix), ctas, slots, max_ctas, ws, _lib.ptr(out), out.stride(0), out.stride(1),
+                      None, _lib.DECODE_PDL if pdl else 0, _lib.stream())
             return out
         splits = self.default_splits(m, L) if splits is None else int(splits)
         ws = self._workspace(m, splits, L, layer)

@@ -457,10 +457,53 @@ template <int BITS>
 __device__ __forceinline__ const char* tile_base(const DecArgs& a, const TileSrc& o) {
   return BITS == 2 ? reinterpret_cast<const char*>(a.K.codes2) + o.c2 : reinterpret_cast<const char*>(a.K.codes4) + o.c4;
 }
+// Ring synchronisation.  Default: 16-byte cp.async per lane, one commit group per stage, the
+// consumer waits for all but the kStages-2 youngest groups.  CKV_DEC_BULK: one lane issues the
+// whole contiguous tile as ONE bulk copy (cp.async.bulk, the 1-D TMA path) completing on the
+// stage's mbarrier (expect_tx of the tile bytes); the consumer waits on that mbarrier's phase.
+// The warp's kStages mbarriers live in a file-scope shared array (both decode kernels).
+#ifndef CKV_DEC_BULK
+#define CKV_DEC_BULK 0
+#endif
+#if CKV_DEC_BULK
+__shared__ __align__(8) uint64_t g_ring_mbar[16][4];
+__device__ __forceinline__ uint32_t ring_mbar(int slot) {
+  return (uint32_t)__cvta_generic_to_shared(&g_ring_mbar[threadIdx.x >> 5][slot]);
+}
+__device__ __forceinline__ void ring_init() {  // whole warp, before its first issue
+  if ((threadIdx.x & 31) < 4)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ring_mbar(threadIdx.x & 31)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+}
+__device__ __forceinline__ void ring_wait(int slot, uint32_t& ph) {
+  const uint32_t mb = ring_mbar(slot), par = (ph >> slot) & 1u;
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(mb), "r"(par) : "memory");
+  ph ^= 1u << slot;
+}
+#else
+__device__ __forceinline__ void ring_init() {}
+#endif
+
 template <int BITS>
-__device__ __forceinline__ void issue_at(int t, int n, const char* base, uint32_t sl) {
+__device__ __forceinline__ void issue_at(int t, int n, const char* base, uint32_t sl, int slot) {
+  constexpr int kB = BITS == 2 ? kBlock2 : kBlock4;
+#if CKV_DEC_BULK
+  // lane 0's stage slot and source are the tile's first bytes (both carry + 16 lane)
+  if (t < n && (threadIdx.x & 31) == 0) {
+    const char* p = base + (int64_t)t * kB;
+    const uint32_t mb = ring_mbar(slot);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "n"(kB) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sl), "l"(p), "n"(kB), "r"(mb) : "memory");
+  }
+#else
+  (void)slot;
   if (t < n) {
-    const char* p = base + (int64_t)t * (BITS == 2 ? kBlock2 : kBlock4);
+    const char* p = base + (int64_t)t * kB;
     cp_async16(sl, p);
     cp_async16(sl + 512, p + 512);
     cp_async16(sl + 1024, p + 1024);
@@ -470,6 +513,7 @@ __device__ __forceinline__ void issue_at(int t, int n, const char* base, uint32_
     }
   }
   cp_commit();
+#endif
 }
 
 // Prologue of a phase: put this warp's first kStages-1 tiles of the range in flight.
@@ -478,7 +522,8 @@ __device__ __forceinline__ void prologue(int n, const DecArgs& a, const TileSrc&
                                          int stride = kDecWarps) {
   const char* base = tile_base<BITS>(a, src);
 #pragma unroll
-  for (int s = 0; s < Ring<BITS>::stages - 1; ++s) issue_at<BITS>(warp + stride * s, n, base, ring_l + s * Ring<BITS>::bytes);
+  for (int s = 0; s < Ring<BITS>::stages - 1; ++s)
+    issue_at<BITS>(warp + stride * s, n, base, ring_l + s * Ring<BITS>::bytes, s);
 }
 
 // Per-unit operand scaling of a warp (E: q, F: V; see "operand scaling").
@@ -493,10 +538,20 @@ struct UnitScale {
 template <int BITS>
 __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc& src, const LaneOff& lo,
                                           uint32_t ring_l, const QS& qs, const UnitScale& us,
-                                          WarpState& st, int warp, int stride = kDecWarps) {
+                                          WarpState& st, int warp, uint32_t& ph, int stride = kDecWarps) {
   constexpr int kStages = Ring<BITS>::stages, kStageBytes = Ring<BITS>::bytes;
   const uint32_t ring_end = ring_l + kStages * kStageBytes;
   auto next = [&](uint32_t x) { return x + kStageBytes == ring_end ? ring_l : x + kStageBytes; };
+  auto nslot = [](int x) { return x + 1 == kStages ? 0 : x + 1; };
+  auto wait = [&](int slot) {
+#if CKV_DEC_BULK
+    ring_wait(slot, ph);
+#else
+    (void)slot;
+    cp_wait<kStages - 2>();
+    __syncwarp();
+#endif
+  };
   int t = warp;
   const int64_t kStep = (int64_t)stride * (BITS == 2 ? kBlock2 : kBlock4);
   // address of the next tile to issue (kStages-1 ahead of the one consumed), advanced by one
@@ -506,34 +561,38 @@ __device__ __forceinline__ void run_tiles(int n, const DecArgs& a, const TileSrc
   const uint32_t f2 = h2_as_u32(__float2half2_rn(exp2f((float)us.F)));
   if (t < n) {
     uint32_t cur = ring_l, put = ring_l + (kStages - 1) * kStageBytes;
-    cp_wait<kStages - 2>();
-    __syncwarp();
+    int cs = 0, ps = kStages - 1;
+    wait(cs);
     float s0[4];
     qk_tile<BITS>(cur, lo, qs, kappa, s0);
     uint32_t bp0, bp1;
     softmax_tile<false>(s0, st, bp0, bp1);
     while (true) {
       const int tn = t + stride;
-      issue_at<BITS>(t + stride * (kStages - 1) < n ? 0 : 1, 1, pn, put);
+      issue_at<BITS>(t + stride * (kStages - 1) < n ? 0 : 1, 1, pn, put, ps);
       pn += kStep;
       if (tn >= n) {
         pv_tile<BITS>(cur, lo, st, bp0, bp1, f2);
         break;
       }
-      cp_wait<kStages - 2>();
-      __syncwarp();
       const uint32_t nx = next(cur);
+      const int ns = nslot(cs);
+      wait(ns);
       float sn[4];
       qk_tile<BITS>(nx, lo, qs, kappa, sn);
       pv_tile<BITS>(cur, lo, st, bp0, bp1, f2);
       __syncwarp();  // slot `cur` (and the scratch) may be refilled from now on
       softmax_tile<false>(sn, st, bp0, bp1);
       put = cur;  // the refill slot trails the consumed one by a full ring (kStages - 1 ahead)
+      ps = cs;
       cur = nx;
+      cs = ns;
       t = tn;
     }
   }
+#if !CKV_DEC_BULK
   cp_wait<0>();
+#endif
 }
 
 // Both phases of a CTA's quantized tiles: INT2 (its prologue issued before the PDL wait), then
@@ -548,12 +607,13 @@ __device__ __forceinline__ void quantized_tiles(int n2, int n4, const DecArgs& a
                                                 const LaneOff& lo, uint32_t ring_l, const QS& qs,
                                                 const UnitScale& us, WarpState& st, int warp,
                                                 int stride = kDecWarps) {
+  uint32_t ph = 0u;  // mbarrier phase parity per ring slot (bulk-copy ring)
   // the INT4 phase starts at the warp after the one that took the last INT2 tile, so every
   // warp's tile count over both phases is within one of the others' (the CTA's warps meet at
   // the merge barrier)
   const int w4 = rotate(warp, n2, stride);
   if (n2 > 0) {
-    run_tiles<2>(n2, a, src, lo, ring_l, qs, us, st, warp, stride);
+    run_tiles<2>(n2, a, src, lo, ring_l, qs, us, st, warp, ph, stride);
     if (n4 > 0) {
       __syncwarp();
       prologue<4>(n4, a, src, ring_l, w4, stride);
@@ -566,7 +626,7 @@ __device__ __forceinline__ void quantized_tiles(int n2, int n4, const DecArgs& a
 #pragma unroll
     for (int e = 0; e < 4; ++e) f[e] = w4w[e] / w2[e];
     scale_acc(st, f);
-    run_tiles<4>(n4, a, src, lo, ring_l, qs, us, st, w4, stride);
+    run_tiles<4>(n4, a, src, lo, ring_l, qs, us, st, w4, ph, stride);
 #pragma unroll
     for (int e = 0; e < 4; ++e) f[e] = 1.0f / w4w[e];
   } else {
@@ -746,6 +806,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     src.c4 = (unit * a.K.rows4 + r4) / kTileRows * kBlock4 + 16 * lane;
   }
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0]) + 16 * lane;
+  ring_init();
   if (cnt2 > 0) prologue<2>(cnt2, a, src, ring_l, warp);
   else prologue<4>(nloc, a, src, ring_l, warp);
 
@@ -1018,7 +1079,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   const int k = r0.y & 0xffff, np = r0.y >> 16;  // this warp's index among the part's np warps
   const int w_lo = r1.z & 0xffff, w_hi = r1.z >> 16, nw = r1.w;
   const int slot = u - u0;
-  const int b = u / a.H, h = u - b * a.H;
+  const int b = a.b0 + u / a.H, h = u % a.H;  // units of this launch: sequences [b0, b0 + Bc)
   const int n2t = r0.z, n4t = r0.w;
   TileSrc src;
   {
@@ -1027,6 +1088,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     src.c4 = (unit * a.K.rows4 + r1.y) / kTileRows * kBlock4 + 16 * lane;
   }
   const uint32_t ring_l = (uint32_t)__cvta_generic_to_shared(&s_ring[warp][0]) + 16 * lane;
+  ring_init();
   if (n2t > 0) prologue<2>(n2t, a, src, ring_l, k, np);
   else prologue<4>(n4t, a, src, ring_l, k, np);
   UnitScale us;
@@ -1061,7 +1123,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
         stage_q_part(qv, j & 3, us.E, s_qall + (j >> 2) * kQBytes, lane);
       } else {
         float qj[32];
-        load_q_rows(a, l, uj / a.H, uj % a.H, g, c, qj);
+        load_q_rows(a, l, a.b0 + uj / a.H, uj % a.H, g, c, qj);
         stage_q_part(qj, j & 3, unit_q_exponent(qj), s_qall + (j >> 2) * kQBytes, lane);
       }
     }
@@ -1175,7 +1237,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
 #pragma unroll
     for (int k = 0; k < 4; ++k) o4[k] = ac[k ^ sw];
     if (si.z == si.w) {
-      const int us = u0 + sl, bs = us / a.H, hs = us - bs * a.H;
+      const int us = u0 + sl, bs = a.b0 + us / a.H, hs = us % a.H;
       const int64_t row = ((int64_t)l * a.B + bs) * Hq + hs * a.m + qi;
       if (a.partial_out) {
         float* dst = a.partial_out + row * kPartStride;
@@ -1266,7 +1328,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     const int4 si = s_slot[sl];
     if (!s_do[sl]) continue;
     const int us = u0 + sl, nc = si.w - si.z + 1;
-    const int bs = us / a.H, hs = us - bs * a.H;
+    const int bs = a.b0 + us / a.H, hs = us % a.H;
     const float* src_p = ws_l + (int64_t)us * w.max_ctas * a.m * kWsStride;  // [ctas][m][stride]
     {
       const float* own = s_own(sl) + qi * kWsStride;
@@ -1550,13 +1612,26 @@ int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_
                                 const int32_t* plan, int32_t ctas, int32_t max_slots,
                                 int32_t max_ctas, void* workspace, uint16_t* out, int64_t o_s_layer,
                                 int64_t o_s_batch, float* partial_out, int32_t flags, void* stream) {
+  return ckv_decode_attention_wp_seqs(q, q_s_layer, q_s_batch, k_arena, v_arena, seq, layers, batch, 0, batch,
+                                      kv_heads, m, scale, plan, ctas, max_slots, max_ctas, workspace, out,
+                                      o_s_layer, o_s_batch, partial_out, flags, stream);
+}
+
+int32_t ckv_decode_attention_wp_seqs(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                                     ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                                     int32_t layers, int32_t batch, int32_t b0, int32_t n_seqs,
+                                     int32_t kv_heads, int32_t m, float scale, const int32_t* plan,
+                                     int32_t ctas, int32_t max_slots, int32_t max_ctas, void* workspace,
+                                     uint16_t* out, int64_t o_s_layer, int64_t o_s_batch,
+                                     float* partial_out, int32_t flags, void* stream) {
   if (layers < 0 || batch < 0 || kv_heads < 0 || ctas < 1) return CKV_ERR_ARG;
+  if (b0 < 0 || n_seqs < 0 || b0 + n_seqs > batch) return CKV_ERR_ARG;
   if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (max_slots < 1 || max_slots > 8 || max_ctas < 1) return CKV_ERR_UNSUPPORTED;
   if (!q || !seq || !plan || !workspace || (!out && !partial_out)) return CKV_ERR_ARG;
   if ((q_s_layer % 8) || (q_s_batch % 8) || (o_s_layer % 8) || (o_s_batch % 8)) return CKV_ERR_UNSUPPORTED;
   if (out && (reinterpret_cast<uintptr_t>(out) & 15)) return CKV_ERR_UNSUPPORTED;
-  if (layers * batch * kv_heads == 0) return CKV_OK;
+  if (layers * n_seqs * kv_heads == 0) return CKV_OK;
   {
     const char* k2 = reinterpret_cast<const char*>(k_arena.codes2);
     const char* k4 = reinterpret_cast<const char*>(k_arena.codes4);
@@ -1576,16 +1651,16 @@ int32_t ckv_decode_attention_wp(const uint16_t* q, int64_t q_s_layer, int64_t q_
   a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
   a.K = k_arena; a.V = v_arena; a.seq = seq;
   a.L = layers; a.B = batch; a.H = kv_heads; a.m = m; a.splits = 1;
-  a.b0 = 0; a.Bc = batch;
+  a.b0 = b0; a.Bc = n_seqs;
   a.scale_log2 = scale * 1.4426950408889634f;
-  const int64_t units = (int64_t)layers * batch * kv_heads;
+  const int64_t units = (int64_t)layers * n_seqs * kv_heads;
   a.counters = reinterpret_cast<uint32_t*>(workspace);
   a.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + cdiv(2 * units * (int64_t)sizeof(uint32_t), 256) * 256);
   a.out = out; a.o_sl = o_s_layer; a.o_sb = o_s_batch;
   a.partial_out = partial_out;
   a.trace = g_trace_host;
   w.plan = plan;
-  w.U = batch * kv_heads;
+  w.U = n_seqs * kv_heads;  // the plan's units: sequences [b0, b0 + n_seqs) x kv heads
   w.max_slots = max_slots;
   w.max_ctas = max_ctas;
   const size_t smem = (size_t)kWpWarps * kWarpRing + (size_t)max_slots * kQBytes;

@@ -1,5 +1,5 @@
 """The warp-plan decode schedule (ckv_decode_attention_wp: one 16-warp CTA per SM, units split
-at warp granularity, multi-CTA units merged by the last CTA to arrive) against the reference
+at warp granularity, multi-CTA units merged in the launch) against the reference
 algorithm (oracle) and against the split schedule, on unit counts from a few (many CTAs per
 unit) to many (several units per CTA), with m = 1 / 4 / 8, decode tokens, partials, per-layer
 PDL launches and CUDA-graph replay."""
@@ -90,6 +90,42 @@ def test_warp_plan_per_layer_graph_and_appends():
         torch.cuda.synchronize()
         assert torch.equal(out, want)   # deterministic: graph replay == eager, bit for bit
         assert torch.equal(cache.decode(qd), want)
+
+
+@pytest.mark.parametrize("chains", [2, 3])
+def test_warp_plan_micro_batch_chains(chains):
+    """Sequence-range launches of the warp plan (ckv_decode_attention_wp_seqs): each range has
+    its own plan and workspace; a decode step as `chains` micro-batch chains of per-layer PDL
+    launches on their own streams (one CUDA graph) equals the whole-batch per-layer step bit for
+    bit per sequence range's own plan, meets the oracle, and leaves other rows untouched."""
+    L, B, H, m = 2, 5, 4, 4
+    cache, k, v, q, tiers = _case(400 + chains, L, B, H, m, 40, 9)
+    qd = torch.from_numpy(q).cuda()
+    ranges = cache._chain_ranges(chains)
+    for r in ranges:
+        assert cache.warp_plan(r) is not None and cache._use_wp(m, r, None, None) is not None
+    # one range alone: rows outside it untouched
+    sentinel = torch.full_like(qd, 7.0)
+    b0, b1 = ranges[1]
+    cache.decode(qd, out=sentinel, seqs=(b0, b1))
+    sn = sentinel.float().cpu().numpy()
+    assert (sn[:, :b0] == 7.0).all() and (sn[:, b1:] == 7.0).all()
+    _check(sn, k, v, q, tiers, m, [(l, b, h) for l in range(L) for b in range(b0, b1) for h in range(H)])
+    # the chained per-layer graph
+    out = torch.empty_like(qd)
+    g = cache.decode_graph(qd, out, chains=chains)
+    g.replay()
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for (r0, r1) in ranges:
+        want = torch.empty_like(qd)
+        for l in range(L):
+            cache.decode(qd[l:l + 1], out=want[l:l + 1], layer=l, pdl=l > 0, seqs=(r0, r1))
+        torch.cuda.synchronize()
+        assert torch.equal(out[:, r0:r1], want[:, r0:r1])
+    _check(got, k, v, q, tiers, m, [(l, b, h) for l in range(L) for b in range(B) for h in range(H)])
+    whole = cache.decode(qd).float().cpu().numpy()
+    assert np.max(np.abs(whole - got)) < SCHED_TOL
 
 
 def test_warp_plan_outlier_precise_and_exact_units():
