@@ -283,7 +283,7 @@ def pick_splits(args, cache, m, layers=1):
     first = None if chains == 1 else cache._chain_ranges(chains)[0]
     if args.schedule != "split" and args.splits is None and cache._use_wp(m, first, None, None) is not None:
         return None
-    return args.splits or cache.default_splits(m, layers)
+    return args.splits or (cache.default_splits(m, layers) if chains == 1 else cache.chain_splits(m))
 
 
 def launch_desc(chains):
@@ -301,7 +301,10 @@ def schedule_desc(cache, splits, chains=1):
         if chains > 1:
             desc += f"; {chains} micro-batch chains, each its own warp plan per launch"
         return desc
-    return f"split: {splits} CTAs of 4 warps per unit"
+    desc = f"split: {splits} CTAs of 4 warps per unit"
+    if chains > 1:
+        desc += f"; {chains} micro-batch chains of {cache.B // chains} sequence(s), launches of {cache.B // chains * cache.H * splits} CTAs"
+    return desc
 
 
 def build_cfg2(torch, dev, rank):
@@ -937,11 +940,14 @@ def main():
                     help="decode schedule of whole-batch launches: wp = warp plan (one 16-warp CTA per SM, "
                          "units split at warp granularity), split = 4-warp CTAs with --splits per unit, "
                          "auto = the warp plan unless the cache has fewer than 8 tiles per warp")
-    ap.add_argument("--chains", type=int, default=1,
+    ap.add_argument("--chains", type=int, default=0,
                     help="micro-batch chains per decode step (cfg2/cfg4): the batch is split into this "
                          "many sequence ranges, each its own chain of per-layer launches on its own "
-                         "stream, so one range's layer boundary overlaps the others' work")
+                         "stream, so one range's layer boundary overlaps the others' work; 0 (default) = "
+                         "one chain per sequence for cfg2, 1 for the other workloads")
     args = ap.parse_args()
+    if args.chains == 0 and args.workload != "cfg2":
+        args.chains = 1
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # launched without torchrun: start one rank per GPU ourselves (127.0.0.1 rendezvous)
@@ -1000,6 +1006,8 @@ def main():
     cache, q, search = build_cfg2(torch, dev, rank)
     L, B = cache.L, cache.B
     m = q.shape[2] // cache.H
+    if args.chains == 0:
+        args.chains = B  # one micro-batch chain per sequence
     splits = pick_splits(args, cache, m)
     wp = splits is None
     out = torch.empty_like(q)
@@ -1070,6 +1078,33 @@ def main():
     torch.cuda.synchronize()
     eager_gbs = world * step_bytes / (e6.elapsed_time(e7) / args.steps * 1e-3) / 1e9
 
+    # lockstep figure: the whole batch as ONE chain of per-layer launches (every layer waits for
+    # the previous layer of every sequence), the schedule the cache would pick for it
+    lockstep = None
+    if args.chains > 1:
+        ls_args = argparse.Namespace(**{**vars(args), "chains": 1})
+        ls_splits = pick_splits(ls_args, cache, m)
+        ls_graph = cache.decode_graph(q, out, splits=ls_splits)
+        for _ in range(3):
+            ls_graph.replay()
+        torch.cuda.synchronize()
+        barrier()
+        e10, e11 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e10.record()
+        for _ in range(args.steps):
+            ls_graph.replay()
+        e11.record()
+        torch.cuda.synchronize()
+        ls_ms = e10.elapsed_time(e11) / args.steps
+        if world > 1:
+            t = torch.tensor([ls_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ls_ms = float(t.item())
+        lockstep = {"value": round(world * step_bytes / (ls_ms * 1e-3) / 1e9, 2), "ms_per_step": round(ls_ms, 4),
+                    "launch": launch_desc(1), "schedule": schedule_desc(cache, ls_splits)}
+        del ls_graph
+        cache.schedule = args.schedule
+
     # single-launch (all 32 layers in one grid) figure for the same cache
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     single_splits = args.splits or cache.default_splits(m, L)  # split schedule: the faster one in one launch
@@ -1118,9 +1153,9 @@ def main():
         tpot = {"steps": n_tok, "ms_per_token": round(tp_ms, 4),
                 "tokens_per_s": round(world * B / (tp_ms * 1e-3), 1),
                 "gbs": round(world * mean_bytes / (tp_ms * 1e-3) / 1e9, 2),
-                "note": "batched.DecodeLoop: per step ckv_append_tokens (one new K/V row per unit) + 32 "
-                        "PDL-chained per-layer decode launches, one CUDA graph replay; the context grows "
-                        f"from {CFG2['context']} to {CFG2['context'] + n_tok} tokens"}
+                "note": "batched.DecodeLoop: per step ckv_append_tokens (one new K/V row per unit) + the "
+                        f"per-layer decode launches ({launch_desc(args.chains)}), one CUDA graph replay; the "
+                        f"context grows from {CFG2['context']} to {CFG2['context'] + n_tok} tokens"}
         del kn, vn, loop
 
     split_kv = None
@@ -1147,9 +1182,9 @@ def main():
 
     if rank == 0:
         peak, peak_kind = measured_peak_gbs()
-        per_launch_bytes = step_bytes / L
-        achieved = per_launch_bytes / (ms * 1e-3 / L) / 1e9 / 1.0
-        launches_per_step = L  # split merge happens inside the decode launch
+        launches_per_step = L * args.chains  # the split merge happens inside the decode launch
+        per_launch_bytes = step_bytes / launches_per_step
+        achieved = per_launch_bytes / (ms * 1e-3 / launches_per_step) / 1e9
         counts = search.seg_counts.cpu().numpy()
         frac = counts.sum(axis=0) / counts.sum()
         line = {
@@ -1167,9 +1202,10 @@ def main():
             "algorithmic_bytes_per_step": step_bytes,
             "eager_launches_gbs": round(eager_gbs, 2),
             "single_launch_all_layers_gbs": round(fused_gbs, 2),
+            "lockstep_per_layer": lockstep,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                         "traffic": profile_traffic("decode_kernel")},
+                         "traffic": profile_traffic("decode_kernel" if args.chains == 1 else "decode_kernel_chain")},
             "e2e": {"value": round(e2e_gbs, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": int(q.numel() * 2), "d2h_bytes_per_step": int(q.numel() * 2)},
             "gpu_launches": args.steps * launches_per_step,

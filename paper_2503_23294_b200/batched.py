@@ -197,6 +197,18 @@ class BatchedKVCache:
                 best, best_cost = s, cost
         return best
 
+    def chain_splits(self, m):
+        """Split-KV factor for micro-batch chains (concurrent per-range launches): the chains'
+        launches together should slightly oversubscribe the resident CTA slots (~1.05x: CTAs of
+        a later wave fill the gaps other chains' tails leave), with >= 16 tiles per CTA."""
+        units = self.B * self.H
+        slots = _num_sms() * max(_lib.load().ckv_decode_ctas_per_sm(), 1)
+        tiles = int(max(1, (self.total_tokens().max() + TILE - 1) // TILE))
+        s = max(1, min(64, -(-int(1.05 * slots) // max(units, 1))))
+        while s > 1 and tiles // s < 16:
+            s -= 1
+        return s
+
     def warp_plan(self, seqs=None):
         """Warp-plan schedule (ckv_decode_attention_wp): unit u = b*H + h gets n_u warps in
         proportion to its tile cost (INT2 1, INT4 1.06, FP16-region 2 per 16-token tile), at

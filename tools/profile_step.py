@@ -1,4 +1,7 @@
-"""One cfg2 decode step (+ optional cfg5 prefill build) for ncu captures; prints nothing measured."""
+"""One cfg2 decode step (+ optional cfg5 prefill build) for ncu captures; prints nothing measured.
+--chains 0 (default) runs the step as bench.py's default does: one micro-batch chain per
+sequence, each its own sequence of per-layer launches (split schedule, chain_splits); --chains 1
+the lockstep whole-batch per-layer launches (the cache's schedule)."""
 import argparse
 import os
 import sys
@@ -18,21 +21,22 @@ def main():
     ap.add_argument("--prefill", action="store_true")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--schedule", choices=["auto", "wp", "split"], default="auto")
+    ap.add_argument("--chains", type=int, default=0)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     bench.CFG2["layers"] = args.layers
     cache, q, _ = bench.build_cfg2(torch, dev, 0)
     m = q.shape[2] // cache.H
-    splits = None if args.schedule != "split" else cache.default_splits(m, 1)  # None: the cache's schedule
-    cache.schedule = args.schedule
+    chains = cache.B if args.chains == 0 else args.chains
+    ns = argparse.Namespace(schedule=args.schedule, splits=None, chains=chains)
+    splits = bench.pick_splits(ns, cache, m)  # None: the warp plan
     out = torch.empty_like(q)
-    for l in range(cache.L):  # warm-up outside the profiled range
-        cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(chains)]
+    cache._launch_layers(q, out, 0, cache.L, splits, None, chains, streams)  # warm-up outside the range
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     for _ in range(args.steps):
-        for l in range(cache.L):
-            cache.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], layer=l, pdl=l > 0)
+        cache._launch_layers(q, out, 0, cache.L, splits, None, chains, streams)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     if args.prefill:

@@ -106,14 +106,18 @@ def main():
              "(`tools/gpu_round.sh`); one launch each.  Launch list: "
              f"`{tag}_launches.csv` (`--metrics gpu__time_duration.sum`).", ""]
     traffic = {}
-    for rep, key in (("decode_prof.ncu-rep", "decode_kernel"), ("decode_split_prof.ncu-rep", "decode_kernel_split"),
-                     ("quant_prof.ncu-rep", "reorder_quantize_pack")):
+    for rep, key, what in (
+            ("decode_chain_prof.ncu-rep", "decode_kernel_chain",
+             "the bench default: one (sequence, layer) launch of the split schedule in a micro-batch chain"),
+            ("decode_prof.ncu-rep", "decode_kernel", "one lockstep per-layer launch (whole batch, warp plan)"),
+            ("decode_split_prof.ncu-rep", "decode_kernel_split", "one lockstep per-layer launch (whole batch, split)"),
+            ("quant_prof.ncu-rep", "reorder_quantize_pack", "the cfg5 build (128K x 32 layers x 8 heads)")):
         path = os.path.join(OUT, rep)
         if not os.path.exists(path):
             continue
         name, metrics, stalls, opmix, dram = summarize(path)
         traffic[key] = dram
-        lines += [f"## {name}", "", "| metric | value |", "|---|---|"]
+        lines += [f"## {name}", "", f"{what}.", "", "| metric | value |", "|---|---|"]
         lines += [f"| {k} | {v} |" for k, v in metrics.items()]
         lines += ["", "Stall mix (sampled): " + ", ".join(f"{k} {x:.1f}%" for k, x in stalls), "",
                   "Dynamic opcode mix: " + ", ".join(f"{k} {x:.1f}%" for k, x in opmix), ""]
