@@ -286,6 +286,12 @@ def pick_splits(args, cache, m, layers=1):
     return args.splits or (cache.default_splits(m, layers) if chains == 1 else cache.chain_splits(m))
 
 
+def auto_chains(batch):
+    """Micro-batch chains of a decode step: up to 8 sequence ranges (one per sequence for the
+    cfg2 batch of 8), each its own chain of per-layer launches on its own stream."""
+    return max(1, min(int(batch), 8))
+
+
 def launch_desc(chains):
     if chains == 1:
         return "per-layer (32 PDL-chained launches per step, replayed as one CUDA graph)"
@@ -695,6 +701,8 @@ def run_cfg4(args, torch, dist, dev, rank, world, local):
     g.manual_seed(11 + rank)
     q = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
     out = torch.empty_like(q)
+    if args.chains == 0:
+        args.chains = auto_chains(B)
     splits = pick_splits(args, cache, m)
     my_bytes = cache.algorithmic_bytes(m)
 
@@ -946,7 +954,7 @@ def main():
                          "stream, so one range's layer boundary overlaps the others' work; 0 (default) = "
                          "one chain per sequence for cfg2, 1 for the other workloads")
     args = ap.parse_args()
-    if args.chains == 0 and args.workload != "cfg2":
+    if args.chains == 0 and args.workload not in ("cfg2", "cfg4"):
         args.chains = 1
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -1007,7 +1015,7 @@ def main():
     L, B = cache.L, cache.B
     m = q.shape[2] // cache.H
     if args.chains == 0:
-        args.chains = B  # one micro-batch chain per sequence
+        args.chains = auto_chains(B)
     splits = pick_splits(args, cache, m)
     wp = splits is None
     out = torch.empty_like(q)

@@ -279,8 +279,12 @@ class BatchedKVCache:
         sched = self.schedule if schedule is None else schedule
         if sched == "split" or splits is not None or m > MAX_Q_PER_KV:
             return None
-        frac = 1.0 if seqs is None else (seqs[1] - seqs[0]) / max(self.B, 1)
-        if sched == "auto" and (self._tiles_per_warp() * frac < 8 or self._fp16_byte_share() > 0.5):
+        if sched == "auto" and seqs is not None and tuple(seqs) != (0, self.B):
+            # a micro-batch chain's range: its launches run beside the other chains' launches,
+            # which the one-CTA-per-SM warp plan cannot share SMs with (cfg2, 8 chains: split
+            # 4641 vs warp plan 2907-3732 GB/s); the split schedule's 4-warp CTAs interleave
+            return None
+        if sched == "auto" and (self._tiles_per_warp() < 8 or self._fp16_byte_share() > 0.5):
             # small caches (a few tiles per warp): the split schedule's latency wins; mostly-FP16
             # caches are HBM bound, where SMs stream at unequal rates and the split schedule's
             # waves of CTAs rebalance dynamically (cfg4 all-FP16: split 6375 vs warp plan 5823 GB/s)
