@@ -86,3 +86,58 @@ def test_memory_footprint_matches_reference_accounting():
     assert rep.fp16_bytes == units * 512 * int((32 * cnt[:, 2] + 5 + 1).sum())
     assert rep.fp16_baseline_bytes == units * 512 * B * (T + 1)
     assert 0 < rep.compression_ratio < rep.reference.compression_ratio
+
+
+def test_bench_default_step_one_chain_per_sequence():
+    """The bench's default decode step: one micro-batch chain per sequence (per-layer PDL launches
+    on their own streams, one CUDA graph), auto schedule (chained ranges run the split kernel)
+    with chain_splits.  Every unit meets the oracle; each chain equals its eager per-range
+    launches bit for bit; decode_step_host (pinned host buffers) and DecodeLoop with the same
+    chains give the same rows."""
+    rng = np.random.default_rng(97)
+    L, B, H, m, D, N = 2, 4, 2, 4, 128, 30
+    T = N * 32 + 5
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    q = rng.normal(size=(L, B, H * m, D)).astype(np.float16)
+    tiers = rng.choice([0, 0, 0, 1, 2], size=(B, N)).astype(np.uint8)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers),
+                                        decode_capacity=4)
+    assert cache.schedule == "auto"
+    splits = cache.chain_splits(m)
+    assert splits >= 1
+    for r in cache._chain_ranges(B):
+        assert cache._use_wp(m, r, None, None) is None  # chained ranges: the split kernel
+    qd = torch.from_numpy(q).cuda()
+    out = torch.empty_like(qd)
+    g = cache.decode_graph(qd, out, splits=splits, chains=B)
+    g.replay()
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for l in range(L):
+        for b in range(B):
+            for h in range(H):
+                oc = O.build_cache(k[l, b, :, h].astype(np.float64), v[l, b, :, h].astype(np.float64), tiers[b], 32, 32)
+                ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+                err = np.max(np.abs(got[l, b, h * m:(h + 1) * m] - ref))
+                assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (l, b, h, err)
+    want = torch.empty_like(qd)
+    for b in range(B):
+        for l in range(L):
+            cache.decode(qd[l:l + 1], splits=splits, out=want[l:l + 1], layer=l, pdl=l > 0, seqs=(b, b + 1))
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+    qh = qd.cpu().pin_memory()
+    oh = torch.empty(qh.shape, dtype=torch.float16, pin_memory=True)
+    cache.decode_step_host(qh, oh, splits=splits, chains=B)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, want.cpu())
+    loop = batched.DecodeLoop(cache, m, splits=splits, chains=B)
+    kn = torch.zeros((L, B, H, D), dtype=torch.float16, device="cuda")
+    step = loop.step(qd, kn, kn).float().cpu().numpy()  # one appended zero key/value per unit
+    for (l, b, h) in ((0, 0, 0), (L - 1, B - 1, H - 1)):
+        oc = O.build_cache(k[l, b, :, h].astype(np.float64), v[l, b, :, h].astype(np.float64), tiers[b], 32, 32)
+        oc.append(np.zeros(D), np.zeros(D))
+        ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+        err = np.max(np.abs(step[l, b, h * m:(h + 1) * m] - ref))
+        assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (l, b, h, err)
