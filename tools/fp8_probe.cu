@@ -1,4 +1,7 @@
-// Probe (tuning aid): mma.sync m16n8k32 e4m3 x e4m3 -> f32 on sm_100a.
+// Probe (tuning aid): mma.sync m16n8k32 e4m3 x e4m3 -> f32 on sm_100a.  Finding: NOT a native
+// tensor-core instruction there — ptxas lowers each one to 16 F2FP.F16.E4M3.UNPACK_B + 4
+// HMMA.16816 + 8 FADD (cuobjdump -sass of this binary); (1) below hoists the conversions of its
+// loop-invariant operands, so its "throughput" is not that of real code.
 //  (1) throughput against m16n8k16 f16 at 16 warps/SM, 8 independent accumulator chains;
 //  (2) precision: D = C + A.B with A = small integer codes as e4m3 bytes (c < 16 is exactly
 //      c * 2^-9), B random finite e4m3, C random fp32; compared with the exact sum in double.
