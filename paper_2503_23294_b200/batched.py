@@ -187,6 +187,11 @@ class BatchedKVCache:
         per_sm = _lib.load().ckv_decode_ctas_per_sm()
         slots = _num_sms() * max(per_sm, 1)
         tiles = int(max(1, (self.total_tokens().max() + TILE - 1) // TILE))
+        if units * tiles < 64 * _num_sms():
+            # latency regime (a few tiles per warp, e.g. cfg1's 15 MB): about two CTAs per SM —
+            # more splits add co-resident CTAs and merge work without adding bandwidth
+            # (cfg1: 8 / 12 / 16 splits 16.5 / 16.8 / 22.0 us)
+            return int(max(1, min(64, (2 * _num_sms()) // max(units, 1), tiles // 4)))
         best, best_cost = 1, None
         for s in range(1, 65):
             if s > 1 and tiles // s < 16:
