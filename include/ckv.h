@@ -222,6 +222,19 @@ int32_t ckv_append_tokens(const uint16_t* k_new, const uint16_t* v_new, int32_t 
 int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, double* scales,
                         double* zero_points, void* stream);
 
+/* kv_store.reconstruct + token_order (kv_store.py:227-253) on the tile-native arenas, on the
+ * device: every row of layers [0, layers) of the arena views (ckv_arena at a layer offset), all
+ * sequences and kv heads, dequantized as the reference's dequantize_codes does (zp + scale code
+ * in f64, _numpy.py:102-112; FP16-region rows widened) and written to its ORIGINAL token position
+ * t (the build permutation perm u32[batch][max_chunks]; the tail and decode tokens follow the
+ * chunks in order): out_k / out_v f64 elements at l s_layer + b s_batch + t s_token + h s_head +
+ * d (d contiguous); rows with t >= t_out are skipped.  max_rows = the largest len2 + len4 +
+ * len_fp over the sequences. */
+int32_t ckv_reconstruct(ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq, const uint32_t* perm,
+                        int32_t max_chunks, int32_t layers, int32_t batch, int32_t kv_heads, int32_t max_rows,
+                        double* out_k, double* out_v, int64_t s_layer, int64_t s_batch, int64_t s_token,
+                        int64_t s_head, int32_t t_out, void* stream);
+
 /* Tile-native arena rows -> reference format (export / verification, quantizer.py:20-57):
  * `rows` (a multiple of 16) rows starting at a tile boundary of one arena (codes + meta of
  * the K arena when is_v == 0, of the V arena otherwise; consecutive tiles `tile_stride` bytes

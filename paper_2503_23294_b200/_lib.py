@@ -75,6 +75,8 @@ _SIGNATURES = {
     "ckv_append_tokens": ([_vp, _vp, _i32, _i32, _i32, _vp, Arena, Arena, _vp], _i32),
     "ckv_expand_meta": ([_vp, _i64, _i32, _vp, _vp, _vp], _i32),
     "ckv_arena_export": ([_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp], _i32),
+    "ckv_reconstruct": ([Arena, Arena, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i64, _i64, _i64, _i64, _i32,
+                         _vp], _i32),
     "ckv_decode_workspace_bytes": ([_i32, _i32, _i32, _i32, _i32], _i64),
     "ckv_decode_ctas_per_sm": ([], _i32),
     "ckv_decode_attention": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _f32, _i32,

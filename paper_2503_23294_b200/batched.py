@@ -601,6 +601,43 @@ class BatchedKVCache:
         return int(((self.k["span_flags"] | self.v["span_flags"]) != 0).sum().item())
 
     # -- export to the reference per-head format ------------------------------------------
+    def token_order(self, seq):
+        """kv_store.token_order (kv_store.py:227-233) of one sequence: the original position of
+        every row in arena order (INT2 ‖ INT4 ‖ FP16 region)."""
+        s = self.seq_host[seq].astype(np.int64)
+        n_chunks = int(s[7]) // CHUNK
+        perm = self._build_perm()[seq].cpu().numpy().astype(np.int64)[:n_chunks]
+        chunks = (perm[:, None] * CHUNK + np.arange(CHUNK)[None, :]).reshape(-1)
+        n_after = int(s[1] + s[3] + s[5]) - n_chunks * CHUNK  # the tail, then the decode tokens
+        return np.concatenate([chunks, n_chunks * CHUNK + np.arange(n_after)]).astype(np.int64)
+
+    def _build_perm(self):
+        if getattr(self, "_perm", None) is None:
+            raise ValueError("cache was not built here: no build permutation")
+        return self._perm
+
+    def reconstruct(self, layer=0, layers=None, t_out=None):
+        """kv_store.reconstruct (kv_store.py:236-253) for the whole cache on the device: K and V
+        f64 [L', B, T_out, H, 128] of layers [layer, layer + L') in ORIGINAL token order (every
+        row dequantized as the reference's dequantize_codes does, FP16-region rows widened; the
+        tail and the decode tokens after the chunks), one launch (ckv_reconstruct).  T_out
+        defaults to the longest sequence's context + decode tokens; shorter sequences leave
+        their later rows zero."""
+        L = self.L - layer if layers is None else int(layers)
+        if layer < 0 or L < 0 or layer + L > self.L:
+            raise ValueError("layer range outside the cache")
+        total = self.total_tokens()  # rows = original positions (context + decode tokens)
+        T = (int(total.max()) if self.B else 0) if t_out is None else int(t_out)
+        shape = (L, self.B, T, self.H, HEAD_DIM)
+        ok = torch.zeros(shape, dtype=torch.float64, device=self.device)
+        ov = torch.zeros_like(ok)
+        perm = self._build_perm()
+        _lib.call("ckv_reconstruct", self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq),
+                  _lib.ptr(perm), perm.shape[1], L, self.B, self.H, int(total.max()) if self.B else 0,
+                  _lib.ptr(ok), _lib.ptr(ov), ok.stride(0), ok.stride(1), ok.stride(2), ok.stride(3), T,
+                  _lib.stream())
+        return ok, ov
+
     def export_unit(self, layer, seq, head, perm=None):
         """The reference-format ChunkedKVCache of one unit (kv_store.py:24-166): packed words and
         (lo, hi) metadata gathered back from the tile-native arenas to reference rows, f64
@@ -632,7 +669,7 @@ class BatchedKVCache:
         if perm is None:  # the permutation this cache was built with
             if getattr(self, "_perm", None) is None:
                 raise ValueError("cache was not built here: pass the build perm to export_unit")
-            perm = self._perm[seq].cpu().numpy()
+            perm = self._build_perm()[seq].cpu().numpy()
         perm = np.asarray(perm)
         if perm.shape[0] < n_chunks:
             raise ValueError("perm shorter than the sequence's chunk count")

@@ -531,6 +531,81 @@ __global__ void arena_export_kernel(const unsigned char* __restrict__ codes,
   }
 }
 
+// kv_store.reconstruct (kv_store.py:236-253) with token_order (:227-233) on the tile-native
+// arenas: one warp per (arena row, unit), 4 elements per lane.  Arena row r of sequence b is
+// INT2 row r (< len2), INT4 row r - len2 (< len4) or FP16-region row r - len2 - len4; chunk slot
+// p = r / 32 holds source chunk perm[b][p]; FP16-region rows past the FP16-tier chunks are the
+// tail then the decode tokens, consecutive in original order from 32 n_chunks.  Quantized
+// values are the reference's dequantize (_numpy.py:102-112): zp + scale code in IEEE f64 with
+// scale = (hi - lo) / qmax and zp = lo from the fp16 metadata (no FMA: two roundings).
+__device__ __forceinline__ double dequant_ref(uint32_t lohi, uint32_t code, double qmax) {
+  const double lo = (double)__half2float(__ushort_as_half((unsigned short)(lohi & 0xFFFFu)));
+  const double hi = (double)__half2float(__ushort_as_half((unsigned short)(lohi >> 16)));
+  return __dadd_rn(lo, __dmul_rn(__ddiv_rn(__dsub_rn(hi, lo), qmax), (double)code));
+}
+__global__ void reconstruct_kernel(ckv_arena K, ckv_arena V, const int32_t* __restrict__ seq,
+                                   const uint32_t* __restrict__ perm, int max_chunks, int B, int H,
+                                   double* __restrict__ ok, double* __restrict__ ov, int64_t sl, int64_t sb,
+                                   int64_t st, int64_t sh, int t_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int h = blockIdx.y, l = blockIdx.z / B, b = blockIdx.z % B;
+  const SeqRow s = load_seq(seq, b);
+  if (r >= (int64_t)s.len2 + s.len4 + s.len_fp) return;
+  const int n_chunks = s.ctx / kChunk, n2 = s.len2 / kChunk, n4 = s.len4 / kChunk;
+  const int64_t unit = (int64_t)l * H + h;
+  int64_t orig;
+  int tier;  // 0 INT2, 1 INT4, 2 FP16 region
+  int64_t row;  // row in its arena (absolute)
+  if (r < s.len2) {
+    tier = 0; row = s.off2 + r;
+    orig = (int64_t)perm[(int64_t)b * max_chunks + r / kChunk] * kChunk + r % kChunk;
+  } else if (r < (int64_t)s.len2 + s.len4) {
+    const int64_t r4 = r - s.len2;
+    tier = 1; row = s.off4 + r4;
+    orig = (int64_t)perm[(int64_t)b * max_chunks + n2 + r4 / kChunk] * kChunk + r4 % kChunk;
+  } else {
+    const int64_t rf = r - s.len2 - s.len4, nfp = n_chunks - n2 - n4;
+    tier = 2; row = s.off_fp + rf;
+    orig = rf < nfp * kChunk ? (int64_t)perm[(int64_t)b * max_chunks + n2 + n4 + rf / kChunk] * kChunk + rf % kChunk
+                             : (int64_t)n_chunks * kChunk + (rf - nfp * kChunk);
+  }
+  if (orig >= t_out) return;
+  for (int which = 0; which < 2; ++which) {
+    const ckv_arena& A = which ? V : K;
+    double* dst = (which ? ov : ok) + l * sl + b * sb + orig * st + h * sh;
+    if (tier == 2) {
+      const uint16_t* src = A.fp + (unit * A.rows_fp + row) * kHeadDim;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        dst[4 * lane + k] = (double)__half2float(__ushort_as_half(src[4 * lane + k]));
+      continue;
+    }
+    const int bits = tier == 0 ? 2 : 4;
+    const int64_t ar = unit * (bits == 2 ? A.rows2 : A.rows4) + row, t = ar / kTileRows;
+    const int rt = (int)(ar % kTileRows);
+    const unsigned char* ct = reinterpret_cast<const unsigned char*>(bits == 2 ? A.codes2 : A.codes4) +
+                              t * (bits == 2 ? kBlock2 : kBlock4);
+    const unsigned char* mt = reinterpret_cast<const unsigned char*>(bits == 2 ? A.meta2 : A.meta4) +
+                              t * (bits == 2 ? kBlock2 : kBlock4);
+    const int G = lane >> 3;  // elements 4 lane .. 4 lane + 3 lie in group lane / 8
+    const int mo0 = which ? tile_off_vm(rt, G, 0) : tile_off_km(rt, G, 0);
+    const int mo1 = which ? tile_off_vm(rt, G, 1) : tile_off_km(rt, G, 1);
+    const uint32_t lohi = (uint32_t)*reinterpret_cast<const uint16_t*>(mt + mo0) |
+                          ((uint32_t)*reinterpret_cast<const uint16_t*>(mt + mo1) << 16);
+    uint32_t codes;  // the 4 codes of elements 4 lane .. 4 lane + 3, b bits each
+    if (bits == 2) {
+      codes = ct[which ? tile_byte_v2(rt, lane) : tile_byte_k2(rt, lane)];
+    } else {  // 16-bit piece P = lane of the row (w = P / 2, hf = P % 2)
+      codes = *reinterpret_cast<const uint16_t*>(ct + (which ? tile_off_v4(rt, lane >> 1, lane & 1)
+                                                              : tile_off_k4(rt, lane >> 1, lane & 1)));
+    }
+    const double qmax = bits == 2 ? 3.0 : 15.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[4 * lane + k] = dequant_ref(lohi, (codes >> (bits * k)) & ((1u << bits) - 1u), qmax);
+  }
+}
+
 }  // namespace ckv
 
 using namespace ckv;
@@ -577,6 +652,23 @@ int32_t ckv_expand_meta(const uint32_t* meta, int64_t n_groups, int32_t bits, do
   if (n_groups == 0) return CKV_OK;
   expand_meta_kernel<<<(unsigned)cdiv(n_groups, 256), 256, 0, as_stream(stream)>>>(
       meta, n_groups, (double)((1 << bits) - 1), scales, zero_points);
+  CKV_LAUNCH_CHECK();
+  return CKV_OK;
+}
+
+int32_t ckv_reconstruct(ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq, const uint32_t* perm,
+                        int32_t max_chunks, int32_t layers, int32_t batch, int32_t kv_heads, int32_t max_rows,
+                        double* out_k, double* out_v, int64_t s_layer, int64_t s_batch, int64_t s_token,
+                        int64_t s_head, int32_t t_out, void* stream) {
+  if (layers < 0 || batch < 0 || kv_heads < 0 || max_rows < 0 || t_out < 0 || max_chunks < 0) return CKV_ERR_ARG;
+  if (layers * batch * kv_heads == 0 || max_rows == 0 || t_out == 0) return CKV_OK;
+  if (!seq || !perm || !out_k || !out_v) return CKV_ERR_ARG;
+  if ((int64_t)layers * batch > 65535 || kv_heads > 65535) return CKV_ERR_UNSUPPORTED;
+  constexpr int kWarps = 8;
+  const dim3 grid((unsigned)cdiv(max_rows, kWarps), (unsigned)kv_heads, (unsigned)(layers * batch));
+  reconstruct_kernel<<<grid, 32 * kWarps, 0, as_stream(stream)>>>(k_arena, v_arena, seq, perm, max_chunks, batch,
+                                                                  kv_heads, out_k, out_v, s_layer, s_batch, s_token,
+                                                                  s_head, t_out);
   CKV_LAUNCH_CHECK();
   return CKV_OK;
 }

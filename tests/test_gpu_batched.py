@@ -400,3 +400,38 @@ def test_decode_more_than_eight_q_heads_per_kv_head(m):
     for b in range(B):
         for h in range(H):
             _check_unit(cache, 0, b, h, k, v, tiers[b], q[0, b, h * m:(h + 1) * m], out[0, b, h * m:(h + 1) * m])
+
+
+def test_reconstruct_and_token_order_tile_native():
+    """BatchedKVCache.reconstruct (ckv_reconstruct: the tile-native arenas dequantized and
+    scattered to original token order on the device) equals the reference's reconstruct of every
+    exported unit bit for bit (f64), including a context tail and appended decode tokens; the
+    per-sequence token_order equals the reference's."""
+    from paper_2503_23294_b200 import kv_store
+    rng = np.random.default_rng(123)
+    L, B, H, D = 2, 3, 2, 128
+    N, tail = 9, 11
+    T = N * 32 + tail
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    tiers = rng.choice([0, 1, 2], size=(B, N), p=(0.5, 0.3, 0.2)).astype(np.uint8)
+    s = retrieval.assign_tiers_batched(tiers.astype(np.float64), np.tile([[0.5, 1.5]], (B, 1)))
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), s,
+                                        decode_capacity=8)
+    for _ in range(3):
+        kn = torch.from_numpy(rng.normal(size=(L, B, H, D)).astype(np.float16)).cuda()
+        cache.append(kn, kn * 0.5)
+    rk, rv = cache.reconstruct()
+    rk, rv = rk.cpu().numpy(), rv.cpu().numpy()
+    assert rk.shape == (L, B, T + 3, H, D)
+    for l in range(L):
+        for b in range(B):
+            for h in range(H):
+                ex = cache.export_unit(l, b, h)
+                wk, wv = kv_store.reconstruct(ex)
+                assert np.array_equal(rk[l, b, :, h], wk) and np.array_equal(rv[l, b, :, h], wv), (l, b, h)
+                assert np.array_equal(cache.token_order(b), kv_store.token_order(ex))
+    # FP16-tier and tail rows come back exactly; quantized rows within the group's half-step
+    assert np.array_equal(rk[:, :, N * 32:T], k[:, :, N * 32:T].astype(np.float64))
+    one = cache.reconstruct(layer=1, layers=1, t_out=T)[0].cpu().numpy()
+    assert one.shape == (1, B, T, H, D) and np.array_equal(one[0], rk[1, :, :T])
