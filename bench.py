@@ -586,6 +586,8 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
         res["per_layer_merge_us"] = round(1e3 * timed(merge_fn, max(steps, 20)) / merge_reps, 2)
         res["per_layer_merge_note"] = ("one layer's all_gather + ckv_lse_merge, " +
                                        ("CUDA-graph replayed" if merge_reps > 1 else "eager launches"))
+        res["p2p"] = measure_p2p_exchange(torch, distributed, cache, q, splits, L, B, Hq, dev, steps, warmup,
+                                          timed, barrier, sync_max, step_bytes=None)
         out_rows = L * B * Hq
         e2e_out = step
     else:
@@ -636,6 +638,100 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
     return res
 
 
+def measure_p2p_exchange(torch, distributed, cache, q, splits, L, B, Hq, dev, steps, warmup, timed, barrier,
+                         sync_max, step_bytes=None):
+    """cfg3 split-KV with the exchange over peer memory (distributed.P2PExchange: every rank's
+    partials in a symmetric-memory buffer, one device barrier, ckv_lse_merge_ptrs reading all
+    ranks' buffers over NVLink) instead of all_gather + merge: the step time, its local / barrier
+    + merge parts (events inside the step) and one layer's barrier + merge latency.  Returns
+    {"unavailable": why} when symmetric memory cannot be set up on these ranks.  A single-GPU
+    run sets up a world-1 group for it (the path then measures its barrier + merge cost alone)."""
+    import torch.distributed as tdist
+
+    own_group = False
+    try:
+        if not tdist.is_initialized():
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            sk.close()
+            tdist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+            own_group = True
+        ex = distributed.P2PExchange(L * B * Hq, device=dev)
+        graphs = []
+        for i in range(2):  # one CUDA graph of the 40 local launches per buffer slot
+            buf = ex.buffer(i)
+
+            def local(qq, buf=buf):
+                for l in range(L):
+                    cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
+                                         out=buf[l * B * Hq:(l + 1) * B * Hq])
+
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                local(q)
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                local(q)
+            graphs.append(g)
+
+        def step():
+            graphs[ex.i].replay()
+            return ex.merge()
+
+        for _ in range(warmup):
+            step()
+        ms = timed(step, steps)
+        torch.cuda.synchronize()
+        barrier()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        for e in ev:
+            e[0].record()
+            graphs[ex.i].replay()
+            e[1].record()
+            ex.merge()
+            e[2].record()
+        torch.cuda.synchronize()
+        barrier()
+        local_ms = sync_max(sum(e[0].elapsed_time(e[1]) for e in ev) / steps)
+        xm_ms = sync_max(sum(e[1].elapsed_time(e[2]) for e in ev) / steps)
+        ex1 = distributed.P2PExchange(B * Hq, device=dev)  # one layer's rows
+        out1 = torch.empty((B * Hq, 128), dtype=torch.float16, device=dev)
+        for _ in range(3):
+            ex1.merge(out1)
+        reps, fn = 1, (lambda: ex1.merge(out1))
+        try:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for i in range(2):
+                    ex1.merge(out1, i=i)
+            torch.cuda.current_stream().wait_stream(side)
+            mg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(mg):
+                for r in range(20):
+                    ex1.merge(out1, i=r % 2)
+            mg.replay()
+            reps, fn = 20, mg.replay
+        except Exception:  # noqa: BLE001 (barrier not capturable here: eager launches)
+            torch.cuda.synchronize()
+        layer_us = 1e3 * timed(fn, max(steps, 20)) / reps
+        return {"ms_per_step": round(ms, 4), "local_decode_ms": round(local_ms, 4),
+                "exchange_merge_ms": round(xm_ms, 4), "per_layer_merge_us": round(layer_us, 2),
+                "note": "partials in symmetric memory (torch.distributed._symmetric_memory), device barrier, "
+                        "ckv_lse_merge_ptrs reading every rank's buffer over the peer mappings; per-layer: "
+                        + ("CUDA-graph replayed" if reps > 1 else "eager launches")}
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    finally:
+        if own_group:
+            tdist.destroy_process_group()
+
+
 def run_cfg3(args, torch, dist, dev, rank, world, local):
     """cfg3 line: --cfg3-split seq (sequence split-KV, default) or head (KV-head partition)."""
     r = measure_cfg3(args, torch, dist, dev, rank, world, split=args.cfg3_split)
@@ -662,9 +758,11 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
                          "frac": round(r["per_rank_gbs"] / peak, 4), "peak_kind": peak_kind, "traffic": None},
             "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
         }
-        for key in ("local_decode_ms", "exchange_merge_ms", "per_layer_merge_us", "per_layer_merge_note"):
+        for key in ("local_decode_ms", "exchange_merge_ms", "per_layer_merge_us", "per_layer_merge_note", "p2p"):
             if key in r:
                 line[key] = r[key]
+        if "ms_per_step" in (r.get("p2p") or {}):
+            line["p2p"]["value"] = round(r["algorithmic_bytes_per_step"] / (r["p2p"]["ms_per_step"] * 1e-3) / 1e9, 2)
         print(json.dumps(line), flush=True)
 
 
@@ -1195,6 +1293,10 @@ def main():
                     "parallelism": seq["parallelism"], "e2e": seq["e2e"],
                     "head_shard": {"value": head["value"], "unit": "GB/s", "ms_per_step": head["ms_per_step"],
                                    "parallelism": head["parallelism"], "e2e": head["e2e"]}}
+        p2p = seq.get("p2p") or {}
+        if "ms_per_step" in p2p:
+            p2p["value"] = round(seq["algorithmic_bytes_per_step"] / (p2p["ms_per_step"] * 1e-3) / 1e9, 2)
+        split_kv["p2p"] = p2p
 
     prefill = None
     if rank == 0 and world == 1 and not args.no_prefill:

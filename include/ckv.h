@@ -323,6 +323,11 @@ int32_t ckv_decode_attention_wp_seqs(const uint16_t* q, int64_t q_s_layer, int64
  * out fp16 [rows][128].  o = sum_p acc_p 2^(m_p - m*) / sum_p l_p 2^(m_p - m*). */
 int32_t ckv_lse_merge(const float* partials, int32_t n_parts, int64_t rows, uint16_t* out,
                       void* stream);
+/* The same merge reading the P partial arrays through a device array of P pointers (each
+ * [rows][130]): the ranks' symmetric-memory buffers, read over NVLink peer mappings after a
+ * device-side barrier (distributed.P2PExchange) — no gathered copy, no NCCL collective. */
+int32_t ckv_lse_merge_ptrs(const float* const* parts, int32_t n_parts, int64_t rows, uint16_t* out,
+                           void* stream);
 
 #ifdef __cplusplus
 }

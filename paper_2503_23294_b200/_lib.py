@@ -92,6 +92,7 @@ _SIGNATURES = {
     "ckv_decode_attention_wp_seqs": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _f32,
                                       _vp, _i32, _i32, _i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp], _i32),
     "ckv_lse_merge": ([_vp, _i32, _i64, _vp, _vp], _i32),
+    "ckv_lse_merge_ptrs": ([_vp, _i32, _i64, _vp, _vp], _i32),
 }
 
 _lib = None

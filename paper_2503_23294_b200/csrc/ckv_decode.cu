@@ -1410,6 +1410,46 @@ __global__ void lse_merge_kernel(const float* __restrict__ parts, int P, int64_t
   out[row * kHeadDim + d] = __half_as_ushort(__float2half_rn(acc / lsum));
 }
 
+// The same merge with the P partial arrays given by pointer (each [rows][130]): peer buffers of
+// a symmetric-memory allocation, read over NVLink by ordinary loads (split-KV exchange without a
+// gathered copy).
+__global__ void lse_merge_ptrs_kernel(const float* const* __restrict__ parts, int P, int64_t rows,
+                                      uint16_t* __restrict__ out) {
+  const int64_t row = blockIdx.x;
+  const int d = threadIdx.x;
+  constexpr int kMax = 8;
+  float mv[kMax], xv[kMax], lv[kMax];
+  float ms = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < kMax; ++p) {  // every peer's (m, acc[d], l) in flight at once
+    if (p < P) {
+      const float* q = parts[p] + row * kPartStride;
+      mv[p] = __ldcv(q + kHeadDim);
+      xv[p] = __ldcv(q + d);
+      lv[p] = __ldcv(q + kHeadDim + 1);
+      ms = fmaxf(ms, mv[p]);
+    }
+  }
+  float acc = 0.f, lsum = 0.f;
+#pragma unroll
+  for (int p = 0; p < kMax; ++p) {
+    if (p < P) {
+      const float f = mv[p] == -INFINITY ? 0.f : fast_exp2(mv[p] - ms);
+      acc += f * xv[p];
+      lsum += f * lv[p];
+    }
+  }
+  for (int p = kMax; p < P; ++p) {  // more than 8 ranks: the rest streamed
+    const float* q = parts[p] + row * kPartStride;
+    const float mw = __ldcv(q + kHeadDim), mn = fmaxf(ms, mw);
+    const float fo = ms == -INFINITY ? 0.f : fast_exp2(ms - mn), f = mw == -INFINITY ? 0.f : fast_exp2(mw - mn);
+    acc = fmaf(f, __ldcv(q + d), acc * fo);
+    lsum = fmaf(f, __ldcv(q + kHeadDim + 1), lsum * fo);
+    ms = mn;
+  }
+  out[row * kHeadDim + d] = __half_as_ushort(__float2half_rn(acc / lsum));
+}
+
 }  // namespace ckv
 
 using namespace ckv;
@@ -1685,6 +1725,15 @@ int32_t ckv_decode_attention_wp_seqs(const uint16_t* q, int64_t q_s_layer, int64
     (void)cudaGetLastError();
     return CKV_ERR_CUDA;
   }
+  return CKV_OK;
+}
+
+int32_t ckv_lse_merge_ptrs(const float* const* parts, int32_t n_parts, int64_t rows, uint16_t* out,
+                           void* stream) {
+  if (n_parts < 1 || rows < 0 || !parts || !out) return CKV_ERR_ARG;
+  if (rows == 0) return CKV_OK;
+  lse_merge_ptrs_kernel<<<(unsigned)rows, kHeadDim, 0, as_stream(stream)>>>(parts, n_parts, rows, out);
+  CKV_LAUNCH_CHECK();
   return CKV_OK;
 }
 

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import kernels
+from . import _lib, kernels
 from .batched import CHUNK, HEAD_DIM, BatchedKVCache, lse_merge
 
 
@@ -133,6 +133,53 @@ def exchange_partials(part, group=None):
     return out.view((world,) + tuple(part.shape)).to(dev)
 
 
+class P2PExchange:
+    """Split-KV partial exchange over peer memory instead of a collective ("use
+    symmetric memory if NCCL latency dominates").  Every rank's partials [rows, 130] live in a
+    symmetric-memory buffer (torch.distributed._symmetric_memory: one allocation per rank, mapped
+    into every peer over NVLink); a step is: decode_partial writes the local buffer, a device-side
+    barrier (the allocation's signal pads) orders all ranks' writes, and ckv_lse_merge_ptrs reads
+    every peer's rows straight from its buffer (ordinary loads through the peer mappings) and
+    writes the merged output — no gathered copy, no NCCL kernel.  Two buffers alternate, so one
+    barrier per step also keeps a rank from overwriting partials a slower peer is still reading
+    (rank r writes buffer i again only after passing the next step's barrier, which every rank
+    reaches after its merge of buffer i)."""
+
+    def __init__(self, rows, group=None, device=None, slots=2):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.group = group or dist.group.WORLD
+        self.P = dist.get_world_size(self.group)
+        self.rows = int(rows)
+        self.device = device
+        self.bufs, self.hdls, self.ptrs = [], [], []
+        for _ in range(slots):
+            t = symm_mem.empty((self.rows, HEAD_DIM + 2), dtype=torch.float32, device=device)
+            h = symm_mem.rendezvous(t, self.group)
+            base = list(h.buffer_ptrs)
+            off = t.data_ptr() - base[h.rank]
+            self.bufs.append(t)
+            self.hdls.append(h)
+            self.ptrs.append(torch.tensor([b + off for b in base], dtype=torch.int64, device=device))
+        self.i = 0
+
+    def buffer(self, i=None):
+        """The local partial buffer of step slot i (default: the current step's)."""
+        return self.bufs[self.i if i is None else i]
+
+    def merge(self, out=None, i=None):
+        """Barrier + peer-read merge of slot i's partials -> fp16 [rows, 128]; advances the slot
+        when i is None."""
+        j = self.i if i is None else i
+        self.hdls[j].barrier(channel=0)
+        if out is None:
+            out = torch.empty((self.rows, HEAD_DIM), dtype=torch.float16, device=self.bufs[j].device)
+        _lib.call("ckv_lse_merge_ptrs", _lib.ptr(self.ptrs[j]), self.P, self.rows, _lib.ptr(out), _lib.stream())
+        if i is None:
+            self.i = (self.i + 1) % len(self.bufs)
+        return out
+
+
 def split_kv_decode(cache: BatchedKVCache, q, group=None, splits=None):
     """Sequence-split decode step across ranks: local partials -> all_gather -> LSE merge.
 
@@ -144,4 +191,4 @@ def split_kv_decode(cache: BatchedKVCache, q, group=None, splits=None):
 
 
 __all__ = ["batch_shard", "head_shard", "build_head_shard", "layer_shard", "sequence_shard_plan",
-           "sequence_shard_cache", "build_sequence_shard", "exchange_partials", "split_kv_decode"]
+           "sequence_shard_cache", "build_sequence_shard", "exchange_partials", "P2PExchange", "split_kv_decode"]
