@@ -22,6 +22,7 @@ export_unit restores reference rows on the device (ckv_arena_export).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import ctypes
@@ -114,6 +115,11 @@ class BatchedKVCache:
         # of its bytes are FP16)
         self.schedule = "auto"
         self._any_empty = bool((self.total_tokens() == 0).any())
+        # micro-batch chains: per-layer launches of a chain as programmatic dependents (PDL).  An
+        # early-launched CTA holds an SM slot while it waits for its chain's previous layer (22 %
+        # of CTA residency, tools/chain_timeline.py), yet PDL still wins: cfg2 8 chains 4706 vs
+        # 4515 GB/s without (launch gaps then leave slots empty: 2.76 vs 3.55 resident of 4)
+        self.chain_pdl = os.environ.get("CKV_CHAIN_PDL", "1") == "1"
 
     # -- construction ------------------------------------------------------------------
     @classmethod
@@ -469,7 +475,7 @@ class BatchedKVCache:
             with torch.cuda.stream(st):
                 for l in range(lo, hi):
                     self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l,
-                                pdl=l > lo, seqs=(b0, b1))
+                                pdl=l > lo and self.chain_pdl, seqs=(b0, b1))
         for st in streams:
             cur.wait_stream(st)
 
@@ -548,6 +554,11 @@ class BatchedKVCache:
             raise ValueError("decode capacity exhausted; rebuild with a larger decode_capacity")
         self.seq_host[:, 5] += 1
         self._any_empty = bool((self.total_tokens() == 0).any())
+        # micro-batch chains: per-layer launches of a chain as programmatic dependents (PDL).  An
+        # early-launched CTA holds an SM slot while it waits for its chain's previous layer (22 %
+        # of CTA residency, tools/chain_timeline.py), yet PDL still wins: cfg2 8 chains 4706 vs
+        # 4515 GB/s without (launch gaps then leave slots empty: 2.76 vs 3.55 resident of 4)
+        self.chain_pdl = os.environ.get("CKV_CHAIN_PDL", "1") == "1"
 
     def _append_device(self, k_new, v_new):
         """ckv_append_tokens on the current stream (device side only; graph-capturable)."""
