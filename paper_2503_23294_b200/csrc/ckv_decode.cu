@@ -465,6 +465,14 @@ __device__ __forceinline__ const char* tile_base(const DecArgs& a, const TileSrc
 #ifndef CKV_DEC_BULK
 #define CKV_DEC_BULK 0
 #endif
+// Programmatic-dependent-launch trigger of the split kernel: right after its own wait (0),
+// after its tiles (1, default) or after its in-CTA merge (2).  With concurrent micro-batch
+// chains an early trigger lets the next layer's CTAs sit in SM slots for a whole tile phase
+// waiting for this one: cfg2 8 chains 4703 (0) / 4754 (1) / 4755 (2) GB/s, e2e 4578 / 4707.
+#ifndef CKV_DEC_LATE_TRIGGER
+#define CKV_DEC_LATE_TRIGGER 1
+#endif
+
 #if CKV_DEC_BULK
 __shared__ __align__(8) uint64_t g_ring_mbar[16][4];
 __device__ __forceinline__ uint32_t ring_mbar(int slot) {
@@ -820,7 +828,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     us.F = unit_v_exponent(a, id.l, id.b, id.h);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if !CKV_DEC_LATE_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;");
+#endif
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[1] = gtime();
 
   // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m).  Every warp loads the
@@ -850,6 +860,12 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
 
   quantized_tiles(cnt2, nloc - cnt2, a, src, lo, ring_l, qs, us, st, warp);
   fp16_tiles(a, qs, st, nloc);
+#if CKV_DEC_LATE_TRIGGER == 1
+  // the next launch on the stream may start once every CTA of this one is past its tiles: its
+  // early CTAs then wait a merge tail for this layer, not a whole tile phase, in SM slots other
+  // launches' tiles could use
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
 
   if (lane == 0 && (a.trace != nullptr)) s_tend[warp] = gtime();
   finish_warp(st, c);
@@ -917,6 +933,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
       dst[7] = (int64_t)a.q;
     }
   };
+#if CKV_DEC_LATE_TRIGGER == 2
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
   if (a.splits == 1) { trace_out(); return; }
   // split-KV: the last CTA of this unit to arrive merges all partials (in-launch, no 2nd
   // kernel).  The CTA barrier orders every thread's partial stores before thread 0's
@@ -1109,7 +1128,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
     asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow));  // the row's 4 lanes cover its 256 B
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.launch_dependents;");  // (after the tiles instead: no change, 1 CTA/SM)
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[1] = gtime();
 
   // q staging: every unit slot of the CTA needs parts 0-3; the warps share the jobs
