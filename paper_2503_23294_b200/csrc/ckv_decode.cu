@@ -472,6 +472,9 @@ __device__ __forceinline__ const char* tile_base(const DecArgs& a, const TileSrc
 #ifndef CKV_DEC_LATE_TRIGGER
 #define CKV_DEC_LATE_TRIGGER 1
 #endif
+#ifndef CKV_DEC_Q_PREFETCH
+#define CKV_DEC_Q_PREFETCH 1
+#endif
 
 #if CKV_DEC_BULK
 __shared__ __align__(8) uint64_t g_ring_mbar[16][4];
@@ -826,6 +829,13 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   {
     const CtaIds id = cta_ids(a.Bc, a.b0);
     us.F = unit_v_exponent(a, id.l, id.b, id.h);
+#if CKV_DEC_Q_PREFETCH
+    // pull the unit's q rows into L2 while the previous launch drains (L2 is the point of
+    // coherence: a producer writing q before the wait below still wins)
+    if (warp == 0 && g < a.m)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.q + id.l * a.q_sl + id.b * a.q_sb +
+                                                     (int64_t)(id.h * a.m + g) * kHeadDim + 32 * c));
+#endif
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #if !CKV_DEC_LATE_TRIGGER
