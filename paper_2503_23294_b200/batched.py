@@ -554,11 +554,6 @@ class BatchedKVCache:
             raise ValueError("decode capacity exhausted; rebuild with a larger decode_capacity")
         self.seq_host[:, 5] += 1
         self._any_empty = bool((self.total_tokens() == 0).any())
-        # micro-batch chains: per-layer launches of a chain as programmatic dependents (PDL).  An
-        # early-launched CTA holds an SM slot while it waits for its chain's previous layer (22 %
-        # of CTA residency, tools/chain_timeline.py), yet PDL still wins: cfg2 8 chains 4706 vs
-        # 4515 GB/s without (launch gaps then leave slots empty: 2.76 vs 3.55 resident of 4)
-        self.chain_pdl = os.environ.get("CKV_CHAIN_PDL", "1") == "1"
 
     def _append_device(self, k_new, v_new):
         """ckv_append_tokens on the current stream (device side only; graph-capturable)."""

@@ -395,8 +395,26 @@ __device__ __forceinline__ void scale_acc(WarpState& st, const float (&f)[4]) {
 
 // ---- FP16 tile straight from global memory (FP16 chunks, tail, decode tokens) ------------
 // Same d order as the quantized tiles (q set 2 = unweighted q); V in value units.
+#ifndef CKV_DEC_FP16_VEARLY
+#define CKV_DEC_FP16_VEARLY 1
+#endif
 __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf, int valid,
                                           const QS& qs, WarpState& st, int g, int c) {
+  const int toks[4] = {2 * c, 2 * c + 1, 2 * c + 8, 2 * c + 9};
+  uint2 w[2][4][2];  // [half][token][G - 2 half]: d = 32G + 4g + [0, 4)
+  auto load_v = [&](int half) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        w[half][t][i] = __ldg(reinterpret_cast<const uint2*>(vf + toks[t] * kHeadDim + 32 * (2 * half + i) + 4 * g));
+  };
+#if CKV_DEC_FP16_VEARLY
+  // the V rows are issued with the K rows: one memory round trip per tile instead of two (K,
+  // then V after the softmax)
+  load_v(0);
+  load_v(1);
+#endif
   float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int G = 0; G < 4; ++G) {
@@ -411,23 +429,20 @@ __device__ __forceinline__ void tile_fp16(const uint16_t* kf, const uint16_t* vf
   if (g + 8 >= valid) { s[2] = -INFINITY; s[3] = -INFINITY; }
   uint32_t bp0, bp1;
   softmax_tile<true>(s, st, bp0, bp1);
-  const int toks[4] = {2 * c, 2 * c + 1, 2 * c + 8, 2 * c + 9};
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    uint2 w[4][2];  // [token][G - 2 half]: d = 32G + 4g + [0, 4)
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-        w[t][i] = __ldg(reinterpret_cast<const uint2*>(vf + toks[t] * kHeadDim + 32 * (2 * half + i) + 4 * g));
+#if !CKV_DEC_FP16_VEARLY
+    load_v(half);
+#endif
+    const uint2 (&wh)[4][2] = w[half];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int G = 2 * half + i;
       // m-tile 2G: rows (e 0 | e 1); 2G+1: (e 2 | e 3); tokens (2c | 2c+1) and (2c+8 | 2c+9)
-      mma_16816(st.acc[2 * G], prmt(w[0][i].x, w[1][i].x, 0x5410), prmt(w[0][i].x, w[1][i].x, 0x7632),
-                prmt(w[2][i].x, w[3][i].x, 0x5410), prmt(w[2][i].x, w[3][i].x, 0x7632), bp0, bp1);
-      mma_16816(st.acc[2 * G + 1], prmt(w[0][i].y, w[1][i].y, 0x5410), prmt(w[0][i].y, w[1][i].y, 0x7632),
-                prmt(w[2][i].y, w[3][i].y, 0x5410), prmt(w[2][i].y, w[3][i].y, 0x7632), bp0, bp1);
+      mma_16816(st.acc[2 * G], prmt(wh[0][i].x, wh[1][i].x, 0x5410), prmt(wh[0][i].x, wh[1][i].x, 0x7632),
+                prmt(wh[2][i].x, wh[3][i].x, 0x5410), prmt(wh[2][i].x, wh[3][i].x, 0x7632), bp0, bp1);
+      mma_16816(st.acc[2 * G + 1], prmt(wh[0][i].y, wh[1][i].y, 0x5410), prmt(wh[0][i].y, wh[1][i].y, 0x7632),
+                prmt(wh[2][i].y, wh[3][i].y, 0x5410), prmt(wh[2][i].y, wh[3][i].y, 0x7632), bp0, bp1);
     }
   }
 }
