@@ -834,13 +834,13 @@ def run_cfg4(args, torch, dist, dev, rank, world, local):
     qh = q.cpu().pin_memory()
     oh = torch.empty(q.shape, dtype=torch.float16, pin_memory=True)
     for _ in range(3):
-        cache.decode_step_host(qh, oh, splits=splits, order_current=False)
+        cache.decode_step_host(qh, oh, splits=splits, order_current=False, chains=args.chains)
     torch.cuda.synchronize()
     barrier()
     e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e4.record()
     for _ in range(args.steps):
-        cache.decode_step_host(qh, oh, splits=splits, order_current=False)
+        cache.decode_step_host(qh, oh, splits=splits, order_current=False, chains=args.chains)
     torch.cuda.current_stream().wait_event(cache.host_step_ready)
     e5.record()
     torch.cuda.synchronize()
