@@ -146,15 +146,36 @@ class P2PExchange:
     reaches after its merge of buffer i)."""
 
     def __init__(self, rows, group=None, device=None, slots=2):
-        import torch.distributed._symmetric_memory as symm_mem
-
         self.group = group or dist.group.WORLD
         self.P = dist.get_world_size(self.group)
         self.rows = int(rows)
         self.device = device
+        # every rank allocates first and the ranks agree before the (collective) rendezvous, so a
+        # rank that cannot use symmetric memory makes all of them raise instead of leaving the
+        # others waiting in the rendezvous
+        bufs, err = [], None
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+            peers_ok = all(torch.cuda.can_device_access_peer(dev.index, j)
+                           for j in range(torch.cuda.device_count()) if j != dev.index)
+            if not peers_ok:
+                raise RuntimeError("no peer access between the visible GPUs")
+            bufs = [symm_mem.empty((self.rows, HEAD_DIM + 2), dtype=torch.float32, device=device)
+                    for _ in range(slots)]
+        except Exception as e:  # noqa: BLE001
+            err = e
+        if self.P > 1:
+            flag = torch.tensor([0 if err else 1], dtype=torch.int32,
+                                device=device if dist.get_backend(self.group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+            if int(flag.item()) == 0 and err is None:
+                err = RuntimeError("symmetric memory unavailable on another rank")
+        if err is not None:
+            raise err
         self.bufs, self.hdls, self.ptrs = [], [], []
-        for _ in range(slots):
-            t = symm_mem.empty((self.rows, HEAD_DIM + 2), dtype=torch.float32, device=device)
+        for t in bufs:
             h = symm_mem.rendezvous(t, self.group)
             base = list(h.buffer_ptrs)
             off = t.data_ptr() - base[h.rank]
