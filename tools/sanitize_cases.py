@@ -1,7 +1,8 @@
 """Small invocations of every kernel for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): search, reorder/quantize/pack, decode (splits 1 and > 1, per-layer PDL chain,
-CUDA-graph replay, partials + LSE merge, m = 1 / 4 / 8, exact and precise modes), append,
-export, the f64 per-head kernels and the text encoders.  Checks results loosely (the parity
+CUDA-graph replay, micro-batch chains on the split kernel and on the warp plan, partials + LSE
+merge by array and by pointers, m = 1 / 4 / 8, outlier-K and huge-scale units), append, export,
+the tile-native reconstruct, the f64 per-head kernels and the text encoders.  Checks results loosely (the parity
 tests do that properly); the point is the sanitizer's verdict."""
 import os
 import sys
@@ -49,11 +50,24 @@ def main():
     g.replay()
     g.replay()
     cache.schedule = "auto"
+    g = cache.decode_graph(q, out, splits=cache.chain_splits(4), chains=B)  # the bench's default step
+    g.replay()
+    g.replay()
+    for b in range(B):  # warp plan over sequence ranges
+        for l in range(L):
+            cache.decode(q[l:l + 1], out=out[l:l + 1], layer=l, pdl=l > 0, seqs=(b, b + 1), schedule="wp")
+    # LSE merge through a device array of partial-buffer pointers (the peer-memory exchange's merge)
+    from paper_2503_23294_b200 import _lib
+    pa, pb = cache.decode_partial(q, splits=2), cache.decode_partial(q, splits=3)
+    ptrs = torch.tensor([pa.data_ptr(), pb.data_ptr()], dtype=torch.int64, device=dev)
+    merged = torch.empty((pa.shape[0], D), dtype=torch.float16, device=dev)
+    _lib.call("ckv_lse_merge_ptrs", _lib.ptr(ptrs), 2, pa.shape[0], _lib.ptr(merged), _lib.stream())
+    cache.reconstruct()
     loop = batched.DecodeLoop(cache, 4, splits=2)
     for _ in range(3):
         loop.step(q, k[:, :, 0], v[:, :, 0])
     cache.export_unit(1, 1, 1)
-    # precise and exact decode modes: outlier channels / a huge-scale unit
+    # outlier channels (wide K groups) / a huge-scale unit
     k2 = k.clone()
     k2[..., ::32] *= 40
     cache2 = batched.build_cache_batched(k2, v, s)
