@@ -491,6 +491,7 @@ __device__ __forceinline__ const char* tile_base(const DecArgs& a, const TileSrc
 #define CKV_DEC_Q_PREFETCH 1
 #endif
 
+
 #if CKV_DEC_BULK
 __shared__ __align__(8) uint64_t g_ring_mbar[16][4];
 __device__ __forceinline__ uint32_t ring_mbar(int slot) {
@@ -715,75 +716,58 @@ __device__ __forceinline__ void finish_warp(WarpState& st, int c) {
 __device__ __forceinline__ int acc_d(int mt, int e2, int g) { return 32 * (mt >> 1) + 4 * g + 2 * (mt & 1) + e2; }
 
 // ---- q staging (shared by both decode kernels) -----------------------------------------
-// q row `row` (zero if >= m) of unit (l, b, h): the lane's 32 elements d = 32G + 8c + k
-// (qv[8G + k]), scaled to log2 units and rounded to the fp16 MMA operand.
-__device__ __forceinline__ void load_q_rows(const DecArgs& a, int l, int b, int h, int row, int c, float (&qv)[32]) {
-  const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + row) * kHeadDim + 8 * c;
-  if (row < a.m) {
-#pragma unroll
-    for (int G = 0; G < 4; ++G) {
-      const uint4 x = reinterpret_cast<const uint4*>(qrow + 32 * G)[0];
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(u32_as_h2(w[e]));
-        qv[8 * G + 2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));  // the fp16 MMA operand
-        qv[8 * G + 2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
-      }
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < 32; ++e) qv[e] = 0.f;
-  }
-}
-
-// the unit's q exponent E from its q rows (all 8 row-groups of the warp)
-__device__ __forceinline__ int unit_q_exponent(const float (&qv)[32]) {
-  float qmaxabs = 0.f;
-#pragma unroll
-  for (int e = 0; e < 32; ++e) qmaxabs = fmaxf(qmaxabs, fabsf(qv[e]));
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) qmaxabs = fmaxf(qmaxabs, __shfl_xor_sync(0xffffffffu, qmaxabs, o));
-  return q_exponent(qmaxabs);
-}
 // the unit's V exponent F (span_max is build-time data: readable before the PDL wait)
 __device__ __forceinline__ int unit_v_exponent(const DecArgs& a, int l, int b, int h) {
   const int64_t fidx = ((int64_t)l * a.H + h) * a.B + b;  // [L][H][B]
   return a.V.span_max ? v_exponent(__uint_as_float(a.V.span_max[fidx])) : 0;
 }
 
-// Part `part` of a unit's q staging into s_qu (kQBytes): 0-2 the q-fragment sets (0: INT2 slot
-// weights 2^(E - j), 1: INT4, 2: unweighted), 3 the zero-point entry.  Whole warp.
-__device__ __forceinline__ void stage_q_part(const float (&qv)[32], int part, int E, unsigned char* s_qu, int lane) {
-  const int c = lane & 3;
-  if (part < 3) {
+// Quarter staging: one warp stages group G of every set for one unit (a quarter of the q values:
+// one 16-byte load per lane), in two phases around a barrier that combines the quarters' max |q|.
+// q row g (zero if >= m), elements 32G + 8c + [0, 8), scaled to log2 units and rounded like the
+// fp16 operand.
+__device__ __forceinline__ void load_q_quarter(const DecArgs& a, int l, int b, int h, int G, int g, int c,
+                                               float (&qv)[8]) {
+  const uint16_t* qrow = a.q + l * a.q_sl + b * a.q_sb + (int64_t)(h * a.m + g) * kHeadDim + 32 * G + 8 * c;
+  uint4 x = make_uint4(0u, 0u, 0u, 0u);
+  if (g < a.m) x = *reinterpret_cast<const uint4*>(qrow);
+  const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-    for (int G = 0; G < 4; ++G) {
-      uint32_t v[4];
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __half22float2(u32_as_h2(w4[e]));
+    qv[2 * e] = __half2float(__float2half_rn(f.x * a.scale_log2));
+    qv[2 * e + 1] = __half2float(__float2half_rn(f.y * a.scale_log2));
+  }
+}
+// phase 1: the quarter's max |q| (returned, warp-uniform) and its zero-point entries (lanes c == G)
+__device__ __forceinline__ float stage_q_quarter_aug(const float (&qv)[8], int G, int lane, unsigned char* s_qu) {
+  float mx = 0.f, P = 0.f;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        // b0: cols 2c, 2c+1 (code e = 2h: INT2 j = 4h, INT4 j = 0); b1: cols 2c+8, 2c+9 (e = 2h+1)
-        const int j0 = part == 0 ? 4 * h : 0, j1 = part == 0 ? 4 * h + 2 : 4;
-        const float w0 = part == 2 ? 1.0f : exp2f((float)(E - j0)), w1 = part == 2 ? 1.0f : exp2f((float)(E - j1));
-        v[2 * h] = h2_as_u32(__floats2half2_rn(qv[8 * G + 2 * h] * w0, qv[8 * G + 4 + 2 * h] * w0));
-        v[2 * h + 1] = h2_as_u32(__floats2half2_rn(qv[8 * G + 2 * h + 1] * w1, qv[8 * G + 5 + 2 * h] * w1));
-      }
-      reinterpret_cast<uint4*>(s_qu + part * kQSet + 512 * G)[lane] = make_uint4(v[0], v[1], v[2], v[3]);
-    }
-  } else {
-    float P[4];
+  for (int e = 0; e < 8; ++e) { mx = fmaxf(mx, fabsf(qv[e])); P += qv[e]; }
 #pragma unroll
-    for (int G = 0; G < 4; ++G) {
-      P[G] = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) P[G] += qv[8 * G + k];
-      P[G] += __shfl_xor_sync(0xffffffffu, P[G], 1);
-      P[G] += __shfl_xor_sync(0xffffffffu, P[G], 2);
-    }
-    const float qsum = c == 0 ? P[0] : (c == 1 ? P[1] : (c == 2 ? P[2] : P[3]));
-    const __half qhi = __float2half_rn(qsum);
-    const __half qlo = __float2half_rn(qsum - __half2float(qhi));
+  for (int o = 1; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  P += __shfl_xor_sync(0xffffffffu, P, 1);
+  P += __shfl_xor_sync(0xffffffffu, P, 2);
+  if ((lane & 3) == G) {  // lane (g, c = G): Q[g][G] as an fp16 (hi, lo) pair
+    const __half qhi = __float2half_rn(P);
+    const __half qlo = __float2half_rn(P - __half2float(qhi));
     reinterpret_cast<uint32_t*>(s_qu + 3 * kQSet)[lane] = h2_as_u32(__halves2half2(qhi, qlo));
+  }
+  return mx;
+}
+// phase 2: group G of the three fragment sets with the unit's exponent E
+__device__ __forceinline__ void stage_q_quarter_sets(const float (&qv)[8], int G, int E, unsigned char* s_qu, int lane) {
+#pragma unroll
+  for (int part = 0; part < 3; ++part) {
+    uint32_t v[4];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int j0 = part == 0 ? 4 * hh : 0, j1 = part == 0 ? 4 * hh + 2 : 4;
+      const float w0 = part == 2 ? 1.0f : exp2f((float)(E - j0)), w1 = part == 2 ? 1.0f : exp2f((float)(E - j1));
+      v[2 * hh] = h2_as_u32(__floats2half2_rn(qv[2 * hh] * w0, qv[4 + 2 * hh] * w0));
+      v[2 * hh + 1] = h2_as_u32(__floats2half2_rn(qv[2 * hh + 1] * w1, qv[5 + 2 * hh] * w1));
+    }
+    reinterpret_cast<uint4*>(s_qu + part * kQSet + 512 * G)[lane] = make_uint4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -805,6 +789,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   unsigned char (*s_ring)[kWarpRing] = reinterpret_cast<unsigned char (*)[kWarpRing]>(s_dyn);
   __shared__ float s_ml[kDecWarps][8][2];
   __shared__ __align__(16) unsigned char s_q[kQBytes];
+  __shared__ float s_qmax[kDecWarps];
   __shared__ int s_last;
   __shared__ __align__(16) unsigned char s_scr[kDecWarps][kScratch];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -858,15 +843,18 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
 #endif
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[1] = gtime();
 
-  // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m).  Every warp loads the
-  // same 8 rows and derives the unit's q exponent from max |q|; then warps 0-2 write q-fragment
-  // sets 0-2, warp 3 the zero-point entry.
+  // Q B-fragments (scaled to log2 units), q-row i = g (zero if g >= m):
+  // warp w stages group G = w of every set (a quarter of the q values each: one 16-byte load per
+  // lane), the unit's max |q| combined through shared memory
   {
     const CtaIds id = cta_ids(a.Bc, a.b0);
-    float qv[32];
-    load_q_rows(a, id.l, id.b, id.h, g, c, qv);
-    us.E = unit_q_exponent(qv);
-    stage_q_part(qv, warp < 3 ? warp : 3, us.E, s_q, lane);
+    float qv[8];
+    load_q_quarter(a, id.l, id.b, id.h, warp, g, c, qv);
+    const float mx = stage_q_quarter_aug(qv, warp, lane, s_q);
+    if (lane == 0) s_qmax[warp] = mx;
+    __syncthreads();
+    us.E = q_exponent(fmaxf(fmaxf(s_qmax[0], s_qmax[1]), fmaxf(s_qmax[2], s_qmax[3])));
+    stage_q_quarter_sets(qv, warp, us.E, s_q, lane);
   }
   __syncthreads();
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[2] = gtime();
@@ -1105,6 +1093,7 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   __shared__ float s_ml[kWpWarps][8][2];
   __shared__ __align__(16) unsigned char s_scr[kWpWarps][kScratch];
   __shared__ int s_lastu[8], s_do[8];
+  __shared__ float s_qmax[4 * kPlanSlots];  // per (slot, group) max |q| of the q staging
   __shared__ int4 s_slot[8];             // per unit slot: warps [x, y) of this CTA, first / last CTA of the unit
   __shared__ unsigned short s_rtab[64];  // merge row r -> (slot << 8 | q row)
   __shared__ int64_t s_tr[12], s_tend[kWpWarps];
@@ -1156,20 +1145,40 @@ __global__ void __launch_bounds__(kWpWarps * 32, 16 / kWpWarps) decode_wp_kernel
   asm volatile("griddepcontrol.launch_dependents;");  // (after the tiles instead: no change, 1 CTA/SM)
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[1] = gtime();
 
-  // q staging: every unit slot of the CTA needs parts 0-3; the warps share the jobs
+  // q staging: every unit slot of the CTA needs groups 0-3 of every set; job j = (slot j / 4,
+  // group j % 4) goes to warp j % 16 (a quarter of the slot's q per job), in two phases around
+  // the barrier that combines each slot's quarter maxima into its exponent
   {
-    float qv[32];
-    load_q_rows(a, l, b, h, g, c, qv);  // this warp's unit: its q exponent (and its staging jobs)
-    us.E = unit_q_exponent(qv);
+    float qv[8];  // the warp's first job's quarter (kept for phase 2; further jobs reload)
+    const int uj0 = u0 + (warp >> 2);
+    if (warp < 4 * nslots) load_q_quarter(a, l, a.b0 + uj0 / a.H, uj0 % a.H, warp & 3, g, c, qv);
     for (int j = warp; j < 4 * nslots; j += kWpWarps) {
       const int uj = u0 + (j >> 2);
-      if (uj == u) {
-        stage_q_part(qv, j & 3, us.E, s_qall + (j >> 2) * kQBytes, lane);
+      float qj[8];
+      if (j == warp) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) qj[e] = qv[e];
       } else {
-        float qj[32];
-        load_q_rows(a, l, a.b0 + uj / a.H, uj % a.H, g, c, qj);
-        stage_q_part(qj, j & 3, unit_q_exponent(qj), s_qall + (j >> 2) * kQBytes, lane);
+        load_q_quarter(a, l, a.b0 + uj / a.H, uj % a.H, j & 3, g, c, qj);
       }
+      const float mx = stage_q_quarter_aug(qj, j & 3, lane, s_qall + (j >> 2) * kQBytes);
+      if (lane == 0) s_qmax[j] = mx;
+    }
+    __syncthreads();
+    auto slot_e = [&](int sl) {
+      return q_exponent(fmaxf(fmaxf(s_qmax[4 * sl], s_qmax[4 * sl + 1]), fmaxf(s_qmax[4 * sl + 2], s_qmax[4 * sl + 3])));
+    };
+    us.E = slot_e(slot);
+    for (int j = warp; j < 4 * nslots; j += kWpWarps) {
+      const int uj = u0 + (j >> 2);
+      float qj[8];
+      if (j == warp) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) qj[e] = qv[e];
+      } else {
+        load_q_quarter(a, l, a.b0 + uj / a.H, uj % a.H, j & 3, g, c, qj);
+      }
+      stage_q_quarter_sets(qj, j & 3, slot_e(j >> 2), s_qall + (j >> 2) * kQBytes, lane);
     }
   }
   __syncthreads();
