@@ -885,12 +885,21 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   __syncthreads();  // ring -> merge buffer reuse
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[8] = gtime();
   float (*s_acc)[8][kHeadDim] = reinterpret_cast<float (*)[8][kHeadDim]>(&s_ring[0][0]);
+  // only the m real q rows; column of (row, d) = d XOR ((row / 2) & 3), so the lanes of one
+  // store instruction (rows 2c, 2c+1 x d = 32G + 4g + e) hit 32 distinct banks
+  {
+    const bool r0 = 2 * c < a.m, r1 = 2 * c + 1 < a.m;
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    s_acc[warp][2 * c][acc_d(mt, 0, g)] = st.acc[mt][0];
-    s_acc[warp][2 * c + 1][acc_d(mt, 0, g)] = st.acc[mt][1];
-    s_acc[warp][2 * c][acc_d(mt, 1, g)] = st.acc[mt][2];
-    s_acc[warp][2 * c + 1][acc_d(mt, 1, g)] = st.acc[mt][3];
+    for (int mt = 0; mt < 8; ++mt) {
+      if (r0) {
+        s_acc[warp][2 * c][acc_d(mt, 0, g) ^ c] = st.acc[mt][0];
+        s_acc[warp][2 * c][acc_d(mt, 1, g) ^ c] = st.acc[mt][2];
+      }
+      if (r1) {
+        s_acc[warp][2 * c + 1][acc_d(mt, 0, g) ^ c] = st.acc[mt][1];
+        s_acc[warp][2 * c + 1][acc_d(mt, 1, g) ^ c] = st.acc[mt][3];
+      }
+    }
   }
   if (g == 0) {
     s_ml[warp][2 * c][0] = st.mrun[0]; s_ml[warp][2 * c][1] = st.lsum[0];
@@ -908,11 +917,12 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
 #pragma unroll
     for (int w = 0; w < kDecWarps; ++w) ms = fmaxf(ms, s_ml[w][qi][0]);
     float acc = 0.f, lsum = 0.f;
+    const int dsw = d ^ ((qi >> 1) & 3);  // the parking swizzle
 #pragma unroll
     for (int w = 0; w < kDecWarps; ++w) {
       const float mw = s_ml[w][qi][0];
       const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - ms);
-      acc += f * s_acc[w][qi][d];
+      acc += f * s_acc[w][qi][dsw];
       lsum += f * s_ml[w][qi][1];
     }
     const int64_t row = ((int64_t)l * a.B + b) * Hq + hq0 + qi;
