@@ -280,10 +280,13 @@ def pick_splits(args, cache, m, layers=1):
     --splits is given, or the cache has no warp plan."""
     cache.schedule = args.schedule
     chains = getattr(args, "chains", 1)
-    first = None if chains == 1 else cache._chain_ranges(chains)[0]
-    if args.schedule != "split" and args.splits is None and cache._use_wp(m, first, None, None) is not None:
+    if chains > 1:  # micro-batch chains run the split kernel over (sequence, head) ranges
+        if args.schedule == "wp" and chains <= cache.B and args.splits is None:
+            return None
+        return args.splits or cache.chain_splits(m)
+    if args.schedule != "split" and args.splits is None and cache._use_wp(m, None, None, None) is not None:
         return None
-    return args.splits or (cache.default_splits(m, layers) if chains == 1 else cache.chain_splits(m))
+    return args.splits or cache.default_splits(m, layers)
 
 
 def auto_chains(batch):
@@ -309,7 +312,10 @@ def schedule_desc(cache, splits, chains=1):
         return desc
     desc = f"split: {splits} CTAs of 4 warps per unit"
     if chains > 1:
-        desc += f"; {chains} micro-batch chains of {cache.B // chains} sequence(s), launches of {cache.B // chains * cache.H * splits} CTAs"
+        u = cache._chain_units(chains)
+        b0, b1, h0, h1 = u[0]
+        desc += (f"; {len(u)} micro-batch chains of {b1 - b0} sequence(s) x {h1 - h0} kv head(s), launches of "
+                 f"{(b1 - b0) * (h1 - h0) * splits} CTAs")
     return desc
 
 
@@ -491,7 +497,30 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
     q_all = torch.randn((L, B, H * m, D), generator=g, device=dev, dtype=torch.float16)
     q = q_all[:, :, h0 * m:h1 * m].contiguous()
     Hq = (h1 - h0) * m
-    splits = pick_splits(args, cache, m)
+    chains = args.chains if args.chains > 0 else 8  # micro-batch chains over the kv heads (batch 1)
+    cargs = argparse.Namespace(**{**vars(args), "chains": chains})
+    splits = pick_splits(cargs, cache, m)
+    units = cache._chain_units(chains)
+    chain_streams = [torch.cuda.Stream(device=dev) for _ in units]
+
+    def partial_layers(qq, buf):
+        """The step's per-layer decode_partial launches into buf: one PDL chain per kv-head range,
+        each on its own stream (forked from / joined into the current stream)."""
+        if len(units) == 1:
+            for l in range(L):
+                cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
+                                     out=buf[l * B * Hq:(l + 1) * B * Hq])
+            return
+        cur = torch.cuda.current_stream()
+        for st in chain_streams:
+            st.wait_stream(cur)
+        for (_, _, ha, hb), st in zip(units, chain_streams):
+            with torch.cuda.stream(st):
+                for l in range(L):
+                    cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
+                                         out=buf[l * B * Hq:(l + 1) * B * Hq], heads=(ha, hb))
+        for st in chain_streams:
+            cur.wait_stream(st)
 
     def barrier():
         if world > 1:
@@ -521,9 +550,7 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
         parts = torch.empty((L * B * Hq, D + 2), dtype=torch.float32, device=dev)
 
         def local_decode(qq):
-            for l in range(L):
-                cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
-                                     out=parts[l * B * Hq:(l + 1) * B * Hq])
+            partial_layers(qq, parts)
 
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
@@ -586,13 +613,13 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
         res["per_layer_merge_us"] = round(1e3 * timed(merge_fn, max(steps, 20)) / merge_reps, 2)
         res["per_layer_merge_note"] = ("one layer's all_gather + ckv_lse_merge, " +
                                        ("CUDA-graph replayed" if merge_reps > 1 else "eager launches"))
-        res["p2p"] = measure_p2p_exchange(torch, distributed, cache, q, splits, L, B, Hq, dev, steps, warmup,
-                                          timed, barrier, sync_max, step_bytes=None)
+        res["p2p"] = measure_p2p_exchange(torch, distributed, partial_layers, q, L, B, Hq, dev, steps, warmup,
+                                          timed, barrier, sync_max)
         out_rows = L * B * Hq
         e2e_out = step
     else:
         out = torch.empty_like(q)
-        graph = cache.decode_graph(q, out, splits=splits)
+        graph = cache.decode_graph(q, out, splits=splits, chains=chains)
         for _ in range(warmup):
             graph.replay()
         with ClockSampler(dev.index or 0) as clk:
@@ -624,7 +651,7 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
     res.update({
         "value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
         "tokens_per_s": round(B / (ms * 1e-3), 1), "algorithmic_bytes_per_step": int(step_bytes),
-        "splits": splits, "split": split, "schedule": schedule_desc(cache, splits),
+        "splits": splits, "split": split, "schedule": schedule_desc(cache, splits, chains),
         "parallelism": f"{'seq-split' if split == 'seq' else 'head-shard'} x{world}",
         "per_rank_gbs": round(my_bytes / (ms * 1e-3) / 1e9, 1),
         "e2e": {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
@@ -638,8 +665,8 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
     return res
 
 
-def measure_p2p_exchange(torch, distributed, cache, q, splits, L, B, Hq, dev, steps, warmup, timed, barrier,
-                         sync_max, step_bytes=None):
+def measure_p2p_exchange(torch, distributed, partial_layers, q, L, B, Hq, dev, steps, warmup, timed, barrier,
+                         sync_max):
     """cfg3 split-KV with the exchange over peer memory (distributed.P2PExchange: every rank's
     partials in a symmetric-memory buffer, one device barrier, ckv_lse_merge_ptrs reading all
     ranks' buffers over NVLink) instead of all_gather + merge: the step time, its local / barrier
@@ -665,9 +692,7 @@ def measure_p2p_exchange(torch, distributed, cache, q, splits, L, B, Hq, dev, st
             buf = ex.buffer(i)
 
             def local(qq, buf=buf):
-                for l in range(L):
-                    cache.decode_partial(qq[l:l + 1], splits=splits, layer=l, pdl=l > 0,
-                                         out=buf[l * B * Hq:(l + 1) * B * Hq])
+                partial_layers(qq, buf)
 
             side = torch.cuda.Stream(device=dev)
             side.wait_stream(torch.cuda.current_stream())
@@ -747,9 +772,10 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
                                       else "KV heads partitioned across the GPUs"),
                        "global_batch": CFG3["batch"], "seq_len": CFG3["context"], "parallelism": r["parallelism"],
                        "tier_fractions_int2_int4_fp16": r["tier_fractions_int2_int4_fp16"],
-                       "launch": ("per-layer decode_partial (40 PDL-chained launches, one CUDA graph) + all_gather "
-                                  "+ merge" if r["split"] == "seq" else
-                                  "per-layer decode (40 PDL-chained launches, one CUDA graph), no collective"),
+                       "launch": ("per-layer decode_partial (40 PDL-chained launches per kv-head chain, 8 chains on "
+                                  "their own streams, one CUDA graph) + all_gather + merge" if r["split"] == "seq" else
+                                  "per-layer decode (40 PDL-chained launches per kv-head chain, one CUDA graph), "
+                                  "no collective"),
                        "splits": r["splits"], "schedule": r["schedule"],
                        "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
             "tokens_per_s": r["tokens_per_s"],
@@ -1066,7 +1092,7 @@ def main():
                          "stream, so one range's layer boundary overlaps the others' work; 0 (default) = "
                          "one chain per sequence for cfg2, 1 for the other workloads")
     args = ap.parse_args()
-    if args.chains == 0 and args.workload not in ("cfg2", "cfg4"):
+    if args.chains == 0 and args.workload not in ("cfg2", "cfg3", "cfg4"):
         args.chains = 1
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

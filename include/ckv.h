@@ -280,6 +280,18 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
                                   int32_t kv_heads, int32_t m, float scale, int32_t splits,
                                   void* workspace, uint16_t* out, int64_t o_s_layer, int64_t o_s_batch,
                                   float* partial_out, int32_t flags, void* stream);
+/* The same over kv heads [head_begin, head_begin + head_count) of sequences [seq_begin,
+ * seq_begin + seq_count) (micro-batch chains over heads, e.g. a batch-1 128K context as 8
+ * chains of 5 heads): rows of other heads and sequences in out / partial_out are left
+ * untouched; the workspace is the whole cache's (ckv_decode_workspace_bytes), so concurrent
+ * launches over disjoint ranges never share a counter. */
+int32_t ckv_decode_attention_range(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                                   ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                                   int32_t layers, int32_t batch, int32_t seq_begin, int32_t seq_count,
+                                   int32_t kv_heads, int32_t head_begin, int32_t head_count, int32_t m,
+                                   float scale, int32_t splits, void* workspace, uint16_t* out,
+                                   int64_t o_s_layer, int64_t o_s_batch, float* partial_out, int32_t flags,
+                                   void* stream);
 
 /* Warp-plan schedule of the same computation (whole-batch launches): unit u = b * kv_heads + h
  * of every layer takes unit_warps[u] >= 1 warps (their sum = 16 * ctas); CTA c (16 warps, one

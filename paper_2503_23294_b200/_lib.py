@@ -83,6 +83,8 @@ _SIGNATURES = {
                               _vp, _vp, _i64, _i64, _vp, _i32, _vp], _i32),
     "ckv_decode_attention_seqs": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
                                    _f32, _i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp], _i32),
+    "ckv_decode_attention_range": ([_vp, _i64, _i64, Arena, Arena, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                    _i32, _f32, _i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp], _i32),
     "ckv_decode_wp_workspace_bytes": ([_i32, _i32, _i32, _i32, _i32], _i64),
     "ckv_decode_wp_cta_warps": ([], _i32),
     "ckv_decode_wp_plan_ints": ([_i32], _i64),

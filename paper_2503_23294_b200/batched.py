@@ -340,7 +340,8 @@ class BatchedKVCache:
         self._ws_ptr[wkey] = ptr = self._ws[key].data_ptr() + off
         return ptr
 
-    def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False, seqs=None, schedule=None):
+    def decode(self, q, splits=None, out=None, scale=None, layer=0, pdl=False, seqs=None, schedule=None,
+               heads=None):
         """Mixed-precision decode attention for q fp16 [L', B, H*m, 128] -> fp16 same shape,
         over layers [layer, layer + L') of the cache (L' = L for the whole model in one launch,
         1 for the per-layer launches of a real decode step).  pdl=True launches as a
@@ -348,7 +349,9 @@ class BatchedKVCache:
         kernel was itself a decode of this cache (it overlaps this launch's K/V prefetch with
         the previous launch's tail).  seqs=(b0, b1) computes sequences [b0, b1) only (q / out
         keep the full batch; the other rows of out are left untouched), so disjoint sequence
-        ranges can run as concurrent micro-batch chains."""
+        ranges can run as concurrent micro-batch chains; heads=(h0, h1) likewise restricts the
+        launch to kv heads [h0, h1) (split kernel), so a batch-1 context can run as chains over
+        its heads."""
         L, B, Hq, D = q.shape
         if B != self.B or layer < 0 or layer + L > self.L or D != HEAD_DIM or Hq % self.H:
             raise ValueError("q shape does not match the cache")
@@ -359,6 +362,9 @@ class BatchedKVCache:
         b0, b1 = (0, B) if seqs is None else (int(seqs[0]), int(seqs[1]))
         if not 0 <= b0 <= b1 <= B:
             raise ValueError("seqs must be a range inside the batch")
+        h0, h1 = (0, self.H) if heads is None else (int(heads[0]), int(heads[1]))
+        if not 0 <= h0 <= h1 <= self.H:
+            raise ValueError("heads must be a range of the kv heads")
         m = Hq // self.H
         if out is None:
             out = torch.empty((L, B, Hq, D), dtype=torch.float16, device=q.device)
@@ -372,12 +378,13 @@ class BatchedKVCache:
             for r0 in range(0, m, MAX_Q_PER_KV):
                 r1 = min(m, r0 + MAX_Q_PER_KV)
                 og = self.decode(qv[:, :, :, r0:r1].reshape(L, B, self.H * (r1 - r0), D),
-                                 splits=splits, scale=scale, layer=layer, pdl=False, seqs=(b0, b1))
+                                 splits=splits, scale=scale, layer=layer, pdl=False, seqs=(b0, b1),
+                                 heads=(h0, h1))
                 out.view(L, B, self.H, m, D)[:, b0:b1, :, r0:r1] = og.view(L, B, self.H, r1 - r0, D)[:, b0:b1]
             return out
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
         rng = None if (b0, b1) == (0, B) else (b0, b1)
-        plan = self._use_wp(m, rng, splits, schedule) if b1 > b0 else None
+        plan = self._use_wp(m, rng, splits, schedule) if b1 > b0 and (h0, h1) == (0, self.H) else None
         if plan is not None:
             prefix, ctas, slots, max_ctas = plan
             ws = self._wp_workspace(m, L, layer, max_ctas, rng)
@@ -388,9 +395,9 @@ class BatchedKVCache:
             return out
         splits = self.default_splits(m, L) if splits is None else int(splits)
         ws = self._workspace(m, splits, L, layer)
-        _lib.call("ckv_decode_attention_seqs", _lib.ptr(q), q.stride(0), q.stride(1),
+        _lib.call("ckv_decode_attention_range", _lib.ptr(q), q.stride(0), q.stride(1),
                   self.arena("k", layer), self.arena("v", layer), _lib.ptr(self.seq), L, B, b0, b1 - b0,
-                  self.H, m, scale, splits, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
+                  self.H, h0, h1 - h0, m, scale, splits, ws, _lib.ptr(out), out.stride(0), out.stride(1), None,
                   _lib.DECODE_PDL if pdl else 0, _lib.stream())
         return out
 
@@ -460,22 +467,32 @@ class BatchedKVCache:
         chains = max(1, min(int(chains), self.B))
         return [(c * self.B // chains, (c + 1) * self.B // chains) for c in range(chains)]
 
+    def _chain_units(self, chains):
+        """Micro-batch chains as (b0, b1, h0, h1) ranges: sequence ranges while chains <= B, else
+        every sequence split further into chains // B kv-head ranges (a batch-1 context runs as
+        chains over its heads)."""
+        chains = max(1, int(chains))
+        if chains <= self.B:
+            return [(b0, b1, 0, self.H) for (b0, b1) in self._chain_ranges(chains)]
+        k = max(1, min(chains // self.B, self.H))
+        return [(b, b + 1, j * self.H // k, (j + 1) * self.H // k) for b in range(self.B) for j in range(k)]
+
     def _launch_layers(self, q, out, lo, hi, splits, scale, chains, streams):
         """Per-layer launches of layers [lo, hi): one PDL chain per micro-batch (sequence range),
         each on its own stream forked from (and joined back into) the current stream."""
-        ranges = self._chain_ranges(chains)
-        if len(ranges) == 1:
+        units = self._chain_units(chains)
+        if len(units) == 1:
             for l in range(lo, hi):
                 self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l, pdl=l > lo)
             return
         cur = torch.cuda.current_stream()
         for st in streams:
             st.wait_stream(cur)
-        for (b0, b1), st in zip(ranges, streams):
+        for (b0, b1, h0, h1), st in zip(units, streams):
             with torch.cuda.stream(st):
                 for l in range(lo, hi):
                     self.decode(q[l:l + 1], splits=splits, out=out[l:l + 1], scale=scale, layer=l,
-                                pdl=l > lo and self.chain_pdl, seqs=(b0, b1))
+                                pdl=l > lo and self.chain_pdl, seqs=(b0, b1), heads=(h0, h1))
         for st in streams:
             cur.wait_stream(st)
 
@@ -484,7 +501,7 @@ class BatchedKVCache:
         segment (one chain per micro-batch), over the fixed staging buffers q / out."""
         graphs = []
         side = torch.cuda.Stream(device=self.device)
-        streams = [torch.cuda.Stream(device=self.device) for _ in self._chain_ranges(chains)]
+        streams = [torch.cuda.Stream(device=self.device) for _ in self._chain_units(chains)]
         side.wait_stream(torch.cuda.current_stream())
         for lo in range(0, self.L, seg):
             hi = min(self.L, lo + seg)
@@ -510,10 +527,12 @@ class BatchedKVCache:
             raise ValueError("q and out must be [L, B, H*m, 128] for all layers")
         return self._segment_graphs(q, out, self.L, splits, scale, chains)[0]
 
-    def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None, schedule=None):
+    def decode_partial(self, q, splits=None, scale=None, layer=0, pdl=False, out=None, schedule=None,
+                       heads=None):
         """Unnormalised split-KV partials f32 [L'*B*H*m, 130] = (acc[128], m (log2), l) for q
         fp16 [L', B, H*m, 128] over layers [layer, layer + L') (per-layer launches: L' = 1,
-        pdl as in decode); `out` may be a preallocated [L'*B*H*m, 130] view."""
+        pdl as in decode); `out` may be a preallocated [L'*B*H*m, 130] view; heads=(h0, h1)
+        computes those kv heads' rows only (split kernel; chains over heads)."""
         L, B, Hq, D = q.shape
         if B != self.B or layer < 0 or layer + L > self.L or D != HEAD_DIM or Hq % self.H:
             raise ValueError("q shape does not match the cache")
@@ -525,6 +544,15 @@ class BatchedKVCache:
         if part.shape != (L * B * Hq, HEAD_DIM + 2) or not part.is_contiguous():
             raise ValueError("partials buffer must be contiguous [L*B*Hq, 130]")
         scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+        if heads is not None and tuple(heads) != (0, self.H):
+            h0, h1 = int(heads[0]), int(heads[1])
+            if not 0 <= h0 <= h1 <= self.H:
+                raise ValueError("heads must be a range of the kv heads")
+            ws = self._workspace(m, splits, L, layer)
+            _lib.call("ckv_decode_attention_range", _lib.ptr(q), q.stride(0), q.stride(1), self.arena("k", layer),
+                      self.arena("v", layer), _lib.ptr(self.seq), L, B, 0, B, self.H, h0, h1 - h0, m, scale, splits,
+                      ws, None, 0, 0, _lib.ptr(part), _lib.DECODE_PDL if pdl else 0, _lib.stream())
+            return part
         plan = self._use_wp(m, None, None if schedule == "wp" else splits_arg, schedule)
         if plan is not None:
             prefix, ctas, slots, max_ctas = plan
@@ -733,7 +761,7 @@ class DecodeLoop:
         self.out = torch.empty_like(self.q)
         self.k_new = torch.zeros((L, B, H, HEAD_DIM), dtype=torch.float16, device=dev)
         self.v_new = torch.zeros_like(self.k_new)
-        streams = [torch.cuda.Stream(device=dev) for _ in cache._chain_ranges(chains)]
+        streams = [torch.cuda.Stream(device=dev) for _ in cache._chain_units(chains)]
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm-up (workspaces, attributes) without appending

@@ -64,6 +64,7 @@ struct DecArgs {
   const int32_t* seq;
   int L, B, H, m, splits;
   int b0, Bc;           // this launch's sequences [b0, b0 + Bc) of the B in the cache
+  int h0;               // and its kv heads [h0, h0 + gridDim.y) (split kernel)
   float scale_log2;
   float* ws;            // [L*B*H*m][splits][130] partials
   uint32_t* counters;   // [L*B*H] arrival counters (self-resetting)
@@ -96,12 +97,12 @@ __device__ __forceinline__ uint32_t smid() {
 struct CtaIds {
   int split, h, l, b;
 };
-__device__ __forceinline__ CtaIds cta_ids(int Bc, int b0) {
+__device__ __forceinline__ CtaIds cta_ids(int Bc, int b0, int h0) {
   uint32_t x, y, z;
   asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(x));
   asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(y));
   asm volatile("mov.u32 %0, %%ctaid.z;" : "=r"(z));
-  return CtaIds{(int)x, (int)y, (int)z / Bc, b0 + (int)z % Bc};
+  return CtaIds{(int)x, h0 + (int)y, (int)z / Bc, b0 + (int)z % Bc};
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -672,7 +673,7 @@ __device__ __forceinline__ void fp16_tiles(const DecArgs& a, const QS& qs, WarpS
   uint32_t tid;
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
   const int warp = (int)(tid >> 5), g = (int)((tid & 31) >> 2), c = (int)(tid & 3);
-  const CtaIds id = cta_ids(a.Bc, a.b0);
+  const CtaIds id = cta_ids(a.Bc, a.b0, a.h0);
   const int off_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 4];
   const int len_fp = reinterpret_cast<const int*>(a.seq)[8 * id.b + 5];
   const int nft = (len_fp + kTile - 1) / kTile;
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   int cnt2, nloc;
   TileSrc src;  // tile-native arenas: a row range starting at a tile is contiguous bytes
   {
-    const CtaIds id = cta_ids(a.Bc, a.b0);
+    const CtaIds id = cta_ids(a.Bc, a.b0, a.h0);
     const int4 s0 = reinterpret_cast<const int4*>(a.seq)[2 * id.b];
     const int n2t = s0.y / kTile, n4t = s0.w / kTile;
     const int a2 = (int)((int64_t)n2t * id.split / a.splits), b2 = (int)((int64_t)n2t * (id.split + 1) / a.splits);
@@ -827,7 +828,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   // the unit's V span bound is build-time data too: read it before the wait
   UnitScale us;
   {
-    const CtaIds id = cta_ids(a.Bc, a.b0);
+    const CtaIds id = cta_ids(a.Bc, a.b0, a.h0);
     us.F = unit_v_exponent(a, id.l, id.b, id.h);
 #if CKV_DEC_Q_PREFETCH
     // pull the unit's q rows into L2 while the previous launch drains (L2 is the point of
@@ -847,7 +848,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   // warp w stages group G = w of every set (a quarter of the q values each: one 16-byte load per
   // lane), the unit's max |q| combined through shared memory
   {
-    const CtaIds id = cta_ids(a.Bc, a.b0);
+    const CtaIds id = cta_ids(a.Bc, a.b0, a.h0);
     float qv[8];
     load_q_quarter(a, id.l, id.b, id.h, warp, g, c, qv);
     const float mx = stage_q_quarter_aug(qv, warp, lane, s_q);
@@ -907,7 +908,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   }
   __syncthreads();
   // merge the 4 warps: thread -> d
-  const CtaIds id = cta_ids(a.Bc, a.b0);
+  const CtaIds id = cta_ids(a.Bc, a.b0, a.h0);
   const int split = id.split, h = id.h, l = id.l, b = id.b;
   const int d = threadIdx.x;
   const int hq0 = h * a.m;
@@ -1558,8 +1559,22 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
                                   int32_t kv_heads, int32_t m, float scale, int32_t splits,
                                   void* workspace, uint16_t* out, int64_t o_s_layer, int64_t o_s_batch,
                                   float* partial_out, int32_t flags, void* stream) {
+  return ckv_decode_attention_range(q, q_s_layer, q_s_batch, k_arena, v_arena, seq, layers, batch, seq_begin,
+                                    seq_count, kv_heads, 0, kv_heads, m, scale, splits, workspace, out,
+                                    o_s_layer, o_s_batch, partial_out, flags, stream);
+}
+
+int32_t ckv_decode_attention_range(const uint16_t* q, int64_t q_s_layer, int64_t q_s_batch,
+                                   ckv_arena k_arena, ckv_arena v_arena, const int32_t* seq,
+                                   int32_t layers, int32_t batch, int32_t seq_begin, int32_t seq_count,
+                                   int32_t kv_heads, int32_t head_begin, int32_t head_count, int32_t m,
+                                   float scale, int32_t splits, void* workspace, uint16_t* out,
+                                   int64_t o_s_layer, int64_t o_s_batch, float* partial_out, int32_t flags,
+                                   void* stream) {
   if (layers < 0 || batch < 0 || kv_heads < 0 || splits < 1) return CKV_ERR_ARG;
   if (seq_begin < 0 || seq_count < 0 || seq_begin + seq_count > batch) return CKV_ERR_ARG;
+  if (head_begin < 0 || head_count < 0 || head_begin + head_count > kv_heads) return CKV_ERR_ARG;
+  if (head_count == 0) return CKV_OK;
   if (m < 1 || m > 8) return CKV_ERR_UNSUPPORTED;
   if (!q || !seq || (!out && !partial_out)) return CKV_ERR_ARG;
   if (splits > 1 && !workspace) return CKV_ERR_ARG;
@@ -1584,7 +1599,7 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
   a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
   a.K = k_arena; a.V = v_arena; a.seq = seq;
   a.L = layers; a.B = batch; a.H = kv_heads; a.m = m; a.splits = splits;
-  a.b0 = seq_begin; a.Bc = seq_count;
+  a.b0 = seq_begin; a.Bc = seq_count; a.h0 = head_begin;
   a.scale_log2 = scale * 1.4426950408889634f;
   const int64_t units = (int64_t)layers * batch * kv_heads;
   a.counters = reinterpret_cast<uint32_t*>(workspace);
@@ -1596,7 +1611,7 @@ int32_t ckv_decode_attention_seqs(const uint16_t* q, int64_t q_s_layer, int64_t 
   a.trace = g_trace_host;
   if (!ensure_decode_attr()) return CKV_ERR_CUDA;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)splits, (unsigned)kv_heads, (unsigned)(layers * seq_count));
+  cfg.gridDim = dim3((unsigned)splits, (unsigned)head_count, (unsigned)(layers * seq_count));
   cfg.blockDim = dim3(kDecWarps * 32);
   cfg.dynamicSmemBytes = kDynSmem;
   cfg.stream = as_stream(stream);
@@ -1754,7 +1769,7 @@ int32_t ckv_decode_attention_wp_seqs(const uint16_t* q, int64_t q_s_layer, int64
   a.q = q; a.q_sl = q_s_layer; a.q_sb = q_s_batch;
   a.K = k_arena; a.V = v_arena; a.seq = seq;
   a.L = layers; a.B = batch; a.H = kv_heads; a.m = m; a.splits = 1;
-  a.b0 = b0; a.Bc = n_seqs;
+  a.b0 = b0; a.Bc = n_seqs; a.h0 = 0;
   a.scale_log2 = scale * 1.4426950408889634f;
   const int64_t units = (int64_t)layers * n_seqs * kv_heads;
   a.counters = reinterpret_cast<uint32_t*>(workspace);

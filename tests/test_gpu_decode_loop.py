@@ -141,3 +141,42 @@ def test_bench_default_step_one_chain_per_sequence():
         ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
         err = np.max(np.abs(step[l, b, h * m:(h + 1) * m] - ref))
         assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (l, b, h, err)
+
+
+def test_head_range_chains_batch_one():
+    """A batch-1 cache decoded as micro-batch chains over its kv heads (ckv_decode_attention_range:
+    each chain's launches cover a kv-head range; decode_partial with heads=) equals the
+    oracle, and each range's launch leaves the other heads' rows untouched."""
+    rng = np.random.default_rng(99)
+    L, B, H, m, D, N = 2, 1, 5, 2, 128, 40
+    T = N * 32 + 3
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    q = rng.normal(size=(L, B, H * m, D)).astype(np.float16)
+    tiers = rng.choice([0, 0, 0, 1, 2], size=(B, N)).astype(np.uint8)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), _search(tiers))
+    units = cache._chain_units(4)
+    assert [u[2:] for u in units] == [(0, 1), (1, 2), (2, 3), (3, 5)]
+    qd = torch.from_numpy(q).cuda()
+    sentinel = torch.full_like(qd, 3.0)
+    cache.decode(qd, out=sentinel, splits=3, heads=(1, 3))
+    sn = sentinel.float().cpu().numpy()
+    assert (sn[:, :, :m] == 3.0).all() and (sn[:, :, 3 * m:] == 3.0).all()
+    out = torch.empty_like(qd)
+    g = cache.decode_graph(qd, out, splits=cache.chain_splits(m), chains=4)
+    g.replay()
+    part = torch.full((L * B * H * m, D + 2), float("nan"), dtype=torch.float32, device="cuda")
+    for (_, _, h0, h1) in units:
+        cache.decode_partial(qd, splits=2, out=part, heads=(h0, h1))
+    merged = batched.lse_merge(part[None]).view(qd.shape).float().cpu().numpy()
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for l in range(L):
+        for h in range(H):
+            oc = O.build_cache(k[l, 0, :, h].astype(np.float64), v[l, 0, :, h].astype(np.float64), tiers[0], 32, 32)
+            ref = O.mixed_decode_attention(q[l, 0, h * m:(h + 1) * m].astype(np.float64), oc)
+            for arr in (got, merged, sn if 1 <= h < 3 else None):
+                if arr is None:
+                    continue
+                err = np.max(np.abs(arr[l, 0, h * m:(h + 1) * m] - ref))
+                assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (l, h, err)
