@@ -1307,18 +1307,19 @@ def main():
         torch.cuda.synchronize()
         barrier()
         e8, e9 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e8.record()
-        for i in range(n_tok):
-            loop.step(q, kn[i], vn[i])
-        e9.record()
-        torch.cuda.synchronize()
+        with ClockSampler(local) as tclk:
+            e8.record()
+            for i in range(n_tok):
+                loop.step(q, kn[i], vn[i])
+            e9.record()
+            torch.cuda.synchronize()
         tp_ms = e8.elapsed_time(e9) / n_tok
         if world > 1:
             t = torch.tensor([tp_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tp_ms = float(t.item())
         mean_bytes = (bytes0 + cache.algorithmic_bytes(m)) / 2
-        tpot = {"steps": n_tok, "ms_per_token": round(tp_ms, 4),
+        tpot = {"steps": n_tok, "ms_per_token": round(tp_ms, 4), "clocks": tclk.summary(),
                 "tokens_per_s": round(world * B / (tp_ms * 1e-3), 1),
                 "gbs": round(world * mean_bytes / (tp_ms * 1e-3) / 1e9, 2),
                 "note": "batched.DecodeLoop: per step ckv_append_tokens (one new K/V row per unit) + the "

@@ -35,3 +35,18 @@ for i in range(20):
     cache._reserve_decode_token(); loop.graph.replay()
 e1.record(); torch.cuda.synchronize()
 print("  %.4f ms" % (e0.elapsed_time(e1) / 20))
+# the append alone, captured the same way
+kn2 = torch.zeros((L, B, H, 128), device=dev, dtype=torch.float16)
+side = torch.cuda.Stream(device=dev)
+side.wait_stream(torch.cuda.current_stream())
+ga = torch.cuda.CUDAGraph()
+with torch.cuda.graph(ga, stream=side):
+    cache._append_device(kn2, kn2)
+torch.cuda.synchronize()
+left = int((cache.cap_fp - cache.seq_host[:, 5]).min())
+e0.record()
+for i in range(min(10, left)):
+    cache._reserve_decode_token(); ga.replay()
+e1.record(); torch.cuda.synchronize()
+print("append graph alone: %.4f ms" % (e0.elapsed_time(e1) / min(10, left)))
+print("decode graph at the final state: %.4f ms" % timeit(g2.replay))
