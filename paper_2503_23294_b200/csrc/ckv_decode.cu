@@ -31,7 +31,11 @@
 
 namespace ckv {
 
-constexpr int kDecWarps = 4;
+#ifndef CKV_DEC_WARPS
+#define CKV_DEC_WARPS 4
+#endif
+constexpr int kDecWarps = CKV_DEC_WARPS;  // warps per split-kernel CTA (4; 8 as a build variant)
+static_assert(kDecWarps == 4 || kDecWarps == 8, "split kernel: 4 or 8 warps per CTA");
 constexpr int kTile = 16;
 // Per-warp cp.async ring.  A stage holds one 16-token tile of the tile-native arenas verbatim
 // (see the tile functions below): INT2 1536 B, INT4 2560 B.  The INT2 and INT4 phases reuse
@@ -52,7 +56,7 @@ template <int BITS> struct Ring {
 };
 constexpr int kWarpRing = Ring<2>::stages * Ring<2>::bytes > Ring<4>::stages * Ring<4>::bytes
                               ? Ring<2>::stages * Ring<2>::bytes : Ring<4>::stages * Ring<4>::bytes;
-constexpr int kDynSmem = kDecWarps * kWarpRing;  // 40 KB per CTA (4 x 2560 B per warp)
+constexpr int kDynSmem = kDecWarps * kWarpRing;  // 40 KB per CTA (4 warps x 4 x 2560 B)
 constexpr int kPartStride = kHeadDim + 2;  // acc[128], m, l (partial_out / cross-rank format)
 constexpr int kWsStride = kHeadDim + 4;    // split workspace rows: acc[128], m, l, pad (16-B rows)
 constexpr float kRescaleThresh = 8.0f;     // lazy rescale: p <= 2^8 in fp16
@@ -850,12 +854,14 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   {
     const CtaIds id = cta_ids(a.Bc, a.b0, a.h0);
     float qv[8];
-    load_q_quarter(a, id.l, id.b, id.h, warp, g, c, qv);
-    const float mx = stage_q_quarter_aug(qv, warp, lane, s_q);
-    if (lane == 0) s_qmax[warp] = mx;
+    if (warp < 4) {
+      load_q_quarter(a, id.l, id.b, id.h, warp, g, c, qv);
+      const float mx = stage_q_quarter_aug(qv, warp, lane, s_q);
+      if (lane == 0) s_qmax[warp] = mx;
+    }
     __syncthreads();
     us.E = q_exponent(fmaxf(fmaxf(s_qmax[0], s_qmax[1]), fmaxf(s_qmax[2], s_qmax[3])));
-    stage_q_quarter_sets(qv, warp, us.E, s_q, lane);
+    if (warp < 4) stage_q_quarter_sets(qv, warp, us.E, s_q, lane);
   }
   __syncthreads();
   if (threadIdx.x == 0 && (a.trace != nullptr)) s_tr[2] = gtime();
@@ -913,7 +919,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
   const int d = threadIdx.x;
   const int hq0 = h * a.m;
   const int Hq = a.H * a.m;
-  for (int qi = 0; qi < a.m; ++qi) {
+  for (int qi = 0; qi < a.m && d < kHeadDim; ++qi) {
     float ms = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kDecWarps; ++w) ms = fmaxf(ms, s_ml[w][qi][0]);
@@ -949,7 +955,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
       int64_t* dst = a.trace + 16 * atomicAdd(&g_trace_n, 1ull);
       for (int i = 0; i < 5; ++i) dst[i] = s_tr[i];
       for (int i = 8; i < 12; ++i) dst[i] = s_tr[i];
-      for (int i = 0; i < kDecWarps; ++i) dst[12 + i] = s_tend[i];
+      for (int i = 0; i < 4; ++i) dst[12 + i] = s_tend[i];
       // launch position | split << 20 | (sequence * H + kv head) << 40
       dst[5] = smid();
       dst[6] = (int64_t)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) | ((int64_t)split << 20) |
@@ -1013,7 +1019,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
       s_ml2[2 * r + 1] = lsum;
     }
     __syncthreads();
-    for (int qi = 0; qi < a.m; ++qi) {
+    for (int qi = 0; qi < a.m && d < kHeadDim; ++qi) {
       const float* pq = s_part + qi * a.splits * kWsStride + d;
       const float* wq = s_w + qi * a.splits;
       float acc = 0.f;
@@ -1031,7 +1037,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, kMinCtas) decode_kernel(const 
     trace_out();
     return;
   }
-  for (int qi = 0; qi < a.m; ++qi) {
+  for (int qi = 0; qi < a.m && d < kHeadDim; ++qi) {
     const int64_t row = row0 + qi;
     const float* p = s_part ? s_part + qi * a.splits * kWsStride : a.ws + row * a.splits * kWsStride;
     float ms = -INFINITY, acc = 0.f, lsum = 0.f;
