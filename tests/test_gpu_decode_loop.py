@@ -180,3 +180,33 @@ def test_head_range_chains_batch_one():
                     continue
                 err = np.max(np.abs(arr[l, 0, h * m:(h + 1) * m] - ref))
                 assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (l, h, err)
+
+
+@pytest.mark.parametrize("m", [3, 12])
+def test_chained_step_mixed_sequences(m):
+    """Chained per-layer graph over sequences of different tier mixes — one all-FP16, one
+    all-INT2, one mixed, each with a 17-token context tail — with m = 3 (odd GQA ratio) and
+    m = 12 (groups of <= 8 q rows per launch): every unit meets the oracle."""
+    rng = np.random.default_rng(200 + m)
+    L, B, H, D = 2, 3, 2, 128
+    N = 12
+    T = N * 32 + 17
+    k = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    v = rng.normal(size=(L, B, T, H, D)).astype(np.float16)
+    q = rng.normal(size=(L, B, H * m, D)).astype(np.float16)
+    tiers = np.stack([np.full(N, 2), np.zeros(N, np.int64), rng.choice([0, 1, 2], size=N)]).astype(np.uint8)
+    s = _search(tiers)
+    cache = batched.build_cache_batched(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), s)
+    qd = torch.from_numpy(q).cuda()
+    out = torch.empty_like(qd)
+    g = cache.decode_graph(qd, out, splits=cache.chain_splits(min(m, 8)), chains=B)
+    g.replay()
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for l in range(L):
+        for b in range(B):
+            for h in range(H):
+                oc = O.build_cache(k[l, b, :, h].astype(np.float64), v[l, b, :, h].astype(np.float64), tiers[b], 32, 32)
+                ref = O.mixed_decode_attention(q[l, b, h * m:(h + 1) * m].astype(np.float64), oc)
+                err = np.max(np.abs(got[l, b, h * m:(h + 1) * m] - ref))
+                assert err <= TOL_ABS and err / np.max(np.abs(ref)) <= TOL_REL, (l, b, h, err)
