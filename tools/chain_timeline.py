@@ -29,7 +29,7 @@ def main():
     ns = argparse.Namespace(schedule="auto", splits=args.splits, chains=args.chains)
     splits = bench.pick_splits(ns, cache, m)
     out = torch.empty_like(q)
-    streams = [torch.cuda.Stream(device=dev) for _ in range(args.chains)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(args.chains)]  # eager warm-up only
     lib = _lib.load()
     lib.ckv_decode_set_trace.argtypes = [ctypes.c_void_p]
 
@@ -44,6 +44,8 @@ def main():
     # it (one CUDA graph; eager chained launches are host-bound)
     lib.ckv_decode_set_trace(ctypes.c_void_p(buf.data_ptr()))
     g = cache.decode_graph(q, out, splits=splits, chains=args.chains)
+    for _ in range(3):  # the first replays of a fresh graph launch its branches late (upload)
+        g.replay()
     torch.cuda.synchronize()
     buf.zero_()
     g.replay()
@@ -83,6 +85,28 @@ def main():
         ends = sorted({int(p): x[x[:, 7] == p, 4].max() for p in np.unique(x[:, 7])}.values())
         d = np.diff(ends) / 1e3
         print(f"chain {c}: {len(ends)} launches, end-to-end spacing median {np.median(d):.1f} us")
+    # the step's ramp and drain: when every chain's first CTA starts / last CTA ends
+    for c in range(min(args.chains, cache.B)):
+        x = t[seq_of == c]
+        print(f"chain {c}: first CTA start +{(x[:, 0].min() - t0) / 1e3:6.1f} us, first tiles +"
+              f"{(x[:, 2].min() - t0) / 1e3:6.1f} us, last CTA end -{(t1 - x[:, 4].max()) / 1e3:6.1f} us")
+    # how the chains drift apart: spread over chains of each layer's end time
+    ptrs = np.unique(t[:, 7])
+    lay = np.searchsorted(ptrs, t[:, 7])
+    spread = []
+    for l in range(len(ptrs)):
+        e = [t[(lay == l) & (seq_of == c), 4].max() for c in range(min(args.chains, cache.B))
+             if ((lay == l) & (seq_of == c)).any()]
+        spread.append((max(e) - min(e)) / 1e3)
+    print("spread of the chains' layer end times us, per layer: " + " ".join(f"{x:.0f}" for x in spread))
+    bins = np.arange(0, 21)
+    for name, ref, sgn in (("start", t0, 1), ("end", t1, -1)):
+        row = []
+        for i in bins[:-1]:
+            a, b = (ref + i * 10000, ref + (i + 1) * 10000) if sgn > 0 else (ref - (i + 1) * 10000, ref - i * 10000)
+            sel = (grid >= a) & (grid < b)
+            row.append(occ[:, sel].mean() if sel.any() else float("nan"))
+        print(f"resident CTAs per SM in 10 us bins from the step {name}: " + " ".join(f"{v:.2f}" for v in row))
 
 
 if __name__ == "__main__":
