@@ -62,6 +62,11 @@ def main():
     for name, a, b in (("launch -> PDL wait done", st, wt), ("q staging", wt, qs), ("tiles", qs, te),
                        ("merge tail", te, en)):
         print(f"  {name:24s} {100 * (b - a).sum() / life:5.1f} % of CTA time, median {np.median(b - a) / 1e3:6.2f} us")
+    t8, t9 = t[:, 8], t[:, 9]
+    ok = (t8 > 0) & (t9 > 0)
+    for name, a, b in (("finish warps + barrier", te, t8), ("park + in-CTA merge + partial", t8, t9),
+                       ("arrival + final merge", t9, en)):
+        print(f"    {name:30s} median {np.median((b - a)[ok]) / 1e3:6.2f} us, p90 {np.percentile((b - a)[ok], 90) / 1e3:6.2f}")
     sp = t[:, 12:16].max(1) - t[:, 12:16].min(1)
     print("warp spread of tile ends within a CTA us: p50 %.2f p90 %.2f max %.2f" % tuple(np.percentile(sp, [50, 90, 100]) / 1e3))
     # CTA-slot utilisation: resident CTAs per SM over time, vs the 4-slot capacity
