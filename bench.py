@@ -669,6 +669,46 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
         for _ in range(3):
             e2e_step()
         e2e_ms = timed(e2e_step, steps)
+    # lockstep figure: every layer ONE launch over all of the rank's kv heads, so layer l+1
+    # starts only after all of layer l (the dependency a batch-1 model step has: every head of
+    # layer l+1 reads the whole layer-l output); the kv-head chains above relax it to "after
+    # layer l of the same head range"
+    if chains > 1:
+        ls_args = argparse.Namespace(**{**vars(args), "chains": 1})
+        ls_splits = pick_splits(ls_args, cache, m)  # the warp plan unless --splits / --schedule split
+        if split == "seq":
+            def ls_local(qq):
+                for l in range(L):
+                    cache.decode_partial(qq[l:l + 1], splits=ls_splits, layer=l, pdl=l > 0,
+                                         out=parts[l * B * Hq:(l + 1) * B * Hq])
+
+            side3 = torch.cuda.Stream(device=dev)
+            side3.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side3):
+                ls_local(q)
+            torch.cuda.current_stream().wait_stream(side3)
+            ls_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ls_graph, stream=side3):
+                ls_local(q)
+
+            def ls_step():
+                ls_graph.replay()
+                gathered = distributed.exchange_partials(parts) if world > 1 else parts[None]
+                return batched.lse_merge(gathered)
+        else:
+            ls_out = torch.empty_like(q)
+            ls_graph = cache.decode_graph(q, ls_out, splits=ls_splits)
+            ls_step = ls_graph.replay
+        for _ in range(warmup):
+            ls_step()
+        ls_ms = timed(ls_step, steps)
+        res["lockstep_per_layer"] = {
+            "value": round(step_bytes / (ls_ms * 1e-3) / 1e9, 2), "ms_per_step": round(ls_ms, 4),
+            "launch": f"per-layer: {L} PDL-chained launches over all kv heads, one CUDA graph"
+                      + (" + all_gather + merge" if split == "seq" else ""),
+            "schedule": schedule_desc(cache, ls_splits)}
+        del ls_graph
+        cache.schedule = args.schedule
     counts0 = counts[0]
     res.update({
         "value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
@@ -797,7 +837,9 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
                        "launch": ("per-layer decode_partial (40 PDL-chained launches per kv-head chain, 8 chains on "
                                   "their own streams, one CUDA graph) + all_gather + merge" if r["split"] == "seq" else
                                   "per-layer decode (40 PDL-chained launches per kv-head chain, one CUDA graph), "
-                                  "no collective"),
+                                  "no collective")
+                                 + "; a head range's layer l+1 waits for its own layer l only (a model step's "
+                                   "layer l+1 needs all heads of layer l: lockstep_per_layer keeps that)",
                        "splits": r["splits"], "schedule": r["schedule"],
                        "l2": "inputs larger than L2 (21 GB of arenas over the ranks)"},
             "tokens_per_s": r["tokens_per_s"],
@@ -806,7 +848,8 @@ def run_cfg3(args, torch, dist, dev, rank, world, local):
                          "frac": round(r["per_rank_gbs"] / peak, 4), "peak_kind": peak_kind, "traffic": None},
             "e2e": r["e2e"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
         }
-        for key in ("local_decode_ms", "exchange_merge_ms", "per_layer_merge_us", "per_layer_merge_note", "p2p"):
+        for key in ("lockstep_per_layer", "local_decode_ms", "exchange_merge_ms", "per_layer_merge_us",
+                    "per_layer_merge_note", "p2p"):
             if key in r:
                 line[key] = r[key]
         if "ms_per_step" in (r.get("p2p") or {}):
@@ -1372,8 +1415,10 @@ def main():
                     "per_layer_merge_us": seq["per_layer_merge_us"],
                     "per_layer_merge_note": seq["per_layer_merge_note"], "splits": seq["splits"],
                     "parallelism": seq["parallelism"], "e2e": seq["e2e"],
+                    "lockstep_per_layer": seq.get("lockstep_per_layer"),
                     "head_shard": {"value": head["value"], "unit": "GB/s", "ms_per_step": head["ms_per_step"],
-                                   "parallelism": head["parallelism"], "e2e": head["e2e"]}}
+                                   "parallelism": head["parallelism"], "e2e": head["e2e"],
+                                   "lockstep_per_layer": head.get("lockstep_per_layer")}}
         p2p = seq.get("p2p") or {}
         if "ms_per_step" in p2p:
             p2p["value"] = round(seq["algorithmic_bytes_per_step"] / (p2p["ms_per_step"] * 1e-3) / 1e9, 2)
