@@ -18,13 +18,27 @@ import bench  # noqa: E402
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", choices=["chains", "lockstep", "single"], default="chains")
+    ap.add_argument("--seconds", type=float, default=6.0)
+    args = ap.parse_args()
     dev = torch.device("cuda", 0)
     cache, q, _ = bench.build_cfg2(torch, dev, 0)
     m = q.shape[2] // cache.H
-    ns = argparse.Namespace(schedule="auto", splits=None, chains=8)
+    chains = 8 if args.mode == "chains" else 1
+    ns = argparse.Namespace(schedule="auto", splits=None, chains=chains)
     splits = bench.pick_splits(ns, cache, m)
     out = torch.empty_like(q)
-    g = cache.decode_graph(q, out, splits=splits, chains=8)
+    if args.mode == "single":
+        sp = cache.default_splits(m, cache.L)
+
+        class G:
+            def replay(self):
+                cache.decode(q, out=out, splits=sp)
+        g = G()
+    else:
+        g = cache.decode_graph(q, out, splits=splits, chains=chains)
+    print(f"mode {args.mode}")
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
@@ -43,7 +57,7 @@ def main():
     th.start()
     t0 = time.time()
     rows = []
-    while time.time() - t0 < 6.0:
+    while time.time() - t0 < args.seconds:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(50):
