@@ -579,6 +579,8 @@ def measure_cfg3(args, torch, dist, dev, rank, world, split="seq", steps=None, w
         # the figure is device latency, not Python launch overhead; eager when capture fails
         merge_fn, merge_reps = layer_merge, 1
         try:
+            if world > 1 and dist.get_backend() != "nccl":
+                raise RuntimeError("host-staged exchange (gloo): not capturable")
             side2 = torch.cuda.Stream(device=dev)
             side2.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side2):
