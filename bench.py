@@ -1260,8 +1260,17 @@ def main():
     value = world * step_bytes / sec / 1e9
     tokens_per_s = world * B / sec
 
+    def idle_gap():
+        """Every figure below starts from the same power state as the headline window: after
+        ~0.3 s of continuous load the board reaches its power limit (see `sustained`), so each
+        one follows a 1 s idle gap."""
+        torch.cuda.synchronize()
+        time.sleep(1.0)
+        barrier()
+
     # end to end through the public API: pinned host q -> H2D, decode (all layers), D2H
     # (decode_step_host: uploads / downloads overlap the per-layer launches on copy streams)
+    idle_gap()
     qh = q.cpu().pin_memory()
     oh = torch.empty(q.shape, dtype=torch.float16, pin_memory=True)
     for _ in range(3):
@@ -1283,7 +1292,7 @@ def main():
     e2e_gbs = world * step_bytes / (e2e_ms * 1e-3) / 1e9
 
     # eager launches (no graph), same step
-    torch.cuda.synchronize()
+    idle_gap()
     e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e6.record()
     for _ in range(args.steps):
@@ -1299,36 +1308,41 @@ def main():
         ls_args = argparse.Namespace(**{**vars(args), "chains": 1})
         ls_splits = pick_splits(ls_args, cache, m)
         ls_graph = cache.decode_graph(q, out, splits=ls_splits)
+        idle_gap()
         for _ in range(3):
             ls_graph.replay()
         torch.cuda.synchronize()
         barrier()
-        e10, e11 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e10.record()
-        for _ in range(args.steps):
-            ls_graph.replay()
-        e11.record()
-        torch.cuda.synchronize()
+        with ClockSampler(local) as lclk:
+            e10, e11 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e10.record()
+            for _ in range(args.steps):
+                ls_graph.replay()
+            e11.record()
+            torch.cuda.synchronize()
         ls_ms = e10.elapsed_time(e11) / args.steps
         if world > 1:
             t = torch.tensor([ls_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ls_ms = float(t.item())
         lockstep = {"value": round(world * step_bytes / (ls_ms * 1e-3) / 1e9, 2), "ms_per_step": round(ls_ms, 4),
-                    "launch": launch_desc(1), "schedule": schedule_desc(cache, ls_splits)}
+                    "launch": launch_desc(1), "schedule": schedule_desc(cache, ls_splits),
+                    "clocks": lclk.summary()}
         del ls_graph
         cache.schedule = args.schedule
 
     # single-launch (all 32 layers in one grid) figure for the same cache
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     single_splits = args.splits or cache.default_splits(m, L)  # split schedule: the faster one in one launch
+    idle_gap()
     for _ in range(3):
         cache.decode(q, out=out, splits=single_splits)
-    e2.record()
-    for _ in range(args.steps):
-        cache.decode(q, out=out, splits=single_splits)
-    e3.record()
-    torch.cuda.synchronize()
+    with ClockSampler(local) as fclk:
+        e2.record()
+        for _ in range(args.steps):
+            cache.decode(q, out=out, splits=single_splits)
+        e3.record()
+        torch.cuda.synchronize()
     fused_gbs = step_bytes / (e2.elapsed_time(e3) / args.steps * 1e-3) / 1e9
 
     sched_desc = schedule_desc(cache, splits, args.chains)
@@ -1350,8 +1364,7 @@ def main():
         vn = torch.randn((n_tok, L, B, cache.H, 128), generator=gt, device=dev, dtype=torch.float16)
         loop = batched_mod.DecodeLoop(cache, m, splits=splits, chains=args.chains)
         bytes0 = cache.algorithmic_bytes(m)
-        torch.cuda.synchronize()
-        barrier()
+        idle_gap()
         e8, e9 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local) as tclk:
             e8.record()
@@ -1454,6 +1467,7 @@ def main():
             "algorithmic_bytes_per_step": step_bytes,
             "eager_launches_gbs": round(eager_gbs, 2),
             "single_launch_all_layers_gbs": round(fused_gbs, 2),
+            "single_launch_clocks": fclk.summary(),
             "lockstep_per_layer": lockstep,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
