@@ -35,6 +35,7 @@ FLAG_NONFINITE_FP16 = 16
 
 SEQ_FIELDS = 8  # CKV_SEQ_FIELDS
 DECODE_PDL = 1  # CKV_DECODE_PDL
+ABI_VERSION = 1  # ckv_abi_version() of the matching include/ckv.h
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -121,6 +122,8 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ret
+    if lib.ckv_abi_version() != ABI_VERSION:  # a stale build of another header revision
+        raise RuntimeError(f"{LIB_PATH} has ABI {lib.ckv_abi_version()}, this package expects {ABI_VERSION}: rebuild")
     _lib = lib
     return lib
 
