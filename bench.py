@@ -381,6 +381,8 @@ def bench_prefill(torch, dev, steps=3, profile=False):
     cache = batched.BatchedKVCache(L, B, H, counts[:, 0], counts[:, 1], counts[:, 2], [T], 0, device=dev)
     flush = torch.ones(64 << 20, dtype=torch.int32, device=dev)  # read-based L2 flush (clean lines)
     times_build, times_search = [], []
+    clk = ClockSampler(dev.index or 0)
+    clk.__enter__()
     for i in range(steps + 2):
         flush.max()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
@@ -398,6 +400,7 @@ def bench_prefill(torch, dev, steps=3, profile=False):
         if i >= 2:
             times_search.append(e0.elapsed_time(e1))
             times_build.append(e1.elapsed_time(e2))
+    clk.__exit__(None, None, None)
     tb = statistics.median(times_build) * 1e-3
     n2, n4, nf = (int(x) for x in counts[0])
     read = 2 * L * H * T * D * 2
@@ -418,6 +421,7 @@ def bench_prefill(torch, dev, steps=3, profile=False):
         "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(ach / peak, 4), "peak_kind": peak_kind,
                      "traffic": profile_traffic("reorder_quantize_pack")},
+        "clocks": clk.summary(),
         "text_search": text,
     }
 
@@ -1443,6 +1447,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_prefill:
         del cache
         torch.cuda.empty_cache()
+        time.sleep(2.0)  # out of the power limit the sustained run left the board at
         prefill = bench_prefill(torch, dev)
 
     if rank == 0:
