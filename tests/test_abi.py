@@ -38,6 +38,15 @@ def test_status_strings_and_version():
         _lib.check(_lib.CKV_ERR_CUDA)
 
 
+def test_load_refuses_a_library_of_another_abi(monkeypatch):
+    """_lib.load() checks ckv_abi_version() against the package's ABI_VERSION: a stale build
+    fails loudly instead of being called with mismatched signatures."""
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "ABI_VERSION", _lib.ABI_VERSION + 1)
+    with pytest.raises(RuntimeError, match="ABI"):
+        _lib.load()
+
+
 def test_argument_validation_without_gpu():
     lib = _lib.load()
     # validation happens before any launch, so these run on a CPU-only host
