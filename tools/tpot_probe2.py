@@ -1,3 +1,7 @@
+"""Probe (tuning aid): what the DecodeLoop's per-step input copies cost beside a plain graph
+replay of the cfg2 default step, variants interleaved 5 times (the step time drifts upward as
+the board reaches its power limit within ~0.3 s of load, so only interleaved variants compare;
+see tools/sustained_probe.py)."""
 import sys, os, torch, argparse
 sys.path.insert(0, os.getcwd())
 import bench
