@@ -1,6 +1,6 @@
 """Small invocations of every kernel for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): search, reorder/quantize/pack, decode (splits 1 and > 1, per-layer PDL chain,
-CUDA-graph replay, micro-batch chains on the split kernel and on the warp plan, partials + LSE
+CUDA-graph replay, micro-batch chains (sequence and kv-head ranges) on the split kernel and on the warp plan, partials + LSE
 merge by array and by pointers, m = 1 / 4 / 8, outlier-K and huge-scale units), append, export,
 the tile-native reconstruct, the f64 per-head kernels and the text encoders.  Checks results loosely (the parity
 tests do that properly); the point is the sanitizer's verdict."""
@@ -53,6 +53,12 @@ def main():
     g = cache.decode_graph(q, out, splits=cache.chain_splits(4), chains=B)  # the bench's default step
     g.replay()
     g.replay()
+    g = cache.decode_graph(q, out, splits=3, chains=B * H)  # chains over (sequence, kv-head range)
+    g.replay()
+    g.replay()
+    for h in range(H):  # split-KV partials of one kv-head range each (cfg3's head chains)
+        for l in range(L):
+            cache.decode_partial(q[l:l + 1], splits=2, layer=l, pdl=l > 0, heads=(h, h + 1))
     for b in range(B):  # warp plan over sequence ranges
         for l in range(L):
             cache.decode(q[l:l + 1], out=out[l:l + 1], layer=l, pdl=l > 0, seqs=(b, b + 1), schedule="wp")
