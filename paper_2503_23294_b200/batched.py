@@ -222,7 +222,7 @@ class BatchedKVCache:
 
     def warp_plan(self, seqs=None):
         """Warp-plan schedule (ckv_decode_attention_wp): unit u = b*H + h gets n_u warps in
-        proportion to its tile cost (INT2 1, INT4 1.06, FP16-region 2 per 16-token tile), at
+        proportion to its tile cost (INT2 1, INT4 1.2, FP16-region 3 per 16-token tile, measured), at
         least 2, summing to 16 x the SM count; returns (plan table i32 on the device, ctas,
         max_slots, max_ctas) or None when the units do not fit (more than 8 per CTA).  Computed
         once per sequence range (``seqs`` = (b0, b1), default the whole batch; a range is one
@@ -244,7 +244,9 @@ class BatchedKVCache:
         n_cta = T // cw
         U = (b1 - b0) * self.H
         s = self.seq_host[b0:b1].astype(np.int64)
-        cost_b = s[:, 1] // TILE + 1.06 * (s[:, 3] // TILE) + 2.0 * (-(-s[:, 5] // TILE))
+        # per-tile costs (INT2 1): INT4 1.2, FP16 region 3 — cfg2 lockstep 4485 GB/s with the
+        # instruction-count ratios (1.06, 2), 4500-4504 anywhere in INT4 1.2-1.4 x FP16 2-4
+        cost_b = s[:, 1] // TILE + 1.2 * (s[:, 3] // TILE) + 3.0 * (-(-s[:, 5] // TILE))
         cost = np.repeat(cost_b, self.H).astype(np.float64)
         if not (U and 2 * U <= T and cost.sum() > 0):
             return None, None
